@@ -1,0 +1,50 @@
+"""Pin the CPU oracle (oracle/bddc_oracle.py) against fixtures produced by
+the unmodified reference (tests/golden/make_golden.py)."""
+
+import numpy as np
+import pytest
+
+from oracle import bddc_oracle as O
+from tests.cases import FIXTURES, counts_match, gevp_values, golden, inputs, variants
+
+FAST = [n for n in FIXTURES if n != "cfg3"]
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("name", FAST)
+def test_oracle_matches_reference(name):
+    g = golden(name)
+    system, part, globs = inputs(name)
+    assert globs.interface_nodes.size == int(g["n_hat"])
+    for v in variants(g):
+        res = O.run_pipeline(system, part, globs, float(g["theta_f"]), float(g["theta_e"]), v,
+                             keep=True)
+        ops = res["ops"]
+        assert np.array_equal([op.n_B for op in ops], g["nB"])
+        for i in g["S_ids"].tolist():
+            assert _rel(ops[i].S, g[f"S_{i}"]) <= 1e-12
+            assert _rel(ops[i].g, g[f"g_{i}"]) <= 1e-12
+            assert _rel(ops[i].bsym_inverse(), g[f"Binv_{i}"]) <= 1e-10
+        n = globs.interface_nodes.size
+        assert _rel(O.interface_rhs(ops, n), g["rhs"]) <= 1e-12
+        assert _rel(O.interface_apply(ops, n)(g["probe"]), g["Sprobe"]) <= 1e-12
+        ref_eig = gevp_values(g, v)
+        for k, ev in ref_eig.items():
+            mine = res["eigenvalues"][k]
+            assert mine.shape == ev.shape
+            fin = np.isfinite(ev)
+            assert np.array_equal(np.isfinite(mine), fin)
+            np.testing.assert_allclose(mine[fin], ev[fin], rtol=1e-8, atol=1e-10 * np.abs(ev[fin]).max(initial=1))
+        kinds = [gl.kind for gl in globs.globs]
+        th = lambda k: float(g["theta_f"]) if kinds[k] == "face" else float(g["theta_e"])
+        mine_np = np.array([res["n_primal"][k] for k in range(len(globs.globs))])
+        assert counts_match(mine_np, g[f"{v}_n_primal"], None, ref_eig, th) == []
+        assert (res["pnumF"], res["pnumE"], res["n_vertex"]) == (
+            int(g[f"{v}_pnumF"]), int(g[f"{v}_pnumE"]), int(g[f"{v}_n_vertex"]))
+        assert abs(res["iterations"] - int(g[f"{v}_iterations"])) <= 1
+        assert _rel(res["pc"].apply(g["probe"]), g[f"{v}_Mprobe"]) <= 1e-10
+        assert _rel(res["solution"], g[f"{v}_solution"]) <= 1e-8
+        assert _rel(res["u"], g[f"{v}_u"]) <= 1e-8
