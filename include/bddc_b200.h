@@ -1,0 +1,226 @@
+/*
+ * bddc_b200.h -- C-ABI of the B200 (sm_100a) adaptive-BDDC hot path.
+ *
+ * The reference (arXiv 2501.01676, package `adbddc`) is pure Python with
+ * no FFI; its boundary for this path is the Python API.
+ * Each entry point below replaces the LAPACK / SuperLU / numpy call sites
+ * named in its comment (paths relative to /root/reference/pkg/src/adbddc).
+ * The Python host package paper_2501_01676_b200 mirrors the reference's
+ * functions on top of these calls; a ctypes binding is in
+ * paper_2501_01676_b200/_lib.py and INTEGRATION.md shows how a maintainer
+ * binds them from the reference side.
+ *
+ * Conventions
+ *  - All pointers are DEVICE pointers (caller-owned, e.g. torch tensors);
+ *    nothing allocates inside.  Work is ordered on `stream`.
+ *  - Batched ("vbatched") dense matrices live in one buffer: matrix b starts
+ *    at base + off[b], row-major, leading dimension ld[b] (or n[b]).
+ *  - Return value: 0 = launched, < 0 = -cudaError_t of the launch.
+ *    Numerical failures are written per batch member into the caller's
+ *    device `status` array (0 = ok, see enum below); the host maps them to
+ *    the reference's NumericalError messages.
+ *  - Stateless and thread-safe apart from one-time kernel attribute setup.
+ */
+#ifndef BDDC_B200_H
+#define BDDC_B200_H
+
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+enum {
+  BDDC_OK = 0,
+  BDDC_NOT_POSITIVE_DEFINITE = 1, /* cho_factor failure (Bsym, deluxe sums, dual certificate) */
+  BDDC_SINGULAR_PIVOT = 2,        /* zero / non-finite pivot (lu_factor on a singular block) */
+  BDDC_NOT_PSD = 3,               /* pencil right-hand side not PSD (linalg.py:151-152) */
+  /* per-glob kernels: 100 + sharer index  = glob Schur block singular
+                       200 + status        = pencil failure                      */
+};
+
+/* ---- local.cu : substructuring -------------------------------------------- */
+
+/* Dense local matrix [I|B] x [I|B|f] from element blocks with Dirichlet lifting.
+ * replaces substructuring.py:98-114 (COO->CSR assembly, load, lifting). */
+int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
+                        const long long* elem_start, const long long* elem_ids, const int* loc4,
+                        const long long* conn, const double* Ke, const double* Fe,
+                        const double* gdir, int nbatch, long long max_elems, cudaStream_t stream);
+
+/* Blocked Schur elimination without pivoting (panel 64, DMMA trailing update):
+ * eliminates npiv[b] leading pivots; trailing block becomes the Schur complement,
+ * pivot rows keep W = A11^-1 A12 for back-substitution.
+ * replaces splu(A_II) + lu.solve + A_BI @ (...)  substructuring.py:120-127,
+ *          lu_factor(coarse) solver.py:123 (with piv_out for the pivot check :124-132),
+ *          cho_factor(sym(Sdd)) certificate solver.py:94 (require_positive = 1). */
+int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const int* npiv,
+                         const int* nrows, const int* ncols, int nbatch, int max_npiv,
+                         int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
+                         long long pinv_step_stride, int* status, int require_positive,
+                         double* piv_out, long long piv_stride, cudaStream_t stream);
+
+/* Blocked in-place Gauss-Jordan inverse (no pivoting).
+ * replaces cho_factor/cho_solve(Bsym, I) substructuring.py:64-75 (require_positive = 1)
+ *          lu_factor(Sdd) + lu_solve solver.py:99, 105, 187, 195 (require_positive = 0). */
+int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n, int nbatch,
+                    int max_n, double* pinv_ws, long long pinv_stride, int* status,
+                    int require_positive, cudaStream_t stream);
+
+/* S, g, Bsym = (S + S^T)/2 from the eliminated local matrices.
+ * replaces SubdomainOperator.__init__ substructuring.py:35-40. */
+int bddc_extract_schur(const double* M, const long long* off, const int* ld, const int* nI,
+                       const int* nB, const long long* soff, const long long* voff, double* S,
+                       double* Bsym, double* g, int nbatch, cudaStream_t stream);
+
+int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
+                    cudaStream_t stream);
+
+/* u_I = A_II^-1 (f_I - A_IB u_B) by block back-substitution.
+ * replaces recover_interior solver.py:318-326. */
+int bddc_recover_interior(const double* M, const long long* off, const int* ld, const int* nI,
+                          const int* nB, const long long* voff, const int* iface_perm,
+                          const long long* ioff, const long long* interior_nodes,
+                          const double* u_hat, double* u, int nbatch, int max_nloc,
+                          cudaStream_t stream);
+
+/* ---- globs.cu : scaling and adaptive coarse space ------------------------- */
+
+/* Deluxe scaling D_s = (sum_k B_k)^-1 B_s per glob; vertices 1/|n(V)|.
+ * replaces deluxe_scaling / vertex_scaling / build_scaling scaling.py:10-57. */
+int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
+                const int* sh_boff, const long long* sh_doff, const int* nB,
+                const long long* soff, const double* Bsym, double* D, double* ws,
+                const long long* ws_off, int* status, int n_globs, cudaStream_t stream);
+
+/* Face GEP + selection + change of basis.
+ * replaces face_gevp adaptive.py:57-72, glob_schur_block substructuring.py:152-171,
+ *          parallel_sum / pseudo_inverse / sym_pencil_gevp linalg.py:23-214,
+ *          build_change_of_basis adaptive.py:190-206. */
+int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
+                   const int* sh_boff, const long long* sh_doff, const int* nB,
+                   const long long* soff, const double* Bsym, const double* Binv, const double* D,
+                   double theta, double* eig, const long long* eig_off, int* n_sel, int* r,
+                   double* Q, const long long* q_off, int* status, double* ws,
+                   const long long* ws_off, const int* face_ids, int n_faces, int max_n,
+                   cudaStream_t stream);
+
+/* Prior blocks of the face-transformed Bsym^-1 per subdomain.
+ * replaces adaptive.py:310-329 (Minv = Q Bsym^-1 Q^T on face rows/cols, prior_idx). */
+int bddc_priors(const int* kind, const int* size, const int* nB, const long long* soff,
+                const double* Binv, const int* sub_glob_start, const int* sub_globs,
+                const int* sub_glob_boff, const int* r, const double* Q, const long long* q_off,
+                const long long* pb_off, const int* nH, double* PB, double* XHH,
+                const long long* xhh_off, int n_sub, cudaStream_t stream);
+
+/* Prior-aware ("new") edge GEP + SVD reduction + change of basis.
+ * replaces edge_block_with_priors substructuring.py:174-190, edge_gevp_new
+ *          adaptive.py:94-156, reduce_edge_constraints adaptive.py:172-187. */
+int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
+                       const int* sh_boff, const long long* sh_doff, const int* nB,
+                       const long long* soff, const double* Bsym, const double* Binv,
+                       const double* D, const long long* pb_off, const int* nH, const double* PB,
+                       const double* XHH, const long long* xhh_off, double theta, double* eig,
+                       const long long* eig_off, int* n_sel, int* r, double* Q,
+                       const long long* q_off, int* status, double* ws, const long long* ws_off,
+                       const int* edge_ids, int n_edges, int max_dim, cudaStream_t stream);
+
+/* Coupled ("old") edge GEP. replaces edge_gevp_old adaptive.py:75-91,
+ *          parallel_sum_chain linalg.py:70-78. */
+int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
+                       const int* sh_boff, const long long* sh_doff, const int* nB,
+                       const long long* soff, const double* Bsym, const double* Binv,
+                       const double* D, double theta, double* eig, const long long* eig_off,
+                       int* n_sel, int* r, double* Q, const long long* q_off, int* status,
+                       double* ws, const long long* ws_off, const int* edge_ids, int n_edges,
+                       int max_n, cudaStream_t stream);
+
+/* workspace sizes (doubles) of the per-glob kernels, for the host planner */
+long long bddc_ws_face(long long n);
+long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long nhmax);
+
+/* ---- precond.cu : preconditioner setup / apply, interface operator -------- */
+
+/* Sbar = Q_i S_i Q_i^T (block diagonal Q_i per glob).  replaces solver.py:85-86. */
+int bddc_pc_transform_schur(const int* nB, const long long* soff, const long long* voff,
+                            const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+                            const int* sub_glob_sh, const int* gsize, const double* Q,
+                            const long long* q_off, const double* S, double* tmp, double* Sbar,
+                            int nbatch, cudaStream_t stream);
+
+/* TT_(g,s) = D_g^(s) Q_g^T blocks.  replaces Dbar solver.py:87-90. */
+int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
+                     const long long* q_off, const double* D, const long long* sh_doff,
+                     double* TT, int n_slots, cudaStream_t stream);
+
+/* Zin = Sbar with primal rows/cols -> identity; Csym = sym(Zin).  solver.py:84, 91-94. */
+int bddc_pc_dual_embed(const int* nB, const long long* soff, const long long* voff,
+                       const unsigned char* primal_mask, const double* Sbar, double* Zin,
+                       double* Csym, int nbatch, cudaStream_t stream);
+
+int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* voff,
+                        const unsigned char* primal_mask, double* Z, int nbatch,
+                        cudaStream_t stream);
+
+/* A_i = T_i^T Z_i T_i (local part of M^-1).  replaces scale/tilde_solve solver.py:163-199. */
+int bddc_pc_local_operator(const int* nB, const long long* soff, const long long* voff,
+                           const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+                           const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
+                           const double* TT, const double* Z, double* tmp, double* A, int nbatch,
+                           cudaStream_t stream);
+
+/* MP = E_P - (Z Sbar)_{:,P}^T rows, RP = E_P - (Sbar Z)_{P,:}, C_i = Sbar_PP - Sbar_P: Z Sbar_:P.
+ * replaces solver.py:102-106. */
+int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstart,
+                          const int* ppos, const long long* poff, const double* Sbar,
+                          const double* Z, double* MP, double* RP, double* Cl,
+                          const long long* coff, int nbatch, cudaStream_t stream);
+
+int bddc_pc_primal_rows_T(const int* nB, const long long* voff, const int* pos2k,
+                          const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,
+                          const int* gsize, const long long* sh_doff, const double* TT,
+                          const int* pstart, const long long* poff, const double* In, double* Out,
+                          int nbatch, cudaStream_t stream);
+
+/* coarse[g,g] += contrib.  replaces solver.py:106. */
+int bddc_coarse_scatter(const int* pstart, const int* pgid, const double* Cl,
+                        const long long* coff, double* C, long long ldc, int nbatch,
+                        cudaStream_t stream);
+
+/* y_i = M_i u[perm_i] (+ c_i = G_i u[perm_i]).  replaces interface_operator solver.py:229-233
+ * (M = S) and the local half of BddcPreconditioner.apply solver.py:201-209 (M = A). */
+int bddc_local_gemv(const int* nB, const long long* soff, const long long* voff,
+                    const int* iface_perm, const double* M, const double* u, double* y,
+                    const int* pstart, const long long* poff, const double* G, double* cvals,
+                    int nbatch, int max_nB, int row_chunks, cudaStream_t stream);
+
+/* y_i += N_i u_P[gprimal_i].  replaces solver.py:193-198 + scale + inject_t. */
+int bddc_prolong_primal(const int* nB, const long long* voff, const int* pstart, const int* pgid,
+                        const long long* poff, const double* Nt, const double* uP, double* y,
+                        int nbatch, cudaStream_t stream);
+
+/* out[t] = sum of y over the CSR sources of t (deterministic subassembly).
+ * replaces out[op.iface_index] += ... solver.py:231-232, 159-160. */
+int bddc_gather_reduce(const long long* tstart, const long long* tsrc, const double* y,
+                       double* out, long long n, cudaStream_t stream);
+
+/* coarse solve with the factors of bddc_schur_eliminate.  replaces lu_solve(coarse_lu) solver.py:192. */
+int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
+                      long long pinv_step_stride, double* b, double* t, cudaStream_t stream);
+
+/* ---- krylov.cu : GMRES vector kernels (solver.py:286-310) ------------------ */
+
+int bddc_multi_dot(const double* V, long long n, int m, const double* w, double* h,
+                   double* partial, int nblocks, int accumulate, cudaStream_t stream);
+int bddc_multi_axpy(const double* V, long long n, int m, const double* coef, double alpha,
+                    double* w, cudaStream_t stream);
+int bddc_norm2(const double* w, long long n, double* out, double* partial, int nblocks,
+               cudaStream_t stream);
+int bddc_scale_copy(const double* a, long long n, const double* den, double* out,
+                    cudaStream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BDDC_B200_H */

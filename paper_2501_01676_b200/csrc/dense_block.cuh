@@ -1,0 +1,444 @@
+// CTA-cooperative small dense linear algebra in fp64 (row-major, any
+// leading dimension, generic pointers: shared or global memory).
+//
+// Every routine must be called by all threads of the block with uniform
+// arguments; each ends with __syncthreads() so results are visible.
+// These are the per-glob building blocks of the face / edge eigenproblems
+// (reference linalg.py, substructuring.py:161-171, scaling.py:10-25,
+// adaptive.py:57-206).
+#pragma once
+#include "common.cuh"
+
+namespace bddc {
+namespace blk {
+
+BDDC_DEV int tid() { return threadIdx.x; }
+BDDC_DEV int nth() { return blockDim.x; }
+
+BDDC_DEV void copy(double* dst, int ldd, const double* src, int lds, int m, int n) {
+  for (int idx = tid(); idx < m * n; idx += nth()) {
+    int r = idx / n, c = idx - r * n;
+    dst[r * ldd + c] = src[r * lds + c];
+  }
+  __syncthreads();
+}
+
+BDDC_DEV void set_identity(double* A, int ld, int m, int n) {
+  for (int idx = tid(); idx < m * n; idx += nth()) {
+    int r = idx / n, c = idx - r * n;
+    A[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+}
+
+BDDC_DEV void fill(double* A, int ld, int m, int n, double v) {
+  for (int idx = tid(); idx < m * n; idx += nth()) {
+    int r = idx / n, c = idx - r * n;
+    A[r * ld + c] = v;
+  }
+  __syncthreads();
+}
+
+// A <- (A + A^T)/2
+BDDC_DEV void symmetrize(double* A, int ld, int n) {
+  for (int idx = tid(); idx < n * n; idx += nth()) {
+    int r = idx / n, c = idx - r * n;
+    if (c > r) {
+      double v = 0.5 * (A[r * ld + c] + A[c * ld + r]);
+      A[r * ld + c] = v;
+      A[c * ld + r] = v;
+    }
+  }
+  __syncthreads();
+}
+
+// C = beta*C + alpha*op(A)*op(B);  op(A) m x k, op(B) k x n.  C must not alias A/B.
+BDDC_DEV void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb,
+                   bool tb, int m, int n, int k, double alpha, double beta) {
+  for (int idx = tid(); idx < m * n; idx += nth()) {
+    int r = idx / n, c = idx - r * n;
+    double s = 0.0;
+    for (int p = 0; p < k; ++p) {
+      double a = ta ? A[p * lda + r] : A[r * lda + p];
+      double b = tb ? B[c * ldb + p] : B[p * ldb + c];
+      s = fma(a, b, s);
+    }
+    double v = alpha * s;
+    if (beta != 0.0) v += beta * C[r * ldc + c];
+    C[r * ldc + c] = v;
+  }
+  __syncthreads();
+}
+
+// In-place scalar Gauss-Jordan inverse without pivoting.  Returns 0 on
+// success, kNotPositiveDefinite if require_positive and a pivot <= 0 (the
+// LDL^T pivots of a symmetric matrix: positive iff SPD, the cho_factor
+// criterion), kSingularPivot on a zero / non-finite pivot.  rowbuf: 2n doubles.
+BDDC_DEV int gj_inverse(double* A, int ld, int n, bool require_positive, double* rowbuf) {
+  __shared__ int bad;
+  if (tid() == 0) bad = 0;
+  __syncthreads();
+  for (int p = 0; p < n; ++p) {
+    const double piv = A[p * ld + p];
+    const bool fail = !(piv == piv) || piv == 0.0 || isinf(piv) || (require_positive && !(piv > 0.0));
+    if (fail) {
+      if (tid() == 0) bad = require_positive ? kNotPositiveDefinite : kSingularPivot;
+      __syncthreads();
+      break;
+    }
+    const double ip = 1.0 / piv;
+    double* colbuf = rowbuf + n;
+    for (int c = tid(); c < n; c += nth()) {
+      rowbuf[c] = (c == p) ? ip : A[p * ld + c] * ip;
+      colbuf[c] = A[c * ld + p];
+    }
+    __syncthreads();
+    for (int idx = tid(); idx < n * n; idx += nth()) {
+      int r = idx / n, c = idx - r * n;
+      if (r == p) {
+        A[r * ld + c] = rowbuf[c];
+      } else {
+        const double f = colbuf[r];
+        A[r * ld + c] = (c == p) ? -f * ip : A[r * ld + c] - f * rowbuf[c];
+      }
+    }
+    __syncthreads();
+  }
+  int out = bad;
+  __syncthreads();
+  return out;
+}
+
+// Cholesky A = L L^T in place (lower triangle).  Returns false when a pivot
+// is <= 0 or not finite (LAPACK potrf failure).
+BDDC_DEV bool cholesky(double* A, int ld, int n) {
+  __shared__ int bad;
+  if (tid() == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    const double d = A[j * ld + j];
+    if (!(d > 0.0) || isinf(d)) {
+      if (tid() == 0) bad = 1;
+      __syncthreads();
+      break;
+    }
+    const double s = sqrt(d);
+    __syncthreads();
+    for (int i = j + 1 + tid(); i < n; i += nth()) A[i * ld + j] /= s;
+    if (tid() == 0) A[j * ld + j] = s;
+    __syncthreads();
+    const int m = n - j - 1;
+    for (int idx = tid(); idx < m * m; idx += nth()) {
+      int r = idx / m, c = idx - r * m;
+      if (c <= r) {
+        int ri = j + 1 + r, ci = j + 1 + c;
+        A[ri * ld + ci] -= A[ri * ld + j] * A[ci * ld + j];
+      }
+    }
+    __syncthreads();
+  }
+  bool ok = bad == 0;
+  __syncthreads();
+  return ok;
+}
+
+// Solve (L L^T) X = B in place for B (n x nrhs), L from cholesky().
+BDDC_DEV void chol_solve(const double* L, int ld, int n, double* B, int ldb, int nrhs) {
+  for (int j = 0; j < n; ++j) {  // forward
+    const double d = L[j * ld + j];
+    for (int c = tid(); c < nrhs; c += nth()) B[j * ldb + c] /= d;
+    __syncthreads();
+    const int m = n - j - 1;
+    for (int idx = tid(); idx < m * nrhs; idx += nth()) {
+      int r = j + 1 + idx / nrhs, c = idx % nrhs;
+      B[r * ldb + c] -= L[r * ld + j] * B[j * ldb + c];
+    }
+    __syncthreads();
+  }
+  for (int j = n - 1; j >= 0; --j) {  // backward with L^T
+    const double d = L[j * ld + j];
+    for (int c = tid(); c < nrhs; c += nth()) B[j * ldb + c] /= d;
+    __syncthreads();
+    for (int idx = tid(); idx < j * nrhs; idx += nth()) {
+      int r = idx / nrhs, c = idx % nrhs;
+      B[r * ldb + c] -= L[j * ld + r] * B[j * ldb + c];
+    }
+    __syncthreads();
+  }
+}
+
+// Block-wide max reduction helper (returns the same value on all threads).
+BDDC_DEV double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = tid() >> 5, l = tid() & 31, nw = (nth() + 31) >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int i = 1; i < nw; ++i) r = fmax(r, red[i]);
+  __syncthreads();
+  return r;
+}
+
+BDDC_DEV double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = tid() >> 5, l = tid() & 31, nw = (nth() + 31) >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int i = 0; i < nw; ++i) r += red[i];
+  __syncthreads();
+  return r;
+}
+
+// Symmetric eigendecomposition by cyclic parallel two-sided Jacobi
+// (round-robin pairing).  A (n x n, symmetric) is destroyed; w gets the
+// eigenvalues in ascending order; if V != nullptr its columns are the
+// matching orthonormal eigenvectors.  cs: 2*(n+1) doubles of scratch,
+// perm: n+1 ints of scratch (shared memory preferred).
+// Returns false if the sweep limit was reached.
+BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ldv, double* cs,
+                          int* perm, double* red) {
+  if (V) set_identity(V, ldv, n, n);
+  if (n <= 1) {
+    if (n == 1 && tid() == 0) w[0] = A[0];
+    __syncthreads();
+    return true;
+  }
+  const int m = n + (n & 1);  // even player count; index n is a bye when n is odd
+  const int half = m / 2;
+  bool converged = false;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, dg = 0.0;
+    for (int idx = tid(); idx < n * n; idx += nth()) {
+      int r = idx / n, c = idx - r * n;
+      double v = A[r * ld + c];
+      if (r == c) dg += v * v; else off += v * v;
+    }
+    off = block_sum(off, red);
+    dg = block_sum(dg, red);
+    const double tol = fmax(1e-30, 4.0 * (double)n * (double)n * 4.9e-32);
+    if (off <= tol * dg || off == 0.0) { converged = true; break; }
+    for (int round = 0; round < m - 1; ++round) {
+      // pairs: (0, m-1 rotated) tournament; slot i pairs position i with m-1-i
+      for (int i = tid(); i < half; i += nth()) {
+        int a = (i == 0) ? 0 : 1 + (i - 1 + round) % (m - 1);
+        int b = 1 + (m - 2 - i + round) % (m - 1);
+        int p = min(a, b), q = max(a, b);
+        double c = 1.0, s = 0.0;
+        if (q < n) {
+          const double apq = A[p * ld + q];
+          const double app = A[p * ld + p], aqq = A[q * ld + q];
+          if (apq != 0.0 && fabs(apq) > 1e-300) {
+            const double tau = (aqq - app) / (2.0 * apq);
+            const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+          }
+        }
+        perm[2 * i] = p;
+        perm[2 * i + 1] = q;
+        cs[2 * i] = c;
+        cs[2 * i + 1] = s;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int idx = tid(); idx < half * n; idx += nth()) {
+        int i = idx / n, j = idx - i * n;
+        int p = perm[2 * i], q = perm[2 * i + 1];
+        if (q >= n) continue;
+        double c = cs[2 * i], s = cs[2 * i + 1];
+        if (s == 0.0) continue;
+        double ap = A[p * ld + j], aq = A[q * ld + j];
+        A[p * ld + j] = c * ap - s * aq;
+        A[q * ld + j] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int idx = tid(); idx < half * n; idx += nth()) {
+        int i = idx / n, j = idx - i * n;
+        int p = perm[2 * i], q = perm[2 * i + 1];
+        if (q >= n) continue;
+        double c = cs[2 * i], s = cs[2 * i + 1];
+        if (s == 0.0) continue;
+        double ap = A[j * ld + p], aq = A[j * ld + q];
+        A[j * ld + p] = c * ap - s * aq;
+        A[j * ld + q] = s * ap + c * aq;
+        if (V) {
+          double vp = V[j * ldv + p], vq = V[j * ldv + q];
+          V[j * ldv + p] = c * vp - s * vq;
+          V[j * ldv + q] = s * vp + c * vq;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // ascending sort of the diagonal (rank by counting; ties by index)
+  for (int i = tid(); i < n; i += nth()) {
+    double di = A[i * ld + i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      double dj = A[j * ld + j];
+      rank += (dj < di) || (dj == di && j < i);
+    }
+    perm[i] = rank;
+  }
+  __syncthreads();
+  for (int i = tid(); i < n; i += nth()) w[perm[i]] = A[i * ld + i];
+  __syncthreads();
+  if (V) {
+    // permute columns of V in place through A as scratch
+    for (int idx = tid(); idx < n * n; idx += nth()) {
+      int r = idx / n, c = idx - r * n;
+      A[r * ld + perm[c]] = V[r * ldv + c];
+    }
+    __syncthreads();
+    copy(V, ldv, A, ld, n, n);
+  }
+  return converged;
+}
+
+// One-sided Jacobi (Hestenes): orthogonalise the q columns of X (p x q) in
+// place by plane rotations; if Y != nullptr accumulate Y <- Y J (q x q,
+// caller initialises).  Afterwards column norms are singular values.
+BDDC_DEV bool onesided_jacobi(double* X, int ldx, int p, int q, double* Y, int ldy, double* cs,
+                              int* perm, double* red) {
+  if (q <= 1) return true;
+  const int m = q + (q & 1), half = m / 2;
+  bool converged = false;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double maxcos = 0.0;
+    for (int round = 0; round < m - 1; ++round) {
+      for (int i = tid(); i < half; i += nth()) {
+        int a = (i == 0) ? 0 : 1 + (i - 1 + round) % (m - 1);
+        int b = 1 + (m - 2 - i + round) % (m - 1);
+        perm[2 * i] = min(a, b);
+        perm[2 * i + 1] = max(a, b);
+      }
+      __syncthreads();
+      // column inner products, one warp per pair
+      const int warp = tid() >> 5, lane = tid() & 31, nw = nth() >> 5;
+      for (int i = warp; i < half; i += nw) {
+        int u = perm[2 * i], v = perm[2 * i + 1];
+        double al = 0.0, be = 0.0, ga = 0.0;
+        if (v < q) {
+          for (int r = lane; r < p; r += 32) {
+            double xu = X[r * ldx + u], xv = X[r * ldx + v];
+            al += xu * xu;
+            be += xv * xv;
+            ga += xu * xv;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (lane == 0) {
+          double c = 1.0, s = 0.0;
+          if (v < q && ga != 0.0 && al > 0.0 && be > 0.0) {
+            double rc = fabs(ga) / sqrt(al * be);
+            maxcos = fmax(maxcos, rc);
+            if (rc > 1e-15) {
+              double zeta = (be - al) / (2.0 * ga);
+              double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              c = 1.0 / sqrt(1.0 + t * t);
+              s = c * t;
+            }
+          }
+          cs[2 * i] = c;
+          cs[2 * i + 1] = s;
+        }
+      }
+      __syncthreads();
+      for (int idx = tid(); idx < half * p; idx += nth()) {
+        int i = idx / p, r = idx - i * p;
+        int u = perm[2 * i], v = perm[2 * i + 1];
+        double c = cs[2 * i], s = cs[2 * i + 1];
+        if (v >= q || s == 0.0) continue;
+        double xu = X[r * ldx + u], xv = X[r * ldx + v];
+        X[r * ldx + u] = c * xu - s * xv;
+        X[r * ldx + v] = s * xu + c * xv;
+      }
+      if (Y) {
+        for (int idx = tid(); idx < half * q; idx += nth()) {
+          int i = idx / q, r = idx - i * q;
+          int u = perm[2 * i], v = perm[2 * i + 1];
+          double c = cs[2 * i], s = cs[2 * i + 1];
+          if (v >= q || s == 0.0) continue;
+          double yu = Y[r * ldy + u], yv = Y[r * ldy + v];
+          Y[r * ldy + u] = c * yu - s * yv;
+          Y[r * ldy + v] = s * yu + c * yv;
+        }
+      }
+      __syncthreads();
+    }
+    // warp-level maxima were written only by lane 0 threads; reduce them
+    double mc = block_max(maxcos, red);
+    if (mc <= 1e-15) { converged = true; break; }
+  }
+  return converged;
+}
+
+// Q (n x n) orthogonal whose first r rows are the given orthonormal rows
+// U (r x n, ldu) and whose remaining rows complete an orthonormal basis,
+// built from Householder reflectors of U^T.  H: n x n scratch,
+// vbuf: n doubles scratch.
+BDDC_DEV void complete_basis(const double* U, int ldu, int r, int n, double* Q, int ldq, double* H,
+                             int ldh, double* vbuf, double* red) {
+  // H <- U^T (n x r) in its first r columns, then QR by Householder
+  for (int idx = tid(); idx < n * r; idx += nth()) {
+    int i = idx / r, j = idx - i * r;
+    H[i * ldh + j] = U[j * ldu + i];
+  }
+  // Qacc (stored in Q as an n x n matrix, columns = basis) starts as I
+  set_identity(Q, ldq, n, n);
+  __syncthreads();
+  for (int j = 0; j < r; ++j) {
+    // v = x - alpha e_j on rows j..n-1 of column j
+    double ss = 0.0;
+    for (int i = j + tid(); i < n; i += nth()) ss += H[i * ldh + j] * H[i * ldh + j];
+    ss = block_sum(ss, red);
+    const double x0 = H[j * ldh + j];
+    const double alpha = (x0 >= 0.0 ? -1.0 : 1.0) * sqrt(ss);
+    for (int i = tid(); i < n; i += nth())
+      vbuf[i] = (i < j) ? 0.0 : (i == j ? x0 - alpha : H[i * ldh + j]);
+    __syncthreads();
+    double vn = 0.0;
+    for (int i = j + tid(); i < n; i += nth()) vn += vbuf[i] * vbuf[i];
+    vn = block_sum(vn, red);
+    if (vn > 0.0) {
+      const double beta = 2.0 / vn;
+      // apply to remaining columns of H (j..r-1): H <- (I - beta v v^T) H
+      for (int c = j + tid(); c < r; c += nth()) {
+        double d = 0.0;
+        for (int i = j; i < n; ++i) d += vbuf[i] * H[i * ldh + c];
+        d *= beta;
+        for (int i = j; i < n; ++i) H[i * ldh + c] -= d * vbuf[i];
+      }
+      // accumulate Qacc <- Qacc (I - beta v v^T): rows of Qacc
+      for (int rr = tid(); rr < n; rr += nth()) {
+        double d = 0.0;
+        for (int i = j; i < n; ++i) d += Q[rr * ldq + i] * vbuf[i];
+        d *= beta;
+        for (int i = j; i < n; ++i) Q[rr * ldq + i] -= d * vbuf[i];
+      }
+    }
+    __syncthreads();
+  }
+  // Qacc columns r.. complete span(U^T); write Q rows: [U; Qacc[:, r:]^T]
+  for (int idx = tid(); idx < n * n; idx += nth()) {
+    int i = idx / n, c = idx - i * n;
+    H[i * ldh + c] = Q[i * ldq + c];
+  }
+  __syncthreads();
+  for (int idx = tid(); idx < n * n; idx += nth()) {
+    int rr = idx / n, c = idx - rr * n;
+    Q[rr * ldq + c] = (rr < r) ? U[rr * ldu + c] : H[c * ldh + rr];
+  }
+  __syncthreads();
+}
+
+}  // namespace blk
+}  // namespace bddc

@@ -1,0 +1,923 @@
+// Per-glob kernels of the adaptive coarse space: deluxe scaling, face
+// eigenproblems, prior blocks, new / old edge eigenproblems, SVD-based
+// change of basis.  One CTA per glob (or per subdomain for the priors),
+// matrices in a per-glob global-memory workspace (L1/L2 resident at these
+// sizes), rotations / pivots staged in shared memory.
+//
+// Reference: scaling.py:10-57, substructuring.py:146-190, linalg.py:23-214,
+// adaptive.py:57-206, 288-342.
+#include "common.cuh"
+#include "dense_block.cuh"
+#include "glob_layout.h"
+
+namespace bddc {
+
+struct GlobTables {
+  // per glob
+  const int* kind;          // 0 face, 1 edge, 2 vertex
+  const int* size;          // n_g
+  const int* sh_start;      // sharer ranges into sh_sub / sh_boff / sh_doff
+  const int* sh_sub;        // sharer subdomain ids (ascending)
+  const int* sh_boff;       // block offset of the glob inside the sharer's glob-major B order
+  const long long* sh_doff; // offset of D_s (n_g x n_g) in the deluxe buffer
+  // per subdomain
+  const int* nB;
+  const long long* soff;    // offset of the nB x nB matrices (S, Bsym, Binv)
+  const double* Bsym;
+  const double* Binv;
+};
+
+// ---------------------------------------------------------------------------
+// pseudo-inverse (linalg.py:23-50) and parallel sum (linalg.py:53-67)
+// ---------------------------------------------------------------------------
+// P <- sym(M)^+ with eigenvalue cut rel_tol*max|w|.  ws: 2 n^2 + n doubles.
+BDDC_DEV void pinv_sym(const double* M, int n, double* P, double* ws, double* cs, int* perm,
+                       double* red) {
+  double* A = ws;
+  double* U = ws + n * n;
+  double* w = ws + 2 * n * n;
+  blk::copy(A, n, M, n, n, n);
+  blk::symmetrize(A, n, n);
+  blk::jacobi_eigh(A, n, n, w, U, n, cs, perm, red);
+  double mx = 0.0;
+  for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(w[i]));
+  const double cut = 1e-12 * mx;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    int r = idx / n, c = idx - r * n;
+    double s = 0.0;
+    for (int k = 0; k < n; ++k)
+      if (fabs(w[k]) > cut) s += U[r * n + k] * (1.0 / w[k]) * U[c * n + k];
+    P[r * n + c] = s;
+  }
+  __syncthreads();
+  blk::symmetrize(P, n, n);
+}
+
+// R <- sym(A (A+B)^+ B).  ws: 4 n^2 + n doubles.
+BDDC_DEV void parallel_sum(const double* A, const double* B, int n, double* R, double* ws,
+                           double* cs, int* perm, double* red) {
+  double* Sm = ws;
+  double* P = ws + n * n;
+  double* T = ws + 2 * n * n;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Sm[idx] = A[idx] + B[idx];
+  __syncthreads();
+  pinv_sym(Sm, n, P, ws + 3 * n * n, cs, perm, red);
+  blk::gemm(T, n, A, n, false, P, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(R, n, T, n, false, B, n, false, n, n, n, 1.0, 0.0);
+  blk::symmetrize(R, n, n);
+}
+
+// ---------------------------------------------------------------------------
+// symmetric pencil B v = lambda Bt v with PSD, possibly singular Bt
+// (linalg.py:116-214).  Output order: +inf | finite descending | degenerate.
+// ws: pencil_ws_doubles(n).  Returns a Status.
+// ---------------------------------------------------------------------------
+BDDC_DEV int pencil(const double* B, const double* Bt, int n, double* vals, double* vecs,
+                    int* degen, double* ws, double* cs, int* perm, double* red) {
+  const int nn = n * n;
+  double* A1 = ws;
+  double* U = A1 + nn;
+  double* mu = U + nn;
+  double* A2 = mu + n;
+  double* bw = A2 + nn;          // eigenvalues of B, later beta
+  double* T1 = bw + n;           // n x n
+  double* T2 = T1 + nn;          // n x n
+  double* T3 = T2 + nn;          // n x n
+  double* T4 = T3 + nn;          // n x n
+  double* T5 = T4 + nn;          // n x n
+  double* lam = T5 + nn;         // n
+  __shared__ int s_n0, s_status;
+  __shared__ double s_bscale;
+
+  blk::copy(A1, n, Bt, n, n, n);
+  blk::jacobi_eigh(A1, n, n, mu, U, n, cs, perm, red);
+  blk::copy(A2, n, B, n, n, n);
+  blk::jacobi_eigh(A2, n, n, bw, nullptr, 0, cs, perm, red);
+  if (threadIdx.x == 0) {
+    double mx = 0.0, mn = 0.0, bs = 0.0;
+    for (int i = 0; i < n; ++i) {
+      mx = fmax(mx, mu[i]);
+      mn = fmin(mn, mu[i]);
+      bs = fmax(bs, fabs(bw[i]));
+    }
+    s_status = (mn < -1e-10 * fmax(mx, 1.0)) ? (int)kNotPSD : 0;
+    int n0 = n;
+    if (mx > 0.0) {
+      n0 = 0;
+      while (n0 < n && !(mu[n0] > 1e-12 * mx)) ++n0;  // mu ascending: range is a suffix
+    }
+    s_n0 = n0;
+    s_bscale = bs;
+  }
+  __syncthreads();
+  if (s_status) return s_status;
+  const int n0 = s_n0, n1 = n - n0;
+  const double tiny = fmax(s_bscale, 1e-300);
+  const double* V0 = U;       // columns 0..n0-1
+  const double* V1 = U + n0;  // columns n0..n-1 (ld n)
+  int n_inf = 0;
+  double* B00p = T5;  // n0 x n0
+  if (n0 > 0) {
+    // B00 = V0^T B V0 ; eigh -> (beta, P)
+    blk::gemm(T1, n0, B, n, false, V0, n, false, n, n0, n, 1.0, 0.0);       // B V0 (n x n0)
+    blk::gemm(T2, n0, V0, n, true, T1, n0, false, n0, n0, n, 1.0, 0.0);     // V0^T B V0
+    blk::jacobi_eigh(T2, n0, n0, bw, T3, n0, cs, perm, red);                 // beta asc, P = T3
+    // acting modes ordered by decreasing |beta| (stable on ties by index)
+    __shared__ int s_ninf;
+    if (threadIdx.x == 0) {
+      int c = 0;
+      for (int j = 0; j < n0; ++j) c += fabs(bw[j]) > 1e-12 * tiny;
+      s_ninf = c;
+    }
+    __syncthreads();
+    n_inf = s_ninf;
+    for (int j = threadIdx.x; j < n0; j += blockDim.x) {
+      const bool act = fabs(bw[j]) > 1e-12 * tiny;
+      int rank = 0;
+      if (act) {
+        for (int i = 0; i < n0; ++i) {
+          if (!(fabs(bw[i]) > 1e-12 * tiny)) continue;
+          rank += (fabs(bw[i]) > fabs(bw[j])) || (fabs(bw[i]) == fabs(bw[j]) && i < j);
+        }
+      } else {
+        // degenerate: appended after all finite modes, in index order
+        for (int i = 0; i < j; ++i) rank += !(fabs(bw[i]) > 1e-12 * tiny);
+        rank += n_inf + n1;
+      }
+      perm[j] = rank;
+    }
+    __syncthreads();
+    // vectors V0 P[:, j]
+    for (int idx = threadIdx.x; idx < n * n0; idx += blockDim.x) {
+      int r = idx / n0, j = idx - r * n0;
+      double s = 0.0;
+      for (int k = 0; k < n0; ++k) s += V0[r * n + k] * T3[k * n0 + j];
+      T4[r * n0 + j] = s;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < n0; j += blockDim.x) {
+      const bool act = fabs(bw[j]) > 1e-12 * tiny;
+      double scale;
+      if (act) {
+        scale = 1.0 / sqrt(fabs(bw[j]));
+      } else {
+        double s = 0.0;
+        for (int r = 0; r < n; ++r) s += T4[r * n0 + j] * T4[r * n0 + j];
+        s = sqrt(s);
+        scale = s > 0.0 ? 1.0 / s : 1.0;
+      }
+      const int o = perm[j];
+      vals[o] = act ? INFINITY : 0.0;
+      degen[o] = act ? 0 : 1;
+      for (int r = 0; r < n; ++r) vecs[r * n + o] = T4[r * n0 + j] * scale;
+    }
+    __syncthreads();
+    // B00^+ = P_act diag(1/beta) P_act^T
+    for (int idx = threadIdx.x; idx < n0 * n0; idx += blockDim.x) {
+      int r = idx / n0, c = idx - r * n0;
+      double s = 0.0;
+      for (int k = 0; k < n0; ++k)
+        if (fabs(bw[k]) > 1e-12 * tiny) s += T3[r * n0 + k] * (1.0 / bw[k]) * T3[c * n0 + k];
+      B00p[r * n0 + c] = s;
+    }
+    __syncthreads();
+  }
+  if (n1 > 0) {
+    // W1 = V1 / sqrt(mu1)  -> T1 (n x n1)
+    for (int idx = threadIdx.x; idx < n * n1; idx += blockDim.x) {
+      int r = idx / n1, j = idx - r * n1;
+      T1[r * n1 + j] = V1[r * n + j] / sqrt(mu[n0 + j]);
+    }
+    __syncthreads();
+    blk::gemm(T2, n1, B, n, false, T1, n1, false, n, n1, n, 1.0, 0.0);   // BW (n x n1)
+    blk::gemm(T3, n1, T1, n1, true, T2, n1, false, n1, n1, n, 1.0, 0.0); // Bh = W1^T BW
+    double* Cm = T4;  // n0 x n1
+    if (n0 > 0) {
+      blk::gemm(Cm, n1, V0, n, true, T2, n1, false, n0, n1, n, 1.0, 0.0);  // C = V0^T BW
+      blk::gemm(T2, n1, B00p, n0, false, Cm, n1, false, n0, n1, n0, 1.0, 0.0);  // B00p C
+      blk::gemm(T3, n1, Cm, n1, true, T2, n1, false, n1, n1, n0, -1.0, 1.0);    // Bh -= C^T B00p C
+    }
+    blk::symmetrize(T3, n1, n1);
+    // eigh(Bh) -> lam asc, Y (reuse A2 for Y)
+    double* Y = A2;
+    blk::jacobi_eigh(T3, n1, n1, lam, Y, n1, cs, perm, red);
+    // Vf = W1 Y  (- V0 B00p C Y)
+    blk::gemm(T3, n1, T1, n1, false, Y, n1, false, n, n1, n1, 1.0, 0.0);
+    if (n0 > 0) {
+      blk::gemm(A1, n1, Cm, n1, false, Y, n1, false, n0, n1, n1, 1.0, 0.0);      // C Y
+      blk::gemm(T1, n1, B00p, n0, false, A1, n1, false, n0, n1, n0, 1.0, 0.0);   // B00p C Y
+      blk::gemm(T3, n1, V0, n, false, T1, n1, false, n, n1, n0, -1.0, 1.0);      // Vf -= V0 (.)
+    }
+    const double floor = 1e-14 * tiny;
+    for (int j = threadIdx.x; j < n1; j += blockDim.x) {
+      const int o = n_inf + (n1 - 1 - j);  // descending
+      const double l = lam[j];
+      const double sc = fabs(l) > floor ? 1.0 / sqrt(fabs(l)) : 1.0;
+      vals[o] = l;
+      degen[o] = 0;
+      for (int r = 0; r < n; ++r) vecs[r * n + o] = T3[r * n1 + j] * sc;
+    }
+    __syncthreads();
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Right singular basis of rows A (m x n): Q (n x n) with Q[:r] spanning the
+// row space, r = #{s >= 1e-10 s_max} (adaptive.py:172-206).  ws:
+// svd_ws_doubles(m, n).
+// ---------------------------------------------------------------------------
+BDDC_DEV int row_space_basis(const double* A, int lda, int m, int n, double* Q, double* ws,
+                             double* cs, int* perm, double* red) {
+  __shared__ int s_r;
+  if (m == 0) {
+    blk::set_identity(Q, n, n, n);
+    return 0;
+  }
+  double* X;
+  double* Y = nullptr;
+  int q;  // number of columns orthogonalised
+  double* U = ws;             // r x n output rows (<= n x n)
+  double* H = U + n * n;      // n x n scratch
+  double* vb = H + n * n;     // n
+  double* sg = vb + n;        // max(m, n)
+  double* Xb = sg + (m > n ? m : n);
+  if (m <= n) {
+    X = Xb;  // n x m = A^T
+    for (int idx = threadIdx.x; idx < n * m; idx += blockDim.x) {
+      int r = idx / m, c = idx - r * m;
+      X[r * m + c] = A[c * lda + r];
+    }
+    __syncthreads();
+    q = m;
+    blk::onesided_jacobi(X, m, n, m, nullptr, 0, cs, perm, red);
+  } else {
+    X = Xb;  // m x n copy
+    Y = Xb + m * n;
+    blk::copy(X, n, A, lda, m, n);
+    blk::set_identity(Y, n, n, n);
+    q = n;
+    blk::onesided_jacobi(X, n, m, n, Y, n, cs, perm, red);
+  }
+  const int rows_x = (m <= n) ? n : m;
+  for (int j = threadIdx.x; j < q; j += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < rows_x; ++r) s += X[r * q + j] * X[r * q + j];
+    sg[j] = sqrt(s);
+  }
+  __syncthreads();
+  // descending order by singular value (ties by index)
+  for (int j = threadIdx.x; j < q; j += blockDim.x) {
+    int rank = 0;
+    for (int i = 0; i < q; ++i) rank += (sg[i] > sg[j]) || (sg[i] == sg[j] && i < j);
+    perm[j] = rank;
+  }
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < q; ++i) mx = fmax(mx, sg[i]);
+    int r = 0;
+    for (int i = 0; i < q; ++i) r += sg[i] >= 1e-10 * mx;
+    s_r = (mx > 0.0) ? r : 0;
+  }
+  __syncthreads();
+  const int r = s_r;
+  for (int j = threadIdx.x; j < q; j += blockDim.x) {
+    const int o = perm[j];
+    if (o >= r) continue;
+    if (m <= n) {
+      const double inv = 1.0 / sg[j];
+      for (int c = 0; c < n; ++c) U[o * n + c] = X[c * q + j] * inv;
+    } else {
+      for (int c = 0; c < n; ++c) U[o * n + c] = Y[c * n + j];
+    }
+  }
+  __syncthreads();
+  blk::complete_basis(U, n, r, n, Q, n, H, n, vb, red);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// deluxe scaling: D_s = (sum_k B_k)^-1 B_s  (scaling.py:10-33)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) deluxe_kernel(GlobTables t, double* __restrict__ D,
+                                                     double* __restrict__ ws,
+                                                     const long long* __restrict__ ws_off,
+                                                     int* __restrict__ status) {
+  __shared__ double rowbuf[2048];
+  const int g = blockIdx.x;
+  const int n = t.size[g];
+  const int s0 = t.sh_start[g], s1 = t.sh_start[g + 1];
+  if (t.kind[g] == 2 && n == 1) {
+    if (threadIdx.x == 0)
+      for (int k = s0; k < s1; ++k) D[t.sh_doff[k]] = 1.0 / (double)(s1 - s0);
+    return;
+  }
+  double* T = ws + ws_off[g];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    int r = idx / n, c = idx - r * n;
+    double s = 0.0;
+    for (int k = s0; k < s1; ++k) {
+      const int sub = t.sh_sub[k], bo = t.sh_boff[k], nb = t.nB[sub];
+      s += t.Bsym[t.soff[sub] + (long long)(bo + r) * nb + bo + c];
+    }
+    T[idx] = s;
+  }
+  __syncthreads();
+  const int st = blk::gj_inverse(T, n, n, true, rowbuf);
+  if (st) {
+    if (threadIdx.x == 0) status[g] = st;
+    return;
+  }
+  for (int k = s0; k < s1; ++k) {
+    const int sub = t.sh_sub[k], bo = t.sh_boff[k], nb = t.nB[sub];
+    const double* Bs = t.Bsym + t.soff[sub] + (long long)bo * nb + bo;
+    blk::gemm(D + t.sh_doff[k], n, T, n, false, Bs, nb, false, n, n, n, 1.0, 0.0);
+  }
+}
+
+// B~_X = sym(((Binv)[X,X])^-1) of sharer k into out (n x n); returns Status.
+BDDC_DEV int glob_schur(const GlobTables& t, int k, int n, double* out, double* rowbuf) {
+  const int sub = t.sh_sub[k], bo = t.sh_boff[k], nb = t.nB[sub];
+  blk::copy(out, n, t.Binv + t.soff[sub] + (long long)bo * nb + bo, nb, n, n);
+  const int st = blk::gj_inverse(out, n, n, true, rowbuf);
+  if (st) return st;
+  blk::symmetrize(out, n, n);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// face eigenproblem (adaptive.py:57-72) + change of basis (adaptive.py:190-206)
+// ---------------------------------------------------------------------------
+struct GlobOut {
+  double* eig;              // eigenvalues, eig_off[g]
+  const long long* eig_off;
+  int* n_sel;               // selected eigenpairs per glob
+  int* r;                   // primal count per glob (rank of constraints)
+  double* Q;                // n_g x n_g, q_off[g]
+  const long long* q_off;
+  int* status;              // per glob
+};
+
+__global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* __restrict__ D,
+                                                   double theta, GlobOut o,
+                                                   double* __restrict__ ws,
+                                                   const long long* __restrict__ ws_off,
+                                                   const int* __restrict__ face_ids) {
+  extern __shared__ double sh[];
+  const int g = face_ids[blockIdx.x];
+  const int n = t.size[g];
+  const int nn = n * n;
+  double* cs = sh;                                  // 2(n+2)
+  double* red = cs + 2 * (n + 2);                   // 32
+  double* rowbuf = red + 32;                        // 2(n+2)
+  int* perm = reinterpret_cast<int*>(rowbuf + 2 * (n + 2));   // 2(n+2)
+  double* W = ws + ws_off[g];
+  double* BF = W;
+  double* Bt = BF + nn;
+  double* Bti = Bt + nn;
+  double* Btj = Bti + nn;
+  double* T = Btj + nn;
+  double* vecs = T + nn;
+  double* rows = vecs + nn;
+  int* degen = reinterpret_cast<int*>(rows + nn);   // n ints (n doubles reserved)
+  double* scratch = rows + nn + n;
+  const int k0 = t.sh_start[g];
+  const int si = t.sh_sub[k0], sj = t.sh_sub[k0 + 1];
+  const double* Di = D + t.sh_doff[k0];
+  const double* Dj = D + t.sh_doff[k0 + 1];
+  const double* Bi = t.Bsym + t.soff[si] + (long long)t.sh_boff[k0] * t.nB[si] + t.sh_boff[k0];
+  const double* Bj = t.Bsym + t.soff[sj] + (long long)t.sh_boff[k0 + 1] * t.nB[sj] + t.sh_boff[k0 + 1];
+  const int ldi = t.nB[si], ldj = t.nB[sj];
+  // B_F = sym(Dj^T Bi Dj + Di^T Bj Di)
+  blk::gemm(T, n, Bi, ldi, false, Dj, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(BF, n, Dj, n, true, T, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(T, n, Bj, ldj, false, Di, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(BF, n, Di, n, true, T, n, false, n, n, n, 1.0, 1.0);
+  blk::symmetrize(BF, n, n);
+  int st = glob_schur(t, k0, n, Bti, rowbuf);
+  if (st) {
+    if (threadIdx.x == 0) o.status[g] = 100;
+    return;
+  }
+  st = glob_schur(t, k0 + 1, n, Btj, rowbuf);
+  if (st) {
+    if (threadIdx.x == 0) o.status[g] = 101;
+    return;
+  }
+  parallel_sum(Bti, Btj, n, Bt, scratch, cs, perm, red);
+  double* vals = o.eig + o.eig_off[g];
+  st = pencil(BF, Bt, n, vals, vecs, degen, scratch, cs, perm, red);
+  if (st) {
+    if (threadIdx.x == 0) o.status[g] = 200 + st;
+    return;
+  }
+  // selected columns -> rows = (B_F V_sel)^T
+  __shared__ int s_nsel;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int j = 0; j < n; ++j) {
+      const bool sel = (vals[j] >= theta) && !degen[j];
+      perm[j] = sel ? c : -1;
+      c += sel;
+    }
+    s_nsel = c;
+  }
+  __syncthreads();
+  const int nsel = s_nsel;
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    int j = idx / n, c = idx - j * n;  // eigen column j, glob dof c
+    if (perm[j] < 0) continue;
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s += BF[c * n + k] * vecs[k * n + j];
+    rows[perm[j] * n + c] = s;
+  }
+  __syncthreads();
+  const int r = row_space_basis(rows, n, nsel, n, o.Q + o.q_off[g], scratch, cs, perm, red);
+  if (threadIdx.x == 0) {
+    o.n_sel[g] = nsel;
+    o.r[g] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// prior blocks per subdomain (adaptive.py:306-329):
+//   PB = P_H Binv (nH x nB),  XHH = PB P_H^T,  P_H rows = Q_F[:r_F] on each
+//   face block, unit rows on vertex positions (faces first, then vertices,
+//   glob order).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) priors_kernel(
+    GlobTables t, const int* __restrict__ sub_glob_start, const int* __restrict__ sub_globs,
+    const int* __restrict__ sub_glob_boff, const int* __restrict__ r, const double* __restrict__ Q,
+    const long long* __restrict__ q_off, const long long* __restrict__ pb_off,
+    const int* __restrict__ nH, double* __restrict__ PB, double* __restrict__ XHH,
+    const long long* __restrict__ xhh_off) {
+  const int s = blockIdx.x;
+  const int nb = t.nB[s];
+  const int h = nH[s];
+  if (h == 0) return;
+  const double* Binv = t.Binv + t.soff[s];
+  double* P = PB + pb_off[s];
+  const int g0 = sub_glob_start[s], g1 = sub_glob_start[s + 1];
+  // row offsets of each prior glob within H
+  // (sequential scan by thread 0 into shared memory)
+  __shared__ int hoff[1024];
+  if (threadIdx.x == 0) {
+    int c = 0, a = 0;
+    for (int k = g0; k < g1; ++k) {
+      const int g = sub_globs[k];
+      const int kd = t.kind[g];
+      if (kd == 1) continue;
+      hoff[a++] = c;
+      c += (kd == 2) ? t.size[g] : r[g];
+    }
+  }
+  __syncthreads();
+  // PB rows
+  int a = 0;
+  for (int k = g0; k < g1; ++k) {
+    const int g = sub_globs[k];
+    const int kd = t.kind[g];
+    if (kd == 1) continue;
+    const int bo = sub_glob_boff[k];
+    const int ng = t.size[g];
+    const int h0 = hoff[a++];
+    if (kd == 2) {
+      for (int idx = threadIdx.x; idx < ng * nb; idx += blockDim.x) {
+        int rr = idx / nb, c = idx - rr * nb;
+        P[(long long)(h0 + rr) * nb + c] = Binv[(long long)(bo + rr) * nb + c];
+      }
+    } else {
+      const int rf = r[g];
+      const double* Qg = Q + q_off[g];
+      for (int idx = threadIdx.x; idx < rf * nb; idx += blockDim.x) {
+        int rr = idx / nb, c = idx - rr * nb;
+        double v = 0.0;
+        for (int q = 0; q < ng; ++q) v += Qg[rr * ng + q] * Binv[(long long)(bo + q) * nb + c];
+        P[(long long)(h0 + rr) * nb + c] = v;
+      }
+    }
+  }
+  __syncthreads();
+  // XHH = PB P_H^T: column block of glob b
+  double* X = XHH + xhh_off[s];
+  a = 0;
+  for (int k = g0; k < g1; ++k) {
+    const int g = sub_globs[k];
+    const int kd = t.kind[g];
+    if (kd == 1) continue;
+    const int bo = sub_glob_boff[k];
+    const int ng = t.size[g];
+    const int h0 = hoff[a++];
+    const int rb = (kd == 2) ? ng : r[g];
+    const double* Qg = Q + q_off[g];
+    for (int idx = threadIdx.x; idx < h * rb; idx += blockDim.x) {
+      int rr = idx / rb, c = idx - rr * rb;
+      double v;
+      if (kd == 2) {
+        v = P[(long long)rr * nb + bo + c];
+      } else {
+        v = 0.0;
+        for (int q = 0; q < ng; ++q) v += P[(long long)rr * nb + bo + q] * Qg[c * ng + q];
+      }
+      X[rr * h + h0 + c] = v;
+    }
+  }
+  __syncthreads();
+  blk::symmetrize(X, h, h);
+}
+
+// ---------------------------------------------------------------------------
+// new edge eigenproblem (adaptive.py:94-156) + SVD reduction and change of
+// basis (adaptive.py:172-206)
+// ---------------------------------------------------------------------------
+struct PriorTables {
+  const long long* pb_off;
+  const int* nH;
+  const double* PB;
+  const double* XHH;
+  const long long* xhh_off;
+};
+
+__global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const double* __restrict__ D,
+                                                       PriorTables pr, double theta, GlobOut o,
+                                                       double* __restrict__ ws,
+                                                       const long long* __restrict__ ws_off,
+                                                       const int* __restrict__ edge_ids) {
+  extern __shared__ double sh[];
+  const int g = edge_ids[blockIdx.x];
+  const int ne = t.size[g];
+  const int k0 = t.sh_start[g], ns = t.sh_start[g + 1] - k0;
+  const int nC = (ns - 1) * ne;
+  int Wd = nC + ne;
+  for (int i = 0; i < ns; ++i) Wd += pr.nH[t.sh_sub[k0 + i]];
+  const int dimmax = Wd;
+  double* cs = sh;
+  double* red = cs + 2 * (dimmax + 2);
+  double* rowbuf = red + 32;
+  int* perm = reinterpret_cast<int*>(rowbuf + 2 * (dimmax + 2));
+
+  double* Wk = ws + ws_off[g];
+  double* Jall = Wk;                         // ns blocks of ne x nC
+  double* M = Jall + (long long)ns * ne * nC; // nC x nC
+  double* Bt = M + nC * nC;                  // Wd x Wd
+  double* X = Bt + (long long)Wd * Wd;       // (ne+nHmax)^2 per-sharer Schur block
+  int nHmax = 0;
+  for (int i = 0; i < ns; ++i) nHmax = max(nHmax, pr.nH[t.sh_sub[k0 + i]]);
+  const int xd = ne + nHmax;
+  double* T1 = X + (long long)xd * xd;       // scratch: max(Wd, nC) x max(Wd, nC)
+  double* T2 = T1 + (long long)Wd * Wd;
+  double* scratch = T2 + (long long)Wd * Wd;
+
+  // J_i = [delta_ik I - D_k]_{k=1..ns-1}
+  for (int idx = threadIdx.x; idx < ns * ne * nC; idx += blockDim.x) {
+    int i = idx / (ne * nC), rem = idx - i * ne * nC;
+    int r = rem / nC, c = rem - r * nC;
+    int kb = c / ne + 1, cc = c - (kb - 1) * ne;
+    const double* Dk = D + t.sh_doff[k0 + kb];
+    Jall[idx] = ((i == kb && r == cc) ? 1.0 : 0.0) - Dk[r * ne + cc];
+  }
+  __syncthreads();
+  // M = sym(sum_i J_i^T B_E^(i) J_i)
+  blk::fill(M, nC, nC, nC, 0.0);
+  for (int i = 0; i < ns; ++i) {
+    const int sub = t.sh_sub[k0 + i], bo = t.sh_boff[k0 + i], nb = t.nB[sub];
+    const double* BE = t.Bsym + t.soff[sub] + (long long)bo * nb + bo;
+    const double* Ji = Jall + (long long)i * ne * nC;
+    blk::gemm(T1, nC, BE, nb, false, Ji, nC, false, ne, nC, ne, 1.0, 0.0);
+    blk::gemm(M, nC, Ji, nC, true, T1, nC, false, nC, nC, ne, 1.0, 1.0);
+  }
+  blk::symmetrize(M, nC, nC);
+  // Bt assembly over (differences, average, priors)
+  const int A0 = nC + ne;
+  blk::fill(Bt, Wd, Wd, Wd, 0.0);
+  int hcol = A0;
+  for (int i = 0; i < ns; ++i) {
+    const int sub = t.sh_sub[k0 + i], bo = t.sh_boff[k0 + i], nb = t.nB[sub];
+    const int h = pr.nH[sub];
+    const int d = ne + h;
+    const double* Binv = t.Binv + t.soff[sub];
+    const double* PBs = pr.PB + pr.pb_off[sub];
+    const double* XH = pr.XHH + pr.xhh_off[sub];
+    // X = [[Binv[E,E], PB[:,E]^T], [PB[:,E], XHH]]
+    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
+      int r = idx / d, c = idx - r * d;
+      double v;
+      if (r < ne && c < ne) v = Binv[(long long)(bo + r) * nb + bo + c];
+      else if (r < ne) v = PBs[(long long)(c - ne) * nb + bo + r];
+      else if (c < ne) v = PBs[(long long)(r - ne) * nb + bo + c];
+      else v = XH[(r - ne) * h + (c - ne)];
+      X[r * d + c] = v;
+    }
+    __syncthreads();
+    int st = blk::gj_inverse(X, d, d, true, rowbuf);
+    if (st) {
+      if (threadIdx.x == 0) o.status[g] = 100 + i;
+      return;
+    }
+    blk::symmetrize(X, d, d);
+    // T_i = [J_i, I] (ne x A0): Bt[0:A0,0:A0] += T^T EE T ; off-diagonal H blocks
+    const double* Ji = Jall + (long long)i * ne * nC;
+    // T1 = EE T  (ne x A0)
+    for (int idx = threadIdx.x; idx < ne * A0; idx += blockDim.x) {
+      int r = idx / A0, c = idx - r * A0;
+      double s = 0.0;
+      for (int q = 0; q < ne; ++q) {
+        double tq = (c < nC) ? Ji[q * nC + c] : ((c - nC) == q ? 1.0 : 0.0);
+        s += X[r * d + q] * tq;
+      }
+      T1[r * A0 + c] = s;
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < A0 * A0; idx += blockDim.x) {
+      int r = idx / A0, c = idx - r * A0;
+      double s = 0.0;
+      for (int q = 0; q < ne; ++q) {
+        double tq = (r < nC) ? Ji[q * nC + r] : ((r - nC) == q ? 1.0 : 0.0);
+        s += tq * T1[q * A0 + c];
+      }
+      Bt[r * Wd + c] += s;
+    }
+    // Bt[0:A0, H] += T^T EH ; Bt[H, 0:A0] += HE T ; Bt[H, H] += HH
+    for (int idx = threadIdx.x; idx < A0 * h; idx += blockDim.x) {
+      int r = idx / h, c = idx - r * h;
+      double s1 = 0.0, s2 = 0.0;
+      for (int q = 0; q < ne; ++q) {
+        double tq = (r < nC) ? Ji[q * nC + r] : ((r - nC) == q ? 1.0 : 0.0);
+        s1 += tq * X[q * d + ne + c];          // T^T EH
+        s2 += X[(ne + c) * d + q] * tq;        // (HE T)^T entry
+      }
+      Bt[r * Wd + hcol + c] += s1;
+      Bt[(hcol + c) * Wd + r] += s2;
+    }
+    for (int idx = threadIdx.x; idx < h * h; idx += blockDim.x) {
+      int r = idx / h, c = idx - r * h;
+      Bt[(hcol + r) * Wd + hcol + c] += X[(ne + r) * d + ne + c];
+    }
+    __syncthreads();
+    hcol += h;
+  }
+  blk::symmetrize(Bt, Wd, Wd);
+  // Btt = sym(KK - KR RR^-1 KR^T)
+  const int nr = Wd - nC;
+  double* RR = T1;   // nr x nr
+  double* Z = T2;    // nr x nC  (RR^-1 KR^T)
+  blk::copy(RR, nr, Bt + (long long)nC * Wd + nC, Wd, nr, nr);
+  for (int idx = threadIdx.x; idx < nr * nC; idx += blockDim.x) {
+    int r = idx / nC, c = idx - r * nC;
+    Z[r * nC + c] = Bt[(long long)c * Wd + nC + r];
+  }
+  __syncthreads();
+  double* Btt = X;   // nC x nC (X no longer needed)
+  if (blk::cholesky(RR, nr, nr)) {
+    blk::chol_solve(RR, nr, nr, Z, nC, nC);
+  } else {
+    // pseudo-inverse fallback (adaptive.py:144-149)
+    blk::copy(RR, nr, Bt + (long long)nC * Wd + nC, Wd, nr, nr);
+    pinv_sym(RR, nr, scratch, scratch + nr * nr, cs, perm, red);
+    for (int idx = threadIdx.x; idx < nr * nC; idx += blockDim.x) {
+      int r = idx / nC, c = idx - r * nC;
+      double s = 0.0;
+      for (int q = 0; q < nr; ++q) s += scratch[r * nr + q] * Bt[(long long)c * Wd + nC + q];
+      RR[r * nC + c] = s;
+    }
+    __syncthreads();
+    blk::copy(Z, nC, RR, nC, nr, nC);
+  }
+  for (int idx = threadIdx.x; idx < nC * nC; idx += blockDim.x) {
+    int r = idx / nC, c = idx - r * nC;
+    double s = 0.0;
+    for (int q = 0; q < nr; ++q) s += Bt[(long long)r * Wd + nC + q] * Z[q * nC + c];
+    Btt[idx] = Bt[(long long)r * Wd + c] - s;
+  }
+  __syncthreads();
+  blk::symmetrize(Btt, nC, nC);
+  // pencil (M, Btt)
+  double* vals = o.eig + o.eig_off[g];
+  double* vecs = T1;
+  int* degen = reinterpret_cast<int*>(T2);
+  double* rows = T2 + nC;
+  int st = pencil(M, Btt, nC, vals, vecs, degen, scratch, cs, perm, red);
+  if (st) {
+    if (threadIdx.x == 0) o.status[g] = 200 + st;
+    return;
+  }
+  __shared__ int s_nsel;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int j = 0; j < nC; ++j) {
+      const bool sel = (vals[j] >= theta) && !degen[j];
+      perm[j] = sel ? c : -1;
+      c += sel;
+    }
+    s_nsel = c;
+  }
+  __syncthreads();
+  const int nsel = s_nsel;
+  for (int idx = threadIdx.x; idx < nC * nC; idx += blockDim.x) {
+    int j = idx / nC, c = idx - j * nC;
+    if (perm[j] < 0) continue;
+    double s = 0.0;
+    for (int k = 0; k < nC; ++k) s += M[c * nC + k] * vecs[k * nC + j];
+    rows[perm[j] * nC + c] = s;
+  }
+  __syncthreads();
+  // reshape (nsel x nC) row-major -> (nsel*(ns-1)) x ne and reduce
+  const int r = row_space_basis(rows, ne, nsel * (ns - 1), ne, o.Q + o.q_off[g], scratch, cs,
+                                perm, red);
+  if (threadIdx.x == 0) {
+    o.n_sel[g] = nsel;
+    o.r[g] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// old (coupled) edge eigenproblem (adaptive.py:75-91)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) edge_old_kernel(GlobTables t, const double* __restrict__ D,
+                                                       double theta, GlobOut o,
+                                                       double* __restrict__ ws,
+                                                       const long long* __restrict__ ws_off,
+                                                       const int* __restrict__ edge_ids) {
+  extern __shared__ double sh[];
+  const int g = edge_ids[blockIdx.x];
+  const int n = t.size[g];
+  const int nn = n * n;
+  const int k0 = t.sh_start[g], ns = t.sh_start[g + 1] - k0;
+  double* cs = sh;
+  double* red = cs + 2 * (n + 2);
+  double* rowbuf = red + 32;
+  int* perm = reinterpret_cast<int*>(rowbuf + 2 * (n + 2));
+  double* W = ws + ws_off[g];
+  double* BE = W;
+  double* acc = BE + nn;
+  double* nxt = acc + nn;
+  double* Sb = nxt + nn;
+  double* T = Sb + nn;
+  double* vecs = T + nn;
+  double* rows = vecs + nn;
+  int* degen = reinterpret_cast<int*>(rows + nn);
+  double* scratch = rows + nn + n;
+  blk::fill(BE, n, n, n, 0.0);
+  for (int i = 0; i < ns; ++i) {
+    const int sub = t.sh_sub[k0 + i], bo = t.sh_boff[k0 + i], nb = t.nB[sub];
+    const double* Bi = t.Bsym + t.soff[sub] + (long long)bo * nb + bo;
+    for (int k = 0; k < ns; ++k) {
+      if (k == i) continue;
+      const double* Dk = D + t.sh_doff[k0 + k];
+      blk::gemm(T, n, Bi, nb, false, Dk, n, false, n, n, n, 1.0, 0.0);
+      blk::gemm(BE, n, Dk, n, true, T, n, false, n, n, n, 1.0, 1.0);
+    }
+  }
+  blk::symmetrize(BE, n, n);
+  int st = glob_schur(t, k0, n, acc, rowbuf);
+  int bad = 0;
+  for (int i = 1; i < ns && !st; ++i) {
+    st = glob_schur(t, k0 + i, n, Sb, rowbuf);
+    if (st) { bad = i; break; }
+    parallel_sum(acc, Sb, n, nxt, scratch, cs, perm, red);
+    blk::copy(acc, n, nxt, n, n, n);
+  }
+  if (st) {
+    if (threadIdx.x == 0) o.status[g] = 100 + bad;
+    return;
+  }
+  double* vals = o.eig + o.eig_off[g];
+  st = pencil(BE, acc, n, vals, vecs, degen, scratch, cs, perm, red);
+  if (st) {
+    if (threadIdx.x == 0) o.status[g] = 200 + st;
+    return;
+  }
+  __shared__ int s_nsel;
+  if (threadIdx.x == 0) {
+    int c = 0;
+    for (int j = 0; j < n; ++j) {
+      const bool sel = (vals[j] >= theta) && !degen[j];
+      perm[j] = sel ? c : -1;
+      c += sel;
+    }
+    s_nsel = c;
+  }
+  __syncthreads();
+  const int nsel = s_nsel;
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
+    int j = idx / n, c = idx - j * n;
+    if (perm[j] < 0) continue;
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s += BE[c * n + k] * vecs[k * n + j];
+    rows[perm[j] * n + c] = s;
+  }
+  __syncthreads();
+  const int r = row_space_basis(rows, n, nsel, n, o.Q + o.q_off[g], scratch, cs, perm, red);
+  if (threadIdx.x == 0) {
+    o.n_sel[g] = nsel;
+    o.r[g] = r;
+  }
+}
+
+}  // namespace bddc
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace bddc;
+
+static int glob_launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+static GlobTables make_tables(const int* kind, const int* size, const int* sh_start,
+                              const int* sh_sub, const int* sh_boff, const long long* sh_doff,
+                              const int* nB, const long long* soff, const double* Bsym,
+                              const double* Binv) {
+  GlobTables t;
+  t.kind = kind; t.size = size; t.sh_start = sh_start; t.sh_sub = sh_sub; t.sh_boff = sh_boff;
+  t.sh_doff = sh_doff; t.nB = nB; t.soff = soff; t.Bsym = Bsym; t.Binv = Binv;
+  return t;
+}
+
+static int shmem_for(int dim) {
+  int bytes = (2 * (dim + 2) + 32 + 2 * (dim + 2)) * 8 + 2 * (dim + 2) * 4 + 64;
+  return bytes;
+}
+
+extern "C" {
+
+long long bddc_ws_face(long long n) { return bddc_face_ws(n); }
+long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long nhmax) {
+  return bddc_edge_new_ws(ns, ne, wd, nhmax);
+}
+
+int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
+                const int* sh_boff, const long long* sh_doff, const int* nB,
+                const long long* soff, const double* Bsym, double* D, double* ws,
+                const long long* ws_off, int* status, int n_globs, cudaStream_t stream) {
+  if (n_globs <= 0) return 0;
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, nullptr);
+  deluxe_kernel<<<n_globs, 256, 0, stream>>>(t, D, ws, ws_off, status);
+  return glob_launch_status();
+}
+
+int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
+                   const int* sh_boff, const long long* sh_doff, const int* nB,
+                   const long long* soff, const double* Bsym, const double* Binv, const double* D,
+                   double theta, double* eig, const long long* eig_off, int* n_sel, int* r,
+                   double* Q, const long long* q_off, int* status, double* ws,
+                   const long long* ws_off, const int* face_ids, int n_faces, int max_n,
+                   cudaStream_t stream) {
+  if (n_faces <= 0) return 0;
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, Binv);
+  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
+  const int smem = shmem_for(max_n);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(face_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  face_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids);
+  return glob_launch_status();
+}
+
+int bddc_priors(const int* kind, const int* size, const int* nB, const long long* soff,
+                const double* Binv, const int* sub_glob_start, const int* sub_globs,
+                const int* sub_glob_boff, const int* r, const double* Q, const long long* q_off,
+                const long long* pb_off, const int* nH, double* PB, double* XHH,
+                const long long* xhh_off, int n_sub, cudaStream_t stream) {
+  if (n_sub <= 0) return 0;
+  GlobTables t = make_tables(kind, size, nullptr, nullptr, nullptr, nullptr, nB, soff, nullptr, Binv);
+  priors_kernel<<<n_sub, 256, 0, stream>>>(t, sub_glob_start, sub_globs, sub_glob_boff, r, Q,
+                                           q_off, pb_off, nH, PB, XHH, xhh_off);
+  return glob_launch_status();
+}
+
+int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
+                       const int* sh_boff, const long long* sh_doff, const int* nB,
+                       const long long* soff, const double* Bsym, const double* Binv,
+                       const double* D, const long long* pb_off, const int* nH, const double* PB,
+                       const double* XHH, const long long* xhh_off, double theta, double* eig,
+                       const long long* eig_off, int* n_sel, int* r, double* Q,
+                       const long long* q_off, int* status, double* ws, const long long* ws_off,
+                       const int* edge_ids, int n_edges, int max_dim, cudaStream_t stream) {
+  if (n_edges <= 0) return 0;
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, Binv);
+  PriorTables pr{pb_off, nH, PB, XHH, xhh_off};
+  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
+  const int smem = shmem_for(max_dim);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(edge_new_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  edge_new_kernel<<<n_edges, 256, smem, stream>>>(t, D, pr, theta, o, ws, ws_off, edge_ids);
+  return glob_launch_status();
+}
+
+int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
+                       const int* sh_boff, const long long* sh_doff, const int* nB,
+                       const long long* soff, const double* Bsym, const double* Binv,
+                       const double* D, double theta, double* eig, const long long* eig_off,
+                       int* n_sel, int* r, double* Q, const long long* q_off, int* status,
+                       double* ws, const long long* ws_off, const int* edge_ids, int n_edges,
+                       int max_n, cudaStream_t stream) {
+  if (n_edges <= 0) return 0;
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, Binv);
+  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
+  const int smem = shmem_for(max_n);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(edge_old_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  edge_old_kernel<<<n_edges, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, edge_ids);
+  return glob_launch_status();
+}
+
+}  // extern "C"

@@ -1,0 +1,400 @@
+// Per-subdomain dense kernels: local assembly, blocked Schur elimination
+// (partial LU without pivoting -> S, g), blocked Gauss-Jordan inversion
+// (Bsym^-1, dual blocks), extraction and interior recovery.
+//
+// Reference call sites replaced (see include/bddc_b200.h for the C-ABI):
+//   substructuring.py:98-127   local assembly, lifting, splu(A_II), S and g
+//   substructuring.py:64-75    cho_factor/cho_solve(Bsym, I)
+//   solver.py:318-326          recover_interior (lu_II.solve)
+//
+// Layout: batch of row-major matrices in one device buffer; matrix b starts
+// at base + off[b] with leading dimension ld[b] (variable sizes, "vbatched").
+#include "common.cuh"
+#include "tile_mma.cuh"
+
+namespace bddc {
+
+// ---------------------------------------------------------------------------
+// local assembly: element 4x4 blocks -> dense [I | B] x [I | B | f] matrix
+// ---------------------------------------------------------------------------
+__global__ void assemble_kernel(double* __restrict__ base, const long long* __restrict__ off,
+                                const int* __restrict__ ld, const int* __restrict__ nloc,
+                                const long long* __restrict__ elem_start,
+                                const long long* __restrict__ elem_ids,
+                                const int* __restrict__ loc4, const long long* __restrict__ conn,
+                                const double* __restrict__ Ke, const double* __restrict__ Fe,
+                                const double* __restrict__ gdir) {
+  const int b = blockIdx.y;
+  const long long e0 = elem_start[b], e1 = elem_start[b + 1];
+  const long long j = e0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= e1) return;
+  const long long e = elem_ids[j];
+  const int nL = nloc[b];
+  const int L = ld[b];
+  double* M = base + off[b];
+  int li[4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) li[a] = loc4[j * 4 + a];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int r = li[a];
+    if (r >= nL) continue;
+    double fr = Fe[e * 4 + a];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double v = Ke[e * 16 + a * 4 + c];
+      if (li[c] < nL)
+        atomicAdd(M + (long long)r * L + li[c], v);
+      else
+        fr -= v * gdir[conn[e * 4 + c]];
+    }
+    atomicAdd(M + (long long)r * L + nL, fr);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// pivot block inverse (w x w, w <= 64) by scalar Gauss-Jordan in shared memory
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) pivot_inverse_kernel(
+    const double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ npiv, int k, double* __restrict__ pinv, long long pinv_stride,
+    int* __restrict__ status, int require_positive, double* __restrict__ piv_out,
+    long long piv_stride) {
+  __shared__ double P[kTile][kTile + 1];
+  __shared__ double prow[kTile];
+  __shared__ double pcol[kTile];
+  __shared__ int bad;
+  const int b = blockIdx.x;
+  const int w = min(kTile, npiv[b] - k);
+  if (w <= 0) return;
+  const double* M = base + off[b] + (long long)k * ld[b] + k;
+  const int L = ld[b];
+  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+    int r = idx / w, c = idx - r * w;
+    P[r][c] = M[(long long)r * L + c];
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int p = 0; p < w; ++p) {
+    const double piv = P[p][p];
+    if (piv_out && threadIdx.x == 0) piv_out[(long long)b * piv_stride + k + p] = piv;
+    if (threadIdx.x == 0) {
+      if (!(piv == piv) || piv == 0.0 || isinf(piv) || (require_positive && !(piv > 0.0))) bad = 1;
+    }
+    const double ip = 1.0 / piv;
+    for (int c = threadIdx.x; c < w; c += blockDim.x) {
+      prow[c] = (c == p) ? ip : P[p][c] * ip;
+      pcol[c] = P[c][p];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+      int r = idx / w, c = idx - r * w;
+      if (r == p) {
+        P[r][c] = prow[c];
+      } else {
+        const double f = pcol[r];
+        P[r][c] = (c == p) ? -f * ip : P[r][c] - f * prow[c];
+      }
+    }
+    __syncthreads();
+  }
+  double* out = pinv + (long long)b * pinv_stride;
+  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+    int r = idx / w, c = idx - r * w;
+    out[r * kTile + c] = P[r][c];
+  }
+  if (threadIdx.x == 0 && bad && status) atomicCAS(status + b, 0,
+      require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
+}
+
+// ---------------------------------------------------------------------------
+// Schur elimination (LU-style, rows below only):
+//   W = A11^-1 A12 stored over A12;   A22 -= A21 W
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTileThreads) schur_row_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ npiv, const int* __restrict__ ncols, int k,
+    const double* __restrict__ pinv, long long pinv_stride) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  const int w = min(kTile, npiv[b] - k);
+  if (w <= 0) return;
+  const int c0 = k + w + blockIdx.x * kTile;
+  if (c0 >= ncols[b]) return;
+  const int L = ld[b];
+  double* C = base + off[b] + (long long)k * L + c0;
+  tile_mma(C, L, w, min(kTile, ncols[b] - c0), pinv + (long long)b * pinv_stride, kTile, C, L, w,
+           1.0, 0.0, sm);
+}
+
+__global__ void __launch_bounds__(kTileThreads) schur_trailing_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ npiv, const int* __restrict__ nrows, const int* __restrict__ ncols,
+    int k) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  const int w = min(kTile, npiv[b] - k);
+  if (w <= 0) return;
+  const int s = k + w;
+  const int tn_count = (ncols[b] - s + kTile - 1) / kTile;
+  if (tn_count <= 0) return;
+  const int tm = blockIdx.x / tn_count, tn = blockIdx.x - tm * tn_count;
+  const int r0 = s + tm * kTile, c0 = s + tn * kTile;
+  if (r0 >= nrows[b]) return;
+  const int L = ld[b];
+  double* M = base + off[b];
+  tile_mma(M + (long long)r0 * L + c0, L, min(kTile, nrows[b] - r0), min(kTile, ncols[b] - c0),
+           M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm);
+}
+
+// ---------------------------------------------------------------------------
+// blocked Gauss-Jordan inversion in place (square n x n, no pivoting)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTileThreads) gj_row_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ n, int k, const double* __restrict__ pinv, long long pinv_stride) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  const int w = min(kTile, n[b] - k);
+  if (w <= 0) return;
+  const int c0 = blockIdx.x * kTile;
+  if (c0 >= n[b] || c0 == k) return;  // pivot column tile is written by gj_col
+  const int L = ld[b];
+  double* C = base + off[b] + (long long)k * L + c0;
+  tile_mma(C, L, w, min(kTile, n[b] - c0), pinv + (long long)b * pinv_stride, kTile, C, L, w, 1.0,
+           0.0, sm);
+}
+
+__global__ void __launch_bounds__(kTileThreads) gj_update_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ n, int k) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  const int nb = n[b];
+  const int w = min(kTile, nb - k);
+  if (w <= 0) return;
+  const int T = (nb + kTile - 1) / kTile;
+  const int tm = blockIdx.x / T, tn = blockIdx.x - tm * T;
+  if (tm >= T) return;
+  const int r0 = tm * kTile, c0 = tn * kTile;
+  if (r0 == k || c0 == k) return;
+  const int L = ld[b];
+  double* M = base + off[b];
+  tile_mma(M + (long long)r0 * L + c0, L, min(kTile, nb - r0), min(kTile, nb - c0),
+           M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm);
+}
+
+__global__ void __launch_bounds__(kTileThreads) gj_col_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ n, int k, const double* __restrict__ pinv, long long pinv_stride) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  const int nb = n[b];
+  const int w = min(kTile, nb - k);
+  if (w <= 0) return;
+  const int r0 = blockIdx.x * kTile;
+  if (r0 >= nb) return;
+  const int L = ld[b];
+  double* M = base + off[b];
+  const double* P = pinv + (long long)b * pinv_stride;
+  if (r0 == k) {  // pivot block <- P
+    for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+      int r = idx / w, c = idx - r * w;
+      M[(long long)(k + r) * L + k + c] = P[r * kTile + c];
+    }
+    return;
+  }
+  double* C = M + (long long)r0 * L + k;
+  tile_mma(C, L, min(kTile, nb - r0), w, C, L, P, kTile, w, -1.0, 0.0, sm);
+}
+
+// ---------------------------------------------------------------------------
+// extraction and small elementwise kernels
+// ---------------------------------------------------------------------------
+// S = M[nI:nL, nI:nL] -> S (ld nB), g = M[nI:nL, nL], Bsym = (S + S^T)/2
+__global__ void extract_schur_kernel(const double* __restrict__ base, const long long* __restrict__ off,
+                                     const int* __restrict__ ld, const int* __restrict__ nI,
+                                     const int* __restrict__ nB, const long long* __restrict__ soff,
+                                     const long long* __restrict__ voff, double* __restrict__ S,
+                                     double* __restrict__ Bsym, double* __restrict__ g) {
+  const int b = blockIdx.y;
+  const int n = nB[b], i0 = nI[b], L = ld[b];
+  const double* M = base + off[b] + (long long)i0 * L + i0;
+  double* Sb = S + soff[b];
+  double* Bb = Bsym + soff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
+    const double v = M[(long long)r * L + c];
+    Sb[idx] = v;
+    Bb[idx] = 0.5 * (v + M[(long long)c * L + r]);
+    if (c == 0) g[voff[b] + r] = M[(long long)r * L + n];
+  }
+}
+
+// X <- (X + X^T)/2 for square batched matrices (ld = n)
+__global__ void symmetrize_kernel(double* __restrict__ X, const long long* __restrict__ soff,
+                                  const int* __restrict__ nB) {
+  const int b = blockIdx.y;
+  const int n = nB[b];
+  double* M = X + soff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
+    if (c > r) {
+      const double v = 0.5 * (M[(long long)r * n + c] + M[(long long)c * n + r]);
+      M[(long long)r * n + c] = v;
+      M[(long long)c * n + r] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// interior recovery by block back-substitution over the stored W rows:
+//   u_I[k:k+w] = Wf_k - W_k,(k+w:nL) u[k+w:nL]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) recover_kernel(
+    const double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ nI, const int* __restrict__ nB, const long long* __restrict__ voff,
+    const int* __restrict__ iface_perm, const long long* __restrict__ ioff,
+    const long long* __restrict__ interior_nodes, const double* __restrict__ u_hat,
+    double* __restrict__ u) {
+  extern __shared__ double us[];  // nI + nB
+  const int b = blockIdx.x;
+  const int ni = nI[b], nb = nB[b], L = ld[b], nl = ni + nb;
+  const double* M = base + off[b];
+  for (int j = threadIdx.x; j < nb; j += blockDim.x) us[ni + j] = u_hat[iface_perm[voff[b] + j]];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int last = ((ni - 1) / kTile) * kTile;
+  for (int k = last; k >= 0; k -= kTile) {
+    const int w = min(kTile, ni - k);
+    for (int r = k + warp; r < k + w; r += nw) {
+      const double* row = M + (long long)r * L;
+      double s = 0.0;
+      for (int c = k + w + lane; c < nl; c += 32) s += row[c] * us[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) us[r] = row[nl] - s;
+    }
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < ni; j += blockDim.x) u[interior_nodes[ioff[b] + j]] = us[j];
+}
+
+}  // namespace bddc
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace bddc;
+
+static int smem_tile_setup() {
+  static bool done = false;
+  if (!done) {
+    int bytes = (int)sizeof(TileSmem);
+    cudaFuncSetAttribute(schur_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(schur_trailing_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(gj_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(gj_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done = true;
+  }
+  return (int)sizeof(TileSmem);
+}
+
+static int launch_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+extern "C" {
+
+int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
+                        const long long* elem_start, const long long* elem_ids, const int* loc4,
+                        const long long* conn, const double* Ke, const double* Fe,
+                        const double* gdir, int nbatch, long long max_elems, cudaStream_t stream) {
+  if (nbatch <= 0 || max_elems <= 0) return 0;
+  dim3 grid(ceil_div(max_elems, 128), nbatch);
+  assemble_kernel<<<grid, 128, 0, stream>>>(K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke,
+                                             Fe, gdir);
+  return launch_status();
+}
+
+int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const int* npiv,
+                         const int* nrows, const int* ncols, int nbatch, int max_npiv,
+                         int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
+                         long long pinv_step_stride, int* status, int require_positive,
+                         double* piv_out, long long piv_stride, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = smem_tile_setup();
+  for (int k = 0; k < max_npiv; k += kTile) {
+    double* P = pinv_ws + (long long)(k / kTile) * pinv_step_stride;
+    pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, k, P, pinv_stride, status,
+                                                     require_positive, piv_out, piv_stride);
+    const int ct = ceil_div(max_cols - k, kTile);
+    const int rt = ceil_div(max_rows - k, kTile);
+    if (ct > 0)
+      schur_row_kernel<<<dim3(ct, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
+                                                                        P, pinv_stride);
+    if (ct > 0 && rt > 0)
+      schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, smem, stream>>>(
+          M, off, ld, npiv, nrows, ncols, k);
+  }
+  return launch_status();
+}
+
+int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n, int nbatch,
+                    int max_n, double* pinv_ws, long long pinv_stride, int* status,
+                    int require_positive, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = smem_tile_setup();
+  const int T = ceil_div(max_n, kTile);
+  for (int k = 0; k < max_n; k += kTile) {
+    pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, pinv_ws, pinv_stride,
+                                                     status, require_positive, nullptr, 0);
+    gj_row_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
+                                                                  pinv_stride);
+    gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k);
+    gj_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
+                                                                  pinv_stride);
+  }
+  return launch_status();
+}
+
+int bddc_extract_schur(const double* M, const long long* off, const int* ld, const int* nI,
+                       const int* nB, const long long* soff, const long long* voff, double* S,
+                       double* Bsym, double* g, int nbatch, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  extract_schur_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(M, off, ld, nI, nB, soff, voff, S,
+                                                             Bsym, g);
+  return launch_status();
+}
+
+int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
+                    cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  symmetrize_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(X, soff, n);
+  return launch_status();
+}
+
+int bddc_recover_interior(const double* M, const long long* off, const int* ld, const int* nI,
+                          const int* nB, const long long* voff, const int* iface_perm,
+                          const long long* ioff, const long long* interior_nodes,
+                          const double* u_hat, double* u, int nbatch, int max_nloc,
+                          cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = max_nloc * (int)sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(recover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  recover_kernel<<<nbatch, 256, smem, stream>>>(M, off, ld, nI, nB, voff, iface_perm, ioff,
+                                                interior_nodes, u_hat, u);
+  return launch_status();
+}
+
+}  // extern "C"

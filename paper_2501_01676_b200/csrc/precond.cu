@@ -1,0 +1,536 @@
+// BDDC preconditioner setup and apply, interface operator, coarse problem.
+//
+// Reference: solver.py:54-134 (setup), 138-209 (apply), 226-242 (S_hat, g_hat).
+//
+// Per subdomain i, in the glob-major local B order (each glob contiguous):
+//   T_i  = blockdiag_g(Q_g D_g^(i)T)                    (transformed deluxe)
+//   Sbar = Q_i S_i Q_i^T,  Z = (Sbar_dd)^-1 embedded (zero on primal rows/cols)
+//   A_i  = T_i^T Z T_i                    local part of M^-1   (nB x nB)
+//   G_i  = (E_P - E_P Sbar Z) T_i         coarse restriction   (n_p x nB)
+//   N_i  = T_i^T (E_P - Z Sbar E_P)       coarse prolongation  (stored n_p x nB)
+//   C_i  = Sbar_PP - Sbar_P: Z Sbar_:P    coarse contribution  (n_p x n_p)
+// so that M^-1 r = sum_i R_i^T (A_i R_i r + N_i u_P,i),
+//         u_P = C^-1 sum_i P_i^T G_i R_i r     (C = sum_i P_i^T C_i P_i).
+// This is algebraically the reference's Qhat^T Rtil^T Dtil Stil^-1 Dtil^T Rtil Qhat.
+#include "common.cuh"
+#include "tile_mma.cuh"
+
+namespace bddc {
+
+struct SubGlobMap {
+  const int* nB;
+  const long long* soff;      // nB x nB matrices
+  const long long* voff;      // nB vectors (prefix sum of nB)
+  const int* pos2k;           // per local B position: index into sub_globs
+  const int* sub_globs;       // glob id per (sub, k)
+  const int* sub_glob_boff;   // block offset per (sub, k)
+  const int* sub_glob_sh;     // sharer slot (into sh_* of the glob) per (sub, k)
+  const int* gsize;           // per glob size
+  const double* Q;            // per glob Q (n_g x n_g)
+  const long long* q_off;
+  const double* D;            // per (glob, sharer) D
+  const long long* sh_doff;
+};
+
+// X = op(Qi) S op(Qi)^T style block transforms ------------------------------
+// out[r][c] = sum_q L_blk(r)[r', q] * in[blk0(r) + q][c]      (left multiply)
+//   mode 0: L = Q_g           mode 1: L = (Q_g D_g^T)^T = D_g Q_g^T
+// Right multiplies are done as (left multiply on the transpose) by the caller
+// through the `trans_in` / `trans_out` flags.
+__device__ __forceinline__ double left_block_value(const SubGlobMap& m, int sub, int r, int q,
+                                                   int mode) {
+  const int k = m.pos2k[m.voff[sub] + r];
+  const int g = m.sub_globs[k];
+  const int bo = m.sub_glob_boff[k];
+  const int ng = m.gsize[g];
+  const int rr = r - bo;
+  const double* Qg = m.Q + m.q_off[g];
+  if (mode == 0) return Qg[rr * ng + q];
+  // T^T[rr][q] = (Q D^T)^T[rr][q] = (D Q^T)[rr][q] = sum_a D[rr][a] Q[q][a]
+  const double* Dg = m.D + m.sh_doff[m.sub_glob_sh[k]];
+  double s = 0.0;
+  for (int a = 0; a < ng; ++a) s += Dg[rr * ng + a] * Qg[q * ng + a];
+  return s;
+}
+
+// out = L * in (in/out nB x nB, ld nB); if right: out = in * L^T.
+// L is block diagonal with blocks given by left_block_value(mode).
+__global__ void block_transform_kernel(SubGlobMap m, const double* __restrict__ in,
+                                       double* __restrict__ out, int mode, int right) {
+  const int b = blockIdx.y;
+  const int n = m.nB[b];
+  const double* X = in + m.soff[b];
+  double* Y = out + m.soff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
+    const int pivot = right ? c : r;
+    const int k = m.pos2k[m.voff[b] + pivot];
+    const int bo = m.sub_glob_boff[k];
+    const int ng = m.gsize[m.sub_globs[k]];
+    double s = 0.0;
+    for (int q = 0; q < ng; ++q) {
+      const double l = left_block_value(m, b, pivot, q, mode);
+      s += right ? X[(long long)r * n + bo + q] * l : l * X[(long long)(bo + q) * n + c];
+    }
+    Y[idx] = s;
+  }
+}
+
+// precompute TT blocks: TTb[(g,s)] = D_g^(s) Q_g^T  (so T^T blocks), per sharer slot
+__global__ void ttblock_kernel(const int* __restrict__ slot_glob, const int* __restrict__ gsize,
+                               const double* __restrict__ Q, const long long* __restrict__ q_off,
+                               const double* __restrict__ D, const long long* __restrict__ sh_doff,
+                               double* __restrict__ TT, int n_slots) {
+  const int s = blockIdx.x;
+  if (s >= n_slots) return;
+  const int g = slot_glob[s];
+  const int n = gsize[g];
+  const double* Qg = Q + q_off[g];
+  const double* Dg = D + sh_doff[s];
+  double* O = TT + sh_doff[s];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    int r = idx / n, c = idx - r * n;
+    double v = 0.0;
+    for (int a = 0; a < n; ++a) v += Dg[r * n + a] * Qg[c * n + a];
+    O[idx] = v;
+  }
+}
+
+// out = TT_blockdiag * in  (left) or in * TT_blockdiag^T (right), TT from ttblock_kernel
+__global__ void tt_transform_kernel(SubGlobMap m, const double* __restrict__ TT,
+                                    const double* __restrict__ in, double* __restrict__ out,
+                                    int right, int transpose_block) {
+  const int b = blockIdx.y;
+  const int n = m.nB[b];
+  const double* X = in + m.soff[b];
+  double* Y = out + m.soff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
+    const int pivot = right ? c : r;
+    const int k = m.pos2k[m.voff[b] + pivot];
+    const int bo = m.sub_glob_boff[k];
+    const int ng = m.gsize[m.sub_globs[k]];
+    const double* Tb = TT + m.sh_doff[m.sub_glob_sh[k]];
+    const int pr = pivot - bo;
+    double s = 0.0;
+    for (int q = 0; q < ng; ++q) {
+      const double l = transpose_block ? Tb[q * ng + pr] : Tb[pr * ng + q];
+      s += right ? X[(long long)r * n + bo + q] * l : l * X[(long long)(bo + q) * n + c];
+    }
+    Y[idx] = s;
+  }
+}
+
+// Zin <- Sbar with primal rows/cols replaced by identity; Csym <- sym(Zin)
+__global__ void dual_embed_kernel(const int* __restrict__ nB, const long long* __restrict__ soff,
+                                  const long long* __restrict__ voff,
+                                  const unsigned char* __restrict__ primal_mask,
+                                  const double* __restrict__ Sbar, double* __restrict__ Zin,
+                                  double* __restrict__ Csym) {
+  const int b = blockIdx.y;
+  const int n = nB[b];
+  const unsigned char* pm = primal_mask + voff[b];
+  const double* S = Sbar + soff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
+    double v, vs;
+    if (pm[r] || pm[c]) {
+      v = vs = (r == c) ? 1.0 : 0.0;
+    } else {
+      v = S[idx];
+      vs = 0.5 * (v + S[(long long)c * n + r]);
+    }
+    Zin[soff[b] + idx] = v;
+    if (Csym) Csym[soff[b] + idx] = vs;
+  }
+}
+
+__global__ void zero_primal_kernel(const int* __restrict__ nB, const long long* __restrict__ soff,
+                                   const long long* __restrict__ voff,
+                                   const unsigned char* __restrict__ primal_mask,
+                                   double* __restrict__ Z) {
+  const int b = blockIdx.y;
+  const int n = nB[b];
+  const unsigned char* pm = primal_mask + voff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
+    if (pm[r] || pm[c]) Z[soff[b] + idx] = 0.0;
+  }
+}
+
+// Per subdomain primal pieces (one CTA per subdomain):
+//   ZS[:, p]  = Z Sbar[:, p]             -> MP[p][:] = e_p - ZS[:, p]   (n_p x nB, "column" form)
+//   SZ[p, :]  = Sbar[p, :] Z             -> RP[p][:] = e_p - SZ[p, :]
+//   C_i[p][q] = Sbar[p][q] - Sbar[p, :] ZS[:, q]
+__global__ void primal_pieces_kernel(const int* __restrict__ nB, const long long* __restrict__ soff,
+                                     const int* __restrict__ pstart, const int* __restrict__ ppos,
+                                     const long long* __restrict__ poff,
+                                     const double* __restrict__ Sbar, const double* __restrict__ Z,
+                                     double* __restrict__ MP, double* __restrict__ RP,
+                                     double* __restrict__ Cl, const long long* __restrict__ coff) {
+  const int b = blockIdx.x;
+  const int n = nB[b];
+  const int p0 = pstart[b], np = pstart[b + 1] - p0;
+  const double* S = Sbar + soff[b];
+  const double* Zb = Z + soff[b];
+  double* M = MP + poff[b];
+  double* R = RP + poff[b];
+  for (int idx = threadIdx.x; idx < np * n; idx += blockDim.x) {
+    const int p = idx / n, r = idx - p * n;
+    const int pc = ppos[p0 + p];
+    double s1 = 0.0, s2 = 0.0;
+    for (int k = 0; k < n; ++k) {
+      s1 += Zb[(long long)r * n + k] * S[(long long)k * n + pc];   // (Z Sbar)[r, pc]
+      s2 += S[(long long)pc * n + k] * Zb[(long long)k * n + r];   // (Sbar Z)[pc, r]
+    }
+    M[(long long)p * n + r] = (r == pc ? 1.0 : 0.0) - s1;
+    R[(long long)p * n + r] = (r == pc ? 1.0 : 0.0) - s2;
+  }
+  __syncthreads();
+  double* C = Cl + coff[b];
+  for (int idx = threadIdx.x; idx < np * np; idx += blockDim.x) {
+    const int p = idx / np, q = idx - p * np;
+    const int pr = ppos[p0 + p], qc = ppos[p0 + q];
+    // Sbar[pr, qc] - Sbar[pr, :] (Z Sbar)[:, qc] = Sbar[pr,:] (e_qc - ZS[:,qc]) = Sbar[pr,:] M[q,:]
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) s += S[(long long)pr * n + k] * M[(long long)q * n + k];
+    C[idx] = s;
+  }
+}
+
+// rows form: Out[p][c] = sum over block of c: In[p][bo+q] * TT-derived value
+//   G = RP T   where T = Q D^T blockdiag: G[p][c] = sum_q RP[p][bo+q] T[bo+q][c]
+//            T[bo+q][c] = TT^T block [q][c-bo]  = TTb[(c-bo)*ng + q]
+//   Nt = (T^T MP^T)^T = MP T : same form as G with In = MP
+__global__ void primal_rows_times_T_kernel(SubGlobMap m, const double* __restrict__ TT,
+                                           const int* __restrict__ pstart,
+                                           const long long* __restrict__ poff,
+                                           const double* __restrict__ In,
+                                           double* __restrict__ Out) {
+  const int b = blockIdx.y;
+  const int n = m.nB[b];
+  const int np = pstart[b + 1] - pstart[b];
+  const double* X = In + poff[b];
+  double* Y = Out + poff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)np * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int p = (int)(idx / n), c = (int)(idx - (long long)p * n);
+    const int k = m.pos2k[m.voff[b] + c];
+    const int bo = m.sub_glob_boff[k];
+    const int ng = m.gsize[m.sub_globs[k]];
+    const double* Tb = TT + m.sh_doff[m.sub_glob_sh[k]];
+    const int cc = c - bo;
+    double s = 0.0;
+    for (int q = 0; q < ng; ++q) s += X[(long long)p * n + bo + q] * Tb[cc * ng + q];
+    Y[idx] = s;
+  }
+}
+
+// coarse assembly C[gp][gq] += C_i[p][q]
+__global__ void coarse_scatter_kernel(const int* __restrict__ pstart, const int* __restrict__ pgid,
+                                      const double* __restrict__ Cl,
+                                      const long long* __restrict__ coff, double* __restrict__ C,
+                                      long long ldc) {
+  const int b = blockIdx.x;
+  const int p0 = pstart[b], np = pstart[b + 1] - p0;
+  const double* Cb = Cl + coff[b];
+  for (int idx = threadIdx.x; idx < np * np; idx += blockDim.x) {
+    const int p = idx / np, q = idx - p * np;
+    atomicAdd(C + (long long)pgid[p0 + p] * ldc + pgid[p0 + q], Cb[idx]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// batched GEMV families for the apply
+// ---------------------------------------------------------------------------
+// y_i = S_i x_i with x_i = u[perm_i]; y written to the local buffer (voff)
+// One CTA per (subdomain, row chunk); x staged in shared memory.
+template <bool ACCUM_PRIMAL>
+__global__ void __launch_bounds__(256) local_gemv_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ soff,
+    const long long* __restrict__ voff, const int* __restrict__ iface_perm,
+    const double* __restrict__ Mat, const double* __restrict__ u, double* __restrict__ y,
+    // primal restriction (only when ACCUM_PRIMAL): c = G x
+    const int* __restrict__ pstart, const long long* __restrict__ poff,
+    const double* __restrict__ G, double* __restrict__ cvals) {
+  extern __shared__ double xs[];
+  const int b = blockIdx.y;
+  const int n = nB[b];
+  const int chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * chunk;
+  const int* pm = iface_perm + voff[b];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) xs[j] = u[pm[j]];
+  __syncthreads();
+  const double* A = Mat + soff[b];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int r1 = min(n, r0 + chunk);
+  for (int r = r0 + warp; r < r1; r += nw) {
+    const double* row = A + (long long)r * n;
+    double s = 0.0;
+    for (int c = lane; c < n; c += 32) s += row[c] * xs[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) y[voff[b] + r] = s;
+  }
+  if (ACCUM_PRIMAL && blockIdx.x == 0) {
+    const int np = pstart[b + 1] - pstart[b];
+    const double* Gb = G + poff[b];
+    for (int p = warp; p < np; p += nw) {
+      const double* row = Gb + (long long)p * n;
+      double s = 0.0;
+      for (int c = lane; c < n; c += 32) s += row[c] * xs[c];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) cvals[pstart[b] + p] = s;
+    }
+  }
+}
+
+// y_i += sum_p Nt_i[p, :] * uP[pgid_i[p]]
+__global__ void prolong_primal_kernel(const int* __restrict__ nB, const long long* __restrict__ voff,
+                                      const int* __restrict__ pstart, const int* __restrict__ pgid,
+                                      const long long* __restrict__ poff,
+                                      const double* __restrict__ Nt, const double* __restrict__ uP,
+                                      double* __restrict__ y) {
+  const int b = blockIdx.y;
+  const int n = nB[b];
+  const int p0 = pstart[b], np = pstart[b + 1] - p0;
+  const double* Nb = Nt + poff[b];
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < np; ++p) s += Nb[(long long)p * n + r] * uP[pgid[p0 + p]];
+    y[voff[b] + r] += s;
+  }
+}
+
+// deterministic gather-reduce: out[t] = sum_{j in src(t)} y[src[j]]  (CSR, sorted by subdomain)
+__global__ void gather_reduce_kernel(const long long* __restrict__ tstart,
+                                     const long long* __restrict__ tsrc,
+                                     const double* __restrict__ y, double* __restrict__ out,
+                                     long long n) {
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (long long j = tstart[t]; j < tstart[t + 1]; ++j) s += y[tsrc[j]];
+    out[t] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// coarse triangular solves with the blocked no-pivot LU from schur_eliminate
+//   forward:  t_k = P_k b_k ; b_i -= A[i, k:k+w] t_k  (i >= k+w)
+//   backward: x_k = t_k     ; t_i -= A[i, k:k+w] x_k  (i < k)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) coarse_fwd_kernel(const double* __restrict__ A, long long ld,
+                                                         int n, int k,
+                                                         const double* __restrict__ Pk,
+                                                         double* __restrict__ b,
+                                                         double* __restrict__ t) {
+  __shared__ double tk[64];
+  const int w = min(64, n - k);
+  // every CTA recomputes t_k = P_k b_k (64 x 64)
+  for (int r = threadIdx.x; r < w; r += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < w; ++c) s += Pk[r * 64 + c] * b[k + c];
+    tk[r] = s;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int r = threadIdx.x; r < w; r += blockDim.x) t[k + r] = tk[r];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rows_per_cta = 64;
+  const int i0 = k + w + blockIdx.x * rows_per_cta;
+  for (int i = i0 + warp; i < min(n, i0 + rows_per_cta); i += 8) {
+    const double* row = A + (long long)i * ld + k;
+    double s = 0.0;
+    for (int c = lane; c < w; c += 32) s += row[c] * tk[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) b[i] -= s;
+  }
+}
+
+__global__ void __launch_bounds__(256) coarse_bwd_kernel(const double* __restrict__ A, long long ld,
+                                                         int n, int k, double* __restrict__ t) {
+  __shared__ double xk[64];
+  const int w = min(64, n - k);
+  for (int r = threadIdx.x; r < w; r += blockDim.x) xk[r] = t[k + r];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i0 = blockIdx.x * 64;
+  for (int i = i0 + warp; i < min(k, i0 + 64); i += 8) {
+    const double* row = A + (long long)i * ld + k;
+    double s = 0.0;
+    for (int c = lane; c < w; c += 32) s += row[c] * xk[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) t[i] -= s;
+  }
+}
+
+}  // namespace bddc
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace bddc;
+
+static int pc_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+static SubGlobMap make_map(const int* nB, const long long* soff, const long long* voff,
+                           const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+                           const int* sub_glob_sh, const int* gsize, const double* Q,
+                           const long long* q_off, const double* D, const long long* sh_doff) {
+  SubGlobMap m;
+  m.nB = nB; m.soff = soff; m.voff = voff; m.pos2k = pos2k; m.sub_globs = sub_globs;
+  m.sub_glob_boff = sub_glob_boff; m.sub_glob_sh = sub_glob_sh; m.gsize = gsize; m.Q = Q;
+  m.q_off = q_off; m.D = D; m.sh_doff = sh_doff;
+  return m;
+}
+
+extern "C" {
+
+// Sbar = Qi S Qi^T (via tmp)
+int bddc_pc_transform_schur(const int* nB, const long long* soff, const long long* voff,
+                            const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+                            const int* sub_glob_sh, const int* gsize, const double* Q,
+                            const long long* q_off, const double* S, double* tmp, double* Sbar,
+                            int nbatch, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  SubGlobMap m = make_map(nB, soff, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize, Q,
+                          q_off, nullptr, nullptr);
+  block_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, S, tmp, 0, 0);
+  block_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, tmp, Sbar, 0, 1);
+  return pc_status();
+}
+
+int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
+                     const long long* q_off, const double* D, const long long* sh_doff,
+                     double* TT, int n_slots, cudaStream_t stream) {
+  if (n_slots <= 0) return 0;
+  ttblock_kernel<<<n_slots, 128, 0, stream>>>(slot_glob, gsize, Q, q_off, D, sh_doff, TT, n_slots);
+  return pc_status();
+}
+
+int bddc_pc_dual_embed(const int* nB, const long long* soff, const long long* voff,
+                       const unsigned char* primal_mask, const double* Sbar, double* Zin,
+                       double* Csym, int nbatch, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  dual_embed_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(nB, soff, voff, primal_mask, Sbar, Zin,
+                                                          Csym);
+  return pc_status();
+}
+
+int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* voff,
+                        const unsigned char* primal_mask, double* Z, int nbatch,
+                        cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  zero_primal_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(nB, soff, voff, primal_mask, Z);
+  return pc_status();
+}
+
+// A = T^T Z T with T^T blocks TT: Y = Z * TT^T... see DESIGN.md
+int bddc_pc_local_operator(const int* nB, const long long* soff, const long long* voff,
+                           const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+                           const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
+                           const double* TT, const double* Z, double* tmp, double* A, int nbatch,
+                           cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  SubGlobMap m = make_map(nB, soff, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
+                          nullptr, nullptr, nullptr, sh_doff);
+  // T = blockdiag(Q D^T) = blockdiag(TT^T).  Y = Z T: right multiply by L^T with L = TT
+  //   (in * L^T)[r][c] = sum_q in[r][bo+q] * L[c'][q]  with L = TT (transpose_block = 0)
+  tt_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, TT, Z, tmp, 1, 0);
+  // A = T^T Y = TT Y: left multiply with L = TT
+  tt_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, TT, tmp, A, 0, 0);
+  return pc_status();
+}
+
+int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstart,
+                          const int* ppos, const long long* poff, const double* Sbar,
+                          const double* Z, double* MP, double* RP, double* Cl,
+                          const long long* coff, int nbatch, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  primal_pieces_kernel<<<nbatch, 256, 0, stream>>>(nB, soff, pstart, ppos, poff, Sbar, Z, MP, RP,
+                                                   Cl, coff);
+  return pc_status();
+}
+
+int bddc_pc_primal_rows_T(const int* nB, const long long* voff, const int* pos2k,
+                          const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,
+                          const int* gsize, const long long* sh_doff, const double* TT,
+                          const int* pstart, const long long* poff, const double* In, double* Out,
+                          int nbatch, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  SubGlobMap m = make_map(nB, nullptr, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
+                          nullptr, nullptr, nullptr, sh_doff);
+  primal_rows_times_T_kernel<<<dim3(16, nbatch), 256, 0, stream>>>(m, TT, pstart, poff, In, Out);
+  return pc_status();
+}
+
+int bddc_coarse_scatter(const int* pstart, const int* pgid, const double* Cl,
+                        const long long* coff, double* C, long long ldc, int nbatch,
+                        cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  coarse_scatter_kernel<<<nbatch, 128, 0, stream>>>(pstart, pgid, Cl, coff, C, ldc);
+  return pc_status();
+}
+
+int bddc_local_gemv(const int* nB, const long long* soff, const long long* voff,
+                    const int* iface_perm, const double* M, const double* u, double* y,
+                    const int* pstart, const long long* poff, const double* G, double* cvals,
+                    int nbatch, int max_nB, int row_chunks, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = max_nB * (int)sizeof(double);
+  if (G) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(local_gemv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    local_gemv_kernel<true><<<dim3(row_chunks, nbatch), 256, smem, stream>>>(
+        nB, soff, voff, iface_perm, M, u, y, pstart, poff, G, cvals);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(local_gemv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    local_gemv_kernel<false><<<dim3(row_chunks, nbatch), 256, smem, stream>>>(
+        nB, soff, voff, iface_perm, M, u, y, nullptr, nullptr, nullptr, nullptr);
+  }
+  return pc_status();
+}
+
+int bddc_prolong_primal(const int* nB, const long long* voff, const int* pstart, const int* pgid,
+                        const long long* poff, const double* Nt, const double* uP, double* y,
+                        int nbatch, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  prolong_primal_kernel<<<dim3(2, nbatch), 256, 0, stream>>>(nB, voff, pstart, pgid, poff, Nt, uP, y);
+  return pc_status();
+}
+
+int bddc_gather_reduce(const long long* tstart, const long long* tsrc, const double* y,
+                       double* out, long long n, cudaStream_t stream) {
+  if (n <= 0) return 0;
+  gather_reduce_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(tstart, tsrc, y, out, n);
+  return pc_status();
+}
+
+int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
+                      long long pinv_step_stride, double* b, double* t, cudaStream_t stream) {
+  if (n <= 0) return 0;
+  for (int k = 0; k < n; k += 64) {
+    const int w = min(64, n - k);
+    const int blocks = max(1, ceil_div(n - k - w, 64));
+    coarse_fwd_kernel<<<blocks, 256, 0, stream>>>(A, ld, n, k, pinv + (long long)(k / 64) * pinv_step_stride, b, t);
+  }
+  const int last = ((n - 1) / 64) * 64;
+  for (int k = last; k > 0; k -= 64) {
+    coarse_bwd_kernel<<<ceil_div(k, 64), 256, 0, stream>>>(A, ld, n, k, t);
+  }
+  return pc_status();
+}
+
+}  // extern "C"

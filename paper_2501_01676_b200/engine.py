@@ -1,0 +1,629 @@
+"""Device engine: batched subdomain setup, adaptive coarse space, BDDC
+preconditioner, interface operator and GMRES on one B200.
+
+Every floating-point operation of the hot path runs in the sm_100a kernels
+of ``_bddc_b200.so`` (include/bddc_b200.h); torch only owns device memory
+and the stream.  The host does integer planning (plan.py), status checks and
+GMRES's (j+2) x (j+1) least-squares recurrence, like the reference driver
+(solver.py:297).
+"""
+
+import math
+import time
+
+import numpy as np
+import scipy.linalg
+import torch
+
+from ._lib import lib, require_cuda, stream
+from .plan import Plan, _excl, _ranges
+
+F64 = torch.float64
+
+
+class NumericalError(RuntimeError):
+    """Raised when a factorization or eigensolve cannot be completed
+    (reference linalg.py:11)."""
+
+
+def dev_i32(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+
+
+def dev_i64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).cuda()
+
+
+def dev_f64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+class PhaseTimer:
+    """CUDA-event phase timer on the current stream (ms)."""
+
+    def __init__(self, enabled=True):
+        self.enabled = enabled
+        self.events = []
+
+    def mark(self, name):
+        if self.enabled:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.events.append((name, e))
+
+    def result(self):
+        if not self.events:
+            return {}
+        self.events[-1][1].synchronize()
+        out = {}
+        for (n0, e0), (_, e1) in zip(self.events[:-1], self.events[1:]):
+            out[n0] = out.get(n0, 0.0) + e0.elapsed_time(e1)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# subdomain operators
+# ---------------------------------------------------------------------------
+
+class LocalSystem:
+    """All subdomain operators of one partition, batched on the device.
+
+    Replaces build_subdomain_operator x N (reference substructuring.py:78-143)
+    and SubdomainOperator.bsym_inverse (substructuring.py:64-75)."""
+
+    def __init__(self, system, partition, globs, plan=None, inputs=None, timer=None):
+        require_cuda()
+        self.system, self.partition, self.globs = system, partition, globs
+        self.plan = plan or Plan(system, partition, globs)
+        self.plan.check()
+        p = self.plan
+        self.N = p.N
+        self.d = _DevicePlan(p)
+        if inputs is None:
+            inputs = upload_inputs(system)
+        self.inputs = inputs
+        self._Binv = None
+        self.timer = timer
+        self._factor()
+
+    def _factor(self):
+        p, d, st = self.plan, self.d, stream()
+        K = torch.zeros(p.K_total, dtype=F64, device="cuda")
+        lib.bddc_local_assemble(K, d.off, d.ld, d.nL, d.elem_start, d.elem_ids, d.loc4,
+                                self.inputs["conn"], self.inputs["Ke"], self.inputs["Fe"],
+                                self.inputs["gdir"], p.N, p.max_elems, st)
+        status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
+        pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
+        lib.bddc_schur_eliminate(K, d.off, d.ld, d.nI, d.nL, d.nL1, p.N, int(p.nI.max()),
+                                 int(p.nL.max()), int(p.nL.max()) + 1, pinv, 4096, 0, status, 0,
+                                 None, 0, st)
+        self.K = K
+        self.S = torch.empty(p.S_total, dtype=F64, device="cuda")
+        self.Bsym = torch.empty(p.S_total, dtype=F64, device="cuda")
+        self.g = torch.empty(int(p.voff[-1]), dtype=F64, device="cuda")
+        lib.bddc_extract_schur(K, d.off, d.ld, d.nI, d.nB, d.soff, d.voff, self.S, self.Bsym,
+                               self.g, p.N, st)
+        bad = _first_bad(status)
+        if bad is not None:
+            raise NumericalError(f"interior block of subdomain {bad} is singular")
+
+    def bsym_inverse(self):
+        """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check."""
+        if self._Binv is None:
+            p, d, st = self.plan, self.d, stream()
+            Binv = self.Bsym.clone()
+            status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
+            pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
+            lib.bddc_gj_inverse(Binv, d.soff, d.nB, d.nB, p.N, int(p.nB.max()), pinv, 4096, status,
+                                1, st)
+            lib.bddc_symmetrize(Binv, d.soff, d.nB, p.N, st)
+            bad = _first_bad(status)
+            if bad is not None:
+                B = self.matrix(self.Bsym, bad)
+                raise NumericalError(f"Bsym of subdomain {bad} is not positive definite "
+                                     f"(cond ~ {np.linalg.cond(B):.2e})")
+            self._Binv = Binv
+        return self._Binv
+
+    # host views (glob-major order) ------------------------------------------
+    def matrix(self, buf, i):
+        p = self.plan
+        n = int(p.nB[i])
+        o = int(p.soff[i])
+        return buf[o:o + n * n].view(n, n).cpu().numpy()
+
+    def vector(self, buf, i):
+        p = self.plan
+        return buf[int(p.voff[i]):int(p.voff[i + 1])].cpu().numpy()
+
+
+def _first_bad(status):
+    s = status.cpu().numpy()
+    nz = np.flatnonzero(s)
+    return int(nz[0]) if nz.size else None
+
+
+class _DevicePlan:
+    def __init__(self, p):
+        self.off = dev_i64(p.off)
+        self.ld = dev_i32(p.ld)
+        self.nI = dev_i32(p.nI)
+        self.nB = dev_i32(p.nB)
+        self.nL = dev_i32(p.nL)
+        self.nL1 = dev_i32(p.nL + 1)
+        self.soff = dev_i64(p.soff)
+        self.voff = dev_i64(p.voff)
+        self.ioff = dev_i64(p.ioff)
+        self.elem_start = dev_i64(p.elem_start)
+        self.elem_ids = dev_i64(p.elem_ids)
+        self.loc4 = dev_i32(p.loc4)
+        self.iface_perm = dev_i32(p.iface_perm)
+        self.I_nodes = dev_i64(p.I_nodes)
+        self.tstart = dev_i64(p.tstart)
+        self.tsrc = dev_i64(p.tsrc)
+        self.pos2k = dev_i32(p.pos2k)
+        self.sub_globs = dev_i32(p.sub_globs)
+        self.sub_glob_boff = dev_i32(p.sub_glob_boff)
+        self.sub_glob_sh = dev_i32(p.sub_glob_sh)
+        self.sub_glob_start = dev_i32(p.sub_glob_start)
+        self.kind = dev_i32(p.kind)
+        self.gsize = dev_i32(p.gsize)
+        self.sh_start = dev_i32(p.sh_start)
+        self.sh_sub = dev_i32(p.sh_sub)
+        self.sh_boff = dev_i32(p.sh_boff)
+        self.sh_doff = dev_i64(p.sh_doff)
+        self.slot_glob = dev_i32(p.slot_glob)
+
+
+def upload_inputs(system, pinned=False):
+    """Element blocks, connectivity and Dirichlet data to the device."""
+    def up(a, dt):
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
+        if pinned:
+            t = t.pin_memory()
+        return t.cuda(non_blocking=pinned)
+    return {
+        "Ke": up(system.elem_matrices.reshape(-1, 16), np.float64),
+        "Fe": up(system.elem_rhs.reshape(-1, 4), np.float64),
+        "conn": up(system.mesh.elements, np.int64),
+        "gdir": up(system.dirichlet_values, np.float64),
+    }
+
+
+# ---------------------------------------------------------------------------
+# deluxe scaling
+# ---------------------------------------------------------------------------
+
+class DeviceScaling:
+    """Deluxe families per glob (reference scaling.py:47-57)."""
+
+    def __init__(self, ls):
+        p, d = ls.plan, ls.d
+        self.ls = ls
+        self.D = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
+        ws_off = _excl(p.gsize.astype(np.int64) ** 2)
+        ws = torch.empty(max(int(ws_off[-1]), 1), dtype=F64, device="cuda")
+        status = torch.zeros(max(p.G, 1), dtype=torch.int32, device="cuda")
+        lib.bddc_deluxe(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, d.nB, d.soff,
+                        ls.Bsym, self.D, ws, dev_i64(ws_off[:-1]), status, p.G, stream())
+        bad = _first_bad(status)
+        if bad is not None:
+            raise NumericalError("deluxe block sum is singular "
+                                 f"(glob {ls.globs.glob_id(ls.globs.globs[bad])})")
+
+    def family(self, k):
+        """{sharer: D (n_g x n_g)} of glob index k, glob-node order."""
+        p = self.ls.plan
+        n = int(p.gsize[k])
+        out = {}
+        for s in range(p.sh_start[k], p.sh_start[k + 1]):
+            o = int(p.sh_doff[s])
+            out[int(p.sh_sub[s])] = self.D[o:o + n * n].view(n, n).cpu().numpy()
+        return out
+
+
+# ---------------------------------------------------------------------------
+# adaptive coarse space
+# ---------------------------------------------------------------------------
+
+def _face_ws(n):
+    n = np.asarray(n, dtype=np.int64)
+    sc = np.maximum(8 * n * n + 3 * n, _rowspace_ws(n, n))
+    return 7 * n * n + n + sc + 64
+
+
+def _rowspace_ws(m, n):
+    m = np.asarray(m, dtype=np.int64)
+    n = np.asarray(n, dtype=np.int64)
+    return 2 * n * n + n + np.maximum(m, n) + np.where(m <= n, n * m, m * n + n * n)
+
+
+def _edge_new_ws(ns, ne, wd, nhmax):
+    ns, ne, wd, nhmax = (np.asarray(x, dtype=np.int64) for x in (ns, ne, wd, nhmax))
+    nC = (ns - 1) * ne
+    nr = wd - nC
+    xd = ne + nhmax
+    base = ns * ne * nC + nC * nC + wd * wd + xd * xd + 2 * wd * wd
+    sc = np.maximum(np.maximum(8 * nC * nC + 3 * nC, 3 * nr * nr + nr), _rowspace_ws(nC * (ns - 1), ne))
+    return base + sc + 64
+
+
+class DevicePrimalSpace:
+    """Per-glob (Q, r) and eigenvalues produced on the device
+    (reference adaptive.py:288-342 / PrimalBasis adaptive.py:209-264)."""
+
+    def __init__(self, ls, scaling, theta_f, theta_e, variant):
+        if variant not in ("old", "new"):
+            raise ValueError(f"unknown variant {variant!r}")
+        p, d, st = ls.plan, ls.d, stream()
+        self.ls, self.variant = ls, variant
+        self.theta_f, self.theta_e = float(theta_f), float(theta_e)
+        Binv = ls.bsym_inverse()
+        G = p.G
+        kind = p.kind
+        nsh = np.diff(p.sh_start).astype(np.int64)
+        self.q_off = _excl(p.gsize.astype(np.int64) ** 2)
+        self.Q = torch.zeros(max(int(self.q_off[-1]), 1), dtype=F64, device="cuda")
+        vert = np.flatnonzero(kind == 2)
+        if vert.size:
+            self.Q[dev_i64(self.q_off[vert])] = 1.0  # 1x1 identity (vertices are fully primal)
+        self.d_q_off = dev_i64(self.q_off[:-1])
+        n_eig = np.where(kind == 0, p.gsize, 0).astype(np.int64)
+        if variant == "new":
+            n_eig = np.where(kind == 1, (nsh - 1) * p.gsize, n_eig)
+        else:
+            n_eig = np.where(kind == 1, p.gsize, n_eig)
+        self.eig_off = _excl(n_eig)
+        self.eig = torch.zeros(max(int(self.eig_off[-1]), 1), dtype=F64, device="cuda")
+        d_eig_off = dev_i64(self.eig_off[:-1])
+        r0 = np.where(kind == 2, p.gsize, 0).astype(np.int32)
+        self.r = dev_i32(r0)
+        self.n_sel = torch.zeros(max(G, 1), dtype=torch.int32, device="cuda")
+        status = torch.zeros(max(G, 1), dtype=torch.int32, device="cuda")
+
+        faces = np.flatnonzero(kind == 0)
+        edges = np.flatnonzero(kind == 1)
+        if faces.size:
+            wsz = _face_ws(p.gsize[faces])
+            woff = np.zeros(G + 1, dtype=np.int64)
+            woff[faces] = _excl(wsz)[:-1]
+            ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
+            lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, d.nB,
+                               d.soff, ls.Bsym, Binv, scaling.D, self.theta_f, self.eig, d_eig_off,
+                               self.n_sel, self.r, self.Q, self.d_q_off, status, ws,
+                               dev_i64(woff[:-1]), dev_i32(faces), faces.size,
+                               int(p.gsize[faces].max()), st)
+            self._raise(status, "face")
+            del ws
+        r_host = self.r.cpu().numpy()
+        if edges.size and variant == "new":
+            # prior sizes per subdomain: vertices + leading r_F of each face
+            k_kind = kind[p.sub_globs]
+            contrib = np.where(k_kind == 2, p.gsize[p.sub_globs],
+                               np.where(k_kind == 0, r_host[p.sub_globs], 0)).astype(np.int64)
+            nH = np.add.reduceat(contrib, p.sub_glob_start[:-1]) if contrib.size else np.zeros(p.N, np.int64)
+            nH = np.where(np.diff(p.sub_glob_start) > 0, nH, 0)
+            pb_off = _excl(nH * p.nB)
+            xhh_off = _excl(nH * nH)
+            PB = torch.empty(max(int(pb_off[-1]), 1), dtype=F64, device="cuda")
+            XHH = torch.empty(max(int(xhh_off[-1]), 1), dtype=F64, device="cuda")
+            d_pb_off, d_nH, d_xhh_off = dev_i64(pb_off[:-1]), dev_i32(nH), dev_i64(xhh_off[:-1])
+            lib.bddc_priors(d.kind, d.gsize, d.nB, d.soff, Binv, d.sub_glob_start, d.sub_globs,
+                            d.sub_glob_boff, self.r, self.Q, self.d_q_off, d_pb_off, d_nH, PB, XHH,
+                            d_xhh_off, p.N, st)
+            ns = nsh[edges]
+            ne = p.gsize[edges].astype(np.int64)
+            sh_nH = nH[p.sh_sub.astype(np.int64)]
+            sumH = np.add.reduceat(sh_nH, p.sh_start[:-1].astype(np.int64))[edges]
+            maxH = np.maximum.reduceat(sh_nH, p.sh_start[:-1].astype(np.int64))[edges]
+            wd = (ns - 1) * ne + ne + sumH
+            wsz = _edge_new_ws(ns, ne, wd, maxH)
+            woff = np.zeros(G + 1, dtype=np.int64)
+            woff[edges] = _excl(wsz)[:-1]
+            ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
+            lib.bddc_edge_gevp_new(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
+                                   d.nB, d.soff, ls.Bsym, Binv, scaling.D, d_pb_off, d_nH, PB, XHH,
+                                   d_xhh_off, self.theta_e, self.eig, d_eig_off, self.n_sel,
+                                   self.r, self.Q, self.d_q_off, status, ws, dev_i64(woff[:-1]),
+                                   dev_i32(edges), edges.size, int(wd.max()), st)
+            self._raise(status, "edge")
+            del ws, PB, XHH
+        elif edges.size:
+            wsz = _face_ws(p.gsize[edges])
+            woff = np.zeros(G + 1, dtype=np.int64)
+            woff[edges] = _excl(wsz)[:-1]
+            ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
+            lib.bddc_edge_gevp_old(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
+                                   d.nB, d.soff, ls.Bsym, Binv, scaling.D, self.theta_e, self.eig,
+                                   d_eig_off, self.n_sel, self.r, self.Q, self.d_q_off, status,
+                                   ws, dev_i64(woff[:-1]), dev_i32(edges), edges.size,
+                                   int(p.gsize[edges].max()), st)
+            self._raise(status, "edge")
+            del ws
+        self.r_host = self.r.cpu().numpy().astype(np.int64)
+        self.n_sel_host = self.n_sel.cpu().numpy().astype(np.int64)
+
+    def _raise(self, status, what):
+        s = status.cpu().numpy()
+        nz = np.flatnonzero(s)
+        if not nz.size:
+            return
+        k = int(nz[0])
+        code = int(s[k])
+        globs = self.ls.globs
+        gid = globs.glob_id(globs.globs[k])
+        p = self.ls.plan
+        if 100 <= code < 200:
+            sub = int(p.sh_sub[p.sh_start[k] + code - 100])
+            inner = f"glob Schur block on subdomain {sub} is singular"
+            raise NumericalError(inner)
+        if code == 200 + 3:
+            raise NumericalError(f"eigenproblem on glob {gid} failed: Btil is not positive semidefinite")
+        raise NumericalError(f"eigenproblem on glob {gid} failed (status {code})")
+
+    def eigenvalues(self, k):
+        a, b = int(self.eig_off[k]), int(self.eig_off[k + 1])
+        return self.eig[a:b].cpu().numpy()
+
+    def all_eigenvalues(self):
+        e = self.eig.cpu().numpy()
+        return {k: e[self.eig_off[k]:self.eig_off[k + 1]] for k in range(self.ls.plan.G)
+                if self.eig_off[k + 1] > self.eig_off[k]}
+
+    def q(self, k):
+        n = int(self.ls.plan.gsize[k])
+        o = int(self.q_off[k])
+        return self.Q[o:o + n * n].view(n, n).cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# preconditioner
+# ---------------------------------------------------------------------------
+
+class DevicePreconditioner:
+    """M^-1 = sum_i R_i^T (A_i R_i + N_i P_i C^-1 sum_j P_j^T G_j R_j)
+    (reference BddcPreconditioner solver.py:46-209, see precond.cu)."""
+
+    def __init__(self, ls, scaling, r_host, Q, q_off, keep_coarse=8192):
+        p, d, st = ls.plan, ls.d, stream()
+        self.ls, self.plan = ls, p
+        r = np.asarray(r_host, dtype=np.int64)
+        self.n_hat = p.n_hat
+        self.n_primal = int(r.sum())
+        if self.n_primal == 0:
+            raise NumericalError("empty primal space: no coarse problem to anchor the solver")
+        go = _excl(r)
+        self.glob_primal_offset = go[:-1]
+        cnt = r[p.sub_globs]
+        self.np_sub = np.add.reduceat(cnt, p.sub_glob_start[:-1].astype(np.int64)) if cnt.size else np.zeros(p.N, np.int64)
+        self.np_sub = np.where(np.diff(p.sub_glob_start) > 0, self.np_sub, 0)
+        pstart = _excl(self.np_sub)
+        ppos = _ranges(p.sub_glob_boff, cnt)
+        pgid = _ranges(go[:-1][p.sub_globs], cnt)
+        mask = np.zeros(int(p.voff[-1]), dtype=np.uint8)
+        psub = np.repeat(np.arange(p.N), self.np_sub)
+        mask[p.voff[psub] + ppos] = 1
+        poff = _excl(self.np_sub * p.nB)
+        coff = _excl(self.np_sub * self.np_sub)
+        self.d_pstart, self.d_ppos, self.d_pgid = dev_i32(pstart), dev_i32(ppos), dev_i32(pgid)
+        self.d_poff, d_coff = dev_i64(poff[:-1]), dev_i64(coff[:-1])
+        d_mask = torch.from_numpy(mask).cuda()
+        csrc = np.argsort(pgid, kind="stable")
+        self.d_csrc = dev_i64(csrc)
+        self.d_cstart = dev_i64(np.searchsorted(pgid[csrc], np.arange(self.n_primal + 1)))
+        self.sum_np = int(pstart[-1])
+
+        TT = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
+        lib.bddc_pc_ttblocks(d.slot_glob, d.gsize, Q, q_off, scaling.D, d.sh_doff, TT,
+                             int(p.sh_sub.size), st)
+        Sbar = torch.empty(p.S_total, dtype=F64, device="cuda")
+        tmp = torch.empty(p.S_total, dtype=F64, device="cuda")
+        lib.bddc_pc_transform_schur(d.nB, d.soff, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
+                                    d.sub_glob_sh, d.gsize, Q, q_off, ls.S, tmp, Sbar, p.N, st)
+        Z = torch.empty(p.S_total, dtype=F64, device="cuda")
+        lib.bddc_pc_dual_embed(d.nB, d.soff, d.voff, d_mask, Sbar, Z, tmp, p.N, st)
+        # certificate: LDL^T of sym(Sbar_dd) must have positive pivots (solver.py:91-98)
+        status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
+        pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
+        nbmax = int(p.nB.max())
+        lib.bddc_schur_eliminate(tmp, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax, nbmax,
+                                 pinv, 4096, 0, status, 1, None, 0, st)
+        bad = _first_bad(status)
+        if bad is not None:
+            raise NumericalError(f"dual block of subdomain {bad} lost positive definiteness")
+        lib.bddc_gj_inverse(Z, d.soff, d.nB, d.nB, p.N, nbmax, pinv, 4096, status, 0, st)
+        bad = _first_bad(status)
+        if bad is not None:
+            raise NumericalError(f"dual block of subdomain {bad} is singular")
+        lib.bddc_pc_zero_primal(d.nB, d.soff, d.voff, d_mask, Z, p.N, st)
+        self.A = torch.empty(p.S_total, dtype=F64, device="cuda")
+        lib.bddc_pc_local_operator(d.nB, d.soff, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
+                                   d.sub_glob_sh, d.gsize, d.sh_doff, TT, Z, tmp, self.A, p.N, st)
+        npn = max(int(poff[-1]), 1)
+        MP = torch.empty(npn, dtype=F64, device="cuda")
+        RP = torch.empty(npn, dtype=F64, device="cuda")
+        Cl = torch.empty(max(int(coff[-1]), 1), dtype=F64, device="cuda")
+        lib.bddc_pc_primal_pieces(d.nB, d.soff, self.d_pstart, self.d_ppos, self.d_poff, Sbar, Z,
+                                  MP, RP, Cl, d_coff, p.N, st)
+        self.G = torch.empty(npn, dtype=F64, device="cuda")
+        self.Nt = torch.empty(npn, dtype=F64, device="cuda")
+        lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
+                                  d.sub_glob_sh, d.gsize, d.sh_doff, TT, self.d_pstart,
+                                  self.d_poff, RP, self.G, p.N, st)
+        lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
+                                  d.sub_glob_sh, d.gsize, d.sh_doff, TT, self.d_pstart,
+                                  self.d_poff, MP, self.Nt, p.N, st)
+        del Sbar, tmp, Z, MP, RP, TT, pinv
+        nc = self.n_primal
+        C = torch.zeros(nc * nc, dtype=F64, device="cuda")
+        lib.bddc_coarse_scatter(self.d_pstart, self.d_pgid, Cl, d_coff, C, nc, p.N, st)
+        del Cl
+        self.coarse = C.view(nc, nc).cpu().numpy().copy() if nc <= keep_coarse else None
+        steps = (nc + 63) // 64
+        self.coarse_pinv = torch.empty(steps * 4096, dtype=F64, device="cuda")
+        piv = torch.zeros(nc, dtype=F64, device="cuda")
+        one_i64, nc_i32 = dev_i64([0]), dev_i32([nc])
+        status1 = torch.zeros(1, dtype=torch.int32, device="cuda")
+        lib.bddc_schur_eliminate(C, one_i64, nc_i32, nc_i32, nc_i32, nc_i32, 1, nc, nc, nc,
+                                 self.coarse_pinv, 4096, 4096, status1, 0, piv, nc, st)
+        self.coarse_lu = C
+        dg = np.abs(piv.cpu().numpy())
+        if dg.size and (dg.min() <= 1e-14 * max(dg.max(), 1.0) or not np.all(np.isfinite(dg))):
+            bad = int(np.argmin(np.where(np.isfinite(dg), dg, 0.0)))
+            gi = int(np.searchsorted(go[:-1], bad, side="right")) - 1
+            gid = ls.globs.glob_id(ls.globs.globs[gi])
+            raise NumericalError(f"coarse matrix is singular at primal dof {bad} "
+                                 f"(glob {gid}, constraint {bad - go[gi]})")
+        self.y = torch.empty(int(p.voff[-1]), dtype=F64, device="cuda")
+        self.cvals = torch.empty(max(self.sum_np, 1), dtype=F64, device="cuda")
+        self.rp = torch.empty(nc, dtype=F64, device="cuda")
+        self.up = torch.empty(nc, dtype=F64, device="cuda")
+
+    def apply_device(self, r, out=None):
+        p, d, st = self.plan, self.ls.d, stream()
+        if out is None:
+            out = torch.empty(self.n_hat, dtype=F64, device="cuda")
+        nbmax = int(p.nB.max())
+        lib.bddc_local_gemv(d.nB, d.soff, d.voff, d.iface_perm, self.A, r, self.y, self.d_pstart,
+                            self.d_poff, self.G, self.cvals, p.N, nbmax, 2, st)
+        lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp, self.n_primal, st)
+        lib.bddc_coarse_solve(self.coarse_lu, self.n_primal, self.n_primal, self.coarse_pinv, 4096,
+                              self.rp, self.up, st)
+        lib.bddc_prolong_primal(d.nB, d.voff, self.d_pstart, self.d_pgid, self.d_poff, self.Nt,
+                                self.up, self.y, p.N, st)
+        lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n_hat, st)
+        return out
+
+    def apply(self, r):
+        """M^-1 r on nodal interface vectors (numpy or device tensor)."""
+        if isinstance(r, torch.Tensor):
+            return self.apply_device(r.to(device="cuda", dtype=F64).contiguous())
+        return self.apply_device(dev_f64(r)).cpu().numpy()
+
+
+class DeviceInterfaceOperator:
+    """S_hat u = sum_i R_i^T S_i R_i u (reference solver.py:226-235)."""
+
+    def __init__(self, ls):
+        self.ls = ls
+        self.n = ls.plan.n_hat
+        self.y = torch.empty(int(ls.plan.voff[-1]), dtype=F64, device="cuda")
+
+    def apply_device(self, u, out=None):
+        p, d, st = self.ls.plan, self.ls.d, stream()
+        if out is None:
+            out = torch.empty(self.n, dtype=F64, device="cuda")
+        lib.bddc_local_gemv(d.nB, d.soff, d.voff, d.iface_perm, self.ls.S, u, self.y, None, None,
+                            None, None, p.N, int(p.nB.max()), 2, st)
+        lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n, st)
+        return out
+
+    def __call__(self, u):
+        if isinstance(u, torch.Tensor):
+            return self.apply_device(u.to(device="cuda", dtype=F64).contiguous())
+        return self.apply_device(dev_f64(u)).cpu().numpy()
+
+    def rhs_device(self):
+        p, d = self.ls.plan, self.ls.d
+        out = torch.empty(self.n, dtype=F64, device="cuda")
+        lib.bddc_gather_reduce(d.tstart, d.tsrc, self.ls.g, out, self.n, stream())
+        return out
+
+
+# ---------------------------------------------------------------------------
+# GMRES
+# ---------------------------------------------------------------------------
+
+class _Basis:
+    """Growable (m x n) stack of device vectors, contiguous."""
+
+    def __init__(self, n, cap=32):
+        self.n = n
+        self.buf = torch.empty((cap, n), dtype=F64, device="cuda")
+
+    def ensure(self, m):
+        if m > self.buf.shape[0]:
+            nb = torch.empty((max(m, 2 * self.buf.shape[0]), self.n), dtype=F64, device="cuda")
+            nb[:self.buf.shape[0]].copy_(self.buf)
+            self.buf = nb
+
+    def __getitem__(self, j):
+        return self.buf[j]
+
+
+def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
+    """Full left-preconditioned GMRES (reference solver.py:262-315).
+
+    Orthogonalisation is classical Gram-Schmidt applied twice (same Krylov
+    space as the reference's MGS x 2); the least-squares problem is solved
+    with gelsd on the host exactly as the reference does; the true residual
+    uses stored S_hat V_j columns instead of an extra S_hat application."""
+    st = stream()
+    n = rhs.shape[0]
+    nblk = 296
+    partial = torch.empty(nblk * (max_iter + 2), dtype=F64, device="cuda")
+    scal = torch.empty(max_iter + 2, dtype=F64, device="cuda")
+    z0 = pc.apply_device(rhs)
+    lib.bddc_norm2(z0, n, scal, partial, nblk, st)
+    ref = float(scal[0].item())
+    if ref == 0.0:
+        return 0, True, torch.zeros(n, dtype=F64, device="cuda"), [0.0], [0.0]
+    V = _Basis(n)
+    U = _Basis(n)
+    lib.bddc_scale_copy(z0, n, scal, V[0], st)
+    H = np.zeros((max_iter + 1, max_iter))
+    e1 = np.zeros(max_iter + 1)
+    e1[0] = ref
+    h1 = torch.empty(max_iter + 1, dtype=F64, device="cuda")
+    w = torch.empty(n, dtype=F64, device="cuda")
+    r = torch.empty(n, dtype=F64, device="cuda")
+    true_hist, pre_hist = [], []
+    conv = False
+    it = 0
+    y = np.zeros(0)
+    for j in range(max_iter):
+        U.ensure(j + 1)
+        operator.apply_device(V[j], out=U[j])
+        pc.apply_device(U[j], out=w)
+        m = j + 1
+        lib.bddc_multi_dot(V.buf, n, m, w, h1, partial, nblk, 0, st)
+        lib.bddc_multi_axpy(V.buf, n, m, h1, -1.0, w, st)
+        lib.bddc_multi_dot(V.buf, n, m, w, scal, partial, nblk, 0, st)
+        lib.bddc_multi_axpy(V.buf, n, m, scal, -1.0, w, st)
+        lib.bddc_norm2(w, n, scal[m:], partial, nblk, st)
+        hs = scal[:m + 1].cpu().numpy()
+        hh = h1[:m].cpu().numpy() + hs[:m]
+        hn = float(hs[m])
+        H[:m, j] = hh
+        H[m, j] = hn
+        y = scipy.linalg.lstsq(H[:m + 1, :m], e1[:m + 1], lapack_driver="gelsd")[0]
+        res = float(np.linalg.norm(e1[:m + 1] - H[:m + 1, :m] @ y))
+        it = m
+        pre_hist.append(res / ref)
+        yd = dev_f64(y)
+        r.copy_(rhs)
+        lib.bddc_multi_axpy(U.buf, n, m, yd, -1.0, r, st)
+        lib.bddc_norm2(r, n, scal, partial, nblk, st)
+        true_hist.append(float(scal[0].item()))
+        if pre_hist[-1] <= rel_tol:
+            conv = True
+            break
+        if hn <= 1e-14 * ref:
+            conv = pre_hist[-1] <= rel_tol
+            break
+        V.ensure(j + 2)
+        lib.bddc_scale_copy(w, n, scal[m:], V[j + 1], st)
+    x = torch.zeros(n, dtype=F64, device="cuda")
+    if it:
+        lib.bddc_multi_axpy(V.buf, n, it, dev_f64(y), 1.0, x, st)
+    return it, conv, x, true_hist, pre_hist
+
+
+def recover_device(ls, u_hat):
+    """Nodal solution with interiors back-substituted (reference solver.py:318-326)."""
+    p, d, st = ls.plan, ls.d, stream()
+    u = ls.inputs["gdir"].clone()
+    u[dev_i64(ls.globs.interface_nodes)] = u_hat
+    lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, d.iface_perm, d.ioff,
+                              d.I_nodes, u_hat, u, p.N, int(p.nL.max()), st)
+    return u

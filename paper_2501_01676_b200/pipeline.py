@@ -1,0 +1,62 @@
+"""End-to-end hot path on the device, with per-phase CUDA-event timings.
+
+Same phases as the reference harness (harness.py:250-292) plus interior
+recovery: subdomain operators -> deluxe scaling -> Bsym^-1 -> adaptive
+primal space -> preconditioner -> GMRES -> recover_interior.
+"""
+
+import time
+
+import numpy as np
+import torch
+
+from .engine import (DeviceInterfaceOperator, DevicePreconditioner, DevicePrimalSpace,
+                     DeviceScaling, LocalSystem, PhaseTimer, gmres_device, recover_device,
+                     upload_inputs)
+from .plan import Plan
+
+
+class Result:
+    pass
+
+
+def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8, max_iter=300,
+        plan=None, inputs=None, timings=True, keep=False):
+    """Run the whole hot path; returns a Result with counts, solutions
+    (device tensors) and phase times in ms (CUDA events)."""
+    tm = PhaseTimer(timings)
+    tm.mark("subdomain_ops")
+    if plan is None:
+        plan = Plan(system, partition, globs)
+    ls = LocalSystem(system, partition, globs, plan=plan, inputs=inputs)
+    tm.mark("bsym_inverse")
+    ls.bsym_inverse()
+    tm.mark("scaling")
+    sc = DeviceScaling(ls)
+    tm.mark("gevp")
+    ps = DevicePrimalSpace(ls, sc, theta_f, theta_e, variant)
+    tm.mark("pc_setup")
+    pc = DevicePreconditioner(ls, sc, ps.r_host, ps.Q, ps.d_q_off)
+    op = DeviceInterfaceOperator(ls)
+    tm.mark("gmres")
+    rhs = op.rhs_device()
+    it, conv, x, th, ph = gmres_device(op, rhs, pc, rel_tol, max_iter)
+    tm.mark("recover")
+    u = recover_device(ls, x)
+    tm.mark("end")
+    res = Result()
+    kinds = plan.kind
+    r = ps.r_host
+    res.iterations, res.converged = it, conv
+    res.solution, res.u = x, u
+    res.true_hist, res.pre_hist = th, ph
+    res.pnumF = int(r[kinds == 0].sum())
+    res.pnumE = int(r[kinds == 1].sum())
+    res.n_vertex = int(r[kinds == 2].sum())
+    res.n_c = int(r.sum())
+    res.n_primal = r
+    res.n_sel = ps.n_sel_host
+    res.times_ms = tm.result()
+    if keep:
+        res.ls, res.scaling, res.space, res.pc, res.op = ls, sc, ps, pc, op
+    return res

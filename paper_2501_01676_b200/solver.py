@@ -1,0 +1,99 @@
+"""BDDC preconditioner, interface system and GMRES (reference solver.py),
+on the device (csrc/precond.cu, csrc/krylov.cu)."""
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .engine import (DeviceInterfaceOperator, DevicePreconditioner, NumericalError, dev_f64,
+                     dev_i64, gmres_device, recover_device)
+
+F64 = torch.float64
+
+
+@dataclass
+class SolveReport:
+    """solver.py:31-43"""
+
+    iterations: int
+    converged: bool
+    solution: np.ndarray
+    residual_history: list
+    preconditioned_history: list
+    setup_time: float = 0.0
+    solve_time: float = 0.0
+    gevp_time: float = 0.0
+    pnumF: int = 0
+    pnumE: int = 0
+    extra: dict = field(default_factory=dict)
+
+
+class BddcPreconditioner(DevicePreconditioner):
+    """Reference class name (solver.py:46); ``apply`` takes numpy or device vectors."""
+
+    def __init__(self, ops, primal, scaling):
+        ls = ops[0].ls
+        self.ops = sorted(ops, key=lambda o: o.sub_id)
+        self.primal = primal
+        self.scaling = scaling
+        if primal.device is not None:
+            Q, q_off = primal.device.Q, primal.device.d_q_off
+        else:
+            Q, q_off = _upload_transforms(ls, primal)
+        super().__init__(ls, scaling.device, primal.r, Q, q_off)
+
+
+def _upload_transforms(ls, primal):
+    sizes = ls.plan.gsize.astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(sizes * sizes)])
+    flat = np.zeros(max(int(off[-1]), 1))
+    for k, (Q, _) in enumerate(primal.transforms):
+        flat[off[k]:off[k + 1]] = np.asarray(Q, dtype=float).ravel()
+    return dev_f64(flat), dev_i64(off[:-1])
+
+
+def build_preconditioner(ops, primal, scaling):
+    """solver.py:212-213"""
+    return BddcPreconditioner(ops, primal, scaling)
+
+
+class InterfaceOperator(DeviceInterfaceOperator):
+    """Callable S_hat (solver.py:226-235) on numpy or device vectors."""
+
+
+def interface_operator(ops, n):
+    op = InterfaceOperator(ops[0].ls)
+    if n != op.n:
+        raise ValueError(f"interface size {n} does not match the operators ({op.n})")
+    return op
+
+
+def interface_rhs(ops, n):
+    """g_hat = sum R_i^T g_i (solver.py:238-242)."""
+    return InterfaceOperator(ops[0].ls).rhs_device().cpu().numpy()
+
+
+def gmres_solve(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
+    """Full left-preconditioned GMRES (solver.py:262-315) on the device."""
+    if not isinstance(operator, DeviceInterfaceOperator) or not isinstance(pc, DevicePreconditioner):
+        raise TypeError("gmres_solve runs on the device: pass interface_operator(...) and "
+                        "build_preconditioner(...) objects from this package")
+    t0 = time.perf_counter()
+    rhs_d = rhs if isinstance(rhs, torch.Tensor) else dev_f64(rhs)
+    it, conv, x, th, ph = gmres_device(operator, rhs_d.to(dtype=F64, device="cuda"), pc,
+                                       rel_tol, max_iter)
+    return SolveReport(it, conv, x.cpu().numpy(), th, ph, solve_time=time.perf_counter() - t0)
+
+
+def recover_interior(ops, globs, system, u_hat):
+    """solver.py:318-326"""
+    ls = ops[0].ls
+    u_d = u_hat if isinstance(u_hat, torch.Tensor) else dev_f64(u_hat)
+    return recover_device(ls, u_d.to(dtype=F64, device="cuda")).cpu().numpy()
+
+
+__all__ = ["BddcPreconditioner", "InterfaceOperator", "NumericalError", "SolveReport",
+           "build_preconditioner", "gmres_solve", "interface_operator", "interface_rhs",
+           "recover_interior"]

@@ -1,0 +1,55 @@
+"""Parity of the CUDA path against the reference golden fixtures (and the
+oracle for intermediate quantities).  Bars (north_star): per-glob primal
+counts exact except eigenvalues within 1e-8 relative of the threshold,
+GMRES iterations +-1, solutions relative difference <= 1e-8 in fp64."""
+
+import numpy as np
+import pytest
+
+from tests.cases import FIXTURES, counts_match, gevp_values, golden, inputs, variants
+
+pytestmark = pytest.mark.gpu
+
+FAST = [n for n in FIXTURES if n != "cfg3"]
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.parametrize("name", FAST)
+def test_pipeline_matches_reference(name):
+    from paper_2501_01676_b200 import pipeline
+    from paper_2501_01676_b200.substructuring import SubdomainOperator
+
+    g = golden(name)
+    system, part, globs = inputs(name)
+    kinds = [gl.kind for gl in globs.globs]
+    for v in variants(g):
+        res = pipeline.run(system, part, globs, float(g["theta_f"]), float(g["theta_e"]), v,
+                           keep=True)
+        ls = res.ls
+        assert np.array_equal(ls.plan.nB, g["nB"])
+        for i in g["S_ids"].tolist():
+            op = SubdomainOperator(ls, i)
+            assert _rel(op.S, g[f"S_{i}"]) <= 1e-12, i
+            assert _rel(op.g, g[f"g_{i}"]) <= 1e-12, i
+            assert _rel(op.bsym_inverse(), g[f"Binv_{i}"]) <= 1e-10, i
+        assert _rel(res.op.rhs_device().cpu().numpy(), g["rhs"]) <= 1e-12
+        assert _rel(res.op(g["probe"]), g["Sprobe"]) <= 1e-12
+        ref_eig = gevp_values(g, v)
+        mine = res.space.all_eigenvalues()
+        for k, ev in ref_eig.items():
+            fin = np.isfinite(ev)
+            assert mine[k].shape == ev.shape, k
+            assert np.array_equal(np.isfinite(mine[k]), fin), k
+            scale = np.abs(ev[fin]).max(initial=1.0)
+            np.testing.assert_allclose(mine[k][fin], ev[fin], rtol=1e-8, atol=1e-10 * scale)
+        th = lambda k: float(g["theta_f"]) if kinds[k] == "face" else float(g["theta_e"])
+        assert counts_match(res.n_primal, g[f"{v}_n_primal"], None, ref_eig, th) == []
+        assert (res.pnumF, res.pnumE, res.n_vertex) == (
+            int(g[f"{v}_pnumF"]), int(g[f"{v}_pnumE"]), int(g[f"{v}_n_vertex"]))
+        assert abs(res.iterations - int(g[f"{v}_iterations"])) <= 1
+        assert _rel(res.pc.apply(g["probe"]), g[f"{v}_Mprobe"]) <= 1e-7
+        assert _rel(res.solution.cpu().numpy(), g[f"{v}_solution"]) <= 1e-8
+        assert _rel(res.u.cpu().numpy(), g[f"{v}_u"]) <= 1e-8
