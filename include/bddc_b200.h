@@ -61,6 +61,15 @@ int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const i
                          long long pinv_step_stride, int* status, int require_positive,
                          double* piv_out, long long piv_stride, cudaStream_t stream);
 
+/* Same, recording CUDA events around every trailing-update launch; the summed
+ * device time (ms) is written to the HOST pointer host_trailing_ms (bench roofline). */
+int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, const int* npiv,
+                               const int* nrows, const int* ncols, int nbatch, int max_npiv,
+                               int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
+                               long long pinv_step_stride, int* status, int require_positive,
+                               double* piv_out, long long piv_stride, cudaStream_t stream,
+                               double* host_trailing_ms);
+
 /* Blocked in-place Gauss-Jordan inverse (no pivoting).
  * replaces cho_factor/cho_solve(Bsym, I) substructuring.py:64-75 (require_positive = 1)
  *          lu_factor(Sdd) + lu_solve solver.py:99, 105, 187, 195 (require_positive = 0). */
@@ -219,6 +228,10 @@ int bddc_norm2(const double* w, long long n, double* out, double* partial, int n
                cudaStream_t stream);
 int bddc_scale_copy(const double* a, long long n, const double* den, double* out,
                     cudaStream_t stream);
+
+/* ---- counters.cu : launch accounting (bench "gpu_launches") ---------------- */
+long long bddc_launch_count(void);
+int bddc_launch_count_reset(void);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,9 @@ def parse_header(path=HEADER):
     for m in re.finditer(r"(int|long long)\s+(bddc_\w+)\s*\(([^)]*)\)\s*;", text):
         ret, name, args = m.group(1), m.group(2), m.group(3)
         types = []
+        if args.strip() in ("", "void"):
+            out[name] = (_CTYPES[ret], types)
+            continue
         for a in args.split(","):
             a = " ".join(a.replace("const", " ").split())
             if "*" in a:
@@ -83,7 +86,7 @@ def _conv(a):
 def _checked(name, fn):
     def call(*args):
         rc = fn(*[_conv(a) for a in args])
-        if isinstance(rc, int) and name.startswith("bddc_ws_") is False and rc < 0:
+        if isinstance(rc, int) and not name.startswith(("bddc_ws_", "bddc_launch")) and rc < 0:
             raise RuntimeError(f"{name}: CUDA launch failed ({torch.cuda.get_device_name()} "
                                f"error {-rc})")
         return rc

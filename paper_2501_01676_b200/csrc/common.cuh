@@ -5,6 +5,8 @@
 
 #define BDDC_DEV __device__ __forceinline__
 
+extern "C" void bddc_note_launches(int n);
+
 namespace bddc {
 
 // Status codes written by kernels into caller-owned device int arrays

@@ -854,7 +854,7 @@ int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int
                 const long long* ws_off, int* status, int n_globs, cudaStream_t stream) {
   if (n_globs <= 0) return 0;
   GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, nullptr);
-  deluxe_kernel<<<n_globs, 256, 0, stream>>>(t, D, ws, ws_off, status);
+  deluxe_kernel<<<n_globs, 256, 0, stream>>>(t, D, ws, ws_off, status); bddc_note_launches(1);
   return glob_launch_status();
 }
 
@@ -870,7 +870,7 @@ int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const 
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int smem = shmem_for(max_n);
   if (smem > 48 * 1024) cudaFuncSetAttribute(face_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  face_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids);
+  face_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids); bddc_note_launches(1);
   return glob_launch_status();
 }
 
@@ -882,7 +882,7 @@ int bddc_priors(const int* kind, const int* size, const int* nB, const long long
   if (n_sub <= 0) return 0;
   GlobTables t = make_tables(kind, size, nullptr, nullptr, nullptr, nullptr, nB, soff, nullptr, Binv);
   priors_kernel<<<n_sub, 256, 0, stream>>>(t, sub_glob_start, sub_globs, sub_glob_boff, r, Q,
-                                           q_off, pb_off, nH, PB, XHH, xhh_off);
+                                           q_off, pb_off, nH, PB, XHH, xhh_off); bddc_note_launches(1);
   return glob_launch_status();
 }
 
@@ -900,7 +900,7 @@ int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, co
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int smem = shmem_for(max_dim);
   if (smem > 48 * 1024) cudaFuncSetAttribute(edge_new_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  edge_new_kernel<<<n_edges, 256, smem, stream>>>(t, D, pr, theta, o, ws, ws_off, edge_ids);
+  edge_new_kernel<<<n_edges, 256, smem, stream>>>(t, D, pr, theta, o, ws, ws_off, edge_ids); bddc_note_launches(1);
   return glob_launch_status();
 }
 
@@ -916,7 +916,7 @@ int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, co
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int smem = shmem_for(max_n);
   if (smem > 48 * 1024) cudaFuncSetAttribute(edge_old_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  edge_old_kernel<<<n_edges, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, edge_ids);
+  edge_old_kernel<<<n_edges, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, edge_ids); bddc_note_launches(1);
   return glob_launch_status();
 }
 

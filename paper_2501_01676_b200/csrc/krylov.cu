@@ -94,9 +94,9 @@ int bddc_multi_dot(const double* V, long long n, int m, const double* w, double*
   if (m <= 0) return 0;
   for (int j0 = 0; j0 < m; j0 += kDotMaxVec) {
     const int mv = min(kDotMaxVec, m - j0);
-    multi_dot_kernel<<<nblocks, kDotThreads, 0, stream>>>(V, n, j0, mv, w, partial, m);
+    multi_dot_kernel<<<nblocks, kDotThreads, 0, stream>>>(V, n, j0, mv, w, partial, m); bddc_note_launches(1);
   }
-  reduce_partials_kernel<<<ceil_div(m, 128), 128, 0, stream>>>(partial, nblocks, m, m, h, accumulate);
+  reduce_partials_kernel<<<ceil_div(m, 128), 128, 0, stream>>>(partial, nblocks, m, m, h, accumulate); bddc_note_launches(1);
   return kr_status();
 }
 
@@ -104,7 +104,7 @@ int bddc_multi_axpy(const double* V, long long n, int m, const double* coef, dou
                     double* w, cudaStream_t stream) {
   if (m <= 0 || n <= 0) return 0;
   const int blocks = min(ceil_div(n, 256), 148 * 8);
-  multi_axpy_kernel<<<blocks, 256, m * sizeof(double), stream>>>(V, n, m, coef, alpha, w);
+  multi_axpy_kernel<<<blocks, 256, m * sizeof(double), stream>>>(V, n, m, coef, alpha, w); bddc_note_launches(1);
   return kr_status();
 }
 
@@ -112,14 +112,14 @@ int bddc_norm2(const double* w, long long n, double* out, double* partial, int n
                cudaStream_t stream) {
   int st = bddc_multi_dot(w, n, 1, w, out, partial, nblocks, 0, stream);
   if (st) return st;
-  sqrt_kernel<<<1, 1, 0, stream>>>(out);
+  sqrt_kernel<<<1, 1, 0, stream>>>(out); bddc_note_launches(1);
   return kr_status();
 }
 
 int bddc_scale_copy(const double* a, long long n, const double* den, double* out,
                     cudaStream_t stream) {
   if (n <= 0) return 0;
-  scale_copy_kernel<<<min(ceil_div(n, 256), 148 * 8), 256, 0, stream>>>(a, n, den, out);
+  scale_copy_kernel<<<min(ceil_div(n, 256), 148 * 8), 256, 0, stream>>>(a, n, den, out); bddc_note_launches(1);
   return kr_status();
 }
 

@@ -323,6 +323,58 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
   dim3 grid(ceil_div(max_elems, 128), nbatch);
   assemble_kernel<<<grid, 128, 0, stream>>>(K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke,
                                              Fe, gdir);
+  bddc_note_launches(1);
+  return launch_status();
+}
+
+static int schur_eliminate_impl(double* M, const long long* off, const int* ld, const int* npiv,
+                                const int* nrows, const int* ncols, int nbatch, int max_npiv,
+                                int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
+                                long long pinv_step_stride, int* status, int require_positive,
+                                double* piv_out, long long piv_stride, cudaStream_t stream,
+                                double* host_trailing_ms) {
+  if (nbatch <= 0) return 0;
+  const int smem = smem_tile_setup();
+  const int nsteps = (max_npiv + kTile - 1) / kTile;
+  cudaEvent_t* ev = nullptr;
+  if (host_trailing_ms) {
+    ev = new cudaEvent_t[2 * nsteps];
+    for (int i = 0; i < 2 * nsteps; ++i) cudaEventCreate(&ev[i]);
+    *host_trailing_ms = 0.0;
+  }
+  int launches = 0, timed = 0;
+  for (int k = 0; k < max_npiv; k += kTile) {
+    double* P = pinv_ws + (long long)(k / kTile) * pinv_step_stride;
+    pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, k, P, pinv_stride, status,
+                                                     require_positive, piv_out, piv_stride);
+    ++launches;
+    const int ct = ceil_div(max_cols - k, kTile);
+    const int rt = ceil_div(max_rows - k, kTile);
+    if (ct > 0) {
+      schur_row_kernel<<<dim3(ct, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
+                                                                        P, pinv_stride);
+      ++launches;
+    }
+    if (ct > 0 && rt > 0) {
+      if (ev) cudaEventRecord(ev[2 * timed], stream);
+      schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, smem, stream>>>(
+          M, off, ld, npiv, nrows, ncols, k);
+      ++launches;
+      if (ev) cudaEventRecord(ev[2 * timed + 1], stream);
+      timed += (ev != nullptr);
+    }
+  }
+  if (ev) {
+    if (timed) cudaEventSynchronize(ev[2 * timed - 1]);
+    for (int i = 0; i < timed; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]);
+      *host_trailing_ms += ms;
+    }
+    for (int i = 0; i < 2 * nsteps; ++i) cudaEventDestroy(ev[i]);
+    delete[] ev;
+  }
+  bddc_note_launches(launches);
   return launch_status();
 }
 
@@ -331,22 +383,20 @@ int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const i
                          int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
                          long long pinv_step_stride, int* status, int require_positive,
                          double* piv_out, long long piv_stride, cudaStream_t stream) {
-  if (nbatch <= 0) return 0;
-  const int smem = smem_tile_setup();
-  for (int k = 0; k < max_npiv; k += kTile) {
-    double* P = pinv_ws + (long long)(k / kTile) * pinv_step_stride;
-    pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, k, P, pinv_stride, status,
-                                                     require_positive, piv_out, piv_stride);
-    const int ct = ceil_div(max_cols - k, kTile);
-    const int rt = ceil_div(max_rows - k, kTile);
-    if (ct > 0)
-      schur_row_kernel<<<dim3(ct, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
-                                                                        P, pinv_stride);
-    if (ct > 0 && rt > 0)
-      schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, smem, stream>>>(
-          M, off, ld, npiv, nrows, ncols, k);
-  }
-  return launch_status();
+  return schur_eliminate_impl(M, off, ld, npiv, nrows, ncols, nbatch, max_npiv, max_rows,
+                              max_cols, pinv_ws, pinv_stride, pinv_step_stride, status,
+                              require_positive, piv_out, piv_stride, stream, nullptr);
+}
+
+int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, const int* npiv,
+                               const int* nrows, const int* ncols, int nbatch, int max_npiv,
+                               int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
+                               long long pinv_step_stride, int* status, int require_positive,
+                               double* piv_out, long long piv_stride, cudaStream_t stream,
+                               double* host_trailing_ms) {
+  return schur_eliminate_impl(M, off, ld, npiv, nrows, ncols, nbatch, max_npiv, max_rows,
+                              max_cols, pinv_ws, pinv_stride, pinv_step_stride, status,
+                              require_positive, piv_out, piv_stride, stream, host_trailing_ms);
 }
 
 int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n, int nbatch,
@@ -363,6 +413,7 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
     gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k);
     gj_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride);
+    bddc_note_launches(4);
   }
   return launch_status();
 }
@@ -373,6 +424,7 @@ int bddc_extract_schur(const double* M, const long long* off, const int* ld, con
   if (nbatch <= 0) return 0;
   extract_schur_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(M, off, ld, nI, nB, soff, voff, S,
                                                              Bsym, g);
+  bddc_note_launches(1);
   return launch_status();
 }
 
@@ -380,6 +432,7 @@ int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
                     cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   symmetrize_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(X, soff, n);
+  bddc_note_launches(1);
   return launch_status();
 }
 
@@ -394,6 +447,7 @@ int bddc_recover_interior(const double* M, const long long* off, const int* ld, 
     cudaFuncSetAttribute(recover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   recover_kernel<<<nbatch, 256, smem, stream>>>(M, off, ld, nI, nB, voff, iface_perm, ioff,
                                                 interior_nodes, u_hat, u);
+  bddc_note_launches(1);
   return launch_status();
 }
 

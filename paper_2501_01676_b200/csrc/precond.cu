@@ -406,8 +406,8 @@ int bddc_pc_transform_schur(const int* nB, const long long* soff, const long lon
   if (nbatch <= 0) return 0;
   SubGlobMap m = make_map(nB, soff, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize, Q,
                           q_off, nullptr, nullptr);
-  block_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, S, tmp, 0, 0);
-  block_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, tmp, Sbar, 0, 1);
+  block_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, S, tmp, 0, 0); bddc_note_launches(1);
+  block_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, tmp, Sbar, 0, 1); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -415,7 +415,7 @@ int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
                      const long long* q_off, const double* D, const long long* sh_doff,
                      double* TT, int n_slots, cudaStream_t stream) {
   if (n_slots <= 0) return 0;
-  ttblock_kernel<<<n_slots, 128, 0, stream>>>(slot_glob, gsize, Q, q_off, D, sh_doff, TT, n_slots);
+  ttblock_kernel<<<n_slots, 128, 0, stream>>>(slot_glob, gsize, Q, q_off, D, sh_doff, TT, n_slots); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -424,7 +424,7 @@ int bddc_pc_dual_embed(const int* nB, const long long* soff, const long long* vo
                        double* Csym, int nbatch, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   dual_embed_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(nB, soff, voff, primal_mask, Sbar, Zin,
-                                                          Csym);
+                                                          Csym); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -432,7 +432,7 @@ int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* v
                         const unsigned char* primal_mask, double* Z, int nbatch,
                         cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  zero_primal_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(nB, soff, voff, primal_mask, Z);
+  zero_primal_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(nB, soff, voff, primal_mask, Z); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -447,9 +447,9 @@ int bddc_pc_local_operator(const int* nB, const long long* soff, const long long
                           nullptr, nullptr, nullptr, sh_doff);
   // T = blockdiag(Q D^T) = blockdiag(TT^T).  Y = Z T: right multiply by L^T with L = TT
   //   (in * L^T)[r][c] = sum_q in[r][bo+q] * L[c'][q]  with L = TT (transpose_block = 0)
-  tt_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, TT, Z, tmp, 1, 0);
+  tt_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, TT, Z, tmp, 1, 0); bddc_note_launches(1);
   // A = T^T Y = TT Y: left multiply with L = TT
-  tt_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, TT, tmp, A, 0, 0);
+  tt_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, TT, tmp, A, 0, 0); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -459,7 +459,7 @@ int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstar
                           const long long* coff, int nbatch, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   primal_pieces_kernel<<<nbatch, 256, 0, stream>>>(nB, soff, pstart, ppos, poff, Sbar, Z, MP, RP,
-                                                   Cl, coff);
+                                                   Cl, coff); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -471,7 +471,7 @@ int bddc_pc_primal_rows_T(const int* nB, const long long* voff, const int* pos2k
   if (nbatch <= 0) return 0;
   SubGlobMap m = make_map(nB, nullptr, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
                           nullptr, nullptr, nullptr, sh_doff);
-  primal_rows_times_T_kernel<<<dim3(16, nbatch), 256, 0, stream>>>(m, TT, pstart, poff, In, Out);
+  primal_rows_times_T_kernel<<<dim3(16, nbatch), 256, 0, stream>>>(m, TT, pstart, poff, In, Out); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -479,7 +479,7 @@ int bddc_coarse_scatter(const int* pstart, const int* pgid, const double* Cl,
                         const long long* coff, double* C, long long ldc, int nbatch,
                         cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  coarse_scatter_kernel<<<nbatch, 128, 0, stream>>>(pstart, pgid, Cl, coff, C, ldc);
+  coarse_scatter_kernel<<<nbatch, 128, 0, stream>>>(pstart, pgid, Cl, coff, C, ldc); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -493,12 +493,12 @@ int bddc_local_gemv(const int* nB, const long long* soff, const long long* voff,
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(local_gemv_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     local_gemv_kernel<true><<<dim3(row_chunks, nbatch), 256, smem, stream>>>(
-        nB, soff, voff, iface_perm, M, u, y, pstart, poff, G, cvals);
+        nB, soff, voff, iface_perm, M, u, y, pstart, poff, G, cvals); bddc_note_launches(1);
   } else {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(local_gemv_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     local_gemv_kernel<false><<<dim3(row_chunks, nbatch), 256, smem, stream>>>(
-        nB, soff, voff, iface_perm, M, u, y, nullptr, nullptr, nullptr, nullptr);
+        nB, soff, voff, iface_perm, M, u, y, nullptr, nullptr, nullptr, nullptr); bddc_note_launches(1);
   }
   return pc_status();
 }
@@ -507,14 +507,14 @@ int bddc_prolong_primal(const int* nB, const long long* voff, const int* pstart,
                         const long long* poff, const double* Nt, const double* uP, double* y,
                         int nbatch, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  prolong_primal_kernel<<<dim3(2, nbatch), 256, 0, stream>>>(nB, voff, pstart, pgid, poff, Nt, uP, y);
+  prolong_primal_kernel<<<dim3(2, nbatch), 256, 0, stream>>>(nB, voff, pstart, pgid, poff, Nt, uP, y); bddc_note_launches(1);
   return pc_status();
 }
 
 int bddc_gather_reduce(const long long* tstart, const long long* tsrc, const double* y,
                        double* out, long long n, cudaStream_t stream) {
   if (n <= 0) return 0;
-  gather_reduce_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(tstart, tsrc, y, out, n);
+  gather_reduce_kernel<<<ceil_div(n, 256), 256, 0, stream>>>(tstart, tsrc, y, out, n); bddc_note_launches(1);
   return pc_status();
 }
 
@@ -524,11 +524,11 @@ int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
   for (int k = 0; k < n; k += 64) {
     const int w = min(64, n - k);
     const int blocks = max(1, ceil_div(n - k - w, 64));
-    coarse_fwd_kernel<<<blocks, 256, 0, stream>>>(A, ld, n, k, pinv + (long long)(k / 64) * pinv_step_stride, b, t);
+    coarse_fwd_kernel<<<blocks, 256, 0, stream>>>(A, ld, n, k, pinv + (long long)(k / 64) * pinv_step_stride, b, t); bddc_note_launches(1);
   }
   const int last = ((n - 1) / 64) * 64;
   for (int k = last; k > 0; k -= 64) {
-    coarse_bwd_kernel<<<ceil_div(k, 64), 256, 0, stream>>>(A, ld, n, k, t);
+    coarse_bwd_kernel<<<ceil_div(k, 64), 256, 0, stream>>>(A, ld, n, k, t); bddc_note_launches(1);
   }
   return pc_status();
 }

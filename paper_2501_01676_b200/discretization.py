@@ -14,6 +14,7 @@ fits in host memory; the per-element arithmetic is evaluation-order identical
 to the reference (np.einsum without BLAS paths), so blocks agree bitwise.
 """
 
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Union
 
@@ -157,7 +158,7 @@ def _chunk_blocks(verts, nu, coeffs):
     return K, F, -1
 
 
-def element_contributions(mesh, coeffs, chunk=1 << 20):
+def element_contributions(mesh, coeffs, chunk=1 << 18):
     """Per-element 4x4 blocks and 4-vectors (reference discretization.py:101-158)."""
     el = mesh.elements
     m = el.shape[0]
@@ -175,14 +176,27 @@ def element_contributions(mesh, coeffs, chunk=1 << 20):
         raise ValueError("viscosity must be positive")
     K = np.empty((m, 4, 4))
     F = np.empty((m, 4))
-    for s in range(0, m, chunk):
+
+    def work(s):
         Kc, Fc, bad = _chunk_blocks(mesh.nodes[el[s:s + chunk]], nu[s:s + chunk], coeffs)
-        if bad >= 0:
-            raise ValueError(
-                f"shifted reaction c - div(a)/2 is not positive on element {s + bad}; "
-                "the symmetric part of the form would lose definiteness")
-        K[s:s + chunk] = Kc
-        F[s:s + chunk] = Fc
+        if bad < 0:
+            K[s:s + chunk] = Kc
+            F[s:s + chunk] = Fc
+        return s + bad if bad >= 0 else -1
+
+    starts = list(range(0, m, chunk))
+    if len(starts) > 1:
+        # numpy releases the GIL in these loops: chunks run on a thread pool
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=min(len(starts), os.cpu_count() or 1)) as ex:
+            bads = list(ex.map(work, starts))
+    else:
+        bads = [work(s) for s in starts]
+    bads = [b for b in bads if b >= 0]
+    if bads:
+        raise ValueError(
+            f"shifted reaction c - div(a)/2 is not positive on element {min(bads)}; "
+            "the symmetric part of the form would lose definiteness")
     return K, F, nu
 
 

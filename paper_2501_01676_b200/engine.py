@@ -8,8 +8,7 @@ GMRES's (j+2) x (j+1) least-squares recurrence, like the reference driver
 (solver.py:297).
 """
 
-import math
-import time
+import ctypes
 
 import numpy as np
 import scipy.linalg
@@ -71,14 +70,17 @@ class LocalSystem:
     Replaces build_subdomain_operator x N (reference substructuring.py:78-143)
     and SubdomainOperator.bsym_inverse (substructuring.py:64-75)."""
 
-    def __init__(self, system, partition, globs, plan=None, inputs=None, timer=None):
+    def __init__(self, system, partition, globs, plan=None, inputs=None, timer=None,
+                 kernel_timing=False, dplan=None):
         require_cuda()
+        self.kernel_timing = kernel_timing
+        self.trailing_ms = None
         self.system, self.partition, self.globs = system, partition, globs
         self.plan = plan or Plan(system, partition, globs)
         self.plan.check()
         p = self.plan
         self.N = p.N
-        self.d = _DevicePlan(p)
+        self.d = dplan if dplan is not None else DevicePlan(p)
         if inputs is None:
             inputs = upload_inputs(system)
         self.inputs = inputs
@@ -94,9 +96,14 @@ class LocalSystem:
                                 self.inputs["gdir"], p.N, p.max_elems, st)
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
-        lib.bddc_schur_eliminate(K, d.off, d.ld, d.nI, d.nL, d.nL1, p.N, int(p.nI.max()),
-                                 int(p.nL.max()), int(p.nL.max()) + 1, pinv, 4096, 0, status, 0,
-                                 None, 0, st)
+        args = (K, d.off, d.ld, d.nI, d.nL, d.nL1, p.N, int(p.nI.max()), int(p.nL.max()),
+                int(p.nL.max()) + 1, pinv, 4096, 0, status, 0, None, 0, st)
+        if self.kernel_timing:
+            ms = ctypes.c_double(0.0)
+            lib.bddc_schur_eliminate_timed(*args, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
+            self.trailing_ms = ms.value
+        else:
+            lib.bddc_schur_eliminate(*args)
         self.K = K
         self.S = torch.empty(p.S_total, dtype=F64, device="cuda")
         self.Bsym = torch.empty(p.S_total, dtype=F64, device="cuda")
@@ -137,13 +144,29 @@ class LocalSystem:
         return buf[int(p.voff[i]):int(p.voff[i + 1])].cpu().numpy()
 
 
+def trailing_flops(plan):
+    """Algorithmic flops of the Schur-elimination trailing updates (DMMA kernel):
+    sum over panels k and subdomains b of 2 * rows * cols * w."""
+    nI, nL = plan.nI.astype(np.int64), plan.nL.astype(np.int64)
+    total = 0
+    for k in range(0, int(nI.max()), 64):
+        act = nI > k
+        w = np.minimum(64, nI[act] - k)
+        rows = nL[act] - k - w
+        cols = nL[act] + 1 - k - w
+        total += int((2 * rows * cols * w).sum())
+    return total
+
+
 def _first_bad(status):
     s = status.cpu().numpy()
     nz = np.flatnonzero(s)
     return int(nz[0]) if nz.size else None
 
 
-class _DevicePlan:
+class DevicePlan:
+    """Plan index arrays resident on the device (uploaded once per plan)."""
+
     def __init__(self, p):
         self.off = dev_i64(p.off)
         self.ld = dev_i32(p.ld)

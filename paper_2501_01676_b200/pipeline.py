@@ -21,14 +21,16 @@ class Result:
 
 
 def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8, max_iter=300,
-        plan=None, inputs=None, timings=True, keep=False):
+        plan=None, inputs=None, timings=True, keep=False, kernel_timing=False,
+        dplan=None):
     """Run the whole hot path; returns a Result with counts, solutions
     (device tensors) and phase times in ms (CUDA events)."""
     tm = PhaseTimer(timings)
     tm.mark("subdomain_ops")
     if plan is None:
         plan = Plan(system, partition, globs)
-    ls = LocalSystem(system, partition, globs, plan=plan, inputs=inputs)
+    ls = LocalSystem(system, partition, globs, plan=plan, inputs=inputs,
+                     kernel_timing=kernel_timing, dplan=dplan)
     tm.mark("bsym_inverse")
     ls.bsym_inverse()
     tm.mark("scaling")
@@ -57,6 +59,7 @@ def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8,
     res.n_primal = r
     res.n_sel = ps.n_sel_host
     res.times_ms = tm.result()
+    res.trailing_ms = ls.trailing_ms
     if keep:
         res.ls, res.scaling, res.space, res.pc, res.op = ls, sc, ps, pc, op
     return res
