@@ -70,6 +70,15 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
                                double* piv_out, long long piv_stride, cudaStream_t stream,
                                double* host_trailing_ms);
 
+/* Envelope LU without pivoting of the coarse matrix (one n x n matrix at
+ * C + off[0], leading dimension ldv[0], nv[0] = n) in a bandwidth-reducing
+ * order: panel k updates only rows/cols below host_lim[k/64] (host array).
+ * Scalar pivots go to piv_out (for the singularity check solver.py:124-132).
+ * replaces lu_factor(coarse) solver.py:123. */
+int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const int* nv, int n,
+                       const int* host_lim, double* pinv, double* piv_out, int* status,
+                       cudaStream_t stream);
+
 /* Blocked in-place Gauss-Jordan inverse (no pivoting).
  * replaces cho_factor/cho_solve(Bsym, I) substructuring.py:64-75 (require_positive = 1)
  *          lu_factor(Sdd) + lu_solve solver.py:99, 105, 187, 195 (require_positive = 0). */
@@ -155,8 +164,9 @@ long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long n
 int bddc_pc_transform_schur(const int* nB, const long long* soff, const long long* voff,
                             const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
                             const int* sub_glob_sh, const int* gsize, const double* Q,
-                            const long long* q_off, const double* S, double* tmp, double* Sbar,
-                            int nbatch, cudaStream_t stream);
+                            const long long* q_off, const int* sub_glob_start, int max_globs,
+                            int max_ng, const double* S, double* tmp, double* Sbar, int nbatch,
+                            cudaStream_t stream);
 
 /* TT_(g,s) = D_g^(s) Q_g^T blocks.  replaces Dbar solver.py:87-90. */
 int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
@@ -176,7 +186,8 @@ int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* v
 int bddc_pc_local_operator(const int* nB, const long long* soff, const long long* voff,
                            const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
                            const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
-                           const double* TT, const double* Z, double* tmp, double* A, int nbatch,
+                           const int* sub_glob_start, int max_globs, int max_ng, const double* TT,
+                           const double* Z, double* tmp, double* A, int nbatch,
                            cudaStream_t stream);
 
 /* MP = E_P - (Z Sbar)_{:,P}^T rows, RP = E_P - (Sbar Z)_{P,:}, C_i = Sbar_PP - Sbar_P: Z Sbar_:P.
@@ -184,7 +195,7 @@ int bddc_pc_local_operator(const int* nB, const long long* soff, const long long
 int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstart,
                           const int* ppos, const long long* poff, const double* Sbar,
                           const double* Z, double* MP, double* RP, double* Cl,
-                          const long long* coff, int nbatch, cudaStream_t stream);
+                          const long long* coff, int nbatch, int max_nB, cudaStream_t stream);
 
 int bddc_pc_primal_rows_T(const int* nB, const long long* voff, const int* pos2k,
                           const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,
@@ -214,9 +225,13 @@ int bddc_prolong_primal(const int* nB, const long long* voff, const int* pstart,
 int bddc_gather_reduce(const long long* tstart, const long long* tsrc, const double* y,
                        double* out, long long n, cudaStream_t stream);
 
-/* coarse solve with the factors of bddc_schur_eliminate.  replaces lu_solve(coarse_lu) solver.py:192. */
+/* Coarse solve with the envelope-LU factors of bddc_coarse_factor: forward
+ * panel k touches rows [k+64, host_lim[k/64]), backward panel k touches rows
+ * [host_first[k/64], k) (host arrays; NULL = dense).  replaces
+ * lu_solve(coarse_lu) solver.py:192. */
 int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
-                      long long pinv_step_stride, double* b, double* t, cudaStream_t stream);
+                      long long pinv_step_stride, const int* host_lim, const int* host_first,
+                      double* b, double* t, cudaStream_t stream);
 
 /* ---- krylov.cu : GMRES vector kernels (solver.py:286-310) ------------------ */
 

@@ -195,8 +195,11 @@ BDDC_DEV double block_sum(double v, double* red) {
 // Symmetric eigendecomposition by cyclic parallel two-sided Jacobi
 // (round-robin pairing).  A (n x n, symmetric) is destroyed; w gets the
 // eigenvalues in ascending order; if V != nullptr its columns are the
-// matching orthonormal eigenvectors.  cs: 2*(n+1) doubles of scratch,
-// perm: n+1 ints of scratch (shared memory preferred).
+// matching orthonormal eigenvectors.  cs: 2*(n+2) doubles of scratch,
+// perm: 2*(n+2) ints of scratch (shared memory preferred).
+// Each round is two barrier phases: rotation parameters for the n/2
+// disjoint pairs, then one fused update in which every (pair_i, pair_j)
+// 2x2 block of A gets J_i^T A J_j (rows and columns at once) and V gets V J.
 // Returns false if the sweep limit was reached.
 BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ldv, double* cs,
                           int* perm, double* red) {
@@ -209,19 +212,18 @@ BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ld
   const int m = n + (n & 1);  // even player count; index n is a bye when n is odd
   const int half = m / 2;
   bool converged = false;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    double off = 0.0, dg = 0.0;
-    for (int idx = tid(); idx < n * n; idx += nth()) {
-      int r = idx / n, c = idx - r * n;
-      double v = A[r * ld + c];
-      if (r == c) dg += v * v; else off += v * v;
-    }
-    off = block_sum(off, red);
-    dg = block_sum(dg, red);
-    const double tol = fmax(1e-30, 4.0 * (double)n * (double)n * 4.9e-32);
-    if (off <= tol * dg || off == 0.0) { converged = true; break; }
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    // threshold Jacobi: rotate (p,q) only while |a_pq| exceeds both a relative
+    // (1e-15 sqrt|a_pp a_qq|) and an absolute (1e-17 max|a_ii|) floor; a sweep
+    // without rotations ends the iteration.
+    double dmax = 0.0;
+    for (int i = tid(); i < n; i += nth()) dmax = fmax(dmax, fabs(A[i * ld + i]));
+    dmax = block_max(dmax, red);
+    const double abs_floor = fmax(1e-17 * dmax, 1e-300);
+    int sweep_rot = 0;
     for (int round = 0; round < m - 1; ++round) {
-      // pairs: (0, m-1 rotated) tournament; slot i pairs position i with m-1-i
+      // phase 1: rotation of each pair (p < q); q == n is the bye
+      int rot = 0;
       for (int i = tid(); i < half; i += nth()) {
         int a = (i == 0) ? 0 : 1 + (i - 1 + round) % (m - 1);
         int b = 1 + (m - 2 - i + round) % (m - 1);
@@ -230,11 +232,12 @@ BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ld
         if (q < n) {
           const double apq = A[p * ld + q];
           const double app = A[p * ld + p], aqq = A[q * ld + q];
-          if (apq != 0.0 && fabs(apq) > 1e-300) {
+          if (fabs(apq) > abs_floor && fabs(apq) > 1e-15 * sqrt(fabs(app) * fabs(aqq))) {
             const double tau = (aqq - app) / (2.0 * apq);
             const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
             c = 1.0 / sqrt(1.0 + t * t);
             s = t * c;
+            rot = 1;
           }
         }
         perm[2 * i] = p;
@@ -242,37 +245,67 @@ BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ld
         cs[2 * i] = c;
         cs[2 * i + 1] = s;
       }
-      __syncthreads();
-      // rows: A <- J^T A
-      for (int idx = tid(); idx < half * n; idx += nth()) {
-        int i = idx / n, j = idx - i * n;
-        int p = perm[2 * i], q = perm[2 * i + 1];
-        if (q >= n) continue;
-        double c = cs[2 * i], s = cs[2 * i + 1];
-        if (s == 0.0) continue;
-        double ap = A[p * ld + j], aq = A[q * ld + j];
-        A[p * ld + j] = c * ap - s * aq;
-        A[q * ld + j] = s * ap + c * aq;
-      }
-      __syncthreads();
-      // columns: A <- A J, V <- V J
-      for (int idx = tid(); idx < half * n; idx += nth()) {
-        int i = idx / n, j = idx - i * n;
-        int p = perm[2 * i], q = perm[2 * i + 1];
-        if (q >= n) continue;
-        double c = cs[2 * i], s = cs[2 * i + 1];
-        if (s == 0.0) continue;
-        double ap = A[j * ld + p], aq = A[j * ld + q];
-        A[j * ld + p] = c * ap - s * aq;
-        A[j * ld + q] = s * ap + c * aq;
-        if (V) {
-          double vp = V[j * ldv + p], vq = V[j * ldv + q];
-          V[j * ldv + p] = c * vp - s * vq;
-          V[j * ldv + q] = s * vp + c * vq;
+      if (!__syncthreads_or(rot)) continue;
+      sweep_rot = 1;
+      // phase 2: A_blk(i,j) <- J_i^T A_blk J_j for bi <= bj (mirrored to (j,i),
+      // A stays exactly symmetric);  V(:, pair j) <- V(:, pair j) J_j
+      const int nblk = half * half;
+      for (int idx = tid(); idx < nblk + (V ? half * n : 0); idx += nth()) {
+        if (idx < nblk) {
+          const int bi = idx / half, bj = idx - bi * half;
+          if (bi > bj) continue;
+          const int p = perm[2 * bi], q = perm[2 * bi + 1];
+          const int pc = perm[2 * bj], qc = perm[2 * bj + 1];
+          const double ci = cs[2 * bi], si = cs[2 * bi + 1];
+          const double cj = cs[2 * bj], sj = cs[2 * bj + 1];
+          const bool hq = q < n, hqc = qc < n;
+          const double a00 = A[p * ld + pc];
+          const double a01 = hqc ? A[p * ld + qc] : 0.0;
+          const double a10 = hq ? A[q * ld + pc] : 0.0;
+          const double a11 = (hq && hqc) ? A[q * ld + qc] : 0.0;
+          // rows: x0 = c a_p - s a_q ; x1 = s a_p + c a_q
+          const double x00 = ci * a00 - si * a10, x01 = ci * a01 - si * a11;
+          const double x10 = si * a00 + ci * a10, x11 = si * a01 + ci * a11;
+          // cols: y[:,0] = c x[:,0] - s x[:,1] ; y[:,1] = s x[:,0] + c x[:,1]
+          const double y00 = cj * x00 - sj * x01, y01 = sj * x00 + cj * x01;
+          const double y10 = cj * x10 - sj * x11, y11 = sj * x10 + cj * x11;
+          if (bi == bj) {
+            A[p * ld + p] = y00;
+            if (hq) {
+              A[p * ld + q] = y01;
+              A[q * ld + p] = y01;
+              A[q * ld + q] = y11;
+            }
+          } else {
+            A[p * ld + pc] = y00;
+            A[pc * ld + p] = y00;
+            if (hqc) {
+              A[p * ld + qc] = y01;
+              A[qc * ld + p] = y01;
+            }
+            if (hq) {
+              A[q * ld + pc] = y10;
+              A[pc * ld + q] = y10;
+            }
+            if (hq && hqc) {
+              A[q * ld + qc] = y11;
+              A[qc * ld + q] = y11;
+            }
+          }
+        } else {
+          const int t2 = idx - nblk;
+          const int bj = t2 / n, r = t2 - bj * n;
+          const int pc = perm[2 * bj], qc = perm[2 * bj + 1];
+          if (qc >= n) continue;
+          const double cj = cs[2 * bj], sj = cs[2 * bj + 1];
+          const double vp = V[r * ldv + pc], vq = V[r * ldv + qc];
+          V[r * ldv + pc] = cj * vp - sj * vq;
+          V[r * ldv + qc] = sj * vp + cj * vq;
         }
       }
       __syncthreads();
     }
+    if (!sweep_rot) { converged = true; break; }
   }
   // ascending sort of the diagonal (rank by counting; ties by index)
   for (int i = tid(); i < n; i += nth()) {

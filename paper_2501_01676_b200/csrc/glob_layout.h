@@ -14,8 +14,8 @@ BDDC_HD long long bddc_rowspace_ws(long long m, long long n) {
   return 2 * n * n + n + mx + (m <= n ? n * m : m * n + n * n);
 }
 
-// face and old-edge kernels: 7 n^2 + n + max(parallel sum, pencil, row space)
-BDDC_HD long long bddc_face_ws(long long n) {
+// old-edge kernel: 7 n^2 + n + max(parallel sum, pencil, row space)
+BDDC_HD long long bddc_edge_old_ws(long long n) {
   long long sc = 8 * n * n + 3 * n;
   long long rs = bddc_rowspace_ws(n, n);
   if (rs > sc) sc = rs;

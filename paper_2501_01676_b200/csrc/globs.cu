@@ -75,17 +75,19 @@ BDDC_DEV void parallel_sum(const double* A, const double* B, int n, double* R, d
 BDDC_DEV int pencil(const double* B, const double* Bt, int n, double* vals, double* vecs,
                     int* degen, double* ws, double* cs, int* perm, double* red) {
   const int nn = n * n;
+  // layout: 8 n x n slots [A1 U A2 T1 T2 T3 T4 T5] then mu, bw, lam (n each);
+  // Bt may alias A1 (it is only read by the first copy)
   double* A1 = ws;
   double* U = A1 + nn;
-  double* mu = U + nn;
-  double* A2 = mu + n;
-  double* bw = A2 + nn;          // eigenvalues of B, later beta
-  double* T1 = bw + n;           // n x n
-  double* T2 = T1 + nn;          // n x n
-  double* T3 = T2 + nn;          // n x n
-  double* T4 = T3 + nn;          // n x n
-  double* T5 = T4 + nn;          // n x n
-  double* lam = T5 + nn;         // n
+  double* A2 = U + nn;
+  double* T1 = A2 + nn;
+  double* T2 = T1 + nn;
+  double* T3 = T2 + nn;
+  double* T4 = T3 + nn;
+  double* T5 = T4 + nn;
+  double* mu = T5 + nn;
+  double* bw = mu + n;           // eigenvalues of B, later beta
+  double* lam = bw + n;
   __shared__ int s_n0, s_status;
   __shared__ double s_bscale;
 
@@ -121,6 +123,7 @@ BDDC_DEV int pencil(const double* B, const double* Bt, int n, double* vals, doub
     // B00 = V0^T B V0 ; eigh -> (beta, P)
     blk::gemm(T1, n0, B, n, false, V0, n, false, n, n0, n, 1.0, 0.0);       // B V0 (n x n0)
     blk::gemm(T2, n0, V0, n, true, T1, n0, false, n0, n0, n, 1.0, 0.0);     // V0^T B V0
+    blk::symmetrize(T2, n0, n0);
     blk::jacobi_eigh(T2, n0, n0, bw, T3, n0, cs, perm, red);                 // beta asc, P = T3
     // acting modes ordered by decreasing |beta| (stable on ties by index)
     __shared__ int s_ninf;
@@ -358,29 +361,36 @@ struct GlobOut {
   int* status;              // per glob
 };
 
+// Arena (doubles) of one face: 10 n^2 + 3 n (+ pad), see face_kernel.
+__host__ __device__ inline long long face_arena(long long n) { return 10 * n * n + 3 * n + 32; }
+
 __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* __restrict__ D,
                                                    double theta, GlobOut o,
                                                    double* __restrict__ ws,
                                                    const long long* __restrict__ ws_off,
-                                                   const int* __restrict__ face_ids) {
+                                                   const int* __restrict__ face_ids,
+                                                   int arena_in_smem, int max_n) {
   extern __shared__ double sh[];
   const int g = face_ids[blockIdx.x];
   const int n = t.size[g];
   const int nn = n * n;
-  double* cs = sh;                                  // 2(n+2)
-  double* red = cs + 2 * (n + 2);                   // 32
-  double* rowbuf = red + 32;                        // 2(n+2)
-  int* perm = reinterpret_cast<int*>(rowbuf + 2 * (n + 2));   // 2(n+2)
-  double* W = ws + ws_off[g];
+  // small scratch sized for max_n, then (optionally) the arena
+  double* cs = sh;                                       // 2(max_n+2)
+  double* red = cs + 2 * (max_n + 2);                    // 32
+  double* rowbuf = red + 32;                             // 2(max_n+2)
+  int* perm = reinterpret_cast<int*>(rowbuf + 2 * (max_n + 2));  // 2(max_n+2)
+  int* degen = perm + 2 * (max_n + 2);                   // max_n + 2
+  double* W = arena_in_smem ? reinterpret_cast<double*>(degen + ((max_n + 2 + 1) & ~1))
+                            : ws + ws_off[g];
+  // arena slots: BF | VEC | pencil (8 slots + 3n)
   double* BF = W;
-  double* Bt = BF + nn;
-  double* Bti = Bt + nn;
-  double* Btj = Bti + nn;
-  double* T = Btj + nn;
-  double* vecs = T + nn;
-  double* rows = vecs + nn;
-  int* degen = reinterpret_cast<int*>(rows + nn);   // n ints (n doubles reserved)
-  double* scratch = rows + nn + n;
+  double* VEC = BF + nn;
+  double* PEN = VEC + nn;
+  double* Bt = PEN;             // pencil slot A1
+  double* Bti = VEC;            // consumed before the pencil writes VEC
+  double* Btj = PEN + 7 * nn;   // pencil slot T5
+  double* psw = PEN + nn;       // parallel-sum workspace: 5 n^2 + n from slot U
+  double* T = PEN + 2 * nn;     // scratch for B_F (slot A2)
   const int k0 = t.sh_start[g];
   const int si = t.sh_sub[k0], sj = t.sh_sub[k0 + 1];
   const double* Di = D + t.sh_doff[k0];
@@ -404,14 +414,14 @@ __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* _
     if (threadIdx.x == 0) o.status[g] = 101;
     return;
   }
-  parallel_sum(Bti, Btj, n, Bt, scratch, cs, perm, red);
+  parallel_sum(Bti, Btj, n, Bt, psw, cs, perm, red);
   double* vals = o.eig + o.eig_off[g];
-  st = pencil(BF, Bt, n, vals, vecs, degen, scratch, cs, perm, red);
+  st = pencil(BF, Bt, n, vals, VEC, degen, PEN, cs, perm, red);
   if (st) {
     if (threadIdx.x == 0) o.status[g] = 200 + st;
     return;
   }
-  // selected columns -> rows = (B_F V_sel)^T
+  // selected columns -> rows = (B_F V_sel)^T  (rows in pencil slot A1)
   __shared__ int s_nsel;
   if (threadIdx.x == 0) {
     int c = 0;
@@ -424,15 +434,16 @@ __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* _
   }
   __syncthreads();
   const int nsel = s_nsel;
+  double* rows = PEN;
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     int j = idx / n, c = idx - j * n;  // eigen column j, glob dof c
     if (perm[j] < 0) continue;
     double s = 0.0;
-    for (int k = 0; k < n; ++k) s += BF[c * n + k] * vecs[k * n + j];
+    for (int k = 0; k < n; ++k) s += BF[c * n + k] * VEC[k * n + j];
     rows[perm[j] * n + c] = s;
   }
   __syncthreads();
-  const int r = row_space_basis(rows, n, nsel, n, o.Q + o.q_off[g], scratch, cs, perm, red);
+  const int r = row_space_basis(rows, n, nsel, n, o.Q + o.q_off[g], PEN + nn, cs, perm, red);
   if (threadIdx.x == 0) {
     o.n_sel[g] = nsel;
     o.r[g] = r;
@@ -836,6 +847,13 @@ static GlobTables make_tables(const int* kind, const int* size, const int* sh_st
   return t;
 }
 
+constexpr int kFaceSmemBudget = 225 * 1024;
+
+static int face_small_bytes(int n) {
+  // cs 2(n+2) + red 32 + rowbuf 2(n+2) doubles, perm 2(n+2) + degen (n+2, even) ints
+  return (4 * (n + 2) + 32) * 8 + (2 * (n + 2) + ((n + 3) & ~1)) * 4 + 64;
+}
+
 static int shmem_for(int dim) {
   int bytes = (2 * (dim + 2) + 32 + 2 * (dim + 2)) * 8 + 2 * (dim + 2) * 4 + 64;
   return bytes;
@@ -843,7 +861,7 @@ static int shmem_for(int dim) {
 
 extern "C" {
 
-long long bddc_ws_face(long long n) { return bddc_face_ws(n); }
+long long bddc_ws_face(long long n) { return face_arena(n); }
 long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long nhmax) {
   return bddc_edge_new_ws(ns, ne, wd, nhmax);
 }
@@ -868,9 +886,12 @@ int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const 
   if (n_faces <= 0) return 0;
   GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, Binv);
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
-  const int smem = shmem_for(max_n);
+  const int small = face_small_bytes(max_n);
+  const long long arena = face_arena(max_n) * 8;
+  const int in_smem = (small + arena) <= kFaceSmemBudget;
+  const int smem = small + (in_smem ? (int)arena : 0);
   if (smem > 48 * 1024) cudaFuncSetAttribute(face_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  face_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids); bddc_note_launches(1);
+  face_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids, in_smem, max_n); bddc_note_launches(1);
   return glob_launch_status();
 }
 

@@ -60,48 +60,57 @@ __global__ void __launch_bounds__(256) pivot_inverse_kernel(
     const int* __restrict__ npiv, int k, double* __restrict__ pinv, long long pinv_stride,
     int* __restrict__ status, int require_positive, double* __restrict__ piv_out,
     long long piv_stride) {
-  __shared__ double P[kTile][kTile + 1];
-  __shared__ double prow[kTile];
-  __shared__ double pcol[kTile];
+  // Register-resident Gauss-Jordan: thread t owns column c = t % 64 and rows
+  // r0 + 4 j (r0 = t / 64, j < 16); the pivot row / column go through
+  // double-buffered shared memory, one barrier per pivot.
+  __shared__ double rowb[2][kTile];
+  __shared__ double colb[2][kTile];
   __shared__ int bad;
   const int b = blockIdx.x;
   const int w = min(kTile, npiv[b] - k);
   if (w <= 0) return;
-  const double* M = base + off[b] + (long long)k * ld[b] + k;
   const int L = ld[b];
-  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
-    int r = idx / w, c = idx - r * w;
-    P[r][c] = M[(long long)r * L + c];
+  const double* M = base + off[b] + (long long)k * L + k;
+  const int c = threadIdx.x & 63, r0 = threadIdx.x >> 6;
+  double a[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int r = r0 + 4 * j;
+    a[j] = (r < w && c < w) ? M[(long long)r * L + c] : (r == c ? 1.0 : 0.0);
   }
   if (threadIdx.x == 0) bad = 0;
-  __syncthreads();
   for (int p = 0; p < w; ++p) {
-    const double piv = P[p][p];
-    if (piv_out && threadIdx.x == 0) piv_out[(long long)b * piv_stride + k + p] = piv;
+    const int par = p & 1;
+    if ((p & 3) == r0) rowb[par][c] = a[p >> 2];
+    if (c == p) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) colb[par][r0 + 4 * j] = a[j];
+    }
+    __syncthreads();
+    const double piv = rowb[par][p];
+    const double ip = 1.0 / piv;
     if (threadIdx.x == 0) {
+      if (piv_out) piv_out[(long long)b * piv_stride + k + p] = piv;
       if (!(piv == piv) || piv == 0.0 || isinf(piv) || (require_positive && !(piv > 0.0))) bad = 1;
     }
-    const double ip = 1.0 / piv;
-    for (int c = threadIdx.x; c < w; c += blockDim.x) {
-      prow[c] = (c == p) ? ip : P[p][c] * ip;
-      pcol[c] = P[c][p];
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
-      int r = idx / w, c = idx - r * w;
+    const double rc = rowb[par][c] * ip;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int r = r0 + 4 * j;
       if (r == p) {
-        P[r][c] = prow[c];
+        a[j] = (c == p) ? ip : rc;
       } else {
-        const double f = pcol[r];
-        P[r][c] = (c == p) ? -f * ip : P[r][c] - f * prow[c];
+        const double f = colb[par][r];
+        a[j] = (c == p) ? -f * ip : a[j] - f * rc;
       }
     }
-    __syncthreads();
   }
+  __syncthreads();
   double* out = pinv + (long long)b * pinv_stride;
-  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
-    int r = idx / w, c = idx - r * w;
-    out[r * kTile + c] = P[r][c];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int r = r0 + 4 * j;
+    if (r < w && c < w) out[r * kTile + c] = a[j];
   }
   if (threadIdx.x == 0 && bad && status) atomicCAS(status + b, 0,
       require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
@@ -114,38 +123,40 @@ __global__ void __launch_bounds__(256) pivot_inverse_kernel(
 __global__ void __launch_bounds__(kTileThreads) schur_row_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ ncols, int k,
-    const double* __restrict__ pinv, long long pinv_stride) {
+    const double* __restrict__ pinv, long long pinv_stride, int lim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
   const int w = min(kTile, npiv[b] - k);
   if (w <= 0) return;
+  const int nc = min(ncols[b], lim);
   const int c0 = k + w + blockIdx.x * kTile;
-  if (c0 >= ncols[b]) return;
+  if (c0 >= nc) return;
   const int L = ld[b];
   double* C = base + off[b] + (long long)k * L + c0;
-  tile_mma(C, L, w, min(kTile, ncols[b] - c0), pinv + (long long)b * pinv_stride, kTile, C, L, w,
+  tile_mma(C, L, w, min(kTile, nc - c0), pinv + (long long)b * pinv_stride, kTile, C, L, w,
            1.0, 0.0, sm);
 }
 
 __global__ void __launch_bounds__(kTileThreads) schur_trailing_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ nrows, const int* __restrict__ ncols,
-    int k) {
+    int k, int lim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
   const int w = min(kTile, npiv[b] - k);
   if (w <= 0) return;
   const int s = k + w;
-  const int tn_count = (ncols[b] - s + kTile - 1) / kTile;
+  const int nr = min(nrows[b], lim), nc = min(ncols[b], lim);
+  const int tn_count = (nc - s + kTile - 1) / kTile;
   if (tn_count <= 0) return;
   const int tm = blockIdx.x / tn_count, tn = blockIdx.x - tm * tn_count;
   const int r0 = s + tm * kTile, c0 = s + tn * kTile;
-  if (r0 >= nrows[b]) return;
+  if (r0 >= nr) return;
   const int L = ld[b];
   double* M = base + off[b];
-  tile_mma(M + (long long)r0 * L + c0, L, min(kTile, nrows[b] - r0), min(kTile, ncols[b] - c0),
+  tile_mma(M + (long long)r0 * L + c0, L, min(kTile, nr - r0), min(kTile, nc - c0),
            M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm);
 }
 
@@ -352,13 +363,13 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
     const int rt = ceil_div(max_rows - k, kTile);
     if (ct > 0) {
       schur_row_kernel<<<dim3(ct, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
-                                                                        P, pinv_stride);
+                                                                        P, pinv_stride, 0x7fffffff);
       ++launches;
     }
     if (ct > 0 && rt > 0) {
       if (ev) cudaEventRecord(ev[2 * timed], stream);
       schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, smem, stream>>>(
-          M, off, ld, npiv, nrows, ncols, k);
+          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff);
       ++launches;
       if (ev) cudaEventRecord(ev[2 * timed + 1], stream);
       timed += (ev != nullptr);
@@ -397,6 +408,33 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
   return schur_eliminate_impl(M, off, ld, npiv, nrows, ncols, nbatch, max_npiv, max_rows,
                               max_cols, pinv_ws, pinv_stride, pinv_step_stride, status,
                               require_positive, piv_out, piv_stride, stream, host_trailing_ms);
+}
+
+// Envelope LU of one n x n matrix (the coarse problem in a bandwidth-reducing
+// order): panel k only updates rows / columns below host_lim[k / 64].
+int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const int* nv, int n,
+                       const int* host_lim, double* pinv, double* piv_out, int* status,
+                       cudaStream_t stream) {
+  if (n <= 0) return 0;
+  const int smem = smem_tile_setup();
+  int launches = 0;
+  for (int k = 0; k < n; k += kTile) {
+    const int step = k / kTile;
+    const int w = min(kTile, n - k);
+    const int lim = min(n, host_lim[step]);
+    double* P = pinv + (long long)step * kTile * kTile;
+    pivot_inverse_kernel<<<1, 256, 0, stream>>>(C, off, ldv, nv, k, P, 0, status, 0, piv_out, 0);
+    ++launches;
+    const int span = lim - k - w;
+    if (span > 0) {
+      const int t = ceil_div(span, kTile);
+      schur_row_kernel<<<dim3(t, 1), kTileThreads, smem, stream>>>(C, off, ldv, nv, nv, k, P, 0, lim);
+      schur_trailing_kernel<<<dim3(t * t, 1), kTileThreads, smem, stream>>>(C, off, ldv, nv, nv, nv, k, lim);
+      launches += 2;
+    }
+  }
+  bddc_note_launches(launches);
+  return launch_status();
 }
 
 int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n, int nbatch,

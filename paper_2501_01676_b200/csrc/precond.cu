@@ -77,6 +77,151 @@ __global__ void block_transform_kernel(SubGlobMap m, const double* __restrict__ 
   }
 }
 
+// Block-diagonal transforms, one CTA per (glob block, subdomain):
+//   left : out[blk, :] = L_blk * in[blk, :]
+//   right: out[:, blk] = in[:, blk] * L_blk^T
+// L_blk = Q_g (src 0) or TT_(g,s) = D_g^(s) Q_g^T (src 1).  in/out nB x nB.
+constexpr int kBT_COLS = 32;
+__global__ void __launch_bounds__(256) glob_block_kernel(SubGlobMap m,
+                                                         const int* __restrict__ sub_glob_start,
+                                                         const double* __restrict__ TT,
+                                                         const double* __restrict__ in,
+                                                         double* __restrict__ out, int src,
+                                                         int right, int max_ng) {
+  extern __shared__ double smb[];
+  const int b = blockIdx.y;
+  const int k = sub_glob_start[b] + blockIdx.x;
+  if (k >= sub_glob_start[b + 1]) return;
+  const int n = m.nB[b];
+  const int g = m.sub_globs[k];
+  const int bo = m.sub_glob_boff[k];
+  const int ng = m.gsize[g];
+  const double* L = src == 0 ? m.Q + m.q_off[g] : TT + m.sh_doff[m.sub_glob_sh[k]];
+  const double* X = in + m.soff[b];
+  double* Y = out + m.soff[b];
+  const bool lsm = ng <= 64;
+  double* Ls = smb;                       // ng x ng (when ng <= 64)
+  double* Xt = smb + (lsm ? 64 * 64 : 0);  // tile: ng x kBT_COLS (left) or kBT_COLS x ng (right)
+  if (lsm) {
+    for (int i = threadIdx.x; i < ng * ng; i += blockDim.x) Ls[i] = L[i];
+  }
+  const double* Lp = lsm ? Ls : L;
+  for (int t0 = 0; t0 < n; t0 += kBT_COLS) {
+    const int tw = min(kBT_COLS, n - t0);
+    __syncthreads();
+    if (!right) {
+      for (int i = threadIdx.x; i < ng * tw; i += blockDim.x) {
+        const int q = i / tw, c = i - q * tw;
+        Xt[q * kBT_COLS + c] = X[(long long)(bo + q) * n + t0 + c];
+      }
+    } else {
+      for (int i = threadIdx.x; i < tw * ng; i += blockDim.x) {
+        const int r = i / ng, q = i - r * ng;
+        Xt[r * max_ng + q] = X[(long long)(t0 + r) * n + bo + q];
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ng * tw; i += blockDim.x) {
+      double s = 0.0;
+      if (!right) {
+        const int r = i / tw, c = i - r * tw;
+        for (int q = 0; q < ng; ++q) s += Lp[r * ng + q] * Xt[q * kBT_COLS + c];
+        Y[(long long)(bo + r) * n + t0 + c] = s;
+      } else {
+        const int r = i / ng, c = i - r * ng;
+        for (int q = 0; q < ng; ++q) s += Xt[r * max_ng + q] * Lp[c * ng + q];
+        Y[(long long)(t0 + r) * n + bo + c] = s;
+      }
+    }
+  }
+}
+
+// Primal pieces, one CTA per subdomain, primal positions in chunks of kPC:
+//   MP[p][r] = d(r,pc) - (Z Sbar)[r][pc]     (warp per row r of Z, coalesced)
+//   RP[p][r] = d(r,pc) - (Sbar Z)[pc][r]     (thread per column r of Z, coalesced)
+//   C_i[p][q] = Sbar[pr, :] . MP[q, :]
+constexpr int kPC = 8;
+__global__ void __launch_bounds__(256) primal_pieces2_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ soff, const int* __restrict__ pstart,
+    const int* __restrict__ ppos, const long long* __restrict__ poff,
+    const double* __restrict__ Sbar, const double* __restrict__ Z, double* __restrict__ MP,
+    double* __restrict__ RP, double* __restrict__ Cl, const long long* __restrict__ coff,
+    int max_nB) {
+  extern __shared__ double smp[];
+  const int b = blockIdx.x;
+  const int n = nB[b];
+  const int p0 = pstart[b], np = pstart[b + 1] - p0;
+  if (np == 0) return;
+  const double* S = Sbar + soff[b];
+  const double* Zb = Z + soff[b];
+  double* M = MP + poff[b];
+  double* R = RP + poff[b];
+  double* Sc = smp;                   // kPC x max_nB: Sbar[:, pc]
+  double* Sr = smp + kPC * max_nB;    // kPC x max_nB: Sbar[pc, :]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c0 = 0; c0 < np; c0 += kPC) {
+    const int pc_n = min(kPC, np - c0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < pc_n * n; i += blockDim.x) {
+      const int p = i / n, k = i - p * n;
+      const int pc = ppos[p0 + c0 + p];
+      Sc[p * max_nB + k] = S[(long long)k * n + pc];
+      Sr[p * max_nB + k] = S[(long long)pc * n + k];
+    }
+    __syncthreads();
+    // MP: warp per row of Z
+    for (int r = warp; r < n; r += nw) {
+      double acc[kPC];
+#pragma unroll
+      for (int p = 0; p < kPC; ++p) acc[p] = 0.0;
+      const double* zr = Zb + (long long)r * n;
+      for (int k = lane; k < n; k += 32) {
+        const double z = zr[k];
+#pragma unroll
+        for (int p = 0; p < kPC; ++p)
+          if (p < pc_n) acc[p] += z * Sc[p * max_nB + k];
+      }
+#pragma unroll
+      for (int p = 0; p < kPC; ++p) {
+        double v = acc[p];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0 && p < pc_n) {
+          const int pc = ppos[p0 + c0 + p];
+          M[(long long)(c0 + p) * n + r] = (r == pc ? 1.0 : 0.0) - v;
+        }
+      }
+    }
+    // RP: thread per column of Z
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+      double acc[kPC];
+#pragma unroll
+      for (int p = 0; p < kPC; ++p) acc[p] = 0.0;
+      for (int k = 0; k < n; ++k) {
+        const double z = Zb[(long long)k * n + r];
+#pragma unroll
+        for (int p = 0; p < kPC; ++p)
+          if (p < pc_n) acc[p] += Sr[p * max_nB + k] * z;
+      }
+#pragma unroll
+      for (int p = 0; p < kPC; ++p)
+        if (p < pc_n) {
+          const int pc = ppos[p0 + c0 + p];
+          R[(long long)(c0 + p) * n + r] = (r == pc ? 1.0 : 0.0) - acc[p];
+        }
+    }
+  }
+  __syncthreads();
+  double* C = Cl + coff[b];
+  for (int i = warp; i < np * np; i += nw) {
+    const int p = i / np, q = i - p * np;
+    const int pr = ppos[p0 + p];
+    double v = 0.0;
+    for (int k = lane; k < n; k += 32) v += S[(long long)pr * n + k] * M[(long long)q * n + k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) C[i] = v;
+  }
+}
+
 // precompute TT blocks: TTb[(g,s)] = D_g^(s) Q_g^T  (so T^T blocks), per sharer slot
 __global__ void ttblock_kernel(const int* __restrict__ slot_glob, const int* __restrict__ gsize,
                                const double* __restrict__ Q, const long long* __restrict__ q_off,
@@ -330,21 +475,30 @@ __global__ void __launch_bounds__(256) coarse_fwd_kernel(const double* __restric
                                                          const double* __restrict__ Pk,
                                                          double* __restrict__ b,
                                                          double* __restrict__ t) {
+  // n here is the row limit of this panel (envelope); n >= k + w
+  __shared__ double Ps[64][65];
+  __shared__ double bk[64];
   __shared__ double tk[64];
   const int w = min(64, n - k);
-  // every CTA recomputes t_k = P_k b_k (64 x 64)
-  for (int r = threadIdx.x; r < w; r += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < w; ++c) s += Pk[r * 64 + c] * b[k + c];
-    tk[r] = s;
+  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
+    const int r = i >> 6, c = i & 63;
+    Ps[r][c] = (r < w && c < w) ? Pk[i] : 0.0;
+  }
+  if (threadIdx.x < 64) bk[threadIdx.x] = threadIdx.x < w ? b[k + threadIdx.x] : 0.0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // t_k = P_k b_k : warp per row, 2 columns per lane
+  for (int r = warp; r < w; r += 8) {
+    double s = Ps[r][lane] * bk[lane] + Ps[r][lane + 32] * bk[lane + 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) tk[r] = s;
   }
   __syncthreads();
   if (blockIdx.x == 0)
     for (int r = threadIdx.x; r < w; r += blockDim.x) t[k + r] = tk[r];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rows_per_cta = 64;
-  const int i0 = k + w + blockIdx.x * rows_per_cta;
-  for (int i = i0 + warp; i < min(n, i0 + rows_per_cta); i += 8) {
+  const int i0 = k + w + blockIdx.x * 32;
+  for (int i = i0 + warp; i < min(n, i0 + 32); i += 8) {
     const double* row = A + (long long)i * ld + k;
     double s = 0.0;
     for (int c = lane; c < w; c += 32) s += row[c] * tk[c];
@@ -355,14 +509,15 @@ __global__ void __launch_bounds__(256) coarse_fwd_kernel(const double* __restric
 }
 
 __global__ void __launch_bounds__(256) coarse_bwd_kernel(const double* __restrict__ A, long long ld,
-                                                         int n, int k, double* __restrict__ t) {
+                                                         int n, int k, int first,
+                                                         double* __restrict__ t) {
   __shared__ double xk[64];
   const int w = min(64, n - k);
-  for (int r = threadIdx.x; r < w; r += blockDim.x) xk[r] = t[k + r];
+  if (threadIdx.x < 64) xk[threadIdx.x] = threadIdx.x < w ? t[k + threadIdx.x] : 0.0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i0 = blockIdx.x * 64;
-  for (int i = i0 + warp; i < min(k, i0 + 64); i += 8) {
+  const int i0 = first + blockIdx.x * 32;
+  for (int i = i0 + warp; i < min(k, i0 + 32); i += 8) {
     const double* row = A + (long long)i * ld + k;
     double s = 0.0;
     for (int c = lane; c < w; c += 32) s += row[c] * xk[c];
@@ -397,17 +552,25 @@ static SubGlobMap make_map(const int* nB, const long long* soff, const long long
 
 extern "C" {
 
+static int glob_block_smem(int max_ng) {
+  return (64 * 64 + (max_ng > kBT_COLS ? max_ng : kBT_COLS) * kBT_COLS) * (int)sizeof(double);
+}
+
 // Sbar = Qi S Qi^T (via tmp)
 int bddc_pc_transform_schur(const int* nB, const long long* soff, const long long* voff,
                             const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
                             const int* sub_glob_sh, const int* gsize, const double* Q,
-                            const long long* q_off, const double* S, double* tmp, double* Sbar,
-                            int nbatch, cudaStream_t stream) {
+                            const long long* q_off, const int* sub_glob_start, int max_globs,
+                            int max_ng, const double* S, double* tmp, double* Sbar, int nbatch,
+                            cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   SubGlobMap m = make_map(nB, soff, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize, Q,
                           q_off, nullptr, nullptr);
-  block_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, S, tmp, 0, 0); bddc_note_launches(1);
-  block_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, tmp, Sbar, 0, 1); bddc_note_launches(1);
+  const int smem = glob_block_smem(max_ng);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(glob_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  glob_block_kernel<<<dim3(max_globs, nbatch), 256, smem, stream>>>(m, sub_glob_start, nullptr, S, tmp, 0, 0, max_ng);
+  glob_block_kernel<<<dim3(max_globs, nbatch), 256, smem, stream>>>(m, sub_glob_start, nullptr, tmp, Sbar, 0, 1, max_ng);
+  bddc_note_launches(2);
   return pc_status();
 }
 
@@ -436,30 +599,34 @@ int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* v
   return pc_status();
 }
 
-// A = T^T Z T with T^T blocks TT: Y = Z * TT^T... see DESIGN.md
+// A = TT_blockdiag Z TT_blockdiag^T  (= T^T Z T with T = blockdiag(Q_g D_g^T))
 int bddc_pc_local_operator(const int* nB, const long long* soff, const long long* voff,
                            const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
                            const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
-                           const double* TT, const double* Z, double* tmp, double* A, int nbatch,
+                           const int* sub_glob_start, int max_globs, int max_ng, const double* TT,
+                           const double* Z, double* tmp, double* A, int nbatch,
                            cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   SubGlobMap m = make_map(nB, soff, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
                           nullptr, nullptr, nullptr, sh_doff);
-  // T = blockdiag(Q D^T) = blockdiag(TT^T).  Y = Z T: right multiply by L^T with L = TT
-  //   (in * L^T)[r][c] = sum_q in[r][bo+q] * L[c'][q]  with L = TT (transpose_block = 0)
-  tt_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, TT, Z, tmp, 1, 0); bddc_note_launches(1);
-  // A = T^T Y = TT Y: left multiply with L = TT
-  tt_transform_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(m, TT, tmp, A, 0, 0); bddc_note_launches(1);
+  const int smem = glob_block_smem(max_ng);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(glob_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  glob_block_kernel<<<dim3(max_globs, nbatch), 256, smem, stream>>>(m, sub_glob_start, TT, Z, tmp, 1, 1, max_ng);
+  glob_block_kernel<<<dim3(max_globs, nbatch), 256, smem, stream>>>(m, sub_glob_start, TT, tmp, A, 1, 0, max_ng);
+  bddc_note_launches(2);
   return pc_status();
 }
 
 int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstart,
                           const int* ppos, const long long* poff, const double* Sbar,
                           const double* Z, double* MP, double* RP, double* Cl,
-                          const long long* coff, int nbatch, cudaStream_t stream) {
+                          const long long* coff, int nbatch, int max_nB, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  primal_pieces_kernel<<<nbatch, 256, 0, stream>>>(nB, soff, pstart, ppos, poff, Sbar, Z, MP, RP,
-                                                   Cl, coff); bddc_note_launches(1);
+  const int smem = 2 * kPC * max_nB * (int)sizeof(double);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(primal_pieces2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  primal_pieces2_kernel<<<nbatch, 256, smem, stream>>>(nB, soff, pstart, ppos, poff, Sbar, Z, MP, RP,
+                                                       Cl, coff, max_nB);
+  bddc_note_launches(1);
   return pc_status();
 }
 
@@ -519,17 +686,25 @@ int bddc_gather_reduce(const long long* tstart, const long long* tsrc, const dou
 }
 
 int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
-                      long long pinv_step_stride, double* b, double* t, cudaStream_t stream) {
+                      long long pinv_step_stride, const int* host_lim, const int* host_first,
+                      double* b, double* t, cudaStream_t stream) {
   if (n <= 0) return 0;
+  int launches = 0;
   for (int k = 0; k < n; k += 64) {
     const int w = min(64, n - k);
-    const int blocks = max(1, ceil_div(n - k - w, 64));
-    coarse_fwd_kernel<<<blocks, 256, 0, stream>>>(A, ld, n, k, pinv + (long long)(k / 64) * pinv_step_stride, b, t); bddc_note_launches(1);
+    const int lim = host_lim ? min(n, host_lim[k / 64]) : n;
+    const int blocks = max(1, ceil_div(lim - k - w, 32));
+    coarse_fwd_kernel<<<blocks, 256, 0, stream>>>(A, ld, lim, k, pinv + (long long)(k / 64) * pinv_step_stride, b, t);
+    ++launches;
   }
   const int last = ((n - 1) / 64) * 64;
   for (int k = last; k > 0; k -= 64) {
-    coarse_bwd_kernel<<<ceil_div(k, 64), 256, 0, stream>>>(A, ld, n, k, t); bddc_note_launches(1);
+    const int first = host_first ? max(0, host_first[k / 64]) : 0;
+    if (first >= k) continue;
+    coarse_bwd_kernel<<<ceil_div(k - first, 32), 256, 0, stream>>>(A, ld, n, k, first, t);
+    ++launches;
   }
+  bddc_note_launches(launches);
   return pc_status();
 }
 

@@ -2,58 +2,134 @@
 //
 // One CTA of 128 threads (2x2 warps, 32x32 per warp = 4x4 DMMA tiles)
 // computes   C[m x n] = beta*C + alpha * A[m x K] * B[K x n]   with
-// m, n <= 64 and K <= 64.  A and B are staged whole into shared memory
-// (row stride 68 doubles: conflict-free DMMA fragment loads), so B may alias
-// C when one CTA owns every row of that C tile (in-place W = P*W updates).
+// m, n <= 64 and K <= 64.  A and B stream through shared memory in K-chunks
+// of 16 with a 3-stage cp.async pipeline (16-byte copies when the source is
+// 16-byte aligned, 8-byte otherwise; out-of-range elements zero-filled); the
+// accumulators start from (beta/alpha)*C so C is read once, early.  B may
+// alias C when one CTA owns every row of that C tile and beta == 0
+// (in-place W = P*W updates): all of B is read before the epilogue writes.
 #pragma once
 #include "common.cuh"
 
 namespace bddc {
 
 constexpr int kTile = 64;
-constexpr int kTileStride = 68;
 constexpr int kTileThreads = 128;
+constexpr int kKC = 16;          // K chunk
+constexpr int kStages = 3;
+constexpr int kAS = kKC + 4;     // A smem row stride (doubles): conflict-free fragments
+constexpr int kBS = kTile + 4;   // B smem row stride
 
 struct TileSmem {
-  double A[kTile][kTileStride];
-  double B[kTile][kTileStride];
+  double A[kStages][kTile][kAS];
+  double B[kStages][kKC][kBS];
 };
 
-// Cooperative fill of a 64 x K4 tile from a row-major source, zero padded.
-BDDC_DEV void tile_load(double (*dst)[kTileStride], const double* src, long long ld, int rows,
-                        int cols, int rows_pad, int cols_pad) {
-  for (int idx = threadIdx.x; idx < rows_pad * cols_pad; idx += kTileThreads) {
-    int r = idx / cols_pad, c = idx - r * cols_pad;
-    dst[r][c] = (r < rows && c < cols) ? src[(long long)r * ld + c] : 0.0;
+BDDC_DEV void cp_async8(double* dst, const double* src, bool valid) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+
+BDDC_DEV void cp_async16(double* dst, const double* src, int valid_doubles) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(src),
+               "r"(valid_doubles * 8));
+}
+
+BDDC_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+BDDC_DEV void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// async load of K-chunk `kc` of A (64 x kKC) and B (kKC x 64) into stage `st`
+BDDC_DEV void tile_issue_chunk(TileSmem& sm, int st, int kc, const double* A, long long lda,
+                               const double* B, long long ldb, int m, int n, int K, bool a16,
+                               bool b16) {
+  const int k0 = kc * kKC;
+  if (a16) {
+    for (int idx = threadIdx.x; idx < kTile * (kKC / 2); idx += kTileThreads) {
+      const int r = idx / (kKC / 2), c = (idx - r * (kKC / 2)) * 2;
+      const int kk = k0 + c;
+      int valid = (r < m) ? max(0, min(2, K - kk)) : 0;
+      const double* src = valid ? A + (long long)r * lda + kk : A;
+      cp_async16(&sm.A[st][r][c], src, valid);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < kTile * kKC; idx += kTileThreads) {
+      const int r = idx / kKC, c = idx - r * kKC;
+      const bool valid = r < m && k0 + c < K;
+      cp_async8(&sm.A[st][r][c], valid ? A + (long long)r * lda + k0 + c : A, valid);
+    }
+  }
+  if (b16) {
+    for (int idx = threadIdx.x; idx < kKC * (kTile / 2); idx += kTileThreads) {
+      const int r = idx / (kTile / 2), c = (idx - r * (kTile / 2)) * 2;
+      int valid = (k0 + r < K) ? max(0, min(2, n - c)) : 0;
+      const double* src = valid ? B + (long long)(k0 + r) * ldb + c : B;
+      cp_async16(&sm.B[st][r][c], src, valid);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < kKC * kTile; idx += kTileThreads) {
+      const int r = idx / kTile, c = idx - r * kTile;
+      const bool valid = k0 + r < K && c < n;
+      cp_async8(&sm.B[st][r][c], valid ? B + (long long)(k0 + r) * ldb + c : B, valid);
+    }
   }
 }
 
 BDDC_DEV void tile_mma(double* C, long long ldc, int m, int n, const double* A, long long lda,
                        const double* B, long long ldb, int K, double alpha, double beta,
                        TileSmem& sm) {
-  const int K4 = (K + 3) & ~3;
-  tile_load(sm.A, A, lda, m, K, kTile, K4);
-  tile_load(sm.B, B, ldb, K, n, K4, kTile);
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
-  double acc[4][4][2];
+  const int nchunks = (K + kKC - 1) / kKC;
+  const bool a16 = ((reinterpret_cast<uintptr_t>(A) | (uintptr_t)(lda * 8)) & 15) == 0;
+  const bool b16 = ((reinterpret_cast<uintptr_t>(B) | (uintptr_t)(ldb * 8)) & 15) == 0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int k0 = 0; k0 < K4; k0 += 4) {
-    double a[4], b[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = sm.A[wm + i * 8 + g][k0 + t];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = sm.B[k0 + t][wn + j * 8 + g];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nchunks) tile_issue_chunk(sm, s, s, A, lda, B, ldb, m, n, K, a16, b16);
+    cp_async_commit();
   }
+  // accumulators start from (beta/alpha) C
+  double acc[4][4][2];
+  const double cscale = (beta != 0.0) ? beta / alpha : 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = wm + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = wn + j * 8 + 2 * t;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        acc[i][j][h] = (cscale != 0.0 && r < m && c + h < n) ? cscale * C[(long long)r * ldc + c + h] : 0.0;
+    }
+  }
+  for (int kc = 0; kc < nchunks; ++kc) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    const int nxt = kc + kStages - 1;
+    if (nxt < nchunks) tile_issue_chunk(sm, nxt % kStages, nxt, A, lda, B, ldb, m, n, K, a16, b16);
+    cp_async_commit();
+    const int st = kc % kStages;
+    const int kmax = min(kKC, K - kc * kKC);
+    for (int k0 = 0; k0 < kmax; k0 += 4) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = sm.A[st][wm + i * 8 + g][k0 + t];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = sm.B[st][k0 + t][wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // every read of B (which may alias C) is done
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = wm + i * 8 + g;
@@ -63,13 +139,8 @@ BDDC_DEV void tile_mma(double* C, long long ldc, int m, int n, const double* A, 
     for (int j = 0; j < 4; ++j) {
       const int c = wn + j * 8 + 2 * t;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (c + h < n) {
-          double v = alpha * acc[i][j][h];
-          if (beta != 0.0) v += beta * crow[c + h];
-          crow[c + h] = v;
-        }
-      }
+      for (int h = 0; h < 2; ++h)
+        if (c + h < n) crow[c + h] = alpha * acc[i][j][h];
     }
   }
 }

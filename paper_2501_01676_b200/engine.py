@@ -250,6 +250,22 @@ class DeviceScaling:
 # ---------------------------------------------------------------------------
 
 def _face_ws(n):
+    """face_arena() in csrc/globs.cu"""
+    n = np.asarray(n, dtype=np.int64)
+    return 10 * n * n + 3 * n + 32
+
+
+def _face_smem_bytes(n):
+    """face_small_bytes() + face_arena() bytes in csrc/globs.cu"""
+    n = np.asarray(n, dtype=np.int64)
+    small = (4 * (n + 2) + 32) * 8 + (2 * (n + 2) + ((n + 3) & ~1)) * 4 + 64
+    return small + 8 * _face_ws(n)
+
+
+FACE_SMEM_BUDGET = 225 * 1024
+
+
+def _edge_old_ws(n):
     n = np.asarray(n, dtype=np.int64)
     sc = np.maximum(8 * n * n + 3 * n, _rowspace_ws(n, n))
     return 7 * n * n + n + sc + 64
@@ -307,17 +323,24 @@ class DevicePrimalSpace:
         faces = np.flatnonzero(kind == 0)
         edges = np.flatnonzero(kind == 1)
         if faces.size:
-            wsz = _face_ws(p.gsize[faces])
-            woff = np.zeros(G + 1, dtype=np.int64)
-            woff[faces] = _excl(wsz)[:-1]
-            ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
-            lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, d.nB,
-                               d.soff, ls.Bsym, Binv, scaling.D, self.theta_f, self.eig, d_eig_off,
-                               self.n_sel, self.r, self.Q, self.d_q_off, status, ws,
-                               dev_i64(woff[:-1]), dev_i32(faces), faces.size,
-                               int(p.gsize[faces].max()), st)
+            small = _face_smem_bytes(p.gsize[faces]) <= FACE_SMEM_BUDGET
+            for grp, in_smem in ((faces[small], True), (faces[~small], False)):
+                if not grp.size:
+                    continue
+                if in_smem:
+                    ws, woff = torch.empty(1, dtype=F64, device="cuda"), np.zeros(G + 1, np.int64)
+                else:
+                    wsz = _face_ws(p.gsize[grp])
+                    woff = np.zeros(G + 1, dtype=np.int64)
+                    woff[grp] = _excl(wsz)[:-1]
+                    ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
+                lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
+                                   d.nB, d.soff, ls.Bsym, Binv, scaling.D, self.theta_f, self.eig,
+                                   d_eig_off, self.n_sel, self.r, self.Q, self.d_q_off, status, ws,
+                                   dev_i64(woff[:-1]), dev_i32(grp), grp.size,
+                                   int(p.gsize[grp].max()), st)
+                del ws
             self._raise(status, "face")
-            del ws
         r_host = self.r.cpu().numpy()
         if edges.size and variant == "new":
             # prior sizes per subdomain: vertices + leading r_F of each face
@@ -352,7 +375,7 @@ class DevicePrimalSpace:
             self._raise(status, "edge")
             del ws, PB, XHH
         elif edges.size:
-            wsz = _face_ws(p.gsize[edges])
+            wsz = _edge_old_ws(p.gsize[edges])
             woff = np.zeros(G + 1, dtype=np.int64)
             woff[edges] = _excl(wsz)[:-1]
             ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
@@ -403,6 +426,41 @@ class DevicePrimalSpace:
 # preconditioner
 # ---------------------------------------------------------------------------
 
+def coarse_ordering(pgid, np_sub, n_c):
+    """Reverse Cuthill-McKee order of the coarse coupling graph and the
+    envelope of the reordered matrix in 64-wide panels.
+
+    Returns (order, new_id, lim, first): order[new] = old primal id;
+    lim[p] = 1 + last row touched by panel p's eliminations; first[p] =
+    first row of panel p's upper envelope (for the backward solve)."""
+    import scipy.sparse as sp
+    from scipy.sparse.csgraph import reverse_cuthill_mckee
+
+    N = np_sub.size
+    sub_of = np.repeat(np.arange(N, dtype=np.int64), np_sub)
+    inc = sp.csr_matrix((np.ones(pgid.size), (pgid, sub_of)), shape=(n_c, N))
+    adj = (inc @ inc.T).tocsr()
+    order = np.asarray(reverse_cuthill_mckee(adj, symmetric_mode=True), dtype=np.int64)
+    new_id = np.empty(n_c, dtype=np.int64)
+    new_id[order] = np.arange(n_c)
+    pg = new_id[pgid]
+    starts = np.concatenate([[0], np.cumsum(np_sub)[:-1]]).astype(np.int64)
+    nz = np_sub > 0
+    cmin = np.full(N, n_c, dtype=np.int64)
+    cmin[nz] = np.minimum.reduceat(pg, starts[nz])
+    fc = np.arange(n_c, dtype=np.int64)
+    np.minimum.at(fc, pg, np.repeat(cmin, np_sub))
+    steps = (n_c + 63) // 64
+    pan = fc // 64
+    last = np.full(steps, -1, dtype=np.int64)
+    np.maximum.at(last, pan, np.arange(n_c, dtype=np.int64))
+    lim = np.maximum.accumulate(last) + 1
+    lim = np.maximum(lim, np.minimum(np.arange(1, steps + 1) * 64, n_c))
+    # W = P_k A12 mixes the rows of a panel: the upper envelope is panel-granular
+    first = (np.minimum.reduceat(fc, np.arange(0, n_c, 64)) // 64) * 64
+    return order, new_id, lim.astype(np.int32), first.astype(np.int32)
+
+
 class DevicePreconditioner:
     """M^-1 = sum_i R_i^T (A_i R_i + N_i P_i C^-1 sum_j P_j^T G_j R_j)
     (reference BddcPreconditioner solver.py:46-209, see precond.cu)."""
@@ -422,7 +480,12 @@ class DevicePreconditioner:
         self.np_sub = np.where(np.diff(p.sub_glob_start) > 0, self.np_sub, 0)
         pstart = _excl(self.np_sub)
         ppos = _ranges(p.sub_glob_boff, cnt)
-        pgid = _ranges(go[:-1][p.sub_globs], cnt)
+        pgid0 = _ranges(go[:-1][p.sub_globs], cnt)
+        # coarse dofs in reverse Cuthill-McKee order of the primal coupling graph
+        # (each subdomain's primal set is a clique) -> envelope LU / solves
+        self.corder, new_id, self.lim, self.first = coarse_ordering(pgid0, self.np_sub, self.n_primal)
+        self.new_id = new_id
+        pgid = new_id[pgid0]
         mask = np.zeros(int(p.voff[-1]), dtype=np.uint8)
         psub = np.repeat(np.arange(p.N), self.np_sub)
         mask[p.voff[psub] + ppos] = 1
@@ -441,8 +504,11 @@ class DevicePreconditioner:
                              int(p.sh_sub.size), st)
         Sbar = torch.empty(p.S_total, dtype=F64, device="cuda")
         tmp = torch.empty(p.S_total, dtype=F64, device="cuda")
+        max_globs = int(np.diff(p.sub_glob_start).max())
+        max_ng = int(p.gsize.max())
         lib.bddc_pc_transform_schur(d.nB, d.soff, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
-                                    d.sub_glob_sh, d.gsize, Q, q_off, ls.S, tmp, Sbar, p.N, st)
+                                    d.sub_glob_sh, d.gsize, Q, q_off, d.sub_glob_start, max_globs,
+                                    max_ng, ls.S, tmp, Sbar, p.N, st)
         Z = torch.empty(p.S_total, dtype=F64, device="cuda")
         lib.bddc_pc_dual_embed(d.nB, d.soff, d.voff, d_mask, Sbar, Z, tmp, p.N, st)
         # certificate: LDL^T of sym(Sbar_dd) must have positive pivots (solver.py:91-98)
@@ -461,13 +527,14 @@ class DevicePreconditioner:
         lib.bddc_pc_zero_primal(d.nB, d.soff, d.voff, d_mask, Z, p.N, st)
         self.A = torch.empty(p.S_total, dtype=F64, device="cuda")
         lib.bddc_pc_local_operator(d.nB, d.soff, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
-                                   d.sub_glob_sh, d.gsize, d.sh_doff, TT, Z, tmp, self.A, p.N, st)
+                                   d.sub_glob_sh, d.gsize, d.sh_doff, d.sub_glob_start, max_globs,
+                                   max_ng, TT, Z, tmp, self.A, p.N, st)
         npn = max(int(poff[-1]), 1)
         MP = torch.empty(npn, dtype=F64, device="cuda")
         RP = torch.empty(npn, dtype=F64, device="cuda")
         Cl = torch.empty(max(int(coff[-1]), 1), dtype=F64, device="cuda")
         lib.bddc_pc_primal_pieces(d.nB, d.soff, self.d_pstart, self.d_ppos, self.d_poff, Sbar, Z,
-                                  MP, RP, Cl, d_coff, p.N, st)
+                                  MP, RP, Cl, d_coff, p.N, nbmax, st)
         self.G = torch.empty(npn, dtype=F64, device="cuda")
         self.Nt = torch.empty(npn, dtype=F64, device="cuda")
         lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
@@ -481,18 +548,25 @@ class DevicePreconditioner:
         C = torch.zeros(nc * nc, dtype=F64, device="cuda")
         lib.bddc_coarse_scatter(self.d_pstart, self.d_pgid, Cl, d_coff, C, nc, p.N, st)
         del Cl
-        self.coarse = C.view(nc, nc).cpu().numpy().copy() if nc <= keep_coarse else None
+        if nc <= keep_coarse:
+            Cn = C.view(nc, nc).cpu().numpy()
+            self.coarse = Cn[np.ix_(new_id, new_id)].copy()
+        else:
+            self.coarse = None
         steps = (nc + 63) // 64
         self.coarse_pinv = torch.empty(steps * 4096, dtype=F64, device="cuda")
         piv = torch.zeros(nc, dtype=F64, device="cuda")
-        one_i64, nc_i32 = dev_i64([0]), dev_i32([nc])
         status1 = torch.zeros(1, dtype=torch.int32, device="cuda")
-        lib.bddc_schur_eliminate(C, one_i64, nc_i32, nc_i32, nc_i32, nc_i32, 1, nc, nc, nc,
-                                 self.coarse_pinv, 4096, 4096, status1, 0, piv, nc, st)
+        self._lim_c = (ctypes.c_int * steps)(*self.lim.tolist())
+        self._first_c = (ctypes.c_int * steps)(*self.first.tolist())
+        lib.bddc_coarse_factor(C, dev_i64([0]), dev_i32([nc]), dev_i32([nc]), nc,
+                               ctypes.cast(self._lim_c, ctypes.c_void_p), self.coarse_pinv, piv,
+                               status1, st)
         self.coarse_lu = C
         dg = np.abs(piv.cpu().numpy())
         if dg.size and (dg.min() <= 1e-14 * max(dg.max(), 1.0) or not np.all(np.isfinite(dg))):
-            bad = int(np.argmin(np.where(np.isfinite(dg), dg, 0.0)))
+            bad_new = int(np.argmin(np.where(np.isfinite(dg), dg, 0.0)))
+            bad = int(self.corder[bad_new])
             gi = int(np.searchsorted(go[:-1], bad, side="right")) - 1
             gid = ls.globs.glob_id(ls.globs.globs[gi])
             raise NumericalError(f"coarse matrix is singular at primal dof {bad} "
@@ -511,7 +585,8 @@ class DevicePreconditioner:
                             self.d_poff, self.G, self.cvals, p.N, nbmax, 2, st)
         lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp, self.n_primal, st)
         lib.bddc_coarse_solve(self.coarse_lu, self.n_primal, self.n_primal, self.coarse_pinv, 4096,
-                              self.rp, self.up, st)
+                              ctypes.cast(self._lim_c, ctypes.c_void_p),
+                              ctypes.cast(self._first_c, ctypes.c_void_p), self.rp, self.up, st)
         lib.bddc_prolong_primal(d.nB, d.voff, self.d_pstart, self.d_pgid, self.d_poff, self.Nt,
                                 self.up, self.y, p.N, st)
         lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n_hat, st)

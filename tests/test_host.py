@@ -1,0 +1,130 @@
+"""CPU tests of the host side: C-ABI exports, symbolic plan, coarse ordering
+and envelope (no GPU needed)."""
+
+import ctypes
+import subprocess
+
+import numpy as np
+import pytest
+
+from tests.cases import inputs
+
+
+def test_library_exports_header():
+    from paper_2501_01676_b200 import build
+    from paper_2501_01676_b200._lib import LIB_PATH, parse_header
+
+    build.build()
+    sigs = parse_header()
+    assert len(sigs) >= 30
+    dll = ctypes.CDLL(LIB_PATH)  # loads without a GPU
+    out = subprocess.check_output(["nm", "-D", "--defined-only", LIB_PATH]).decode()
+    exported = {ln.split()[-1] for ln in out.splitlines()}
+    missing = [name for name in sigs if name not in exported]
+    assert missing == []
+    for name in sigs:
+        getattr(dll, name)
+
+
+def test_workspace_formulas_match_library():
+    from paper_2501_01676_b200 import build, engine
+    from paper_2501_01676_b200._lib import LIB_PATH
+
+    build.build()
+    dll = ctypes.CDLL(LIB_PATH)
+    dll.bddc_ws_face.restype = ctypes.c_longlong
+    dll.bddc_ws_face.argtypes = [ctypes.c_longlong]
+    dll.bddc_ws_edge_new.restype = ctypes.c_longlong
+    dll.bddc_ws_edge_new.argtypes = [ctypes.c_longlong] * 4
+    for n in (1, 7, 49, 193):
+        assert dll.bddc_ws_face(n) == int(engine._face_ws(n))
+    for ns, ne, wd, h in ((2, 7, 30, 8), (4, 7, 80, 14), (3, 20, 700, 150)):
+        assert dll.bddc_ws_edge_new(ns, ne, wd, h) == int(engine._edge_new_ws(ns, ne, wd, h))
+
+
+@pytest.mark.parametrize("name", ["jump", "cfg1", "cfg4_small"])
+def test_plan_local_numbering(name):
+    from paper_2501_01676_b200.plan import Plan
+
+    system, part, globs = inputs(name)
+    p = Plan(system, part, globs)
+    el = system.mesh.elements
+    for i in range(p.N):
+        elems = np.flatnonzero(part.subdomain_of == i)
+        nodes = np.unique(el[elems])
+        free = system.node_to_free[nodes] >= 0
+        iface = np.isin(nodes, globs.interface_nodes)
+        ref_B = np.sort(nodes[free & iface])
+        ref_I = nodes[free & ~iface]
+        B = p.B_nodes[p.voff[i]:p.voff[i + 1]]
+        assert np.array_equal(np.sort(B), ref_B)
+        assert np.array_equal(p.I_nodes[p.ioff[i]:p.ioff[i + 1]], ref_I)
+        # glob-major: every glob of the subdomain is one contiguous block
+        for k in range(p.sub_glob_start[i], p.sub_glob_start[i + 1]):
+            g = globs.globs[p.sub_globs[k]]
+            bo = p.sub_glob_boff[k]
+            assert np.array_equal(B[bo:bo + g.size], g.nodes)
+        # element-local indices point at the right nodes
+        e0, e1 = p.elem_start[i], p.elem_start[i + 1]
+        ids = p.elem_ids[e0:e1]
+        order = np.concatenate([ref_I, B])
+        loc = p.loc4[e0:e1]
+        conn = el[ids]
+        inside = loc < p.nL[i]
+        assert np.array_equal(order[loc[inside]], conn[inside])
+        assert np.all(system.node_to_free[conn[~inside]] < 0)
+    # interface CSR covers every local interface entry once
+    assert p.tstart[-1] == p.voff[-1]
+    assert np.array_equal(np.sort(p.tsrc), np.arange(p.voff[-1]))
+
+
+def _envelope_solve(C, lim, first):
+    n = C.shape[0]
+    A = C.copy()
+    P = []
+    for k in range(0, n, 64):
+        w = min(64, n - k)
+        L = min(n, lim[k // 64])
+        Pk = np.linalg.inv(A[k:k + w, k:k + w])
+        P.append(Pk)
+        A[k:k + w, k + w:L] = Pk @ A[k:k + w, k + w:L]
+        A[k + w:L, k + w:L] -= A[k + w:L, k:k + w] @ A[k:k + w, k + w:L]
+    return A, P
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_coarse_envelope_exact(seed):
+    """The coarse envelope LU / solve schedule (engine.coarse_ordering,
+    csrc coarse_factor / coarse_solve) equals a dense solve."""
+    from paper_2501_01676_b200.engine import coarse_ordering
+
+    rng = np.random.default_rng(seed)
+    N, n_c = 64, 300 + 70 * seed
+    np_sub = rng.integers(3, 12, size=N)
+    pgid = np.concatenate([rng.choice(n_c, size=k, replace=False) for k in np_sub])
+    pgid = np.concatenate([pgid, np.arange(n_c)])
+    np_sub = np.concatenate([np_sub, np.ones(n_c, dtype=np.int64)])
+    C = np.zeros((n_c, n_c))
+    off = 0
+    for k in np_sub:
+        g = pgid[off:off + k]
+        off += k
+        X = rng.standard_normal((k, k))
+        C[np.ix_(g, g)] += X @ X.T + k * np.eye(k) + 0.3 * (X - X.T)
+    order, new_id, lim, first = coarse_ordering(pgid, np_sub, n_c)
+    assert np.array_equal(order[new_id], np.arange(n_c))
+    Cn = C[np.ix_(order, order)]
+    A, P = _envelope_solve(Cn, lim, first)
+    b = rng.standard_normal(n_c)
+    bb, t = b.copy(), np.zeros(n_c)
+    for k in range(0, n_c, 64):
+        w = min(64, n_c - k)
+        L = min(n_c, lim[k // 64])
+        t[k:k + w] = P[k // 64] @ bb[k:k + w]
+        bb[k + w:L] -= A[k + w:L, k:k + w] @ t[k:k + w]
+    for k in range(((n_c - 1) // 64) * 64, 0, -64):
+        w = min(64, n_c - k)
+        f = first[k // 64]
+        t[f:k] -= A[f:k, k:k + w] @ t[k:k + w]
+    x = np.linalg.solve(Cn, b)
+    assert np.abs(t - x).max() <= 1e-12 * np.abs(x).max()
