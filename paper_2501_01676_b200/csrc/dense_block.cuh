@@ -167,6 +167,21 @@ BDDC_DEV void chol_solve(const double* L, int ld, int n, double* B, int ldb, int
   }
 }
 
+// Forward substitution in place: B <- L^-1 B (L lower triangular, n x n; B n x nrhs).
+BDDC_DEV void trsm_lower(const double* L, int ld, int n, double* B, int ldb, int nrhs) {
+  for (int j = 0; j < n; ++j) {
+    const double d = L[j * ld + j];
+    for (int c = tid(); c < nrhs; c += nth()) B[j * ldb + c] /= d;
+    __syncthreads();
+    const int m = n - j - 1;
+    for (int idx = tid(); idx < m * nrhs; idx += nth()) {
+      int r = j + 1 + idx / nrhs, c = idx % nrhs;
+      B[r * ldb + c] -= L[r * ld + j] * B[j * ldb + c];
+    }
+    __syncthreads();
+  }
+}
+
 // Block-wide max reduction helper (returns the same value on all threads).
 BDDC_DEV double block_max(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -190,6 +205,17 @@ BDDC_DEV double block_sum(double v, double* red) {
   for (int i = 0; i < nw; ++i) r += red[i];
   __syncthreads();
   return r;
+}
+
+// Squared Frobenius norm of an m x n block (same value on all threads).
+BDDC_DEV double frob2(const double* A, int ld, int m, int n, double* red) {
+  double s = 0.0;
+  for (int idx = tid(); idx < m * n; idx += nth()) {
+    int r = idx / n, c = idx - r * n;
+    double v = A[r * ld + c];
+    s += v * v;
+  }
+  return block_sum(s, red);
 }
 
 // Symmetric eigendecomposition by cyclic parallel two-sided Jacobi
