@@ -255,7 +255,9 @@ def run_mine(args):
         torch.distributed.barrier()
     clocks = ClockSampler(local)
     clocks.start()
+    from paper_2501_01676_b200.engine import GRAPH_STATS
     lib.bddc_launch_count_reset()
+    g0 = dict(GRAPH_STATS)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -269,7 +271,8 @@ def run_mine(args):
             phases[k] = phases.get(k, 0.0) + v / args.steps
     e1.record()
     torch.cuda.synchronize()
-    launches = int(lib.bddc_launch_count()) // args.steps
+    launches = (int(lib.bddc_launch_count()) - (GRAPH_STATS["captured"] - g0["captured"])
+                + (GRAPH_STATS["replayed"] - g0["replayed"])) // args.steps
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:

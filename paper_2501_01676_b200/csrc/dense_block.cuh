@@ -15,34 +15,30 @@ namespace blk {
 BDDC_DEV int tid() { return threadIdx.x; }
 BDDC_DEV int nth() { return blockDim.x; }
 
+// row-major 2D iteration without integer division: warp w takes rows
+// w, w + nwarps, ...; lanes stride the columns.
+#define BLK_FOR_RC(M, N)                                                   \
+  for (int r = (int)(threadIdx.x >> 5); r < (M); r += (int)(blockDim.x >> 5)) \
+    for (int c = (int)(threadIdx.x & 31); c < (N); c += 32)
+
 BDDC_DEV void copy(double* dst, int ldd, const double* src, int lds, int m, int n) {
-  for (int idx = tid(); idx < m * n; idx += nth()) {
-    int r = idx / n, c = idx - r * n;
-    dst[r * ldd + c] = src[r * lds + c];
-  }
+  BLK_FOR_RC(m, n) dst[r * ldd + c] = src[r * lds + c];
   __syncthreads();
 }
 
 BDDC_DEV void set_identity(double* A, int ld, int m, int n) {
-  for (int idx = tid(); idx < m * n; idx += nth()) {
-    int r = idx / n, c = idx - r * n;
-    A[r * ld + c] = (r == c) ? 1.0 : 0.0;
-  }
+  BLK_FOR_RC(m, n) A[r * ld + c] = (r == c) ? 1.0 : 0.0;
   __syncthreads();
 }
 
 BDDC_DEV void fill(double* A, int ld, int m, int n, double v) {
-  for (int idx = tid(); idx < m * n; idx += nth()) {
-    int r = idx / n, c = idx - r * n;
-    A[r * ld + c] = v;
-  }
+  BLK_FOR_RC(m, n) A[r * ld + c] = v;
   __syncthreads();
 }
 
 // A <- (A + A^T)/2
 BDDC_DEV void symmetrize(double* A, int ld, int n) {
-  for (int idx = tid(); idx < n * n; idx += nth()) {
-    int r = idx / n, c = idx - r * n;
+  BLK_FOR_RC(n, n) {
     if (c > r) {
       double v = 0.5 * (A[r * ld + c] + A[c * ld + r]);
       A[r * ld + c] = v;
@@ -52,15 +48,14 @@ BDDC_DEV void symmetrize(double* A, int ld, int n) {
   __syncthreads();
 }
 
-// C = beta*C + alpha*op(A)*op(B);  op(A) m x k, op(B) k x n.  C must not alias A/B.
-BDDC_DEV void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb,
-                   bool tb, int m, int n, int k, double alpha, double beta) {
-  for (int idx = tid(); idx < m * n; idx += nth()) {
-    int r = idx / n, c = idx - r * n;
+template <bool TA, bool TB>
+BDDC_DEV void gemm_t(double* C, int ldc, const double* A, int lda, const double* B, int ldb, int m,
+                     int n, int k, double alpha, double beta) {
+  BLK_FOR_RC(m, n) {
     double s = 0.0;
     for (int p = 0; p < k; ++p) {
-      double a = ta ? A[p * lda + r] : A[r * lda + p];
-      double b = tb ? B[c * ldb + p] : B[p * ldb + c];
+      const double a = TA ? A[p * lda + r] : A[r * lda + p];
+      const double b = TB ? B[c * ldb + p] : B[p * ldb + c];
       s = fma(a, b, s);
     }
     double v = alpha * s;
@@ -68,6 +63,15 @@ BDDC_DEV void gemm(double* C, int ldc, const double* A, int lda, bool ta, const 
     C[r * ldc + c] = v;
   }
   __syncthreads();
+}
+
+// C = beta*C + alpha*op(A)*op(B);  op(A) m x k, op(B) k x n.  C must not alias A/B.
+BDDC_DEV void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb,
+                   bool tb, int m, int n, int k, double alpha, double beta) {
+  if (!ta && !tb) gemm_t<false, false>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
+  else if (ta && !tb) gemm_t<true, false>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
+  else if (!ta && tb) gemm_t<false, true>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
+  else gemm_t<true, true>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
 }
 
 // In-place scalar Gauss-Jordan inverse without pivoting.  Returns 0 on
@@ -93,8 +97,7 @@ BDDC_DEV int gj_inverse(double* A, int ld, int n, bool require_positive, double*
       colbuf[c] = A[c * ld + p];
     }
     __syncthreads();
-    for (int idx = tid(); idx < n * n; idx += nth()) {
-      int r = idx / n, c = idx - r * n;
+    BLK_FOR_RC(n, n) {
       if (r == p) {
         A[r * ld + c] = rowbuf[c];
       } else {
@@ -128,8 +131,7 @@ BDDC_DEV bool cholesky(double* A, int ld, int n) {
     if (tid() == 0) A[j * ld + j] = s;
     __syncthreads();
     const int m = n - j - 1;
-    for (int idx = tid(); idx < m * m; idx += nth()) {
-      int r = idx / m, c = idx - r * m;
+    BLK_FOR_RC(m, m) {
       if (c <= r) {
         int ri = j + 1 + r, ci = j + 1 + c;
         A[ri * ld + ci] -= A[ri * ld + j] * A[ci * ld + j];
@@ -149,20 +151,14 @@ BDDC_DEV void chol_solve(const double* L, int ld, int n, double* B, int ldb, int
     for (int c = tid(); c < nrhs; c += nth()) B[j * ldb + c] /= d;
     __syncthreads();
     const int m = n - j - 1;
-    for (int idx = tid(); idx < m * nrhs; idx += nth()) {
-      int r = j + 1 + idx / nrhs, c = idx % nrhs;
-      B[r * ldb + c] -= L[r * ld + j] * B[j * ldb + c];
-    }
+    BLK_FOR_RC(m, nrhs) B[(j + 1 + r) * ldb + c] -= L[(j + 1 + r) * ld + j] * B[j * ldb + c];
     __syncthreads();
   }
   for (int j = n - 1; j >= 0; --j) {  // backward with L^T
     const double d = L[j * ld + j];
     for (int c = tid(); c < nrhs; c += nth()) B[j * ldb + c] /= d;
     __syncthreads();
-    for (int idx = tid(); idx < j * nrhs; idx += nth()) {
-      int r = idx / nrhs, c = idx % nrhs;
-      B[r * ldb + c] -= L[j * ld + r] * B[j * ldb + c];
-    }
+    BLK_FOR_RC(j, nrhs) B[r * ldb + c] -= L[j * ld + r] * B[j * ldb + c];
     __syncthreads();
   }
 }
@@ -174,10 +170,7 @@ BDDC_DEV void trsm_lower(const double* L, int ld, int n, double* B, int ldb, int
     for (int c = tid(); c < nrhs; c += nth()) B[j * ldb + c] /= d;
     __syncthreads();
     const int m = n - j - 1;
-    for (int idx = tid(); idx < m * nrhs; idx += nth()) {
-      int r = j + 1 + idx / nrhs, c = idx % nrhs;
-      B[r * ldb + c] -= L[r * ld + j] * B[j * ldb + c];
-    }
+    BLK_FOR_RC(m, nrhs) B[(j + 1 + r) * ldb + c] -= L[(j + 1 + r) * ld + j] * B[j * ldb + c];
     __syncthreads();
   }
 }
@@ -210,8 +203,7 @@ BDDC_DEV double block_sum(double v, double* red) {
 // Squared Frobenius norm of an m x n block (same value on all threads).
 BDDC_DEV double frob2(const double* A, int ld, int m, int n, double* red) {
   double s = 0.0;
-  for (int idx = tid(); idx < m * n; idx += nth()) {
-    int r = idx / n, c = idx - r * n;
+  BLK_FOR_RC(m, n) {
     double v = A[r * ld + c];
     s += v * v;
   }
@@ -251,8 +243,12 @@ BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ld
       // phase 1: rotation of each pair (p < q); q == n is the bye
       int rot = 0;
       for (int i = tid(); i < half; i += nth()) {
-        int a = (i == 0) ? 0 : 1 + (i - 1 + round) % (m - 1);
-        int b = 1 + (m - 2 - i + round) % (m - 1);
+        int a = i - 1 + round;
+        if (a >= m - 1) a -= m - 1;
+        a = (i == 0) ? 0 : 1 + a;
+        int b = m - 2 - i + round;
+        if (b >= m - 1) b -= m - 1;
+        b += 1;
         int p = min(a, b), q = max(a, b);
         double c = 1.0, s = 0.0;
         if (q < n) {
@@ -275,16 +271,15 @@ BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ld
       sweep_rot = 1;
       // phase 2: A_blk(i,j) <- J_i^T A_blk J_j for bi <= bj (mirrored to (j,i),
       // A stays exactly symmetric);  V(:, pair j) <- V(:, pair j) J_j
-      const int nblk = half * half;
-      for (int idx = tid(); idx < nblk + (V ? half * n : 0); idx += nth()) {
-        if (idx < nblk) {
-          const int bi = idx / half, bj = idx - bi * half;
-          if (bi > bj) continue;
-          const int p = perm[2 * bi], q = perm[2 * bi + 1];
+      for (int bi = (int)(threadIdx.x >> 5); bi < half; bi += (int)(blockDim.x >> 5)) {
+        const int p = perm[2 * bi], q = perm[2 * bi + 1];
+        const double ci = cs[2 * bi], si = cs[2 * bi + 1];
+        const bool hq = q < n;
+        for (int bj = bi + (int)(threadIdx.x & 31); bj < half; bj += 32) {
           const int pc = perm[2 * bj], qc = perm[2 * bj + 1];
-          const double ci = cs[2 * bi], si = cs[2 * bi + 1];
           const double cj = cs[2 * bj], sj = cs[2 * bj + 1];
-          const bool hq = q < n, hqc = qc < n;
+          if (si == 0.0 && sj == 0.0) continue;  // both identity: block unchanged
+          const bool hqc = qc < n;
           const double a00 = A[p * ld + pc];
           const double a01 = hqc ? A[p * ld + qc] : 0.0;
           const double a10 = hq ? A[q * ld + pc] : 0.0;
@@ -318,15 +313,18 @@ BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ld
               A[qc * ld + q] = y11;
             }
           }
-        } else {
-          const int t2 = idx - nblk;
-          const int bj = t2 / n, r = t2 - bj * n;
+        }
+      }
+      if (V) {
+        for (int bj = (int)(threadIdx.x >> 5); bj < half; bj += (int)(blockDim.x >> 5)) {
           const int pc = perm[2 * bj], qc = perm[2 * bj + 1];
-          if (qc >= n) continue;
+          if (qc >= n || cs[2 * bj + 1] == 0.0) continue;
           const double cj = cs[2 * bj], sj = cs[2 * bj + 1];
-          const double vp = V[r * ldv + pc], vq = V[r * ldv + qc];
-          V[r * ldv + pc] = cj * vp - sj * vq;
-          V[r * ldv + qc] = sj * vp + cj * vq;
+          for (int r = (int)(threadIdx.x & 31); r < n; r += 32) {
+            const double vp = V[r * ldv + pc], vq = V[r * ldv + qc];
+            V[r * ldv + pc] = cj * vp - sj * vq;
+            V[r * ldv + qc] = sj * vp + cj * vq;
+          }
         }
       }
       __syncthreads();
@@ -348,10 +346,7 @@ BDDC_DEV bool jacobi_eigh(double* A, int ld, int n, double* w, double* V, int ld
   __syncthreads();
   if (V) {
     // permute columns of V in place through A as scratch
-    for (int idx = tid(); idx < n * n; idx += nth()) {
-      int r = idx / n, c = idx - r * n;
-      A[r * ld + perm[c]] = V[r * ldv + c];
-    }
+    BLK_FOR_RC(n, n) A[r * ld + perm[c]] = V[r * ldv + c];
     __syncthreads();
     copy(V, ldv, A, ld, n, n);
   }

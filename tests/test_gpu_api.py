@@ -1,0 +1,169 @@
+"""The drop-in API on the device, exercised like the reference's own tests
+(reference tests/test_solver.py, tests/test_coarse.py, tests/test_acceptance.py):
+error paths with the reference's messages, exact-inverse limit, GMRES edge
+cases, interior recovery against a direct solve."""
+
+import math
+
+import numpy as np
+import pytest
+
+from tests.cases import const_coefficients, golden, inputs
+
+pytestmark = pytest.mark.gpu
+
+THETA_F = 1.0 + math.log(4.0)
+
+
+def _api():
+    import paper_2501_01676_b200 as P
+
+    return P
+
+
+def _setup(name):
+    P = _api()
+    system, part, globs = inputs(name)
+    ops = [P.build_subdomain_operator(system, part, globs, i) for i in range(part.n_subdomains)]
+    scaling = P.build_scaling(globs, ops)
+    return system, part, globs, ops, scaling
+
+
+def test_harness_sequence_matches_reference():
+    """harness._run_problem order of calls (reference harness.py:250-292)."""
+    P = _api()
+    g = golden("jump")
+    system, part, globs, ops, scaling = _setup("jump")
+    for op in ops:
+        op.bsym_inverse()
+    n_hat = globs.interface_nodes.shape[0]
+    operator = P.interface_operator(ops, n_hat)
+    rhs = P.interface_rhs(ops, n_hat)
+    np.testing.assert_allclose(rhs, g["rhs"], rtol=1e-12, atol=1e-15)
+    for variant in ("old", "new"):
+        basis, reports = P.adaptive_primal_space(globs, ops, scaling, THETA_F, 10.0, variant)
+        assert (basis.pnumF, basis.pnumE, basis.n_vertex) == (
+            int(g[f"{variant}_pnumF"]), int(g[f"{variant}_pnumE"]), int(g[f"{variant}_n_vertex"]))
+        pc = P.build_preconditioner(ops, basis, scaling)
+        assert pc.n_primal == basis.pnumF + basis.pnumE + basis.n_vertex
+        rep = P.gmres_solve(operator, rhs, pc)
+        assert rep.converged and abs(rep.iterations - int(g[f"{variant}_iterations"])) <= 1
+        assert len(rep.residual_history) == rep.iterations == len(rep.preconditioned_history)
+        sol = g[f"{variant}_solution"]
+        assert np.linalg.norm(rep.solution - sol) <= 1e-8 * np.linalg.norm(sol)
+        u = P.recover_interior(ops, globs, system, rep.solution)
+        ref_u = g[f"{variant}_u"]
+        assert np.linalg.norm(u - ref_u) <= 1e-8 * np.linalg.norm(ref_u)
+
+
+def test_recovery_matches_direct_solve():
+    from paper_2501_01676_b200.discretization import solve_direct
+
+    P = _api()
+    system, part, globs, ops, scaling = _setup("jump")
+    basis, _ = P.adaptive_primal_space(globs, ops, scaling, THETA_F, 10.0, "new")
+    pc = P.build_preconditioner(ops, basis, scaling)
+    n = globs.interface_nodes.size
+    rep = P.gmres_solve(P.interface_operator(ops, n), P.interface_rhs(ops, n), pc, rel_tol=1e-12)
+    u = P.recover_interior(ops, globs, system, rep.solution)
+    ud = solve_direct(system)
+    assert np.linalg.norm(u - ud) <= 1e-8 * np.linalg.norm(ud)
+
+
+def test_scaling_partition_of_unity():
+    system, part, globs, ops, scaling = _setup("jump")
+    for G in globs.globs:
+        fam = scaling.of(G)
+        total = sum(fam[s] for s in G.sharers)
+        np.testing.assert_allclose(total, np.eye(G.size), atol=1e-12)
+
+
+def test_apply_zero_and_linearity():
+    P = _api()
+    system, part, globs, ops, scaling = _setup("jump")
+    basis, _ = P.adaptive_primal_space(globs, ops, scaling, THETA_F, 10.0, "new")
+    pc = P.build_preconditioner(ops, basis, scaling)
+    assert np.all(pc.apply(np.zeros(pc.n_hat)) == 0)
+    rng = np.random.default_rng(2)
+    r1, r2 = rng.standard_normal(pc.n_hat), rng.standard_normal(pc.n_hat)
+    a, b = 0.37, -2.5
+    lhs = pc.apply(a * r1 + b * r2)
+    rhs = a * pc.apply(r1) + b * pc.apply(r2)
+    assert np.abs(lhs - rhs).max() <= 1e-12 * max(np.abs(lhs).max(), 1.0)
+
+
+def test_full_primal_is_exact_inverse():
+    """Every interface dof primal: M^-1 = S_hat^-1 (reference test_solver.py:109-116)."""
+    from oracle import bddc_oracle as O
+
+    P = _api()
+    system, part, globs, ops, scaling = _setup("jump")
+    basis = P.PrimalBasis(globs, [(np.eye(g.size), g.size) for g in globs.globs], "old")
+    pc = P.build_preconditioner(ops, basis, scaling)
+    ref_ops = O.all_local_operators(system, part, globs)
+    n = globs.interface_nodes.size
+    S = np.zeros((n, n))
+    for op in ref_ops:
+        S[np.ix_(op.iface_index, op.iface_index)] += op.S
+    rhs = P.interface_rhs(ops, n)
+    x = np.linalg.solve(S, rhs)
+    y = pc.apply(rhs)
+    assert np.linalg.norm(y - x) <= 1e-9 * np.linalg.norm(x)
+    rep = P.gmres_solve(P.interface_operator(ops, n), rhs, pc)
+    assert rep.iterations == 1 and rep.converged
+
+
+def test_empty_primal_rejected():
+    """2x1x1 partition, infinite thresholds: no primal dof (test_solver.py:50-60)."""
+    from paper_2501_01676_b200.decomposition import classify_globs, partition_regular
+    from paper_2501_01676_b200.discretization import assemble_system
+    from paper_2501_01676_b200.mesh import box_mesh
+
+    P = _api()
+    mesh = box_mesh(((0, 1), (0, 1), (0, 1)), (4, 2, 2))
+    part = partition_regular(mesh, (2, 1, 1))
+    globs = classify_globs(mesh, part, mesh.boundary_nodes)
+    system = assemble_system(mesh, const_coefficients(nu=1.0))
+    ops = [P.build_subdomain_operator(system, part, globs, i) for i in range(2)]
+    scaling = P.build_scaling(globs, ops)
+    basis, _ = P.adaptive_primal_space(globs, ops, scaling, np.inf, np.inf, "old")
+    assert basis.n_primal_total == 0
+    with pytest.raises(P.NumericalError, match="primal"):
+        P.build_preconditioner(ops, basis, scaling)
+
+
+def test_degenerate_primal_space_diagnosed():
+    """Duplicated constraint rows make the coarse matrix singular (test_solver.py:62-77)."""
+    P = _api()
+    system, part, globs, ops, scaling = _setup("jump")
+    transforms = []
+    for g in globs.globs:
+        if g.kind == "face" and g.size >= 2:
+            Q = np.eye(g.size)
+            Q[1] = Q[0]
+            transforms.append((Q, 2))
+        else:
+            transforms.append((np.eye(g.size), g.size if g.kind == "vertex" else 0))
+    bad = P.PrimalBasis(globs, transforms, "old")
+    with pytest.raises(P.NumericalError, match="singular at primal dof"):
+        P.build_preconditioner(ops, bad, scaling)
+
+
+def test_gmres_zero_rhs():
+    P = _api()
+    system, part, globs, ops, scaling = _setup("jump")
+    basis, _ = P.adaptive_primal_space(globs, ops, scaling, THETA_F, 10.0, "new")
+    pc = P.build_preconditioner(ops, basis, scaling)
+    n = globs.interface_nodes.size
+    rep = P.gmres_solve(P.interface_operator(ops, n), np.zeros(n), pc)
+    assert rep.iterations == 0 and rep.converged and np.all(rep.solution == 0)
+
+
+def test_operator_views_match_reference_order():
+    g = golden("jump")
+    system, part, globs, ops, scaling = _setup("jump")
+    for i in g["S_ids"].tolist():
+        np.testing.assert_allclose(ops[i].S, g[f"S_{i}"], rtol=0, atol=1e-12 * np.abs(g[f"S_{i}"]).max())
+        Bi = ops[i].bsym_inverse()
+        np.testing.assert_allclose(Bi, g[f"Binv_{i}"], rtol=0, atol=1e-10 * np.abs(g[f"Binv_{i}"]).max())
+        assert np.allclose(ops[i].Bsym, ops[i].Bsym.T)
