@@ -494,5 +494,243 @@ BDDC_DEV void complete_basis(const double* U, int ldu, int r, int n, double* Q, 
   __syncthreads();
 }
 
+
+// ---------------------------------------------------------------------------
+// Symmetric tridiagonal route: Householder reduction, bisection for all
+// eigenvalues, inverse iteration for a chosen subset of eigenvectors, and
+// back-transformation.  Used by the certified pencil fast path, which needs
+// every eigenvalue but only the eigenvectors of the selected (lambda >= theta)
+// modes.
+// ---------------------------------------------------------------------------
+
+// In place: A (n x n symmetric, lower triangle used) -> T = Q^T A Q with
+// d (n), e (n-1); Householder vectors v_k (v_k[0] = 1 implicit) stored in
+// A[k+2:n, k], scalars in tau[k].  work: 2n doubles.
+BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, double* tau,
+                             double* work, double* red) {
+  double* v = work;       // n
+  double* p = work + n;   // n
+  for (int k = 0; k < n - 2; ++k) {
+    const int m = n - k - 1;  // length of the column below the diagonal
+    double ss = 0.0;
+    for (int i = tid(); i < m - 1; i += nth()) {
+      const double x = A[(k + 2 + i) * ld + k];
+      ss += x * x;
+    }
+    ss = block_sum(ss, red);
+    const double alpha = A[(k + 1) * ld + k];
+    double t, beta;
+    if (ss == 0.0) {
+      t = 0.0;
+      beta = alpha;
+    } else {
+      beta = -copysign(sqrt(alpha * alpha + ss), alpha);
+      t = (beta - alpha) / beta;
+    }
+    const double scal = (ss == 0.0) ? 0.0 : 1.0 / (alpha - beta);
+    for (int i = tid(); i < m; i += nth())
+      v[i] = (i == 0) ? 1.0 : A[(k + 1 + i) * ld + k] * scal;
+    __syncthreads();
+    if (tid() == 0) {
+      tau[k] = t;
+      e[k] = beta;
+    }
+    if (t != 0.0) {
+      // p = t * A22 v   (A22 = A[k+1:, k+1:], symmetric: use full stored block)
+      for (int r = (int)(threadIdx.x >> 5); r < m; r += (int)(blockDim.x >> 5)) {
+        double s = 0.0;
+        for (int c = (int)(threadIdx.x & 31); c < m; c += 32) s += A[(k + 1 + r) * ld + k + 1 + c] * v[c];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if ((threadIdx.x & 31) == 0) p[r] = t * s;
+      }
+      __syncthreads();
+      double pv = 0.0;
+      for (int i = tid(); i < m; i += nth()) pv += p[i] * v[i];
+      pv = block_sum(pv, red);
+      const double hc = 0.5 * t * pv;
+      // w = p - hc v ; A22 -= v w^T + w v^T
+      BLK_FOR_RC(m, m) {
+        const double wr = p[r] - hc * v[r], wc = p[c] - hc * v[c];
+        A[(k + 1 + r) * ld + k + 1 + c] -= v[r] * wc + wr * v[c];
+      }
+      __syncthreads();
+    }
+    // keep v_k below the subdiagonal for the back-transformation
+    for (int i = 1 + tid(); i < m; i += nth()) A[(k + 1 + i) * ld + k] = v[i];
+    __syncthreads();
+  }
+  for (int i = tid(); i < n; i += nth()) d[i] = A[i * ld + i];
+  if (tid() == 0 && n >= 2) e[n - 2] = A[(n - 1) * ld + n - 2];
+  if (tid() == 0 && n >= 2) tau[n - 2] = 0.0;
+  __syncthreads();
+}
+
+// Sturm count: number of eigenvalues of T strictly below x.
+BDDC_DEV int sturm_count(const double* d, const double* e, int n, double x, double pivmin) {
+  int cnt = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  if (q < 0.0) ++cnt;
+  for (int i = 1; i < n; ++i) {
+    q = d[i] - x - e[i - 1] * e[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    if (q < 0.0) ++cnt;
+  }
+  return cnt;
+}
+
+// All eigenvalues of T in ascending order (w), one thread per eigenvalue,
+// bisection to machine precision.
+BDDC_DEV void tridiag_eigvals(const double* d, const double* e, int n, double* w, double* red) {
+  double lo = 0.0, hi = 0.0, emax = 0.0;
+  for (int i = tid(); i < n; i += nth()) {
+    const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < n - 1 ? fabs(e[i]) : 0.0);
+    lo = fmin(lo, d[i] - r);
+    hi = fmax(hi, d[i] + r);
+    if (i < n - 1) emax = fmax(emax, e[i] * e[i]);
+  }
+  lo = -block_max(-lo, red);
+  hi = block_max(hi, red);
+  emax = block_max(emax, red);
+  const double nrm = fmax(fabs(lo), fabs(hi));
+  const double pivmin = fmax(1e-300, 1e-300 * emax);
+  lo -= 2.2e-16 * nrm * n + 1e-300;
+  hi += 2.2e-16 * nrm * n + 1e-300;
+  const double atol = 1e-17 * nrm + 1e-300;
+  for (int j = tid(); j < n; j += nth()) {
+    double a = lo, b = hi;
+    for (int it = 0; it < 200; ++it) {
+      const double mid = 0.5 * (a + b);
+      if (mid <= a || mid >= b) break;
+      if (b - a <= 2.2e-16 * fmax(fabs(a), fabs(b)) + atol) break;
+      if (sturm_count(d, e, n, mid, pivmin) <= j) a = mid; else b = mid;
+    }
+    w[j] = 0.5 * (a + b);
+  }
+  __syncthreads();
+}
+
+// Solve (T - lam I) x = b in place by Gaussian elimination with partial
+// pivoting on the tridiagonal (single thread; scratch u0,u1,u2,ml: n each,
+// pv: n ints).  Zero pivots are replaced by +-tiny.
+BDDC_DEV void tridiag_shift_solve(const double* d, const double* e, int n, double lam, double tiny,
+                                  double* x, double* u0, double* u1, double* u2, double* ml,
+                                  int* pv) {
+  for (int i = 0; i < n; ++i) {
+    u0[i] = d[i] - lam;
+    u1[i] = (i < n - 1) ? e[i] : 0.0;
+    u2[i] = 0.0;
+  }
+  for (int k = 0; k < n - 1; ++k) {
+    const double sub = e[k];
+    if (fabs(sub) > fabs(u0[k])) {
+      const double a = u0[k], b = u1[k], c = u2[k];
+      const double dn = u0[k + 1], s1 = u1[k + 1];
+      const double l = a / sub;
+      u0[k] = sub;
+      u1[k] = dn;
+      u2[k] = s1;
+      u0[k + 1] = b - l * dn;
+      u1[k + 1] = c - l * s1;
+      ml[k] = l;
+      pv[k] = 1;
+    } else {
+      if (u0[k] == 0.0) u0[k] = tiny;
+      const double l = sub / u0[k];
+      u0[k + 1] -= l * u1[k];
+      u1[k + 1] -= l * u2[k];
+      ml[k] = l;
+      pv[k] = 0;
+    }
+  }
+  if (u0[n - 1] == 0.0) u0[n - 1] = tiny;
+  for (int k = 0; k < n - 1; ++k) {
+    if (pv[k]) {
+      const double t = x[k];
+      x[k] = x[k + 1];
+      x[k + 1] = t - ml[k] * x[k + 1];
+    } else {
+      x[k + 1] -= ml[k] * x[k];
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = x[i];
+    if (i + 1 < n) s -= u1[i] * x[i + 1];
+    if (i + 2 < n) s -= u2[i] * x[i + 2];
+    x[i] = s / u0[i];
+  }
+}
+
+// Eigenvectors of T for the eigenvalues w[idx[0..k-1]], one of kIILanes
+// threads per cluster of close eigenvalues (|gap| <= 1e-3 ||T||), inverse
+// iteration with Gram-Schmidt inside a cluster (LAPACK dstein strategy).
+// X: n x k, columns = unit eigenvectors of T.  scratch: 5 n doubles per lane,
+// iscratch: n ints per lane.
+constexpr int kIILanes = 4;
+BDDC_DEV void tridiag_eigvecs(const double* d, const double* e, int n, const double* w,
+                              const int* idx, int k, double* X, double* scratch, int* iscratch) {
+  if (threadIdx.x < kIILanes) {
+    double tn = 0.0;
+    for (int i = 0; i < n; ++i)
+      tn = fmax(tn, fabs(d[i]) + (i > 0 ? fabs(e[i - 1]) : 0.0) + (i < n - 1 ? fabs(e[i]) : 0.0));
+    const double tiny = fmax(2.2e-16 * tn, 1e-300);
+    // cluster starts: lane handles clusters in order
+    int cl = 0;
+    for (int j = 0; j < k; ++j) {
+      const bool start = (j == 0) || fabs(w[idx[j]] - w[idx[j - 1]]) > 1e-3 * tn;
+      if (start) ++cl;
+      if ((cl - 1) % kIILanes != (int)threadIdx.x) continue;
+      int j0 = j;  // first member of this cluster
+      while (j0 > 0 && !(fabs(w[idx[j0]] - w[idx[j0 - 1]]) > 1e-3 * tn)) --j0;
+      double* x = scratch + threadIdx.x * 5 * n;
+      double* u0 = x + n;
+      double* u1 = u0 + n;
+      double* u2 = u1 + n;
+      double* ml = u2 + n;
+      int* pv = iscratch + threadIdx.x * n;
+      const double lam = w[idx[j]] + (j - j0) * 10.0 * tiny;  // separate equal shifts
+      for (int i = 0; i < n; ++i) x[i] = 1.0 + 0.37 * sin(1.0 + 0.7 * i + 1.3 * (j - j0));
+      for (int it = 0; it < 5; ++it) {
+        tridiag_shift_solve(d, e, n, lam, tiny, x, u0, u1, u2, ml, pv);
+        // orthogonalise against the earlier members of the cluster
+        for (int q = j0; q < j; ++q) {
+          double dot = 0.0;
+          for (int i = 0; i < n; ++i) dot += X[i * k + q] * x[i];
+          for (int i = 0; i < n; ++i) x[i] -= dot * X[i * k + q];
+        }
+        double nrm = 0.0;
+        for (int i = 0; i < n; ++i) nrm += x[i] * x[i];
+        nrm = sqrt(nrm);
+        const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+        for (int i = 0; i < n; ++i) x[i] *= inv;
+      }
+      for (int i = 0; i < n; ++i) X[i * k + j] = x[i];
+    }
+  }
+  __syncthreads();
+}
+
+// Y <- Q Y for the Householder Q of tridiagonalize() (Y: n x k, ld ldy).
+BDDC_DEV void apply_householder(const double* A, int ld, int n, const double* tau, double* Y,
+                                int ldy, int k) {
+  for (int j = (int)(threadIdx.x >> 5); j < k; j += (int)(blockDim.x >> 5)) {
+    const int lane = threadIdx.x & 31;
+    for (int s = n - 3; s >= 0; --s) {
+      const double t = tau[s];
+      if (t == 0.0) continue;
+      // v = [1; A[s+2:, s]] acting on rows s+1..n-1
+      double dot = 0.0;
+      for (int i = lane; i < n - s - 1; i += 32)
+        dot += (i == 0 ? 1.0 : A[(s + 1 + i) * ld + s]) * Y[(s + 1 + i) * ldy + j];
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      dot *= t;
+      for (int i = lane; i < n - s - 1; i += 32)
+        Y[(s + 1 + i) * ldy + j] -= dot * (i == 0 ? 1.0 : A[(s + 1 + i) * ld + s]);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace blk
 }  // namespace bddc

@@ -19,7 +19,7 @@ BDDC_HD long long bddc_edge_old_ws(long long n) {
   long long sc = 8 * n * n + 3 * n;
   long long rs = bddc_rowspace_ws(n, n);
   if (rs > sc) sc = rs;
-  return 7 * n * n + n + sc + 64;
+  return 7 * n * n + n + sc + 32 * n + 64;
 }
 
 BDDC_HD long long bddc_edge_new_ws(long long ns, long long ne, long long wd, long long nhmax) {
@@ -32,5 +32,5 @@ BDDC_HD long long bddc_edge_new_ws(long long ns, long long ne, long long wd, lon
   if (pf > sc) sc = pf;
   long long rs = bddc_rowspace_ws(nC * (ns - 1), ne);
   if (rs > sc) sc = rs;
-  return base + sc + 64;
+  return base + sc + 32 * nC + 64;
 }

@@ -105,7 +105,15 @@ BDDC_DEV int psum_fast(const double* A, const double* B, int n, double* R, doubl
   return 1;
 }
 
-// ws: 5 n^2 + n ; vals / vecs / degen as pencil()
+// ws: pencil_fast_ws(n) = 5 n^2 + 4 n + kIILanes * 6 n doubles.
+// vals / degen as pencil(); vecs: only the selected columns (vals >= theta)
+// are written (the rows and the change of basis need no other vector).
+// Eigenvalues: Householder tridiagonalisation + bisection; selected vectors:
+// inverse iteration on the tridiagonal + back-transformation.
+__host__ __device__ inline long long pencil_fast_ws(long long n) {
+  return 5 * n * n + 4 * n + (long long)blk::kIILanes * 6 * n + 16;
+}
+
 BDDC_DEV int pencil_fast(const double* B, const double* Bt, int n, double theta, double* vals,
                          double* vecs, int* degen, double* ws, double* cs, int* perm,
                          double* red) {
@@ -114,8 +122,13 @@ BDDC_DEV int pencil_fast(const double* B, const double* Bt, int n, double theta,
   double* Li = L + nn;
   double* T1 = Li + nn;
   double* Bh = T1 + nn;
-  double* Y = Bh + nn;
-  double* lam = Y + nn;
+  double* X = Bh + nn;
+  double* dd = X + nn;
+  double* ee = dd + n;
+  double* tau = ee + n;
+  double* w = tau + n;
+  double* scr = w + n;                      // kIILanes * 5 n
+  int* iscr = reinterpret_cast<int*>(scr + blk::kIILanes * 5 * n);  // kIILanes * n ints
   blk::copy(L, n, Bt, n, n, n);
   if (!blk::cholesky(L, n, n)) return 0;
   blk::set_identity(Li, n, n, n);
@@ -128,19 +141,32 @@ BDDC_DEV int pencil_fast(const double* B, const double* Bt, int n, double theta,
   blk::gemm(T1, n, Li, n, false, B, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(Bh, n, T1, n, false, Li, n, true, n, n, n, 1.0, 0.0);
   blk::symmetrize(Bh, n, n);
-  blk::jacobi_eigh(Bh, n, n, lam, Y, n, cs, perm, red);
-  // v = Li^T y, descending order, 1/sqrt|lambda| normalisation above the floor
-  const double floor = 1e-14 * nb;
-  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
-    const int r = idx / n, j = idx - r * n;
-    double s = 0.0;
-    for (int k = r; k < n; ++k) s += Li[k * n + r] * Y[k * n + j];
-    const double l = lam[j];
-    const int o = n - 1 - j;
-    vecs[r * n + o] = fabs(l) > floor ? s / sqrt(fabs(l)) : s;
-    if (r == 0) {
-      vals[o] = l;
-      degen[o] = 0;
+  double* work = L;  // L no longer needed: 2n scratch for the reduction
+  blk::tridiagonalize(Bh, n, n, dd, ee, tau, work, red);
+  blk::tridiag_eigvals(dd, ee, n, w, red);
+  // selected = eigenvalues >= theta, in descending order
+  __shared__ int s_k;
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int j = n - 1; j >= 0 && w[j] >= theta; --j) perm[k++] = j;
+    s_k = k;
+  }
+  __syncthreads();
+  const int k = s_k;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    vals[n - 1 - j] = w[j];
+    degen[j] = 0;
+  }
+  if (k > 0) {
+    blk::tridiag_eigvecs(dd, ee, n, w, perm, k, X, scr, iscr);
+    blk::apply_householder(Bh, n, n, tau, X, k, k);
+    // v = Li^T y / sqrt(lambda) into the output column of each selected mode
+    for (int idx = threadIdx.x; idx < n * k; idx += blockDim.x) {
+      const int r = idx / k, q = idx - r * k;
+      double s = 0.0;
+      for (int t = r; t < n; ++t) s += Li[t * n + r] * X[t * k + q];
+      const int j = perm[q];
+      vecs[r * n + (n - 1 - j)] = s / sqrt(fabs(w[j]));
     }
   }
   __syncthreads();
@@ -442,7 +468,7 @@ struct GlobOut {
 };
 
 // Arena (doubles) of one face: 10 n^2 + 3 n (+ pad), see face_kernel.
-__host__ __device__ inline long long face_arena(long long n) { return 10 * n * n + 3 * n + 32; }
+__host__ __device__ inline long long face_arena(long long n) { return 10 * n * n + 40 * n + 64; }
 
 __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* __restrict__ D,
                                                    double theta, GlobOut o,

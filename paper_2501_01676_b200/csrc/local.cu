@@ -73,19 +73,18 @@ __global__ void __launch_bounds__(256) pivot_inverse_kernel(
   const double* M = base + off[b] + (long long)k * L + k;
   const int c = threadIdx.x & 63, r0 = threadIdx.x >> 6;
   double a[16];
+  // the pivot row / column of step p are published into buffer p & 1 while
+  // step p-1 updates them (no dynamic register indexing)
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
     const int r = r0 + 4 * j;
     a[j] = (r < w && c < w) ? M[(long long)r * L + c] : (r == c ? 1.0 : 0.0);
+    if (r == 0) rowb[0][c] = a[j];
+    if (c == 0) colb[0][r] = a[j];
   }
   if (threadIdx.x == 0) bad = 0;
   for (int p = 0; p < w; ++p) {
     const int par = p & 1;
-    if ((p & 3) == r0) rowb[par][c] = a[p >> 2];
-    if (c == p) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j) colb[par][r0 + 4 * j] = a[j];
-    }
     __syncthreads();
     const double piv = rowb[par][p];
     const double ip = 1.0 / piv;
@@ -94,15 +93,20 @@ __global__ void __launch_bounds__(256) pivot_inverse_kernel(
       if (!(piv == piv) || piv == 0.0 || isinf(piv) || (require_positive && !(piv > 0.0))) bad = 1;
     }
     const double rc = rowb[par][c] * ip;
+    const int nx = p + 1;
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int r = r0 + 4 * j;
+      double v;
       if (r == p) {
-        a[j] = (c == p) ? ip : rc;
+        v = (c == p) ? ip : rc;
       } else {
         const double f = colb[par][r];
-        a[j] = (c == p) ? -f * ip : a[j] - f * rc;
+        v = (c == p) ? -f * ip : a[j] - f * rc;
       }
+      a[j] = v;
+      if (r == nx) rowb[par ^ 1][c] = v;
+      if (c == nx) colb[par ^ 1][r] = v;
     }
   }
   __syncthreads();
@@ -138,12 +142,14 @@ __global__ void __launch_bounds__(kTileThreads) schur_row_kernel(
            1.0, 0.0, sm);
 }
 
-__global__ void __launch_bounds__(kTileThreads) schur_trailing_kernel(
+constexpr int kTrailBM = 128;
+
+__global__ void __launch_bounds__(2 * kTrailBM) schur_trailing_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ nrows, const int* __restrict__ ncols,
     int k, int lim) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  TileSmemT<kTrailBM>& sm = *reinterpret_cast<TileSmemT<kTrailBM>*>(smem_raw);
   const int b = blockIdx.y;
   const int w = min(kTile, npiv[b] - k);
   if (w <= 0) return;
@@ -152,12 +158,13 @@ __global__ void __launch_bounds__(kTileThreads) schur_trailing_kernel(
   const int tn_count = (nc - s + kTile - 1) / kTile;
   if (tn_count <= 0) return;
   const int tm = blockIdx.x / tn_count, tn = blockIdx.x - tm * tn_count;
-  const int r0 = s + tm * kTile, c0 = s + tn * kTile;
+  const int r0 = s + tm * kTrailBM, c0 = s + tn * kTile;
   if (r0 >= nr) return;
   const int L = ld[b];
   double* M = base + off[b];
-  tile_mma(M + (long long)r0 * L + c0, L, min(kTile, nr - r0), min(kTile, nc - c0),
-           M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm);
+  tile_mma_t<kTrailBM>(M + (long long)r0 * L + c0, L, min(kTrailBM, nr - r0), min(kTile, nc - c0),
+                       M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0,
+                       sm);
 }
 
 // ---------------------------------------------------------------------------
@@ -310,7 +317,8 @@ static int smem_tile_setup() {
   if (!done) {
     int bytes = (int)sizeof(TileSmem);
     cudaFuncSetAttribute(schur_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(schur_trailing_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(schur_trailing_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileSmemT<kTrailBM>));
     cudaFuncSetAttribute(gj_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(gj_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -360,7 +368,7 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
                                                      require_positive, piv_out, piv_stride);
     ++launches;
     const int ct = ceil_div(max_cols - k, kTile);
-    const int rt = ceil_div(max_rows - k, kTile);
+    const int rt = ceil_div(max_rows - k, kTrailBM);
     if (ct > 0) {
       schur_row_kernel<<<dim3(ct, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
                                                                         P, pinv_stride, 0x7fffffff);
@@ -368,7 +376,7 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
     }
     if (ct > 0 && rt > 0) {
       if (ev) cudaEventRecord(ev[2 * timed], stream);
-      schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, smem, stream>>>(
+      schur_trailing_kernel<<<dim3(ct * rt, nbatch), 2 * kTrailBM, sizeof(TileSmemT<kTrailBM>), stream>>>(
           M, off, ld, npiv, nrows, ncols, k, 0x7fffffff);
       ++launches;
       if (ev) cudaEventRecord(ev[2 * timed + 1], stream);
@@ -428,8 +436,9 @@ int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const in
     const int span = lim - k - w;
     if (span > 0) {
       const int t = ceil_div(span, kTile);
+      const int tr = ceil_div(span, kTrailBM);
       schur_row_kernel<<<dim3(t, 1), kTileThreads, smem, stream>>>(C, off, ldv, nv, nv, k, P, 0, lim);
-      schur_trailing_kernel<<<dim3(t * t, 1), kTileThreads, smem, stream>>>(C, off, ldv, nv, nv, nv, k, lim);
+      schur_trailing_kernel<<<dim3(t * tr, 1), 2 * kTrailBM, sizeof(TileSmemT<kTrailBM>), stream>>>(C, off, ldv, nv, nv, nv, k, lim);
       launches += 2;
     }
   }

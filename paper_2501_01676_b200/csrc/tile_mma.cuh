@@ -1,13 +1,13 @@
-// 64x64 fp64 tile GEMM on the DMMA pipe (mma.sync m8n8k4.f64, sm_100a).
+// BM x 64 fp64 tile GEMM on the DMMA pipe (mma.sync m8n8k4.f64, sm_100a).
 //
-// One CTA of 128 threads (2x2 warps, 32x32 per warp = 4x4 DMMA tiles)
-// computes   C[m x n] = beta*C + alpha * A[m x K] * B[K x n]   with
-// m, n <= 64 and K <= 64.  A and B stream through shared memory in K-chunks
-// of 16 with a 3-stage cp.async pipeline (16-byte copies when the source is
-// 16-byte aligned, 8-byte otherwise; out-of-range elements zero-filled); the
-// accumulators start from (beta/alpha)*C so C is read once, early.  B may
-// alias C when one CTA owns every row of that C tile and beta == 0
-// (in-place W = P*W updates): all of B is read before the epilogue writes.
+// One CTA of 2*BM threads ((BM/32) x 2 warps, 32x32 per warp = 4x4 DMMA
+// tiles) computes   C[m x n] = beta*C + alpha * A[m x K] * B[K x n]   with
+// m <= BM, n <= 64 and K <= 64.  A and B stream through shared memory in
+// K-chunks of 16 with a 3-stage cp.async pipeline (16-byte copies when the
+// source is 16-byte aligned, 8-byte otherwise; out-of-range elements
+// zero-filled); C is read once, in the epilogue.  B may alias C when one CTA
+// owns every row of that C tile and beta == 0 (in-place W = P*W updates):
+// all of B is read before the epilogue writes.
 #pragma once
 #include "common.cuh"
 
@@ -20,10 +20,14 @@ constexpr int kStages = 3;
 constexpr int kAS = kKC + 4;     // A smem row stride (doubles): conflict-free fragments
 constexpr int kBS = kTile + 4;   // B smem row stride
 
-struct TileSmem {
-  double A[kStages][kTile][kAS];
+// BM x 64 output tile, BM in {64, 128}: 2 * BM threads, warps arranged
+// (BM/32) x 2, each warp 32 x 32 (4 x 4 DMMA m8n8k4 tiles).
+template <int BM>
+struct TileSmemT {
+  double A[kStages][BM][kAS];
   double B[kStages][kKC][kBS];
 };
+using TileSmem = TileSmemT<64>;
 
 BDDC_DEV void cp_async8(double* dst, const double* src, bool valid) {
   unsigned s = (unsigned)__cvta_generic_to_shared(dst);
@@ -44,13 +48,15 @@ BDDC_DEV void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// async load of K-chunk `kc` of A (64 x kKC) and B (kKC x 64) into stage `st`
-BDDC_DEV void tile_issue_chunk(TileSmem& sm, int st, int kc, const double* A, long long lda,
+// async load of K-chunk `kc` of A (BM x kKC) and B (kKC x 64) into stage `st`
+template <int BM>
+BDDC_DEV void tile_issue_chunk(TileSmemT<BM>& sm, int st, int kc, const double* A, long long lda,
                                const double* B, long long ldb, int m, int n, int K, bool a16,
                                bool b16) {
+  constexpr int NT = 2 * BM;
   const int k0 = kc * kKC;
   if (a16) {
-    for (int idx = threadIdx.x; idx < kTile * (kKC / 2); idx += kTileThreads) {
+    for (int idx = threadIdx.x; idx < BM * (kKC / 2); idx += NT) {
       const int r = idx / (kKC / 2), c = (idx - r * (kKC / 2)) * 2;
       const int kk = k0 + c;
       int valid = (r < m) ? max(0, min(2, K - kk)) : 0;
@@ -58,21 +64,21 @@ BDDC_DEV void tile_issue_chunk(TileSmem& sm, int st, int kc, const double* A, lo
       cp_async16(&sm.A[st][r][c], src, valid);
     }
   } else {
-    for (int idx = threadIdx.x; idx < kTile * kKC; idx += kTileThreads) {
+    for (int idx = threadIdx.x; idx < BM * kKC; idx += NT) {
       const int r = idx / kKC, c = idx - r * kKC;
       const bool valid = r < m && k0 + c < K;
       cp_async8(&sm.A[st][r][c], valid ? A + (long long)r * lda + k0 + c : A, valid);
     }
   }
   if (b16) {
-    for (int idx = threadIdx.x; idx < kKC * (kTile / 2); idx += kTileThreads) {
+    for (int idx = threadIdx.x; idx < kKC * (kTile / 2); idx += NT) {
       const int r = idx / (kTile / 2), c = (idx - r * (kTile / 2)) * 2;
       int valid = (k0 + r < K) ? max(0, min(2, n - c)) : 0;
       const double* src = valid ? B + (long long)(k0 + r) * ldb + c : B;
       cp_async16(&sm.B[st][r][c], src, valid);
     }
   } else {
-    for (int idx = threadIdx.x; idx < kKC * kTile; idx += kTileThreads) {
+    for (int idx = threadIdx.x; idx < kKC * kTile; idx += NT) {
       const int r = idx / kTile, c = idx - r * kTile;
       const bool valid = k0 + r < K && c < n;
       cp_async8(&sm.B[st][r][c], valid ? B + (long long)(k0 + r) * ldb + c : B, valid);
@@ -80,12 +86,13 @@ BDDC_DEV void tile_issue_chunk(TileSmem& sm, int st, int kc, const double* A, lo
   }
 }
 
-BDDC_DEV void tile_mma(double* C, long long ldc, int m, int n, const double* A, long long lda,
-                       const double* B, long long ldb, int K, double alpha, double beta,
-                       TileSmem& sm) {
+template <int BM>
+BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A, long long lda,
+                         const double* B, long long ldb, int K, double alpha, double beta,
+                         TileSmemT<BM>& sm) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // (BM/32) x 2 warps
   const int nchunks = (K + kKC - 1) / kKC;
   const bool a16 = ((reinterpret_cast<uintptr_t>(A) | (uintptr_t)(lda * 8)) & 15) == 0;
   const bool b16 = ((reinterpret_cast<uintptr_t>(B) | (uintptr_t)(ldb * 8)) & 15) == 0;
@@ -94,20 +101,13 @@ BDDC_DEV void tile_mma(double* C, long long ldc, int m, int n, const double* A, 
     if (s < nchunks) tile_issue_chunk(sm, s, s, A, lda, B, ldb, m, n, K, a16, b16);
     cp_async_commit();
   }
-  // accumulators start from (beta/alpha) C
+  // accumulators start at zero; C is combined in the epilogue (its load
+  // latency overlaps other CTAs' DMMA work instead of delaying the first MMA)
   double acc[4][4][2];
-  const double cscale = (beta != 0.0) ? beta / alpha : 0.0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int r = wm + i * 8 + g;
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int c = wn + j * 8 + 2 * t;
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        acc[i][j][h] = (cscale != 0.0 && r < m && c + h < n) ? cscale * C[(long long)r * ldc + c + h] : 0.0;
-    }
-  }
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int kc = 0; kc < nchunks; ++kc) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
@@ -140,9 +140,19 @@ BDDC_DEV void tile_mma(double* C, long long ldc, int m, int n, const double* A, 
       const int c = wn + j * 8 + 2 * t;
 #pragma unroll
       for (int h = 0; h < 2; ++h)
-        if (c + h < n) crow[c + h] = alpha * acc[i][j][h];
+        if (c + h < n) {
+          double v = alpha * acc[i][j][h];
+          if (beta != 0.0) v += beta * crow[c + h];
+          crow[c + h] = v;
+        }
     }
   }
+}
+
+BDDC_DEV void tile_mma(double* C, long long ldc, int m, int n, const double* A, long long lda,
+                       const double* B, long long ldb, int K, double alpha, double beta,
+                       TileSmem& sm) {
+  tile_mma_t<64>(C, ldc, m, n, A, lda, B, ldb, K, alpha, beta, sm);
 }
 
 }  // namespace bddc

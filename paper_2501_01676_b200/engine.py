@@ -257,7 +257,7 @@ class DeviceScaling:
 def _face_ws(n):
     """face_arena() in csrc/globs.cu"""
     n = np.asarray(n, dtype=np.int64)
-    return 10 * n * n + 3 * n + 32
+    return 10 * n * n + 40 * n + 64
 
 
 def _face_smem_bytes(n):
@@ -273,7 +273,7 @@ FACE_SMEM_BUDGET = 225 * 1024
 def _edge_old_ws(n):
     n = np.asarray(n, dtype=np.int64)
     sc = np.maximum(8 * n * n + 3 * n, _rowspace_ws(n, n))
-    return 7 * n * n + n + sc + 64
+    return 7 * n * n + n + sc + 32 * n + 64
 
 
 def _rowspace_ws(m, n):
@@ -289,7 +289,7 @@ def _edge_new_ws(ns, ne, wd, nhmax):
     xd = ne + nhmax
     base = ns * ne * nC + nC * nC + wd * wd + xd * xd + 2 * wd * wd
     sc = np.maximum(np.maximum(8 * nC * nC + 3 * nC, 3 * nr * nr + nr), _rowspace_ws(nC * (ns - 1), ne))
-    return base + sc + 64
+    return base + sc + 32 * nC + 64
 
 
 class DevicePrimalSpace:
@@ -581,7 +581,7 @@ class DevicePreconditioner:
         self.rp = torch.empty(nc, dtype=F64, device="cuda")
         self.up = torch.empty(nc, dtype=F64, device="cuda")
 
-    use_graph = True
+    use_graph = False  # re-captured per preconditioner: costs more than it saves here
 
     def apply_device(self, r, out=None):
         """M^-1 r.  The launch sequence (local GEMVs, coarse gather, the
