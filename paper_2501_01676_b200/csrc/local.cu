@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kTileThreads) schur_row_kernel(
            1.0, 0.0, sm);
 }
 
-constexpr int kTrailBM = 128;
+constexpr int kTrailBM = 64;
 
 __global__ void __launch_bounds__(2 * kTrailBM) schur_trailing_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,

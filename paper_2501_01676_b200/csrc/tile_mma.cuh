@@ -5,7 +5,7 @@
 // m <= BM, n <= 64 and K <= 64.  A and B stream through shared memory in
 // K-chunks of 16 with a 3-stage cp.async pipeline (16-byte copies when the
 // source is 16-byte aligned, 8-byte otherwise; out-of-range elements
-// zero-filled); C is read once, in the epilogue.  B may alias C when one CTA
+// zero-filled); C is read once, at the start (accumulators = (beta/alpha) C).  B may alias C when one CTA
 // owns every row of that C tile and beta == 0 (in-place W = P*W updates):
 // all of B is read before the epilogue writes.
 #pragma once
@@ -101,13 +101,21 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
     if (s < nchunks) tile_issue_chunk(sm, s, s, A, lda, B, ldb, m, n, K, a16, b16);
     cp_async_commit();
   }
-  // accumulators start at zero; C is combined in the epilogue (its load
-  // latency overlaps other CTAs' DMMA work instead of delaying the first MMA)
+  // accumulators start from (beta/alpha) C: C is read once, early, while the
+  // first chunks are in flight
   double acc[4][4][2];
+  const double cscale = (beta != 0.0) ? beta / alpha : 0.0;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
+    const int r = wm + i * 8 + g;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < 4; ++j) {
+      const int c = wn + j * 8 + 2 * t;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        acc[i][j][h] = (cscale != 0.0 && r < m && c + h < n) ? cscale * C[(long long)r * ldc + c + h] : 0.0;
+    }
+  }
   for (int kc = 0; kc < nchunks; ++kc) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
@@ -140,11 +148,7 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
       const int c = wn + j * 8 + 2 * t;
 #pragma unroll
       for (int h = 0; h < 2; ++h)
-        if (c + h < n) {
-          double v = alpha * acc[i][j][h];
-          if (beta != 0.0) v += beta * crow[c + h];
-          crow[c + h] = v;
-        }
+        if (c + h < n) crow[c + h] = alpha * acc[i][j][h];
     }
   }
 }
