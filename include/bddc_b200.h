@@ -225,13 +225,14 @@ int bddc_prolong_primal(const int* nB, const long long* voff, const int* pstart,
 int bddc_gather_reduce(const long long* tstart, const long long* tsrc, const double* y,
                        double* out, long long n, cudaStream_t stream);
 
-/* Coarse solve with the envelope-LU factors of bddc_coarse_factor: forward
- * panel k touches rows [k+64, host_lim[k/64]), backward panel k touches rows
- * [host_first[k/64], k) (host arrays; NULL = dense).  replaces
- * lu_solve(coarse_lu) solver.py:192. */
+/* Coarse solve with the envelope-LU factors of bddc_coarse_factor, one
+ * cooperative persistent launch (grid-wide barrier per 64-wide panel):
+ * forward panel k updates rows [k+64, lim[k/64]), backward panel k updates
+ * rows [first[k/64], k) (device int arrays).  b is overwritten; the solution
+ * is returned in t.  replaces lu_solve(coarse_lu) solver.py:192. */
 int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
-                      long long pinv_step_stride, const int* host_lim, const int* host_first,
-                      double* b, double* t, cudaStream_t stream);
+                      long long pinv_step_stride, const int* lim, const int* first, double* b,
+                      double* t, cudaStream_t stream);
 
 /* ---- krylov.cu : GMRES vector kernels (solver.py:286-310) ------------------ */
 

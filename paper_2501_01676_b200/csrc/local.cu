@@ -167,6 +167,20 @@ __global__ void __launch_bounds__(2 * kTrailBM) schur_trailing_kernel(
                        sm);
 }
 
+// L' = A21 P_k in place on the panel column rows [k+w, lim) (coarse envelope
+// LU: the forward solve then needs no P_k product)
+__global__ void __launch_bounds__(kTileThreads) panel_scale_kernel(double* __restrict__ M,
+                                                                   long long ld, int k, int w,
+                                                                   int lim,
+                                                                   const double* __restrict__ P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int r0 = k + w + blockIdx.x * kTile;
+  if (r0 >= lim) return;
+  double* C = M + (long long)r0 * ld + k;
+  tile_mma(C, ld, min(kTile, lim - r0), w, C, ld, P, kTile, w, 1.0, 0.0, sm);
+}
+
 // ---------------------------------------------------------------------------
 // blocked Gauss-Jordan inversion in place (square n x n, no pivoting)
 // ---------------------------------------------------------------------------
@@ -322,6 +336,7 @@ static int smem_tile_setup() {
     cudaFuncSetAttribute(gj_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(gj_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(panel_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     done = true;
   }
   return (int)sizeof(TileSmem);
@@ -419,7 +434,9 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
 }
 
 // Envelope LU of one n x n matrix (the coarse problem in a bandwidth-reducing
-// order): panel k only updates rows / columns below host_lim[k / 64].
+// order): panel k only updates rows / columns below host_lim[k / 64]; the
+// panel column is stored as L' = A21 P_k (P_k = inverse pivot block, kept in
+// pinv) and the pivot rows as W = P_k A12.  C + off[0] must have ld == n.
 int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const int* nv, int n,
                        const int* host_lim, double* pinv, double* piv_out, int* status,
                        cudaStream_t stream) {
@@ -439,7 +456,8 @@ int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const in
       const int tr = ceil_div(span, kTrailBM);
       schur_row_kernel<<<dim3(t, 1), kTileThreads, smem, stream>>>(C, off, ldv, nv, nv, k, P, 0, lim);
       schur_trailing_kernel<<<dim3(t * tr, 1), 2 * kTrailBM, sizeof(TileSmemT<kTrailBM>), stream>>>(C, off, ldv, nv, nv, nv, k, lim);
-      launches += 2;
+      panel_scale_kernel<<<t, kTileThreads, smem, stream>>>(C, (long long)n, k, w, lim, P);
+      launches += 3;
     }
   }
   bddc_note_launches(launches);

@@ -12,8 +12,12 @@
 // so that M^-1 r = sum_i R_i^T (A_i R_i r + N_i u_P,i),
 //         u_P = C^-1 sum_i P_i^T G_i R_i r     (C = sum_i P_i^T C_i P_i).
 // This is algebraically the reference's Qhat^T Rtil^T Dtil Stil^-1 Dtil^T Rtil Qhat.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "tile_mma.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace bddc {
 
@@ -470,60 +474,57 @@ __global__ void gather_reduce_kernel(const long long* __restrict__ tstart,
 //   forward:  t_k = P_k b_k ; b_i -= A[i, k:k+w] t_k  (i >= k+w)
 //   backward: x_k = t_k     ; t_i -= A[i, k:k+w] x_k  (i < k)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) coarse_fwd_kernel(const double* __restrict__ A, long long ld,
-                                                         int n, int k,
-                                                         const double* __restrict__ Pk,
-                                                         double* __restrict__ b,
-                                                         double* __restrict__ t) {
-  // n here is the row limit of this panel (envelope); n >= k + w
-  __shared__ double Ps[64][65];
-  __shared__ double bk[64];
-  __shared__ double tk[64];
-  const int w = min(64, n - k);
-  for (int i = threadIdx.x; i < 64 * 64; i += blockDim.x) {
-    const int r = i >> 6, c = i & 63;
-    Ps[r][c] = (r < w && c < w) ? Pk[i] : 0.0;
+// Coarse envelope solve in one cooperative persistent kernel (grid-wide
+// barrier per 64-wide panel instead of a kernel launch):
+//   forward  b_i -= L'_ik b_k            i in [k+w, lim_k)
+//   t = blockdiag(P_k) b
+//   backward t_i -= W_ik x_k (x_k = t_k)  i in [first_k, k)
+__global__ void __launch_bounds__(256) coarse_solve_coop_kernel(
+    const double* __restrict__ A, long long ld, int n, const double* __restrict__ pinv,
+    long long pstride, const int* __restrict__ lim, const int* __restrict__ first,
+    double* __restrict__ b, double* __restrict__ t) {
+  cg::grid_group grid = cg::this_grid();
+  const int nP = (n + 63) / 64;
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  for (int p = 0; p < nP; ++p) {
+    const int k = p * 64, w = min(64, n - k), L = min(n, lim[p]);
+    if (p > 0) grid.sync();
+    if (k + w >= L) continue;
+    const double b0 = lane < w ? b[k + lane] : 0.0;
+    const double b1 = lane + 32 < w ? b[k + lane + 32] : 0.0;
+    for (int i = k + w + gw; i < L; i += nwarps) {
+      const double* row = A + (long long)i * ld + k;
+      double s = (lane < w ? row[lane] * b0 : 0.0) + (lane + 32 < w ? row[lane + 32] * b1 : 0.0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) b[i] -= s;
+    }
   }
-  if (threadIdx.x < 64) bk[threadIdx.x] = threadIdx.x < w ? b[k + threadIdx.x] : 0.0;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // t_k = P_k b_k : warp per row, 2 columns per lane
-  for (int r = warp; r < w; r += 8) {
-    double s = Ps[r][lane] * bk[lane] + Ps[r][lane + 32] * bk[lane + 32];
+  grid.sync();
+  for (int r = gw; r < n; r += nwarps) {
+    const int p = r >> 6, k = p * 64, w = min(64, n - k);
+    const double* Pr = pinv + (long long)p * pstride + (r - k) * 64;
+    double s = (lane < w ? Pr[lane] * b[k + lane] : 0.0) +
+               (lane + 32 < w ? Pr[lane + 32] * b[k + lane + 32] : 0.0);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) tk[r] = s;
+    if (lane == 0) t[r] = s;
   }
-  __syncthreads();
-  if (blockIdx.x == 0)
-    for (int r = threadIdx.x; r < w; r += blockDim.x) t[k + r] = tk[r];
-  const int i0 = k + w + blockIdx.x * 32;
-  for (int i = i0 + warp; i < min(n, i0 + 32); i += 8) {
-    const double* row = A + (long long)i * ld + k;
-    double s = 0.0;
-    for (int c = lane; c < w; c += 32) s += row[c] * tk[c];
+  for (int p = nP - 1; p >= 1; --p) {
+    const int k = p * 64, w = min(64, n - k), F = max(0, first[p]);
+    grid.sync();
+    if (F >= k) continue;
+    const double x0 = lane < w ? t[k + lane] : 0.0;
+    const double x1 = lane + 32 < w ? t[k + lane + 32] : 0.0;
+    for (int i = F + gw; i < k; i += nwarps) {
+      const double* row = A + (long long)i * ld + k;
+      double s = (lane < w ? row[lane] * x0 : 0.0) + (lane + 32 < w ? row[lane + 32] * x1 : 0.0);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) b[i] -= s;
-  }
-}
-
-__global__ void __launch_bounds__(256) coarse_bwd_kernel(const double* __restrict__ A, long long ld,
-                                                         int n, int k, int first,
-                                                         double* __restrict__ t) {
-  __shared__ double xk[64];
-  const int w = min(64, n - k);
-  if (threadIdx.x < 64) xk[threadIdx.x] = threadIdx.x < w ? t[k + threadIdx.x] : 0.0;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i0 = first + blockIdx.x * 32;
-  for (int i = i0 + warp; i < min(k, i0 + 32); i += 8) {
-    const double* row = A + (long long)i * ld + k;
-    double s = 0.0;
-    for (int c = lane; c < w; c += 32) s += row[c] * xk[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) t[i] -= s;
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) t[i] -= s;
+    }
   }
 }
 
@@ -686,26 +687,24 @@ int bddc_gather_reduce(const long long* tstart, const long long* tsrc, const dou
 }
 
 int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
-                      long long pinv_step_stride, const int* host_lim, const int* host_first,
-                      double* b, double* t, cudaStream_t stream) {
+                      long long pinv_step_stride, const int* lim, const int* first, double* b,
+                      double* t, cudaStream_t stream) {
   if (n <= 0) return 0;
-  int launches = 0;
-  for (int k = 0; k < n; k += 64) {
-    const int w = min(64, n - k);
-    const int lim = host_lim ? min(n, host_lim[k / 64]) : n;
-    const int blocks = max(1, ceil_div(lim - k - w, 32));
-    coarse_fwd_kernel<<<blocks, 256, 0, stream>>>(A, ld, lim, k, pinv + (long long)(k / 64) * pinv_step_stride, b, t);
-    ++launches;
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_solve_coop_kernel, 256, 0);
+    grid = sms * (per_sm >= 1 ? 1 : 0);
+    if (grid <= 0) grid = 1;
   }
-  const int last = ((n - 1) / 64) * 64;
-  for (int k = last; k > 0; k -= 64) {
-    const int first = host_first ? max(0, host_first[k / 64]) : 0;
-    if (first >= k) continue;
-    coarse_bwd_kernel<<<ceil_div(k - first, 32), 256, 0, stream>>>(A, ld, n, k, first, t);
-    ++launches;
-  }
-  bddc_note_launches(launches);
-  return pc_status();
+  void* args[] = {(void*)&A, (void*)&ld, (void*)&n, (void*)&pinv, (void*)&pinv_step_stride,
+                  (void*)&lim, (void*)&first, (void*)&b, (void*)&t};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)coarse_solve_coop_kernel, dim3(grid),
+                                              dim3(256), args, 0, stream);
+  bddc_note_launches(1);
+  return e == cudaSuccess ? pc_status() : -(int)e;
 }
 
 }  // extern "C"

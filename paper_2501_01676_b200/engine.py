@@ -564,6 +564,7 @@ class DevicePreconditioner:
         status1 = torch.zeros(1, dtype=torch.int32, device="cuda")
         self._lim_c = (ctypes.c_int * steps)(*self.lim.tolist())
         self._first_c = (ctypes.c_int * steps)(*self.first.tolist())
+        self.d_lim, self.d_first = dev_i32(self.lim), dev_i32(self.first)
         lib.bddc_coarse_factor(C, dev_i64([0]), dev_i32([nc]), dev_i32([nc]), nc,
                                ctypes.cast(self._lim_c, ctypes.c_void_p), self.coarse_pinv, piv,
                                status1, st)
@@ -618,8 +619,7 @@ class DevicePreconditioner:
                             self.d_poff, self.G, self.cvals, p.N, nbmax, 2, st)
         lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp, self.n_primal, st)
         lib.bddc_coarse_solve(self.coarse_lu, self.n_primal, self.n_primal, self.coarse_pinv, 4096,
-                              ctypes.cast(self._lim_c, ctypes.c_void_p),
-                              ctypes.cast(self._first_c, ctypes.c_void_p), self.rp, self.up, st)
+                              self.d_lim, self.d_first, self.rp, self.up, st)
         lib.bddc_prolong_primal(d.nB, d.voff, self.d_pstart, self.d_pgid, self.d_poff, self.Nt,
                                 self.up, self.y, p.N, st)
         lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n_hat, st)

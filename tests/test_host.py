@@ -89,6 +89,7 @@ def _envelope_solve(C, lim, first):
         P.append(Pk)
         A[k:k + w, k + w:L] = Pk @ A[k:k + w, k + w:L]
         A[k + w:L, k + w:L] -= A[k + w:L, k:k + w] @ A[k:k + w, k + w:L]
+        A[k + w:L, k:k + w] = A[k + w:L, k:k + w] @ Pk   # L' = A21 P_k (panel_scale_kernel)
     return A, P
 
 
@@ -117,11 +118,13 @@ def test_coarse_envelope_exact(seed):
     A, P = _envelope_solve(Cn, lim, first)
     b = rng.standard_normal(n_c)
     bb, t = b.copy(), np.zeros(n_c)
-    for k in range(0, n_c, 64):
+    for k in range(0, n_c, 64):      # forward with L' (coarse_solve_coop_kernel)
         w = min(64, n_c - k)
         L = min(n_c, lim[k // 64])
+        bb[k + w:L] -= A[k + w:L, k:k + w] @ bb[k:k + w]
+    for k in range(0, n_c, 64):      # t = blockdiag(P) b
+        w = min(64, n_c - k)
         t[k:k + w] = P[k // 64] @ bb[k:k + w]
-        bb[k + w:L] -= A[k + w:L, k:k + w] @ t[k:k + w]
     for k in range(((n_c - 1) // 64) * 64, 0, -64):
         w = min(64, n_c - k)
         f = first[k // 64]
