@@ -3,14 +3,14 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
                     [--config 5] [--n N --subs S]
 
-One step = the whole hot path on one problem: local assembly and Schur
+One step = the whole hot path on one problem: symbolic plan (index maps, on
+the device), local assembly and Schur
 elimination, Bsym^-1, deluxe scaling, face and new-edge GEPs with their
 change of basis, preconditioner setup with the coarse LU, left-preconditioned
 GMRES (rtol 1e-8) and interior recovery.  ``value`` is with element blocks,
-connectivity and the symbolic plan resident in HBM; ``e2e`` starts from host
-(numpy) element blocks through the package API and includes the symbolic
-plan, the pinned host->device copies and the device->host copy of the nodal
-solution.  Workload (BASELINE.json configs[4]): 128^3 cells (6 Kuhn tets /
+connectivity, partition and Dirichlet data resident in HBM; ``e2e`` starts
+from host (numpy) arrays through the package API and includes the
+host->device copies and the device->host copy of the nodal solution.  Workload (BASELINE.json configs[4]): 128^3 cells (6 Kuhn tets /
 cell, 2,048,383 DOFs), 16^3 subdomains (H/h = 8), nu = 1e-2, b = (1,1,1),
 f = 1, c = 1, Theta = 10.  Working set (~50 GB) >> L2, so no flush is needed.
 
@@ -229,24 +229,20 @@ def run_mine(args):
     _build.build()
     from paper_2501_01676_b200 import configs, pipeline
     from paper_2501_01676_b200._lib import lib
-    from paper_2501_01676_b200.engine import DevicePlan, trailing_flops, upload_inputs
-    from paper_2501_01676_b200.plan import Plan
+    from paper_2501_01676_b200.engine import trailing_flops, upload_inputs
 
     cfg = args.config
     t0 = time.perf_counter()
     prob = configs.build_problem(cfg, n=args.n, subs=args.subs)
     t_pre = time.perf_counter() - t0
     n_cells = prob.mesh.cells[0]
-    t0 = time.perf_counter()
-    plan = Plan(prob.system, prob.partition, prob.globs)
-    t_plan = time.perf_counter() - t0
-    dplan = DevicePlan(plan)
-    inputs = upload_inputs(prob.system)
+    inputs = upload_inputs(prob.system, prob.partition)
     torch.cuda.synchronize()
 
     def step(kernel_timing=False):
+        # the symbolic plan (index maps) is rebuilt inside every step
         return pipeline.run(prob.system, prob.partition, prob.globs, THETA, THETA, "new",
-                            plan=plan, inputs=inputs, dplan=dplan, kernel_timing=kernel_timing)
+                            inputs=inputs, kernel_timing=kernel_timing)
 
     for _ in range(max(args.warmup, 3)):
         res = step()
@@ -284,7 +280,8 @@ def run_mine(args):
 
     # apply-path bandwidth: one M^-1 and one S_hat application (HBM bound)
     keep = pipeline.run(prob.system, prob.partition, prob.globs, THETA, THETA, "new",
-                        plan=plan, inputs=inputs, dplan=dplan, keep=True)
+                        inputs=inputs, keep=True)
+    plan = keep.ls.plan
     pc, op = keep.pc, keep.op
     r = torch.randn(plan.n_hat, dtype=torch.float64, device="cuda")
     out = torch.empty_like(r)
@@ -313,27 +310,20 @@ def run_mine(args):
         + 8 * pc.n_primal * pc.n_primal
     del keep, pc, op
 
-    # e2e through the host API: numpy element blocks -> plan -> pinned H2D -> solve -> D2H u
+    # e2e through the host API: numpy element blocks -> H2D -> plan -> solve -> D2H u
     sysm = prob.system
     h2d = (sysm.elem_matrices.nbytes + sysm.elem_rhs.nbytes + prob.mesh.elements.size * 8
-           + sysm.dirichlet_values.nbytes)
+           + sysm.dirichlet_values.nbytes + sysm.node_to_free.size + prob.partition.subdomain_of.size * 8)
     e2e_ms = []
     for _ in range(args.e2e_steps):
         torch.cuda.synchronize()
         w0 = time.perf_counter()
-        pl = Plan(sysm, prob.partition, prob.globs)
-        dp = DevicePlan(pl)
-        inp = upload_inputs(sysm, pinned=True)
-        rr = pipeline.run(sysm, prob.partition, prob.globs, THETA, THETA, "new", plan=pl,
-                          inputs=inp, dplan=dp)
+        inp = upload_inputs(sysm, prob.partition)
+        rr = pipeline.run(sysm, prob.partition, prob.globs, THETA, THETA, "new", inputs=inp)
         u_host = rr.u.cpu().numpy()
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - w0) * 1e3)
-        del rr, inp, dp
-    plan_bytes = sum(getattr(plan, k).nbytes for k in ("off", "ld", "nI", "nB", "nL", "soff", "voff",
-                     "ioff", "elem_start", "elem_ids", "loc4", "iface_perm", "I_nodes", "tstart",
-                     "tsrc", "pos2k", "sub_globs", "sub_glob_boff", "sub_glob_sh", "sub_glob_start",
-                     "kind", "gsize", "sh_start", "sh_sub", "sh_boff", "sh_doff", "slot_glob"))
+        del rr, inp
     e2e_step_ms = float(np.mean(e2e_ms))
 
     tflops = trailing_flops(plan)
@@ -367,12 +357,12 @@ def run_mine(args):
         "phases_ms": phases,
         "iterations": res.iterations, "converged": bool(res.converged),
         "pnumF": res.pnumF, "pnumE": res.pnumE, "n_vertex": res.n_vertex, "n_c": res.n_c,
-        "host_preprocessing_s": t_pre, "symbolic_plan_s": t_plan,
+        "host_preprocessing_s": t_pre,
         "clocks": clk,
         "e2e": {"value": dofs / (e2e_step_ms * 1e-3), "unit": "DOF/s",
-                "h2d_bytes_per_step": int(h2d + plan_bytes), "d2h_bytes_per_step": int(u_host.nbytes),
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(u_host.nbytes),
                 "ms_per_step": e2e_step_ms,
-                "includes": "symbolic plan (host), pinned H2D of element blocks + plan, full hot path, D2H of nodal u"},
+                "includes": "H2D of element blocks/connectivity/partition/Dirichlet data, symbolic plan, full hot path, D2H of nodal u"},
         "gpu_launches": launches,
     }
     if rank == 0 and not args.no_cpu_baseline:

@@ -81,14 +81,16 @@ class LocalSystem:
         self.kernel_timing = kernel_timing
         self.trailing_ms = None
         self.system, self.partition, self.globs = system, partition, globs
-        self.plan = plan or Plan(system, partition, globs)
+        if inputs is None:
+            inputs = upload_inputs(system, partition)
+        self.inputs = inputs
+        if plan is None:
+            plan = Plan(system, partition, globs, device_inputs=inputs)
+        self.plan = plan
         self.plan.check()
         p = self.plan
         self.N = p.N
         self.d = dplan if dplan is not None else DevicePlan(p)
-        if inputs is None:
-            inputs = upload_inputs(system)
-        self.inputs = inputs
         self._Binv = None
         self.timer = timer
         self._factor()
@@ -137,6 +139,12 @@ class LocalSystem:
             self._Binv = Binv
         return self._Binv
 
+    @property
+    def interior_nodes_host(self):
+        if getattr(self, "_inodes", None) is None:
+            self._inodes = self.plan.I_nodes_host
+        return self._inodes
+
     # host views (glob-major order) ------------------------------------------
     def matrix(self, buf, i):
         p = self.plan
@@ -183,10 +191,13 @@ class DevicePlan:
         self.voff = dev_i64(p.voff)
         self.ioff = dev_i64(p.ioff)
         self.elem_start = dev_i64(p.elem_start)
-        self.elem_ids = dev_i64(p.elem_ids)
-        self.loc4 = dev_i32(p.loc4)
+        if p.on_device:
+            self.elem_ids, self.loc4, self.I_nodes = p.elem_ids_d, p.loc4_d, p.I_nodes_d
+        else:
+            self.elem_ids = dev_i64(p.elem_ids)
+            self.loc4 = dev_i32(p.loc4)
+            self.I_nodes = dev_i64(p.I_nodes)
         self.iface_perm = dev_i32(p.iface_perm)
-        self.I_nodes = dev_i64(p.I_nodes)
         self.tstart = dev_i64(p.tstart)
         self.tsrc = dev_i64(p.tsrc)
         self.pos2k = dev_i32(p.pos2k)
@@ -203,19 +214,24 @@ class DevicePlan:
         self.slot_glob = dev_i32(p.slot_glob)
 
 
-def upload_inputs(system, pinned=False):
-    """Element blocks, connectivity and Dirichlet data to the device."""
+def upload_inputs(system, partition=None, pinned=False):
+    """Element blocks, connectivity, Dirichlet data (and the element ->
+    subdomain map, for the device-side symbolic plan) to the device."""
     def up(a, dt):
         t = torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
         if pinned:
             t = t.pin_memory()
         return t.cuda(non_blocking=pinned)
-    return {
+    out = {
         "Ke": up(system.elem_matrices.reshape(-1, 16), np.float64),
         "Fe": up(system.elem_rhs.reshape(-1, 4), np.float64),
         "conn": up(system.mesh.elements, np.int64),
         "gdir": up(system.dirichlet_values, np.float64),
+        "free": up(np.asarray(system.node_to_free) >= 0, np.bool_),
     }
+    if partition is not None:
+        out["sub_of"] = up(partition.subdomain_of, np.int64)
+    return out
 
 
 # ---------------------------------------------------------------------------

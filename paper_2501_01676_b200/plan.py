@@ -1,5 +1,5 @@
-"""Host symbolic plan: index maps from (system, partition, globs) to the
-batched device layout.  Integer work only; the numbers are all on the GPU.
+"""Symbolic plan: integer index maps from (system, partition, globs) to the
+batched device layout.  No floating-point work.
 
 Local numbering per subdomain (reference substructuring.py:85-96 sorts B and
 I dofs by global node id; here B dofs are *glob-major*: the subdomain's globs
@@ -7,6 +7,13 @@ in glob order, each glob's nodes in glob order, so every glob is a
 contiguous block and the per-glob change of basis, deluxe blocks and prior
 rows are contiguous block operations).  Interior dofs stay sorted by node
 id.  Nothing downstream depends on the ordering beyond rounding.
+
+Two builders produce identical plans:
+* ``Plan(system, partition, globs)`` — numpy on the host (reference for tests);
+* ``Plan(..., device_inputs={"conn": ..., "sub_of": ...})`` — the per-element
+  part (the only part that scales with the mesh: 4 x n_elements entries) runs
+  as torch sort / unique / searchsorted on the GPU and stays resident there.
+  The glob part (O(sum nB)) is always host numpy.
 """
 
 import numpy as np
@@ -32,14 +39,22 @@ def _excl(a):
 
 
 class Plan:
-    def __init__(self, system, partition, globs):
-        mesh = system.mesh
+    def __init__(self, system, partition, globs, device_inputs=None):
         N = int(partition.n_subdomains)
-        sub_of = np.asarray(partition.subdomain_of, dtype=np.int64)
-        el = np.asarray(mesh.elements, dtype=np.int64)
-        n_nodes = mesh.n_nodes
         self.N = N
+        self.n_nodes = system.mesh.n_nodes
         self.n_hat = int(globs.interface_nodes.size)
+        self.on_device = device_inputs is not None
+        self._glob_part(globs)
+        if self.on_device:
+            self._element_part_torch(system, partition, device_inputs)
+        else:
+            self._element_part_numpy(system, partition)
+        self._layout()
+
+    # -- globs: sharers, glob-major B order, interface maps (host) ----------
+    def _glob_part(self, globs):
+        N = self.N
         gl = globs.globs
         G = len(gl)
         self.G = G
@@ -51,12 +66,9 @@ class Plan:
                        if G else np.zeros(0, np.int64)).astype(np.int32)
         slot_glob = np.repeat(np.arange(G, dtype=np.int64), nsh)
         self.slot_glob = slot_glob.astype(np.int32)
-        # D blocks per (glob, sharer) slot
         self.sh_doff = _excl(self.gsize[slot_glob].astype(np.int64) ** 2)
         self.d_total = int(self.sh_doff[-1])
         self.sh_doff = self.sh_doff[:-1]
-
-        # per-subdomain glob lists in glob order
         order = np.lexsort((slot_glob, self.sh_sub.astype(np.int64)))
         self.sub_globs = slot_glob[order].astype(np.int32)
         pair_sub = self.sh_sub[order].astype(np.int64)
@@ -64,23 +76,30 @@ class Plan:
         self.sub_glob_start = np.searchsorted(pair_sub, np.arange(N + 1)).astype(np.int32)
         sizes_k = self.gsize[self.sub_globs].astype(np.int64)
         cs = _excl(sizes_k)
-        boff = cs[:-1] - cs[self.sub_glob_start[:-1]][np.repeat(np.arange(N), np.diff(self.sub_glob_start))] \
-            if sizes_k.size else np.zeros(0, np.int64)
+        if sizes_k.size:
+            owner = np.repeat(np.arange(N), np.diff(self.sub_glob_start))
+            boff = cs[:-1] - cs[self.sub_glob_start[:-1]][owner]
+        else:
+            boff = np.zeros(0, np.int64)
         self.sub_glob_boff = boff.astype(np.int32)
         self.sh_boff = np.empty(order.size, dtype=np.int32)
         self.sh_boff[order] = self.sub_glob_boff
         self.nB = np.bincount(pair_sub, weights=sizes_k, minlength=N).astype(np.int64)
         self.voff = _excl(self.nB)
-
-        # glob-major B nodes and global interface positions
         gnodes = np.concatenate([g.nodes for g in gl]).astype(np.int64) if G else np.zeros(0, np.int64)
         gstart = _excl(self.gsize)
-        idx = _ranges(gstart[self.sub_globs], sizes_k)
-        self.B_nodes = gnodes[idx]
+        self.B_nodes = gnodes[_ranges(gstart[self.sub_globs], sizes_k)]
         self.iface_perm = np.searchsorted(globs.interface_nodes, self.B_nodes).astype(np.int32)
         self.pos2k = np.repeat(np.arange(self.sub_globs.size, dtype=np.int32), sizes_k)
+        src = np.argsort(self.iface_perm, kind="stable")
+        self.tsrc = src.astype(np.int64)
+        self.tstart = np.searchsorted(self.iface_perm[src], np.arange(self.n_hat + 1)).astype(np.int64)
 
-        # interior nodes: free nodes touched by exactly one subdomain
+    # -- elements: interior dofs, element lists, element-local indices ------
+    def _element_part_numpy(self, system, partition):
+        N, n_nodes = self.N, self.n_nodes
+        sub_of = np.asarray(partition.subdomain_of, dtype=np.int64)
+        el = np.asarray(system.mesh.elements, dtype=np.int64)
         key = np.unique((el * N + sub_of[:, None]).ravel())
         node, sub = key // N, key % N
         cnt = np.bincount(node, minlength=n_nodes)
@@ -91,13 +110,13 @@ class Plan:
         self.I_nodes = I_node[o]
         self.nI = np.bincount(I_sub, minlength=N).astype(np.int64)
         self.ioff = _excl(self.nI)
-        self.nL = self.nI + self.nB
-
-        # element lists and local indices of their nodes
         eorder = np.argsort(sub_of, kind="stable")
         self.elem_ids = eorder.astype(np.int64)
         self.elem_start = _excl(np.bincount(sub_of, minlength=N))
-        self.max_elems = int(np.diff(self.elem_start).max()) if N else 0
+        self.loc4 = self._local_index_numpy(el[eorder], sub_of[eorder])
+
+    def _local_index_numpy(self, conn, sub):
+        N, n_nodes = self.N, self.n_nodes
         Bsub = np.repeat(np.arange(N, dtype=np.int64), self.nB)
         Bloc = np.arange(self.B_nodes.size, dtype=np.int64) - self.voff[Bsub] + self.nI[Bsub]
         Isub = np.repeat(np.arange(N, dtype=np.int64), self.nI)
@@ -106,14 +125,55 @@ class Plan:
         vals = np.concatenate([Bloc, Iloc])
         ko = np.argsort(keys)
         keys, vals = keys[ko], vals[ko]
-        q = sub_of[eorder][:, None] * n_nodes + el[eorder]
-        pos = np.searchsorted(keys, q)
-        pos = np.minimum(pos, keys.size - 1)
+        q = sub[:, None] * n_nodes + conn
+        pos = np.minimum(np.searchsorted(keys, q), keys.size - 1)
         found = keys[pos] == q
-        big = np.int64(2 ** 30)
-        self.loc4 = np.where(found, vals[pos], big).astype(np.int32)
+        return np.where(found, vals[pos], np.int64(2 ** 30)).astype(np.int32)
 
-        # local matrix layout [I|B] x [I|B|f]
+    def _element_part_torch(self, system, partition, dev):
+        import torch
+
+        N, n_nodes = self.N, self.n_nodes
+        conn = dev["conn"]                     # (E, 4) int64 on the GPU
+        sub_of = dev["sub_of"]                 # (E,) int64 on the GPU
+        free = dev.get("free")
+        if free is None:
+            free = torch.from_numpy(np.asarray(system.node_to_free) >= 0).to(conn.device)
+        key = torch.unique(conn * N + sub_of[:, None])
+        node, sub = key // N, key % N
+        cnt = torch.bincount(node, minlength=n_nodes)
+        interior = (cnt[node] == 1) & free[node]
+        I_node, I_sub = node[interior], sub[interior]
+        k2 = torch.sort(I_sub * n_nodes + I_node).values
+        I_sub, I_node = k2 // n_nodes, k2 % n_nodes
+        nI = torch.bincount(I_sub, minlength=N)
+        self.nI = nI.cpu().numpy().astype(np.int64)
+        self.ioff = _excl(self.nI)
+        self.I_nodes_d = I_node
+        eorder = torch.sort(sub_of, stable=True).indices
+        self.elem_ids_d = eorder
+        self.elem_start = _excl(torch.bincount(sub_of, minlength=N).cpu().numpy())
+        dv = conn.device
+        Bsub = torch.repeat_interleave(torch.arange(N, device=dv), torch.from_numpy(self.nB).to(dv))
+        voff = torch.from_numpy(self.voff).to(dv)
+        nI_d = nI.to(torch.int64)
+        Bloc = torch.arange(self.B_nodes.size, device=dv) - voff[Bsub] + nI_d[Bsub]
+        Bn = torch.from_numpy(self.B_nodes).to(dv)
+        ioff = torch.from_numpy(self.ioff).to(dv)
+        Isub = I_sub
+        Iloc = torch.arange(I_node.numel(), device=dv) - ioff[Isub]
+        keys = torch.cat([Bsub * n_nodes + Bn, Isub * n_nodes + I_node])
+        vals = torch.cat([Bloc, Iloc])
+        keys, ko = torch.sort(keys)
+        vals = vals[ko]
+        q = sub_of[eorder][:, None] * n_nodes + conn[eorder]
+        pos = torch.clamp(torch.searchsorted(keys, q.reshape(-1)), max=keys.numel() - 1).reshape(q.shape)
+        found = keys[pos] == q
+        self.loc4_d = torch.where(found, vals[pos], torch.full_like(pos, 2 ** 30)).to(torch.int32)
+
+    def _layout(self):
+        self.nL = self.nI + self.nB
+        self.max_elems = int(np.diff(self.elem_start).max()) if self.N else 0
         self.ld = (self.nL + 2) // 2 * 2  # >= nL + 1, even
         self.off = _excl(self.nL * self.ld)
         self.K_total = int(self.off[-1])
@@ -122,28 +182,22 @@ class Plan:
         self.S_total = int(self.soff[-1])
         self.soff = self.soff[:-1]
 
-        # interface CSR (gather-reduce of local vectors)
-        src = np.argsort(self.iface_perm, kind="stable")
-        self.tsrc = src.astype(np.int64)
-        self.tstart = np.searchsorted(self.iface_perm[src], np.arange(self.n_hat + 1)).astype(np.int64)
+    # -- host views of the element part -----------------------------------
+    @property
+    def I_nodes_host(self):
+        return self.I_nodes_d.cpu().numpy() if self.on_device else self.I_nodes
 
     def check(self):
         """Reference errors of build_subdomain_operator (substructuring.py:93-96)."""
-        for i in range(self.N):
-            if self.elem_start[i + 1] == self.elem_start[i]:
+        bad_e = np.flatnonzero(np.diff(self.elem_start) == 0)
+        bad_b = np.flatnonzero(self.nB == 0)
+        bad_i = np.flatnonzero(self.nI == 0)
+        for i in sorted(set(bad_e.tolist()) | set(bad_b.tolist()) | set(bad_i.tolist())):
+            if i in bad_e:
                 raise ValueError(f"subdomain {i} has no elements")
-            if self.nB[i] == 0:
+            if i in bad_b:
                 raise ValueError(f"subdomain {i} has no interface unknowns")
-            if self.nI[i] == 0:
-                raise ValueError(f"subdomain {i} has no interior unknowns")
-
-    def glob_positions(self, sub, g):
-        """Glob-major local block (start, size) of glob g in subdomain sub."""
-        k0, k1 = self.sub_glob_start[sub], self.sub_glob_start[sub + 1]
-        ks = np.flatnonzero(self.sub_globs[k0:k1] == g)
-        if ks.size == 0:
-            return None
-        return int(self.sub_glob_boff[k0 + ks[0]]), int(self.gsize[g])
+            raise ValueError(f"subdomain {i} has no interior unknowns")
 
     def nodal_order(self, sub):
         """Permutation p with B_glob_major[p] = sorted interface nodes of sub."""

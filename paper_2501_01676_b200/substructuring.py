@@ -40,7 +40,7 @@ class SubdomainOperator:
         self._perm = p.nodal_order(sub_id)  # glob-major -> nodal
         gm_nodes = p.B_nodes[p.voff[sub_id]:p.voff[sub_id + 1]]
         self.interface_nodes = gm_nodes[self._perm]
-        self.interior_nodes = p.I_nodes[p.ioff[sub_id]:p.ioff[sub_id + 1]]
+        self.interior_nodes = ls.interior_nodes_host[p.ioff[sub_id]:p.ioff[sub_id + 1]]
         self.iface_index = ls.globs.interface_index(self.interface_nodes)
         self._pos = {int(n): k for k, n in enumerate(self.interface_nodes)}
 

@@ -167,3 +167,19 @@ def test_operator_views_match_reference_order():
         Bi = ops[i].bsym_inverse()
         np.testing.assert_allclose(Bi, g[f"Binv_{i}"], rtol=0, atol=1e-10 * np.abs(g[f"Binv_{i}"]).max())
         assert np.allclose(ops[i].Bsym, ops[i].Bsym.T)
+
+
+@pytest.mark.parametrize("name", ["jump", "cfg4_small", "cfg1"])
+def test_device_plan_matches_host_plan(name):
+    from paper_2501_01676_b200.engine import upload_inputs
+    from paper_2501_01676_b200.plan import Plan
+
+    system, part, globs = inputs(name)
+    host = Plan(system, part, globs)
+    dev = Plan(system, part, globs, device_inputs=upload_inputs(system, part))
+    assert np.array_equal(host.nI, dev.nI)
+    assert np.array_equal(host.elem_start, dev.elem_start)
+    assert np.array_equal(host.I_nodes, dev.I_nodes_d.cpu().numpy())
+    assert np.array_equal(host.elem_ids, dev.elem_ids_d.cpu().numpy())
+    assert np.array_equal(host.loc4, dev.loc4_d.cpu().numpy())
+    assert host.K_total == dev.K_total and host.S_total == dev.S_total

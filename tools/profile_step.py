@@ -15,16 +15,12 @@ args = ap.parse_args()
 import torch  # noqa: E402
 
 from paper_2501_01676_b200 import configs, pipeline  # noqa: E402
-from paper_2501_01676_b200.engine import DevicePlan, upload_inputs  # noqa: E402
-from paper_2501_01676_b200.plan import Plan  # noqa: E402
+from paper_2501_01676_b200.engine import upload_inputs  # noqa: E402
 
 prob = configs.build_problem(args.config, n=args.n, subs=args.subs)
-plan = Plan(prob.system, prob.partition, prob.globs)
-dplan = DevicePlan(plan)
-inputs = upload_inputs(prob.system)
+inputs = upload_inputs(prob.system, prob.partition)
 for _ in range(args.steps):
     t0 = time.time()
-    res = pipeline.run(prob.system, prob.partition, prob.globs, 10.0, 10.0, "new", plan=plan,
-                       inputs=inputs, dplan=dplan)
+    res = pipeline.run(prob.system, prob.partition, prob.globs, 10.0, 10.0, "new", inputs=inputs)
     torch.cuda.synchronize()
     print(f"step {time.time() - t0:.3f}s iters {res.iterations} n_c {res.n_c} phases {res.times_ms}", flush=True)
