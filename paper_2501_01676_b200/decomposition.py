@@ -70,6 +70,7 @@ class GlobSet:
         else:
             self.interface_nodes = np.zeros(0, dtype=np.int64)
         self._pos = {id(g): k for k, g in enumerate(globs)}
+        self._flat = flatten_globs(globs)  # array form consumed by the symbolic plan
 
     @property
     def faces(self):
@@ -86,6 +87,11 @@ class GlobSet:
     def index(self, g):
         return self._pos[id(g)]
 
+    def flat(self):
+        """Flat arrays of the glob list (kind code, size, sharers, nodes),
+        built with the GlobSet: the symbolic plan's input format."""
+        return self._flat
+
     def glob_id(self, g):
         return f"{g.kind[0].upper()}{self._pos[id(g)]}"
 
@@ -98,6 +104,20 @@ class GlobSet:
             bad = nodes[self.interface_nodes[pos] != nodes][0] if self.interface_nodes.size else nodes[0]
             raise KeyError(int(bad))
         return pos.astype(np.int64)
+
+
+_KIND_CODE = {"face": 0, "edge": 1, "vertex": 2}
+
+
+def flatten_globs(globs):
+    """(kind, size, sharer_count, sharers_flat, nodes_flat) of a glob list."""
+    kind = np.fromiter((_KIND_CODE[g.kind] for g in globs), dtype=np.int32, count=len(globs))
+    size = np.fromiter((len(g.nodes) for g in globs), dtype=np.int32, count=len(globs))
+    nsh = np.fromiter((len(g.sharers) for g in globs), dtype=np.int64, count=len(globs))
+    sharers = (np.fromiter((s for g in globs for s in g.sharers), dtype=np.int64, count=int(nsh.sum()))
+               if globs else np.zeros(0, np.int64))
+    nodes = np.concatenate([g.nodes for g in globs]).astype(np.int64) if globs else np.zeros(0, np.int64)
+    return {"kind": kind, "size": size, "nsh": nsh, "sharers": sharers, "nodes": nodes}
 
 
 _TET_EDGES = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))

