@@ -21,20 +21,24 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-I", INCLUDE]
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, defines=(), out=None):
+    """Compile csrc/*.cu into OUT (or `out`), optionally with -D defines
+    (tuning variants for tools/bench_tile.py)."""
+    global OUT
+    target = out or OUT
     sources = sorted(glob.glob(os.path.join(SRC, "*.cu")))
     deps = sources + glob.glob(os.path.join(SRC, "*.cuh")) + glob.glob(os.path.join(SRC, "*.h"))
-    if not force and os.path.exists(OUT):
-        if os.path.getmtime(OUT) >= max(os.path.getmtime(d) for d in deps):
-            return OUT
-    objdir = os.path.join(HERE, "build")
+    if not force and not defines and os.path.exists(target):
+        if os.path.getmtime(target) >= max(os.path.getmtime(d) for d in deps):
+            return target
+    objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
     for s in sources:
         o = os.path.join(objdir, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
-        cmd = [NVCC, *FLAGS, "-c", s, "-o", o]
+        cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-c", s, "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -44,11 +48,11 @@ def build(force=False, verbose=False):
             raise RuntimeError(f"nvcc failed on {s}:\n{out.decode()}")
         if verbose and out:
             sys.stdout.write(out.decode())
-    tmp = OUT + ".tmp"
+    tmp = target + ".tmp"
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a",
                            *objs, "-o", tmp, "-lcudart"])
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

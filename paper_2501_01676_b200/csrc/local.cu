@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(256) pivot_inverse_kernel(
 // Schur elimination (LU-style, rows below only):
 //   W = A11^-1 A12 stored over A12;   A22 -= A21 W
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTileThreads) schur_row_kernel(
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_row_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ ncols, int k,
     const double* __restrict__ pinv, long long pinv_stride, int lim) {
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kTileThreads) schur_row_kernel(
 
 constexpr int kTrailBM = 64;
 
-__global__ void __launch_bounds__(2 * kTrailBM) schur_trailing_kernel(
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ nrows, const int* __restrict__ ncols,
     int k, int lim) {
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(2 * kTrailBM) schur_trailing_kernel(
 
 // L' = A21 P_k in place on the panel column rows [k+w, lim) (coarse envelope
 // LU: the forward solve then needs no P_k product)
-__global__ void __launch_bounds__(kTileThreads) panel_scale_kernel(double* __restrict__ M,
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) panel_scale_kernel(double* __restrict__ M,
                                                                    long long ld, int k, int w,
                                                                    int lim,
                                                                    const double* __restrict__ P) {
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kTileThreads) panel_scale_kernel(double* __res
 // ---------------------------------------------------------------------------
 // blocked Gauss-Jordan inversion in place (square n x n, no pivoting)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTileThreads) gj_row_kernel(
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_row_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ n, int k, const double* __restrict__ pinv, long long pinv_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kTileThreads) gj_row_kernel(
            0.0, sm);
 }
 
-__global__ void __launch_bounds__(kTileThreads) gj_update_kernel(
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ n, int k) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kTileThreads) gj_update_kernel(
            M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm);
 }
 
-__global__ void __launch_bounds__(kTileThreads) gj_col_kernel(
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ n, int k, const double* __restrict__ pinv, long long pinv_stride) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -391,7 +391,7 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
     }
     if (ct > 0 && rt > 0) {
       if (ev) cudaEventRecord(ev[2 * timed], stream);
-      schur_trailing_kernel<<<dim3(ct * rt, nbatch), 2 * kTrailBM, sizeof(TileSmemT<kTrailBM>), stream>>>(
+      schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, sizeof(TileSmemT<kTrailBM>), stream>>>(
           M, off, ld, npiv, nrows, ncols, k, 0x7fffffff);
       ++launches;
       if (ev) cudaEventRecord(ev[2 * timed + 1], stream);
@@ -455,7 +455,7 @@ int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const in
       const int t = ceil_div(span, kTile);
       const int tr = ceil_div(span, kTrailBM);
       schur_row_kernel<<<dim3(t, 1), kTileThreads, smem, stream>>>(C, off, ldv, nv, nv, k, P, 0, lim);
-      schur_trailing_kernel<<<dim3(t * tr, 1), 2 * kTrailBM, sizeof(TileSmemT<kTrailBM>), stream>>>(C, off, ldv, nv, nv, nv, k, lim);
+      schur_trailing_kernel<<<dim3(t * tr, 1), kTileThreads, sizeof(TileSmemT<kTrailBM>), stream>>>(C, off, ldv, nv, nv, nv, k, lim);
       panel_scale_kernel<<<t, kTileThreads, smem, stream>>>(C, (long long)n, k, w, lim, P);
       launches += 3;
     }

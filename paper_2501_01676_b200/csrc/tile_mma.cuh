@@ -1,7 +1,8 @@
 // BM x 64 fp64 tile GEMM on the DMMA pipe (mma.sync m8n8k4.f64, sm_100a).
 //
-// One CTA of 2*BM threads ((BM/32) x 2 warps, 32x32 per warp = 4x4 DMMA
-// tiles) computes   C[m x n] = beta*C + alpha * A[m x K] * B[K x n]   with
+// One CTA ((BM/32) x (64/kWN) warps, 32 x kWN per warp; default kWN = 16,
+// 8 warps, <= 64 registers so 4 CTAs fit per SM — measured best with
+// tools/bench_tile.py) computes   C[m x n] = beta*C + alpha * A[m x K] * B[K x n]   with
 // m <= BM, n <= 64 and K <= 64.  A and B stream through shared memory in
 // K-chunks of 16 with a 3-stage cp.async pipeline (16-byte copies when the
 // source is 16-byte aligned, 8-byte otherwise; out-of-range elements
@@ -13,15 +14,32 @@
 
 namespace bddc {
 
+#ifndef BDDC_KC
+#define BDDC_KC 16
+#endif
+#ifndef BDDC_KSTAGES
+#define BDDC_KSTAGES 3
+#endif
+#ifndef BDDC_TILE_MINB
+#define BDDC_TILE_MINB 4   // <= 64 registers: 4 CTAs x 8 warps per SM (tools/bench_tile.py)
+#endif
+
+#ifndef BDDC_WN
+#define BDDC_WN 16         // 32x16 warp tiles, 8 warps per 64x64 CTA tile
+#endif
+
 constexpr int kTile = 64;
-constexpr int kTileThreads = 128;
-constexpr int kKC = 16;          // K chunk
-constexpr int kStages = 3;
+constexpr int kWN = BDDC_WN;                       // warp tile width (32 or 16)
+constexpr int kNJ = kWN / 8;                        // DMMA tiles per warp along n
+constexpr int kTileThreads = 2 * 32 * (64 / kWN);  // BM = 64: 2 x (64 / kWN) warps
+constexpr int kKC = BDDC_KC;          // K chunk
+constexpr int kStages = BDDC_KSTAGES;
+constexpr int kTileMinBlocks = BDDC_TILE_MINB;
 constexpr int kAS = kKC + 4;     // A smem row stride (doubles): conflict-free fragments
 constexpr int kBS = kTile + 4;   // B smem row stride
 
-// BM x 64 output tile, BM in {64, 128}: 2 * BM threads, warps arranged
-// (BM/32) x 2, each warp 32 x 32 (4 x 4 DMMA m8n8k4 tiles).
+// BM x 64 output tile: (BM/32) x (64/kWN) warps, each warp 32 x kWN
+// (4 x kWN/8 DMMA m8n8k4 tiles).
 template <int BM>
 struct TileSmemT {
   double A[kStages][BM][kAS];
@@ -53,7 +71,7 @@ template <int BM>
 BDDC_DEV void tile_issue_chunk(TileSmemT<BM>& sm, int st, int kc, const double* A, long long lda,
                                const double* B, long long ldb, int m, int n, int K, bool a16,
                                bool b16) {
-  constexpr int NT = 2 * BM;
+  constexpr int NT = (BM / 32) * (64 / kWN) * 32;
   const int k0 = kc * kKC;
   if (a16) {
     for (int idx = threadIdx.x; idx < BM * (kKC / 2); idx += NT) {
@@ -90,9 +108,10 @@ template <int BM>
 BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A, long long lda,
                          const double* B, long long ldb, int K, double alpha, double beta,
                          TileSmemT<BM>& sm) {
+  constexpr int WNW = 64 / kWN;  // warps along n
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // (BM/32) x 2 warps
+  const int wm = (warp / WNW) * 32, wn = (warp % WNW) * kWN;  // (BM/32) x WNW warps
   const int nchunks = (K + kKC - 1) / kKC;
   const bool a16 = ((reinterpret_cast<uintptr_t>(A) | (uintptr_t)(lda * 8)) & 15) == 0;
   const bool b16 = ((reinterpret_cast<uintptr_t>(B) | (uintptr_t)(ldb * 8)) & 15) == 0;
@@ -103,17 +122,24 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
   }
   // accumulators start from (beta/alpha) C: C is read once, early, while the
   // first chunks are in flight
-  double acc[4][4][2];
+  double acc[4][kNJ][2];
   const double cscale = (beta != 0.0) ? beta / alpha : 0.0;
+  const bool c16 = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t)(ldc * 8)) & 15) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = wm + i * 8 + g;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kNJ; ++j) {
       const int c = wn + j * 8 + 2 * t;
+      if (cscale != 0.0 && r < m && c + 1 < n && c16) {
+        const double2 v = *reinterpret_cast<const double2*>(C + (long long)r * ldc + c);
+        acc[i][j][0] = cscale * v.x;
+        acc[i][j][1] = cscale * v.y;
+      } else {
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        acc[i][j][h] = (cscale != 0.0 && r < m && c + h < n) ? cscale * C[(long long)r * ldc + c + h] : 0.0;
+        for (int h = 0; h < 2; ++h)
+          acc[i][j][h] = (cscale != 0.0 && r < m && c + h < n) ? cscale * C[(long long)r * ldc + c + h] : 0.0;
+      }
     }
   }
   for (int kc = 0; kc < nchunks; ++kc) {
@@ -125,15 +151,15 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
     const int st = kc % kStages;
     const int kmax = min(kKC, K - kc * kKC);
     for (int k0 = 0; k0 < kmax; k0 += 4) {
-      double a[4], b[4];
+      double a[4], b[kNJ];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = sm.A[st][wm + i * 8 + g][k0 + t];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = sm.B[st][k0 + t][wn + j * 8 + g];
+      for (int j = 0; j < kNJ; ++j) b[j] = sm.B[st][k0 + t][wn + j * 8 + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int j = 0; j < kNJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
     }
   }
   cp_async_wait<0>();
@@ -144,11 +170,15 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
     if (r >= m) continue;
     double* crow = C + (long long)r * ldc;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kNJ; ++j) {
       const int c = wn + j * 8 + 2 * t;
+      if (c + 1 < n && c16) {
+        *reinterpret_cast<double2*>(crow + c) = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+      } else {
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (c + h < n) crow[c + h] = alpha * acc[i][j][h];
+        for (int h = 0; h < 2; ++h)
+          if (c + h < n) crow[c + h] = alpha * acc[i][j][h];
+      }
     }
   }
 }
