@@ -112,7 +112,9 @@ int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int
                 const long long* soff, const double* Bsym, double* D, double* ws,
                 const long long* ws_off, int* status, int n_globs, cudaStream_t stream);
 
-/* Face GEP + selection + change of basis.
+/* Face GEP + selection + change of basis.  fast = 1: certified fast path in a
+ * compact arena (faces whose certificate fails get status 900 and must be
+ * re-run with fast = 0, the general algorithm).
  * replaces face_gevp adaptive.py:57-72, glob_schur_block substructuring.py:152-171,
  *          parallel_sum / pseudo_inverse / sym_pencil_gevp linalg.py:23-214,
  *          build_change_of_basis adaptive.py:190-206. */
@@ -122,7 +124,7 @@ int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const 
                    double theta, double* eig, const long long* eig_off, int* n_sel, int* r,
                    double* Q, const long long* q_off, int* status, double* ws,
                    const long long* ws_off, const int* face_ids, int n_faces, int max_n,
-                   cudaStream_t stream);
+                   int fast, cudaStream_t stream);
 
 /* Prior blocks of the face-transformed Bsym^-1 per subdomain.
  * replaces adaptive.py:310-329 (Minv = Q Bsym^-1 Q^T on face rows/cols, prior_idx). */
@@ -156,6 +158,7 @@ int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, co
 
 /* workspace sizes (doubles) of the per-glob kernels, for the host planner */
 long long bddc_ws_face(long long n);
+long long bddc_ws_face_fast(long long n);
 long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long nhmax);
 
 /* ---- precond.cu : preconditioner setup / apply, interface operator -------- */

@@ -559,6 +559,141 @@ __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* _
 }
 
 // ---------------------------------------------------------------------------
+// Face eigenproblem, certified fast path only, in a compact shared-memory
+// arena (5 n^2 + vector region) so that two faces of 49 dofs run per SM.
+// Faces whose certificates fail get status kNeedFallback and are re-run by
+// face_kernel (general algorithm) in a second launch.
+// ---------------------------------------------------------------------------
+constexpr int kNeedFallback = 900;
+
+__host__ __device__ inline long long face_fast_arena(long long n) {
+  return 5 * n * n + 4 * n + (long long)blk::kIILanes * 6 * n + 4 * n + 32;
+}
+
+__global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const double* __restrict__ D,
+                                                        double theta, GlobOut o,
+                                                        double* __restrict__ ws,
+                                                        const long long* __restrict__ ws_off,
+                                                        const int* __restrict__ face_ids,
+                                                        int arena_in_smem, int max_n) {
+  extern __shared__ double sh[];
+  const int g = face_ids[blockIdx.x];
+  const int n = t.size[g];
+  const int nn = n * n;
+  double* cs = sh;                                       // 2(max_n+2)
+  double* red = cs + 2 * (max_n + 2);                    // 32
+  double* rowbuf = red + 32;                             // 2(max_n+2)
+  int* perm = reinterpret_cast<int*>(rowbuf + 2 * (max_n + 2));  // 2(max_n+2)
+  int* degen = perm + 2 * (max_n + 2);                   // max_n + 2
+  double* W = arena_in_smem ? reinterpret_cast<double*>(degen + ((max_n + 2 + 1) & ~1))
+                            : ws + ws_off[g];
+  double* S0 = W;            // B_F
+  double* S1 = S0 + nn;      // scratch / Bt_i / L^-1 / rows
+  double* S2 = S1 + nn;      // Bt_j / L^-1 B_F / eigenvectors
+  double* S3 = S2 + nn;      // M^-1 -> Bt -> L -> X
+  double* S4 = S3 + nn;      // T -> Bh (reflectors)
+  double* vr = S4 + nn;      // vectors: d, e, tau, w, inverse-iteration scratch
+  double* dd = vr;
+  double* ee = dd + n;
+  double* tau = ee + n;
+  double* w = tau + n;
+  double* scr = w + n;                                              // kIILanes * 5 n
+  int* iscr = reinterpret_cast<int*>(scr + blk::kIILanes * 5 * n);  // kIILanes * n ints
+  const int k0 = t.sh_start[g];
+  const int si = t.sh_sub[k0], sj = t.sh_sub[k0 + 1];
+  const double* Di = D + t.sh_doff[k0];
+  const double* Dj = D + t.sh_doff[k0 + 1];
+  const double* Bi = t.Bsym + t.soff[si] + (long long)t.sh_boff[k0] * t.nB[si] + t.sh_boff[k0];
+  const double* Bj = t.Bsym + t.soff[sj] + (long long)t.sh_boff[k0 + 1] * t.nB[sj] + t.sh_boff[k0 + 1];
+  const int ldi = t.nB[si], ldj = t.nB[sj];
+  // 1. B_F = sym(Dj^T Bi Dj + Di^T Bj Di)
+  blk::gemm(S1, n, Bi, ldi, false, Dj, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(S0, n, Dj, n, true, S1, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(S1, n, Bj, ldj, false, Di, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(S0, n, Di, n, true, S1, n, false, n, n, n, 1.0, 1.0);
+  blk::symmetrize(S0, n, n);
+  // 2. glob Schur blocks
+  int st = glob_schur(t, k0, n, S1, rowbuf);
+  if (st) {
+    if (threadIdx.x == 0) o.status[g] = 100;
+    return;
+  }
+  st = glob_schur(t, k0 + 1, n, S2, rowbuf);
+  if (st) {
+    if (threadIdx.x == 0) o.status[g] = 101;
+    return;
+  }
+  // 3. parallel sum Bt = Bti (Bti + Btj)^-1 Btj with the pinv = inv certificate
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) S3[idx] = S1[idx] + S2[idx];
+  __syncthreads();
+  const double fm = blk::frob2(S3, n, n, n, red);
+  if (blk::gj_inverse(S3, n, n, true, rowbuf) ||
+      !(sqrt(fm) * sqrt(blk::frob2(S3, n, n, n, red)) < 1e11)) {
+    if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+    return;
+  }
+  blk::symmetrize(S3, n, n);
+  blk::gemm(S4, n, S1, n, false, S3, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(S3, n, S4, n, false, S2, n, false, n, n, n, 1.0, 0.0);
+  blk::symmetrize(S3, n, n);
+  // 4. pencil (B_F, Bt): Cholesky whitening with its certificate
+  const double nbt = sqrt(blk::frob2(S3, n, n, n, red));
+  const double nb = sqrt(blk::frob2(S0, n, n, n, red));
+  if (!blk::cholesky(S3, n, n)) {
+    if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+    return;
+  }
+  blk::set_identity(S1, n, n, n);
+  blk::trsm_lower(S3, n, n, S1, n, n);
+  const double nli = blk::frob2(S1, n, n, n, red);
+  if (!(nbt * nli < 1e11) || !(theta > 1e-14 * nb)) {
+    if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+    return;
+  }
+  blk::gemm(S2, n, S1, n, false, S0, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(S4, n, S2, n, false, S1, n, true, n, n, n, 1.0, 0.0);
+  blk::symmetrize(S4, n, n);
+  blk::tridiagonalize(S4, n, n, dd, ee, tau, S2, red);
+  blk::tridiag_eigvals(dd, ee, n, w, red);
+  double* vals = o.eig + o.eig_off[g];
+  __shared__ int s_k;
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int j = n - 1; j >= 0 && w[j] >= theta; --j) perm[k++] = j;
+    s_k = k;
+  }
+  for (int j = threadIdx.x; j < n; j += blockDim.x) vals[n - 1 - j] = w[j];
+  __syncthreads();
+  const int k = s_k;
+  if (k > 0) {
+    blk::tridiag_eigvecs(dd, ee, n, w, perm, k, S3, scr, iscr);
+    blk::apply_householder(S4, n, n, tau, S3, k, k);
+    // V (S2, n x k) = Li^T X / sqrt(lambda)
+    for (int idx = threadIdx.x; idx < n * k; idx += blockDim.x) {
+      const int r = idx / k, q = idx - r * k;
+      double s = 0.0;
+      for (int tt = r; tt < n; ++tt) s += S1[tt * n + r] * S3[tt * k + q];
+      S2[r * k + q] = s / sqrt(fabs(w[perm[q]]));
+    }
+    __syncthreads();
+    // 5. rows (S1, k x n) = (B_F V)^T
+    for (int idx = threadIdx.x; idx < k * n; idx += blockDim.x) {
+      const int q = idx / n, c = idx - q * n;
+      double s = 0.0;
+      for (int r = 0; r < n; ++r) s += S0[c * n + r] * S2[r * k + q];
+      S1[q * n + c] = s;
+    }
+    __syncthreads();
+  }
+  // 6. change of basis from the constraint rows (workspace S2..S4 + vectors)
+  const int r = row_space_basis(S1, n, k, n, o.Q + o.q_off[g], S2, cs, perm, red);
+  if (threadIdx.x == 0) {
+    o.n_sel[g] = k;
+    o.r[g] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // prior blocks per subdomain (adaptive.py:306-329):
 //   PB = P_H Binv (nH x nB),  XHH = PB P_H^T,  P_H rows = Q_F[:r_F] on each
 //   face block, unit rows on vertex positions (faces first, then vertices,
@@ -960,6 +1095,7 @@ static GlobTables make_tables(const int* kind, const int* size, const int* sh_st
 }
 
 constexpr int kFaceSmemBudget = 225 * 1024;
+constexpr int kFaceFastSmemBudget = 112 * 1024;  // two faces per SM
 
 static int face_small_bytes(int n) {
   // cs 2(n+2) + red 32 + rowbuf 2(n+2) doubles, perm 2(n+2) + degen (n+2, even) ints
@@ -974,6 +1110,7 @@ static int shmem_for(int dim) {
 extern "C" {
 
 long long bddc_ws_face(long long n) { return face_arena(n); }
+long long bddc_ws_face_fast(long long n) { return face_fast_arena(n); }
 long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long nhmax) {
   return bddc_edge_new_ws(ns, ne, wd, nhmax);
 }
@@ -994,16 +1131,25 @@ int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const 
                    double theta, double* eig, const long long* eig_off, int* n_sel, int* r,
                    double* Q, const long long* q_off, int* status, double* ws,
                    const long long* ws_off, const int* face_ids, int n_faces, int max_n,
-                   cudaStream_t stream) {
+                   int fast, cudaStream_t stream) {
   if (n_faces <= 0) return 0;
   GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, Binv);
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int small = face_small_bytes(max_n);
-  const long long arena = face_arena(max_n) * 8;
-  const int in_smem = (small + arena) <= kFaceSmemBudget;
-  const int smem = small + (in_smem ? (int)arena : 0);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(face_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  face_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids, in_smem, max_n); bddc_note_launches(1);
+  if (fast) {
+    const long long arena = face_fast_arena(max_n) * 8;
+    const int in_smem = (small + arena) <= kFaceFastSmemBudget;
+    const int smem = small + (in_smem ? (int)arena : 0);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(face_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    face_fast_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids, in_smem, max_n);
+  } else {
+    const long long arena = face_arena(max_n) * 8;
+    const int in_smem = (small + arena) <= kFaceSmemBudget;
+    const int smem = small + (in_smem ? (int)arena : 0);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(face_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    face_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids, in_smem, max_n);
+  }
+  bddc_note_launches(1);
   return glob_launch_status();
 }
 

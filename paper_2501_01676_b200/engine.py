@@ -278,14 +278,20 @@ def _face_ws(n):
     return 10 * n * n + 40 * n + 64
 
 
-def _face_smem_bytes(n):
-    """face_small_bytes() + face_arena() bytes in csrc/globs.cu"""
+def _face_fast_ws(n):
+    """face_fast_arena() in csrc/globs.cu"""
     n = np.asarray(n, dtype=np.int64)
-    small = (4 * (n + 2) + 32) * 8 + (2 * (n + 2) + ((n + 3) & ~1)) * 4 + 64
-    return small + 8 * _face_ws(n)
+    return 5 * n * n + 4 * n + 4 * 6 * n + 4 * n + 32
+
+
+def _face_small_bytes(n):
+    """face_small_bytes() in csrc/globs.cu"""
+    n = np.asarray(n, dtype=np.int64)
+    return (4 * (n + 2) + 32) * 8 + (2 * (n + 2) + ((n + 3) & ~1)) * 4 + 64
 
 
 FACE_SMEM_BUDGET = 225 * 1024
+FACE_FAST_SMEM_BUDGET = 112 * 1024
 
 
 def _edge_old_ws(n):
@@ -346,23 +352,12 @@ class DevicePrimalSpace:
         faces = np.flatnonzero(kind == 0)
         edges = np.flatnonzero(kind == 1)
         if faces.size:
-            small = _face_smem_bytes(p.gsize[faces]) <= FACE_SMEM_BUDGET
-            for grp, in_smem in ((faces[small], True), (faces[~small], False)):
-                if not grp.size:
-                    continue
-                if in_smem:
-                    ws, woff = torch.empty(1, dtype=F64, device="cuda"), np.zeros(G + 1, np.int64)
-                else:
-                    wsz = _face_ws(p.gsize[grp])
-                    woff = np.zeros(G + 1, dtype=np.int64)
-                    woff[grp] = _excl(wsz)[:-1]
-                    ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
-                lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
-                                   d.nB, d.soff, ls.Bsym, Binv, scaling.D, self.theta_f, self.eig,
-                                   d_eig_off, self.n_sel, self.r, self.Q, self.d_q_off, status, ws,
-                                   dev_i64(woff[:-1]), dev_i32(grp), grp.size,
-                                   int(p.gsize[grp].max()), st)
-                del ws
+            self._run_faces(faces, True, status, scaling, Binv, d_eig_off)
+            s = status.cpu().numpy()
+            redo = faces[s[faces] == 900]
+            if redo.size:  # certificates failed: general algorithm (linalg.py:116-214)
+                status[dev_i64(redo)] = 0
+                self._run_faces(redo, False, status, scaling, Binv, d_eig_off)
             self._raise(status, "face")
         r_host = self.r.cpu().numpy()
         if edges.size and variant == "new":
@@ -411,6 +406,30 @@ class DevicePrimalSpace:
             del ws
         self.r_host = self.r.cpu().numpy().astype(np.int64)
         self.n_sel_host = self.n_sel.cpu().numpy().astype(np.int64)
+
+    def _run_faces(self, faces, fast, status, scaling, Binv, d_eig_off):
+        ls, p, d, st = self.ls, self.ls.plan, self.ls.d, stream()
+        G = p.G
+        sizes = p.gsize[faces]
+        budget = FACE_FAST_SMEM_BUDGET if fast else FACE_SMEM_BUDGET
+        arena = _face_fast_ws if fast else _face_ws
+        small = _face_small_bytes(sizes) + 8 * arena(sizes) <= budget
+        for grp, in_smem in ((faces[small], True), (faces[~small], False)):
+            if not grp.size:
+                continue
+            woff = np.zeros(G + 1, dtype=np.int64)
+            if in_smem:
+                ws = torch.empty(1, dtype=F64, device="cuda")
+            else:
+                wsz = arena(p.gsize[grp])
+                woff[grp] = _excl(wsz)[:-1]
+                ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
+            lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, d.nB,
+                               d.soff, ls.Bsym, Binv, scaling.D, self.theta_f, self.eig, d_eig_off,
+                               self.n_sel, self.r, self.Q, self.d_q_off, status, ws,
+                               dev_i64(woff[:-1]), dev_i32(grp), grp.size, int(p.gsize[grp].max()),
+                               1 if fast else 0, st)
+            del ws
 
     def _raise(self, status, what):
         s = status.cpu().numpy()

@@ -36,8 +36,11 @@ def test_workspace_formulas_match_library():
     dll.bddc_ws_face.argtypes = [ctypes.c_longlong]
     dll.bddc_ws_edge_new.restype = ctypes.c_longlong
     dll.bddc_ws_edge_new.argtypes = [ctypes.c_longlong] * 4
+    dll.bddc_ws_face_fast.restype = ctypes.c_longlong
+    dll.bddc_ws_face_fast.argtypes = [ctypes.c_longlong]
     for n in (1, 7, 49, 193):
         assert dll.bddc_ws_face(n) == int(engine._face_ws(n))
+        assert dll.bddc_ws_face_fast(n) == int(engine._face_fast_ws(n))
     for ns, ne, wd, h in ((2, 7, 30, 8), (4, 7, 80, 14), (3, 20, 700, 150)):
         assert dll.bddc_ws_edge_new(ns, ne, wd, h) == int(engine._edge_new_ws(ns, ne, wd, h))
 
