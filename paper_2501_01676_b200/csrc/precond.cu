@@ -140,6 +140,70 @@ __global__ void __launch_bounds__(256) glob_block_kernel(SubGlobMap m,
   }
 }
 
+// DMMA version of the block-diagonal transforms: one CTA per (glob block of a
+// subdomain, 64-wide tile of the free dimension, 64-chunk of the glob
+// dimension), block products on the tensor pipe via tile_mma:
+//   left : out[blk, tile] = L_blk * in[blk, tile]
+//   right: out[tile, blk] = in[tile, blk] * L_blk^T   (B operand = L^T, from LT)
+// L_blk = base + off[g] (by_slot = 0) or base + off[sub_glob_sh[k]] (by_slot = 1).
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) glob_mma_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ soff,
+    const int* __restrict__ sub_glob_start, int nsub, const int* __restrict__ sub_globs,
+    const int* __restrict__ sub_glob_boff, const int* __restrict__ sub_glob_sh,
+    const int* __restrict__ gsize, const double* __restrict__ L, const double* __restrict__ LT,
+    const long long* __restrict__ loff, int by_slot, int right, const double* __restrict__ in,
+    double* __restrict__ out, int tiles_per_item) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int item = blockIdx.x / tiles_per_item, tile = blockIdx.x - item * tiles_per_item;
+  const int rc = blockIdx.y;
+  // subdomain owning glob item `item` (binary search in sub_glob_start)
+  int lo = 0, hi = nsub;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (sub_glob_start[mid] <= item) lo = mid; else hi = mid;
+  }
+  const int b = lo;
+  const int n = nB[b];
+  const int g = sub_globs[item];
+  const int ng = gsize[g];
+  const int bo = sub_glob_boff[item];
+  if (rc * 64 >= ng || tile * 64 >= n) return;
+  const long long lo_off = loff[by_slot ? sub_glob_sh[item] : g];
+  const double* X = in + soff[b];
+  double* Y = out + soff[b];
+  for (int kc = 0; kc < ng; kc += 64) {
+    const int K = min(64, ng - kc);
+    if (!right) {
+      const int m = min(64, ng - rc * 64), nc = min(64, n - tile * 64);
+      tile_mma(Y + (long long)(bo + rc * 64) * n + tile * 64, n, m, nc,
+               L + lo_off + (long long)(rc * 64) * ng + kc, ng,
+               X + (long long)(bo + kc) * n + tile * 64, n, K, 1.0, kc ? 1.0 : 0.0, sm);
+    } else {
+      const int m = min(64, n - tile * 64), nc = min(64, ng - rc * 64);
+      tile_mma(Y + (long long)(tile * 64) * n + bo + rc * 64, n, m, nc,
+               X + (long long)(tile * 64) * n + bo + kc, n,
+               LT + lo_off + (long long)kc * ng + rc * 64, ng, K, 1.0, kc ? 1.0 : 0.0, sm);
+    }
+  }
+}
+
+// dst block = src block^T for square blocks (size[gidx[i]]) at off[i]
+__global__ void transpose_blocks_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                        const long long* __restrict__ off,
+                                        const int* __restrict__ gidx,
+                                        const int* __restrict__ gsize, int nblocks) {
+  const int i = blockIdx.x;
+  if (i >= nblocks) return;
+  const int n = gsize[gidx ? gidx[i] : i];
+  const double* s = src + off[i];
+  double* d = dst + off[i];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    d[c * n + r] = s[idx];
+  }
+}
+
 // Primal pieces, one CTA per subdomain, primal positions in chunks of kPC:
 //   MP[p][r] = d(r,pc) - (Z Sbar)[r][pc]     (warp per row r of Z, coalesced)
 //   RP[p][r] = d(r,pc) - (Sbar Z)[pc][r]     (thread per column r of Z, coalesced)
@@ -557,22 +621,41 @@ static int glob_block_smem(int max_ng) {
   return (64 * 64 + (max_ng > kBT_COLS ? max_ng : kBT_COLS) * kBT_COLS) * (int)sizeof(double);
 }
 
-// Sbar = Qi S Qi^T (via tmp)
-int bddc_pc_transform_schur(const int* nB, const long long* soff, const long long* voff,
-                            const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+static int glob_mma(const int* nB, const long long* soff, const int* sub_glob_start, int nsub,
+                    const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,
+                    const int* gsize, const double* L, const double* LT, const long long* loff,
+                    int by_slot, int right, const double* in, double* out, int n_items,
+                    int max_nB, int max_ng, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(glob_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileSmem));
+    attr = true;
+  }
+  const int tpi = ceil_div(max_nB, 64);
+  dim3 grid((unsigned)(n_items * tpi), ceil_div(max_ng, 64));
+  glob_mma_kernel<<<grid, kTileThreads, sizeof(TileSmem), stream>>>(
+      nB, soff, sub_glob_start, nsub, sub_globs, sub_glob_boff, sub_glob_sh, gsize, L, LT, loff,
+      by_slot, right, in, out, tpi);
+  bddc_note_launches(1);
+  return pc_status();
+}
+
+// Sbar = Qi S Qi^T (via tmp); QT: caller scratch of the Q buffer's size
+int bddc_pc_transform_schur(const int* nB, const long long* soff, const int* sub_glob_start,
+                            int nbatch, const int* sub_globs, const int* sub_glob_boff,
                             const int* sub_glob_sh, const int* gsize, const double* Q,
-                            const long long* q_off, const int* sub_glob_start, int max_globs,
-                            int max_ng, const double* S, double* tmp, double* Sbar, int nbatch,
+                            const long long* q_off, double* QT, int n_globs, int n_items,
+                            int max_nB, int max_ng, const double* S, double* tmp, double* Sbar,
                             cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  SubGlobMap m = make_map(nB, soff, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize, Q,
-                          q_off, nullptr, nullptr);
-  const int smem = glob_block_smem(max_ng);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(glob_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  glob_block_kernel<<<dim3(max_globs, nbatch), 256, smem, stream>>>(m, sub_glob_start, nullptr, S, tmp, 0, 0, max_ng);
-  glob_block_kernel<<<dim3(max_globs, nbatch), 256, smem, stream>>>(m, sub_glob_start, nullptr, tmp, Sbar, 0, 1, max_ng);
-  bddc_note_launches(2);
-  return pc_status();
+  transpose_blocks_kernel<<<n_globs, 128, 0, stream>>>(Q, QT, q_off, nullptr, gsize, n_globs);
+  bddc_note_launches(1);
+  int st = glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
+                    Q, QT, q_off, 0, 0, S, tmp, n_items, max_nB, max_ng, stream);
+  if (st) return st;
+  return glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
+                  Q, QT, q_off, 0, 1, tmp, Sbar, n_items, max_nB, max_ng, stream);
 }
 
 int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
@@ -600,22 +683,22 @@ int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* v
   return pc_status();
 }
 
-// A = TT_blockdiag Z TT_blockdiag^T  (= T^T Z T with T = blockdiag(Q_g D_g^T))
-int bddc_pc_local_operator(const int* nB, const long long* soff, const long long* voff,
-                           const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+// A = TT_blockdiag Z TT_blockdiag^T  (= T^T Z T with T = blockdiag(Q_g D_g^T));
+// TTT: caller scratch of the TT buffer's size
+int bddc_pc_local_operator(const int* nB, const long long* soff, const int* sub_glob_start,
+                           int nbatch, const int* sub_globs, const int* sub_glob_boff,
                            const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
-                           const int* sub_glob_start, int max_globs, int max_ng, const double* TT,
-                           const double* Z, double* tmp, double* A, int nbatch,
-                           cudaStream_t stream) {
+                           const int* slot_glob, int n_slots, int n_items, int max_nB,
+                           int max_ng, const double* TT, double* TTT, const double* Z,
+                           double* tmp, double* A, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  SubGlobMap m = make_map(nB, soff, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
-                          nullptr, nullptr, nullptr, sh_doff);
-  const int smem = glob_block_smem(max_ng);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(glob_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  glob_block_kernel<<<dim3(max_globs, nbatch), 256, smem, stream>>>(m, sub_glob_start, TT, Z, tmp, 1, 1, max_ng);
-  glob_block_kernel<<<dim3(max_globs, nbatch), 256, smem, stream>>>(m, sub_glob_start, TT, tmp, A, 1, 0, max_ng);
-  bddc_note_launches(2);
-  return pc_status();
+  transpose_blocks_kernel<<<n_slots, 128, 0, stream>>>(TT, TTT, sh_doff, slot_glob, gsize, n_slots);
+  bddc_note_launches(1);
+  int st = glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
+                    TT, TTT, sh_doff, 1, 1, Z, tmp, n_items, max_nB, max_ng, stream);
+  if (st) return st;
+  return glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
+                  TT, TTT, sh_doff, 1, 0, tmp, A, n_items, max_nB, max_ng, stream);
 }
 
 int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstart,

@@ -546,11 +546,14 @@ class DevicePreconditioner:
                              int(p.sh_sub.size), st)
         Sbar = torch.empty(p.S_total, dtype=F64, device="cuda")
         tmp = torch.empty(p.S_total, dtype=F64, device="cuda")
-        max_globs = int(np.diff(p.sub_glob_start).max())
         max_ng = int(p.gsize.max())
-        lib.bddc_pc_transform_schur(d.nB, d.soff, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
-                                    d.sub_glob_sh, d.gsize, Q, q_off, d.sub_glob_start, max_globs,
-                                    max_ng, ls.S, tmp, Sbar, p.N, st)
+        nbmax = int(p.nB.max())
+        n_items = int(p.sub_globs.size)
+        QT = torch.empty(int(Q.numel()), dtype=F64, device="cuda")
+        lib.bddc_pc_transform_schur(d.nB, d.soff, d.sub_glob_start, p.N, d.sub_globs,
+                                    d.sub_glob_boff, d.sub_glob_sh, d.gsize, Q, q_off, QT, p.G,
+                                    n_items, nbmax, max_ng, ls.S, tmp, Sbar, st)
+        del QT
         Z = torch.empty(p.S_total, dtype=F64, device="cuda")
         lib.bddc_pc_dual_embed(d.nB, d.soff, d.voff, d_mask, Sbar, Z, tmp, p.N, st)
         # certificate: LDL^T of sym(Sbar_dd) must have positive pivots (solver.py:91-98)
@@ -568,9 +571,12 @@ class DevicePreconditioner:
             raise NumericalError(f"dual block of subdomain {bad} is singular")
         lib.bddc_pc_zero_primal(d.nB, d.soff, d.voff, d_mask, Z, p.N, st)
         self.A = torch.empty(p.S_total, dtype=F64, device="cuda")
-        lib.bddc_pc_local_operator(d.nB, d.soff, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
-                                   d.sub_glob_sh, d.gsize, d.sh_doff, d.sub_glob_start, max_globs,
-                                   max_ng, TT, Z, tmp, self.A, p.N, st)
+        TTT = torch.empty_like(TT)
+        lib.bddc_pc_local_operator(d.nB, d.soff, d.sub_glob_start, p.N, d.sub_globs,
+                                   d.sub_glob_boff, d.sub_glob_sh, d.gsize, d.sh_doff, d.slot_glob,
+                                   int(p.sh_sub.size), n_items, nbmax, max_ng, TT, TTT, Z, tmp,
+                                   self.A, st)
+        del TTT
         npn = max(int(poff[-1]), 1)
         MP = torch.empty(npn, dtype=F64, device="cuda")
         RP = torch.empty(npn, dtype=F64, device="cuda")
