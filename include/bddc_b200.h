@@ -163,12 +163,13 @@ long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long n
 
 /* ---- precond.cu : preconditioner setup / apply, interface operator -------- */
 
-/* Sbar = Q_i S_i Q_i^T (block diagonal Q_i per glob).  replaces solver.py:85-86. */
-int bddc_pc_transform_schur(const int* nB, const long long* soff, const long long* voff,
-                            const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+/* Sbar = Q_i S_i Q_i^T (block diagonal Q_i per glob; DMMA block products).
+ * QT: caller scratch the size of the Q buffer.  replaces solver.py:85-86. */
+int bddc_pc_transform_schur(const int* nB, const long long* soff, const int* sub_glob_start,
+                            int nbatch, const int* sub_globs, const int* sub_glob_boff,
                             const int* sub_glob_sh, const int* gsize, const double* Q,
-                            const long long* q_off, const int* sub_glob_start, int max_globs,
-                            int max_ng, const double* S, double* tmp, double* Sbar, int nbatch,
+                            const long long* q_off, double* QT, int n_globs, int n_items,
+                            int max_nB, int max_ng, const double* S, double* tmp, double* Sbar,
                             cudaStream_t stream);
 
 /* TT_(g,s) = D_g^(s) Q_g^T blocks.  replaces Dbar solver.py:87-90. */
@@ -185,13 +186,14 @@ int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* v
                         const unsigned char* primal_mask, double* Z, int nbatch,
                         cudaStream_t stream);
 
-/* A_i = T_i^T Z_i T_i (local part of M^-1).  replaces scale/tilde_solve solver.py:163-199. */
-int bddc_pc_local_operator(const int* nB, const long long* soff, const long long* voff,
-                           const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+/* A_i = T_i^T Z T_i (local part of M^-1; DMMA block products).  TTT: caller
+ * scratch the size of the TT buffer.  replaces scale/tilde_solve solver.py:163-199. */
+int bddc_pc_local_operator(const int* nB, const long long* soff, const int* sub_glob_start,
+                           int nbatch, const int* sub_globs, const int* sub_glob_boff,
                            const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
-                           const int* sub_glob_start, int max_globs, int max_ng, const double* TT,
-                           const double* Z, double* tmp, double* A, int nbatch,
-                           cudaStream_t stream);
+                           const int* slot_glob, int n_slots, int n_items, int max_nB,
+                           int max_ng, const double* TT, double* TTT, const double* Z,
+                           double* tmp, double* A, cudaStream_t stream);
 
 /* MP = E_P - (Z Sbar)_{:,P}^T rows, RP = E_P - (Sbar Z)_{P,:}, C_i = Sbar_PP - Sbar_P: Z Sbar_:P.
  * replaces solver.py:102-106. */

@@ -1,6 +1,7 @@
 // Launch accounting for the bench's "gpu_launches" field: every C-ABI entry
 // point adds the number of kernels it launched.
 #include <atomic>
+#include "bddc_b200.h"
 
 static std::atomic<long long> g_launches{0};
 

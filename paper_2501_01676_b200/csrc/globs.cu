@@ -7,6 +7,7 @@
 // Reference: scaling.py:10-57, substructuring.py:146-190, linalg.py:23-214,
 // adaptive.py:57-206, 288-342.
 #include "common.cuh"
+#include "bddc_b200.h"
 #include "dense_block.cuh"
 #include "glob_layout.h"
 

@@ -4,6 +4,7 @@
 // Reductions are two-pass with a fixed order, so runs are bitwise
 // reproducible.
 #include "common.cuh"
+#include "bddc_b200.h"
 
 namespace bddc {
 

@@ -10,6 +10,7 @@
 // Layout: batch of row-major matrices in one device buffer; matrix b starts
 // at base + off[b] with leading dimension ld[b] (variable sizes, "vbatched").
 #include "common.cuh"
+#include "bddc_b200.h"
 #include "tile_mma.cuh"
 
 namespace bddc {

@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "bddc_b200.h"
 #include "tile_mma.cuh"
 
 namespace cg = cooperative_groups;
