@@ -169,8 +169,8 @@ int bddc_pc_transform_schur(const int* nB, const long long* soff, const int* sub
                             int nbatch, const int* sub_globs, const int* sub_glob_boff,
                             const int* sub_glob_sh, const int* gsize, const double* Q,
                             const long long* q_off, double* QT, int n_globs, int n_items,
-                            int max_nB, int max_ng, const double* S, double* tmp, double* Sbar,
-                            cudaStream_t stream);
+                            int max_nB, int max_ng, int max_globs, const double* S, double* tmp,
+                            double* Sbar, cudaStream_t stream);
 
 /* TT_(g,s) = D_g^(s) Q_g^T blocks.  replaces Dbar solver.py:87-90. */
 int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
@@ -192,8 +192,8 @@ int bddc_pc_local_operator(const int* nB, const long long* soff, const int* sub_
                            int nbatch, const int* sub_globs, const int* sub_glob_boff,
                            const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
                            const int* slot_glob, int n_slots, int n_items, int max_nB,
-                           int max_ng, const double* TT, double* TTT, const double* Z,
-                           double* tmp, double* A, cudaStream_t stream);
+                           int max_ng, int max_globs, const double* TT, double* TTT,
+                           const double* Z, double* tmp, double* A, cudaStream_t stream);
 
 /* MP = E_P - (Z Sbar)_{:,P}^T rows, RP = E_P - (Sbar Z)_{P,:}, C_i = Sbar_PP - Sbar_P: Z Sbar_:P.
  * replaces solver.py:102-106. */

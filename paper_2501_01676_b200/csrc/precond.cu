@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) glob_block_kernel(SubGlobMap m,
                                                          const double* __restrict__ TT,
                                                          const double* __restrict__ in,
                                                          double* __restrict__ out, int src,
-                                                         int right, int max_ng) {
+                                                         int right, int max_ng, int skip_ge) {
   extern __shared__ double smb[];
   const int b = blockIdx.y;
   const int k = sub_glob_start[b] + blockIdx.x;
@@ -101,6 +101,7 @@ __global__ void __launch_bounds__(256) glob_block_kernel(SubGlobMap m,
   const int g = m.sub_globs[k];
   const int bo = m.sub_glob_boff[k];
   const int ng = m.gsize[g];
+  if (ng >= skip_ge) return;  // large blocks go through glob_mma_kernel
   const double* L = src == 0 ? m.Q + m.q_off[g] : TT + m.sh_doff[m.sub_glob_sh[k]];
   const double* X = in + m.soff[b];
   double* Y = out + m.soff[b];
@@ -153,7 +154,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) glob_mma_kernel(
     const int* __restrict__ sub_glob_boff, const int* __restrict__ sub_glob_sh,
     const int* __restrict__ gsize, const double* __restrict__ L, const double* __restrict__ LT,
     const long long* __restrict__ loff, int by_slot, int right, const double* __restrict__ in,
-    double* __restrict__ out, int tiles_per_item) {
+    double* __restrict__ out, int tiles_per_item, int min_ng) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int item = blockIdx.x / tiles_per_item, tile = blockIdx.x - item * tiles_per_item;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) glob_mma_kernel(
   const int g = sub_globs[item];
   const int ng = gsize[g];
   const int bo = sub_glob_boff[item];
-  if (rc * 64 >= ng || tile * 64 >= n) return;
+  if (ng < min_ng || rc * 64 >= ng || tile * 64 >= n) return;
   const long long lo_off = loff[by_slot ? sub_glob_sh[item] : g];
   const double* X = in + soff[b];
   double* Y = out + soff[b];
@@ -622,22 +623,36 @@ static int glob_block_smem(int max_ng) {
   return (64 * 64 + (max_ng > kBT_COLS ? max_ng : kBT_COLS) * kBT_COLS) * (int)sizeof(double);
 }
 
+constexpr int kMmaMinNg = 16;  // smaller glob blocks: per-element kernel
+
 static int glob_mma(const int* nB, const long long* soff, const int* sub_glob_start, int nsub,
                     const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,
                     const int* gsize, const double* L, const double* LT, const long long* loff,
                     int by_slot, int right, const double* in, double* out, int n_items,
-                    int max_nB, int max_ng, cudaStream_t stream) {
+                    int max_nB, int max_ng, int max_globs, cudaStream_t stream) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(glob_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(TileSmem));
     attr = true;
   }
-  const int tpi = ceil_div(max_nB, 64);
-  dim3 grid((unsigned)(n_items * tpi), ceil_div(max_ng, 64));
-  glob_mma_kernel<<<grid, kTileThreads, sizeof(TileSmem), stream>>>(
-      nB, soff, sub_glob_start, nsub, sub_globs, sub_glob_boff, sub_glob_sh, gsize, L, LT, loff,
-      by_slot, right, in, out, tpi);
+  if (max_ng >= kMmaMinNg) {
+    const int tpi = ceil_div(max_nB, 64);
+    dim3 grid((unsigned)(n_items * tpi), ceil_div(max_ng, 64));
+    glob_mma_kernel<<<grid, kTileThreads, sizeof(TileSmem), stream>>>(
+        nB, soff, sub_glob_start, nsub, sub_globs, sub_glob_boff, sub_glob_sh, gsize, L, LT, loff,
+        by_slot, right, in, out, tpi, kMmaMinNg);
+    bddc_note_launches(1);
+  }
+  // small blocks (vertices, short edges): per-element kernel, L from Q (by glob) or TT (by slot)
+  SubGlobMap m;
+  m.nB = nB; m.soff = soff; m.voff = nullptr; m.pos2k = nullptr; m.sub_globs = sub_globs;
+  m.sub_glob_boff = sub_glob_boff; m.sub_glob_sh = sub_glob_sh; m.gsize = gsize;
+  m.Q = by_slot ? nullptr : L; m.q_off = by_slot ? nullptr : loff; m.D = nullptr;
+  m.sh_doff = by_slot ? loff : nullptr;
+  const int smem = (64 * 64 + 32 * 32) * (int)sizeof(double);
+  glob_block_kernel<<<dim3(max_globs, nsub), 256, smem, stream>>>(
+      m, sub_glob_start, by_slot ? L : nullptr, in, out, by_slot ? 1 : 0, right, 16, kMmaMinNg);
   bddc_note_launches(1);
   return pc_status();
 }
@@ -647,16 +662,16 @@ int bddc_pc_transform_schur(const int* nB, const long long* soff, const int* sub
                             int nbatch, const int* sub_globs, const int* sub_glob_boff,
                             const int* sub_glob_sh, const int* gsize, const double* Q,
                             const long long* q_off, double* QT, int n_globs, int n_items,
-                            int max_nB, int max_ng, const double* S, double* tmp, double* Sbar,
-                            cudaStream_t stream) {
+                            int max_nB, int max_ng, int max_globs, const double* S, double* tmp,
+                            double* Sbar, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   transpose_blocks_kernel<<<n_globs, 128, 0, stream>>>(Q, QT, q_off, nullptr, gsize, n_globs);
   bddc_note_launches(1);
   int st = glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
-                    Q, QT, q_off, 0, 0, S, tmp, n_items, max_nB, max_ng, stream);
+                    Q, QT, q_off, 0, 0, S, tmp, n_items, max_nB, max_ng, max_globs, stream);
   if (st) return st;
   return glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
-                  Q, QT, q_off, 0, 1, tmp, Sbar, n_items, max_nB, max_ng, stream);
+                  Q, QT, q_off, 0, 1, tmp, Sbar, n_items, max_nB, max_ng, max_globs, stream);
 }
 
 int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
@@ -690,16 +705,16 @@ int bddc_pc_local_operator(const int* nB, const long long* soff, const int* sub_
                            int nbatch, const int* sub_globs, const int* sub_glob_boff,
                            const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
                            const int* slot_glob, int n_slots, int n_items, int max_nB,
-                           int max_ng, const double* TT, double* TTT, const double* Z,
-                           double* tmp, double* A, cudaStream_t stream) {
+                           int max_ng, int max_globs, const double* TT, double* TTT,
+                           const double* Z, double* tmp, double* A, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   transpose_blocks_kernel<<<n_slots, 128, 0, stream>>>(TT, TTT, sh_doff, slot_glob, gsize, n_slots);
   bddc_note_launches(1);
   int st = glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
-                    TT, TTT, sh_doff, 1, 1, Z, tmp, n_items, max_nB, max_ng, stream);
+                    TT, TTT, sh_doff, 1, 1, Z, tmp, n_items, max_nB, max_ng, max_globs, stream);
   if (st) return st;
   return glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
-                  TT, TTT, sh_doff, 1, 0, tmp, A, n_items, max_nB, max_ng, stream);
+                  TT, TTT, sh_doff, 1, 0, tmp, A, n_items, max_nB, max_ng, max_globs, stream);
 }
 
 int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstart,

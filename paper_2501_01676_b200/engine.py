@@ -549,10 +549,11 @@ class DevicePreconditioner:
         max_ng = int(p.gsize.max())
         nbmax = int(p.nB.max())
         n_items = int(p.sub_globs.size)
+        max_globs = int(np.diff(p.sub_glob_start).max())
         QT = torch.empty(int(Q.numel()), dtype=F64, device="cuda")
         lib.bddc_pc_transform_schur(d.nB, d.soff, d.sub_glob_start, p.N, d.sub_globs,
                                     d.sub_glob_boff, d.sub_glob_sh, d.gsize, Q, q_off, QT, p.G,
-                                    n_items, nbmax, max_ng, ls.S, tmp, Sbar, st)
+                                    n_items, nbmax, max_ng, max_globs, ls.S, tmp, Sbar, st)
         del QT
         Z = torch.empty(p.S_total, dtype=F64, device="cuda")
         lib.bddc_pc_dual_embed(d.nB, d.soff, d.voff, d_mask, Sbar, Z, tmp, p.N, st)
@@ -574,8 +575,8 @@ class DevicePreconditioner:
         TTT = torch.empty_like(TT)
         lib.bddc_pc_local_operator(d.nB, d.soff, d.sub_glob_start, p.N, d.sub_globs,
                                    d.sub_glob_boff, d.sub_glob_sh, d.gsize, d.sh_doff, d.slot_glob,
-                                   int(p.sh_sub.size), n_items, nbmax, max_ng, TT, TTT, Z, tmp,
-                                   self.A, st)
+                                   int(p.sh_sub.size), n_items, nbmax, max_ng, max_globs, TT, TTT,
+                                   Z, tmp, self.A, st)
         del TTT
         npn = max(int(poff[-1]), 1)
         MP = torch.empty(npn, dtype=F64, device="cuda")
