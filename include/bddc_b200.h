@@ -49,7 +49,8 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
                         const long long* conn, const double* Ke, const double* Fe,
                         const double* gdir, int nbatch, long long max_elems, cudaStream_t stream);
 
-/* Blocked Schur elimination without pivoting (panel 64, DMMA trailing update):
+/* Blocked Schur elimination without pivoting (panel 64 or 128 = two 64-wide
+ * sub-panels combined so the DMMA trailing update runs with K = 128):
  * eliminates npiv[b] leading pivots; trailing block becomes the Schur complement,
  * pivot rows keep W = A11^-1 A12 for back-substitution.
  * replaces splu(A_II) + lu.solve + A_BI @ (...)  substructuring.py:120-127,
@@ -57,18 +58,19 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
  *          cho_factor(sym(Sdd)) certificate solver.py:94 (require_positive = 1). */
 int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const int* npiv,
                          const int* nrows, const int* ncols, int nbatch, int max_npiv,
-                         int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
-                         long long pinv_step_stride, int* status, int require_positive,
-                         double* piv_out, long long piv_stride, cudaStream_t stream);
+                         int max_rows, int max_cols, int panel, double* pinv_ws,
+                         long long pinv_stride, long long pinv_step_stride, int* status,
+                         int require_positive, double* piv_out, long long piv_stride,
+                         cudaStream_t stream);
 
 /* Same, recording CUDA events around every trailing-update launch; the summed
  * device time (ms) is written to the HOST pointer host_trailing_ms (bench roofline). */
 int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, const int* npiv,
                                const int* nrows, const int* ncols, int nbatch, int max_npiv,
-                               int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
-                               long long pinv_step_stride, int* status, int require_positive,
-                               double* piv_out, long long piv_stride, cudaStream_t stream,
-                               double* host_trailing_ms);
+                               int max_rows, int max_cols, int panel, double* pinv_ws,
+                               long long pinv_stride, long long pinv_step_stride, int* status,
+                               int require_positive, double* piv_out, long long piv_stride,
+                               cudaStream_t stream, double* host_trailing_ms);
 
 /* Envelope LU without pivoting of the coarse matrix (one n x n matrix at
  * C + off[0], leading dimension ldv[0], nv[0] = n) in a bandwidth-reducing
@@ -100,7 +102,7 @@ int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
 int bddc_recover_interior(const double* M, const long long* off, const int* ld, const int* nI,
                           const int* nB, const long long* voff, const int* iface_perm,
                           const long long* ioff, const long long* interior_nodes,
-                          const double* u_hat, double* u, int nbatch, int max_nloc,
+                          const double* u_hat, double* u, int nbatch, int max_nloc, int panel,
                           cudaStream_t stream);
 
 /* ---- globs.cu : scaling and adaptive coarse space ------------------------- */

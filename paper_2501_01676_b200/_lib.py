@@ -12,7 +12,7 @@ import re
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_bddc_b200.so")
+LIB_PATH = os.environ.get("BDDC_LIB") or os.path.join(HERE, "_bddc_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "bddc_b200.h")
 
 _CTYPES = {

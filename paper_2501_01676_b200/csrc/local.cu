@@ -206,27 +206,64 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_row_kernel
 
 constexpr int kTrailBM = 64;
 
+// Trailing update of a panel step.  mode 0: rows/cols from k + w, K = w with
+// w = min(nbw, npiv - k) (nbw = 64 or 128).  mode 1 (strip inside a 128-wide
+// panel): rows [k + w1, k + w), cols from k + w1, K = w1, w1 = min(64, npiv - k).
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ nrows, const int* __restrict__ ncols,
-    int k, int lim) {
+    int k, int lim, int nbw, int mode) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmemT<kTrailBM>& sm = *reinterpret_cast<TileSmemT<kTrailBM>*>(smem_raw);
   const int b = blockIdx.y;
-  const int w = min(kTile, npiv[b] - k);
-  if (w <= 0) return;
-  const int s = k + w;
-  const int nr = min(nrows[b], lim), nc = min(ncols[b], lim);
+  const int np = npiv[b] - k;
+  if (np <= 0) return;
+  int w, s, r_begin, r_end;
+  const int nc = min(ncols[b], lim);
+  if (mode == 0) {
+    w = min(nbw, np);
+    s = k + w;
+    r_begin = s;
+    r_end = min(nrows[b], lim);
+  } else {
+    const int w1 = min(kTile, np), wt = min(2 * kTile, np);
+    if (wt <= w1) return;
+    w = w1;
+    s = k + w1;
+    r_begin = k + w1;
+    r_end = k + wt;
+  }
   const int tn_count = (nc - s + kTile - 1) / kTile;
   if (tn_count <= 0) return;
   const int tm = blockIdx.x / tn_count, tn = blockIdx.x - tm * tn_count;
-  const int r0 = s + tm * kTrailBM, c0 = s + tn * kTile;
-  if (r0 >= nr) return;
+  const int r0 = r_begin + tm * kTrailBM, c0 = s + tn * kTile;
+  if (r0 >= r_end) return;
   const int L = ld[b];
   double* M = base + off[b];
-  tile_mma_t<kTrailBM>(M + (long long)r0 * L + c0, L, min(kTrailBM, nr - r0), min(kTile, nc - c0),
+  tile_mma_t<kTrailBM>(M + (long long)r0 * L + c0, L, min(kTrailBM, r_end - r0), min(kTile, nc - c0),
                        M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0,
                        sm);
+}
+
+// 128-wide panels: W_top -= W1_Q W2 on rows [k, k+64), cols [k + w, ncols),
+// where W1_Q = M[k:k+64, k+64:k+w] and W2 = M[k+64:k+w, k+w:]
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_fix_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ npiv, const int* __restrict__ ncols, int k) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  const int np = npiv[b] - k;
+  const int wt = min(2 * kTile, np);
+  if (wt <= kTile) return;
+  const int w2 = wt - kTile;
+  const int c0 = k + wt + blockIdx.x * kTile;
+  if (c0 >= ncols[b]) return;
+  const int L = ld[b];
+  double* M = base + off[b];
+  tile_mma(M + (long long)k * L + c0, L, kTile, min(kTile, ncols[b] - c0),
+           M + (long long)k * L + k + kTile, L, M + (long long)(k + kTile) * L + c0, L, w2, -1.0,
+           1.0, sm);
 }
 
 // L' = A21 P_k in place on the panel column rows [k+w, lim) (coarse envelope
@@ -357,7 +394,7 @@ __global__ void __launch_bounds__(256) recover_kernel(
     const int* __restrict__ nI, const int* __restrict__ nB, const long long* __restrict__ voff,
     const int* __restrict__ iface_perm, const long long* __restrict__ ioff,
     const long long* __restrict__ interior_nodes, const double* __restrict__ u_hat,
-    double* __restrict__ u) {
+    double* __restrict__ u, int panel) {
   extern __shared__ double us[];  // nI + nB
   const int b = blockIdx.x;
   const int ni = nI[b], nb = nB[b], L = ld[b], nl = ni + nb;
@@ -365,9 +402,10 @@ __global__ void __launch_bounds__(256) recover_kernel(
   for (int j = threadIdx.x; j < nb; j += blockDim.x) us[ni + j] = u_hat[iface_perm[voff[b] + j]];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int last = ((ni - 1) / kTile) * kTile;
-  for (int k = last; k >= 0; k -= kTile) {
-    const int w = min(kTile, ni - k);
+  // panels of the elimination (W = A11^-1 A12 per panel, identity diagonal)
+  const int last = ((ni - 1) / panel) * panel;
+  for (int k = last; k >= 0; k -= panel) {
+    const int w = min(panel, ni - k);
     for (int r = k + warp; r < k + w; r += nw) {
       const double* row = M + (long long)r * L;
       double s = 0.0;
@@ -399,6 +437,7 @@ static int smem_tile_setup() {
     cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(gj_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(panel_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(schur_fix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     done = true;
   }
   return (int)sizeof(TileSmem);
@@ -425,13 +464,14 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
 
 static int schur_eliminate_impl(double* M, const long long* off, const int* ld, const int* npiv,
                                 const int* nrows, const int* ncols, int nbatch, int max_npiv,
-                                int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
-                                long long pinv_step_stride, int* status, int require_positive,
-                                double* piv_out, long long piv_stride, cudaStream_t stream,
-                                double* host_trailing_ms) {
+                                int max_rows, int max_cols, int panel, double* pinv_ws,
+                                long long pinv_stride, long long pinv_step_stride, int* status,
+                                int require_positive, double* piv_out, long long piv_stride,
+                                cudaStream_t stream, double* host_trailing_ms) {
   if (nbatch <= 0) return 0;
+  if (panel != 2 * kTile) panel = kTile;
   const int smem = smem_tile_setup();
-  const int nsteps = (max_npiv + kTile - 1) / kTile;
+  const int nsteps = (max_npiv + panel - 1) / panel;
   cudaEvent_t* ev = nullptr;
   if (host_trailing_ms) {
     ev = new cudaEvent_t[2 * nsteps];
@@ -439,22 +479,39 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
     *host_trailing_ms = 0.0;
   }
   int launches = 0, timed = 0;
-  for (int k = 0; k < max_npiv; k += kTile) {
-    double* P = pinv_ws + (long long)(k / kTile) * pinv_step_stride;
+  const size_t tsm = sizeof(TileSmemT<kTrailBM>);
+  for (int k = 0; k < max_npiv; k += panel) {
+    double* P = pinv_ws + (long long)(k / panel) * pinv_step_stride;
+    // first (or only) 64-wide sub-panel: pivot inverse, W1 = P1 A12
     pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, k, P, pinv_stride, status,
                                                      require_positive, piv_out, piv_stride);
     ++launches;
-    const int ct = ceil_div(max_cols - k, kTile);
-    const int rt = ceil_div(max_rows - k, kTrailBM);
-    if (ct > 0) {
-      schur_row_kernel<<<dim3(ct, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
-                                                                        P, pinv_stride, 0x7fffffff);
+    const int ct1 = ceil_div(max_cols - k, kTile);
+    if (ct1 > 0) {
+      schur_row_kernel<<<dim3(ct1, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
+                                                                         P, pinv_stride, 0x7fffffff);
       ++launches;
     }
+    if (panel == 2 * kTile && k + kTile < max_npiv) {
+      // second sub-panel: strip update of its 64 rows, pivot inverse, W2,
+      // then W_top -= W1_Q W2 so the pivot rows hold A11^-1 A12 for all 128
+      const int cts = ceil_div(max_cols - k - kTile, kTile);
+      schur_trailing_kernel<<<dim3(cts, nbatch), kTileThreads, tsm, stream>>>(
+          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1);
+      pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, k + kTile, P, pinv_stride,
+                                                       status, require_positive, piv_out,
+                                                       piv_stride);
+      schur_row_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(
+          M, off, ld, npiv, ncols, k + kTile, P, pinv_stride, 0x7fffffff);
+      schur_fix_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k);
+      launches += 4;
+    }
+    const int ct = ceil_div(max_cols - k, kTile);
+    const int rt = ceil_div(max_rows - k, kTrailBM);
     if (ct > 0 && rt > 0) {
       if (ev) cudaEventRecord(ev[2 * timed], stream);
-      schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, sizeof(TileSmemT<kTrailBM>), stream>>>(
-          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff);
+      schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, tsm, stream>>>(
+          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, panel, 0);
       ++launches;
       if (ev) cudaEventRecord(ev[2 * timed + 1], stream);
       timed += (ev != nullptr);
@@ -476,22 +533,23 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
 
 int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const int* npiv,
                          const int* nrows, const int* ncols, int nbatch, int max_npiv,
-                         int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
-                         long long pinv_step_stride, int* status, int require_positive,
-                         double* piv_out, long long piv_stride, cudaStream_t stream) {
+                         int max_rows, int max_cols, int panel, double* pinv_ws,
+                         long long pinv_stride, long long pinv_step_stride, int* status,
+                         int require_positive, double* piv_out, long long piv_stride,
+                         cudaStream_t stream) {
   return schur_eliminate_impl(M, off, ld, npiv, nrows, ncols, nbatch, max_npiv, max_rows,
-                              max_cols, pinv_ws, pinv_stride, pinv_step_stride, status,
+                              max_cols, panel, pinv_ws, pinv_stride, pinv_step_stride, status,
                               require_positive, piv_out, piv_stride, stream, nullptr);
 }
 
 int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, const int* npiv,
                                const int* nrows, const int* ncols, int nbatch, int max_npiv,
-                               int max_rows, int max_cols, double* pinv_ws, long long pinv_stride,
-                               long long pinv_step_stride, int* status, int require_positive,
-                               double* piv_out, long long piv_stride, cudaStream_t stream,
-                               double* host_trailing_ms) {
+                               int max_rows, int max_cols, int panel, double* pinv_ws,
+                               long long pinv_stride, long long pinv_step_stride, int* status,
+                               int require_positive, double* piv_out, long long piv_stride,
+                               cudaStream_t stream, double* host_trailing_ms) {
   return schur_eliminate_impl(M, off, ld, npiv, nrows, ncols, nbatch, max_npiv, max_rows,
-                              max_cols, pinv_ws, pinv_stride, pinv_step_stride, status,
+                              max_cols, panel, pinv_ws, pinv_stride, pinv_step_stride, status,
                               require_positive, piv_out, piv_stride, stream, host_trailing_ms);
 }
 
@@ -517,7 +575,7 @@ int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const in
       const int t = ceil_div(span, kTile);
       const int tr = ceil_div(span, kTrailBM);
       schur_row_kernel<<<dim3(t, 1), kTileThreads, smem, stream>>>(C, off, ldv, nv, nv, k, P, 0, lim);
-      schur_trailing_kernel<<<dim3(t * tr, 1), kTileThreads, sizeof(TileSmemT<kTrailBM>), stream>>>(C, off, ldv, nv, nv, nv, k, lim);
+      schur_trailing_kernel<<<dim3(t * tr, 1), kTileThreads, sizeof(TileSmemT<kTrailBM>), stream>>>(C, off, ldv, nv, nv, nv, k, lim, kTile, 0);
       panel_scale_kernel<<<t, kTileThreads, smem, stream>>>(C, (long long)n, k, w, lim, P);
       launches += 3;
     }
@@ -566,14 +624,14 @@ int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
 int bddc_recover_interior(const double* M, const long long* off, const int* ld, const int* nI,
                           const int* nB, const long long* voff, const int* iface_perm,
                           const long long* ioff, const long long* interior_nodes,
-                          const double* u_hat, double* u, int nbatch, int max_nloc,
+                          const double* u_hat, double* u, int nbatch, int max_nloc, int panel,
                           cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   const int smem = max_nloc * (int)sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(recover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   recover_kernel<<<nbatch, 256, smem, stream>>>(M, off, ld, nI, nB, voff, iface_perm, ioff,
-                                                interior_nodes, u_hat, u);
+                                                interior_nodes, u_hat, u, panel);
   bddc_note_launches(1);
   return launch_status();
 }

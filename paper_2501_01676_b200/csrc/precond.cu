@@ -545,7 +545,14 @@ __global__ void gather_reduce_kernel(const long long* __restrict__ tstart,
 //   forward  b_i -= L'_ik b_k            i in [k+w, lim_k)
 //   t = blockdiag(P_k) b
 //   backward t_i -= W_ik x_k (x_k = t_k)  i in [first_k, k)
-__global__ void __launch_bounds__(256) coarse_solve_coop_kernel(
+#ifndef BDDC_COOP_THREADS
+#define BDDC_COOP_THREADS 256
+#endif
+#ifndef BDDC_COOP_CTAS
+#define BDDC_COOP_CTAS 0   // 0: one CTA per SM
+#endif
+
+__global__ void __launch_bounds__(BDDC_COOP_THREADS) coarse_solve_coop_kernel(
     const double* __restrict__ A, long long ld, int n, const double* __restrict__ pinv,
     long long pstride, const int* __restrict__ lim, const int* __restrict__ first,
     double* __restrict__ b, double* __restrict__ t) {
@@ -794,14 +801,16 @@ int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_solve_coop_kernel, 256, 0);
-    grid = sms * (per_sm >= 1 ? 1 : 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_solve_coop_kernel,
+                                                  BDDC_COOP_THREADS, 0);
+    grid = BDDC_COOP_CTAS > 0 ? BDDC_COOP_CTAS : sms;
+    if (grid > sms * per_sm) grid = sms * per_sm;
     if (grid <= 0) grid = 1;
   }
   void* args[] = {(void*)&A, (void*)&ld, (void*)&n, (void*)&pinv, (void*)&pinv_step_stride,
                   (void*)&lim, (void*)&first, (void*)&b, (void*)&t};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)coarse_solve_coop_kernel, dim3(grid),
-                                              dim3(256), args, 0, stream);
+                                              dim3(BDDC_COOP_THREADS), args, 0, stream);
   bddc_note_launches(1);
   return e == cudaSuccess ? pc_status() : -(int)e;
 }

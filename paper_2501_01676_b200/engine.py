@@ -18,6 +18,7 @@ from ._lib import lib, require_cuda, stream
 from .plan import Plan, _excl, _ranges
 
 F64 = torch.float64
+PANEL = 128  # elimination panel width (two 64-wide sub-panels; DMMA trailing update with K = 128)
 
 
 # kernels launched through CUDA-graph replays (the C-ABI launch counter sees
@@ -104,7 +105,7 @@ class LocalSystem:
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
         args = (K, d.off, d.ld, d.nI, d.nL, d.nL1, p.N, int(p.nI.max()), int(p.nL.max()),
-                int(p.nL.max()) + 1, pinv, 4096, 0, status, 0, None, 0, st)
+                int(p.nL.max()) + 1, PANEL, pinv, 4096, 0, status, 0, None, 0, st)
         if self.kernel_timing:
             ms = ctypes.c_double(0.0)
             lib.bddc_schur_eliminate_timed(*args, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
@@ -157,14 +158,14 @@ class LocalSystem:
         return buf[int(p.voff[i]):int(p.voff[i + 1])].cpu().numpy()
 
 
-def trailing_flops(plan):
-    """Algorithmic flops of the Schur-elimination trailing updates (DMMA kernel):
-    sum over panels k and subdomains b of 2 * rows * cols * w."""
+def trailing_flops(plan, panel=PANEL):
+    """Algorithmic flops of the Schur-elimination trailing updates (DMMA kernel,
+    mode 0): sum over panels k and subdomains b of 2 * rows * cols * w."""
     nI, nL = plan.nI.astype(np.int64), plan.nL.astype(np.int64)
     total = 0
-    for k in range(0, int(nI.max()), 64):
+    for k in range(0, int(nI.max()), panel):
         act = nI > k
-        w = np.minimum(64, nI[act] - k)
+        w = np.minimum(panel, nI[act] - k)
         rows = nL[act] - k - w
         cols = nL[act] + 1 - k - w
         total += int((2 * rows * cols * w).sum())
@@ -562,7 +563,7 @@ class DevicePreconditioner:
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
         nbmax = int(p.nB.max())
         lib.bddc_schur_eliminate(tmp, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax, nbmax,
-                                 pinv, 4096, 0, status, 1, None, 0, st)
+                                 PANEL, pinv, 4096, 0, status, 1, None, 0, st)
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError(f"dual block of subdomain {bad} lost positive definiteness")
@@ -800,5 +801,5 @@ def recover_device(ls, u_hat):
     u = ls.inputs["gdir"].clone()
     u[dev_i64(ls.globs.interface_nodes)] = u_hat
     lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, d.iface_perm, d.ioff,
-                              d.I_nodes, u_hat, u, p.N, int(p.nL.max()), st)
+                              d.I_nodes, u_hat, u, p.N, int(p.nL.max()), PANEL, st)
     return u

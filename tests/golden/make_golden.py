@@ -125,6 +125,7 @@ CASES = {
     "cfg5_small": (lambda: ref_inputs_from_config(5, n=24, subs=3), 10.0, 10.0, ("new",), 1),
     "jump": (ref_inputs_jump, 1.0 + math.log(4), 10.0, ("new", "old"), 8),
     "cfg3": (lambda: ref_inputs_from_config(3), 10.0, 10.0, ("new",), 0),
+    "cfg4": (lambda: ref_inputs_from_config(4), 10.0, 10.0, ("new",), 0),
 }
 
 
@@ -144,4 +145,4 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or [k for k in CASES if k != "cfg3"])
+    main(sys.argv[1:] or [k for k in CASES if k not in ("cfg3", "cfg4")])

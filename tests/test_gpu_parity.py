@@ -10,7 +10,7 @@ from tests.cases import FIXTURES, counts_match, gevp_values, golden, inputs, var
 
 pytestmark = pytest.mark.gpu
 
-FAST = [n for n in FIXTURES if n != "cfg3"]
+FAST = [n for n in FIXTURES if n not in ("cfg3", "cfg4")]
 
 
 def _rel(a, b):
@@ -53,3 +53,28 @@ def test_pipeline_matches_reference(name):
         assert _rel(res.pc.apply(g["probe"]), g[f"{v}_Mprobe"]) <= 1e-7
         assert _rel(res.solution.cpu().numpy(), g[f"{v}_solution"]) <= 1e-8
         assert _rel(res.u.cpu().numpy(), g[f"{v}_u"]) <= 1e-8
+
+
+@pytest.mark.parametrize("name", [n for n in ("cfg3", "cfg4") if n in FIXTURES])
+def test_large_configs_match_reference(name):
+    """BASELINE configs[2] (512 subdomains) and configs[3] (irregular BFS
+    partition, 511 subdomains, faces up to 193 dofs) against the reference."""
+    from paper_2501_01676_b200 import pipeline
+
+    g = golden(name)
+    system, part, globs = inputs(name)
+    kinds = [gl.kind for gl in globs.globs]
+    v = "new"
+    res = pipeline.run(system, part, globs, float(g["theta_f"]), float(g["theta_e"]), v, keep=True)
+    assert np.array_equal(res.ls.plan.nB, g["nB"])
+    ref_eig = gevp_values(g, v)
+    mine = res.space.all_eigenvalues()
+    for k, ev in ref_eig.items():
+        fin = np.isfinite(ev)
+        scale = np.abs(ev[fin]).max(initial=1.0)
+        np.testing.assert_allclose(mine[k][fin], ev[fin], rtol=1e-8, atol=1e-10 * scale)
+    th = lambda k: float(g["theta_f"]) if kinds[k] == "face" else float(g["theta_e"])
+    assert counts_match(res.n_primal, g[f"{v}_n_primal"], None, ref_eig, th) == []
+    assert abs(res.iterations - int(g[f"{v}_iterations"])) <= 1
+    assert _rel(res.solution.cpu().numpy(), g[f"{v}_solution"]) <= 1e-8
+    assert _rel(res.u.cpu().numpy(), g[f"{v}_u"]) <= 1e-8

@@ -10,6 +10,8 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2501_01676_b200 import _lib  # noqa: E402
+import os  # noqa: E402
+PANEL = int(os.environ.get("PANEL", "128"))
 
 
 def run(path, N=4096, nI=343, nB=386, reps=3):
@@ -30,15 +32,15 @@ def run(path, N=4096, nI=343, nB=386, reps=3):
     P = lambda t: ctypes.c_void_p(t.data_ptr())
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
     flops = 0
-    for k in range(0, nI, 64):
-        w = min(64, nI - k)
+    for k in range(0, nI, PANEL):
+        w = min(PANEL, nI - k)
         flops += 2 * (nL - k - w) * (nL + 1 - k - w) * w * N
     best = 1e30
     for _ in range(reps):
         M = M0.clone()
         ms = ctypes.c_double(0)
         torch.cuda.synchronize()
-        f(P(M), P(off), P(i32(ld)), P(i32(nI)), P(i32(nL)), P(i32(nL + 1)), N, nI, nL, nL + 1,
+        f(P(M), P(off), P(i32(ld)), P(i32(nI)), P(i32(nL)), P(i32(nL + 1)), N, nI, nL, nL + 1, PANEL,
           P(pinv), 4096, 0, P(st), 0, None, 0, stream, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
         torch.cuda.synchronize()
         best = min(best, ms.value)
