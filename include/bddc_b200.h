@@ -108,11 +108,12 @@ int bddc_recover_interior(const double* M, const long long* off, const int* ld, 
 /* ---- globs.cu : scaling and adaptive coarse space ------------------------- */
 
 /* Deluxe scaling D_s = (sum_k B_k)^-1 B_s per glob; vertices 1/|n(V)|.
+ * Globs glob_ids[0..n_globs) (NULL: 0..n_globs-1); reads the slot blocks BsC.
  * replaces deluxe_scaling / vertex_scaling / build_scaling scaling.py:10-57. */
 int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
-                const int* sh_boff, const long long* sh_doff, const int* nB,
-                const long long* soff, const double* Bsym, double* D, double* ws,
-                const long long* ws_off, int* status, int n_globs, cudaStream_t stream);
+                const int* sh_boff, const long long* sh_doff, const double* BsC, double* D,
+                double* ws, const long long* ws_off, int* status, const int* glob_ids, int n_globs,
+                cudaStream_t stream);
 
 /* Face GEP + selection + change of basis.  fast = 1: certified fast path in a
  * compact arena (faces whose certificate fails get status 900 and must be
@@ -121,12 +122,11 @@ int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int
  *          parallel_sum / pseudo_inverse / sym_pencil_gevp linalg.py:23-214,
  *          build_change_of_basis adaptive.py:190-206. */
 int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
-                   const int* sh_boff, const long long* sh_doff, const int* nB,
-                   const long long* soff, const double* Bsym, const double* Binv, const double* D,
-                   double theta, double* eig, const long long* eig_off, int* n_sel, int* r,
-                   double* Q, const long long* q_off, int* status, double* ws,
-                   const long long* ws_off, const int* face_ids, int n_faces, int max_n,
-                   int fast, cudaStream_t stream);
+                   const int* sh_boff, const long long* sh_doff, const double* BsC,
+                   const double* BiC, const double* D, double theta, double* eig,
+                   const long long* eig_off, int* n_sel, int* r, double* Q, const long long* q_off,
+                   int* status, double* ws, const long long* ws_off, const int* face_ids,
+                   int n_faces, int max_n, int fast, cudaStream_t stream);
 
 /* Prior blocks of the face-transformed Bsym^-1 per subdomain.
  * replaces adaptive.py:310-329 (Minv = Q Bsym^-1 Q^T on face rows/cols, prior_idx). */
@@ -140,10 +140,9 @@ int bddc_priors(const int* kind, const int* size, const int* nB, const long long
  * replaces edge_block_with_priors substructuring.py:174-190, edge_gevp_new
  *          adaptive.py:94-156, reduce_edge_constraints adaptive.py:172-187. */
 int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
-                       const int* sh_boff, const long long* sh_doff, const int* nB,
-                       const long long* soff, const double* Bsym, const double* Binv,
-                       const double* D, const long long* pb_off, const int* nH, const double* PB,
-                       const double* XHH, const long long* xhh_off, double theta, double* eig,
+                       const int* sh_boff, const long long* sh_doff, const double* BsC,
+                       const double* BiC, const double* D, const double* EX,
+                       const long long* ex_off, const int* ex_h, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
                        const int* edge_ids, int n_edges, int max_dim, cudaStream_t stream);
@@ -151,12 +150,33 @@ int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, co
 /* Coupled ("old") edge GEP. replaces edge_gevp_old adaptive.py:75-91,
  *          parallel_sum_chain linalg.py:70-78. */
 int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
-                       const int* sh_boff, const long long* sh_doff, const int* nB,
-                       const long long* soff, const double* Bsym, const double* Binv,
-                       const double* D, double theta, double* eig, const long long* eig_off,
-                       int* n_sel, int* r, double* Q, const long long* q_off, int* status,
-                       double* ws, const long long* ws_off, const int* edge_ids, int n_edges,
-                       int max_n, cudaStream_t stream);
+                       const int* sh_boff, const long long* sh_doff, const double* BsC,
+                       const double* BiC, const double* D, double theta, double* eig,
+                       const long long* eig_off, int* n_sel, int* r, double* Q,
+                       const long long* q_off, int* status, double* ws, const long long* ws_off,
+                       const int* edge_ids, int n_edges, int max_n, cudaStream_t stream);
+
+/* Slot-compact glob blocks.  Every (glob, sharer) slot k whose sharer is a
+ * subdomain of this rank (slot_sub[k] = its local index, -1 otherwise) gets
+ * the n_g x n_g principal blocks of Bsym / Bsym^-1 at BsC / BiC + sh_doff[k]
+ * (BiC may be NULL); the per-glob kernels read only these buffers, so a
+ * sum-allreduce of them is the whole exchange the glob phase needs when the
+ * subdomains are sharded over ranks.
+ * replaces the per-glob Bsym[g_idx][:, g_idx] slicing of build_scaling
+ *          scaling.py:33-41 and glob_schur_block substructuring.py:152-171. */
+int bddc_extract_slot_blocks(const int* slot_sub, const int* slot_glob, const int* size,
+                             const int* sh_boff, const long long* sh_doff, const int* nB,
+                             const long long* soff, const double* Bsym, const double* Binv,
+                             double* BsC, double* BiC, int n_slots, cudaStream_t stream);
+
+/* Per local (edge, sharer) slot: X = [[Binv_EE, PB_E^T], [PB_E, XHH]] at
+ * EX + ex_off[k] ((ne+nH) x (ne+nH)), the input of the prior-aware edge Schur
+ * complement.  replaces edge_block_with_priors substructuring.py:174-190. */
+int bddc_edge_x_extract(const int* slot_sub, const int* slot_glob, const int* size,
+                        const int* kind, const int* sh_boff, const int* nB, const long long* soff,
+                        const double* Binv, const long long* pb_off, const int* nH,
+                        const double* PB, const double* XHH, const long long* xhh_off, double* EX,
+                        const long long* ex_off, int n_slots, cudaStream_t stream);
 
 /* workspace sizes (doubles) of the per-glob kernels, for the host planner */
 long long bddc_ws_face(long long n);

@@ -21,11 +21,15 @@ struct GlobTables {
   const int* sh_sub;        // sharer subdomain ids (ascending)
   const int* sh_boff;       // block offset of the glob inside the sharer's glob-major B order
   const long long* sh_doff; // offset of D_s (n_g x n_g) in the deluxe buffer
-  // per subdomain
+  // per subdomain (rank-local; priors only)
   const int* nB;
   const long long* soff;    // offset of the nB x nB matrices (S, Bsym, Binv)
   const double* Bsym;
   const double* Binv;
+  // per (glob, sharer) slot: compact Bsym / Bsym^-1 principal blocks at
+  // sh_doff[slot] (n_g x n_g, ld n_g), gathered from the owning ranks
+  const double* BsC;
+  const double* BiC;
 };
 
 // ---------------------------------------------------------------------------
@@ -412,9 +416,10 @@ BDDC_DEV int row_space_basis(const double* A, int lda, int m, int n, double* Q, 
 __global__ void __launch_bounds__(256) deluxe_kernel(GlobTables t, double* __restrict__ D,
                                                      double* __restrict__ ws,
                                                      const long long* __restrict__ ws_off,
-                                                     int* __restrict__ status) {
+                                                     int* __restrict__ status,
+                                                     const int* __restrict__ glob_ids) {
   __shared__ double rowbuf[2048];
-  const int g = blockIdx.x;
+  const int g = glob_ids ? glob_ids[blockIdx.x] : blockIdx.x;
   const int n = t.size[g];
   const int s0 = t.sh_start[g], s1 = t.sh_start[g + 1];
   if (t.kind[g] == 2 && n == 1) {
@@ -427,8 +432,7 @@ __global__ void __launch_bounds__(256) deluxe_kernel(GlobTables t, double* __res
     int r = idx / n, c = idx - r * n;
     double s = 0.0;
     for (int k = s0; k < s1; ++k) {
-      const int sub = t.sh_sub[k], bo = t.sh_boff[k], nb = t.nB[sub];
-      s += t.Bsym[t.soff[sub] + (long long)(bo + r) * nb + bo + c];
+      s += t.BsC[t.sh_doff[k] + (long long)r * n + c];
     }
     T[idx] = s;
   }
@@ -439,16 +443,14 @@ __global__ void __launch_bounds__(256) deluxe_kernel(GlobTables t, double* __res
     return;
   }
   for (int k = s0; k < s1; ++k) {
-    const int sub = t.sh_sub[k], bo = t.sh_boff[k], nb = t.nB[sub];
-    const double* Bs = t.Bsym + t.soff[sub] + (long long)bo * nb + bo;
-    blk::gemm(D + t.sh_doff[k], n, T, n, false, Bs, nb, false, n, n, n, 1.0, 0.0);
+    const double* Bs = t.BsC + t.sh_doff[k];
+    blk::gemm(D + t.sh_doff[k], n, T, n, false, Bs, n, false, n, n, n, 1.0, 0.0);
   }
 }
 
 // B~_X = sym(((Binv)[X,X])^-1) of sharer k into out (n x n); returns Status.
 BDDC_DEV int glob_schur(const GlobTables& t, int k, int n, double* out, double* rowbuf) {
-  const int sub = t.sh_sub[k], bo = t.sh_boff[k], nb = t.nB[sub];
-  blk::copy(out, n, t.Binv + t.soff[sub] + (long long)bo * nb + bo, nb, n, n);
+  blk::copy(out, n, t.BiC + t.sh_doff[k], n, n, n);
   const int st = blk::gj_inverse(out, n, n, true, rowbuf);
   if (st) return st;
   blk::symmetrize(out, n, n);
@@ -499,12 +501,11 @@ __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* _
   double* psw = PEN + nn;       // parallel-sum workspace: 5 n^2 + n from slot U
   double* T = PEN + 2 * nn;     // scratch for B_F (slot A2)
   const int k0 = t.sh_start[g];
-  const int si = t.sh_sub[k0], sj = t.sh_sub[k0 + 1];
   const double* Di = D + t.sh_doff[k0];
   const double* Dj = D + t.sh_doff[k0 + 1];
-  const double* Bi = t.Bsym + t.soff[si] + (long long)t.sh_boff[k0] * t.nB[si] + t.sh_boff[k0];
-  const double* Bj = t.Bsym + t.soff[sj] + (long long)t.sh_boff[k0 + 1] * t.nB[sj] + t.sh_boff[k0 + 1];
-  const int ldi = t.nB[si], ldj = t.nB[sj];
+  const double* Bi = t.BsC + t.sh_doff[k0];
+  const double* Bj = t.BsC + t.sh_doff[k0 + 1];
+  const int ldi = n, ldj = n;
   // B_F = sym(Dj^T Bi Dj + Di^T Bj Di)
   blk::gemm(T, n, Bi, ldi, false, Dj, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(BF, n, Dj, n, true, T, n, false, n, n, n, 1.0, 0.0);
@@ -601,12 +602,11 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   double* scr = w + n;                                              // kIILanes * 5 n
   int* iscr = reinterpret_cast<int*>(scr + blk::kIILanes * 5 * n);  // kIILanes * n ints
   const int k0 = t.sh_start[g];
-  const int si = t.sh_sub[k0], sj = t.sh_sub[k0 + 1];
   const double* Di = D + t.sh_doff[k0];
   const double* Dj = D + t.sh_doff[k0 + 1];
-  const double* Bi = t.Bsym + t.soff[si] + (long long)t.sh_boff[k0] * t.nB[si] + t.sh_boff[k0];
-  const double* Bj = t.Bsym + t.soff[sj] + (long long)t.sh_boff[k0 + 1] * t.nB[sj] + t.sh_boff[k0 + 1];
-  const int ldi = t.nB[si], ldj = t.nB[sj];
+  const double* Bi = t.BsC + t.sh_doff[k0];
+  const double* Bj = t.BsC + t.sh_doff[k0 + 1];
+  const int ldi = n, ldj = n;
   // 1. B_F = sym(Dj^T Bi Dj + Di^T Bj Di)
   blk::gemm(S1, n, Bi, ldi, false, Dj, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(S0, n, Dj, n, true, S1, n, false, n, n, n, 1.0, 0.0);
@@ -691,6 +691,72 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   if (threadIdx.x == 0) {
     o.n_sel[g] = k;
     o.r[g] = r;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Slot blocks owned by this rank: Bsym / Bsym^-1 principal blocks of every
+// (glob, sharer) slot whose sharer is a local subdomain, into the compact
+// per-slot buffers (sh_doff offsets).  Other ranks' slots stay untouched
+// (zero) so a sum-allreduce assembles the global buffers.
+// ---------------------------------------------------------------------------
+__global__ void extract_slot_blocks_kernel(const int* __restrict__ slot_sub,
+                                           const int* __restrict__ slot_glob,
+                                           const int* __restrict__ gsize,
+                                           const int* __restrict__ sh_boff,
+                                           const long long* __restrict__ sh_doff,
+                                           const int* __restrict__ nB,
+                                           const long long* __restrict__ soff,
+                                           const double* __restrict__ Bsym,
+                                           const double* __restrict__ Binv,
+                                           double* __restrict__ BsC, double* __restrict__ BiC,
+                                           int n_slots) {
+  const int k = blockIdx.x;
+  if (k >= n_slots) return;
+  const int s = slot_sub[k];
+  if (s < 0) return;
+  const int n = gsize[slot_glob[k]], bo = sh_boff[k], nb = nB[s];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    const long long src = soff[s] + (long long)(bo + r) * nb + bo + c;
+    BsC[sh_doff[k] + idx] = Bsym[src];
+    if (BiC) BiC[sh_doff[k] + idx] = Binv[src];
+  }
+}
+
+// X block of every local (edge, sharer) slot: [[Binv[E,E], PB[:,E]^T], [PB[:,E], XHH]]
+__global__ void edge_x_extract_kernel(const int* __restrict__ slot_sub,
+                                      const int* __restrict__ slot_glob,
+                                      const int* __restrict__ gsize,
+                                      const int* __restrict__ kind,
+                                      const int* __restrict__ sh_boff,
+                                      const int* __restrict__ nB,
+                                      const long long* __restrict__ soff,
+                                      const double* __restrict__ Binv,
+                                      const long long* __restrict__ pb_off,
+                                      const int* __restrict__ nH, const double* __restrict__ PB,
+                                      const double* __restrict__ XHH,
+                                      const long long* __restrict__ xhh_off,
+                                      double* __restrict__ EX, const long long* __restrict__ ex_off,
+                                      int n_slots) {
+  const int k = blockIdx.x;
+  if (k >= n_slots) return;
+  const int s = slot_sub[k];
+  const int g = slot_glob[k];
+  if (s < 0 || kind[g] != 1) return;
+  const int ne = gsize[g], bo = sh_boff[k], nb = nB[s], h = nH[s], d = ne + h;
+  const double* Bi = Binv + soff[s];
+  const double* P = PB + pb_off[s];
+  const double* XH = XHH + xhh_off[s];
+  double* X = EX + ex_off[k];
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
+    const int r = idx / d, c = idx - r * d;
+    double v;
+    if (r < ne && c < ne) v = Bi[(long long)(bo + r) * nb + bo + c];
+    else if (r < ne) v = P[(long long)(c - ne) * nb + bo + r];
+    else if (c < ne) v = P[(long long)(r - ne) * nb + bo + c];
+    else v = XH[(r - ne) * h + (c - ne)];
+    X[idx] = v;
   }
 }
 
@@ -786,11 +852,10 @@ __global__ void __launch_bounds__(256) priors_kernel(
 // basis (adaptive.py:172-206)
 // ---------------------------------------------------------------------------
 struct PriorTables {
-  const long long* pb_off;
-  const int* nH;
-  const double* PB;
-  const double* XHH;
-  const long long* xhh_off;
+  // per (edge, sharer) slot: Schur input block X = [[Binv_EE, PB_E^T], [PB_E, XHH]]
+  const double* EX;
+  const long long* ex_off;
+  const int* ex_h;         // nH of the sharer
 };
 
 __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const double* __restrict__ D,
@@ -804,7 +869,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
   const int k0 = t.sh_start[g], ns = t.sh_start[g + 1] - k0;
   const int nC = (ns - 1) * ne;
   int Wd = nC + ne;
-  for (int i = 0; i < ns; ++i) Wd += pr.nH[t.sh_sub[k0 + i]];
+  for (int i = 0; i < ns; ++i) Wd += pr.ex_h[k0 + i];
   const int dimmax = Wd;
   double* cs = sh;
   double* red = cs + 2 * (dimmax + 2);
@@ -817,7 +882,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
   double* Bt = M + nC * nC;                  // Wd x Wd
   double* X = Bt + (long long)Wd * Wd;       // (ne+nHmax)^2 per-sharer Schur block
   int nHmax = 0;
-  for (int i = 0; i < ns; ++i) nHmax = max(nHmax, pr.nH[t.sh_sub[k0 + i]]);
+  for (int i = 0; i < ns; ++i) nHmax = max(nHmax, pr.ex_h[k0 + i]);
   const int xd = ne + nHmax;
   double* T1 = X + (long long)xd * xd;       // scratch: max(Wd, nC) x max(Wd, nC)
   double* T2 = T1 + (long long)Wd * Wd;
@@ -835,10 +900,9 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
   // M = sym(sum_i J_i^T B_E^(i) J_i)
   blk::fill(M, nC, nC, nC, 0.0);
   for (int i = 0; i < ns; ++i) {
-    const int sub = t.sh_sub[k0 + i], bo = t.sh_boff[k0 + i], nb = t.nB[sub];
-    const double* BE = t.Bsym + t.soff[sub] + (long long)bo * nb + bo;
+    const double* BE = t.BsC + t.sh_doff[k0 + i];
     const double* Ji = Jall + (long long)i * ne * nC;
-    blk::gemm(T1, nC, BE, nb, false, Ji, nC, false, ne, nC, ne, 1.0, 0.0);
+    blk::gemm(T1, nC, BE, ne, false, Ji, nC, false, ne, nC, ne, 1.0, 0.0);
     blk::gemm(M, nC, Ji, nC, true, T1, nC, false, nC, nC, ne, 1.0, 1.0);
   }
   blk::symmetrize(M, nC, nC);
@@ -847,23 +911,10 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
   blk::fill(Bt, Wd, Wd, Wd, 0.0);
   int hcol = A0;
   for (int i = 0; i < ns; ++i) {
-    const int sub = t.sh_sub[k0 + i], bo = t.sh_boff[k0 + i], nb = t.nB[sub];
-    const int h = pr.nH[sub];
+    const int h = pr.ex_h[k0 + i];
     const int d = ne + h;
-    const double* Binv = t.Binv + t.soff[sub];
-    const double* PBs = pr.PB + pr.pb_off[sub];
-    const double* XH = pr.XHH + pr.xhh_off[sub];
-    // X = [[Binv[E,E], PB[:,E]^T], [PB[:,E], XHH]]
-    for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
-      int r = idx / d, c = idx - r * d;
-      double v;
-      if (r < ne && c < ne) v = Binv[(long long)(bo + r) * nb + bo + c];
-      else if (r < ne) v = PBs[(long long)(c - ne) * nb + bo + r];
-      else if (c < ne) v = PBs[(long long)(r - ne) * nb + bo + c];
-      else v = XH[(r - ne) * h + (c - ne)];
-      X[r * d + c] = v;
-    }
-    __syncthreads();
+    // X = [[Binv[E,E], PB[:,E]^T], [PB[:,E], XHH]] of this sharer (edge_x_extract)
+    blk::copy(X, d, pr.EX + pr.ex_off[k0 + i], d, d, d);
     int st = blk::gj_inverse(X, d, d, true, rowbuf);
     if (st) {
       if (threadIdx.x == 0) o.status[g] = 100 + i;
@@ -1016,12 +1067,11 @@ __global__ void __launch_bounds__(256) edge_old_kernel(GlobTables t, const doubl
   double* scratch = rows + nn + n;
   blk::fill(BE, n, n, n, 0.0);
   for (int i = 0; i < ns; ++i) {
-    const int sub = t.sh_sub[k0 + i], bo = t.sh_boff[k0 + i], nb = t.nB[sub];
-    const double* Bi = t.Bsym + t.soff[sub] + (long long)bo * nb + bo;
+    const double* Bi = t.BsC + t.sh_doff[k0 + i];
     for (int k = 0; k < ns; ++k) {
       if (k == i) continue;
       const double* Dk = D + t.sh_doff[k0 + k];
-      blk::gemm(T, n, Bi, nb, false, Dk, n, false, n, n, n, 1.0, 0.0);
+      blk::gemm(T, n, Bi, n, false, Dk, n, false, n, n, n, 1.0, 0.0);
       blk::gemm(BE, n, Dk, n, true, T, n, false, n, n, n, 1.0, 1.0);
     }
   }
@@ -1087,11 +1137,10 @@ static int glob_launch_status() {
 
 static GlobTables make_tables(const int* kind, const int* size, const int* sh_start,
                               const int* sh_sub, const int* sh_boff, const long long* sh_doff,
-                              const int* nB, const long long* soff, const double* Bsym,
-                              const double* Binv) {
-  GlobTables t;
+                              const double* BsC, const double* BiC) {
+  GlobTables t{};
   t.kind = kind; t.size = size; t.sh_start = sh_start; t.sh_sub = sh_sub; t.sh_boff = sh_boff;
-  t.sh_doff = sh_doff; t.nB = nB; t.soff = soff; t.Bsym = Bsym; t.Binv = Binv;
+  t.sh_doff = sh_doff; t.BsC = BsC; t.BiC = BiC;
   return t;
 }
 
@@ -1116,25 +1165,48 @@ long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long n
   return bddc_edge_new_ws(ns, ne, wd, nhmax);
 }
 
+int bddc_extract_slot_blocks(const int* slot_sub, const int* slot_glob, const int* size,
+                             const int* sh_boff, const long long* sh_doff, const int* nB,
+                             const long long* soff, const double* Bsym, const double* Binv,
+                             double* BsC, double* BiC, int n_slots, cudaStream_t stream) {
+  if (n_slots <= 0) return 0;
+  extract_slot_blocks_kernel<<<n_slots, 128, 0, stream>>>(slot_sub, slot_glob, size, sh_boff, sh_doff,
+                                                          nB, soff, Bsym, Binv, BsC, BiC, n_slots);
+  bddc_note_launches(1);
+  return glob_launch_status();
+}
+
+int bddc_edge_x_extract(const int* slot_sub, const int* slot_glob, const int* size,
+                        const int* kind, const int* sh_boff, const int* nB, const long long* soff,
+                        const double* Binv, const long long* pb_off, const int* nH,
+                        const double* PB, const double* XHH, const long long* xhh_off, double* EX,
+                        const long long* ex_off, int n_slots, cudaStream_t stream) {
+  if (n_slots <= 0) return 0;
+  edge_x_extract_kernel<<<n_slots, 128, 0, stream>>>(slot_sub, slot_glob, size, kind, sh_boff, nB, soff,
+                                                     Binv, pb_off, nH, PB, XHH, xhh_off, EX, ex_off,
+                                                     n_slots);
+  bddc_note_launches(1);
+  return glob_launch_status();
+}
+
 int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
-                const int* sh_boff, const long long* sh_doff, const int* nB,
-                const long long* soff, const double* Bsym, double* D, double* ws,
-                const long long* ws_off, int* status, int n_globs, cudaStream_t stream) {
+                const int* sh_boff, const long long* sh_doff, const double* BsC, double* D,
+                double* ws, const long long* ws_off, int* status, const int* glob_ids, int n_globs,
+                cudaStream_t stream) {
   if (n_globs <= 0) return 0;
-  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, nullptr);
-  deluxe_kernel<<<n_globs, 256, 0, stream>>>(t, D, ws, ws_off, status); bddc_note_launches(1);
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, nullptr);
+  deluxe_kernel<<<n_globs, 256, 0, stream>>>(t, D, ws, ws_off, status, glob_ids); bddc_note_launches(1);
   return glob_launch_status();
 }
 
 int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
-                   const int* sh_boff, const long long* sh_doff, const int* nB,
-                   const long long* soff, const double* Bsym, const double* Binv, const double* D,
-                   double theta, double* eig, const long long* eig_off, int* n_sel, int* r,
-                   double* Q, const long long* q_off, int* status, double* ws,
-                   const long long* ws_off, const int* face_ids, int n_faces, int max_n,
-                   int fast, cudaStream_t stream) {
+                   const int* sh_boff, const long long* sh_doff, const double* BsC,
+                   const double* BiC, const double* D, double theta, double* eig,
+                   const long long* eig_off, int* n_sel, int* r, double* Q, const long long* q_off,
+                   int* status, double* ws, const long long* ws_off, const int* face_ids,
+                   int n_faces, int max_n, int fast, cudaStream_t stream) {
   if (n_faces <= 0) return 0;
-  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, Binv);
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC);
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int small = face_small_bytes(max_n);
   if (fast) {
@@ -1160,23 +1232,23 @@ int bddc_priors(const int* kind, const int* size, const int* nB, const long long
                 const long long* pb_off, const int* nH, double* PB, double* XHH,
                 const long long* xhh_off, int n_sub, cudaStream_t stream) {
   if (n_sub <= 0) return 0;
-  GlobTables t = make_tables(kind, size, nullptr, nullptr, nullptr, nullptr, nB, soff, nullptr, Binv);
+  GlobTables t{};
+  t.kind = kind; t.size = size; t.nB = nB; t.soff = soff; t.Binv = Binv;
   priors_kernel<<<n_sub, 256, 0, stream>>>(t, sub_glob_start, sub_globs, sub_glob_boff, r, Q,
                                            q_off, pb_off, nH, PB, XHH, xhh_off); bddc_note_launches(1);
   return glob_launch_status();
 }
 
 int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
-                       const int* sh_boff, const long long* sh_doff, const int* nB,
-                       const long long* soff, const double* Bsym, const double* Binv,
-                       const double* D, const long long* pb_off, const int* nH, const double* PB,
-                       const double* XHH, const long long* xhh_off, double theta, double* eig,
+                       const int* sh_boff, const long long* sh_doff, const double* BsC,
+                       const double* BiC, const double* D, const double* EX,
+                       const long long* ex_off, const int* ex_h, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
                        const int* edge_ids, int n_edges, int max_dim, cudaStream_t stream) {
   if (n_edges <= 0) return 0;
-  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, Binv);
-  PriorTables pr{pb_off, nH, PB, XHH, xhh_off};
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC);
+  PriorTables pr{EX, ex_off, ex_h};
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int smem = shmem_for(max_dim);
   if (smem > 48 * 1024) cudaFuncSetAttribute(edge_new_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1185,14 +1257,13 @@ int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, co
 }
 
 int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
-                       const int* sh_boff, const long long* sh_doff, const int* nB,
-                       const long long* soff, const double* Bsym, const double* Binv,
-                       const double* D, double theta, double* eig, const long long* eig_off,
-                       int* n_sel, int* r, double* Q, const long long* q_off, int* status,
-                       double* ws, const long long* ws_off, const int* edge_ids, int n_edges,
-                       int max_n, cudaStream_t stream) {
+                       const int* sh_boff, const long long* sh_doff, const double* BsC,
+                       const double* BiC, const double* D, double theta, double* eig,
+                       const long long* eig_off, int* n_sel, int* r, double* Q,
+                       const long long* q_off, int* status, double* ws, const long long* ws_off,
+                       const int* edge_ids, int n_edges, int max_n, cudaStream_t stream) {
   if (n_edges <= 0) return 0;
-  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, nB, soff, Bsym, Binv);
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC);
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int smem = shmem_for(max_n);
   if (smem > 48 * 1024) cudaFuncSetAttribute(edge_old_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

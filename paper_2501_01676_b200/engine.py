@@ -6,6 +6,11 @@ of ``_bddc_b200.so`` (include/bddc_b200.h); torch only owns device memory
 and the stream.  The host does integer planning (plan.py), status checks and
 GMRES's (j+2) x (j+1) least-squares recurrence, like the reference driver
 (solver.py:297).
+
+With a ``comm`` (dist.py) the subdomains are sharded over ranks: each
+LocalSystem holds only its rank's subdomains and the exchange points are the
+sum-allreduces listed in dist.py; without one (or with one rank) nothing is
+exchanged and the code path is the single-GPU one.
 """
 
 import ctypes
@@ -29,6 +34,16 @@ GRAPH_STATS = {"captured": 0, "replayed": 0}
 class NumericalError(RuntimeError):
     """Raised when a factorization or eigensolve cannot be completed
     (reference linalg.py:11)."""
+
+
+def _multi(comm):
+    return comm is not None and comm.size > 1
+
+
+def _allreduce(comm, *ts):
+    if _multi(comm):
+        for t in ts:
+            comm.allreduce_(t)
 
 
 def dev_i32(a):
@@ -77,17 +92,26 @@ class LocalSystem:
     and SubdomainOperator.bsym_inverse (substructuring.py:64-75)."""
 
     def __init__(self, system, partition, globs, plan=None, inputs=None, timer=None,
-                 kernel_timing=False, dplan=None):
+                 kernel_timing=False, dplan=None, comm=None):
         require_cuda()
         self.kernel_timing = kernel_timing
         self.trailing_ms = None
+        self.comm = comm
         self.system, self.partition, self.globs = system, partition, globs
+        if plan is not None:
+            owned = plan.owned
+        elif _multi(comm):
+            owned = comm.owned(partition.n_subdomains)
+        else:
+            owned = None
         if inputs is None:
-            inputs = upload_inputs(system, partition)
+            inputs = upload_inputs(system, partition, owned=owned if plan is None else None)
         self.inputs = inputs
         if plan is None:
-            plan = Plan(system, partition, globs, device_inputs=inputs)
+            plan = Plan(system, partition, globs, device_inputs=inputs, owned=owned)
         self.plan = plan
+        self.s0 = plan.owned[0]
+        self._BsC = self._BiC = None
         self.plan.check()
         p = self.plan
         self.N = p.N
@@ -120,7 +144,7 @@ class LocalSystem:
                                self.g, p.N, st)
         bad = _first_bad(status)
         if bad is not None:
-            raise NumericalError(f"interior block of subdomain {bad} is singular")
+            raise NumericalError(f"interior block of subdomain {bad + self.s0} is singular")
 
     def bsym_inverse(self):
         """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check."""
@@ -135,10 +159,31 @@ class LocalSystem:
             bad = _first_bad(status)
             if bad is not None:
                 B = self.matrix(self.Bsym, bad)
-                raise NumericalError(f"Bsym of subdomain {bad} is not positive definite "
+                raise NumericalError(f"Bsym of subdomain {bad + self.s0} is not positive definite "
                                      f"(cond ~ {np.linalg.cond(B):.2e})")
             self._Binv = Binv
         return self._Binv
+
+    def _slot_blocks(self, src):
+        p, d = self.plan, self.d
+        out = torch.zeros(max(p.d_total, 1), dtype=F64, device="cuda")
+        lib.bddc_extract_slot_blocks(d.slot_local, d.slot_glob, d.gsize, d.sh_boff, d.sh_doff,
+                                     d.nB, d.soff, src, None, out, None, int(p.sh_sub.size),
+                                     stream())
+        _allreduce(self.comm, out)
+        return out
+
+    def slot_bsym(self):
+        """Bsym[g, g] of every (glob, sharer) slot, all ranks' (sh_doff layout)."""
+        if self._BsC is None:
+            self._BsC = self._slot_blocks(self.Bsym)
+        return self._BsC
+
+    def slot_binv(self):
+        """(Bsym^-1)[g, g] of every (glob, sharer) slot, all ranks'."""
+        if self._BiC is None:
+            self._BiC = self._slot_blocks(self.bsym_inverse())
+        return self._BiC
 
     @property
     def interior_nodes_host(self):
@@ -215,25 +260,34 @@ class DevicePlan:
         self.sh_boff = dev_i32(p.sh_boff)
         self.sh_doff = dev_i64(p.sh_doff)
         self.slot_glob = dev_i32(p.slot_glob)
+        self.slot_local = dev_i32(p.slot_local)
 
 
-def upload_inputs(system, partition=None, pinned=False):
+def upload_inputs(system, partition=None, pinned=False, owned=None):
     """Element blocks, connectivity, Dirichlet data (and the element ->
-    subdomain map, for the device-side symbolic plan) to the device."""
+    subdomain map, for the device-side symbolic plan) to the device.
+    owned=(s0, s1): only the elements of subdomains s0..s1-1 (a rank's shard)."""
     def up(a, dt):
         t = torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
         if pinned:
             t = t.pin_memory()
         return t.cuda(non_blocking=pinned)
+    Ke = system.elem_matrices.reshape(-1, 16)
+    Fe = system.elem_rhs.reshape(-1, 4)
+    conn = system.mesh.elements
+    sub_of = None if partition is None else np.asarray(partition.subdomain_of)
+    if owned is not None and sub_of is not None and tuple(owned) != (0, partition.n_subdomains):
+        sel = np.flatnonzero((sub_of >= owned[0]) & (sub_of < owned[1]))
+        Ke, Fe, conn, sub_of = Ke[sel], Fe[sel], conn[sel], sub_of[sel]
     out = {
-        "Ke": up(system.elem_matrices.reshape(-1, 16), np.float64),
-        "Fe": up(system.elem_rhs.reshape(-1, 4), np.float64),
-        "conn": up(system.mesh.elements, np.int64),
+        "Ke": up(Ke, np.float64),
+        "Fe": up(Fe, np.float64),
+        "conn": up(conn, np.int64),
         "gdir": up(system.dirichlet_values, np.float64),
         "free": up(np.asarray(system.node_to_free) >= 0, np.bool_),
     }
-    if partition is not None:
-        out["sub_of"] = up(partition.subdomain_of, np.int64)
+    if sub_of is not None:
+        out["sub_of"] = up(sub_of, np.int64)
     return out
 
 
@@ -245,14 +299,20 @@ class DeviceScaling:
     """Deluxe families per glob (reference scaling.py:47-57)."""
 
     def __init__(self, ls):
-        p, d = ls.plan, ls.d
+        p, d, comm = ls.plan, ls.d, ls.comm
         self.ls = ls
-        self.D = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
+        multi = _multi(comm)
+        alloc = torch.zeros if multi else torch.empty
+        self.D = alloc(max(p.d_total, 1), dtype=F64, device="cuda")
         ws_off = _excl(p.gsize.astype(np.int64) ** 2)
         ws = torch.empty(max(int(ws_off[-1]), 1), dtype=F64, device="cuda")
         status = torch.zeros(max(p.G, 1), dtype=torch.int32, device="cuda")
-        lib.bddc_deluxe(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, d.nB, d.soff,
-                        ls.Bsym, self.D, ws, dev_i64(ws_off[:-1]), status, p.G, stream())
+        mine = np.flatnonzero(p.glob_mine) if multi else None
+        lib.bddc_deluxe(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
+                        ls.slot_bsym(), self.D, ws, dev_i64(ws_off[:-1]), status,
+                        None if mine is None else dev_i32(mine),
+                        p.G if mine is None else mine.size, stream())
+        _allreduce(comm, self.D, status)
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError("deluxe block sum is singular "
@@ -324,18 +384,16 @@ class DevicePrimalSpace:
     def __init__(self, ls, scaling, theta_f, theta_e, variant):
         if variant not in ("old", "new"):
             raise ValueError(f"unknown variant {variant!r}")
-        p, d, st = ls.plan, ls.d, stream()
+        p, d, st, comm = ls.plan, ls.d, stream(), ls.comm
+        multi = _multi(comm)
         self.ls, self.variant = ls, variant
         self.theta_f, self.theta_e = float(theta_f), float(theta_e)
-        Binv = ls.bsym_inverse()
+        BsC, BiC = ls.slot_bsym(), ls.slot_binv()
         G = p.G
         kind = p.kind
         nsh = np.diff(p.sh_start).astype(np.int64)
         self.q_off = _excl(p.gsize.astype(np.int64) ** 2)
         self.Q = torch.zeros(max(int(self.q_off[-1]), 1), dtype=F64, device="cuda")
-        vert = np.flatnonzero(kind == 2)
-        if vert.size:
-            self.Q[dev_i64(self.q_off[vert])] = 1.0  # 1x1 identity (vertices are fully primal)
         self.d_q_off = dev_i64(self.q_off[:-1])
         n_eig = np.where(kind == 0, p.gsize, 0).astype(np.int64)
         if variant == "new":
@@ -345,71 +403,99 @@ class DevicePrimalSpace:
         self.eig_off = _excl(n_eig)
         self.eig = torch.zeros(max(int(self.eig_off[-1]), 1), dtype=F64, device="cuda")
         d_eig_off = dev_i64(self.eig_off[:-1])
-        r0 = np.where(kind == 2, p.gsize, 0).astype(np.int32)
-        self.r = dev_i32(r0)
+        self.r = torch.zeros(max(G, 1), dtype=torch.int32, device="cuda")
         self.n_sel = torch.zeros(max(G, 1), dtype=torch.int32, device="cuda")
         status = torch.zeros(max(G, 1), dtype=torch.int32, device="cuda")
+        out = (self.eig, self.n_sel, self.r, self.Q, status)
 
-        faces = np.flatnonzero(kind == 0)
-        edges = np.flatnonzero(kind == 1)
+        # each glob is computed by the rank owning its first sharer
+        faces = np.flatnonzero((kind == 0) & p.glob_mine)
+        edges = np.flatnonzero((kind == 1) & p.glob_mine)
         if faces.size:
-            self._run_faces(faces, True, status, scaling, Binv, d_eig_off)
+            self._run_faces(faces, True, out, scaling, BsC, BiC, d_eig_off)
             s = status.cpu().numpy()
             redo = faces[s[faces] == 900]
             if redo.size:  # certificates failed: general algorithm (linalg.py:116-214)
                 status[dev_i64(redo)] = 0
-                self._run_faces(redo, False, status, scaling, Binv, d_eig_off)
-            self._raise(status, "face")
+                self._run_faces(redo, False, out, scaling, BsC, BiC, d_eig_off)
+        _allreduce(comm, *out)
+        self._raise(status, "face")
+        vert = np.flatnonzero(kind == 2)
+        if vert.size:  # vertices are fully primal: 1x1 identity, r = 1
+            self.Q[dev_i64(self.q_off[vert])] = 1.0
+            self.r[dev_i64(vert)] = dev_i32(p.gsize[vert])
         r_host = self.r.cpu().numpy()
-        if edges.size and variant == "new":
+        n_edges_all = int((kind == 1).sum())
+        # edge results of all ranks are summed into zeroed buffers, then added
+        eout = tuple(torch.zeros_like(t) for t in out) if multi else out
+        if n_edges_all and variant == "new":
             # prior sizes per subdomain: vertices + leading r_F of each face
-            k_kind = kind[p.sub_globs]
-            contrib = np.where(k_kind == 2, p.gsize[p.sub_globs],
-                               np.where(k_kind == 0, r_host[p.sub_globs], 0)).astype(np.int64)
-            nH = np.add.reduceat(contrib, p.sub_glob_start[:-1]) if contrib.size else np.zeros(p.N, np.int64)
-            nH = np.where(np.diff(p.sub_glob_start) > 0, nH, 0)
+            sh = p.sh_sub.astype(np.int64)
+            contrib = np.where(kind == 2, p.gsize, np.where(kind == 0, r_host[:G], 0))[p.slot_glob]
+            nH_glob = np.bincount(sh, weights=contrib, minlength=p.N_glob).astype(np.int64)
+            s0, s1 = p.owned
+            nH = nH_glob[s0:s1]
             pb_off = _excl(nH * p.nB)
             xhh_off = _excl(nH * nH)
             PB = torch.empty(max(int(pb_off[-1]), 1), dtype=F64, device="cuda")
             XHH = torch.empty(max(int(xhh_off[-1]), 1), dtype=F64, device="cuda")
             d_pb_off, d_nH, d_xhh_off = dev_i64(pb_off[:-1]), dev_i32(nH), dev_i64(xhh_off[:-1])
-            lib.bddc_priors(d.kind, d.gsize, d.nB, d.soff, Binv, d.sub_glob_start, d.sub_globs,
-                            d.sub_glob_boff, self.r, self.Q, self.d_q_off, d_pb_off, d_nH, PB, XHH,
-                            d_xhh_off, p.N, st)
-            ns = nsh[edges]
-            ne = p.gsize[edges].astype(np.int64)
-            sh_nH = nH[p.sh_sub.astype(np.int64)]
-            sumH = np.add.reduceat(sh_nH, p.sh_start[:-1].astype(np.int64))[edges]
-            maxH = np.maximum.reduceat(sh_nH, p.sh_start[:-1].astype(np.int64))[edges]
-            wd = (ns - 1) * ne + ne + sumH
-            wsz = _edge_new_ws(ns, ne, wd, maxH)
-            woff = np.zeros(G + 1, dtype=np.int64)
-            woff[edges] = _excl(wsz)[:-1]
-            ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
-            lib.bddc_edge_gevp_new(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
-                                   d.nB, d.soff, ls.Bsym, Binv, scaling.D, d_pb_off, d_nH, PB, XHH,
-                                   d_xhh_off, self.theta_e, self.eig, d_eig_off, self.n_sel,
-                                   self.r, self.Q, self.d_q_off, status, ws, dev_i64(woff[:-1]),
-                                   dev_i32(edges), edges.size, int(wd.max()), st)
-            self._raise(status, "edge")
-            del ws, PB, XHH
-        elif edges.size:
+            lib.bddc_priors(d.kind, d.gsize, d.nB, d.soff, ls.bsym_inverse(), d.sub_glob_start,
+                            d.sub_globs, d.sub_glob_boff, self.r, self.Q, self.d_q_off, d_pb_off,
+                            d_nH, PB, XHH, d_xhh_off, p.N, st)
+            # X blocks [[Binv_EE, PB_E^T], [PB_E, XHH]] per (edge, sharer) slot
+            sh_nH = nH_glob[sh]
+            is_edge_slot = kind[p.slot_glob] == 1
+            ex_sz = np.where(is_edge_slot, (p.gsize[p.slot_glob] + sh_nH) ** 2, 0).astype(np.int64)
+            ex_off = _excl(ex_sz)
+            EX = (torch.zeros if multi else torch.empty)(max(int(ex_off[-1]), 1), dtype=F64, device="cuda")
+            d_ex_off = dev_i64(ex_off[:-1])
+            lib.bddc_edge_x_extract(d.slot_local, d.slot_glob, d.gsize, d.kind, d.sh_boff, d.nB,
+                                    d.soff, ls.bsym_inverse(), d_pb_off, d_nH, PB, XHH, d_xhh_off,
+                                    EX, d_ex_off, int(sh.size), st)
+            _allreduce(comm, EX)
+            del PB, XHH
+            if edges.size:
+                ns = nsh[edges]
+                ne = p.gsize[edges].astype(np.int64)
+                sumH = np.add.reduceat(sh_nH, p.sh_start[:-1].astype(np.int64))[edges]
+                maxH = np.maximum.reduceat(sh_nH, p.sh_start[:-1].astype(np.int64))[edges]
+                wd = (ns - 1) * ne + ne + sumH
+                wsz = _edge_new_ws(ns, ne, wd, maxH)
+                woff = np.zeros(G + 1, dtype=np.int64)
+                woff[edges] = _excl(wsz)[:-1]
+                ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
+                e_eig, e_nsel, e_r, e_Q, e_status = eout
+                lib.bddc_edge_gevp_new(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
+                                       BsC, BiC, scaling.D, EX, d_ex_off, dev_i32(sh_nH),
+                                       self.theta_e, e_eig, d_eig_off, e_nsel, e_r, e_Q,
+                                       self.d_q_off, e_status, ws, dev_i64(woff[:-1]),
+                                       dev_i32(edges), edges.size, int(wd.max()), st)
+                del ws
+            del EX
+        elif n_edges_all and edges.size:
             wsz = _edge_old_ws(p.gsize[edges])
             woff = np.zeros(G + 1, dtype=np.int64)
             woff[edges] = _excl(wsz)[:-1]
             ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
+            e_eig, e_nsel, e_r, e_Q, e_status = eout
             lib.bddc_edge_gevp_old(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
-                                   d.nB, d.soff, ls.Bsym, Binv, scaling.D, self.theta_e, self.eig,
-                                   d_eig_off, self.n_sel, self.r, self.Q, self.d_q_off, status,
-                                   ws, dev_i64(woff[:-1]), dev_i32(edges), edges.size,
-                                   int(p.gsize[edges].max()), st)
-            self._raise(status, "edge")
+                                   BsC, BiC, scaling.D, self.theta_e, e_eig, d_eig_off, e_nsel,
+                                   e_r, e_Q, self.d_q_off, e_status, ws, dev_i64(woff[:-1]),
+                                   dev_i32(edges), edges.size, int(p.gsize[edges].max()), st)
             del ws
+        if multi and n_edges_all:
+            _allreduce(comm, *eout)
+            for t, e in zip(out, eout):
+                t += e
+        if n_edges_all:
+            self._raise(status, "edge")
         self.r_host = self.r.cpu().numpy().astype(np.int64)
         self.n_sel_host = self.n_sel.cpu().numpy().astype(np.int64)
 
-    def _run_faces(self, faces, fast, status, scaling, Binv, d_eig_off):
+    def _run_faces(self, faces, fast, out, scaling, BsC, BiC, d_eig_off):
         ls, p, d, st = self.ls, self.ls.plan, self.ls.d, stream()
+        eig, n_sel, r, Q, status = out
         G = p.G
         sizes = p.gsize[faces]
         budget = FACE_FAST_SMEM_BUDGET if fast else FACE_SMEM_BUDGET
@@ -425,11 +511,10 @@ class DevicePrimalSpace:
                 wsz = arena(p.gsize[grp])
                 woff[grp] = _excl(wsz)[:-1]
                 ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
-            lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, d.nB,
-                               d.soff, ls.Bsym, Binv, scaling.D, self.theta_f, self.eig, d_eig_off,
-                               self.n_sel, self.r, self.Q, self.d_q_off, status, ws,
-                               dev_i64(woff[:-1]), dev_i32(grp), grp.size, int(p.gsize[grp].max()),
-                               1 if fast else 0, st)
+            lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, BsC,
+                               BiC, scaling.D, self.theta_f, eig, d_eig_off, n_sel, r, Q,
+                               self.d_q_off, status, ws, dev_i64(woff[:-1]), dev_i32(grp),
+                               grp.size, int(p.gsize[grp].max()), 1 if fast else 0, st)
             del ws
 
     def _raise(self, status, what):
@@ -510,7 +595,7 @@ class DevicePreconditioner:
 
     def __init__(self, ls, scaling, r_host, Q, q_off, keep_coarse=8192):
         p, d, st = ls.plan, ls.d, stream()
-        self.ls, self.plan = ls, p
+        self.ls, self.plan, self.comm = ls, p, ls.comm
         r = np.asarray(r_host, dtype=np.int64)
         self.n_hat = p.n_hat
         self.n_primal = int(r.sum())
@@ -518,22 +603,33 @@ class DevicePreconditioner:
             raise NumericalError("empty primal space: no coarse problem to anchor the solver")
         go = _excl(r)
         self.glob_primal_offset = go[:-1]
-        cnt = r[p.sub_globs]
-        self.np_sub = np.add.reduceat(cnt, p.sub_glob_start[:-1].astype(np.int64)) if cnt.size else np.zeros(p.N, np.int64)
-        self.np_sub = np.where(np.diff(p.sub_glob_start) > 0, self.np_sub, 0)
+
+        def primal_counts(sub_globs, sub_glob_start):
+            cnt = r[sub_globs]
+            n = sub_glob_start.size - 1
+            nps = np.add.reduceat(cnt, sub_glob_start[:-1].astype(np.int64)) if cnt.size else np.zeros(n, np.int64)
+            return cnt, np.where(np.diff(sub_glob_start) > 0, nps, 0).astype(np.int64)
+
+        # global coarse numbering (all subdomains, every rank computes the same)
+        gcnt, np_glob = primal_counts(p.g_sub_globs, p.g_sub_glob_start)
+        gpgid0 = _ranges(go[:-1][p.g_sub_globs], gcnt)
+        # coarse dofs in reverse Cuthill-McKee order of the primal coupling graph
+        # (each subdomain's primal set is a clique) -> envelope LU / solves
+        self.corder, new_id, self.lim, self.first = coarse_ordering(gpgid0, np_glob, self.n_primal)
+        self.new_id = new_id
+        s0, s1 = p.owned
+        cnt, self.np_sub = primal_counts(p.sub_globs, p.sub_glob_start)
         pstart = _excl(self.np_sub)
         ppos = _ranges(p.sub_glob_boff, cnt)
         pgid0 = _ranges(go[:-1][p.sub_globs], cnt)
-        # coarse dofs in reverse Cuthill-McKee order of the primal coupling graph
-        # (each subdomain's primal set is a clique) -> envelope LU / solves
-        self.corder, new_id, self.lim, self.first = coarse_ordering(pgid0, self.np_sub, self.n_primal)
-        self.new_id = new_id
         pgid = new_id[pgid0]
         mask = np.zeros(int(p.voff[-1]), dtype=np.uint8)
         psub = np.repeat(np.arange(p.N), self.np_sub)
         mask[p.voff[psub] + ppos] = 1
         poff = _excl(self.np_sub * p.nB)
-        coff = _excl(self.np_sub * self.np_sub)
+        gcoff = _excl(np_glob * np_glob)  # coarse blocks C_i of all subdomains, global layout
+        c0, c1 = int(gcoff[s0]), int(gcoff[s1])
+        coff = gcoff[s0:s1 + 1] - c0
         self.d_pstart, self.d_ppos, self.d_pgid = dev_i32(pstart), dev_i32(ppos), dev_i32(pgid)
         self.d_poff, d_coff = dev_i64(poff[:-1]), dev_i64(coff[:-1])
         d_mask = torch.from_numpy(mask).cuda()
@@ -566,11 +662,11 @@ class DevicePreconditioner:
                                  PANEL, pinv, 4096, 0, status, 1, None, 0, st)
         bad = _first_bad(status)
         if bad is not None:
-            raise NumericalError(f"dual block of subdomain {bad} lost positive definiteness")
+            raise NumericalError(f"dual block of subdomain {bad + ls.s0} lost positive definiteness")
         lib.bddc_gj_inverse(Z, d.soff, d.nB, d.nB, p.N, nbmax, pinv, 4096, status, 0, st)
         bad = _first_bad(status)
         if bad is not None:
-            raise NumericalError(f"dual block of subdomain {bad} is singular")
+            raise NumericalError(f"dual block of subdomain {bad + ls.s0} is singular")
         lib.bddc_pc_zero_primal(d.nB, d.soff, d.voff, d_mask, Z, p.N, st)
         self.A = torch.empty(p.S_total, dtype=F64, device="cuda")
         TTT = torch.empty_like(TT)
@@ -582,9 +678,10 @@ class DevicePreconditioner:
         npn = max(int(poff[-1]), 1)
         MP = torch.empty(npn, dtype=F64, device="cuda")
         RP = torch.empty(npn, dtype=F64, device="cuda")
-        Cl = torch.empty(max(int(coff[-1]), 1), dtype=F64, device="cuda")
+        multi = _multi(self.comm)
+        Clg = (torch.zeros if multi else torch.empty)(max(int(gcoff[-1]), 1), dtype=F64, device="cuda")
         lib.bddc_pc_primal_pieces(d.nB, d.soff, self.d_pstart, self.d_ppos, self.d_poff, Sbar, Z,
-                                  MP, RP, Cl, d_coff, p.N, nbmax, st)
+                                  MP, RP, Clg[c0:], d_coff, p.N, nbmax, st)
         self.G = torch.empty(npn, dtype=F64, device="cuda")
         self.Nt = torch.empty(npn, dtype=F64, device="cuda")
         lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
@@ -596,8 +693,13 @@ class DevicePreconditioner:
         del Sbar, tmp, Z, MP, RP, TT, pinv
         nc = self.n_primal
         C = torch.zeros(nc * nc, dtype=F64, device="cuda")
-        lib.bddc_coarse_scatter(self.d_pstart, self.d_pgid, Cl, d_coff, C, nc, p.N, st)
-        del Cl
+        _allreduce(self.comm, Clg)
+        if multi:
+            lib.bddc_coarse_scatter(dev_i32(_excl(np_glob)), dev_i32(new_id[gpgid0]), Clg,
+                                    dev_i64(gcoff[:-1]), C, nc, p.N_glob, st)
+        else:
+            lib.bddc_coarse_scatter(self.d_pstart, self.d_pgid, Clg, d_coff, C, nc, p.N, st)
+        del Clg
         if nc <= keep_coarse:
             Cn = C.view(nc, nc).cpu().numpy()
             self.coarse = Cn[np.ix_(new_id, new_id)].copy()
@@ -663,11 +765,13 @@ class DevicePreconditioner:
         lib.bddc_local_gemv(d.nB, d.soff, d.voff, d.iface_perm, self.A, r, self.y, self.d_pstart,
                             self.d_poff, self.G, self.cvals, p.N, nbmax, 2, st)
         lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp, self.n_primal, st)
+        _allreduce(self.comm, self.rp)
         lib.bddc_coarse_solve(self.coarse_lu, self.n_primal, self.n_primal, self.coarse_pinv, 4096,
                               self.d_lim, self.d_first, self.rp, self.up, st)
         lib.bddc_prolong_primal(d.nB, d.voff, self.d_pstart, self.d_pgid, self.d_poff, self.Nt,
                                 self.up, self.y, p.N, st)
         lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n_hat, st)
+        _allreduce(self.comm, out)
         return out
 
     def apply(self, r):
@@ -692,6 +796,7 @@ class DeviceInterfaceOperator:
         lib.bddc_local_gemv(d.nB, d.soff, d.voff, d.iface_perm, self.ls.S, u, self.y, None, None,
                             None, None, p.N, int(p.nB.max()), 2, st)
         lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n, st)
+        _allreduce(self.ls.comm, out)
         return out
 
     def __call__(self, u):
@@ -703,6 +808,7 @@ class DeviceInterfaceOperator:
         p, d = self.ls.plan, self.ls.d
         out = torch.empty(self.n, dtype=F64, device="cuda")
         lib.bddc_gather_reduce(d.tstart, d.tsrc, self.ls.g, out, self.n, stream())
+        _allreduce(self.ls.comm, out)
         return out
 
 
@@ -798,8 +904,20 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
 def recover_device(ls, u_hat):
     """Nodal solution with interiors back-substituted (reference solver.py:318-326)."""
     p, d, st = ls.plan, ls.d, stream()
-    u = ls.inputs["gdir"].clone()
-    u[dev_i64(ls.globs.interface_nodes)] = u_hat
+    iface = dev_i64(ls.globs.interface_nodes)
+    if not _multi(ls.comm):
+        u = ls.inputs["gdir"].clone()
+        u[iface] = u_hat
+        lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, d.iface_perm, d.ioff,
+                                  d.I_nodes, u_hat, u, p.N, int(p.nL.max()), PANEL, st)
+        return u
+    # sharded: each rank writes its interiors into zeros, the sum is the union
+    ui = torch.zeros_like(ls.inputs["gdir"])
     lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, d.iface_perm, d.ioff,
-                              d.I_nodes, u_hat, u, p.N, int(p.nL.max()), PANEL, st)
+                              d.I_nodes, u_hat, ui, p.N, int(p.nL.max()), PANEL, st)
+    ls.comm.allreduce_(ui)
+    interior = ls.inputs["free"].clone()
+    interior[iface] = False
+    u = torch.where(interior, ui, ls.inputs["gdir"])
+    u[iface] = u_hat
     return u

@@ -22,18 +22,24 @@ class Result:
 
 def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8, max_iter=300,
         plan=None, inputs=None, timings=True, keep=False, kernel_timing=False,
-        dplan=None):
+        dplan=None, comm=None):
     """Run the whole hot path; returns a Result with counts, solutions
-    (device tensors) and phase times in ms (CUDA events)."""
+    (device tensors) and phase times in ms (CUDA events).
+
+    comm (dist.py): shard the subdomains over its ranks (each rank passes
+    its own comm; results are replicated on every rank)."""
     tm = PhaseTimer(timings)
+    owned = None
+    if comm is not None and comm.size > 1:
+        owned = plan.owned if plan is not None else comm.owned(partition.n_subdomains)
     if inputs is None:
-        inputs = upload_inputs(system, partition)
+        inputs = upload_inputs(system, partition, owned=owned if plan is None or plan.on_device else None)
     if plan is None:
         tm.mark("symbolic_plan")
-        plan = Plan(system, partition, globs, device_inputs=inputs)
+        plan = Plan(system, partition, globs, device_inputs=inputs, owned=owned)
     tm.mark("subdomain_ops")
     ls = LocalSystem(system, partition, globs, plan=plan, inputs=inputs,
-                     kernel_timing=kernel_timing, dplan=dplan)
+                     kernel_timing=kernel_timing, dplan=dplan, comm=comm)
     tm.mark("bsym_inverse")
     ls.bsym_inverse()
     tm.mark("scaling")

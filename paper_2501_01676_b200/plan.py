@@ -14,6 +14,18 @@ Two builders produce identical plans:
   part (the only part that scales with the mesh: 4 x n_elements entries) runs
   as torch sort / unique / searchsorted on the GPU and stays resident there.
   The glob part (O(sum nB)) is always host numpy.
+
+Sharding (one rank per GPU): ``owned=(s0, s1)`` restricts every
+per-subdomain array (element lists, interior / interface dofs, the
+subdomain -> glob incidence) to subdomains s0..s1-1, numbered locally from 0;
+the per-glob tables (kinds, sizes, sharers, slot offsets ``sh_doff``) stay
+global, ``slot_local`` maps each (glob, sharer) slot to its local subdomain
+(-1 when another rank owns it), ``glob_mine`` marks the globs whose first
+sharer is local (this rank computes their deluxe blocks and eigenproblems),
+and the ``g_*`` arrays keep the global subdomain -> glob incidence that the
+coarse numbering needs.  Interior dofs follow the reference's definition
+(free and not an interface node, substructuring.py:88-91), which needs no
+cross-rank node counts.
 """
 
 import numpy as np
@@ -39,13 +51,19 @@ def _excl(a):
 
 
 class Plan:
-    def __init__(self, system, partition, globs, device_inputs=None):
-        N = int(partition.n_subdomains)
-        self.N = N
+    def __init__(self, system, partition, globs, device_inputs=None, owned=None):
+        N_glob = int(partition.n_subdomains)
+        s0, s1 = (0, N_glob) if owned is None else (int(owned[0]), int(owned[1]))
+        if not 0 <= s0 <= s1 <= N_glob:
+            raise ValueError(f"owned range {owned} outside 0..{N_glob}")
+        self.N_glob = N_glob
+        self.owned = (s0, s1)
+        self.N = N_glob  # the glob part works on global subdomain ids first
         self.n_nodes = system.mesh.n_nodes
         self.n_hat = int(np.asarray(globs.interface_nodes).size)
         self.on_device = device_inputs is not None
         self._glob_part(globs)
+        self._restrict(s0, s1)
         if self.on_device:
             self._interface_maps_torch(device_inputs["conn"].device)
             self._element_part_torch(system, partition, device_inputs)
@@ -97,6 +115,30 @@ class Plan:
         self.pos2k = np.repeat(np.arange(self.sub_globs.size, dtype=np.int32), sizes_k)
         self._iface_nodes = np.asarray(globs.interface_nodes, dtype=np.int64)
 
+    def _restrict(self, s0, s1):
+        """Keep subdomains s0..s1-1 (local ids 0..s1-s0-1)."""
+        self.g_sub_globs = self.sub_globs
+        self.g_sub_glob_start = self.sub_glob_start
+        self.g_sub_glob_boff = self.sub_glob_boff
+        self.g_nB = self.nB
+        sh = self.sh_sub.astype(np.int64)
+        self.slot_local = np.where((sh >= s0) & (sh < s1), sh - s0, -1).astype(np.int32)
+        first = self.sh_sub[self.sh_start[:-1]] if self.G else np.zeros(0, np.int32)
+        self.glob_mine = (first >= s0) & (first < s1)
+        self.N = s1 - s0
+        if (s0, s1) == (0, self.N_glob):
+            return
+        a, b = int(self.sub_glob_start[s0]), int(self.sub_glob_start[s1])
+        self.sub_globs = self.sub_globs[a:b]
+        self.sub_glob_sh = self.sub_glob_sh[a:b]
+        self.sub_glob_boff = self.sub_glob_boff[a:b]
+        self.sub_glob_start = (self.sub_glob_start[s0:s1 + 1] - a).astype(np.int32)
+        self.nB = self.g_nB[s0:s1]
+        v0, v1 = int(self.voff[s0]), int(self.voff[s1])
+        self.voff = self.voff[s0:s1 + 1] - v0
+        self.B_nodes = self.B_nodes[v0:v1]
+        self.pos2k = (self.pos2k[v0:v1] - a).astype(np.int32)
+
     def _interface_maps_numpy(self):
         self.iface_perm = np.searchsorted(self._iface_nodes, self.B_nodes).astype(np.int32)
         src = np.argsort(self.iface_perm, kind="stable")
@@ -122,20 +164,24 @@ class Plan:
     # -- elements: interior dofs, element lists, element-local indices ------
     def _element_part_numpy(self, system, partition):
         N, n_nodes = self.N, self.n_nodes
-        sub_of = np.asarray(partition.subdomain_of, dtype=np.int64)
-        el = np.asarray(system.mesh.elements, dtype=np.int64)
-        key = np.unique((el * N + sub_of[:, None]).ravel())
-        node, sub = key // N, key % N
-        cnt = np.bincount(node, minlength=n_nodes)
+        s0, s1 = self.owned
+        sub_all = np.asarray(partition.subdomain_of, dtype=np.int64)
+        mine = np.flatnonzero((sub_all >= s0) & (sub_all < s1))
+        sub_of = sub_all[mine] - s0
+        el = np.asarray(system.mesh.elements, dtype=np.int64)[mine]
+        key = np.unique((el * max(N, 1) + sub_of[:, None]).ravel())
+        node, sub = key // max(N, 1), key % max(N, 1)
         free = np.asarray(system.node_to_free) >= 0
-        interior = (cnt[node] == 1) & free[node]
+        on_iface = np.zeros(n_nodes, dtype=bool)
+        on_iface[self._iface_nodes] = True
+        interior = free[node] & ~on_iface[node]
         I_sub, I_node = sub[interior], node[interior]
         o = np.lexsort((I_node, I_sub))
         self.I_nodes = I_node[o]
         self.nI = np.bincount(I_sub, minlength=N).astype(np.int64)
         self.ioff = _excl(self.nI)
         eorder = np.argsort(sub_of, kind="stable")
-        self.elem_ids = eorder.astype(np.int64)
+        self.elem_ids = mine[eorder].astype(np.int64)
         self.elem_start = _excl(np.bincount(sub_of, minlength=N))
         self.loc4 = self._local_index_numpy(el[eorder], sub_of[eorder])
 
@@ -158,15 +204,17 @@ class Plan:
         import torch
 
         N, n_nodes = self.N, self.n_nodes
-        conn = dev["conn"]                     # (E, 4) int64 on the GPU
-        sub_of = dev["sub_of"]                 # (E,) int64 on the GPU
+        conn = dev["conn"]                     # (E_local, 4) int64 on the GPU
+        sub_of = dev["sub_of"] - self.owned[0]  # (E_local,) local subdomain ids
         free = dev.get("free")
         if free is None:
             free = torch.from_numpy(np.asarray(system.node_to_free) >= 0).to(conn.device)
-        key = torch.unique(conn * N + sub_of[:, None])
-        node, sub = key // N, key % N
-        cnt = torch.bincount(node, minlength=n_nodes)
-        interior = (cnt[node] == 1) & free[node]
+        Nk = max(N, 1)
+        key = torch.unique(conn * Nk + sub_of[:, None])
+        node, sub = key // Nk, key % Nk
+        on_iface = torch.zeros(n_nodes, dtype=torch.bool, device=conn.device)
+        on_iface[torch.from_numpy(self._iface_nodes).to(conn.device)] = True
+        interior = free[node] & ~on_iface[node]
         I_node, I_sub = node[interior], sub[interior]
         k2 = torch.sort(I_sub * n_nodes + I_node).values
         I_sub, I_node = k2 // n_nodes, k2 % n_nodes
@@ -216,12 +264,13 @@ class Plan:
         bad_e = np.flatnonzero(np.diff(self.elem_start) == 0)
         bad_b = np.flatnonzero(self.nB == 0)
         bad_i = np.flatnonzero(self.nI == 0)
+        s0 = self.owned[0]
         for i in sorted(set(bad_e.tolist()) | set(bad_b.tolist()) | set(bad_i.tolist())):
             if i in bad_e:
-                raise ValueError(f"subdomain {i} has no elements")
+                raise ValueError(f"subdomain {i + s0} has no elements")
             if i in bad_b:
-                raise ValueError(f"subdomain {i} has no interface unknowns")
-            raise ValueError(f"subdomain {i} has no interior unknowns")
+                raise ValueError(f"subdomain {i + s0} has no interface unknowns")
+            raise ValueError(f"subdomain {i + s0} has no interior unknowns")
 
     def nodal_order(self, sub):
         """Permutation p with B_glob_major[p] = sorted interface nodes of sub."""
