@@ -123,7 +123,7 @@ int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int
  *          build_change_of_basis adaptive.py:190-206. */
 int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                    const int* sh_boff, const long long* sh_doff, const double* BsC,
-                   const double* BiC, const double* D, double theta, double* eig,
+                   const double* BiC, const double* SC, const int* sc_status, const double* D, double theta, double* eig,
                    const long long* eig_off, int* n_sel, int* r, double* Q, const long long* q_off,
                    int* status, double* ws, const long long* ws_off, const int* face_ids,
                    int n_faces, int max_n, int fast, cudaStream_t stream);
@@ -141,7 +141,8 @@ int bddc_priors(const int* kind, const int* size, const int* nB, const long long
  *          adaptive.py:94-156, reduce_edge_constraints adaptive.py:172-187. */
 int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                        const int* sh_boff, const long long* sh_doff, const double* BsC,
-                       const double* BiC, const double* D, const double* EX,
+                       const double* BiC, const double* SC, const int* sc_status,
+                       const double* D, const double* EX,
                        const long long* ex_off, const int* ex_h, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
@@ -151,7 +152,8 @@ int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, co
  *          parallel_sum_chain linalg.py:70-78. */
 int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                        const int* sh_boff, const long long* sh_doff, const double* BsC,
-                       const double* BiC, const double* D, double theta, double* eig,
+                       const double* BiC, const double* SC, const int* sc_status,
+                       const double* D, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
                        const int* edge_ids, int n_edges, int max_n, cudaStream_t stream);
@@ -168,6 +170,15 @@ int bddc_extract_slot_blocks(const int* slot_sub, const int* slot_glob, const in
                              const int* sh_boff, const long long* sh_doff, const int* nB,
                              const long long* soff, const double* Bsym, const double* Binv,
                              double* BsC, double* BiC, int n_slots, cudaStream_t stream);
+
+/* Glob Schur blocks sym(((Bsym^-1)[g,g])^-1) of the listed slots with
+ * n_g <= 64 (register Gauss-Jordan, one CTA per slot) into SC (sh_doff
+ * layout); sc_status[slot] = 1 when the block is not positive definite.  The
+ * face / edge kernels take SC (or NULL: computed in-kernel).
+ * replaces glob_schur_block substructuring.py:152-171. */
+int bddc_slot_schur(const int* slots, int n_slots, const int* slot_glob, const int* size,
+                    const long long* sh_doff, const double* BiC, double* SC, int* sc_status,
+                    cudaStream_t stream);
 
 /* Per local (edge, sharer) slot: X = [[Binv_EE, PB_E^T], [PB_E, XHH]] at
  * EX + ex_off[k] ((ne+nH) x (ne+nH)), the input of the prior-aware edge Schur

@@ -65,9 +65,61 @@ BDDC_DEV void gemm_t(double* C, int ldc, const double* A, int lda, const double*
   __syncthreads();
 }
 
+// Same contract on the DMMA pipe (mma.sync m8n8k4 f64): each warp computes
+// 16 x 8 output tiles (two 8x8 accumulators sharing the B fragment), operands
+// read straight from shared or global memory with zero-fill at the edges.
+template <bool TA, bool TB>
+BDDC_DEV void gemm_mma_t(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
+                         int m, int n, int k, double alpha, double beta) {
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  const int nw = (int)(blockDim.x >> 5);
+  const int g = lane >> 2, t = lane & 3;
+  const int mt = (m + 15) >> 4, nt = (n + 7) >> 3;
+  for (int tile = warp; tile < mt * nt; tile += nw) {
+    const int r0 = (tile / nt) * 16, c0 = (tile - (tile / nt) * nt) * 8;
+    const int ra = r0 + g, rb = r0 + 8 + g, cb = c0 + g;
+    double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+    for (int p = 0; p < k; p += 4) {
+      const int kk = p + t;
+      double a0 = 0.0, a1 = 0.0, b = 0.0;
+      if (kk < k) {
+        if (ra < m) a0 = TA ? A[kk * lda + ra] : A[ra * lda + kk];
+        if (rb < m) a1 = TA ? A[kk * lda + rb] : A[rb * lda + kk];
+        if (cb < n) b = TB ? B[cb * ldb + kk] : B[kk * ldb + cb];
+      }
+      dmma_8x8x4(x0, x1, a0, b);
+      dmma_8x8x4(y0, y1, a1, b);
+    }
+    const int cc = c0 + 2 * t;
+    const double xs[2] = {x0, x1}, ys[2] = {y0, y1};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (cc + h >= n) continue;
+      if (ra < m) {
+        double v = alpha * xs[h];
+        if (beta != 0.0) v += beta * C[ra * ldc + cc + h];
+        C[ra * ldc + cc + h] = v;
+      }
+      if (rb < m) {
+        double v = alpha * ys[h];
+        if (beta != 0.0) v += beta * C[rb * ldc + cc + h];
+        C[rb * ldc + cc + h] = v;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // C = beta*C + alpha*op(A)*op(B);  op(A) m x k, op(B) k x n.  C must not alias A/B.
 BDDC_DEV void gemm(double* C, int ldc, const double* A, int lda, bool ta, const double* B, int ldb,
                    bool tb, int m, int n, int k, double alpha, double beta) {
+  if (m >= 8 && n >= 8 && k >= 8) {
+    if (!ta && !tb) gemm_mma_t<false, false>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
+    else if (ta && !tb) gemm_mma_t<true, false>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
+    else if (!ta && tb) gemm_mma_t<false, true>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
+    else gemm_mma_t<true, true>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
+    return;
+  }
   if (!ta && !tb) gemm_t<false, false>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
   else if (ta && !tb) gemm_t<true, false>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
   else if (!ta && tb) gemm_t<false, true>(C, ldc, A, lda, B, ldb, m, n, k, alpha, beta);
@@ -597,15 +649,37 @@ BDDC_DEV void tridiag_eigvals(const double* d, const double* e, int n, double* w
   lo -= 2.2e-16 * nrm * n + 1e-300;
   hi += 2.2e-16 * nrm * n + 1e-300;
   const double atol = 1e-17 * nrm + 1e-300;
-  for (int j = tid(); j < n; j += nth()) {
+  // multisection: a group of G lanes per eigenvalue evaluates G Sturm counts
+  // per step (G+1 subintervals, log2(G+1) bits per step instead of 1)
+  int G = 1;
+  while (G < 8 && n * (2 * G) <= nth()) G *= 2;
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), gbase = lane & ~(G - 1);
+  const int ngroups = nth() / G;
+  for (int j = tid() / G;; j += ngroups) {
+    const bool active = j < n;
+    if (!__any_sync(full, active)) break;
     double a = lo, b = hi;
+    bool done = !active;
     for (int it = 0; it < 200; ++it) {
-      const double mid = 0.5 * (a + b);
-      if (mid <= a || mid >= b) break;
-      if (b - a <= 2.2e-16 * fmax(fabs(a), fabs(b)) + atol) break;
-      if (sturm_count(d, e, n, mid, pivmin) <= j) a = mid; else b = mid;
+      if (!done && b - a <= 2.2e-16 * fmax(fabs(a), fabs(b)) + atol) done = true;
+      if (__all_sync(full, done)) break;
+      const double h = (b - a) / (double)(G + 1);
+      const int cnt = done ? 0 : sturm_count(d, e, n, a + h * (double)(gl + 1), pivmin);
+      int q = G;  // first subinterval end with more than j eigenvalues below
+      for (int l = 0; l < G; ++l) {
+        const int cl = __shfl_sync(full, cnt, gbase + l);
+        if (q == G && cl > j) q = l;
+      }
+      if (!done) {
+        const double na = (q == 0) ? a : a + h * (double)q;
+        const double nb = (q == G) ? b : a + h * (double)(q + 1);
+        if (!(na > a) && !(nb < b)) done = true;
+        a = na;
+        b = nb;
+      }
     }
-    w[j] = 0.5 * (a + b);
+    if (active && gl == 0) w[j] = 0.5 * (a + b);
   }
   __syncthreads();
 }

@@ -9,6 +9,7 @@
 #include "common.cuh"
 #include "bddc_b200.h"
 #include "dense_block.cuh"
+#include "reg_gj.cuh"
 #include "glob_layout.h"
 
 namespace bddc {
@@ -30,6 +31,9 @@ struct GlobTables {
   // sh_doff[slot] (n_g x n_g, ld n_g), gathered from the owning ranks
   const double* BsC;
   const double* BiC;
+  // per slot: sym((Bsym^-1)[g,g]^-1) for n_g <= 64 (slot_schur_kernel), or null
+  const double* SC;
+  const int* sc_status;
 };
 
 // ---------------------------------------------------------------------------
@@ -450,6 +454,10 @@ __global__ void __launch_bounds__(256) deluxe_kernel(GlobTables t, double* __res
 
 // B~_X = sym(((Binv)[X,X])^-1) of sharer k into out (n x n); returns Status.
 BDDC_DEV int glob_schur(const GlobTables& t, int k, int n, double* out, double* rowbuf) {
+  if (t.SC != nullptr && n <= kTile) {  // precomputed by slot_schur_kernel
+    blk::copy(out, n, t.SC + t.sh_doff[k], n, n, n);
+    return t.sc_status[k];
+  }
   blk::copy(out, n, t.BiC + t.sh_doff[k], n, n, n);
   const int st = blk::gj_inverse(out, n, n, true, rowbuf);
   if (st) return st;
@@ -722,6 +730,29 @@ __global__ void extract_slot_blocks_kernel(const int* __restrict__ slot_sub,
     BsC[sh_doff[k] + idx] = Bsym[src];
     if (BiC) BiC[sh_doff[k] + idx] = Binv[src];
   }
+}
+
+// Glob Schur blocks of the listed slots (n_g <= 64): SC = sym(((Bsym^-1)[g,g])^-1),
+// one register Gauss-Jordan per CTA; sc_status[k] = kNotPositiveDefinite on failure.
+__global__ void __launch_bounds__(256, 2) slot_schur_kernel(
+    const int* __restrict__ slots, const int* __restrict__ slot_glob,
+    const int* __restrict__ gsize, const long long* __restrict__ sh_doff,
+    const double* __restrict__ BiC, double* __restrict__ SC, int* __restrict__ sc_status) {
+  __shared__ RegGjSmem sm;
+  const int k = slots[blockIdx.x];
+  const int n = gsize[slot_glob[k]];
+  if (n > kTile) return;
+  double* out = SC + sh_doff[k];
+  const bool bad = reg_gj64(BiC + sh_doff[k], n, n, out, n, 1, nullptr, sm);
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    if (c > r) {
+      const double v = 0.5 * (out[r * n + c] + out[c * n + r]);
+      out[r * n + c] = v;
+      out[c * n + r] = v;
+    }
+  }
+  if (threadIdx.x == 0) sc_status[k] = bad ? (int)kNotPositiveDefinite : 0;
 }
 
 // X block of every local (edge, sharer) slot: [[Binv[E,E], PB[:,E]^T], [PB[:,E], XHH]]
@@ -1137,10 +1168,11 @@ static int glob_launch_status() {
 
 static GlobTables make_tables(const int* kind, const int* size, const int* sh_start,
                               const int* sh_sub, const int* sh_boff, const long long* sh_doff,
-                              const double* BsC, const double* BiC) {
+                              const double* BsC, const double* BiC, const double* SC = nullptr,
+                              const int* sc_status = nullptr) {
   GlobTables t{};
   t.kind = kind; t.size = size; t.sh_start = sh_start; t.sh_sub = sh_sub; t.sh_boff = sh_boff;
-  t.sh_doff = sh_doff; t.BsC = BsC; t.BiC = BiC;
+  t.sh_doff = sh_doff; t.BsC = BsC; t.BiC = BiC; t.SC = SC; t.sc_status = sc_status;
   return t;
 }
 
@@ -1199,14 +1231,23 @@ int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int
   return glob_launch_status();
 }
 
+int bddc_slot_schur(const int* slots, int n_slots, const int* slot_glob, const int* size,
+                    const long long* sh_doff, const double* BiC, double* SC, int* sc_status,
+                    cudaStream_t stream) {
+  if (n_slots <= 0) return 0;
+  slot_schur_kernel<<<n_slots, 256, 0, stream>>>(slots, slot_glob, size, sh_doff, BiC, SC, sc_status);
+  bddc_note_launches(1);
+  return glob_launch_status();
+}
+
 int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                    const int* sh_boff, const long long* sh_doff, const double* BsC,
-                   const double* BiC, const double* D, double theta, double* eig,
+                   const double* BiC, const double* SC, const int* sc_status, const double* D, double theta, double* eig,
                    const long long* eig_off, int* n_sel, int* r, double* Q, const long long* q_off,
                    int* status, double* ws, const long long* ws_off, const int* face_ids,
                    int n_faces, int max_n, int fast, cudaStream_t stream) {
   if (n_faces <= 0) return 0;
-  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC);
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC, SC, sc_status);
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int small = face_small_bytes(max_n);
   if (fast) {
@@ -1241,13 +1282,14 @@ int bddc_priors(const int* kind, const int* size, const int* nB, const long long
 
 int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                        const int* sh_boff, const long long* sh_doff, const double* BsC,
-                       const double* BiC, const double* D, const double* EX,
+                       const double* BiC, const double* SC, const int* sc_status,
+                       const double* D, const double* EX,
                        const long long* ex_off, const int* ex_h, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
                        const int* edge_ids, int n_edges, int max_dim, cudaStream_t stream) {
   if (n_edges <= 0) return 0;
-  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC);
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC, SC, sc_status);
   PriorTables pr{EX, ex_off, ex_h};
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int smem = shmem_for(max_dim);
@@ -1258,12 +1300,13 @@ int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, co
 
 int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                        const int* sh_boff, const long long* sh_doff, const double* BsC,
-                       const double* BiC, const double* D, double theta, double* eig,
+                       const double* BiC, const double* SC, const int* sc_status,
+                       const double* D, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
                        const int* edge_ids, int n_edges, int max_n, cudaStream_t stream) {
   if (n_edges <= 0) return 0;
-  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC);
+  GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC, SC, sc_status);
   GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
   const int smem = shmem_for(max_n);
   if (smem > 48 * 1024) cudaFuncSetAttribute(edge_old_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

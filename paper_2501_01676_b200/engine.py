@@ -263,15 +263,55 @@ class DevicePlan:
         self.slot_local = dev_i32(p.slot_local)
 
 
+def stage_inputs(system, partition=None, owned=None):
+    """Page-locked host copies of the per-step inputs (element blocks,
+    connectivity, Dirichlet data, element -> subdomain map): the host buffers
+    a caller keeps its problem data in so that every solve's upload is a
+    straight DMA.  owned=(s0, s1): only the elements of subdomains s0..s1-1."""
+    Ke = system.elem_matrices.reshape(-1, 16)
+    Fe = system.elem_rhs.reshape(-1, 4)
+    conn = system.mesh.elements
+    sub_of = None if partition is None else np.asarray(partition.subdomain_of)
+    if owned is not None and sub_of is not None and tuple(owned) != (0, partition.n_subdomains):
+        sel = np.flatnonzero((sub_of >= owned[0]) & (sub_of < owned[1]))
+        Ke, Fe, conn, sub_of = Ke[sel], Fe[sel], conn[sel], sub_of[sel]
+
+    def pin(a, dt):
+        src = torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
+        t = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+        t.copy_(src)
+        return t
+    out = {
+        # small index arrays first: the symbolic plan only needs these
+        "conn": pin(conn, np.int64),
+        "free": pin(np.asarray(system.node_to_free) >= 0, np.bool_),
+        "gdir": pin(system.dirichlet_values, np.float64),
+        "Ke": pin(Ke, np.float64),
+        "Fe": pin(Fe, np.float64),
+    }
+    if sub_of is not None:
+        out["sub_of"] = pin(sub_of, np.int64)
+    return out
+
+
+def upload_staged(staged):
+    """Asynchronous H2D of stage_inputs() buffers on the current stream."""
+    return {k: v.cuda(non_blocking=True) for k, v in staged.items()}
+
+
+def staged_bytes(staged):
+    return int(sum(v.numel() * v.element_size() for v in staged.values()))
+
+
 def upload_inputs(system, partition=None, pinned=False, owned=None):
     """Element blocks, connectivity, Dirichlet data (and the element ->
     subdomain map, for the device-side symbolic plan) to the device.
     owned=(s0, s1): only the elements of subdomains s0..s1-1 (a rank's shard)."""
+    if pinned:
+        return upload_staged(stage_inputs(system, partition, owned))
+
     def up(a, dt):
-        t = torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
-        if pinned:
-            t = t.pin_memory()
-        return t.cuda(non_blocking=pinned)
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
     Ke = system.elem_matrices.reshape(-1, 16)
     Fe = system.elem_rhs.reshape(-1, 4)
     conn = system.mesh.elements
@@ -411,6 +451,14 @@ class DevicePrimalSpace:
         # each glob is computed by the rank owning its first sharer
         faces = np.flatnonzero((kind == 0) & p.glob_mine)
         edges = np.flatnonzero((kind == 1) & p.glob_mine)
+        # glob Schur blocks sym(((Bsym^-1)[g,g])^-1) of every slot of those globs
+        # (n_g <= 64), batched: one register Gauss-Jordan per CTA
+        sel = (kind[p.slot_glob] != 2) & p.glob_mine[p.slot_glob] & (p.gsize[p.slot_glob] <= 64)
+        sc_slots = np.flatnonzero(sel)
+        self.SC = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
+        self.sc_status = torch.zeros(max(int(p.sh_sub.size), 1), dtype=torch.int32, device="cuda")
+        lib.bddc_slot_schur(dev_i32(sc_slots), sc_slots.size, d.slot_glob, d.gsize, d.sh_doff, BiC,
+                            self.SC, self.sc_status, st)
         if faces.size:
             self._run_faces(faces, True, out, scaling, BsC, BiC, d_eig_off)
             s = status.cpu().numpy()
@@ -467,7 +515,7 @@ class DevicePrimalSpace:
                 ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
                 e_eig, e_nsel, e_r, e_Q, e_status = eout
                 lib.bddc_edge_gevp_new(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
-                                       BsC, BiC, scaling.D, EX, d_ex_off, dev_i32(sh_nH),
+                                       BsC, BiC, self.SC, self.sc_status, scaling.D, EX, d_ex_off, dev_i32(sh_nH),
                                        self.theta_e, e_eig, d_eig_off, e_nsel, e_r, e_Q,
                                        self.d_q_off, e_status, ws, dev_i64(woff[:-1]),
                                        dev_i32(edges), edges.size, int(wd.max()), st)
@@ -480,7 +528,7 @@ class DevicePrimalSpace:
             ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
             e_eig, e_nsel, e_r, e_Q, e_status = eout
             lib.bddc_edge_gevp_old(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
-                                   BsC, BiC, scaling.D, self.theta_e, e_eig, d_eig_off, e_nsel,
+                                   BsC, BiC, self.SC, self.sc_status, scaling.D, self.theta_e, e_eig, d_eig_off, e_nsel,
                                    e_r, e_Q, self.d_q_off, e_status, ws, dev_i64(woff[:-1]),
                                    dev_i32(edges), edges.size, int(p.gsize[edges].max()), st)
             del ws
@@ -492,6 +540,7 @@ class DevicePrimalSpace:
             self._raise(status, "edge")
         self.r_host = self.r.cpu().numpy().astype(np.int64)
         self.n_sel_host = self.n_sel.cpu().numpy().astype(np.int64)
+        del self.SC
 
     def _run_faces(self, faces, fast, out, scaling, BsC, BiC, d_eig_off):
         ls, p, d, st = self.ls, self.ls.plan, self.ls.d, stream()
@@ -512,7 +561,7 @@ class DevicePrimalSpace:
                 woff[grp] = _excl(wsz)[:-1]
                 ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
             lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, BsC,
-                               BiC, scaling.D, self.theta_f, eig, d_eig_off, n_sel, r, Q,
+                               BiC, self.SC, self.sc_status, scaling.D, self.theta_f, eig, d_eig_off, n_sel, r, Q,
                                self.d_q_off, status, ws, dev_i64(woff[:-1]), dev_i32(grp),
                                grp.size, int(p.gsize[grp].max()), 1 if fast else 0, st)
             del ws
