@@ -81,12 +81,14 @@ int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const in
                        const int* host_lim, double* pinv, double* piv_out, int* status,
                        cudaStream_t stream);
 
-/* Blocked in-place Gauss-Jordan inverse (no pivoting).
+/* Blocked in-place Gauss-Jordan inverse (no pivoting).  symmetric = 1 (exactly
+ * symmetric input): only the lower half of each trailing update is computed and
+ * mirrored, the result is exactly symmetric.
  * replaces cho_factor/cho_solve(Bsym, I) substructuring.py:64-75 (require_positive = 1)
  *          lu_factor(Sdd) + lu_solve solver.py:99, 105, 187, 195 (require_positive = 0). */
 int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n, int nbatch,
                     int max_n, double* pinv_ws, long long pinv_stride, int* status,
-                    int require_positive, cudaStream_t stream);
+                    int require_positive, int symmetric, cudaStream_t stream);
 
 /* S, g, Bsym = (S + S^T)/2 from the eliminated local matrices.
  * replaces SubdomainOperator.__init__ substructuring.py:35-40. */

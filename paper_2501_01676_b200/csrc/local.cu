@@ -191,9 +191,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_row_kernel(
            0.0, sm);
 }
 
+// symmetric != 0 (symmetric input): in-place GJ keeps G_JJ and G_KK symmetric
+// and G_JK = -G_KJ^T (K = processed pivots), so only tiles tm >= tn are
+// computed and each off-diagonal result is mirrored with that sign.
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ n, int k) {
+    const int* __restrict__ n, int k, int symmetric) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
@@ -205,15 +208,20 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel
   if (tm >= T) return;
   const int r0 = tm * kTile, c0 = tn * kTile;
   if (r0 == k || c0 == k) return;
+  if (symmetric && tn > tm) return;
   const int L = ld[b];
   double* M = base + off[b];
+  double* Ct = (symmetric && tn < tm) ? M + (long long)c0 * L + r0 : nullptr;
+  const double sgn = ((r0 < k) != (c0 < k)) ? -1.0 : 1.0;
   tile_mma(M + (long long)r0 * L + c0, L, min(kTile, nb - r0), min(kTile, nb - c0),
-           M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm);
+           M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm, Ct, L,
+           sgn);
 }
 
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ n, int k, const double* __restrict__ pinv, long long pinv_stride) {
+    const int* __restrict__ n, int k, const double* __restrict__ pinv, long long pinv_stride,
+    int symmetric) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
@@ -225,10 +233,20 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
   const int L = ld[b];
   double* M = base + off[b];
   const double* P = pinv + (long long)b * pinv_stride;
-  if (r0 == k) {  // pivot block <- P
+  if (r0 == k) {  // pivot block <- P (symmetric part when symmetric)
     for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
       int r = idx / w, c = idx - r * w;
-      M[(long long)(k + r) * L + k + c] = P[r * kTile + c];
+      M[(long long)(k + r) * L + k + c] =
+          symmetric ? 0.5 * (P[r * kTile + c] + P[c * kTile + r]) : P[r * kTile + c];
+    }
+    return;
+  }
+  if (symmetric) {  // column panel = +-(row panel)^T: + for processed rows (G_KK), - for G_JK
+    const int h = min(kTile, nb - r0);
+    const double sgn = r0 < k ? 1.0 : -1.0;
+    for (int idx = threadIdx.x; idx < h * w; idx += blockDim.x) {
+      const int r = idx / w, c = idx - r * w;
+      M[(long long)(r0 + r) * L + k + c] = sgn * M[(long long)(k + c) * L + r0 + r];
     }
     return;
   }
@@ -478,7 +496,7 @@ int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const in
 
 int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n, int nbatch,
                     int max_n, double* pinv_ws, long long pinv_stride, int* status,
-                    int require_positive, cudaStream_t stream) {
+                    int require_positive, int symmetric, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   const int smem = smem_tile_setup();
   const int T = ceil_div(max_n, kTile);
@@ -487,9 +505,10 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
                                                      status, require_positive, nullptr, 0);
     gj_row_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride);
-    gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k);
+    gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k,
+                                                                         symmetric);
     gj_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
-                                                                  pinv_stride);
+                                                                  pinv_stride, symmetric);
     bddc_note_launches(4);
   }
   return launch_status();

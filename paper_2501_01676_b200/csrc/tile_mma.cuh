@@ -107,7 +107,8 @@ BDDC_DEV void tile_issue_chunk(TileSmemT<BM>& sm, int st, int kc, const double* 
 template <int BM>
 BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A, long long lda,
                          const double* B, long long ldb, int K, double alpha, double beta,
-                         TileSmemT<BM>& sm) {
+                         TileSmemT<BM>& sm, double* Ct = nullptr, long long ldct = 0,
+                         double tsign = 1.0) {
   constexpr int WNW = 64 / kWN;  // warps along n
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -164,6 +165,27 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
   }
   cp_async_wait<0>();
   __syncthreads();  // every read of B (which may alias C) is done
+  if (Ct != nullptr) {
+    // mirrored copy: Ct[c][r] = tsign * C[r][c], staged through shared memory
+    // (the pipeline buffers are free now) so both stores are coalesced
+    static_assert(sizeof(TileSmemT<BM>) >= sizeof(double) * 64 * 65, "staging tile");
+    double* st = reinterpret_cast<double*>(&sm);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < kNJ; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t + h;
+          st[c * 65 + r] = tsign * alpha * acc[i][j][h];
+        }
+    __syncthreads();
+    constexpr int NT = (BM / 32) * (64 / kWN) * 32;
+    for (int idx = threadIdx.x; idx < 64 * BM; idx += NT) {
+      const int c = idx / BM, r = idx - c * BM;
+      if (c < n && r < m) Ct[(long long)c * ldct + r] = st[c * 65 + r];
+    }
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = wm + i * 8 + g;
@@ -185,8 +207,9 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
 
 BDDC_DEV void tile_mma(double* C, long long ldc, int m, int n, const double* A, long long lda,
                        const double* B, long long ldb, int K, double alpha, double beta,
-                       TileSmem& sm) {
-  tile_mma_t<64>(C, ldc, m, n, A, lda, B, ldb, K, alpha, beta, sm);
+                       TileSmem& sm, double* Ct = nullptr, long long ldct = 0,
+                       double tsign = 1.0) {
+  tile_mma_t<64>(C, ldc, m, n, A, lda, B, ldb, K, alpha, beta, sm, Ct, ldct, tsign);
 }
 
 }  // namespace bddc

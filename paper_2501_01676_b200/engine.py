@@ -153,9 +153,9 @@ class LocalSystem:
             Binv = self.Bsym.clone()
             status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
             pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
+            # Bsym is exactly symmetric (extract_schur): symmetric GJ, exact symmetric result
             lib.bddc_gj_inverse(Binv, d.soff, d.nB, d.nB, p.N, int(p.nB.max()), pinv, 4096, status,
-                                1, st)
-            lib.bddc_symmetrize(Binv, d.soff, d.nB, p.N, st)
+                                1, 1, st)
             bad = _first_bad(status)
             if bad is not None:
                 B = self.matrix(self.Bsym, bad)
@@ -712,7 +712,7 @@ class DevicePreconditioner:
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError(f"dual block of subdomain {bad + ls.s0} lost positive definiteness")
-        lib.bddc_gj_inverse(Z, d.soff, d.nB, d.nB, p.N, nbmax, pinv, 4096, status, 0, st)
+        lib.bddc_gj_inverse(Z, d.soff, d.nB, d.nB, p.N, nbmax, pinv, 4096, status, 0, 0, st)
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError(f"dual block of subdomain {bad + ls.s0} is singular")

@@ -44,21 +44,27 @@ def run(path, N=4096, nI=343, nB=386, reps=3):
           P(pinv), 4096, 0, P(st), 0, None, 0, stream, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
         torch.cuda.synchronize()
         best = min(best, ms.value)
-    # GJ inverse of N x nB^2
+    # GJ inverse of N x nB^2: general, and symmetric (SPD input)
     S0 = torch.rand(N, nB, nB, dtype=torch.float64, device="cuda") + 4 * nB * torch.eye(nB, dtype=torch.float64, device="cuda")
     soff = torch.arange(N, dtype=torch.int64, device="cuda") * nB * nB
-    gbest = 1e30
-    for _ in range(reps):
-        S = S0.clone()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        g(P(S), P(soff), P(i32(nB)), P(i32(nB)), N, nB, P(pinv), 4096, P(st), 0, stream)
-        e1.record()
-        torch.cuda.synchronize()
-        gbest = min(gbest, e0.elapsed_time(e1))
-    gflops = 2 * nB ** 3 * N
-    print(f"{path}: trailing {best:.2f} ms {flops / best / 1e9:.2f} TF/s | GJ inverse {gbest:.2f} ms {gflops / gbest / 1e9:.2f} TF/s", flush=True)
+    out = []
+    for sym in (0, 1):
+        A = 0.5 * (S0 + S0.transpose(1, 2)) if sym else S0
+        gbest = 1e30
+        for _ in range(reps):
+            S = A.clone()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g(P(S), P(soff), P(i32(nB)), P(i32(nB)), N, nB, P(pinv), 4096, P(st), sym, sym, stream)
+            e1.record()
+            torch.cuda.synchronize()
+            gbest = min(gbest, e0.elapsed_time(e1))
+        ref = torch.linalg.inv(A[:4])
+        err = ((S[:4] - ref).abs().max() / ref.abs().max()).item()
+        asym = (S[:4] - S[:4].transpose(1, 2)).abs().max().item()
+        out.append(f"GJ{'-sym' if sym else ''} {gbest:.2f} ms {2 * nB ** 3 * N / gbest / 1e9:.2f} TF/s-equiv err {err:.1e} asym {asym:.1e}")
+    print(f"{path}: trailing {best:.2f} ms {flops / best / 1e9:.2f} TF/s | " + " | ".join(out), flush=True)
 
 
 if __name__ == "__main__":
