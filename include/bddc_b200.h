@@ -243,6 +243,34 @@ int bddc_pc_primal_rows_T(const int* nB, const long long* voff, const int* pos2k
                           const int* pstart, const long long* poff, const double* In, double* Out,
                           int nbatch, cudaStream_t stream);
 
+/* Copy the per-panel inverse pivot blocks P_k^-1 of a batched 64-panel
+ * schur_eliminate (pinv + k * step_stride + b * pinv_stride, ld 64) into the
+ * diagonal blocks, completing the in-place LU used by the dual solves. */
+int bddc_lu_diag_pinv(double* LU, const long long* soff, const int* nB, int nbatch, int max_n,
+                      const double* pinv, long long pinv_stride, long long step_stride,
+                      cudaStream_t stream);
+
+/* Local part of the preconditioner and the coarse restriction per subdomain:
+ * x = u[perm]; cvals = G x; y = TT (Sdd^-1 (TT^T x with primal entries zeroed))
+ * through the dual-block LU (the reference's lu_solve of Stil, solver.py:187-195).
+ * replaces BddcPreconditioner.apply local solves solver.py:138-209. */
+int bddc_pc_local_solve(const int* nB, const long long* soff, const long long* voff,
+                        const int* iface_perm, const double* LU, const int* pos2k,
+                        const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,
+                        const int* gsize, const long long* sh_doff, const double* TT,
+                        const unsigned char* primal_mask, const double* u, double* y,
+                        const int* pstart, const long long* poff, const double* G, double* cvals,
+                        int nbatch, int max_nB, cudaStream_t stream);
+
+/* MP = e - Z Sbar[:, P], RP = e - Z^T Sbar[P, :]^T and C_i = Sbar[P, :] MP^T per
+ * subdomain through the dual-block LU (Z = Sdd^-1 embedded).
+ * replaces the coarse basis / coarse matrix assembly of solver.py:99-134. */
+int bddc_pc_primal_pieces_lu(const int* nB, const long long* soff, const long long* voff,
+                             const unsigned char* primal_mask, const int* pstart, const int* ppos,
+                             const long long* poff, const double* Sbar, const double* LU,
+                             double* MP, double* RP, double* Cl, const long long* coff,
+                             int nbatch, int max_nB, cudaStream_t stream);
+
 /* coarse[g,g] += contrib.  replaces solver.py:106. */
 int bddc_coarse_scatter(const int* pstart, const int* pgid, const double* Cl,
                         const long long* coff, double* C, long long ldc, int nbatch,

@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "bddc_b200.h"
 #include "tile_mma.cuh"
+#include "lu_solve.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -417,6 +418,133 @@ __global__ void primal_pieces_kernel(const int* __restrict__ nB, const long long
   }
 }
 
+// ---------------------------------------------------------------------------
+// dual solves with the blocked LU of the embedded dual block (lu_solve.cuh)
+// ---------------------------------------------------------------------------
+// P_k^-1 (kept per panel by schur_eliminate) into the diagonal blocks
+__global__ void lu_diag_pinv_kernel(double* __restrict__ LU, const long long* __restrict__ soff,
+                                    const int* __restrict__ nB, const double* __restrict__ pinv,
+                                    long long pinv_stride, long long step_stride) {
+  const int b = blockIdx.y, k = blockIdx.x;
+  const int n = nB[b], k0 = k * 64;
+  if (k0 >= n) return;
+  const int w = min(64, n - k0);
+  const double* P = pinv + (long long)k * step_stride + (long long)b * pinv_stride;
+  double* D = LU + soff[b] + (long long)k0 * n + k0;
+  for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+    const int r = idx / w, c = idx - r * w;
+    D[(long long)r * n + c] = P[r * 64 + c];
+  }
+}
+
+// local part of M^-1 and the coarse restriction, one CTA per subdomain:
+//   x = r[perm];  cvals = G x;  t = TT^T x (primal entries zeroed);  t = Sdd^-1 t (LU);
+//   y = TT t        (= A_i x with A_i = TT Z TT^T, without forming A_i)
+__global__ void __launch_bounds__(256) local_solve_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ soff,
+    const long long* __restrict__ voff, const int* __restrict__ iface_perm,
+    const double* __restrict__ LU, const int* __restrict__ pos2k,
+    const int* __restrict__ sub_globs, const int* __restrict__ sub_glob_boff,
+    const int* __restrict__ sub_glob_sh, const int* __restrict__ gsize,
+    const long long* __restrict__ sh_doff, const double* __restrict__ TT,
+    const unsigned char* __restrict__ primal_mask, const double* __restrict__ u,
+    double* __restrict__ y, const int* __restrict__ pstart, const long long* __restrict__ poff,
+    const double* __restrict__ G, double* __restrict__ cvals) {
+  extern __shared__ double lsm[];
+  const int b = blockIdx.x;
+  const int n = nB[b];
+  double* xs = lsm;             // n
+  double* ts = lsm + n;         // n
+  double* tmp = lsm + 2 * n;    // 64
+  const long long v0 = voff[b];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) xs[j] = u[iface_perm[v0 + j]];
+  __syncthreads();
+  const int np = pstart[b + 1] - pstart[b];
+  if (np) lus::rows_gemv<1>(G + poff[b], n, np, n, xs, cvals + pstart[b], 1.0, 0.0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    double s = 0.0;
+    if (!primal_mask[v0 + i]) {
+      const int k = pos2k[v0 + i];
+      const int bo = sub_glob_boff[k], ng = gsize[sub_globs[k]];
+      const double* Tb = TT + sh_doff[sub_glob_sh[k]];
+      const int ii = i - bo;
+      for (int j = 0; j < ng; ++j) s += Tb[j * ng + ii] * xs[bo + j];
+    }
+    ts[i] = s;
+  }
+  __syncthreads();
+  lus::lu_solve<1, false>(LU + soff[b], n, ts, tmp, nullptr);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int k = pos2k[v0 + i];
+    const int bo = sub_glob_boff[k], ng = gsize[sub_globs[k]];
+    const double* Tb = TT + sh_doff[sub_glob_sh[k]] + (long long)(i - bo) * ng;
+    double s = 0.0;
+    for (int j = 0; j < ng; ++j) s += Tb[j] * ts[bo + j];
+    y[v0 + i] = s;
+  }
+}
+
+// Primal pieces through the LU, one CTA per subdomain, 8 primal columns at a time:
+//   MP[p] = e_pc - Z Sbar[:, pc],  RP[p] = e_pc - Z^T Sbar[pc, :]^T,  C_i[p][q] = Sbar[pr, :] . MP[q]
+// (Z = Sdd^-1 embedded with zero primal rows / columns)
+constexpr int kPL = 8;
+__global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ soff,
+    const long long* __restrict__ voff, const unsigned char* __restrict__ primal_mask,
+    const int* __restrict__ pstart, const int* __restrict__ ppos,
+    const long long* __restrict__ poff, const double* __restrict__ Sbar,
+    const double* __restrict__ LU, double* __restrict__ MP, double* __restrict__ RP,
+    double* __restrict__ Cl, const long long* __restrict__ coff) {
+  extern __shared__ double psm[];
+  const int b = blockIdx.x;
+  const int n = nB[b];
+  const int p0 = pstart[b], np = pstart[b + 1] - p0;
+  if (np == 0) return;
+  double* X = psm;                      // n x kPL
+  double* tmp = psm + n * kPL;          // 64 x kPL
+  double* red = tmp + 64 * kPL;         // blockDim x kPL
+  const double* S = Sbar + soff[b];
+  const double* L = LU + soff[b];
+  const unsigned char* pm = primal_mask + voff[b];
+  double* Mb = MP + poff[b];
+  double* Rb = RP + poff[b];
+  for (int c0 = 0; c0 < np; c0 += kPL) {
+    const int pc_n = min(kPL, np - c0);
+    for (int idx = threadIdx.x; idx < n * kPL; idx += blockDim.x) {
+      const int r = idx / kPL, q = idx - r * kPL;
+      X[idx] = (q < pc_n && !pm[r]) ? S[(long long)r * n + ppos[p0 + c0 + q]] : 0.0;
+    }
+    __syncthreads();
+    lus::lu_solve<kPL, false>(L, n, X, tmp, red);
+    for (int idx = threadIdx.x; idx < n * pc_n; idx += blockDim.x) {
+      const int q = idx / n, r = idx - q * n;
+      Mb[(long long)(c0 + q) * n + r] = (r == ppos[p0 + c0 + q] ? 1.0 : 0.0) - X[r * kPL + q];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < n * kPL; idx += blockDim.x) {
+      const int r = idx / kPL, q = idx - r * kPL;
+      X[idx] = (q < pc_n && !pm[r]) ? S[(long long)ppos[p0 + c0 + q] * n + r] : 0.0;
+    }
+    __syncthreads();
+    lus::lu_solve<kPL, true>(L, n, X, tmp, red);
+    for (int idx = threadIdx.x; idx < n * pc_n; idx += blockDim.x) {
+      const int q = idx / n, r = idx - q * n;
+      Rb[(long long)(c0 + q) * n + r] = (r == ppos[p0 + c0 + q] ? 1.0 : 0.0) - X[r * kPL + q];
+    }
+    __syncthreads();
+  }
+  double* C = Cl + coff[b];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int i = warp; i < np * np; i += nw) {
+    const int p = i / np, q = i - p * np;
+    const int pr = ppos[p0 + p];
+    double v = 0.0;
+    for (int k = lane; k < n; k += 32) v += S[(long long)pr * n + k] * Mb[(long long)q * n + k];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) C[i] = v;
+  }
+}
+
 // rows form: Out[p][c] = sum over block of c: In[p][bo+q] * TT-derived value
 //   G = RP T   where T = Q D^T blockdiag: G[p][c] = sum_q RP[p][bo+q] T[bo+q][c]
 //            T[bo+q][c] = TT^T block [q][c-bo]  = TTb[(c-bo)*ng + q]
@@ -746,6 +874,49 @@ int bddc_pc_primal_rows_T(const int* nB, const long long* voff, const int* pos2k
   SubGlobMap m = make_map(nB, nullptr, voff, pos2k, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
                           nullptr, nullptr, nullptr, sh_doff);
   primal_rows_times_T_kernel<<<dim3(16, nbatch), 256, 0, stream>>>(m, TT, pstart, poff, In, Out); bddc_note_launches(1);
+  return pc_status();
+}
+
+int bddc_lu_diag_pinv(double* LU, const long long* soff, const int* nB, int nbatch, int max_n,
+                      const double* pinv, long long pinv_stride, long long step_stride,
+                      cudaStream_t stream) {
+  if (nbatch <= 0 || max_n <= 0) return 0;
+  lu_diag_pinv_kernel<<<dim3(ceil_div(max_n, 64), nbatch), 256, 0, stream>>>(LU, soff, nB, pinv,
+                                                                             pinv_stride, step_stride);
+  bddc_note_launches(1);
+  return pc_status();
+}
+
+int bddc_pc_local_solve(const int* nB, const long long* soff, const long long* voff,
+                        const int* iface_perm, const double* LU, const int* pos2k,
+                        const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,
+                        const int* gsize, const long long* sh_doff, const double* TT,
+                        const unsigned char* primal_mask, const double* u, double* y,
+                        const int* pstart, const long long* poff, const double* G, double* cvals,
+                        int nbatch, int max_nB, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = (2 * max_nB + 64) * (int)sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(local_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  local_solve_kernel<<<nbatch, 256, smem, stream>>>(nB, soff, voff, iface_perm, LU, pos2k, sub_globs,
+                                                    sub_glob_boff, sub_glob_sh, gsize, sh_doff, TT,
+                                                    primal_mask, u, y, pstart, poff, G, cvals);
+  bddc_note_launches(1);
+  return pc_status();
+}
+
+int bddc_pc_primal_pieces_lu(const int* nB, const long long* soff, const long long* voff,
+                             const unsigned char* primal_mask, const int* pstart, const int* ppos,
+                             const long long* poff, const double* Sbar, const double* LU,
+                             double* MP, double* RP, double* Cl, const long long* coff,
+                             int nbatch, int max_nB, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = (max_nB * kPL + 64 * kPL + 256 * kPL) * (int)sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(primal_pieces_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  primal_pieces_lu_kernel<<<nbatch, 256, smem, stream>>>(nB, soff, voff, primal_mask, pstart, ppos,
+                                                         poff, Sbar, LU, MP, RP, Cl, coff);
+  bddc_note_launches(1);
   return pc_status();
 }
 

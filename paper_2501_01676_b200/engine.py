@@ -712,25 +712,25 @@ class DevicePreconditioner:
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError(f"dual block of subdomain {bad + ls.s0} lost positive definiteness")
-        lib.bddc_gj_inverse(Z, d.soff, d.nB, d.nB, p.N, nbmax, pinv, 4096, status, 0, 0, st)
+        # blocked LU of the embedded dual block (64-wide panels, every P_k^-1 kept and
+        # moved into the diagonal blocks): the reference's lu_factor(Stil)
+        nsteps = (nbmax + 63) // 64
+        pinv_all = torch.empty(nsteps * p.N * 4096, dtype=F64, device="cuda")
+        lib.bddc_schur_eliminate(Z, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax, nbmax,
+                                 64, pinv_all, 4096, p.N * 4096, status, 0, None, 0, st)
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError(f"dual block of subdomain {bad + ls.s0} is singular")
-        lib.bddc_pc_zero_primal(d.nB, d.soff, d.voff, d_mask, Z, p.N, st)
-        self.A = torch.empty(p.S_total, dtype=F64, device="cuda")
-        TTT = torch.empty_like(TT)
-        lib.bddc_pc_local_operator(d.nB, d.soff, d.sub_glob_start, p.N, d.sub_globs,
-                                   d.sub_glob_boff, d.sub_glob_sh, d.gsize, d.sh_doff, d.slot_glob,
-                                   int(p.sh_sub.size), n_items, nbmax, max_ng, max_globs, TT, TTT,
-                                   Z, tmp, self.A, st)
-        del TTT
+        lib.bddc_lu_diag_pinv(Z, d.soff, d.nB, p.N, nbmax, pinv_all, 4096, p.N * 4096, st)
+        del pinv_all
+        self.LU, self.TT, self.d_mask = Z, TT, d_mask
         npn = max(int(poff[-1]), 1)
         MP = torch.empty(npn, dtype=F64, device="cuda")
         RP = torch.empty(npn, dtype=F64, device="cuda")
         multi = _multi(self.comm)
         Clg = (torch.zeros if multi else torch.empty)(max(int(gcoff[-1]), 1), dtype=F64, device="cuda")
-        lib.bddc_pc_primal_pieces(d.nB, d.soff, self.d_pstart, self.d_ppos, self.d_poff, Sbar, Z,
-                                  MP, RP, Clg[c0:], d_coff, p.N, nbmax, st)
+        lib.bddc_pc_primal_pieces_lu(d.nB, d.soff, d.voff, d_mask, self.d_pstart, self.d_ppos,
+                                     self.d_poff, Sbar, Z, MP, RP, Clg[c0:], d_coff, p.N, nbmax, st)
         self.G = torch.empty(npn, dtype=F64, device="cuda")
         self.Nt = torch.empty(npn, dtype=F64, device="cuda")
         lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
@@ -739,7 +739,7 @@ class DevicePreconditioner:
         lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
                                   d.sub_glob_sh, d.gsize, d.sh_doff, TT, self.d_pstart,
                                   self.d_poff, MP, self.Nt, p.N, st)
-        del Sbar, tmp, Z, MP, RP, TT, pinv
+        del Sbar, tmp, MP, RP, pinv
         nc = self.n_primal
         C = torch.zeros(nc * nc, dtype=F64, device="cuda")
         _allreduce(self.comm, Clg)
@@ -811,8 +811,10 @@ class DevicePreconditioner:
     def _launch(self, r, out):
         p, d, st = self.plan, self.ls.d, stream()
         nbmax = int(p.nB.max())
-        lib.bddc_local_gemv(d.nB, d.soff, d.voff, d.iface_perm, self.A, r, self.y, self.d_pstart,
-                            self.d_poff, self.G, self.cvals, p.N, nbmax, 2, st)
+        lib.bddc_pc_local_solve(d.nB, d.soff, d.voff, d.iface_perm, self.LU, d.pos2k, d.sub_globs,
+                                d.sub_glob_boff, d.sub_glob_sh, d.gsize, d.sh_doff, self.TT,
+                                self.d_mask, r, self.y, self.d_pstart, self.d_poff, self.G,
+                                self.cvals, p.N, nbmax, st)
         lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp, self.n_primal, st)
         _allreduce(self.comm, self.rp)
         lib.bddc_coarse_solve(self.coarse_lu, self.n_primal, self.n_primal, self.coarse_pinv, 4096,
