@@ -302,6 +302,14 @@ int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
                       long long pinv_step_stride, const int* lim, const int* first, double* b,
                       double* t, cudaStream_t stream);
 
+/* Same solve as a dataflow over 128-row super-panels (one cooperative launch,
+ * per-super-panel ready flags instead of grid-wide barriers): jmin[Q] / jmax[Q]
+ * = first / last super-panel coupled to super-panel Q in L' / W; flags: 2 *
+ * ceil(n / 128) ints, epoch: a value different from every earlier call's. */
+int bddc_coarse_solve_flow(const double* A, long long ld, int n, const double* pinv,
+                           long long pinv_step_stride, const int* jmin, const int* jmax, double* b,
+                           double* t, int* flags, int epoch, cudaStream_t stream);
+
 /* ---- krylov.cu : GMRES vector kernels (solver.py:286-310) ------------------ */
 
 int bddc_multi_dot(const double* V, long long n, int m, const double* w, double* h,

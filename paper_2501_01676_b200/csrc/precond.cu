@@ -729,6 +729,198 @@ __global__ void __launch_bounds__(BDDC_COOP_THREADS) coarse_solve_coop_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Coarse envelope solve as a dataflow over 128-row super-panels: CTA c owns
+// super-panels Q = c, c + grid, ...; a super-panel's rows are final once the
+// super-panels it depends on have published theirs (flag == epoch), so the
+// only serial chain is "flag -> 128x128 block GEMV -> flag" instead of one
+// grid-wide barrier per 64-wide panel.  The block on the critical path (the
+// neighbouring super-panel) is prefetched into shared memory with cp.async
+// while the older contributions are applied.
+//   forward:  b_Q -= sum_{J<Q} L'[Q, J] b_J ; then within Q: b_hi -= L'[hi, lo] b_lo
+//             t_Q = blockdiag(P) b_Q
+//   backward: x_Q = t_Q - sum_{J>Q} W[Q, J] x_J ; then x_lo -= W[lo, hi] x_hi
+// ---------------------------------------------------------------------------
+constexpr int kSP = 128;
+
+BDDC_DEV int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+BDDC_DEV void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+BDDC_DEV void wait_flag(const int* f, int epoch) {
+  if (threadIdx.x == 0) {
+    while (ld_acquire(f) != epoch) __nanosleep(32);
+  }
+  __syncthreads();
+}
+
+// acc[r] -= sum_c blk[r][c] v[c]   (r < h, c < w <= 128); warp per 4 rows (16 loads in
+// flight per lane when blk is in global memory)
+BDDC_DEV void block_gemv_sub(const double* blk, long long ldb, int h, int w, const double* v,
+                             double* acc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double vv[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) vv[j] = (lane + 32 * j < w) ? v[lane + 32 * j] : 0.0;
+  for (int r0 = 4 * warp; r0 < h; r0 += 4 * nw) {
+    double s[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      s[i] = 0.0;
+      if (r0 + i < h) {
+        const double* row = blk + (long long)(r0 + i) * ldb;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (lane + 32 * j < w) s[i] = fma(row[lane + 32 * j], vv[j], s[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+    if (lane < 4 && r0 + lane < h) {
+      double x = s[0];
+#pragma unroll
+      for (int i = 1; i < 4; ++i)
+        if (lane == i) x = s[i];
+      acc[r0 + lane] -= x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) coarse_solve_flow_kernel(
+    const double* __restrict__ A, long long ld, int n, const double* __restrict__ pinv,
+    long long pstride, const int* __restrict__ jmin, const int* __restrict__ jmax,
+    double* __restrict__ b, double* __restrict__ t, int* __restrict__ flags, int epoch) {
+  extern __shared__ __align__(16) double fsm[];
+  double* buf = fsm;                 // kSP x kSP prefetched block (neighbour super-panel)
+  double* dg = buf + kSP * kSP;      // 64 x 64 prefetched intra-super-panel block
+  double* acc = dg + 64 * 64;        // kSP
+  double* v = acc + kSP;             // kSP
+  const int nQ = (n + kSP - 1) / kSP;
+  int* fflag = flags;
+  int* bflag = flags + nQ;
+  // ---- forward + diagonal ----
+  for (int Q = blockIdx.x; Q < nQ; Q += gridDim.x) {
+    const int r0 = Q * kSP, h = min(kSP, n - r0);
+    const int Jlo = jmin[Q];
+    const bool pre = Q - 1 >= Jlo;
+    if (h > 64) {
+      const double* src = A + (long long)(r0 + 64) * ld + r0;
+      for (int idx = threadIdx.x; idx < (h - 64) * 64; idx += blockDim.x) {
+        const int r = idx >> 6, c = idx & 63;
+        cp_async8(dg + idx, src + (long long)r * ld + c, true);
+      }
+    }
+    if (pre) {
+      const double* src = A + (long long)r0 * ld + (Q - 1) * kSP;
+      for (int idx = threadIdx.x; idx < h * kSP; idx += blockDim.x) {
+        const int r = idx / kSP, c = idx - r * kSP;
+        cp_async8(buf + idx, src + (long long)r * ld + c, true);
+      }
+    }
+    cp_async_commit();
+    for (int i = threadIdx.x; i < h; i += blockDim.x) acc[i] = b[r0 + i];
+    __syncthreads();
+    for (int J = Jlo; J < Q - 1; ++J) {
+      wait_flag(fflag + J, epoch);
+      for (int i = threadIdx.x; i < kSP; i += blockDim.x) v[i] = __ldcg(b + J * kSP + i);
+      __syncthreads();
+      block_gemv_sub(A + (long long)r0 * ld + J * kSP, ld, h, kSP, v, acc);
+      __syncthreads();
+    }
+    if (pre) {
+      wait_flag(fflag + Q - 1, epoch);
+      for (int i = threadIdx.x; i < kSP; i += blockDim.x) v[i] = __ldcg(b + (Q - 1) * kSP + i);
+      cp_async_wait<0>();
+      __syncthreads();
+      block_gemv_sub(buf, kSP, h, kSP, v, acc);
+      __syncthreads();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (h > 64) {  // lower half of the super-panel from its upper half
+      block_gemv_sub(dg, 64, h - 64, 64, acc, acc + 64);
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < h; i += blockDim.x) b[r0 + i] = acc[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release(fflag + Q, epoch);
+    }
+    // t = blockdiag(P_p) b for the two 64-panels (v = 0 - P b, then negated)
+    for (int i = threadIdx.x; i < kSP; i += blockDim.x) v[i] = 0.0;
+    __syncthreads();
+    for (int hp = 0; hp * 64 < h; ++hp) {
+      const int w = min(64, h - hp * 64);
+      block_gemv_sub(pinv + (long long)(2 * Q + hp) * pstride, 64, w, w, acc + hp * 64, v + hp * 64);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < h; i += blockDim.x) t[r0 + i] = -v[i];
+    __syncthreads();
+  }
+  // ---- backward ----
+  const int qlast = blockIdx.x + ((nQ - 1 - (int)blockIdx.x) / (int)gridDim.x) * (int)gridDim.x;
+  for (int Q = qlast; Q >= 0 && Q < nQ; Q -= gridDim.x) {
+    const int r0 = Q * kSP, h = min(kSP, n - r0);
+    const int Jhi = jmax[Q];
+    const bool pre = Q + 1 <= Jhi;
+    if (h > 64) {
+      const double* src = A + (long long)r0 * ld + r0 + 64;
+      for (int idx = threadIdx.x; idx < 64 * 64; idx += blockDim.x) {
+        const int r = idx >> 6, c = idx & 63;
+        cp_async8(dg + idx, c < h - 64 ? src + (long long)r * ld + c : src, c < h - 64);
+      }
+    }
+    if (pre) {
+      const int w = min(kSP, n - (Q + 1) * kSP);
+      const double* src = A + (long long)r0 * ld + (Q + 1) * kSP;
+      for (int idx = threadIdx.x; idx < h * kSP; idx += blockDim.x) {
+        const int r = idx / kSP, c = idx - r * kSP;
+        cp_async8(buf + idx, c < w ? src + (long long)r * ld + c : src, c < w);
+      }
+    }
+    cp_async_commit();
+    for (int i = threadIdx.x; i < h; i += blockDim.x) acc[i] = t[r0 + i];
+    __syncthreads();
+    for (int J = Jhi; J > Q + 1; --J) {
+      const int w = min(kSP, n - J * kSP);
+      wait_flag(bflag + J, epoch);
+      for (int i = threadIdx.x; i < w; i += blockDim.x) v[i] = __ldcg(t + J * kSP + i);
+      __syncthreads();
+      block_gemv_sub(A + (long long)r0 * ld + J * kSP, ld, h, w, v, acc);
+      __syncthreads();
+    }
+    if (pre) {
+      const int w = min(kSP, n - (Q + 1) * kSP);
+      wait_flag(bflag + Q + 1, epoch);
+      for (int i = threadIdx.x; i < w; i += blockDim.x) v[i] = __ldcg(t + (Q + 1) * kSP + i);
+      cp_async_wait<0>();
+      __syncthreads();
+      block_gemv_sub(buf, kSP, h, w, v, acc);
+      __syncthreads();
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    if (h > 64) {  // upper half from the (final) lower half
+      block_gemv_sub(dg, 64, 64, h - 64, acc + 64, acc);
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < h; i += blockDim.x) t[r0 + i] = acc[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release(bflag + Q, epoch);
+    }
+  }
+}
+
 }  // namespace bddc
 
 // ===========================================================================
@@ -982,6 +1174,31 @@ int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
                   (void*)&lim, (void*)&first, (void*)&b, (void*)&t};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)coarse_solve_coop_kernel, dim3(grid),
                                               dim3(BDDC_COOP_THREADS), args, 0, stream);
+  bddc_note_launches(1);
+  return e == cudaSuccess ? pc_status() : -(int)e;
+}
+
+int bddc_coarse_solve_flow(const double* A, long long ld, int n, const double* pinv,
+                           long long pinv_step_stride, const int* jmin, const int* jmax, double* b,
+                           double* t, int* flags, int epoch, cudaStream_t stream) {
+  if (n <= 0) return 0;
+  const int smem = (kSP * kSP + 64 * 64 + 2 * kSP) * (int)sizeof(double);
+  static int grid = 0;
+  if (grid == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(coarse_solve_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_solve_flow_kernel, 256, smem);
+    grid = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  const int nQ = (n + kSP - 1) / kSP;
+  int g = nQ < grid ? nQ : grid;
+  void* args[] = {(void*)&A, (void*)&ld, (void*)&n, (void*)&pinv, (void*)&pinv_step_stride,
+                  (void*)&jmin, (void*)&jmax, (void*)&b, (void*)&t, (void*)&flags, (void*)&epoch};
+  // cooperative launch: every CTA co-resident (the dataflow waits on other CTAs)
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)coarse_solve_flow_kernel, dim3(g),
+                                              dim3(256), args, smem, stream);
   bddc_note_launches(1);
   return e == cudaSuccess ? pc_status() : -(int)e;
 }

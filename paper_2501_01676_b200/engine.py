@@ -761,6 +761,17 @@ class DevicePreconditioner:
         self._lim_c = (ctypes.c_int * steps)(*self.lim.tolist())
         self._first_c = (ctypes.c_int * steps)(*self.first.tolist())
         self.d_lim, self.d_first = dev_i32(self.lim), dev_i32(self.first)
+        # super-panel (128-row) dependency ranges for the dataflow solve
+        nq = (nc + 127) // 128
+        lim64 = self.lim.astype(np.int64)
+        lsup = np.array([lim64[min(2 * q + 1, lim64.size - 1)] for q in range(nq)], dtype=np.int64)
+        lsup = np.maximum.accumulate(lsup)
+        q_idx = np.arange(nq, dtype=np.int64)
+        jmin = np.minimum(np.searchsorted(lsup, 128 * q_idx, side="right"), q_idx)
+        jmax = np.maximum((lsup - 1) // 128, q_idx)
+        self.d_jmin, self.d_jmax = dev_i32(jmin), dev_i32(jmax)
+        self.flow_flags = torch.zeros(2 * nq, dtype=torch.int32, device="cuda")
+        self.flow_epoch = 0
         lib.bddc_coarse_factor(C, dev_i64([0]), dev_i32([nc]), dev_i32([nc]), nc,
                                ctypes.cast(self._lim_c, ctypes.c_void_p), self.coarse_pinv, piv,
                                status1, st)
@@ -779,6 +790,7 @@ class DevicePreconditioner:
         self.up = torch.empty(nc, dtype=F64, device="cuda")
 
     use_graph = False  # re-captured per preconditioner: costs more than it saves here
+    coarse_flow = True  # dataflow coarse solve (flags) instead of one grid barrier per panel
 
     def apply_device(self, r, out=None):
         """M^-1 r.  The launch sequence (local GEMVs, coarse gather, the
@@ -817,8 +829,14 @@ class DevicePreconditioner:
                                 self.cvals, p.N, nbmax, st)
         lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp, self.n_primal, st)
         _allreduce(self.comm, self.rp)
-        lib.bddc_coarse_solve(self.coarse_lu, self.n_primal, self.n_primal, self.coarse_pinv, 4096,
-                              self.d_lim, self.d_first, self.rp, self.up, st)
+        if self.coarse_flow:
+            self.flow_epoch = self.flow_epoch % 2000000000 + 1
+            lib.bddc_coarse_solve_flow(self.coarse_lu, self.n_primal, self.n_primal,
+                                       self.coarse_pinv, 4096, self.d_jmin, self.d_jmax, self.rp,
+                                       self.up, self.flow_flags, self.flow_epoch, st)
+        else:
+            lib.bddc_coarse_solve(self.coarse_lu, self.n_primal, self.n_primal, self.coarse_pinv,
+                                  4096, self.d_lim, self.d_first, self.rp, self.up, st)
         lib.bddc_prolong_primal(d.nB, d.voff, self.d_pstart, self.d_pgid, self.d_poff, self.Nt,
                                 self.up, self.y, p.N, st)
         lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n_hat, st)
