@@ -10,7 +10,8 @@
 //              for k down: x_k -= W_k x_(>k)
 //   A^T x = b: for k up:   x_(>k) -= W_k^T x_k
 //              for k down: x_k = P_k^-T (x_k - A21^(k)T x_(>k))
-// X is n x NR row-major (X[r * NR + q]).
+// X is n x NR row-major with row stride xstride(NR) (NR + 1 for NR > 1: the
+// padding spreads the lanes of a warp over the shared-memory banks).
 #pragma once
 #include "common.cuh"
 
@@ -19,10 +20,46 @@ namespace lus {
 
 constexpr int kP = 64;
 
+template <int NR>
+__host__ __device__ constexpr int xstride() { return NR == 1 ? 1 : NR + 1; }
+
+// single right-hand side: warp per 4 rows (4 independent loads per lane in flight)
+BDDC_DEV void rows_gemv1(const double* __restrict__ A, long long lda, int m, int k,
+                         const double* X, double* Y, double alpha, double beta) {
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  const int nw = (int)(blockDim.x >> 5);
+  for (int r0 = 4 * warp; r0 < m; r0 += 4 * nw) {
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* a0 = A + (long long)r0 * lda;
+    const int nr = min(4, m - r0);
+    for (int c = lane; c < k; c += 32) {
+      const double x = X[c];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i < nr) s[i] = fma(a0[(long long)i * lda + c], x, s[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s[i] += __shfl_xor_sync(0xffffffffu, s[i], o);
+    if (lane < nr) {
+      double t = s[0];
+#pragma unroll
+      for (int i = 1; i < 4; ++i)
+        if (lane == i) t = s[i];
+      Y[r0 + lane] = (beta == 0.0 ? 0.0 : beta * Y[r0 + lane]) + alpha * t;
+    }
+  }
+}
+
 // Y[r][q] = beta * Y[r][q] + alpha * sum_c A[r][c] X[c][q]   (r < m, c < k); warp per row
 template <int NR>
 BDDC_DEV void rows_gemv(const double* __restrict__ A, long long lda, int m, int k,
                         const double* X, double* Y, double alpha, double beta) {
+  if (NR == 1) {
+    rows_gemv1(A, lda, m, k, X, Y, alpha, beta);
+    return;
+  }
   const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
   const int nw = (int)(blockDim.x >> 5);
   for (int r = warp; r < m; r += nw) {
@@ -33,7 +70,7 @@ BDDC_DEV void rows_gemv(const double* __restrict__ A, long long lda, int m, int 
     for (int c = lane; c < k; c += 32) {
       const double v = a[c];
 #pragma unroll
-      for (int q = 0; q < NR; ++q) s[q] = fma(v, X[c * NR + q], s[q]);
+      for (int q = 0; q < NR; ++q) s[q] = fma(v, X[c * xstride<NR>() + q], s[q]);
     }
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
@@ -47,7 +84,7 @@ BDDC_DEV void rows_gemv(const double* __restrict__ A, long long lda, int m, int 
 #pragma unroll
       for (int q = 0; q < NR; ++q)
         if (q == lane) t = s[q];
-      Y[r * NR + lane] = (beta == 0.0 ? 0.0 : beta * Y[r * NR + lane]) + alpha * t;
+      Y[r * xstride<NR>() + lane] = (beta == 0.0 ? 0.0 : beta * Y[r * xstride<NR>() + lane]) + alpha * t;
     }
   }
 }
@@ -55,8 +92,32 @@ BDDC_DEV void rows_gemv(const double* __restrict__ A, long long lda, int m, int 
 // Y[c][q] = beta * Y[c][q] + alpha * sum_r A[r][c] X[r][q]   (c < n, r < m); thread per column,
 // the rows split over blockDim / n_cols groups and reduced through red (>= blockDim * NR doubles)
 template <int NR>
+BDDC_DEV void cols_acc(const double* __restrict__ A, long long lda, int r0, int m, int step, int c,
+                       const double* X, double* s) {
+  constexpr int XS = xstride<NR>();
+  int r = r0;
+  for (; r + 3 * step < m; r += 4 * step) {
+    const double v0 = A[(long long)r * lda + c], v1 = A[(long long)(r + step) * lda + c];
+    const double v2 = A[(long long)(r + 2 * step) * lda + c], v3 = A[(long long)(r + 3 * step) * lda + c];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      s[q] = fma(v0, X[r * XS + q], s[q]);
+      s[q] = fma(v1, X[(r + step) * XS + q], s[q]);
+      s[q] = fma(v2, X[(r + 2 * step) * XS + q], s[q]);
+      s[q] = fma(v3, X[(r + 3 * step) * XS + q], s[q]);
+    }
+  }
+  for (; r < m; r += step) {
+    const double v = A[(long long)r * lda + c];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) s[q] = fma(v, X[r * XS + q], s[q]);
+  }
+}
+
+template <int NR>
 BDDC_DEV void cols_gemv(const double* __restrict__ A, long long lda, int m, int n,
                         const double* X, double* Y, double alpha, double beta, double* red) {
+  constexpr int XS = xstride<NR>();
   const int nt = (int)blockDim.x;
   const int groups = max(1, nt / max(n, 1));
   const int grp = (int)threadIdx.x / max(n, 1), c = (int)threadIdx.x - grp * max(n, 1);
@@ -64,13 +125,7 @@ BDDC_DEV void cols_gemv(const double* __restrict__ A, long long lda, int m, int 
     double s[NR];
 #pragma unroll
     for (int q = 0; q < NR; ++q) s[q] = 0.0;
-    if (grp < groups && c < n) {
-      for (int r = grp; r < m; r += groups) {
-        const double v = A[(long long)r * lda + c];
-#pragma unroll
-        for (int q = 0; q < NR; ++q) s[q] = fma(v, X[r * NR + q], s[q]);
-      }
-    }
+    if (grp < groups && c < n) cols_acc<NR>(A, lda, grp, m, groups, c, X, s);
     if (groups > 1) {
       if (grp < groups && c < n)
 #pragma unroll
@@ -85,56 +140,54 @@ BDDC_DEV void cols_gemv(const double* __restrict__ A, long long lda, int m, int 
     if (grp == 0 && c < n)
 #pragma unroll
       for (int q = 0; q < NR; ++q)
-        Y[c * NR + q] = (beta == 0.0 ? 0.0 : beta * Y[c * NR + q]) + alpha * s[q];
+        Y[c * XS + q] = (beta == 0.0 ? 0.0 : beta * Y[c * XS + q]) + alpha * s[q];
   } else {
     for (int cc = threadIdx.x; cc < n; cc += nt) {
       double s[NR];
 #pragma unroll
       for (int q = 0; q < NR; ++q) s[q] = 0.0;
-      for (int r = 0; r < m; ++r) {
-        const double v = A[(long long)r * lda + cc];
-#pragma unroll
-        for (int q = 0; q < NR; ++q) s[q] = fma(v, X[r * NR + q], s[q]);
-      }
+      cols_acc<NR>(A, lda, 0, m, 1, cc, X, s);
 #pragma unroll
       for (int q = 0; q < NR; ++q)
-        Y[cc * NR + q] = (beta == 0.0 ? 0.0 : beta * Y[cc * NR + q]) + alpha * s[q];
+        Y[cc * XS + q] = (beta == 0.0 ? 0.0 : beta * Y[cc * XS + q]) + alpha * s[q];
     }
   }
   __syncthreads();
 }
 
 // x <- A^-1 x (TRANS: A^-T x); M: n x n LU (ld n) with P^-1 diagonal blocks;
-// tmp: 64 * NR doubles; red: blockDim * NR doubles (transposed solve only)
+// X: n rows of stride xstride(NR); tmp: 64 * xstride(NR) doubles; red: blockDim * NR
+// doubles (transposed solve only)
 template <int NR, bool TRANS>
 BDDC_DEV void lu_solve(const double* __restrict__ M, int n, double* X, double* tmp, double* red) {
+  constexpr int XS = xstride<NR>();
   const int np = (n + kP - 1) / kP;
   if (!TRANS) {
     for (int j = 0; j < np; ++j) {
       const int j0 = j * kP, w = min(kP, n - j0), j1 = j0 + w;
-      rows_gemv<NR>(M + (long long)j0 * n + j0, n, w, w, X + j0 * NR, tmp, 1.0, 0.0);
+      rows_gemv<NR>(M + (long long)j0 * n + j0, n, w, w, X + j0 * XS, tmp, 1.0, 0.0);
       __syncthreads();
-      for (int i = threadIdx.x; i < w * NR; i += blockDim.x) X[j0 * NR + i] = tmp[i];
+      for (int i = threadIdx.x; i < w * XS; i += blockDim.x) X[j0 * XS + i] = tmp[i];
       __syncthreads();
-      if (j1 < n) rows_gemv<NR>(M + (long long)j1 * n + j0, n, n - j1, w, X + j0 * NR, X + j1 * NR, -1.0, 1.0);
+      if (j1 < n) rows_gemv<NR>(M + (long long)j1 * n + j0, n, n - j1, w, X + j0 * XS, X + j1 * XS, -1.0, 1.0);
       __syncthreads();
     }
     for (int k = np - 1; k >= 0; --k) {
       const int k0 = k * kP, w = min(kP, n - k0), k1 = k0 + w;
-      if (k1 < n) rows_gemv<NR>(M + (long long)k0 * n + k1, n, w, n - k1, X + k1 * NR, X + k0 * NR, -1.0, 1.0);
+      if (k1 < n) rows_gemv<NR>(M + (long long)k0 * n + k1, n, w, n - k1, X + k1 * XS, X + k0 * XS, -1.0, 1.0);
       __syncthreads();
     }
   } else {
     for (int j = 0; j < np; ++j) {
       const int j0 = j * kP, w = min(kP, n - j0), j1 = j0 + w;
-      if (j1 < n) cols_gemv<NR>(M + (long long)j0 * n + j1, n, w, n - j1, X + j0 * NR, X + j1 * NR, -1.0, 1.0, red);
+      if (j1 < n) cols_gemv<NR>(M + (long long)j0 * n + j1, n, w, n - j1, X + j0 * XS, X + j1 * XS, -1.0, 1.0, red);
     }
     for (int k = np - 1; k >= 0; --k) {
       const int k0 = k * kP, w = min(kP, n - k0), k1 = k0 + w;
-      if (k1 < n) cols_gemv<NR>(M + (long long)k1 * n + k0, n, n - k1, w, X + k1 * NR, X + k0 * NR, -1.0, 1.0, red);
+      if (k1 < n) cols_gemv<NR>(M + (long long)k1 * n + k0, n, n - k1, w, X + k1 * XS, X + k0 * XS, -1.0, 1.0, red);
       // x_k = P_k^-T x_k
-      cols_gemv<NR>(M + (long long)k0 * n + k0, n, w, w, X + k0 * NR, tmp, 1.0, 0.0, red);
-      for (int i = threadIdx.x; i < w * NR; i += blockDim.x) X[k0 * NR + i] = tmp[i];
+      cols_gemv<NR>(M + (long long)k0 * n + k0, n, w, w, X + k0 * XS, tmp, 1.0, 0.0, red);
+      for (int i = threadIdx.x; i < w * XS; i += blockDim.x) X[k0 * XS + i] = tmp[i];
       __syncthreads();
     }
   }

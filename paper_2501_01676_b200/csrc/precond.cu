@@ -18,6 +18,7 @@
 #include "bddc_b200.h"
 #include "tile_mma.cuh"
 #include "lu_solve.cuh"
+#include "dense_block.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -302,15 +303,8 @@ __global__ void ttblock_kernel(const int* __restrict__ slot_glob, const int* __r
   if (s >= n_slots) return;
   const int g = slot_glob[s];
   const int n = gsize[g];
-  const double* Qg = Q + q_off[g];
-  const double* Dg = D + sh_doff[s];
-  double* O = TT + sh_doff[s];
-  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
-    int r = idx / n, c = idx - r * n;
-    double v = 0.0;
-    for (int a = 0; a < n; ++a) v += Dg[r * n + a] * Qg[c * n + a];
-    O[idx] = v;
-  }
+  // TT = D Q^T on the DMMA pipe (dense_block.cuh)
+  blk::gemm(TT + sh_doff[s], n, D + sh_doff[s], n, false, Q + q_off[g], n, true, n, n, n, 1.0, 0.0);
 }
 
 // out = TT_blockdiag * in  (left) or in * TT_blockdiag^T (right), TT from ttblock_kernel
@@ -500,9 +494,10 @@ __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
   const int n = nB[b];
   const int p0 = pstart[b], np = pstart[b + 1] - p0;
   if (np == 0) return;
-  double* X = psm;                      // n x kPL
-  double* tmp = psm + n * kPL;          // 64 x kPL
-  double* red = tmp + 64 * kPL;         // blockDim x kPL
+  constexpr int XS = lus::xstride<kPL>();
+  double* X = psm;                      // n x XS
+  double* tmp = psm + n * XS;           // 64 x XS
+  double* red = tmp + 64 * XS;          // blockDim x kPL
   const double* S = Sbar + soff[b];
   const double* L = LU + soff[b];
   const unsigned char* pm = primal_mask + voff[b];
@@ -512,24 +507,24 @@ __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
     const int pc_n = min(kPL, np - c0);
     for (int idx = threadIdx.x; idx < n * kPL; idx += blockDim.x) {
       const int r = idx / kPL, q = idx - r * kPL;
-      X[idx] = (q < pc_n && !pm[r]) ? S[(long long)r * n + ppos[p0 + c0 + q]] : 0.0;
+      X[r * XS + q] = (q < pc_n && !pm[r]) ? S[(long long)r * n + ppos[p0 + c0 + q]] : 0.0;
     }
     __syncthreads();
     lus::lu_solve<kPL, false>(L, n, X, tmp, red);
     for (int idx = threadIdx.x; idx < n * pc_n; idx += blockDim.x) {
       const int q = idx / n, r = idx - q * n;
-      Mb[(long long)(c0 + q) * n + r] = (r == ppos[p0 + c0 + q] ? 1.0 : 0.0) - X[r * kPL + q];
+      Mb[(long long)(c0 + q) * n + r] = (r == ppos[p0 + c0 + q] ? 1.0 : 0.0) - X[r * XS + q];
     }
     __syncthreads();
     for (int idx = threadIdx.x; idx < n * kPL; idx += blockDim.x) {
-      const int r = idx / kPL, q = idx - r * kPL;
-      X[idx] = (q < pc_n && !pm[r]) ? S[(long long)ppos[p0 + c0 + q] * n + r] : 0.0;
+      const int q = idx / n, r = idx - q * n;  // coalesced along the Sbar row
+      X[r * XS + q] = (q < pc_n && !pm[r]) ? S[(long long)ppos[p0 + c0 + q] * n + r] : 0.0;
     }
     __syncthreads();
     lus::lu_solve<kPL, true>(L, n, X, tmp, red);
     for (int idx = threadIdx.x; idx < n * pc_n; idx += blockDim.x) {
       const int q = idx / n, r = idx - q * n;
-      Rb[(long long)(c0 + q) * n + r] = (r == ppos[p0 + c0 + q] ? 1.0 : 0.0) - X[r * kPL + q];
+      Rb[(long long)(c0 + q) * n + r] = (r == ppos[p0 + c0 + q] ? 1.0 : 0.0) - X[r * XS + q];
     }
     __syncthreads();
   }
@@ -1103,7 +1098,7 @@ int bddc_pc_primal_pieces_lu(const int* nB, const long long* soff, const long lo
                              double* MP, double* RP, double* Cl, const long long* coff,
                              int nbatch, int max_nB, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  const int smem = (max_nB * kPL + 64 * kPL + 256 * kPL) * (int)sizeof(double);
+  const int smem = (max_nB * lus::xstride<kPL>() + 64 * lus::xstride<kPL>() + 256 * kPL) * (int)sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(primal_pieces_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   primal_pieces_lu_kernel<<<nbatch, 256, smem, stream>>>(nB, soff, voff, primal_mask, pstart, ppos,
