@@ -734,11 +734,11 @@ __global__ void extract_slot_blocks_kernel(const int* __restrict__ slot_sub,
 
 // Glob Schur blocks of the listed slots (n_g <= 64): SC = sym(((Bsym^-1)[g,g])^-1),
 // one register Gauss-Jordan per CTA; sc_status[k] = kNotPositiveDefinite on failure.
-__global__ void __launch_bounds__(256, 2) slot_schur_kernel(
+__global__ void __launch_bounds__(256, 4) slot_schur_kernel(
     const int* __restrict__ slots, const int* __restrict__ slot_glob,
     const int* __restrict__ gsize, const long long* __restrict__ sh_doff,
     const double* __restrict__ BiC, double* __restrict__ SC, int* __restrict__ sc_status) {
-  __shared__ RegGjSmem sm;
+  __shared__ MmaGjSmem sm;
   const int k = slots[blockIdx.x];
   const int n = gsize[slot_glob[k]];
   if (n > kTile) return;

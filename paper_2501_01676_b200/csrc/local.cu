@@ -57,12 +57,12 @@ __global__ void assemble_kernel(double* __restrict__ base, const long long* __re
 // ---------------------------------------------------------------------------
 // pivot block inverse (w x w, w <= 64): register block Gauss-Jordan (reg_gj.cuh)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) pivot_inverse_kernel(
+__global__ void __launch_bounds__(256, 4) pivot_inverse_kernel(
     const double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, int k, double* __restrict__ pinv, long long pinv_stride,
     int* __restrict__ status, int require_positive, double* __restrict__ piv_out,
     long long piv_stride) {
-  __shared__ RegGjSmem sm;
+  __shared__ MmaGjSmem sm;
   const int b = blockIdx.x;
   const int w = min(kTile, npiv[b] - k);
   if (w <= 0) return;

@@ -13,14 +13,21 @@ struct RegGjSmem {
   int bad;
 };
 
+struct MmaGjSmem {
+  double R[2][4][kTile];     // pivot rows (double-buffered by step parity)
+  double F[2][kTile][4];     // pivot columns
+  double U[4][68];           // Mi * R (pivot columns: I + Mi); stride 68: conflict-free B fragments
+  int bad;
+};
+
 // Inverse of the w x w (w <= 64) matrix M (leading dimension L) by
 // Gauss-Jordan without pivoting, written to out (leading dimension ldo).
 // Needs blockDim.x == 256.  Returns true (in every thread) when a pivot is
 // zero / non-finite, or <= 0 with require_positive (the LDL^T pivots: the
 // cho_factor criterion).  piv: the w scalar pivots (may be null).
-BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double* __restrict__ out,
-                       long long ldo, int require_positive, double* __restrict__ piv,
-                       RegGjSmem& sm) {
+BDDC_DEV bool reg_gj64_fma(const double* __restrict__ M, long long L, int w,
+                           double* __restrict__ out, long long ldo, int require_positive,
+                           double* __restrict__ piv, RegGjSmem& sm) {
   // Register-resident block Gauss-Jordan with 4x4 pivot blocks: thread t owns
   // column c = t % 64 and rows r0 + 4 j (r0 = t / 64, j < 16), so the four
   // rows of a pivot block are rows of the four thread groups.  The pivot rows
@@ -137,5 +144,119 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
   return failed;
 }
 
+
+// Same inverse with the rank-4 updates on the DMMA pipe.  The matrix lives in
+// DMMA accumulator fragments: warp w owns rows 8w..8w+7, thread (g, t) holds
+// (8w + g, 8j + 2t + h) for j < 8, h < 2.  Step s (pivots p = 4s..4s+3):
+//   publish pivot rows R (owner warp) and pivot columns F (all warps);
+//   Mi = R[:, p:p+4]^-1 (one thread: the 4x4 Gauss-Jordan, scalar pivots);
+//   U = Mi R with U[:, p:p+4] = I + Mi, so that the single update
+//   M -= F U (one m8n8k4 DMMA per 8x8 tile) also produces the new pivot
+//   columns -F Mi; the pivot rows are then overwritten with U (Mi on the
+//   pivot block).
+BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double* __restrict__ out,
+                       long long ldo, int require_positive, double* __restrict__ piv,
+                       MmaGjSmem& sm, int max_steps = 1 << 30) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int row = 8 * warp + g;
+  double c[8][2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = 8 * j + 2 * t + h;
+      c[j][h] = (row < w && col < w) ? M[(long long)row * L + col] : (row == col ? 1.0 : 0.0);
+    }
+  if (threadIdx.x == 0) sm.bad = 0;
+  const int nsteps = min((w + 3) >> 2, max_steps);
+  for (int s = 0; s < nsteps; ++s) {
+    const int par = s & 1, p = 4 * s, pw = s >> 1, g0 = 4 * (s & 1);
+    // publish pivot rows (owner warp) and pivot columns (tile jp = pw, lanes holding them)
+    if (warp == pw && g >= g0 && g < g0 + 4) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) sm.R[par][g - g0][8 * j + 2 * t + h] = c[j][h];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j != pw) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int cc = 2 * t + h - g0;
+        if (cc >= 0 && cc < 4) sm.F[par][row][cc] = c[j][h];
+      }
+    }
+    __syncthreads();
+    // 4x4 Gauss-Jordan of the pivot block in every warp (lane 4i+j holds Mi[i][j],
+    // lanes 16..31 mirror lanes 0..15): no shared-memory round trip for Mi
+    double m;
+    {
+      const int i = (lane >> 2) & 3, jj = lane & 3;
+      m = sm.R[par][i][p + jj];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double pv = __shfl_sync(0xffffffffu, m, 5 * q);
+        const double rq = __shfl_sync(0xffffffffu, m, 4 * q + jj);
+        const double cq = __shfl_sync(0xffffffffu, m, 4 * i + q);
+        if (threadIdx.x == 0 && p + q < w) {
+          if (piv) piv[p + q] = pv;
+          if (!(pv == pv) || pv == 0.0 || isinf(pv) || (require_positive && !(pv > 0.0))) sm.bad = 1;
+        }
+        const double ip = 1.0 / pv;
+        if (i == q) m = (jj == q) ? ip : rq * ip;
+        else m = (jj == q) ? -cq * ip : m - cq * rq * ip;
+      }
+    }
+    {  // U = Mi R, pivot columns I + Mi: one value per thread (i is warp-uniform)
+      const int i = threadIdx.x >> 6, col = threadIdx.x & 63;
+      const double m0 = __shfl_sync(0xffffffffu, m, 4 * i), m1 = __shfl_sync(0xffffffffu, m, 4 * i + 1);
+      const double m2 = __shfl_sync(0xffffffffu, m, 4 * i + 2), m3 = __shfl_sync(0xffffffffu, m, 4 * i + 3);
+      double u;
+      if (col >= p && col < p + 4) {
+        const int k = col - p;
+        u = (k == 0 ? m0 : k == 1 ? m1 : k == 2 ? m2 : m3) + (i == k ? 1.0 : 0.0);
+      } else {
+        u = m0 * sm.R[par][0][col] + m1 * sm.R[par][1][col] + m2 * sm.R[par][2][col] +
+            m3 * sm.R[par][3][col];
+      }
+      sm.U[i][col] = u;
+    }
+    // the pivot-block values a pivot-row lane needs: Mi[g - g0][2t + h - (p - 8 pw)]
+    double mp[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int gi = (g - g0) & 3, k = (2 * t + h - g0) & 3;
+      mp[h] = __shfl_sync(0xffffffffu, m, 4 * gi + k);
+    }
+    __syncthreads();
+    // M -= F U on the tensor pipe
+    const double a = -sm.F[par][row][t];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dmma_8x8x4(c[j][0], c[j][1], a, sm.U[t][8 * j + g]);
+    // pivot rows <- U (Mi on the pivot block)
+    if (warp == pw && g >= g0 && g < g0 + 4) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = 8 * j + 2 * t + h;
+          c[j][h] = (col >= p && col < p + 4) ? mp[h] : sm.U[g - g0][col];
+        }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int col = 8 * j + 2 * t + h;
+      if (row < w && col < w) out[(long long)row * ldo + col] = c[j][h];
+    }
+  const bool failed = sm.bad != 0;
+  __syncthreads();
+  return failed;
+}
 
 }  // namespace bddc
