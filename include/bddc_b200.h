@@ -42,6 +42,16 @@ enum {
 
 /* ---- local.cu : substructuring -------------------------------------------- */
 
+/* Symbolic plan, element part: local dof index (interior first, then the
+ * glob-major interface block, 2^30 for Dirichlet nodes) of every corner of
+ * the rank's elements (input order); sub_of holds global subdomain ids, nI is
+ * indexed by local subdomain (global - s0).
+ * replaces the pos/loc maps of build_subdomain_operator substructuring.py:98-101. */
+int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_elements, int s0,
+                   const int* iloc_of_node, const int* glob_of_node, const int* pos_in_glob,
+                   const int* sh_start, const int* sh_sub, const int* sh_boff,
+                   const long long* nI, int* loc4, cudaStream_t stream);
+
 /* Dense local matrix [I|B] x [I|B|f] from element blocks with Dirichlet lifting.
  * replaces substructuring.py:98-114 (COO->CSR assembly, load, lifting). */
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,

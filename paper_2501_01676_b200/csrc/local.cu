@@ -36,7 +36,7 @@ __global__ void assemble_kernel(double* __restrict__ base, const long long* __re
   double* M = base + off[b];
   int li[4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a) li[a] = loc4[j * 4 + a];
+  for (int a = 0; a < 4; ++a) li[a] = loc4[e * 4 + a];
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int r = li[a];
@@ -51,6 +51,39 @@ __global__ void assemble_kernel(double* __restrict__ base, const long long* __re
         fr -= v * gdir[conn[e * 4 + c]];
     }
     atomicAdd(M + (long long)r * L + nL, fr);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// symbolic plan: element-local dof index of every element corner
+//   interior node      -> its interior index (iloc_of_node)
+//   interface node     -> nI[s] + block offset of its glob in s + position in glob
+//   Dirichlet / absent -> 2^30
+// ---------------------------------------------------------------------------
+__global__ void plan_loc4_kernel(const long long* __restrict__ conn,
+                                 const long long* __restrict__ sub_of, long long n_corners,
+                                 int s0, const int* __restrict__ iloc_of_node,
+                                 const int* __restrict__ glob_of_node,
+                                 const int* __restrict__ pos_in_glob,
+                                 const int* __restrict__ sh_start, const int* __restrict__ sh_sub,
+                                 const int* __restrict__ sh_boff, const long long* __restrict__ nI,
+                                 int* __restrict__ loc4) {
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n_corners;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long nd = conn[idx];
+    const int il = iloc_of_node[nd];
+    if (il >= 0) {
+      loc4[idx] = il;
+      continue;
+    }
+    int v = 1 << 30;
+    const int g = glob_of_node[nd];
+    if (g >= 0) {
+      const int s = (int)sub_of[idx >> 2];
+      for (int k = sh_start[g]; k < sh_start[g + 1]; ++k)
+        if (sh_sub[k] == s) v = (int)nI[s - s0] + sh_boff[k] + pos_in_glob[nd];
+    }
+    loc4[idx] = v;
   }
 }
 
@@ -359,6 +392,19 @@ static int launch_status() {
 }
 
 extern "C" {
+
+int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_elements, int s0,
+                   const int* iloc_of_node, const int* glob_of_node, const int* pos_in_glob,
+                   const int* sh_start, const int* sh_sub, const int* sh_boff,
+                   const long long* nI, int* loc4, cudaStream_t stream) {
+  if (n_elements <= 0) return 0;
+  const long long nc = 4 * n_elements;
+  const int grid = (int)((nc + 255) / 256 < 148 * 16 ? (nc + 255) / 256 : 148 * 16);
+  plan_loc4_kernel<<<grid, 256, 0, stream>>>(conn, sub_of, nc, s0, iloc_of_node, glob_of_node,
+                                             pos_in_glob, sh_start, sh_sub, sh_boff, nI, loc4);
+  bddc_note_launches(1);
+  return launch_status();
+}
 
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
                         const long long* elem_start, const long long* elem_ids, const int* loc4,

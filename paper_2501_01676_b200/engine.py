@@ -46,16 +46,26 @@ def _allreduce(comm, *ts):
             comm.allreduce_(t)
 
 
+def _upload(a, dt):
+    """Host array -> device without a host/device sync: staged through torch's
+    caching pinned allocator and copied asynchronously on the current stream
+    (a pageable .cuda() would wait for all queued kernels first)."""
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
+    if t.numel() == 0:
+        return torch.empty(t.shape, dtype=t.dtype, device="cuda")
+    return t.pin_memory().cuda(non_blocking=True)
+
+
 def dev_i32(a):
-    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()
+    return _upload(a, np.int32)
 
 
 def dev_i64(a):
-    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.int64)).cuda()
+    return _upload(a, np.int64)
 
 
 def dev_f64(a):
-    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+    return _upload(a, np.float64)
 
 
 class PhaseTimer:

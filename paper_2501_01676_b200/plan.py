@@ -43,6 +43,16 @@ def _ranges(starts, counts):
     return rep + np.arange(total, dtype=np.int64)
 
 
+def _up(a, dv):
+    """Host array -> device, asynchronously through pinned staging."""
+    import torch
+
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if t.numel() == 0:
+        return torch.empty(t.shape, dtype=t.dtype, device=dv)
+    return t.pin_memory().to(dv, non_blocking=True)
+
+
 def _excl(a):
     a = np.asarray(a, dtype=np.int64)
     out = np.zeros(a.size + 1, dtype=np.int64)
@@ -110,6 +120,7 @@ class Plan:
         self.nB = np.bincount(pair_sub, weights=sizes_k, minlength=N).astype(np.int64)
         self.voff = _excl(self.nB)
         gnodes = f["nodes"]
+        self._gnodes = gnodes
         gstart = _excl(self.gsize)
         self.B_nodes = gnodes[_ranges(gstart[self.sub_globs], sizes_k)]
         self.pos2k = np.repeat(np.arange(self.sub_globs.size, dtype=np.int32), sizes_k)
@@ -148,8 +159,9 @@ class Plan:
     def _interface_maps_torch(self, dv):
         import torch
 
-        Bn = torch.from_numpy(self.B_nodes).to(dv)
-        ifn = torch.from_numpy(self._iface_nodes).to(dv)
+        self._node_maps_device(dv)
+        Bn = _up(self.B_nodes, dv)
+        ifn = self._iface_nodes_d
         perm = torch.searchsorted(ifn, Bn)
         self.iface_perm_d = perm.to(torch.int32)
         srt = torch.sort(perm, stable=True)
@@ -183,7 +195,9 @@ class Plan:
         eorder = np.argsort(sub_of, kind="stable")
         self.elem_ids = mine[eorder].astype(np.int64)
         self.elem_start = _excl(np.bincount(sub_of, minlength=N))
-        self.loc4 = self._local_index_numpy(el[eorder], sub_of[eorder])
+        # loc4 is indexed like the element inputs (element id), not by sorted position
+        self.loc4 = np.full((sub_all.size, 4), 2 ** 30, dtype=np.int32)
+        self.loc4[mine] = self._local_index_numpy(el, sub_of)
 
     def _local_index_numpy(self, conn, sub):
         N, n_nodes = self.N, self.n_nodes
@@ -203,45 +217,51 @@ class Plan:
     def _element_part_torch(self, system, partition, dev):
         import torch
 
+        from ._lib import lib, stream
+
         N, n_nodes = self.N, self.n_nodes
-        conn = dev["conn"]                     # (E_local, 4) int64 on the GPU
-        sub_of = dev["sub_of"] - self.owned[0]  # (E_local,) local subdomain ids
+        s0 = self.owned[0]
+        conn = dev["conn"]                 # (E_local, 4) int64 on the GPU, input order
+        sub_g = dev["sub_of"]              # (E_local,) global subdomain ids
+        dv = conn.device
+        sub_of = sub_g - s0
         free = dev.get("free")
         if free is None:
-            free = torch.from_numpy(np.asarray(system.node_to_free) >= 0).to(conn.device)
-        Nk = max(N, 1)
-        key = torch.unique(conn * Nk + sub_of[:, None])
-        node, sub = key // Nk, key % Nk
-        on_iface = torch.zeros(n_nodes, dtype=torch.bool, device=conn.device)
-        on_iface[torch.from_numpy(self._iface_nodes).to(conn.device)] = True
-        interior = free[node] & ~on_iface[node]
-        I_node, I_sub = node[interior], sub[interior]
-        k2 = torch.sort(I_sub * n_nodes + I_node).values
-        I_sub, I_node = k2 // n_nodes, k2 % n_nodes
+            free = _up(np.asarray(system.node_to_free) >= 0, dv)
+        # interior nodes: free, not on the interface, touched by a (single) local
+        # subdomain -- its owner, read off any element containing it
+        owner = torch.full((n_nodes,), -1, dtype=torch.int64, device=dv)
+        owner[conn.reshape(-1)] = sub_of[:, None].expand(-1, 4).reshape(-1)
+        on_iface = torch.zeros(n_nodes, dtype=torch.bool, device=dv)
+        on_iface[self._iface_nodes_d] = True
+        I_all = torch.nonzero(free & ~on_iface & (owner >= 0)).squeeze(1)   # ascending node ids
+        I_sub_all = owner[I_all]
+        o = torch.sort(I_sub_all, stable=True).indices
+        I_node, I_sub = I_all[o], I_sub_all[o]
         nI = torch.bincount(I_sub, minlength=N)
         self.nI = nI.cpu().numpy().astype(np.int64)
         self.ioff = _excl(self.nI)
         self.I_nodes_d = I_node
+        iloc = torch.full((n_nodes,), -1, dtype=torch.int32, device=dv)
+        iloc[I_node] = (torch.arange(I_node.numel(), device=dv) - _up(self.ioff, dv)[I_sub]).to(torch.int32)
         eorder = torch.sort(sub_of, stable=True).indices
         self.elem_ids_d = eorder
         self.elem_start = _excl(torch.bincount(sub_of, minlength=N).cpu().numpy())
-        dv = conn.device
-        Bsub = torch.repeat_interleave(torch.arange(N, device=dv), torch.from_numpy(self.nB).to(dv))
-        voff = torch.from_numpy(self.voff).to(dv)
-        nI_d = nI.to(torch.int64)
-        Bloc = torch.arange(self.B_nodes.size, device=dv) - voff[Bsub] + nI_d[Bsub]
-        Bn = self._B_nodes_d
-        ioff = torch.from_numpy(self.ioff).to(dv)
-        Isub = I_sub
-        Iloc = torch.arange(I_node.numel(), device=dv) - ioff[Isub]
-        keys = torch.cat([Bsub * n_nodes + Bn, Isub * n_nodes + I_node])
-        vals = torch.cat([Bloc, Iloc])
-        keys, ko = torch.sort(keys)
-        vals = vals[ko]
-        q = sub_of[eorder][:, None] * n_nodes + conn[eorder]
-        pos = torch.clamp(torch.searchsorted(keys, q.reshape(-1)), max=keys.numel() - 1).reshape(q.shape)
-        found = keys[pos] == q
-        self.loc4_d = torch.where(found, vals[pos], torch.full_like(pos, 2 ** 30)).to(torch.int32)
+        self.loc4_d = torch.empty((conn.shape[0], 4), dtype=torch.int32, device=dv)
+        lib.bddc_plan_loc4(conn, sub_g, conn.shape[0], s0, iloc, self._glob_of_node_d,
+                           self._pos_in_glob_d, _up(self.sh_start, dv), _up(self.sh_sub, dv),
+                           _up(self.sh_boff, dv), nI.to(torch.int64), self.loc4_d, stream())
+
+    def _node_maps_device(self, dv):
+        """node -> glob index and position in the glob (-1 off the interface)."""
+        gnodes = self._gnodes
+        gof = np.full(self.n_nodes, -1, dtype=np.int32)
+        pos = np.zeros(self.n_nodes, dtype=np.int32)
+        gof[gnodes] = np.repeat(np.arange(self.G, dtype=np.int32), self.gsize)
+        pos[gnodes] = (np.arange(gnodes.size) - np.repeat(_excl(self.gsize)[:-1], self.gsize)).astype(np.int32)
+        self._glob_of_node_d = _up(gof, dv)
+        self._pos_in_glob_d = _up(pos, dv)
+        self._iface_nodes_d = _up(self._iface_nodes, dv)
 
     def _layout(self):
         self.nL = self.nI + self.nB

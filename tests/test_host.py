@@ -71,7 +71,7 @@ def test_plan_local_numbering(name):
         e0, e1 = p.elem_start[i], p.elem_start[i + 1]
         ids = p.elem_ids[e0:e1]
         order = np.concatenate([ref_I, B])
-        loc = p.loc4[e0:e1]
+        loc = p.loc4[ids]
         conn = el[ids]
         inside = loc < p.nL[i]
         assert np.array_equal(order[loc[inside]], conn[inside])
