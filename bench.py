@@ -313,8 +313,19 @@ def run_mine(args):
     nB = plan.nB.astype(np.int64)
     op_bytes = 8 * int((nB * nB).sum()) + 8 * (3 * int(nB.sum()) + plan.n_hat)
     npn = pc.np_sub.astype(np.int64)
-    pc_bytes = 8 * int((nB * nB).sum() + 2 * (npn * nB).sum()) + 8 * (6 * int(nB.sum()) + 4 * plan.n_hat) \
-        + 8 * pc.n_primal * pc.n_primal
+    nd = nB - npn
+    slot_ng2 = int((plan.gsize[plan.sub_globs].astype(np.int64) ** 2).sum())
+    # SURVEY 8(d) B_apply_local (dual LU, Phi/primal rows, (Q D) glob blocks at both
+    # ends, vectors) + the coarse block-inverse operators read by the coarse solve
+    pc_local_bytes = 8 * int((nd * nd).sum() + 2 * (nd * npn).sum() + 2 * slot_ng2) \
+        + 8 * (6 * int(nB.sum()) + 4 * plan.n_hat)
+    pc_bytes = pc_local_bytes + pc.coarse_factor_bytes
+    a0.record()
+    for _ in range(reps):
+        pc.coarse_solve(pc.rp, pc.up)
+    a1.record()
+    torch.cuda.synchronize()
+    coarse_ms = a0.elapsed_time(a1) / reps
     del keep, pc, op
 
     # e2e through the host API: the problem's inputs live in page-locked host
@@ -371,6 +382,10 @@ def run_mine(args):
             "hbm_peak_GBps": hbm, "hbm_peak_source": hbm_src,
             "interface_operator_frac": op_bytes / (op_ms * 1e-3) / 1e9 / hbm,
             "preconditioner_frac": pc_bytes / (pc_ms * 1e-3) / 1e9 / hbm,
+            "preconditioner_bytes": pc_bytes,
+            "coarse_solve_ms": coarse_ms, "coarse_operator_bytes": pc.coarse_factor_bytes,
+            "bytes_formula": "SURVEY 8(d) B_apply_local + coarse block-inverse operator bytes; "
+                             "B_op = 8 sum nB^2 + 8 (3 sum nB + n_hat)",
         },
         "phases_ms": phases,
         "iterations": res.iterations, "converged": bool(res.converged),

@@ -320,6 +320,33 @@ int bddc_coarse_solve_flow(const double* A, long long ld, int n, const double* p
                            long long pinv_step_stride, const int* jmin, const int* jmax, double* b,
                            double* t, int* flags, int epoch, cudaStream_t stream);
 
+/* ---- coarse.cu : block-inverse coarse solve --------------------------------- */
+
+/* Build the block-inverse solve operators from the factors of
+ * bddc_coarse_factor (A, ld, pinv as left by it).  Rows are grouped in blocks
+ * of 512; for block D (rows [512 D, 512 D + h)):
+ *   F_D = Linv_DD [L_(D, cl[D]:512 D) | I_h]       h x ldF, at foff[D]
+ *   G_D = Uinv_DD [P_D | W_(D, 512 D + h:cu[D])]    h x ldG, at goff[D]
+ * ldF = (512 D - cl[D]) + roundup2(h), ldG = roundup2(cu[D] - 512 D); cl[D]
+ * (64-aligned) is the first column of L coupled to the block, cu[D] the end
+ * of its U coupling (device arrays; engine.coarse_blockinv_layout).  max_ldf /
+ * max_ldg: largest ldF / ldG.  Part of replacing lu_factor(coarse) solver.py:123. */
+int bddc_coarse_blockinv(const double* A, long long ld, int n, const double* pinv,
+                         long long pinv_step_stride, int nD, const int* cl, const int* cu,
+                         const long long* foff, const long long* goff, int max_ldf, int max_ldg,
+                         double* F, double* G, cudaStream_t stream);
+
+/* x = C^-1 b with the operators of bddc_coarse_blockinv: 2 nD dependent
+ * row-parallel GEMV steps in one cooperative launch (128 CTAs).  z: n doubles
+ * of scratch (the forward result); counters: 2 nD ints zeroed once, epoch:
+ * 1, 2, 3, ... on successive calls with the same counters (reset counters and
+ * restart at 1 before epoch * 128 overflows).  replaces lu_solve(coarse_lu)
+ * solver.py:192. */
+int bddc_coarse_solve_blockinv(const double* F, const double* G, int n, int nD, const int* cl,
+                               const int* cu, const long long* foff, const long long* goff,
+                               const double* b, double* z, double* x, int* counters, int epoch,
+                               cudaStream_t stream);
+
 /* ---- krylov.cu : GMRES vector kernels (solver.py:286-310) ------------------ */
 
 int bddc_multi_dot(const double* V, long long n, int m, const double* w, double* h,

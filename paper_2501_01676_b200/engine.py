@@ -648,6 +648,23 @@ def coarse_ordering(pgid, np_sub, n_c):
     return order, new_id, lim.astype(np.int32), first.astype(np.int32)
 
 
+def coarse_blockinv_layout(lim, n_c, block=512):
+    """Row blocks of the block-inverse coarse solve (coarse.cu): per block D
+    (rows [D*block, D*block + h)) the first coupled column cl (first 64-panel
+    whose L' reaches the block), the end of its U coupling cu, and the offsets
+    of F_D (h x ldF) and G_D (h x ldG)."""
+    lim = np.asarray(lim, dtype=np.int64)
+    nD = (n_c + block - 1) // block
+    DB = np.arange(nD, dtype=np.int64) * block
+    h = np.minimum(block, n_c - DB)
+    cl = np.minimum(64 * np.searchsorted(lim, DB, side="right"), DB)
+    cu = np.maximum(lim[(DB + h - 1) // 64], DB + h)
+    ldF = (DB - cl) + ((h + 1) & ~1)
+    ldG = ((cu - DB) + 1) & ~1
+    return dict(nD=int(nD), cl=cl, cu=cu, foff=_excl(h * ldF), goff=_excl(h * ldG),
+                max_ldf=int(ldF.max()), max_ldg=int(ldG.max()))
+
+
 class DevicePreconditioner:
     """M^-1 = sum_i R_i^T (A_i R_i + N_i P_i C^-1 sum_j P_j^T G_j R_j)
     (reference BddcPreconditioner solver.py:46-209, see precond.cu)."""
@@ -771,17 +788,6 @@ class DevicePreconditioner:
         self._lim_c = (ctypes.c_int * steps)(*self.lim.tolist())
         self._first_c = (ctypes.c_int * steps)(*self.first.tolist())
         self.d_lim, self.d_first = dev_i32(self.lim), dev_i32(self.first)
-        # super-panel (128-row) dependency ranges for the dataflow solve
-        nq = (nc + 127) // 128
-        lim64 = self.lim.astype(np.int64)
-        lsup = np.array([lim64[min(2 * q + 1, lim64.size - 1)] for q in range(nq)], dtype=np.int64)
-        lsup = np.maximum.accumulate(lsup)
-        q_idx = np.arange(nq, dtype=np.int64)
-        jmin = np.minimum(np.searchsorted(lsup, 128 * q_idx, side="right"), q_idx)
-        jmax = np.maximum((lsup - 1) // 128, q_idx)
-        self.d_jmin, self.d_jmax = dev_i32(jmin), dev_i32(jmax)
-        self.flow_flags = torch.zeros(2 * nq, dtype=torch.int32, device="cuda")
-        self.flow_epoch = 0
         lib.bddc_coarse_factor(C, dev_i64([0]), dev_i32([nc]), dev_i32([nc]), nc,
                                ctypes.cast(self._lim_c, ctypes.c_void_p), self.coarse_pinv, piv,
                                status1, st)
@@ -794,13 +800,27 @@ class DevicePreconditioner:
             gid = ls.globs.glob_id(ls.globs.globs[gi])
             raise NumericalError(f"coarse matrix is singular at primal dof {bad} "
                                  f"(glob {gid}, constraint {bad - go[gi]})")
+        # block-inverse solve operators (coarse.cu); the dense factor is not kept
+        lay = coarse_blockinv_layout(self.lim, nc)
+        self.cb_nD = lay["nD"]
+        self.cb_cl, self.cb_cu = dev_i32(lay["cl"]), dev_i32(lay["cu"])
+        self.cb_foff, self.cb_goff = dev_i64(lay["foff"][:-1]), dev_i64(lay["goff"][:-1])
+        self.cb_F = torch.empty(max(int(lay["foff"][-1]), 1), dtype=F64, device="cuda")
+        self.cb_G = torch.empty(max(int(lay["goff"][-1]), 1), dtype=F64, device="cuda")
+        lib.bddc_coarse_blockinv(C, nc, nc, self.coarse_pinv, 4096, self.cb_nD, self.cb_cl,
+                                 self.cb_cu, self.cb_foff, self.cb_goff, lay["max_ldf"],
+                                 lay["max_ldg"], self.cb_F, self.cb_G, st)
+        self.cb_cnt = torch.zeros(2 * self.cb_nD, dtype=torch.int32, device="cuda")
+        self.cb_epoch = 0
+        self.cb_z = torch.empty(nc, dtype=F64, device="cuda")
+        self.coarse_factor_bytes = 8 * (int(lay["foff"][-1]) + int(lay["goff"][-1]))
+        del C, self.coarse_lu, self.coarse_pinv
         self.y = torch.empty(int(p.voff[-1]), dtype=F64, device="cuda")
         self.cvals = torch.empty(max(self.sum_np, 1), dtype=F64, device="cuda")
         self.rp = torch.empty(nc, dtype=F64, device="cuda")
         self.up = torch.empty(nc, dtype=F64, device="cuda")
 
     use_graph = False  # re-captured per preconditioner: costs more than it saves here
-    coarse_flow = True  # dataflow coarse solve (flags) instead of one grid barrier per panel
 
     def apply_device(self, r, out=None):
         """M^-1 r.  The launch sequence (local GEMVs, coarse gather, the
@@ -839,19 +859,24 @@ class DevicePreconditioner:
                                 self.cvals, p.N, nbmax, st)
         lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp, self.n_primal, st)
         _allreduce(self.comm, self.rp)
-        if self.coarse_flow:
-            self.flow_epoch = self.flow_epoch % 2000000000 + 1
-            lib.bddc_coarse_solve_flow(self.coarse_lu, self.n_primal, self.n_primal,
-                                       self.coarse_pinv, 4096, self.d_jmin, self.d_jmax, self.rp,
-                                       self.up, self.flow_flags, self.flow_epoch, st)
-        else:
-            lib.bddc_coarse_solve(self.coarse_lu, self.n_primal, self.n_primal, self.coarse_pinv,
-                                  4096, self.d_lim, self.d_first, self.rp, self.up, st)
+        self.coarse_solve(self.rp, self.up)
         lib.bddc_prolong_primal(d.nB, d.voff, self.d_pstart, self.d_pgid, self.d_poff, self.Nt,
                                 self.up, self.y, p.N, st)
         lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n_hat, st)
         _allreduce(self.comm, out)
         return out
+
+    def coarse_solve(self, b, x):
+        """x = C^-1 b (reference lu_solve(coarse_lu) solver.py:192) through the
+        block-inverse operators, one cooperative launch."""
+        self.cb_epoch += 1
+        if self.cb_epoch >= 1 << 24:  # counters = epoch * chunks: restart before overflow
+            self.cb_cnt.zero_()
+            self.cb_epoch = 1
+        lib.bddc_coarse_solve_blockinv(self.cb_F, self.cb_G, self.n_primal, self.cb_nD, self.cb_cl,
+                                       self.cb_cu, self.cb_foff, self.cb_goff, b, self.cb_z, x,
+                                       self.cb_cnt, self.cb_epoch, stream())
+        return x
 
     def apply(self, r):
         """M^-1 r on nodal interface vectors (numpy or device tensor)."""

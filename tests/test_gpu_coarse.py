@@ -1,4 +1,4 @@
-"""Coarse envelope LU and both solve kernels (grid-barrier and dataflow)
+"""Coarse envelope LU and the solve kernels (grid-barrier, dataflow, block-inverse)
 against a dense solve, on a coarse matrix with the structure the
 preconditioner builds (subdomain cliques of primal dofs, reverse
 Cuthill-McKee order, many 128-row super-panels)."""
@@ -16,7 +16,8 @@ def test_coarse_solves_match_dense(n_sub, seed):
     import torch
 
     from paper_2501_01676_b200._lib import lib, stream
-    from paper_2501_01676_b200.engine import coarse_ordering, dev_i32, dev_i64
+    from paper_2501_01676_b200.engine import (coarse_blockinv_layout, coarse_ordering, dev_i32,
+                                              dev_i64)
 
     rng = np.random.default_rng(seed)
     # chain of subdomains, each sharing primal dofs with its neighbours
@@ -73,8 +74,28 @@ def test_coarse_solves_match_dense(n_sub, seed):
         assert e2 <= 1e-12, e2
     e1 = np.linalg.norm(x1.cpu().numpy() - x_ref) / np.linalg.norm(x_ref)
     assert e1 <= 1e-12, e1
+    # block-inverse operators (coarse.cu), three successive solves (epochs)
+    lay = coarse_blockinv_layout(lim, n)
+    F = torch.empty(int(lay["foff"][-1]), dtype=torch.float64, device="cuda")
+    G = torch.empty(int(lay["goff"][-1]), dtype=torch.float64, device="cuda")
+    cl, cu = dev_i32(lay["cl"]), dev_i32(lay["cu"])
+    foff, goff = dev_i64(lay["foff"][:-1]), dev_i64(lay["goff"][:-1])
+    assert lib.bddc_coarse_blockinv(Cd, n, n, pinv, 4096, lay["nD"], cl, cu, foff, goff,
+                                    lay["max_ldf"], lay["max_ldg"], F, G, st) == 0
+    cnt = torch.zeros(2 * lay["nD"], dtype=torch.int32, device="cuda")
+    zb = torch.empty(n, dtype=torch.float64, device="cuda")
+    for epoch in (1, 2, 3):
+        rhs = rng.standard_normal(n)
+        x3 = torch.empty(n, dtype=torch.float64, device="cuda")
+        assert lib.bddc_coarse_solve_blockinv(F, G, n, lay["nD"], cl, cu, foff, goff,
+                                              torch.from_numpy(rhs).cuda(), zb, x3, cnt, epoch,
+                                              st) == 0
+        torch.cuda.synchronize()
+        xr = np.linalg.solve(C, rhs)
+        e3 = np.linalg.norm(x3.cpu().numpy() - xr) / np.linalg.norm(xr)
+        assert e3 <= 1e-12, (epoch, e3)
     # timing (informational)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     ev[0].record()
     for _ in range(10):
         lib.bddc_coarse_solve(Cd, n, n, pinv, 4096, dev_i32(lim), dev_i32(first), rb, x1, st)
@@ -83,6 +104,12 @@ def test_coarse_solves_match_dense(n_sub, seed):
         lib.bddc_coarse_solve_flow(Cd, n, n, pinv, 4096, dev_i32(jmin), dev_i32(jmax), rb2, x2,
                                    flags, 10 + e, st)
     ev[2].record()
+    for e in range(10):
+        lib.bddc_coarse_solve_blockinv(F, G, n, lay["nD"], cl, cu, foff, goff, rb2, zb, x3, cnt,
+                                       4 + e, st)
+    ev[3].record()
     torch.cuda.synchronize()
-    print(f"n={n}: barrier solve {ev[0].elapsed_time(ev[1]) / 10:.3f} ms, "
-          f"dataflow solve {ev[1].elapsed_time(ev[2]) / 10:.3f} ms")
+    print(f"n={n} (nD={lay['nD']}, F+G {8 * (lay['foff'][-1] + lay['goff'][-1]) / 1e6:.1f} MB): "
+          f"barrier solve {ev[0].elapsed_time(ev[1]) / 10:.3f} ms, "
+          f"dataflow solve {ev[1].elapsed_time(ev[2]) / 10:.3f} ms, "
+          f"block-inverse solve {ev[2].elapsed_time(ev[3]) / 10:.3f} ms")
