@@ -319,7 +319,8 @@ def run_mine(args):
     # ends, vectors) + the coarse block-inverse operators read by the coarse solve
     pc_local_bytes = 8 * int((nd * nd).sum() + 2 * (nd * npn).sum() + 2 * slot_ng2) \
         + 8 * (6 * int(nB.sum()) + 4 * plan.n_hat)
-    pc_bytes = pc_local_bytes + pc.coarse_factor_bytes
+    coarse_bytes = pc.coarse_factor_bytes
+    pc_bytes = pc_local_bytes + coarse_bytes
     a0.record()
     for _ in range(reps):
         pc.coarse_solve(pc.rp, pc.up)
@@ -383,7 +384,7 @@ def run_mine(args):
             "interface_operator_frac": op_bytes / (op_ms * 1e-3) / 1e9 / hbm,
             "preconditioner_frac": pc_bytes / (pc_ms * 1e-3) / 1e9 / hbm,
             "preconditioner_bytes": pc_bytes,
-            "coarse_solve_ms": coarse_ms, "coarse_operator_bytes": pc.coarse_factor_bytes,
+            "coarse_solve_ms": coarse_ms, "coarse_operator_bytes": coarse_bytes,
             "bytes_formula": "SURVEY 8(d) B_apply_local + coarse block-inverse operator bytes; "
                              "B_op = 8 sum nB^2 + 8 (3 sum nB + n_hat)",
         },

@@ -24,8 +24,78 @@
 #include "common.cuh"
 #include "bddc_b200.h"
 #include "tile_mma.cuh"
+#include "reg_gj.cuh"
 
 namespace bddc {
+
+// ---------------------------------------------------------------------------
+// Envelope LU (no pivoting) in 64-wide panels with a one-panel lookahead.
+// Per panel k: [W = P_k A12 row tiles + L' = A21 P_(k-1) of the previous
+// panel] in one launch, then [A22 -= A21 W, with CTA 0 updating the next
+// diagonal block first and inverting it: P_(k+1)] in a second launch, so the
+// pivot inverse and the column scaling leave the critical path.
+// ---------------------------------------------------------------------------
+union CoarseFactorSmem {
+  TileSmem tile;
+  MmaGjSmem gj;
+};
+
+BDDC_DEV void coarse_pivot(double* M, int n, int k, double* pinv, double* piv_out, int* status,
+                           CoarseFactorSmem& sm) {
+  const int w = min(kTile, n - k);
+  const bool bad = reg_gj64(M + (long long)k * n + k, n, w, pinv + (long long)(k / kTile) * kTile * kTile,
+                            kTile, 0, piv_out + k, sm.gj);
+  if (threadIdx.x == 0 && bad && status) atomicCAS(status, 0, (int)kSingularPivot);
+}
+
+__global__ void __launch_bounds__(kTileThreads) coarse_pivot_kernel(double* M, int n, int k,
+                                                                    double* pinv, double* piv_out,
+                                                                    int* status) {
+  extern __shared__ __align__(16) unsigned char cf_raw[];
+  coarse_pivot(M, n, k, pinv, piv_out, status, *reinterpret_cast<CoarseFactorSmem*>(cf_raw));
+}
+
+// blocks [0, trow): W row tiles of panel k (cols [k + w, lim));
+// blocks [trow, ...): L' = A21 P_kp on rows [kp + 64, limp) of panel kp = k - 64
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) coarse_row_scale_kernel(
+    double* M, int n, int k, int lim, int trow, int limp, const double* pinv) {
+  extern __shared__ __align__(16) unsigned char cf_raw[];
+  TileSmem& sm = reinterpret_cast<CoarseFactorSmem*>(cf_raw)->tile;
+  const int w = min(kTile, n - k);
+  if ((int)blockIdx.x < trow) {
+    const int c0 = k + w + blockIdx.x * kTile;
+    if (c0 >= lim) return;
+    double* C = M + (long long)k * n + c0;
+    tile_mma(C, n, w, min(kTile, lim - c0), pinv + (long long)(k / kTile) * kTile * kTile, kTile, C,
+             n, w, 1.0, 0.0, sm);
+  } else {
+    const int kp = k - kTile;
+    const int r0 = k + (blockIdx.x - trow) * kTile;
+    if (kp < 0 || r0 >= limp) return;
+    double* C = M + (long long)r0 * n + kp;
+    tile_mma(C, n, min(kTile, limp - r0), kTile, C, n, pinv + (long long)(kp / kTile) * kTile * kTile,
+             kTile, kTile, 1.0, 0.0, sm);
+  }
+}
+
+// A22 -= A21 W over [k + w, lim)^2; CTA 0 owns the next diagonal block and
+// inverts it right after its update (next != 0)
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) coarse_trail_pivot_kernel(
+    double* M, int n, int k, int lim, int next, double* pinv, double* piv_out, int* status) {
+  extern __shared__ __align__(16) unsigned char cf_raw[];
+  CoarseFactorSmem& sm = *reinterpret_cast<CoarseFactorSmem*>(cf_raw);
+  const int w = min(kTile, n - k);
+  const int s = k + w;
+  const int tn_count = (lim - s + kTile - 1) / kTile;
+  const int tm = blockIdx.x / tn_count, tn = blockIdx.x - tm * tn_count;
+  const int r0 = s + tm * kTile, c0 = s + tn * kTile;
+  tile_mma(M + (long long)r0 * n + c0, n, min(kTile, lim - r0), min(kTile, lim - c0),
+           M + (long long)r0 * n + k, n, M + (long long)k * n + c0, n, w, -1.0, 1.0, sm.tile);
+  if (blockIdx.x == 0 && next) {
+    __syncthreads();  // the updated diagonal block is in memory; smem reused
+    coarse_pivot(M, n, s, pinv, piv_out, status, sm);
+  }
+}
 
 constexpr int kCB = 512;            // rows per block (multiple of 64)
 constexpr int kCRC = 4;             // rows per CTA per block
@@ -282,6 +352,57 @@ __global__ void __launch_bounds__(kCThreads, 1) coarse_blk_solve_kernel(
 using namespace bddc;
 
 extern "C" {
+
+int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const int* nv, int n,
+                       const int* host_lim, double* pinv, double* piv_out, int* status,
+                       cudaStream_t stream) {
+  (void)ldv;
+  (void)nv;
+  if (n <= 0) return 0;
+  const int smem = (int)sizeof(CoarseFactorSmem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(coarse_pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(coarse_row_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(coarse_trail_pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         smem);
+    attr = true;
+  }
+  long long off0 = 0;
+  cudaMemcpyAsync(&off0, off, sizeof(long long), cudaMemcpyDeviceToHost, stream);
+  cudaStreamSynchronize(stream);
+  double* M = C + off0;
+  int launches = 1;
+  coarse_pivot_kernel<<<1, kTileThreads, smem, stream>>>(M, n, 0, pinv, piv_out, status);
+  int limp = 0;  // envelope end of the previous panel (its L' still to scale)
+  for (int k = 0; k < n; k += kTile) {
+    const int w = min(kTile, n - k);
+    const int lim = min(n, host_lim[k / kTile]);
+    const int span = lim - k - w;
+    const int trow = span > 0 ? ceil_div(span, kTile) : 0;
+    const int tsc = (k > 0 && limp > k) ? ceil_div(limp - k, kTile) : 0;
+    if (trow + tsc > 0) {
+      coarse_row_scale_kernel<<<trow + tsc, kTileThreads, smem, stream>>>(M, n, k, lim, trow, limp,
+                                                                          pinv);
+      ++launches;
+    }
+    const int next = k + w < n;
+    if (span > 0) {
+      const int t = ceil_div(span, kTile);
+      coarse_trail_pivot_kernel<<<t * t, kTileThreads, smem, stream>>>(M, n, k, lim, next, pinv,
+                                                                       piv_out, status);
+      ++launches;
+    } else if (next) {
+      coarse_pivot_kernel<<<1, kTileThreads, smem, stream>>>(M, n, k + w, pinv, piv_out, status);
+      ++launches;
+    }
+    limp = span > 0 ? lim : 0;
+  }
+  // the last panel has no rows below it (k + w == n): nothing left to scale
+  bddc_note_launches(launches);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -(int)e;
+}
 
 int bddc_coarse_blockinv(const double* A, long long ld, int n, const double* pinv,
                          long long pinv_step_stride, int nD, const int* cl, const int* cu,

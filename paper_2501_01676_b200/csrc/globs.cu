@@ -12,6 +12,33 @@
 #include "reg_gj.cuh"
 #include "glob_layout.h"
 
+// Optional phase profile (tools/prof_globs.py builds a -DBDDC_PROF variant):
+// thread 0 of every CTA adds the clock64 cycles of each phase into g_prof.
+#ifdef BDDC_PROF
+__device__ unsigned long long g_prof[64];
+#define PROF_INIT long long _tp = clock64();
+#define PROF(i)                                                                \
+  do {                                                                         \
+    if (threadIdx.x == 0) {                                                    \
+      long long _t = clock64();                                                \
+      atomicAdd(&g_prof[i], (unsigned long long)(_t - _tp));                   \
+      _tp = _t;                                                                \
+    }                                                                          \
+  } while (0)
+extern "C" int bddc_prof_read(unsigned long long* host, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(host, g_prof, sizeof(unsigned long long) * 64);
+  if (reset) {
+    unsigned long long z[64] = {0};
+    cudaMemcpyToSymbol(g_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#else
+#define PROF_INIT
+#define PROF(i)
+#endif
+
 namespace bddc {
 
 struct GlobTables {
@@ -615,12 +642,14 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   const double* Bi = t.BsC + t.sh_doff[k0];
   const double* Bj = t.BsC + t.sh_doff[k0 + 1];
   const int ldi = n, ldj = n;
+  PROF_INIT
   // 1. B_F = sym(Dj^T Bi Dj + Di^T Bj Di)
   blk::gemm(S1, n, Bi, ldi, false, Dj, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(S0, n, Dj, n, true, S1, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(S1, n, Bj, ldj, false, Di, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(S0, n, Di, n, true, S1, n, false, n, n, n, 1.0, 1.0);
   blk::symmetrize(S0, n, n);
+  PROF(0);
   // 2. glob Schur blocks
   int st = glob_schur(t, k0, n, S1, rowbuf);
   if (st) {
@@ -632,6 +661,7 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
     if (threadIdx.x == 0) o.status[g] = 101;
     return;
   }
+  PROF(1);
   // 3. parallel sum Bt = Bti (Bti + Btj)^-1 Btj with the pinv = inv certificate
   for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) S3[idx] = S1[idx] + S2[idx];
   __syncthreads();
@@ -645,6 +675,7 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   blk::gemm(S4, n, S1, n, false, S3, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(S3, n, S4, n, false, S2, n, false, n, n, n, 1.0, 0.0);
   blk::symmetrize(S3, n, n);
+  PROF(2);
   // 4. pencil (B_F, Bt): Cholesky whitening with its certificate
   const double nbt = sqrt(blk::frob2(S3, n, n, n, red));
   const double nb = sqrt(blk::frob2(S0, n, n, n, red));
@@ -652,8 +683,10 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
     if (threadIdx.x == 0) o.status[g] = kNeedFallback;
     return;
   }
+  PROF(3);
   blk::set_identity(S1, n, n, n);
   blk::trsm_lower(S3, n, n, S1, n, n);
+  PROF(4);
   const double nli = blk::frob2(S1, n, n, n, red);
   if (!(nbt * nli < 1e11) || !(theta > 1e-14 * nb)) {
     if (threadIdx.x == 0) o.status[g] = kNeedFallback;
@@ -662,8 +695,11 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   blk::gemm(S2, n, S1, n, false, S0, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(S4, n, S2, n, false, S1, n, true, n, n, n, 1.0, 0.0);
   blk::symmetrize(S4, n, n);
+  PROF(5);
   blk::tridiagonalize(S4, n, n, dd, ee, tau, S2, red);
+  PROF(6);
   blk::tridiag_eigvals(dd, ee, n, w, red);
+  PROF(7);
   double* vals = o.eig + o.eig_off[g];
   __shared__ int s_k;
   if (threadIdx.x == 0) {
@@ -694,8 +730,10 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
     }
     __syncthreads();
   }
+  PROF(8);
   // 6. change of basis from the constraint rows (workspace S2..S4 + vectors)
   const int r = row_space_basis(S1, n, k, n, o.Q + o.q_off[g], S2, cs, perm, red);
+  PROF(9);
   if (threadIdx.x == 0) {
     o.n_sel[g] = k;
     o.r[g] = r;
@@ -919,6 +957,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
   double* T2 = T1 + (long long)Wd * Wd;
   double* scratch = T2 + (long long)Wd * Wd;
 
+  PROF_INIT
   // J_i = [delta_ik I - D_k]_{k=1..ns-1}
   for (int idx = threadIdx.x; idx < ns * ne * nC; idx += blockDim.x) {
     int i = idx / (ne * nC), rem = idx - i * ne * nC;
@@ -937,6 +976,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
     blk::gemm(M, nC, Ji, nC, true, T1, nC, false, nC, nC, ne, 1.0, 1.0);
   }
   blk::symmetrize(M, nC, nC);
+  PROF(16);
   // Bt assembly over (differences, average, priors)
   const int A0 = nC + ne;
   blk::fill(Bt, Wd, Wd, Wd, 0.0);
@@ -994,6 +1034,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
     hcol += h;
   }
   blk::symmetrize(Bt, Wd, Wd);
+  PROF(17);
   // Btt = sym(KK - KR RR^-1 KR^T)
   const int nr = Wd - nC;
   double* RR = T1;   // nr x nr
@@ -1028,6 +1069,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
   }
   __syncthreads();
   blk::symmetrize(Btt, nC, nC);
+  PROF(18);
   // pencil (M, Btt)
   double* vals = o.eig + o.eig_off[g];
   double* vecs = T1;
@@ -1040,6 +1082,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
     if (threadIdx.x == 0) o.status[g] = 200 + st;
     return;
   }
+  PROF(19);
   __shared__ int s_nsel;
   if (threadIdx.x == 0) {
     int c = 0;
@@ -1060,9 +1103,11 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
     rows[perm[j] * nC + c] = s;
   }
   __syncthreads();
+  PROF(20);
   // reshape (nsel x nC) row-major -> (nsel*(ns-1)) x ne and reduce
   const int r = row_space_basis(rows, ne, nsel * (ns - 1), ne, o.Q + o.q_off[g], scratch, cs,
                                 perm, red);
+  PROF(21);
   if (threadIdx.x == 0) {
     o.n_sel[g] = nsel;
     o.r[g] = r;

@@ -509,37 +509,6 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
                               require_positive, piv_out, piv_stride, stream, host_trailing_ms);
 }
 
-// Envelope LU of one n x n matrix (the coarse problem in a bandwidth-reducing
-// order): panel k only updates rows / columns below host_lim[k / 64]; the
-// panel column is stored as L' = A21 P_k (P_k = inverse pivot block, kept in
-// pinv) and the pivot rows as W = P_k A12.  C + off[0] must have ld == n.
-int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const int* nv, int n,
-                       const int* host_lim, double* pinv, double* piv_out, int* status,
-                       cudaStream_t stream) {
-  if (n <= 0) return 0;
-  const int smem = smem_tile_setup();
-  int launches = 0;
-  for (int k = 0; k < n; k += kTile) {
-    const int step = k / kTile;
-    const int w = min(kTile, n - k);
-    const int lim = min(n, host_lim[step]);
-    double* P = pinv + (long long)step * kTile * kTile;
-    pivot_inverse_kernel<<<1, 256, 0, stream>>>(C, off, ldv, nv, k, P, 0, status, 0, piv_out, 0);
-    ++launches;
-    const int span = lim - k - w;
-    if (span > 0) {
-      const int t = ceil_div(span, kTile);
-      const int tr = ceil_div(span, kTrailBM);
-      schur_row_kernel<<<dim3(t, 1), kTileThreads, smem, stream>>>(C, off, ldv, nv, nv, k, P, 0, lim);
-      schur_trailing_kernel<<<dim3(t * tr, 1), kTileThreads, sizeof(TileSmemT<kTrailBM>), stream>>>(C, off, ldv, nv, nv, nv, k, lim, kTile, 0);
-      panel_scale_kernel<<<t, kTileThreads, smem, stream>>>(C, (long long)n, k, w, lim, P);
-      launches += 3;
-    }
-  }
-  bddc_note_launches(launches);
-  return launch_status();
-}
-
 int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n, int nbatch,
                     int max_n, double* pinv_ws, long long pinv_stride, int* status,
                     int require_positive, int symmetric, cudaStream_t stream) {
