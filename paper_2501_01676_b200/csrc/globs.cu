@@ -650,50 +650,101 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   blk::gemm(S0, n, Di, n, true, S1, n, false, n, n, n, 1.0, 1.0);
   blk::symmetrize(S0, n, n);
   PROF(0);
-  // 2. glob Schur blocks
-  int st = glob_schur(t, k0, n, S1, rowbuf);
-  if (st) {
-    if (threadIdx.x == 0) o.status[g] = 100;
-    return;
-  }
-  st = glob_schur(t, k0 + 1, n, S2, rowbuf);
-  if (st) {
-    if (threadIdx.x == 0) o.status[g] = 101;
-    return;
-  }
-  PROF(1);
-  // 3. parallel sum Bt = Bti (Bti + Btj)^-1 Btj with the pinv = inv certificate
-  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) S3[idx] = S1[idx] + S2[idx];
-  __syncthreads();
-  const double fm = blk::frob2(S3, n, n, n, red);
-  if (blk::gj_inverse(S3, n, n, true, rowbuf) ||
-      !(sqrt(fm) * sqrt(blk::frob2(S3, n, n, n, red)) < 1e11)) {
-    if (threadIdx.x == 0) o.status[g] = kNeedFallback;
-    return;
-  }
-  blk::symmetrize(S3, n, n);
-  blk::gemm(S4, n, S1, n, false, S3, n, false, n, n, n, 1.0, 0.0);
-  blk::gemm(S3, n, S4, n, false, S2, n, false, n, n, n, 1.0, 0.0);
-  blk::symmetrize(S3, n, n);
-  PROF(2);
-  // 4. pencil (B_F, Bt): Cholesky whitening with its certificate
-  const double nbt = sqrt(blk::frob2(S3, n, n, n, red));
   const double nb = sqrt(blk::frob2(S0, n, n, n, red));
-  if (!blk::cholesky(S3, n, n)) {
-    if (threadIdx.x == 0) o.status[g] = kNeedFallback;
-    return;
+  const bool lw_lower = t.SC != nullptr && n <= kTile;
+  // whitening Bh = Lw^T B_F Lw with Bt = Lw^-T Lw^-1; the selected vectors are
+  // v = Lw y / sqrt(lambda) (v^T Bt v = 1, the reference's scaling).  lw_lower:
+  // S1 = Lw (lower); otherwise S1 = L^-1 with Bt = L L^T and Lw = (L^-1)^T.
+  if (t.SC != nullptr && n <= kTile) {
+    // 2.-4. The parallel sum's inverse is the sum of the inverses:
+    //   Bt^-1 = Bt_i^-1 + Bt_j^-1 = (Bsym_i^-1)[F,F] + (Bsym_j^-1)[F,F],
+    // so Bt needs no inverse: Bt^-1 = Lw Lw^T (Cholesky) whitens the pencil,
+    // Bh = Lw^T B_F Lw.  Certificates (Frobenius bounds on the extreme
+    // eigenvalues): cond(Bt_i + Bt_j) < 1e11 (the reference's pinv is the
+    // inverse, linalg.py:44-48) and cond(Bt) < 1e11 (no null / degenerate
+    // modes, linalg.py:153); otherwise the general kernel re-runs the face.
+    if (t.sc_status[k0]) {
+      if (threadIdx.x == 0) o.status[g] = 100;
+      return;
+    }
+    if (t.sc_status[k0 + 1]) {
+      if (threadIdx.x == 0) o.status[g] = 101;
+      return;
+    }
+    const double* Xi = t.BiC + t.sh_doff[k0];
+    const double* Xj = t.BiC + t.sh_doff[k0 + 1];
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
+      const int r = idx / n, c = idx - r * n;
+      S1[idx] = 0.5 * ((Xi[idx] + Xi[c * n + r]) + (Xj[idx] + Xj[c * n + r]));
+    }
+    __syncthreads();
+    const double nsi = sqrt(blk::frob2(t.SC + t.sh_doff[k0], n, n, n, red));
+    const double nsj = sqrt(blk::frob2(t.SC + t.sh_doff[k0 + 1], n, n, n, red));
+    const double nxi = sqrt(blk::frob2(Xi, n, n, n, red));
+    const double nxj = sqrt(blk::frob2(Xj, n, n, n, red));
+    const double nx = sqrt(blk::frob2(S1, n, n, n, red));
+    const double cond_m = (nsi + nsj) / (1.0 / nxi + 1.0 / nxj);
+    const double cond_x = nx / (1.0 / nsi + 1.0 / nsj);
+    if (!(nsi > 0.0) || !(nsj > 0.0) || !(nxi > 0.0) || !(nxj > 0.0) ||
+        !(cond_m < 1e11) || !(cond_x < 1e11) || !(theta > 1e-14 * nb) ||
+        !blk::cholesky(S1, n, n)) {
+      if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+      return;
+    }
+    PROF(2);
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
+      const int r = idx / n, c = idx - r * n;
+      if (c > r) S1[idx] = 0.0;
+    }
+    __syncthreads();
+    PROF(3);
+    blk::gemm(S2, n, S0, n, false, S1, n, false, n, n, n, 1.0, 0.0);
+    blk::gemm(S4, n, S1, n, true, S2, n, false, n, n, n, 1.0, 0.0);
+  } else {
+    // 2. glob Schur blocks
+    int st = glob_schur(t, k0, n, S1, rowbuf);
+    if (st) {
+      if (threadIdx.x == 0) o.status[g] = 100;
+      return;
+    }
+    st = glob_schur(t, k0 + 1, n, S2, rowbuf);
+    if (st) {
+      if (threadIdx.x == 0) o.status[g] = 101;
+      return;
+    }
+    PROF(1);
+    // 3. parallel sum Bt = Bti (Bti + Btj)^-1 Btj with the pinv = inv certificate
+    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) S3[idx] = S1[idx] + S2[idx];
+    __syncthreads();
+    const double fm = blk::frob2(S3, n, n, n, red);
+    if (blk::gj_inverse(S3, n, n, true, rowbuf) ||
+        !(sqrt(fm) * sqrt(blk::frob2(S3, n, n, n, red)) < 1e11)) {
+      if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+      return;
+    }
+    blk::symmetrize(S3, n, n);
+    blk::gemm(S4, n, S1, n, false, S3, n, false, n, n, n, 1.0, 0.0);
+    blk::gemm(S3, n, S4, n, false, S2, n, false, n, n, n, 1.0, 0.0);
+    blk::symmetrize(S3, n, n);
+    PROF(2);
+    // 4. pencil (B_F, Bt): Cholesky whitening with its certificate, Lw = L^-T
+    const double nbt = sqrt(blk::frob2(S3, n, n, n, red));
+    if (!blk::cholesky(S3, n, n)) {
+      if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+      return;
+    }
+    PROF(3);
+    blk::set_identity(S1, n, n, n);
+    blk::trsm_lower(S3, n, n, S1, n, n);  // S1 = L^-1
+    const double nli = blk::frob2(S1, n, n, n, red);
+    if (!(nbt * nli < 1e11) || !(theta > 1e-14 * nb)) {
+      if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+      return;
+    }
+    blk::gemm(S2, n, S1, n, false, S0, n, false, n, n, n, 1.0, 0.0);
+    blk::gemm(S4, n, S2, n, false, S1, n, true, n, n, n, 1.0, 0.0);
   }
-  PROF(3);
-  blk::set_identity(S1, n, n, n);
-  blk::trsm_lower(S3, n, n, S1, n, n);
   PROF(4);
-  const double nli = blk::frob2(S1, n, n, n, red);
-  if (!(nbt * nli < 1e11) || !(theta > 1e-14 * nb)) {
-    if (threadIdx.x == 0) o.status[g] = kNeedFallback;
-    return;
-  }
-  blk::gemm(S2, n, S1, n, false, S0, n, false, n, n, n, 1.0, 0.0);
-  blk::gemm(S4, n, S2, n, false, S1, n, true, n, n, n, 1.0, 0.0);
   blk::symmetrize(S4, n, n);
   PROF(5);
   blk::tridiagonalize(S4, n, n, dd, ee, tau, S2, red);
@@ -713,11 +764,14 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   if (k > 0) {
     blk::tridiag_eigvecs(dd, ee, n, w, perm, k, S3, scr, iscr);
     blk::apply_householder(S4, n, n, tau, S3, k, k);
-    // V (S2, n x k) = Li^T X / sqrt(lambda)
+    // V (S2, n x k) = Lw X / sqrt(lambda)
     for (int idx = threadIdx.x; idx < n * k; idx += blockDim.x) {
       const int r = idx / k, q = idx - r * k;
       double s = 0.0;
-      for (int tt = r; tt < n; ++tt) s += S1[tt * n + r] * S3[tt * k + q];
+      if (lw_lower)  // v = Lw y
+        for (int tt = 0; tt <= r; ++tt) s += S1[r * n + tt] * S3[tt * k + q];
+      else           // v = L^-T y
+        for (int tt = r; tt < n; ++tt) s += S1[tt * n + r] * S3[tt * k + q];
       S2[r * k + q] = s / sqrt(fabs(w[perm[q]]));
     }
     __syncthreads();
@@ -933,6 +987,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
                                                        const long long* __restrict__ ws_off,
                                                        const int* __restrict__ edge_ids) {
   extern __shared__ double sh[];
+  __shared__ MmaGjSmem gsm;  // register Gauss-Jordan (reg_gj.cuh) for blocks <= 64
   const int g = edge_ids[blockIdx.x];
   const int ne = t.size[g];
   const int k0 = t.sh_start[g], ns = t.sh_start[g + 1] - k0;
@@ -986,7 +1041,9 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
     const int d = ne + h;
     // X = [[Binv[E,E], PB[:,E]^T], [PB[:,E], XHH]] of this sharer (edge_x_extract)
     blk::copy(X, d, pr.EX + pr.ex_off[k0 + i], d, d, d);
-    int st = blk::gj_inverse(X, d, d, true, rowbuf);
+    // positive pivots <=> SPD: the cho_factor criterion of _invert_principal
+    int st = d <= kTile ? (reg_gj64(X, d, d, X, d, 1, nullptr, gsm) ? (int)kNotPositiveDefinite : 0)
+                        : blk::gj_inverse(X, d, d, true, rowbuf);
     if (st) {
       if (threadIdx.x == 0) o.status[g] = 100 + i;
       return;
@@ -1039,16 +1096,25 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
   const int nr = Wd - nC;
   double* RR = T1;   // nr x nr
   double* Z = T2;    // nr x nC  (RR^-1 KR^T)
-  blk::copy(RR, nr, Bt + (long long)nC * Wd + nC, Wd, nr, nr);
-  for (int idx = threadIdx.x; idx < nr * nC; idx += blockDim.x) {
-    int r = idx / nC, c = idx - r * nC;
-    Z[r * nC + c] = Bt[(long long)c * Wd + nC + r];
-  }
-  __syncthreads();
-  double* Btt = X;   // nC x nC (X no longer needed)
-  if (blk::cholesky(RR, nr, nr)) {
-    blk::chol_solve(RR, nr, nr, Z, nC, nC);
+  bool rr_ok;
+  if (nr <= kTile) {
+    // RR^-1 by register Gauss-Jordan (positive pivots <=> RR SPD, the
+    // cho_factor criterion); Z = RR^-1 KR^T with KR^T = Bt[nC:, :nC]
+    rr_ok = !reg_gj64(Bt + (long long)nC * Wd + nC, Wd, nr, RR, nr, 1, nullptr, gsm);
+    if (rr_ok)
+      blk::gemm(Z, nC, RR, nr, false, Bt + (long long)nC * Wd, Wd, false, nr, nC, nr, 1.0, 0.0);
   } else {
+    blk::copy(RR, nr, Bt + (long long)nC * Wd + nC, Wd, nr, nr);
+    for (int idx = threadIdx.x; idx < nr * nC; idx += blockDim.x) {
+      int r = idx / nC, c = idx - r * nC;
+      Z[r * nC + c] = Bt[(long long)c * Wd + nC + r];
+    }
+    __syncthreads();
+    rr_ok = blk::cholesky(RR, nr, nr);
+    if (rr_ok) blk::chol_solve(RR, nr, nr, Z, nC, nC);
+  }
+  double* Btt = X;   // nC x nC (X no longer needed)
+  if (!rr_ok) {
     // pseudo-inverse fallback (adaptive.py:144-149)
     blk::copy(RR, nr, Bt + (long long)nC * Wd + nC, Wd, nr, nr);
     pinv_sym(RR, nr, scratch, scratch + nr * nr, cs, perm, red);

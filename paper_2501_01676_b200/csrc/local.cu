@@ -275,11 +275,19 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
     return;
   }
   if (symmetric) {  // column panel = +-(row panel)^T: + for processed rows (G_KK), - for G_JK
+    // transposed through shared memory so that both the reads (rows of the
+    // row panel) and the writes (rows of the column panel) are coalesced
     const int h = min(kTile, nb - r0);
     const double sgn = r0 < k ? 1.0 : -1.0;
+    double* st = reinterpret_cast<double*>(smem_raw);  // w x 65 staging tile
+    for (int idx = threadIdx.x; idx < h * w; idx += blockDim.x) {
+      const int c = idx / h, r = idx - c * h;
+      st[c * 65 + r] = M[(long long)(k + c) * L + r0 + r];
+    }
+    __syncthreads();
     for (int idx = threadIdx.x; idx < h * w; idx += blockDim.x) {
       const int r = idx / w, c = idx - r * w;
-      M[(long long)(r0 + r) * L + k + c] = sgn * M[(long long)(k + c) * L + r0 + r];
+      M[(long long)(r0 + r) * L + k + c] = sgn * st[c * 65 + r];
     }
     return;
   }
