@@ -560,16 +560,20 @@ BDDC_DEV void complete_basis(const double* U, int ldu, int r, int n, double* Q, 
 // A[k+2:n, k], scalars in tau[k].  work: 2n doubles.
 BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, double* tau,
                              double* work, double* red) {
+  // Three barriers per Householder step: the column norm and p.v are reduced
+  // redundantly inside every warp (shuffles) instead of with block reductions.
+  (void)red;
   double* v = work;       // n
   double* p = work + n;   // n
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = 0; k < n - 2; ++k) {
     const int m = n - k - 1;  // length of the column below the diagonal
     double ss = 0.0;
-    for (int i = tid(); i < m - 1; i += nth()) {
+    for (int i = lane; i < m - 1; i += 32) {
       const double x = A[(k + 2 + i) * ld + k];
       ss += x * x;
     }
-    ss = block_sum(ss, red);
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     const double alpha = A[(k + 1) * ld + k];
     double t, beta;
     if (ss == 0.0) {
@@ -582,32 +586,39 @@ BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, dou
     const double scal = (ss == 0.0) ? 0.0 : 1.0 / (alpha - beta);
     for (int i = tid(); i < m; i += nth())
       v[i] = (i == 0) ? 1.0 : A[(k + 1 + i) * ld + k] * scal;
-    __syncthreads();
     if (tid() == 0) {
       tau[k] = t;
       e[k] = beta;
     }
+    __syncthreads();
     if (t != 0.0) {
-      // p = t * A22 v   (A22 = A[k+1:, k+1:], symmetric: use full stored block)
-      for (int r = (int)(threadIdx.x >> 5); r < m; r += (int)(blockDim.x >> 5)) {
+      // p = t * A22 v   (A22 = A[k+1:, k+1:], symmetric: use full stored block);
+      // 4 lanes per row, each a strided quarter of the columns (short
+      // dependency chains instead of one warp-wide reduction per row)
+      for (int q0 = 0; q0 < 4 * m; q0 += nth()) {  // uniform trip count: full-warp shuffles
+        const int q = q0 + tid(), r = q >> 2, part = q & 3;
         double s = 0.0;
-        for (int c = (int)(threadIdx.x & 31); c < m; c += 32) s += A[(k + 1 + r) * ld + k + 1 + c] * v[c];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if ((threadIdx.x & 31) == 0) p[r] = t * s;
+        if (q < 4 * m) {
+          const double* ar = A + (k + 1 + r) * ld + k + 1;
+          for (int c = part; c < m; c += 4) s += ar[c] * v[c];
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (q < 4 * m && part == 0) p[r] = t * s;
       }
       __syncthreads();
       double pv = 0.0;
-      for (int i = tid(); i < m; i += nth()) pv += p[i] * v[i];
-      pv = block_sum(pv, red);
+      for (int i = lane; i < m; i += 32) pv += p[i] * v[i];
+      for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
       const double hc = 0.5 * t * pv;
       // w = p - hc v ; A22 -= v w^T + w v^T
       BLK_FOR_RC(m, m) {
         const double wr = p[r] - hc * v[r], wc = p[c] - hc * v[c];
         A[(k + 1 + r) * ld + k + 1 + c] -= v[r] * wc + wr * v[c];
       }
-      __syncthreads();
     }
-    // keep v_k below the subdiagonal for the back-transformation
+    // keep v_k below the subdiagonal for the back-transformation (column k is
+    // outside A22: no conflict with the update)
     for (int i = 1 + tid(); i < m; i += nth()) A[(k + 1 + i) * ld + k] = v[i];
     __syncthreads();
   }
@@ -618,13 +629,25 @@ BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, dou
 }
 
 // Sturm count: number of eigenvalues of T strictly below x.
+// q_i = d_i - x - e_(i-1)^2 / q_(i-1) with |q| >= pivmin (normal numbers):
+// the reciprocal is the MUFU approximation plus two Newton steps (a few ulps,
+// i.e. a relative perturbation of e^2 of that size -- the recurrence stays
+// backward stable; only the signs are used).
+BDDC_DEV double fast_rcp(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  r = fma(r, fma(-q, r, 1.0), r);
+  r = fma(r, fma(-q, r, 1.0), r);
+  return r;
+}
+
 BDDC_DEV int sturm_count(const double* d, const double* e, int n, double x, double pivmin) {
   int cnt = 0;
   double q = d[0] - x;
   if (fabs(q) < pivmin) q = -pivmin;
   if (q < 0.0) ++cnt;
   for (int i = 1; i < n; ++i) {
-    q = d[i] - x - e[i - 1] * e[i - 1] / q;
+    q = d[i] - x - e[i - 1] * e[i - 1] * fast_rcp(q);
     if (fabs(q) < pivmin) q = -pivmin;
     if (q < 0.0) ++cnt;
   }
@@ -764,7 +787,14 @@ BDDC_DEV void tridiag_eigvecs(const double* d, const double* e, int n, const dou
       int* pv = iscratch + threadIdx.x * n;
       const double lam = w[idx[j]] + (j - j0) * 10.0 * tiny;  // separate equal shifts
       for (int i = 0; i < n; ++i) x[i] = 1.0 + 0.37 * sin(1.0 + 0.7 * i + 1.3 * (j - j0));
-      for (int it = 0; it < 5; ++it) {
+      // an isolated eigenvalue (gap > 1e-3 ||T|| to both spectral neighbours,
+      // bisection-accurate shift)
+      // converges to machine precision in two solves; clusters get five
+      const int wi = idx[j];
+      const bool isolated = (j == j0) && (wi == 0 || w[wi] - w[wi - 1] > 1e-3 * tn) &&
+                            (wi == n - 1 || w[wi + 1] - w[wi] > 1e-3 * tn);
+      const int iters = isolated ? 3 : 5;
+      for (int it = 0; it < iters; ++it) {
         tridiag_shift_solve(d, e, n, lam, tiny, x, u0, u1, u2, ml, pv);
         // orthogonalise against the earlier members of the cluster
         for (int q = j0; q < j; ++q) {
