@@ -217,6 +217,24 @@ int bddc_pc_transform_schur(const int* nB, const long long* soff, const int* sub
                             int max_nB, int max_ng, int max_globs, const double* S, double* tmp,
                             double* Sbar, cudaStream_t stream);
 
+/* Householder form of the change of basis: per glob with r > 0 (not a vertex,
+ * n_g > 1) Q_g <- H_r ... H_1 from the Householder QR of Q_g[:r]^T (same
+ * primal span), reflector j stored as w_j (H_j = I - w_j w_j^T) in row j of
+ * HV at q_off[g]; W: scratch of n_g * r_g doubles per glob at w_off[g].
+ * max_ng: largest n_g.  Part of replacing the transforms of solver.py:70-90. */
+int bddc_pc_glob_reflectors(const int* kind, const int* gsize, const int* r, double* Q,
+                            const long long* q_off, double* HV, double* W, const long long* w_off,
+                            int n_globs, int max_ng, cudaStream_t stream);
+
+/* Sbar_i = Q_i S_i Q_i^T with Q_i = blockdiag of the reflector products of
+ * bddc_pc_glob_reflectors (2 r n_g nB flops per glob block and side).
+ * replaces the S-bar transform solver.py:86-90. */
+int bddc_pc_transform_refl(const int* nB, const long long* soff, const int* sub_glob_start,
+                           const int* sub_globs, const int* sub_glob_boff, const int* kind,
+                           const int* gsize, const int* r, const double* HV,
+                           const long long* q_off, const double* S, double* Sbar, int nbatch,
+                           cudaStream_t stream);
+
 /* TT_(g,s) = D_g^(s) Q_g^T blocks.  replaces Dbar solver.py:87-90. */
 int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
                      const long long* q_off, const double* D, const long long* sh_doff,

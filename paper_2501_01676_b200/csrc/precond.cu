@@ -192,6 +192,140 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) glob_mma_kernel(
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Change of basis in Householder form.  The preconditioner only needs a Q_g
+// whose first r rows span the primal constraints of glob g (M^-1 is invariant
+// under rotations inside the primal span and inside its complement), so Q_g
+// is replaced by H_r ... H_1 from the Householder QR of Q_g[:r]^T.  Then
+// Sbar = Q S Q^T costs 2 r n_g nB flops per glob block and side instead of a
+// dense n_g x n_g block product.  Reflector j is stored as w_j = sqrt(beta_j) v_j
+// (H_j = I - w_j w_j^T) in row j of the glob's n_g x n_g block of HV.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) glob_reflectors_kernel(
+    const int* __restrict__ kind, const int* __restrict__ gsize, const int* __restrict__ r,
+    double* __restrict__ Q, const long long* __restrict__ q_off, double* __restrict__ HV,
+    double* __restrict__ W, const long long* __restrict__ w_off) {
+  extern __shared__ double rsm[];
+  const int g = blockIdx.x;
+  const int n = gsize[g];
+  const int rr = kind[g] == 2 ? 0 : min(r[g], n);
+  double* Qg = Q + q_off[g];
+  double* Hg = HV + q_off[g];
+  double* Wg = W + w_off[g];       // n x rr: Q_g[:rr]^T, reduced in place
+  double* v = rsm;                 // n
+  double* red = rsm + n;           // 4 warps
+  if (rr == 0) return;             // Q_g = I (no constraint) or a vertex: untouched
+  if (n == 1) {                    // [+-1] -> [1]: same span, no reflector
+    if (threadIdx.x == 0) Qg[0] = 1.0;
+    return;
+  }
+  for (int idx = threadIdx.x; idx < n * rr; idx += blockDim.x) {
+    const int i = idx / rr, j = idx - i * rr;
+    Wg[idx] = Qg[j * n + i];
+  }
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = 0; j < rr; ++j) {
+    double ss = 0.0;
+    for (int i = j + threadIdx.x; i < n; i += blockDim.x) ss += Wg[i * rr + j] * Wg[i * rr + j];
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    ss = red[0] + red[1] + red[2] + red[3];
+    const double x0 = Wg[j * rr + j];
+    const double alpha = (x0 >= 0.0 ? -1.0 : 1.0) * sqrt(ss);
+    const double vn = ss - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+    const double beta = vn > 0.0 ? 2.0 / vn : 0.0;
+    const double sb = sqrt(beta);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double vi = i < j ? 0.0 : (i == j ? x0 - alpha : Wg[i * rr + j]);
+      v[i] = vi;
+      Hg[j * n + i] = sb * vi;
+    }
+    __syncthreads();
+    if (beta != 0.0) {
+      for (int c = j + 1 + threadIdx.x; c < rr; c += blockDim.x) {  // W <- H_j W
+        double d = 0.0;
+        for (int i = j; i < n; ++i) d += v[i] * Wg[i * rr + c];
+        d *= beta;
+        for (int i = j; i < n; ++i) Wg[i * rr + c] -= d * v[i];
+      }
+      for (int row = threadIdx.x; row < n; row += blockDim.x) {  // Qacc <- Qacc H_j
+        double d = 0.0;
+        for (int i = j; i < n; ++i) d += Qg[row * n + i] * v[i];
+        d *= beta;
+        for (int i = j; i < n; ++i) Qg[row * n + i] -= d * v[i];
+      }
+    }
+    __syncthreads();
+  }
+  // Q_g = Qacc^T = H_r ... H_1 (reflectors are symmetric)
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int a = idx / n, b = idx - a * n;
+    if (a < b) {
+      const double t = Qg[a * n + b];
+      Qg[a * n + b] = Qg[b * n + a];
+      Qg[b * n + a] = t;
+    }
+  }
+}
+
+// Sbar = Q S Q^T with Q = blockdiag_g(H_r ... H_1), one CTA per subdomain:
+// rows (left product, S -> Sbar) then columns (right product, in place).
+__global__ void __launch_bounds__(256) transform_refl_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ soff,
+    const int* __restrict__ sub_glob_start, const int* __restrict__ sub_globs,
+    const int* __restrict__ sub_glob_boff, const int* __restrict__ kind,
+    const int* __restrict__ gsize, const int* __restrict__ r, const double* __restrict__ HV,
+    const long long* __restrict__ q_off, const double* __restrict__ S, double* __restrict__ Sbar) {
+  const int b = blockIdx.x;
+  const int n = nB[b];
+  const double* Sb = S + soff[b];
+  double* Tb = Sbar + soff[b];
+  const int k0 = sub_glob_start[b], k1 = sub_glob_start[b + 1];
+  // left: thread per column, every glob block of rows
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    for (int k = k0; k < k1; ++k) {
+      const int g = sub_globs[k], ng = gsize[g], bo = sub_glob_boff[k];
+      const int nref = (kind[g] == 2 || ng == 1) ? 0 : min(r[g], ng);
+      if (nref == 0) {
+        for (int i = 0; i < ng; ++i) Tb[(long long)(bo + i) * n + c] = Sb[(long long)(bo + i) * n + c];
+        continue;
+      }
+      const double* Hg = HV + q_off[g];
+      for (int j = 0; j < nref; ++j) {
+        const double* src = j == 0 ? Sb : Tb;
+        const double* w = Hg + j * ng;
+        double d = 0.0;
+        for (int i = j; i < ng; ++i) d += w[i] * src[(long long)(bo + i) * n + c];
+        for (int i = 0; i < ng; ++i)
+          Tb[(long long)(bo + i) * n + c] = src[(long long)(bo + i) * n + c] - (i < j ? 0.0 : d * w[i]);
+      }
+    }
+  }
+  __syncthreads();
+  // right: warp per row, lanes along the glob's columns
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int row = warp; row < n; row += nw) {
+    double* tr = Tb + (long long)row * n;
+    for (int k = k0; k < k1; ++k) {
+      const int g = sub_globs[k], ng = gsize[g], bo = sub_glob_boff[k];
+      const int nref = (kind[g] == 2 || ng == 1) ? 0 : min(r[g], ng);
+      const double* Hg = HV + q_off[g];
+      for (int j = 0; j < nref; ++j) {
+        const double* w = Hg + j * ng;
+        double d = 0.0;
+        for (int i = j + lane; i < ng; i += 32) d += tr[bo + i] * w[i];
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        for (int i = j + lane; i < ng; i += 32) tr[bo + i] -= d * w[i];
+        __syncwarp();
+      }
+    }
+  }
+}
+
 // dst block = src block^T for square blocks (size[gidx[i]]) at off[i]
 __global__ void transpose_blocks_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                         const long long* __restrict__ off,
@@ -994,6 +1128,29 @@ int bddc_pc_transform_schur(const int* nB, const long long* soff, const int* sub
   if (st) return st;
   return glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
                   Q, QT, q_off, 0, 1, tmp, Sbar, n_items, max_nB, max_ng, max_globs, stream);
+}
+
+int bddc_pc_glob_reflectors(const int* kind, const int* gsize, const int* r, double* Q,
+                            const long long* q_off, double* HV, double* W, const long long* w_off,
+                            int n_globs, int max_ng, cudaStream_t stream) {
+  if (n_globs <= 0) return 0;
+  glob_reflectors_kernel<<<n_globs, 128, (max_ng + 4) * (int)sizeof(double), stream>>>(
+      kind, gsize, r, Q, q_off, HV, W, w_off);
+  bddc_note_launches(1);
+  return pc_status();
+}
+
+int bddc_pc_transform_refl(const int* nB, const long long* soff, const int* sub_glob_start,
+                           const int* sub_globs, const int* sub_glob_boff, const int* kind,
+                           const int* gsize, const int* r, const double* HV,
+                           const long long* q_off, const double* S, double* Sbar, int nbatch,
+                           cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  transform_refl_kernel<<<nbatch, 256, 0, stream>>>(nB, soff, sub_glob_start, sub_globs,
+                                                    sub_glob_boff, kind, gsize, r, HV, q_off, S,
+                                                    Sbar);
+  bddc_note_launches(1);
+  return pc_status();
 }
 
 int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,

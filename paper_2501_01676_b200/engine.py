@@ -669,7 +669,10 @@ class DevicePreconditioner:
     """M^-1 = sum_i R_i^T (A_i R_i + N_i P_i C^-1 sum_j P_j^T G_j R_j)
     (reference BddcPreconditioner solver.py:46-209, see precond.cu)."""
 
-    def __init__(self, ls, scaling, r_host, Q, q_off, keep_coarse=8192):
+    def __init__(self, ls, scaling, r_host, Q, q_off, keep_coarse=8192, householder=True):
+        """householder: Q comes from the device primal space (orthogonal, full-rank
+        primal rows), so it may be replaced by its Householder form; caller-given
+        transforms (possibly degenerate, test_solver.py:62-77) are used as given."""
         p, d, st = ls.plan, ls.d, stream()
         self.ls, self.plan, self.comm = ls, p, ls.comm
         r = np.asarray(r_host, dtype=np.int64)
@@ -714,20 +717,37 @@ class DevicePreconditioner:
         self.d_cstart = dev_i64(np.searchsorted(pgid[csrc], np.arange(self.n_primal + 1)))
         self.sum_np = int(pstart[-1])
 
+        # change of basis in Householder form (same primal spans; precond.cu)
+        r_d = dev_i32(r)
+        HV = None
+        if householder:
+            Q = Q.clone()
+            HV = torch.zeros_like(Q)
+            w_sz = np.where(p.kind == 2, 0, p.gsize.astype(np.int64) * np.minimum(r, p.gsize))
+            w_off = _excl(w_sz)
+            Wsc = torch.empty(max(int(w_off[-1]), 1), dtype=F64, device="cuda")
+            lib.bddc_pc_glob_reflectors(d.kind, d.gsize, r_d, Q, q_off, HV, Wsc,
+                                        dev_i64(w_off[:-1]), p.G, int(p.gsize.max()), st)
+            del Wsc
         TT = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
         lib.bddc_pc_ttblocks(d.slot_glob, d.gsize, Q, q_off, scaling.D, d.sh_doff, TT,
                              int(p.sh_sub.size), st)
         Sbar = torch.empty(p.S_total, dtype=F64, device="cuda")
         tmp = torch.empty(p.S_total, dtype=F64, device="cuda")
-        max_ng = int(p.gsize.max())
-        nbmax = int(p.nB.max())
-        n_items = int(p.sub_globs.size)
-        max_globs = int(np.diff(p.sub_glob_start).max())
-        QT = torch.empty(int(Q.numel()), dtype=F64, device="cuda")
-        lib.bddc_pc_transform_schur(d.nB, d.soff, d.sub_glob_start, p.N, d.sub_globs,
-                                    d.sub_glob_boff, d.sub_glob_sh, d.gsize, Q, q_off, QT, p.G,
-                                    n_items, nbmax, max_ng, max_globs, ls.S, tmp, Sbar, st)
-        del QT
+        if householder:
+            lib.bddc_pc_transform_refl(d.nB, d.soff, d.sub_glob_start, d.sub_globs,
+                                       d.sub_glob_boff, d.kind, d.gsize, r_d, HV, q_off, ls.S,
+                                       Sbar, p.N, st)
+            del HV
+        else:  # dense block products with the given Q
+            QT = torch.empty(int(Q.numel()), dtype=F64, device="cuda")
+            lib.bddc_pc_transform_schur(d.nB, d.soff, d.sub_glob_start, p.N, d.sub_globs,
+                                        d.sub_glob_boff, d.sub_glob_sh, d.gsize, Q, q_off, QT,
+                                        p.G, int(p.sub_globs.size), int(p.nB.max()),
+                                        int(p.gsize.max()),
+                                        int(np.diff(p.sub_glob_start).max()), ls.S, tmp, Sbar,
+                                        st)
+            del QT
         Z = torch.empty(p.S_total, dtype=F64, device="cuda")
         lib.bddc_pc_dual_embed(d.nB, d.soff, d.voff, d_mask, Sbar, Z, tmp, p.N, st)
         # certificate: LDL^T of sym(Sbar_dd) must have positive pivots (solver.py:91-98)

@@ -42,7 +42,8 @@ class BddcPreconditioner(DevicePreconditioner):
             Q, q_off = primal.device.Q, primal.device.d_q_off
         else:
             Q, q_off = _upload_transforms(ls, primal)
-        super().__init__(ls, scaling.device, primal.r, Q, q_off)
+        super().__init__(ls, scaling.device, primal.r, Q, q_off,
+                         householder=primal.device is not None)
 
 
 def _upload_transforms(ls, primal):
