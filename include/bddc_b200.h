@@ -109,6 +109,12 @@ int bddc_extract_schur(const double* M, const long long* off, const int* ld, con
 int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
                     cudaStream_t stream);
 
+/* out[b] += ||X_b||_F^2 (square n[b] x n[b] at soff[b]; out zeroed by the caller).
+ * Feeds the certified shortcut of the dual-block Cholesky certificate
+ * (engine.DevicePreconditioner, reference solver.py:91-98). */
+int bddc_frob2(const double* X, const long long* soff, const int* n, int nbatch, double* out,
+               cudaStream_t stream);
+
 /* u_I = A_II^-1 (f_I - A_IB u_B) by block back-substitution.
  * replaces recover_interior solver.py:318-326. */
 int bddc_recover_interior(const double* M, const long long* off, const int* ld, const int* nI,

@@ -319,6 +319,29 @@ __global__ void extract_schur_kernel(const double* __restrict__ base, const long
   }
 }
 
+// out[b] += ||X_b||_F^2 for square batched matrices (ld = n); out zeroed by the caller
+__global__ void frob2_kernel(const double* __restrict__ X, const long long* __restrict__ soff,
+                             const int* __restrict__ nB, double* __restrict__ out) {
+  __shared__ double red[8];
+  const int b = blockIdx.y;
+  const long long nn = (long long)nB[b] * nB[b];
+  const double* M = X + soff[b];
+  double s = 0.0;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < nn;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const double v = M[idx];
+    s = fma(v, v, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    atomicAdd(out + b, t);
+  }
+}
+
 // X <- (X + X^T)/2 for square batched matrices (ld = n)
 __global__ void symmetrize_kernel(double* __restrict__ X, const long long* __restrict__ soff,
                                   const int* __restrict__ nB) {
@@ -543,6 +566,14 @@ int bddc_extract_schur(const double* M, const long long* off, const int* ld, con
   if (nbatch <= 0) return 0;
   extract_schur_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(M, off, ld, nI, nB, soff, voff, S,
                                                              Bsym, g);
+  bddc_note_launches(1);
+  return launch_status();
+}
+
+int bddc_frob2(const double* X, const long long* soff, const int* n, int nbatch, double* out,
+               cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  frob2_kernel<<<dim3(16, nbatch), 256, 0, stream>>>(X, soff, n, out);
   bddc_note_launches(1);
   return launch_status();
 }

@@ -754,11 +754,13 @@ class DevicePreconditioner:
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
         nbmax = int(p.nB.max())
-        lib.bddc_schur_eliminate(tmp, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax, nbmax,
-                                 PANEL, pinv, 4096, 0, status, 1, None, 0, st)
-        bad = _first_bad(status)
-        if bad is not None:
-            raise NumericalError(f"dual block of subdomain {bad + ls.s0} lost positive definiteness")
+        if not self._dual_pd_certified(ls):
+            lib.bddc_schur_eliminate(tmp, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax,
+                                     nbmax, PANEL, pinv, 4096, 0, status, 1, None, 0, st)
+            bad = _first_bad(status)
+            if bad is not None:
+                raise NumericalError(
+                    f"dual block of subdomain {bad + ls.s0} lost positive definiteness")
         # blocked LU of the embedded dual block (64-wide panels, every P_k^-1 kept and
         # moved into the diagonal blocks): the reference's lu_factor(Stil)
         nsteps = (nbmax + 63) // 64
@@ -839,6 +841,27 @@ class DevicePreconditioner:
         self.cvals = torch.empty(max(self.sum_np, 1), dtype=F64, device="cuda")
         self.rp = torch.empty(nc, dtype=F64, device="cuda")
         self.up = torch.empty(nc, dtype=F64, device="cuda")
+
+    @staticmethod
+    def _dual_pd_certified(ls):
+        """True when the reference's cho_factor(sym(Sdd)) (solver.py:94) provably
+        succeeds for every subdomain, so the LDL^T certificate can be skipped.
+        sym(Sbar_dd) is a principal block of Q Bsym Q^T (Q orthogonal), so with
+        Bsym SPD (already checked by bsym_inverse) its eigenvalues lie in
+        [1/||Bsym^-1||, ||S||] up to the rounding of forming Sbar (<= 8 nB eps ||S||);
+        Cholesky of an SPD matrix of order n runs to completion when
+        20 n^1.5 eps cond < 1.  Certified when
+        ||S||_F ||Bsym^-1||_F (20 nB^1.5 + 8 nB) eps < 1/4 for every subdomain."""
+        p, d, st = ls.plan, ls.d, stream()
+        if getattr(ls, "_frob", None) is None:
+            f = torch.zeros(2 * p.N, dtype=F64, device="cuda")
+            lib.bddc_frob2(ls.S, d.soff, d.nB, p.N, f[:p.N], st)
+            lib.bddc_frob2(ls.bsym_inverse(), d.soff, d.nB, p.N, f[p.N:], st)
+            ls._frob = f.cpu().numpy()
+        fs, fi = np.sqrt(ls._frob[:p.N]), np.sqrt(ls._frob[p.N:])
+        n = p.nB.astype(np.float64)
+        bound = fs * fi * (20.0 * n ** 1.5 + 8.0 * n) * np.finfo(np.float64).eps
+        return bool(np.all(np.isfinite(bound)) and np.all(bound < 0.25))
 
     use_graph = False  # re-captured per preconditioner: costs more than it saves here
 

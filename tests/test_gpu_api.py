@@ -183,3 +183,23 @@ def test_device_plan_matches_host_plan(name):
     assert np.array_equal(host.elem_ids, dev.elem_ids_d.cpu().numpy())
     assert np.array_equal(host.loc4, dev.loc4_d.cpu().numpy())
     assert host.K_total == dev.K_total and host.S_total == dev.S_total
+
+
+def test_dual_certificate_full_path_matches_certified(monkeypatch):
+    """The LDL^T certificate of sym(Sdd) (solver.py:91-98) is skipped only when a
+    norm bound proves it succeeds; forcing the factorization changes nothing."""
+    import torch
+
+    from paper_2501_01676_b200 import configs, pipeline
+    from paper_2501_01676_b200.engine import DevicePreconditioner
+
+    prob = configs.build_problem(2, n=16, subs=2)
+    a = pipeline.run(prob.system, prob.partition, prob.globs, 1.0 + math.log(8.0), 10.0, "new",
+                     keep=True)
+    assert DevicePreconditioner._dual_pd_certified(a.ls)
+    monkeypatch.setattr(DevicePreconditioner, "_dual_pd_certified", staticmethod(lambda ls: False))
+    b = pipeline.run(prob.system, prob.partition, prob.globs, 1.0 + math.log(8.0), 10.0, "new")
+    assert a.iterations == b.iterations
+    x, y = a.solution.cpu().numpy(), b.solution.cpu().numpy()
+    assert np.linalg.norm(x - y) <= 1e-12 * np.linalg.norm(y)
+    torch.cuda.synchronize()
