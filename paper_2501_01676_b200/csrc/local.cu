@@ -134,10 +134,22 @@ constexpr int kTrailBM = 64;
 // Trailing update of a panel step.  mode 0: rows/cols from k + w, K = w with
 // w = min(nbw, npiv - k) (nbw = 64 or 128).  mode 1 (strip inside a 128-wide
 // panel): rows [k + w1, k + w), cols from k + w1, K = w1, w1 = min(64, npiv - k).
+// Lookahead (pnext != null): CTA 0 of each matrix owns the next pivot block
+// (rows / cols from s) and inverts it right after its tile update, so the
+// next panel needs no separate pivot launch.
+struct NextPivot {
+  double* pinv;           // P of the next pivot block (+ b * stride), null: no lookahead
+  long long stride;
+  int* status;
+  int require_positive;
+  double* piv_out;        // scalar pivots (+ b * piv_stride + next k), may be null
+  long long piv_stride;
+};
+
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ nrows, const int* __restrict__ ncols,
-    int k, int lim, int nbw, int mode) {
+    int k, int lim, int nbw, int mode, NextPivot nx) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmemT<kTrailBM>& sm = *reinterpret_cast<TileSmemT<kTrailBM>*>(smem_raw);
   const int b = blockIdx.y;
@@ -168,6 +180,21 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_k
   tile_mma_t<kTrailBM>(M + (long long)r0 * L + c0, L, min(kTrailBM, r_end - r0), min(kTile, nc - c0),
                        M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0,
                        sm);
+  if (nx.pinv != nullptr && blockIdx.x == 0) {
+    const int wn = min(kTile, npiv[b] - s);
+    if (wn > 0) {
+      __syncthreads();  // tile written; the pipeline smem is free
+      static_assert(sizeof(MmaGjSmem) <= sizeof(TileSmemT<kTrailBM>), "smem reuse");
+      MmaGjSmem& gsm = *reinterpret_cast<MmaGjSmem*>(smem_raw);
+      const bool bad = reg_gj64(M + (long long)s * L + s, L, wn, nx.pinv + (long long)b * nx.stride,
+                                kTile, nx.require_positive,
+                                nx.piv_out ? nx.piv_out + (long long)b * nx.piv_stride + s : nullptr,
+                                gsm);
+      if (threadIdx.x == 0 && bad && nx.status)
+        atomicCAS(nx.status + b, 0,
+                  nx.require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
+    }
+  }
 }
 
 // 128-wide panels: W_top -= W1_Q W2 on rows [k, k+64), cols [k + w, ncols),
@@ -467,12 +494,19 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
   }
   int launches = 0, timed = 0;
   const size_t tsm = sizeof(TileSmemT<kTrailBM>);
+  const NextPivot none{nullptr, 0, nullptr, 0, nullptr, 0};
+  // pivot blocks after the first are inverted inside the launch that last
+  // updates them (lookahead); pivoted[k / 64] tracks which were
+  pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, 0, pinv_ws, pinv_stride,
+                                                   status, require_positive, piv_out, piv_stride);
+  ++launches;
   for (int k = 0; k < max_npiv; k += panel) {
     double* P = pinv_ws + (long long)(k / panel) * pinv_step_stride;
-    // first (or only) 64-wide sub-panel: pivot inverse, W1 = P1 A12
-    pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, k, P, pinv_stride, status,
-                                                     require_positive, piv_out, piv_stride);
-    ++launches;
+    double* Pn = pinv_ws + (long long)(k / panel + 1) * pinv_step_stride;
+    const NextPivot nx_sub{P, pinv_stride, status, require_positive, piv_out, piv_stride};
+    const NextPivot nx_next{Pn, pinv_stride, status, require_positive, piv_out, piv_stride};
+    bool next_done = false;
+    // first (or only) 64-wide sub-panel: W1 = P1 A12 (P1 from the previous launch)
     const int ct1 = ceil_div(max_cols - k, kTile);
     if (ct1 > 0) {
       schur_row_kernel<<<dim3(ct1, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
@@ -480,28 +514,33 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
       ++launches;
     }
     if (panel == 2 * kTile && k + kTile < max_npiv) {
-      // second sub-panel: strip update of its 64 rows, pivot inverse, W2,
-      // then W_top -= W1_Q W2 so the pivot rows hold A11^-1 A12 for all 128
+      // second sub-panel: strip update of its 64 rows (+ its pivot inverse),
+      // W2, then W_top -= W1_Q W2 so the pivot rows hold A11^-1 A12 for all 128
       const int cts = ceil_div(max_cols - k - kTile, kTile);
       schur_trailing_kernel<<<dim3(cts, nbatch), kTileThreads, tsm, stream>>>(
-          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1);
-      pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, k + kTile, P, pinv_stride,
-                                                       status, require_positive, piv_out,
-                                                       piv_stride);
+          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1, nx_sub);
       schur_row_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(
           M, off, ld, npiv, ncols, k + kTile, P, pinv_stride, 0x7fffffff);
       schur_fix_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k);
-      launches += 4;
+      launches += 3;
     }
     const int ct = ceil_div(max_cols - k, kTile);
     const int rt = ceil_div(max_rows - k, kTrailBM);
+    const bool more = k + panel < max_npiv;
     if (ct > 0 && rt > 0) {
       if (ev) cudaEventRecord(ev[2 * timed], stream);
       schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, tsm, stream>>>(
-          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, panel, 0);
+          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, panel, 0, more ? nx_next : none);
       ++launches;
+      next_done = true;
       if (ev) cudaEventRecord(ev[2 * timed + 1], stream);
       timed += (ev != nullptr);
+    }
+    if (more && !next_done) {
+      pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, npiv, k + panel, Pn, pinv_stride,
+                                                       status, require_positive, piv_out,
+                                                       piv_stride);
+      ++launches;
     }
   }
   if (ev) {
