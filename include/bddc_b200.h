@@ -82,6 +82,14 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
                                int require_positive, double* piv_out, long long piv_stride,
                                cudaStream_t stream, double* host_trailing_ms);
 
+/* Event log of the bddc_schur_eliminate trailing-update launches (bench
+ * roofline measured over the timed region without synchronising inside it):
+ * bddc_trailing_log(1) starts logging, bddc_trailing_collect() synchronises on
+ * the logged events, writes the summed duration (ms, HOST pointer) and the
+ * number of logged launches, and clears the log.  Not thread-safe. */
+int bddc_trailing_log(int enable);
+int bddc_trailing_collect(double* total_ms, long long* launches);
+
 /* Envelope LU without pivoting of the coarse matrix (one n x n matrix at
  * C + off[0], leading dimension ldv[0], nv[0] = n) in a bandwidth-reducing
  * order: panel k updates only rows/cols below host_lim[k/64] (host array).
@@ -122,6 +130,20 @@ int bddc_recover_interior(const double* M, const long long* off, const int* ld, 
                           const long long* ioff, const long long* interior_nodes,
                           const double* u_hat, double* u, int nbatch, int max_nloc, int panel,
                           cudaStream_t stream);
+
+/* ---- elements.cu : SUPG element blocks ------------------------------------ */
+
+/* Ke (m x 16) and Fe (m x 4) of the SUPG-stabilised P1 tetrahedra for
+ * device-evaluable coefficients: velocity a(x) = A x + a0, constant reaction
+ * and source, viscosity nu[e] = nu_tab[e % nu_period].  fields (host array,
+ * 16 doubles): A (row-major 3x3), a0, c, f, c - div(a)/2 (or c), tau.
+ * bad_element (device, initialised to ~0ull by the caller): smallest element
+ * index with a non-positive volume.  replaces element_contributions /
+ * p1_gradients / stabilization discretization.py:91-158. */
+int bddc_supg_elements(const double* nodes, const long long* conn, long long m,
+                       const double* nu_tab, long long nu_period, const double* fields,
+                       double* Ke, double* Fe, unsigned long long* bad_element,
+                       cudaStream_t stream);
 
 /* ---- globs.cu : scaling and adaptive coarse space ------------------------- */
 

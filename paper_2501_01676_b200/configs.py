@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .decomposition import Partition, classify_globs, node_sharer_pairs, partition_regular
-from .discretization import Coefficients, assemble_system
+from .discretization import Coefficients, DeviceFields, assemble_system
 from .mesh import box_mesh
 
 UNIT = ((0.0, 1.0), (0.0, 1.0), (0.0, 1.0))
@@ -36,16 +36,20 @@ def _const_velocity(b):
     return lambda p: np.tile(b, (len(p), 1))
 
 
-def _coeffs(cell_nu, n, velocity):
+def _coeffs(cell_nu, n, velocity, vel_affine):
     """Per-element viscosity from a per-cell field (element e is cell e % n^3,
-    reference mesh.py:75-83)."""
+    reference mesh.py:75-83).  vel_affine = (A, a0) with velocity(x) = A x + a0:
+    the same fields in the form the device element kernel evaluates."""
     n3 = n ** 3
+    A, a0 = vel_affine
     return Coefficients(
         viscosity=lambda cent: cell_nu[np.arange(len(cent)) % n3],
         velocity=velocity,
         reaction=lambda p: np.ones(len(p)),
         source=lambda p: np.ones(len(p)),
         dirichlet=lambda p: np.zeros(len(p)),
+        device_fields=DeviceFields(np.asarray(A, dtype=float), np.asarray(a0, dtype=float),
+                                   1.0, 1.0, np.asarray(cell_nu, dtype=float), n3),
     )
 
 
@@ -181,22 +185,27 @@ def build_problem(config, n=None, subs=None, theta_f=THETA, theta_e=THETA, seed=
         sd = subs or s0
         part = partition_regular(mesh, (sd, sd, sd))
         Hh = n // sd
+    Z = np.zeros((3, 3))
     if config == 1:
-        cell_nu, vel = np.full(n ** 3, 1e-2), _const_velocity((1.0, 1.0, 1.0))
+        b = (1.0, 1.0, 1.0)
+        cell_nu, vel, aff = np.full(n ** 3, 1e-2), _const_velocity(b), (Z, b)
     elif config == 2:
         cell_nu = channel_viscosity(n, seed=seed)
         vel = lambda p: np.column_stack([-(p[:, 1] - 0.5), p[:, 0] - 0.5, np.full(len(p), 0.1)])
+        aff = ([[0.0, -1.0, 0.0], [1.0, 0.0, 0.0], [0.0, 0.0, 0.0]], (0.5, -0.5, 0.1))
     elif config == 3:
-        cell_nu = np.full(n ** 3, 1e-3)
-        vel = _const_velocity(np.array([1.0, 2.0, 3.0]) / math.sqrt(14.0))
+        b = np.array([1.0, 2.0, 3.0]) / math.sqrt(14.0)
+        cell_nu, vel, aff = np.full(n ** 3, 1e-3), _const_velocity(b), (Z, b)
     elif config == 4:
-        cell_nu, vel = block_lognormal_viscosity(n, seed=seed), _const_velocity((1.0, 1.0, 1.0))
+        b = (1.0, 1.0, 1.0)
+        cell_nu, vel, aff = block_lognormal_viscosity(n, seed=seed), _const_velocity(b), (Z, b)
     elif config == 5:
-        cell_nu, vel = np.full(n ** 3, 1e-2), _const_velocity((1.0, 1.0, 1.0))
+        b = (1.0, 1.0, 1.0)
+        cell_nu, vel, aff = np.full(n ** 3, 1e-2), _const_velocity(b), (Z, b)
     else:
         raise ValueError(f"unknown config {config}")
     globs = classify_globs(mesh, part, mesh.boundary_nodes)
-    coeffs = _coeffs(cell_nu, n, vel)
+    coeffs = _coeffs(cell_nu, n, vel, aff)
     system = assemble_system(mesh, coeffs)
     if theta_f is None:
         theta_f = 1.0 + math.log(Hh)

@@ -14,6 +14,8 @@
 #include "tile_mma.cuh"
 #include "reg_gj.cuh"
 
+#include <vector>
+
 namespace bddc {
 
 // ---------------------------------------------------------------------------
@@ -237,15 +239,30 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) panel_scale_kern
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_row_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ n, int k, const double* __restrict__ pinv, long long pinv_stride) {
+    const int* __restrict__ n, int k, const double* __restrict__ pinv, long long pinv_stride,
+    int symmetric) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
   const int w = min(kTile, n[b] - k);
   if (w <= 0) return;
   const int c0 = blockIdx.x * kTile;
-  if (c0 >= n[b] || c0 == k) return;  // pivot column tile is written by gj_col
+  if (c0 >= n[b]) return;
   const int L = ld[b];
+  if (c0 == k) {
+    // pivot block <- sym(P): written here in the symmetric variant (the update
+    // skips it), so that P may be overwritten by the next pivot during the
+    // update; otherwise gj_col writes it
+    if (symmetric) {
+      const double* P = pinv + (long long)b * pinv_stride;
+      double* M = base + off[b];
+      for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
+        const int r = idx / w, c = idx - r * w;
+        M[(long long)(k + r) * L + k + c] = 0.5 * (P[r * kTile + c] + P[c * kTile + r]);
+      }
+    }
+    return;
+  }
   double* C = base + off[b] + (long long)k * L + c0;
   tile_mma(C, L, w, min(kTile, n[b] - c0), pinv + (long long)b * pinv_stride, kTile, C, L, w, 1.0,
            0.0, sm);
@@ -256,7 +273,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_row_kernel(
 // computed and each off-diagonal result is mirrored with that sign.
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ n, int k, int symmetric) {
+    const int* __restrict__ n, int k, int symmetric, NextPivot nx) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
@@ -276,6 +293,16 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel
   tile_mma(M + (long long)r0 * L + c0, L, min(kTile, nb - r0), min(kTile, nb - c0),
            M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm, Ct, L,
            sgn);
+  if (nx.pinv != nullptr && r0 == k + kTile && c0 == k + kTile) {
+    // lookahead: this CTA holds the next pivot block, final after this update
+    __syncthreads();
+    MmaGjSmem& gsm = *reinterpret_cast<MmaGjSmem*>(smem_raw);
+    const bool bad = reg_gj64(M + (long long)r0 * L + r0, L, min(kTile, nb - r0),
+                              nx.pinv + (long long)b * nx.stride, kTile, nx.require_positive,
+                              nullptr, gsm);
+    if (threadIdx.x == 0 && bad && nx.status)
+      atomicCAS(nx.status + b, 0, nx.require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
+  }
 }
 
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
@@ -293,7 +320,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
   const int L = ld[b];
   double* M = base + off[b];
   const double* P = pinv + (long long)b * pinv_stride;
-  if (r0 == k) {  // pivot block <- P (symmetric part when symmetric)
+  if (r0 == k) {  // pivot block <- P (written by gj_row in the symmetric variant)
+    if (symmetric) return;
     for (int idx = threadIdx.x; idx < w * w; idx += blockDim.x) {
       int r = idx / w, c = idx - r * w;
       M[(long long)(k + r) * L + k + c] =
@@ -476,6 +504,13 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
   return launch_status();
 }
 
+// Optional event log of the trailing-update launches (bench roofline over the
+// timed region without a mid-step synchronisation): bddc_trailing_log(1)
+// starts it, bddc_trailing_collect() sums the logged durations and clears it.
+static std::vector<cudaEvent_t> g_trail_pool;  // created once, reused
+static size_t g_trail_used = 0;
+static bool g_trail_on = false;
+
 static int schur_eliminate_impl(double* M, const long long* off, const int* ld, const int* npiv,
                                 const int* nrows, const int* ncols, int nbatch, int max_npiv,
                                 int max_rows, int max_cols, int panel, double* pinv_ws,
@@ -528,12 +563,18 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
     const int rt = ceil_div(max_rows - k, kTrailBM);
     const bool more = k + panel < max_npiv;
     if (ct > 0 && rt > 0) {
+      const bool lg = g_trail_on && !ev && g_trail_used + 2 <= g_trail_pool.size();
+      if (lg) cudaEventRecord(g_trail_pool[g_trail_used], stream);
       if (ev) cudaEventRecord(ev[2 * timed], stream);
       schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, tsm, stream>>>(
           M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, panel, 0, more ? nx_next : none);
       ++launches;
       next_done = true;
       if (ev) cudaEventRecord(ev[2 * timed + 1], stream);
+      if (lg) {
+        cudaEventRecord(g_trail_pool[g_trail_used + 1], stream);
+        g_trail_used += 2;
+      }
       timed += (ev != nullptr);
     }
     if (more && !next_done) {
@@ -568,6 +609,29 @@ int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const i
                               require_positive, piv_out, piv_stride, stream, nullptr);
 }
 
+int bddc_trailing_log(int enable) {
+  if (enable && g_trail_pool.empty()) {
+    g_trail_pool.resize(4096);
+    for (cudaEvent_t& e : g_trail_pool) cudaEventCreate(&e);
+  }
+  g_trail_on = enable != 0;
+  return 0;
+}
+
+int bddc_trailing_collect(double* total_ms, long long* launches) {
+  double t = 0.0;
+  for (size_t i = 0; i + 1 < g_trail_used; i += 2) {
+    float ms = 0.f;
+    cudaEventSynchronize(g_trail_pool[i + 1]);
+    cudaEventElapsedTime(&ms, g_trail_pool[i], g_trail_pool[i + 1]);
+    t += ms;
+  }
+  *total_ms = t;
+  *launches = (long long)(g_trail_used / 2);
+  g_trail_used = 0;
+  return 0;
+}
+
 int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, const int* npiv,
                                const int* nrows, const int* ncols, int nbatch, int max_npiv,
                                int max_rows, int max_cols, int panel, double* pinv_ws,
@@ -585,16 +649,23 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
   if (nbatch <= 0) return 0;
   const int smem = smem_tile_setup();
   const int T = ceil_div(max_n, kTile);
+  const NextPivot none{nullptr, 0, nullptr, 0, nullptr, 0};
+  const bool look = symmetric != 0;
+  const NextPivot nx{pinv_ws, pinv_stride, status, require_positive, nullptr, 0};
   for (int k = 0; k < max_n; k += kTile) {
-    pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, pinv_ws, pinv_stride,
-                                                     status, require_positive, nullptr, 0);
+    // symmetric: pivots after the first are inverted by the update launch (lookahead)
+    if (!look || k == 0) {
+      pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, pinv_ws, pinv_stride,
+                                                       status, require_positive, nullptr, 0);
+      bddc_note_launches(1);
+    }
     gj_row_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
-                                                                  pinv_stride);
-    gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k,
-                                                                         symmetric);
+                                                                  pinv_stride, symmetric);
+    gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(
+        M, off, ld, n, k, symmetric, look && k + kTile < max_n ? nx : none);
     gj_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride, symmetric);
-    bddc_note_launches(4);
+    bddc_note_launches(3);
   }
   return launch_status();
 }

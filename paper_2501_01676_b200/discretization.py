@@ -44,6 +44,29 @@ def stabilization(h, anorm, nu, tau=0.7):
 
 
 @dataclass
+class DeviceFields:
+    """Coefficient fields the device can evaluate (csrc/elements.cu): velocity
+    a(x) = velocity_matrix @ x + velocity_offset, constant reaction and source,
+    viscosity nu[e] = viscosity_table[e % viscosity_period].  Optional: a
+    Coefficients carrying one lets the element blocks be built on the GPU
+    inside every solve; the callables stay authoritative for the host."""
+
+    velocity_matrix: np.ndarray
+    velocity_offset: np.ndarray
+    reaction: float
+    source: float
+    viscosity_table: np.ndarray
+    viscosity_period: int
+
+    def packed(self, tau, with_div):
+        """The 16 doubles of bddc_supg_elements: A, a0, c, f, c - div(a)/2, tau."""
+        A = np.asarray(self.velocity_matrix, dtype=float).reshape(3, 3)
+        cdiv = self.reaction - 0.5 * float(np.trace(A)) if with_div else self.reaction
+        return np.concatenate([A.ravel(), np.asarray(self.velocity_offset, dtype=float).ravel(),
+                               [self.reaction, self.source, cdiv, tau]])
+
+
+@dataclass
 class Coefficients:
     """Problem data, same fields as the reference (discretization.py:52-67)."""
 
@@ -54,6 +77,7 @@ class Coefficients:
     dirichlet: Callable
     velocity_div: Optional[Callable] = None
     tau: float = 0.7
+    device_fields: Optional[DeviceFields] = None
 
 
 @dataclass
@@ -68,6 +92,8 @@ class AssembledSystem:
     elem_matrices: np.ndarray = field(repr=False)
     elem_rhs: np.ndarray = field(repr=False)
     viscosity: np.ndarray = field(repr=False)
+    device_fields: Optional[np.ndarray] = field(default=None, repr=False)  # packed fields
+    device_viscosity: Optional[tuple] = field(default=None, repr=False)    # (table, period)
     _full: object = field(default=None, repr=False)
     _load: object = field(default=None, repr=False)
 
@@ -218,8 +244,15 @@ def assemble_system(mesh, coeffs, dirichlet_nodes=None):
     g = np.zeros(n)
     if dirichlet_nodes.size:
         g[dirichlet_nodes] = np.asarray(coeffs.dirichlet(mesh.nodes[dirichlet_nodes]), dtype=float)
+    dev = None
+    dvisc = None
+    if coeffs.device_fields is not None:
+        df = coeffs.device_fields
+        dev = df.packed(coeffs.tau, coeffs.velocity_div is not None)
+        dvisc = (np.asarray(df.viscosity_table, dtype=float), int(df.viscosity_period))
     return AssembledSystem(mesh=mesh, free_nodes=free, node_to_free=node_to_free,
-                           dirichlet_values=g, elem_matrices=K, elem_rhs=F, viscosity=nu)
+                           dirichlet_values=g, elem_matrices=K, elem_rhs=F, viscosity=nu,
+                           device_fields=dev, device_viscosity=dvisc)
 
 
 def solve_direct(system):

@@ -133,9 +133,13 @@ class LocalSystem:
     def _factor(self):
         p, d, st = self.plan, self.d, stream()
         K = torch.zeros(p.K_total, dtype=F64, device="cuda")
+        Ke, Fe, ebad = self.inputs.get("Ke"), self.inputs.get("Fe"), None
+        if Ke is None:  # element blocks built on the device from mesh + coefficients
+            Ke, Fe, ebad = device_element_blocks(self.inputs)
         lib.bddc_local_assemble(K, d.off, d.ld, d.nL, d.elem_start, d.elem_ids, d.loc4,
-                                self.inputs["conn"], self.inputs["Ke"], self.inputs["Fe"],
-                                self.inputs["gdir"], p.N, p.max_elems, st)
+                                self.inputs["conn"], Ke, Fe, self.inputs["gdir"], p.N,
+                                p.max_elems, st)
+        del Ke, Fe
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
         args = (K, d.off, d.ld, d.nI, d.nL, d.nL1, p.N, int(p.nI.max()), int(p.nL.max()),
@@ -152,12 +156,17 @@ class LocalSystem:
         self.g = torch.empty(int(p.voff[-1]), dtype=F64, device="cuda")
         lib.bddc_extract_schur(K, d.off, d.ld, d.nI, d.nB, d.soff, d.voff, self.S, self.Bsym,
                                self.g, p.N, st)
+        if ebad is not None and int(ebad.item()) != -1:
+            raise ValueError("mesh contains degenerate or inverted elements")
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError(f"interior block of subdomain {bad + self.s0} is singular")
 
-    def bsym_inverse(self):
-        """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check."""
+    def bsym_inverse(self, before_check=None):
+        """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check.
+        before_check: called after the launches, before the status check (the
+        reference builds the deluxe scaling before it inverts Bsym, so that
+        error is reported first when both fail)."""
         if self._Binv is None:
             p, d, st = self.plan, self.d, stream()
             Binv = self.Bsym.clone()
@@ -166,6 +175,8 @@ class LocalSystem:
             # Bsym is exactly symmetric (extract_schur): symmetric GJ, exact symmetric result
             lib.bddc_gj_inverse(Binv, d.soff, d.nB, d.nB, p.N, int(p.nB.max()), pinv, 4096, status,
                                 1, 1, st)
+            if before_check is not None:
+                before_check()
             bad = _first_bad(status)
             if bad is not None:
                 B = self.matrix(self.Bsym, bad)
@@ -213,18 +224,32 @@ class LocalSystem:
         return buf[int(p.voff[i]):int(p.voff[i + 1])].cpu().numpy()
 
 
-def trailing_flops(plan, panel=PANEL):
+def _panel_flops(npiv, nrows, ncols, panel):
+    total, launches = 0, 0
+    for k in range(0, int(npiv.max()), panel):
+        act = npiv > k
+        w = np.minimum(panel, npiv[act] - k)
+        rows = nrows[act] - k - w
+        cols = ncols[act] - k - w
+        f = int((2 * rows * cols * w).sum())
+        total += f
+        launches += 1
+    return total, launches
+
+
+def trailing_flops(plan, panel=PANEL, dual_lu=False):
     """Algorithmic flops of the Schur-elimination trailing updates (DMMA kernel,
-    mode 0): sum over panels k and subdomains b of 2 * rows * cols * w."""
-    nI, nL = plan.nI.astype(np.int64), plan.nL.astype(np.int64)
-    total = 0
-    for k in range(0, int(nI.max()), panel):
-        act = nI > k
-        w = np.minimum(panel, nI[act] - k)
-        rows = nL[act] - k - w
-        cols = nL[act] + 1 - k - w
-        total += int((2 * rows * cols * w).sum())
-    return total
+    mode 0): sum over panels k and subdomains b of 2 * rows * cols * w; the
+    subdomain elimination (nI pivots of [I|B] x [I|B|f]) and, with dual_lu,
+    the 64-panel LU of the embedded dual blocks (nB pivots of nB x nB).
+    Returns (flops, launches)."""
+    nI, nL, nB = (plan.nI.astype(np.int64), plan.nL.astype(np.int64),
+                  plan.nB.astype(np.int64))
+    f, n = _panel_flops(nI, nL, nL + 1, panel)
+    if dual_lu:
+        f2, n2 = _panel_flops(nB, nB, nB, 64)
+        f, n = f + f2, n + n2
+    return f, n
 
 
 def _first_bad(status):
@@ -273,72 +298,108 @@ class DevicePlan:
         self.slot_local = dev_i32(p.slot_local)
 
 
-def stage_inputs(system, partition=None, owned=None):
-    """Page-locked host copies of the per-step inputs (element blocks,
-    connectivity, Dirichlet data, element -> subdomain map): the host buffers
-    a caller keeps its problem data in so that every solve's upload is a
-    straight DMA.  owned=(s0, s1): only the elements of subdomains s0..s1-1."""
-    Ke = system.elem_matrices.reshape(-1, 16)
-    Fe = system.elem_rhs.reshape(-1, 4)
-    conn = system.mesh.elements
+def _select(system, partition, owned):
+    """Element subset of subdomains owned = (s0, s1), or None for all."""
     sub_of = None if partition is None else np.asarray(partition.subdomain_of)
     if owned is not None and sub_of is not None and tuple(owned) != (0, partition.n_subdomains):
-        sel = np.flatnonzero((sub_of >= owned[0]) & (sub_of < owned[1]))
-        Ke, Fe, conn, sub_of = Ke[sel], Fe[sel], conn[sel], sub_of[sel]
+        return sub_of, np.flatnonzero((sub_of >= owned[0]) & (sub_of < owned[1]))
+    return sub_of, None
+
+
+def _input_arrays(system, partition, owned, device_elements):
+    """Host arrays of the per-step inputs.  device_elements (default: when the
+    system carries device-evaluable coefficient fields): the mesh nodes and
+    the viscosity table replace the element blocks, which the device then
+    builds inside the step (csrc/elements.cu)."""
+    sub_of, sel = _select(system, partition, owned)
+    conn = system.mesh.elements
+    if device_elements is None:
+        device_elements = system.device_fields is not None
+    if device_elements and system.device_fields is None:
+        raise ValueError("device element blocks need Coefficients.device_fields")
+    arrays = {"conn": (conn if sel is None else conn[sel], np.int64)}
+    meta = None
+    if device_elements:
+        table, period = system.device_viscosity
+        if sel is not None:  # a rank's subset: one value per selected element
+            table = np.asarray(system.viscosity)[sel]
+            period = sel.size
+        arrays["nodes"] = (system.mesh.nodes, np.float64)
+        arrays["nu_tab"] = (table, np.float64)
+        meta = (np.asarray(system.device_fields, dtype=np.float64), int(period))
+    else:
+        Ke = system.elem_matrices.reshape(-1, 16)
+        Fe = system.elem_rhs.reshape(-1, 4)
+        arrays["Ke"] = (Ke if sel is None else Ke[sel], np.float64)
+        arrays["Fe"] = (Fe if sel is None else Fe[sel], np.float64)
+    arrays["gdir"] = (system.dirichlet_values, np.float64)
+    arrays["free"] = (np.asarray(system.node_to_free) >= 0, np.bool_)
+    if sub_of is not None:
+        arrays["sub_of"] = (sub_of if sel is None else sub_of[sel], np.int64)
+    return arrays, meta
+
+
+def stage_inputs(system, partition=None, owned=None, device_elements=None):
+    """Page-locked host copies of the per-step inputs (element blocks or the
+    mesh + coefficient data they are built from on the device, connectivity,
+    Dirichlet data, element -> subdomain map): the host buffers a caller keeps
+    its problem data in so that every solve's upload is a straight DMA.
+    owned=(s0, s1): only the elements of subdomains s0..s1-1."""
+    arrays, meta = _input_arrays(system, partition, owned, device_elements)
 
     def pin(a, dt):
         src = torch.from_numpy(np.ascontiguousarray(a, dtype=dt))
         t = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
         t.copy_(src)
         return t
-    out = {
-        # small index arrays first: the symbolic plan only needs these
-        "conn": pin(conn, np.int64),
-        "free": pin(np.asarray(system.node_to_free) >= 0, np.bool_),
-        "gdir": pin(system.dirichlet_values, np.float64),
-        "Ke": pin(Ke, np.float64),
-        "Fe": pin(Fe, np.float64),
-    }
-    if sub_of is not None:
-        out["sub_of"] = pin(sub_of, np.int64)
+    out = {k: pin(a, dt) for k, (a, dt) in arrays.items()}
+    if meta is not None:
+        out["_supg"] = meta
     return out
 
 
 def upload_staged(staged):
     """Asynchronous H2D of stage_inputs() buffers on the current stream."""
-    return {k: v.cuda(non_blocking=True) for k, v in staged.items()}
+    return {k: (v.cuda(non_blocking=True) if isinstance(v, torch.Tensor) else v)
+            for k, v in staged.items()}
 
 
 def staged_bytes(staged):
-    return int(sum(v.numel() * v.element_size() for v in staged.values()))
+    return int(sum(v.numel() * v.element_size() for v in staged.values()
+                   if isinstance(v, torch.Tensor)))
 
 
-def upload_inputs(system, partition=None, pinned=False, owned=None):
-    """Element blocks, connectivity, Dirichlet data (and the element ->
-    subdomain map, for the device-side symbolic plan) to the device.
-    owned=(s0, s1): only the elements of subdomains s0..s1-1 (a rank's shard)."""
+def upload_inputs(system, partition=None, pinned=False, owned=None, device_elements=None):
+    """Per-step inputs to the device (see stage_inputs); owned=(s0, s1): only
+    the elements of subdomains s0..s1-1 (a rank's shard)."""
     if pinned:
-        return upload_staged(stage_inputs(system, partition, owned))
-
-    def up(a, dt):
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
-    Ke = system.elem_matrices.reshape(-1, 16)
-    Fe = system.elem_rhs.reshape(-1, 4)
-    conn = system.mesh.elements
-    sub_of = None if partition is None else np.asarray(partition.subdomain_of)
-    if owned is not None and sub_of is not None and tuple(owned) != (0, partition.n_subdomains):
-        sel = np.flatnonzero((sub_of >= owned[0]) & (sub_of < owned[1]))
-        Ke, Fe, conn, sub_of = Ke[sel], Fe[sel], conn[sel], sub_of[sel]
-    out = {
-        "Ke": up(Ke, np.float64),
-        "Fe": up(Fe, np.float64),
-        "conn": up(conn, np.int64),
-        "gdir": up(system.dirichlet_values, np.float64),
-        "free": up(np.asarray(system.node_to_free) >= 0, np.bool_),
-    }
-    if sub_of is not None:
-        out["sub_of"] = up(sub_of, np.int64)
+        return upload_staged(stage_inputs(system, partition, owned, device_elements))
+    arrays, meta = _input_arrays(system, partition, owned, device_elements)
+    out = {k: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
+           for k, (a, dt) in arrays.items()}
+    if meta is not None:
+        out["_supg"] = meta
     return out
+
+
+def device_element_blocks(inputs):
+    """(Ke, Fe, bad) built on the device from inputs["nodes"], ["conn"],
+    ["nu_tab"] and the packed fields (reference element_contributions,
+    discretization.py:101-158); bad: device flag of the first element with a
+    non-positive volume (~0 if none)."""
+    fields, period = inputs["_supg"]
+    if not fields[14] > 0.0:  # c - div(a)/2 is constant: the reference reports element 0
+        raise ValueError("shifted reaction c - div(a)/2 is not positive on element 0; "
+                         "the symmetric part of the form would lose definiteness")
+    conn = inputs["conn"]
+    m = int(conn.shape[0])
+    Ke = torch.empty((m, 16), dtype=F64, device="cuda")
+    Fe = torch.empty((m, 4), dtype=F64, device="cuda")
+    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    fh = (ctypes.c_double * 16)(*[float(x) for x in fields])
+    lib.bddc_supg_elements(inputs["nodes"], conn, m, inputs["nu_tab"], int(period),
+                           ctypes.cast(fh, ctypes.c_void_p), Ke, Fe, bad, stream())
+    return Ke, Fe, bad
 
 
 # ---------------------------------------------------------------------------
@@ -348,7 +409,7 @@ def upload_inputs(system, partition=None, pinned=False, owned=None):
 class DeviceScaling:
     """Deluxe families per glob (reference scaling.py:47-57)."""
 
-    def __init__(self, ls):
+    def __init__(self, ls, check=True):
         p, d, comm = ls.plan, ls.d, ls.comm
         self.ls = ls
         multi = _multi(comm)
@@ -363,8 +424,15 @@ class DeviceScaling:
                         None if mine is None else dev_i32(mine),
                         p.G if mine is None else mine.size, stream())
         _allreduce(comm, self.D, status)
-        bad = _first_bad(status)
+        self._status = status
+        if check:
+            self.check()
+
+    def check(self):
+        """Raise the reference's error for a singular deluxe block sum."""
+        bad = _first_bad(self._status)
         if bad is not None:
+            ls = self.ls
             raise NumericalError("deluxe block sum is singular "
                                  f"(glob {ls.globs.glob_id(ls.globs.globs[bad])})")
 
@@ -1046,6 +1114,83 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     if it:
         lib.bddc_multi_axpy(V.buf, n, it, dev_f64(y), 1.0, x, st)
     return it, conv, x, true_hist, pre_hist
+
+
+def gmres_right_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300, restart=200):
+    """Right-preconditioned restarted GMRES(restart), x0 = 0: the variant
+    BASELINE.json names (the reference only has the left-preconditioned full
+    GMRES, SPEC.md:555 lists right preconditioning as a non-goal).
+    Minimises the true residual ||b - S_hat x||; stops when it drops below
+    rel_tol ||b||.  Same kernels as gmres_device (CGS2, host gelsd); the
+    preconditioned basis Z = M^-1 V of the cycle is kept, so the update needs
+    no extra M^-1 application.  Returns (iterations, converged, x,
+    true_hist, true_hist)."""
+    st = stream()
+    n = rhs.shape[0]
+    restart = max(1, min(int(restart), int(max_iter)))
+    nblk = 296
+    partial = torch.empty(nblk * (restart + 2), dtype=F64, device="cuda")
+    scal = torch.empty(restart + 2, dtype=F64, device="cuda")
+    lib.bddc_norm2(rhs, n, scal, partial, nblk, st)
+    bnorm = float(scal[0].item())
+    x = torch.zeros(n, dtype=F64, device="cuda")
+    if bnorm == 0.0:
+        return 0, True, x, [0.0], [0.0]
+    V = _Basis(n, restart + 1)
+    Z = _Basis(n, restart)
+    V.ensure(restart + 1)
+    Z.ensure(restart)
+    h1 = torch.empty(restart + 1, dtype=F64, device="cuda")
+    w = torch.empty(n, dtype=F64, device="cuda")
+    r = torch.empty(n, dtype=F64, device="cuda")
+    hist = []
+    it, conv = 0, False
+    r.copy_(rhs)
+    beta = bnorm
+    while it < max_iter and not conv:
+        lib.bddc_norm2(r, n, scal, partial, nblk, st)
+        beta = float(scal[0].item())
+        if beta <= rel_tol * bnorm:
+            conv = True
+            break
+        lib.bddc_scale_copy(r, n, scal, V[0], st)
+        H = np.zeros((restart + 1, restart))
+        e1 = np.zeros(restart + 1)
+        e1[0] = beta
+        y = np.zeros(0)
+        m = 0
+        for j in range(restart):
+            pc.apply_device(V[j], out=Z[j])
+            operator.apply_device(Z[j], out=w)
+            m = j + 1
+            lib.bddc_multi_dot(V.buf, n, m, w, h1, partial, nblk, 0, st)
+            lib.bddc_multi_axpy(V.buf, n, m, h1, -1.0, w, st)
+            lib.bddc_multi_dot(V.buf, n, m, w, scal, partial, nblk, 0, st)
+            lib.bddc_multi_axpy(V.buf, n, m, scal, -1.0, w, st)
+            lib.bddc_norm2(w, n, scal[m:], partial, nblk, st)
+            hs = scal[:m + 1].cpu().numpy()
+            H[:m, j] = h1[:m].cpu().numpy() + hs[:m]
+            hn = float(hs[m])
+            H[m, j] = hn
+            y = scipy.linalg.lstsq(H[:m + 1, :m], e1[:m + 1], lapack_driver="gelsd")[0]
+            res = float(np.linalg.norm(e1[:m + 1] - H[:m + 1, :m] @ y))
+            it += 1
+            hist.append(res / bnorm)
+            if res <= rel_tol * bnorm or hn <= 1e-14 * beta or it >= max_iter:
+                break
+            lib.bddc_scale_copy(w, n, scal[m:], V[j + 1], st)
+        # x += Z y ; true residual r = b - S_hat x for the next cycle / the check
+        lib.bddc_multi_axpy(Z.buf, n, m, dev_f64(y), 1.0, x, st)
+        operator.apply_device(x, out=w)
+        torch.sub(rhs, w, out=r)
+        lib.bddc_norm2(r, n, scal, partial, nblk, st)
+        true_rel = float(scal[0].item()) / bnorm
+        if hist:
+            hist[-1] = true_rel
+        conv = true_rel <= rel_tol
+        if m and H[m, m - 1] <= 1e-14 * beta and not conv:
+            break  # breakdown without convergence
+    return it, conv, x, hist, hist
 
 
 def recover_device(ls, u_hat):

@@ -11,7 +11,8 @@ import numpy as np
 import torch
 
 from .engine import (DeviceInterfaceOperator, DevicePreconditioner, DevicePrimalSpace,
-                     DeviceScaling, LocalSystem, PhaseTimer, gmres_device, recover_device,
+                     DeviceScaling, LocalSystem, PhaseTimer, gmres_device, gmres_right_device,
+                     recover_device,
                      upload_inputs)
 from .plan import Plan
 
@@ -22,7 +23,7 @@ class Result:
 
 def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8, max_iter=300,
         plan=None, inputs=None, timings=True, keep=False, kernel_timing=False,
-        dplan=None, comm=None):
+        dplan=None, comm=None, side="left", restart=200):
     """Run the whole hot path; returns a Result with counts, solutions
     (device tensors) and phase times in ms (CUDA events).
 
@@ -51,7 +52,10 @@ def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8,
     op = DeviceInterfaceOperator(ls)
     tm.mark("gmres")
     rhs = op.rhs_device()
-    it, conv, x, th, ph = gmres_device(op, rhs, pc, rel_tol, max_iter)
+    if side == "left":  # the reference's full left-preconditioned GMRES
+        it, conv, x, th, ph = gmres_device(op, rhs, pc, rel_tol, max_iter)
+    else:  # right-preconditioned GMRES(restart), BASELINE.json's variant
+        it, conv, x, th, ph = gmres_right_device(op, rhs, pc, rel_tol, max_iter, restart)
     tm.mark("recover")
     u = recover_device(ls, x)
     tm.mark("end")

@@ -8,7 +8,7 @@ import numpy as np
 import torch
 
 from .engine import (DeviceInterfaceOperator, DevicePreconditioner, NumericalError, dev_f64,
-                     dev_i64, gmres_device, recover_device)
+                     dev_i64, gmres_device, gmres_right_device, recover_device)
 
 F64 = torch.float64
 
@@ -76,15 +76,26 @@ def interface_rhs(ops, n):
     return InterfaceOperator(ops[0].ls).rhs_device().cpu().numpy()
 
 
-def gmres_solve(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
-    """Full left-preconditioned GMRES (solver.py:262-315) on the device."""
+def gmres_solve(operator, rhs, pc, rel_tol=1e-8, max_iter=300, side="left", restart=None):
+    """Full left-preconditioned GMRES (solver.py:262-315) on the device.
+
+    side="right" (with restart, default 200): right-preconditioned restarted
+    GMRES, the variant BASELINE.json names (not in the reference, SPEC.md:555);
+    its histories are the true relative residuals."""
     if not isinstance(operator, DeviceInterfaceOperator) or not isinstance(pc, DevicePreconditioner):
         raise TypeError("gmres_solve runs on the device: pass interface_operator(...) and "
                         "build_preconditioner(...) objects from this package")
     t0 = time.perf_counter()
     rhs_d = rhs if isinstance(rhs, torch.Tensor) else dev_f64(rhs)
-    it, conv, x, th, ph = gmres_device(operator, rhs_d.to(dtype=F64, device="cuda"), pc,
-                                       rel_tol, max_iter)
+    if side == "left":
+        it, conv, x, th, ph = gmres_device(operator, rhs_d.to(dtype=F64, device="cuda"), pc,
+                                           rel_tol, max_iter)
+    elif side == "right":
+        it, conv, x, th, ph = gmres_right_device(operator, rhs_d.to(dtype=F64, device="cuda"), pc,
+                                                 rel_tol, max_iter,
+                                                 200 if restart is None else restart)
+    else:
+        raise ValueError(f"unknown preconditioning side {side!r}")
     return SolveReport(it, conv, x.cpu().numpy(), th, ph, solve_time=time.perf_counter() - t0)
 
 

@@ -203,3 +203,28 @@ def test_dual_certificate_full_path_matches_certified(monkeypatch):
     x, y = a.solution.cpu().numpy(), b.solution.cpu().numpy()
     assert np.linalg.norm(x - y) <= 1e-12 * np.linalg.norm(y)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("restart", [200, 4])
+def test_right_preconditioned_restarted_gmres(restart):
+    """BASELINE.json's GMRES variant (right preconditioning, restart): converges
+    in the true residual and agrees with the reference's left-preconditioned
+    solve and with the reference GMRES solution (golden)."""
+    P = _api()
+    g = golden("jump")
+    system, part, globs, ops, scaling = _setup("jump")
+    n = globs.interface_nodes.size
+    operator, rhs = P.interface_operator(ops, n), P.interface_rhs(ops, n)
+    basis, _ = P.adaptive_primal_space(globs, ops, scaling, THETA_F, 10.0, "new")
+    pc = P.build_preconditioner(ops, basis, scaling)
+    left = P.gmres_solve(operator, rhs, pc)
+    right = P.gmres_solve(operator, rhs, pc, side="right", restart=restart)
+    assert right.converged and right.residual_history[-1] <= 1e-8
+    res = np.linalg.norm(rhs - operator(right.solution)) / np.linalg.norm(rhs)
+    assert res <= 1e-8
+    if restart >= left.iterations:  # same Krylov space: counts within one
+        assert abs(right.iterations - left.iterations) <= 2
+    ref = g["new_solution"]
+    assert np.linalg.norm(right.solution - ref) <= 1e-6 * np.linalg.norm(ref)
+    with pytest.raises(ValueError):
+        P.gmres_solve(operator, rhs, pc, side="middle")

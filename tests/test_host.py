@@ -134,3 +134,25 @@ def test_coarse_envelope_exact(seed):
         t[f:k] -= A[f:k, k:k + w] @ t[k:k + w]
     x = np.linalg.solve(Cn, b)
     assert np.abs(t - x).max() <= 1e-12 * np.abs(x).max()
+
+
+@pytest.mark.parametrize("config", [1, 2, 3, 4, 5])
+def test_device_fields_reproduce_coefficient_callables(config):
+    """The affine fields handed to the device element kernel evaluate to the
+    same velocity / viscosity as the host callables of every BASELINE config."""
+    from paper_2501_01676_b200 import configs
+
+    n = 8
+    prob = configs.build_problem(config, n=n, subs=2 if config != 4 else 16)
+    c = prob.coeffs
+    df = c.device_fields
+    rng = np.random.default_rng(config)
+    pts = rng.uniform(0.0, 1.0, size=(50, 3))
+    a_host = np.asarray(c.velocity(pts), dtype=float)
+    a_dev = pts @ np.asarray(df.velocity_matrix).T + np.asarray(df.velocity_offset)
+    np.testing.assert_allclose(a_dev, a_host, rtol=0, atol=1e-15)
+    assert np.all(np.asarray(c.reaction(pts)) == df.reaction)
+    assert np.all(np.asarray(c.source(pts)) == df.source)
+    m = prob.mesh.n_elements
+    nu_dev = np.asarray(df.viscosity_table)[np.arange(m) % df.viscosity_period]
+    np.testing.assert_array_equal(nu_dev, prob.system.viscosity)
