@@ -318,14 +318,33 @@ int bddc_pc_local_solve(const int* nB, const long long* soff, const long long* v
                         const int* pstart, const long long* poff, const double* G, double* cvals,
                         int nbatch, int max_nB, cudaStream_t stream);
 
-/* MP = e - Z Sbar[:, P], RP = e - Z^T Sbar[P, :]^T and C_i = Sbar[P, :] MP^T per
- * subdomain through the dual-block LU (Z = Sdd^-1 embedded).
- * replaces the coarse basis / coarse matrix assembly of solver.py:99-134. */
+/* Householder-path fusion of the S-bar transform and the dual embedding, one
+ * CTA per (glob slot, subdomain): Sbar = Q S Q^T (reflectors HV, r), then Z =
+ * embedded dual block (identity on primal rows / columns), Srows[q] =
+ * Sbar[ppos_q, :] and Scols[q] = Sbar[:, ppos_q] (n_p x nB at poff); pidx: per
+ * local B position its primal index or -1.  max_rows_block: largest glob size;
+ * blocks up to 200 KB are staged in shared memory.  replaces solver.py:85-99. */
+int bddc_pc_transform_embed(const int* nB, const long long* soff, const long long* voff,
+                            const int* sub_glob_start, const int* sub_globs,
+                            const int* sub_glob_boff, const int* kind, const int* gsize,
+                            const int* r, const double* HV, const long long* q_off,
+                            const int* pidx, const long long* poff, const double* S, double* Z,
+                            double* Srows, double* Scols, int nbatch, int max_globs,
+                            int max_rows_block, int max_nB, cudaStream_t stream);
+
+/* Srows / Scols (as above) from a full Sbar (dense-Q path). */
+int bddc_pc_primal_extract(const int* nB, const long long* soff, const long long* voff,
+                           const int* pidx, const long long* poff, const double* Sbar,
+                           double* Srows, double* Scols, int nbatch, cudaStream_t stream);
+
+/* Primal pieces through the dual LU: MP = e_P - Z Sbar[:, P], RP = e_P -
+ * Z^T Sbar[P, :]^T, coarse blocks C_i = Sbar[P, :] MP (Srows / Scols: the
+ * compact primal rows / columns).  replaces solver.py:100-110. */
 int bddc_pc_primal_pieces_lu(const int* nB, const long long* soff, const long long* voff,
                              const unsigned char* primal_mask, const int* pstart, const int* ppos,
-                             const long long* poff, const double* Sbar, const double* LU,
-                             double* MP, double* RP, double* Cl, const long long* coff,
-                             int nbatch, int max_nB, cudaStream_t stream);
+                             const long long* poff, const double* Srows, const double* Scols,
+                             const double* LU, double* MP, double* RP, double* Cl,
+                             const long long* coff, int nbatch, int max_nB, cudaStream_t stream);
 
 /* coarse[g,g] += contrib.  replaces solver.py:106. */
 int bddc_coarse_scatter(const int* pstart, const int* pgid, const double* Cl,

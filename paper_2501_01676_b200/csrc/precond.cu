@@ -326,6 +326,105 @@ __global__ void __launch_bounds__(256) transform_refl_kernel(
   }
 }
 
+
+// Sbar = Q S Q^T (Householder Q), then in the same pass: the compact primal
+// rows / columns of Sbar (Srows[q] = Sbar[ppos_q, :], Scols[q] = Sbar[:, ppos_q],
+// n_p x n at poff) and the embedded dual block Z (identity on primal rows and
+// columns, Sbar elsewhere) -- the inputs of the dual LU and the primal pieces.
+// CTA (k, b): glob slot k of subdomain b = rows [bo, bo + ng), staged in shared
+// memory (SMEM) or worked on in place in Z's rows.
+template <bool SMEM>
+__global__ void __launch_bounds__(256) transform_embed_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ soff,
+    const long long* __restrict__ voff, const int* __restrict__ sub_glob_start,
+    const int* __restrict__ sub_globs, const int* __restrict__ sub_glob_boff,
+    const int* __restrict__ kind, const int* __restrict__ gsize, const int* __restrict__ r,
+    const double* __restrict__ HV, const long long* __restrict__ q_off,
+    const int* __restrict__ pidx, const long long* __restrict__ poff,
+    const double* __restrict__ S, double* __restrict__ Z, double* __restrict__ Srows,
+    double* __restrict__ Scols) {
+  extern __shared__ double xs[];
+  const int b = blockIdx.y;
+  const int kk = sub_glob_start[b] + blockIdx.x;
+  if (kk >= sub_glob_start[b + 1]) return;
+  const int n = nB[b];
+  const int g = sub_globs[kk], ng = gsize[g], bo = sub_glob_boff[kk];
+  const double* Sb = S + soff[b] + (long long)bo * n;
+  double* Zb = Z + soff[b] + (long long)bo * n;
+  double* X = SMEM ? xs : Zb;
+  const int nref = (kind[g] == 2 || ng == 1) ? 0 : min(r[g], ng);
+  const double* Hg = HV + q_off[g];
+  // left: X = Q_g S[rows of g]   (thread per column)
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    if (nref == 0) {
+      for (int i = 0; i < ng; ++i) X[(long long)i * n + c] = Sb[(long long)i * n + c];
+      continue;
+    }
+    for (int j = 0; j < nref; ++j) {
+      const double* src = j == 0 ? Sb : X;
+      const double* w = Hg + j * ng;
+      double d = 0.0;
+      for (int i = j; i < ng; ++i) d += w[i] * src[(long long)i * n + c];
+      for (int i = 0; i < ng; ++i)
+        X[(long long)i * n + c] = src[(long long)i * n + c] - (i < j ? 0.0 : d * w[i]);
+    }
+  }
+  __syncthreads();
+  // right: X <- X Q^T on every glob column block (warp per row)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int k0 = sub_glob_start[b], k1 = sub_glob_start[b + 1];
+  for (int row = warp; row < ng; row += nw) {
+    double* xr = X + (long long)row * n;
+    for (int k = k0; k < k1; ++k) {
+      const int h = sub_globs[k], nh = gsize[h], bh = sub_glob_boff[k];
+      const int nrh = (kind[h] == 2 || nh == 1) ? 0 : min(r[h], nh);
+      const double* Hh = HV + q_off[h];
+      for (int j = 0; j < nrh; ++j) {
+        const double* w = Hh + j * nh;
+        double d = 0.0;
+        for (int i = j + lane; i < nh; i += 32) d += xr[bh + i] * w[i];
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        for (int i = j + lane; i < nh; i += 32) xr[bh + i] -= d * w[i];
+        __syncwarp();
+      }
+    }
+  }
+  __syncthreads();
+  // compact primal rows / columns and the embedded dual block
+  const int* pi = pidx + voff[b];
+  double* Sr = Srows + poff[b];
+  double* Sc = Scols + poff[b];
+  for (long long idx = threadIdx.x; idx < (long long)ng * n; idx += blockDim.x) {
+    const int i = (int)(idx / n), c = (int)(idx - (long long)i * n);
+    const int rho = bo + i;
+    const double v = X[idx];
+    const int qr = pi[rho], qc = pi[c];
+    if (qr >= 0) Sr[(long long)qr * n + c] = v;
+    if (qc >= 0) Sc[(long long)qc * n + rho] = v;
+    Zb[idx] = (qr >= 0 || qc >= 0) ? (rho == c ? 1.0 : 0.0) : v;
+  }
+}
+
+// compact primal rows / columns of a full Sbar (dense-Q path)
+__global__ void primal_extract_kernel(const int* __restrict__ nB, const long long* __restrict__ soff,
+                                      const long long* __restrict__ voff,
+                                      const int* __restrict__ pidx,
+                                      const long long* __restrict__ poff,
+                                      const double* __restrict__ Sbar, double* __restrict__ Srows,
+                                      double* __restrict__ Scols) {
+  const int b = blockIdx.y;
+  const int n = nB[b];
+  const int* pi = pidx + voff[b];
+  const double* Sb = Sbar + soff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int rr = (int)(idx / n), c = (int)(idx - (long long)rr * n);
+    const int qr = pi[rr], qc = pi[c];
+    if (qr >= 0) Srows[poff[b] + (long long)qr * n + c] = Sb[idx];
+    if (qc >= 0) Scols[poff[b] + (long long)qc * n + rr] = Sb[idx];
+  }
+}
+
 // dst block = src block^T for square blocks (size[gidx[i]]) at off[i]
 __global__ void transpose_blocks_kernel(const double* __restrict__ src, double* __restrict__ dst,
                                         const long long* __restrict__ off,
@@ -620,9 +719,9 @@ __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
     const int* __restrict__ nB, const long long* __restrict__ soff,
     const long long* __restrict__ voff, const unsigned char* __restrict__ primal_mask,
     const int* __restrict__ pstart, const int* __restrict__ ppos,
-    const long long* __restrict__ poff, const double* __restrict__ Sbar,
-    const double* __restrict__ LU, double* __restrict__ MP, double* __restrict__ RP,
-    double* __restrict__ Cl, const long long* __restrict__ coff) {
+    const long long* __restrict__ poff, const double* __restrict__ Srows,
+    const double* __restrict__ Scols, const double* __restrict__ LU, double* __restrict__ MP,
+    double* __restrict__ RP, double* __restrict__ Cl, const long long* __restrict__ coff) {
   extern __shared__ double psm[];
   const int b = blockIdx.x;
   const int n = nB[b];
@@ -632,7 +731,8 @@ __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
   double* X = psm;                      // n x XS
   double* tmp = psm + n * XS;           // 64 x XS
   double* red = tmp + 64 * XS;          // blockDim x kPL
-  const double* S = Sbar + soff[b];
+  const double* Sr = Srows + poff[b];  // Sbar[ppos_q, :] as row q (n_p x n)
+  const double* Sc = Scols + poff[b];  // Sbar[:, ppos_q] as row q
   const double* L = LU + soff[b];
   const unsigned char* pm = primal_mask + voff[b];
   double* Mb = MP + poff[b];
@@ -641,7 +741,7 @@ __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
     const int pc_n = min(kPL, np - c0);
     for (int idx = threadIdx.x; idx < n * kPL; idx += blockDim.x) {
       const int r = idx / kPL, q = idx - r * kPL;
-      X[r * XS + q] = (q < pc_n && !pm[r]) ? S[(long long)r * n + ppos[p0 + c0 + q]] : 0.0;
+      X[r * XS + q] = (q < pc_n && !pm[r]) ? Sc[(long long)(c0 + q) * n + r] : 0.0;
     }
     __syncthreads();
     lus::lu_solve<kPL, false>(L, n, X, tmp, red);
@@ -652,7 +752,7 @@ __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
     __syncthreads();
     for (int idx = threadIdx.x; idx < n * kPL; idx += blockDim.x) {
       const int q = idx / n, r = idx - q * n;  // coalesced along the Sbar row
-      X[r * XS + q] = (q < pc_n && !pm[r]) ? S[(long long)ppos[p0 + c0 + q] * n + r] : 0.0;
+      X[r * XS + q] = (q < pc_n && !pm[r]) ? Sr[(long long)(c0 + q) * n + r] : 0.0;
     }
     __syncthreads();
     lus::lu_solve<kPL, true>(L, n, X, tmp, red);
@@ -666,9 +766,8 @@ __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int i = warp; i < np * np; i += nw) {
     const int p = i / np, q = i - p * np;
-    const int pr = ppos[p0 + p];
     double v = 0.0;
-    for (int k = lane; k < n; k += 32) v += S[(long long)pr * n + k] * Mb[(long long)q * n + k];
+    for (int k = lane; k < n; k += 32) v += Sr[(long long)p * n + k] * Mb[(long long)q * n + k];
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if (lane == 0) C[i] = v;
   }
@@ -1249,17 +1348,56 @@ int bddc_pc_local_solve(const int* nB, const long long* soff, const long long* v
   return pc_status();
 }
 
+int bddc_pc_transform_embed(const int* nB, const long long* soff, const long long* voff,
+                            const int* sub_glob_start, const int* sub_globs,
+                            const int* sub_glob_boff, const int* kind, const int* gsize,
+                            const int* r, const double* HV, const long long* q_off,
+                            const int* pidx, const long long* poff, const double* S, double* Z,
+                            double* Srows, double* Scols, int nbatch, int max_globs,
+                            int max_rows_block, int max_nB, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const long long bytes = (long long)max_rows_block * max_nB * (long long)sizeof(double);
+  dim3 grid((unsigned)max_globs, (unsigned)nbatch);
+  if (bytes <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(transform_embed_kernel<true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    transform_embed_kernel<true><<<grid, 256, (size_t)bytes, stream>>>(
+        nB, soff, voff, sub_glob_start, sub_globs, sub_glob_boff, kind, gsize, r, HV, q_off, pidx,
+        poff, S, Z, Srows, Scols);
+  } else {
+    transform_embed_kernel<false><<<grid, 256, 0, stream>>>(
+        nB, soff, voff, sub_glob_start, sub_globs, sub_glob_boff, kind, gsize, r, HV, q_off, pidx,
+        poff, S, Z, Srows, Scols);
+  }
+  bddc_note_launches(1);
+  return pc_status();
+}
+
+int bddc_pc_primal_extract(const int* nB, const long long* soff, const long long* voff,
+                           const int* pidx, const long long* poff, const double* Sbar,
+                           double* Srows, double* Scols, int nbatch, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  primal_extract_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(nB, soff, voff, pidx, poff, Sbar,
+                                                              Srows, Scols);
+  bddc_note_launches(1);
+  return pc_status();
+}
+
 int bddc_pc_primal_pieces_lu(const int* nB, const long long* soff, const long long* voff,
                              const unsigned char* primal_mask, const int* pstart, const int* ppos,
-                             const long long* poff, const double* Sbar, const double* LU,
-                             double* MP, double* RP, double* Cl, const long long* coff,
-                             int nbatch, int max_nB, cudaStream_t stream) {
+                             const long long* poff, const double* Srows, const double* Scols,
+                             const double* LU, double* MP, double* RP, double* Cl,
+                             const long long* coff, int nbatch, int max_nB, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   const int smem = (max_nB * lus::xstride<kPL>() + 64 * lus::xstride<kPL>() + 256 * kPL) * (int)sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(primal_pieces_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   primal_pieces_lu_kernel<<<nbatch, 256, smem, stream>>>(nB, soff, voff, primal_mask, pstart, ppos,
-                                                         poff, Sbar, LU, MP, RP, Cl, coff);
+                                                         poff, Srows, Scols, LU, MP, RP, Cl, coff);
   bddc_note_launches(1);
   return pc_status();
 }

@@ -14,6 +14,7 @@ exchanged and the code path is the single-GPU one.
 """
 
 import ctypes
+import os
 
 import numpy as np
 import scipy.linalg
@@ -23,6 +24,7 @@ from ._lib import lib, require_cuda, stream
 from .plan import Plan, _excl, _ranges
 
 F64 = torch.float64
+EMBED_SMEM = bool(int(os.environ.get("BDDC_EMBED_SMEM", "0")))  # fused transform staging
 PANEL = 128  # elimination panel width (two 64-wide sub-panels; DMMA trailing update with K = 128)
 
 
@@ -800,14 +802,26 @@ class DevicePreconditioner:
         TT = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
         lib.bddc_pc_ttblocks(d.slot_glob, d.gsize, Q, q_off, scaling.D, d.sh_doff, TT,
                              int(p.sh_sub.size), st)
-        Sbar = torch.empty(p.S_total, dtype=F64, device="cuda")
-        tmp = torch.empty(p.S_total, dtype=F64, device="cuda")
-        if householder:
-            lib.bddc_pc_transform_refl(d.nB, d.soff, d.sub_glob_start, d.sub_globs,
-                                       d.sub_glob_boff, d.kind, d.gsize, r_d, HV, q_off, ls.S,
-                                       Sbar, p.N, st)
+        npn = max(int(poff[-1]), 1)
+        # per local B position: its primal index (or -1), for the compact Sbar rows / columns
+        pidx = np.full(int(p.voff[-1]), -1, dtype=np.int32)
+        pidx[p.voff[psub] + ppos] = (np.arange(ppos.size) - pstart[psub]).astype(np.int32)
+        d_pidx = dev_i32(pidx)
+        d_poff_all = dev_i64(poff[:-1])
+        Srows = torch.empty(npn, dtype=F64, device="cuda")
+        Scols = torch.empty(npn, dtype=F64, device="cuda")
+        Z = torch.empty(p.S_total, dtype=F64, device="cuda")
+        if householder:  # Sbar, compact primal rows / columns and Z in one pass
+            lib.bddc_pc_transform_embed(d.nB, d.soff, d.voff, d.sub_glob_start, d.sub_globs,
+                                        d.sub_glob_boff, d.kind, d.gsize, r_d, HV, q_off, d_pidx,
+                                        d_poff_all, ls.S, Z, Srows, Scols, p.N,
+                                        int(np.diff(p.sub_glob_start).max()),
+                                        int(p.gsize.max()) if EMBED_SMEM else 1 << 30,
+                                        int(p.nB.max()), st)
             del HV
         else:  # dense block products with the given Q
+            Sbar = torch.empty(p.S_total, dtype=F64, device="cuda")
+            tmp = torch.empty(p.S_total, dtype=F64, device="cuda")
             QT = torch.empty(int(Q.numel()), dtype=F64, device="cuda")
             lib.bddc_pc_transform_schur(d.nB, d.soff, d.sub_glob_start, p.N, d.sub_globs,
                                         d.sub_glob_boff, d.sub_glob_sh, d.gsize, Q, q_off, QT,
@@ -815,16 +829,21 @@ class DevicePreconditioner:
                                         int(p.gsize.max()),
                                         int(np.diff(p.sub_glob_start).max()), ls.S, tmp, Sbar,
                                         st)
-            del QT
-        Z = torch.empty(p.S_total, dtype=F64, device="cuda")
-        lib.bddc_pc_dual_embed(d.nB, d.soff, d.voff, d_mask, Sbar, Z, tmp, p.N, st)
+            del QT, tmp
+            lib.bddc_pc_dual_embed(d.nB, d.soff, d.voff, d_mask, Sbar, Z, None, p.N, st)
+            lib.bddc_pc_primal_extract(d.nB, d.soff, d.voff, d_pidx, d_poff_all, Sbar, Srows,
+                                       Scols, p.N, st)
+            del Sbar
         # certificate: LDL^T of sym(Sbar_dd) must have positive pivots (solver.py:91-98)
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
         nbmax = int(p.nB.max())
         if not self._dual_pd_certified(ls):
-            lib.bddc_schur_eliminate(tmp, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax,
+            Csym = Z.clone()  # sym(Z): sym(Sbar_dd) embedded with the identity
+            lib.bddc_symmetrize(Csym, d.soff, d.nB, p.N, st)
+            lib.bddc_schur_eliminate(Csym, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax,
                                      nbmax, PANEL, pinv, 4096, 0, status, 1, None, 0, st)
+            del Csym
             bad = _first_bad(status)
             if bad is not None:
                 raise NumericalError(
@@ -841,13 +860,13 @@ class DevicePreconditioner:
         lib.bddc_lu_diag_pinv(Z, d.soff, d.nB, p.N, nbmax, pinv_all, 4096, p.N * 4096, st)
         del pinv_all
         self.LU, self.TT, self.d_mask = Z, TT, d_mask
-        npn = max(int(poff[-1]), 1)
         MP = torch.empty(npn, dtype=F64, device="cuda")
         RP = torch.empty(npn, dtype=F64, device="cuda")
         multi = _multi(self.comm)
         Clg = (torch.zeros if multi else torch.empty)(max(int(gcoff[-1]), 1), dtype=F64, device="cuda")
         lib.bddc_pc_primal_pieces_lu(d.nB, d.soff, d.voff, d_mask, self.d_pstart, self.d_ppos,
-                                     self.d_poff, Sbar, Z, MP, RP, Clg[c0:], d_coff, p.N, nbmax, st)
+                                     self.d_poff, Srows, Scols, Z, MP, RP, Clg[c0:], d_coff, p.N,
+                                     nbmax, st)
         self.G = torch.empty(npn, dtype=F64, device="cuda")
         self.Nt = torch.empty(npn, dtype=F64, device="cuda")
         lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
@@ -856,7 +875,7 @@ class DevicePreconditioner:
         lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
                                   d.sub_glob_sh, d.gsize, d.sh_doff, TT, self.d_pstart,
                                   self.d_poff, MP, self.Nt, p.N, st)
-        del Sbar, tmp, MP, RP, pinv
+        del Srows, Scols, MP, RP, pinv
         nc = self.n_primal
         C = torch.zeros(nc * nc, dtype=F64, device="cuda")
         _allreduce(self.comm, Clg)

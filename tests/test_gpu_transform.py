@@ -68,3 +68,65 @@ def test_reflector_basis_and_transform():
     torch.cuda.synchronize()
     a, b = Sb1.cpu().numpy(), Sb2.cpu().numpy()
     assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
+
+
+@pytest.mark.parametrize("smem", [True, False])
+def test_fused_transform_embed_matches_two_pass(smem, monkeypatch):
+    """bddc_pc_transform_embed (Sbar, embedded dual block Z, compact primal
+    rows / columns in one pass) equals the two-pass reflector transform +
+    dual embedding + extraction."""
+    import torch
+
+    from paper_2501_01676_b200 import configs, pipeline
+    from paper_2501_01676_b200._lib import lib, stream
+    from paper_2501_01676_b200.engine import dev_i32, dev_i64
+    from paper_2501_01676_b200.plan import _excl, _ranges
+
+    prob = configs.build_problem(2, n=16, subs=2)
+    res = pipeline.run(prob.system, prob.partition, prob.globs, 1.05, 1.05, "new", keep=True)
+    ls, ps = res.ls, res.space
+    p, d, st = ls.plan, ls.d, stream()
+    r = ps.r_host
+    Q = ps.Q.clone()
+    HV = torch.zeros_like(Q)
+    w_sz = np.where(p.kind == 2, 0, p.gsize.astype(np.int64) * np.minimum(r, p.gsize))
+    w_off = _excl(w_sz)
+    W = torch.empty(max(int(w_off[-1]), 1), dtype=torch.float64, device="cuda")
+    r_d = dev_i32(r)
+    lib.bddc_pc_glob_reflectors(d.kind, d.gsize, r_d, Q, ps.d_q_off, HV, W, dev_i64(w_off[:-1]),
+                                p.G, int(p.gsize.max()), st)
+    cnt = r[p.sub_globs]
+    np_sub = np.add.reduceat(cnt, p.sub_glob_start[:-1].astype(np.int64))
+    pstart = _excl(np_sub)
+    ppos = _ranges(p.sub_glob_boff, cnt)
+    psub = np.repeat(np.arange(p.N), np_sub)
+    pidx = np.full(int(p.voff[-1]), -1, dtype=np.int32)
+    pidx[p.voff[psub] + ppos] = (np.arange(ppos.size) - pstart[psub]).astype(np.int32)
+    mask = (pidx >= 0).astype(np.uint8)
+    poff = _excl(np_sub * p.nB)
+    npn = int(poff[-1])
+    S = ls.S
+    f64 = dict(dtype=torch.float64, device="cuda")
+    # two-pass reference
+    Sbar = torch.empty_like(S)
+    lib.bddc_pc_transform_refl(d.nB, d.soff, d.sub_glob_start, d.sub_globs, d.sub_glob_boff,
+                               d.kind, d.gsize, r_d, HV, ps.d_q_off, S, Sbar, p.N, st)
+    Z0 = torch.empty_like(S)
+    lib.bddc_pc_dual_embed(d.nB, d.soff, d.voff, torch.from_numpy(mask).cuda(), Sbar, Z0, None,
+                           p.N, st)
+    Sr0, Sc0 = torch.empty(npn, **f64), torch.empty(npn, **f64)
+    lib.bddc_pc_primal_extract(d.nB, d.soff, d.voff, dev_i32(pidx), dev_i64(poff[:-1]), Sbar, Sr0,
+                               Sc0, p.N, st)
+    # fused (shared-memory staging or in place in Z)
+    Z1 = torch.empty_like(S)
+    Sr1, Sc1 = torch.empty(npn, **f64), torch.empty(npn, **f64)
+    rows_block = int(p.gsize.max()) if smem else 10 ** 6  # force the global-memory variant
+    lib.bddc_pc_transform_embed(d.nB, d.soff, d.voff, d.sub_glob_start, d.sub_globs,
+                                d.sub_glob_boff, d.kind, d.gsize, r_d, HV, ps.d_q_off,
+                                dev_i32(pidx), dev_i64(poff[:-1]), S, Z1, Sr1, Sc1, p.N,
+                                int(np.diff(p.sub_glob_start).max()), rows_block,
+                                int(p.nB.max()), st)
+    torch.cuda.synchronize()
+    for a, b in ((Z1, Z0), (Sr1, Sr0), (Sc1, Sc0)):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
