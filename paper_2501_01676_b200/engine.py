@@ -14,7 +14,6 @@ exchanged and the code path is the single-GPU one.
 """
 
 import ctypes
-import os
 
 import numpy as np
 import scipy.linalg
@@ -24,7 +23,6 @@ from ._lib import lib, require_cuda, stream
 from .plan import Plan, _excl, _ranges
 
 F64 = torch.float64
-EMBED_SMEM = bool(int(os.environ.get("BDDC_EMBED_SMEM", "0")))  # fused transform staging
 PANEL = 128  # elimination panel width (two 64-wide sub-panels; DMMA trailing update with K = 128)
 
 
@@ -815,8 +813,7 @@ class DevicePreconditioner:
             lib.bddc_pc_transform_embed(d.nB, d.soff, d.voff, d.sub_glob_start, d.sub_globs,
                                         d.sub_glob_boff, d.kind, d.gsize, r_d, HV, q_off, d_pidx,
                                         d_poff_all, ls.S, Z, Srows, Scols, p.N,
-                                        int(np.diff(p.sub_glob_start).max()),
-                                        int(p.gsize.max()) if EMBED_SMEM else 1 << 30,
+                                        int(np.diff(p.sub_glob_start).max()), 1 << 30,
                                         int(p.nB.max()), st)
             del HV
         else:  # dense block products with the given Q

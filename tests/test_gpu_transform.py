@@ -71,7 +71,7 @@ def test_reflector_basis_and_transform():
 
 
 @pytest.mark.parametrize("smem", [True, False])
-def test_fused_transform_embed_matches_two_pass(smem, monkeypatch):
+def test_fused_transform_embed_matches_two_pass(smem):
     """bddc_pc_transform_embed (Sbar, embedded dual block Z, compact primal
     rows / columns in one pass) equals the two-pass reflector transform +
     dual embedding + extraction."""
