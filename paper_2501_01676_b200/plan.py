@@ -253,14 +253,21 @@ class Plan:
                            _up(self.sh_boff, dv), nI.to(torch.int64), self.loc4_d, stream())
 
     def _node_maps_device(self, dv):
-        """node -> glob index and position in the glob (-1 off the interface)."""
-        gnodes = self._gnodes
-        gof = np.full(self.n_nodes, -1, dtype=np.int32)
-        pos = np.zeros(self.n_nodes, dtype=np.int32)
-        gof[gnodes] = np.repeat(np.arange(self.G, dtype=np.int32), self.gsize)
-        pos[gnodes] = (np.arange(gnodes.size) - np.repeat(_excl(self.gsize)[:-1], self.gsize)).astype(np.int32)
-        self._glob_of_node_d = _up(gof, dv)
-        self._pos_in_glob_d = _up(pos, dv)
+        """node -> glob index and position in the glob (-1 off the interface),
+        scattered on the device from the glob-ordered interface nodes."""
+        import torch
+
+        gn = _up(self._gnodes.astype(np.int64), dv)
+        gsz = _up(self.gsize.astype(np.int64), dv)
+        gid = torch.repeat_interleave(torch.arange(self.G, device=dv), gsz,
+                                      output_size=int(self._gnodes.size))
+        gst = torch.cumsum(gsz, 0) - gsz
+        gof = torch.full((self.n_nodes,), -1, dtype=torch.int32, device=dv)
+        pos = torch.zeros(self.n_nodes, dtype=torch.int32, device=dv)
+        gof[gn] = gid.to(torch.int32)
+        pos[gn] = (torch.arange(gn.numel(), device=dv) - gst[gid]).to(torch.int32)
+        self._glob_of_node_d = gof
+        self._pos_in_glob_d = pos
         self._iface_nodes_d = _up(self._iface_nodes, dv)
 
     def _layout(self):
