@@ -273,18 +273,18 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_row_kernel(
 // computed and each off-diagonal result is mirrored with that sign.
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ n, int k, int symmetric, NextPivot nx) {
+    const int* __restrict__ n, int k, int symmetric, NextPivot nx, int pw) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
   const int nb = n[b];
-  const int w = min(kTile, nb - k);
+  const int w = min(pw, nb - k);  // pivots of this step (panel width pw = 64 or 128)
   if (w <= 0) return;
   const int T = (nb + kTile - 1) / kTile;
   const int tm = blockIdx.x / T, tn = blockIdx.x - tm * T;
   if (tm >= T) return;
   const int r0 = tm * kTile, c0 = tn * kTile;
-  if (r0 == k || c0 == k) return;
+  if ((r0 >= k && r0 < k + pw) || (c0 >= k && c0 < k + pw)) return;
   if (symmetric && tn > tm) return;
   const int L = ld[b];
   double* M = base + off[b];
@@ -303,6 +303,87 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel
     if (threadIdx.x == 0 && bad && nx.status)
       atomicCAS(nx.status + b, 0, nx.require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
   }
+}
+
+// M[r0 + r][k + c] = sgn * M[k + c][r0 + r] for r < h, c < w, transposed through
+// shared memory (64 x 65 staging, 64 columns at a time) so that both the reads
+// (rows of the row panel) and the writes (rows of the column panel) are coalesced
+BDDC_DEV void gj_mirror_tile(double* M, long long L, int k, int w, int r0, int h, double sgn,
+                             double* st) {
+  for (int c0 = 0; c0 < w; c0 += kTile) {
+    const int wc = min(kTile, w - c0);
+    for (int idx = threadIdx.x; idx < h * wc; idx += blockDim.x) {
+      const int c = idx / h, r = idx - c * h;
+      st[c * 65 + r] = M[(long long)(k + c0 + c) * L + r0 + r];
+    }
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < h * wc; idx += blockDim.x) {
+      const int r = idx / wc, c = idx - r * wc;
+      M[(long long)(r0 + r) * L + k + c0 + c] = sgn * st[c * 65 + r];
+    }
+    __syncthreads();
+  }
+}
+
+// ---- symmetric Gauss-Jordan in 128-wide panels (K = 128 trailing updates) ----
+// pivot block of step k -> work (128 x 128, ld 128), identity beyond w
+__global__ void gj128_extract_kernel(const double* __restrict__ base,
+                                     const long long* __restrict__ off,
+                                     const int* __restrict__ ld, const int* __restrict__ n, int k,
+                                     double* __restrict__ work) {
+  const int b = blockIdx.x;
+  const int w = max(0, min(128, n[b] - k));
+  const double* M = base + off[b] + (long long)k * ld[b] + k;
+  double* W = work + (long long)b * 128 * 128;
+  for (int idx = threadIdx.x; idx < 128 * 128; idx += blockDim.x) {
+    const int r = idx >> 7, c = idx & 127;
+    W[idx] = (r < w && c < w) ? M[(long long)r * ld[b] + c] : (r == c ? 1.0 : 0.0);
+  }
+}
+
+// W = P A_(k, c0) in place (one 128 x 64 tile per CTA; BM = 128 so a single CTA
+// owns every row it overwrites); the pivot column tiles receive sym(P)
+__global__ void __launch_bounds__(512) gj128_row_kernel(double* __restrict__ base,
+                                                        const long long* __restrict__ off,
+                                                        const int* __restrict__ ld,
+                                                        const int* __restrict__ n, int k,
+                                                        const double* __restrict__ work) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmemT<128>& sm = *reinterpret_cast<TileSmemT<128>*>(smem_raw);
+  const int b = blockIdx.y;
+  const int nb = n[b];
+  const int w = min(128, nb - k);
+  if (w <= 0) return;
+  const int c0 = blockIdx.x * kTile;
+  if (c0 >= nb) return;
+  const long long L = ld[b];
+  double* M = base + off[b];
+  const double* P = work + (long long)b * 128 * 128;
+  if (c0 >= k && c0 < k + 128) {
+    const int cc = c0 - k, wc = min(kTile, w - cc);
+    for (int idx = threadIdx.x; idx < w * wc; idx += blockDim.x) {
+      const int r = idx / wc, c = idx - r * wc;
+      M[(long long)(k + r) * L + c0 + c] = 0.5 * (P[r * 128 + cc + c] + P[(cc + c) * 128 + r]);
+    }
+    return;
+  }
+  double* C = M + (long long)k * L + c0;
+  tile_mma_t<128>(C, L, w, min(kTile, nb - c0), P, 128, C, L, w, 1.0, 0.0, sm);
+}
+
+// column panel of step k = +-(row panel)^T (symmetric variant)
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj128_col_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ n, int k) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.y;
+  const int nb = n[b];
+  const int w = min(128, nb - k);
+  if (w <= 0) return;
+  const int r0 = blockIdx.x * kTile;
+  if (r0 >= nb || (r0 >= k && r0 < k + 128)) return;
+  gj_mirror_tile(base + off[b], ld[b], k, w, r0, min(kTile, nb - r0), r0 < k ? 1.0 : -1.0,
+                 reinterpret_cast<double*>(smem_raw));
 }
 
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
@@ -330,20 +411,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
     return;
   }
   if (symmetric) {  // column panel = +-(row panel)^T: + for processed rows (G_KK), - for G_JK
-    // transposed through shared memory so that both the reads (rows of the
-    // row panel) and the writes (rows of the column panel) are coalesced
-    const int h = min(kTile, nb - r0);
-    const double sgn = r0 < k ? 1.0 : -1.0;
-    double* st = reinterpret_cast<double*>(smem_raw);  // w x 65 staging tile
-    for (int idx = threadIdx.x; idx < h * w; idx += blockDim.x) {
-      const int c = idx / h, r = idx - c * h;
-      st[c * 65 + r] = M[(long long)(k + c) * L + r0 + r];
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < h * w; idx += blockDim.x) {
-      const int r = idx / w, c = idx - r * w;
-      M[(long long)(r0 + r) * L + k + c] = sgn * st[c * 65 + r];
-    }
+    gj_mirror_tile(M, L, k, w, r0, min(kTile, nb - r0), r0 < k ? 1.0 : -1.0,
+                   reinterpret_cast<double*>(smem_raw));
     return;
   }
   double* C = M + (long long)r0 * L + k;
@@ -662,9 +731,42 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
     gj_row_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride, symmetric);
     gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(
-        M, off, ld, n, k, symmetric, look && k + kTile < max_n ? nx : none);
+        M, off, ld, n, k, symmetric, look && k + kTile < max_n ? nx : none, kTile);
     gj_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride, symmetric);
+    bddc_note_launches(3);
+  }
+  return launch_status();
+}
+
+int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int* n, int nbatch,
+                       int max_n, double* work, const long long* work_off, const int* work_ld,
+                       const int* work_n, double* pinv_ws, int* status, int require_positive,
+                       cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = smem_tile_setup();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gj128_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileSmemT<128>));
+    cudaFuncSetAttribute(gj128_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  const int T = ceil_div(max_n, kTile);
+  const NextPivot none{nullptr, 0, nullptr, 0, nullptr, 0};
+  for (int k = 0; k < max_n; k += 128) {
+    gj128_extract_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work);
+    bddc_note_launches(1);
+    // P = (pivot block)^-1: symmetric 64-panel Gauss-Jordan on the 128 x 128 copies
+    // (positive LDL^T pivots <=> positive definite: the cho_factor criterion)
+    int rc = bddc_gj_inverse(work, work_off, work_ld, work_n, nbatch, 128, pinv_ws, 4096, status,
+                             require_positive, 1, stream);
+    if (rc) return rc;
+    gj128_row_kernel<<<dim3(T, nbatch), 512, sizeof(TileSmemT<128>), stream>>>(M, off, ld, n, k,
+                                                                               work);
+    gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 1,
+                                                                         none, 128);
+    gj128_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k);
     bddc_note_launches(3);
   }
   return launch_status();

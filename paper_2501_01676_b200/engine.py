@@ -172,9 +172,14 @@ class LocalSystem:
             Binv = self.Bsym.clone()
             status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
             pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
-            # Bsym is exactly symmetric (extract_schur): symmetric GJ, exact symmetric result
-            lib.bddc_gj_inverse(Binv, d.soff, d.nB, d.nB, p.N, int(p.nB.max()), pinv, 4096, status,
-                                1, 1, st)
+            # Bsym is exactly symmetric (extract_schur): symmetric GJ in 128-wide panels,
+            # exact symmetric result
+            work = torch.empty(p.N * 128 * 128, dtype=F64, device="cuda")
+            w_off = torch.arange(p.N, dtype=torch.int64, device="cuda") * (128 * 128)
+            w128 = torch.full((p.N,), 128, dtype=torch.int32, device="cuda")
+            lib.bddc_gj_inverse128(Binv, d.soff, d.nB, d.nB, p.N, int(p.nB.max()), work, w_off,
+                                   w128, w128, pinv, status, 1, st)
+            del work
             if before_check is not None:
                 before_check()
             bad = _first_bad(status)
