@@ -106,12 +106,8 @@ def best_threads(prob):
 
 def run_reference(args):
     rank, world, _ = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo")
-        if rank != 0:
-            dist.barrier()
-            return
+    if rank != 0:  # under torchrun only rank 0 runs the CPU reference arm
+        return
     prob = cpu_sample_problem(args.config, args.sample_n, args.sample_subs)
     threads, _ = best_threads(prob)
     for _ in range(max(args.warmup - 1, 0)):
@@ -129,15 +125,14 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tstep * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_desc(args.config, args.sample_n, args.sample_subs, prob),
+        "data": "synthetic",
+        "config": dict(workload_desc(args.config, args.sample_n, args.sample_subs, prob),
+                       parallelism=f"host CPU, {threads} BLAS thread(s) (no GPU)"),
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
 
 
 # ---------------------------------------------------------------------------
@@ -208,6 +203,19 @@ def fp64_peak():
         return max(v["dmma_m8n8k4_tflops"] for k, v in d.items() if k.startswith("tpb")), "measured DMMA m8n8k4 (profiles/fp64_peak_r01.json)"
     except (OSError, ValueError, KeyError):
         return 37.0, "fallback: DMMA m8n8k4 measured 37.1 TF/s on B200"
+
+
+def trailing_traffic():
+    """DRAM bytes per trailing-update launch from the committed ncu capture
+    (tools/traffic.py -> profiles/trailing_traffic_*.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "trailing_traffic_*.json")))
+    if not files:
+        return None, None
+    d = json.load(open(files[-1]))
+    return d["traffic_bytes_per_launch"], (f"{os.path.basename(files[-1])}: dram read+write per "
+                                          f"launch, mean over {d['mode0_launches']} launches of "
+                                          f"one cfg5 step (ncu --set full)")
 
 
 def hbm_peak():
@@ -367,6 +375,7 @@ def run_mine(args):
     if int(t_n.value) != n_trail * args.steps:
         raise RuntimeError(f"logged {t_n.value} trailing launches, expected {n_trail} x {args.steps}")
     peak, peak_src = fp64_peak()
+    traffic, traffic_src = trailing_traffic()
     achieved = tflops / (tms * 1e-3) / 1e12
     hbm, hbm_src = hbm_peak()
 
@@ -380,7 +389,8 @@ def run_mine(args):
             "kernel": "schur_trailing_kernel (batched trailing updates of the subdomain Schur "
                       "elimination and of the dual-block LU, DMMA m8n8k4)",
             "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": None,
+            "frac": achieved / peak, "traffic": traffic,
+            "traffic_source": traffic_src,
             "peak_source": peak_src,
             "algorithmic_flops_per_step": tflops, "launches_per_step": n_trail,
             "kernel_ms_per_step": tms,
