@@ -277,16 +277,23 @@ def run_mine(args):
     e0.record()
     phases = {}
     lib.bddc_trailing_log(1)  # CUDA events around the trailing launches, read after the loop
+    step_ev = [e0]
+    per_step_phases = []
     for _ in range(args.steps):
         res = step()
+        per_step_phases.append({k: round(v, 2) for k, v in res.times_ms.items()})
         for k, v in res.times_ms.items():
             phases[k] = phases.get(k, 0.0) + v / args.steps
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        step_ev.append(ev)
     e1.record()
     torch.cuda.synchronize()
     launches = (int(lib.bddc_launch_count()) - (GRAPH_STATS["captured"] - g0["captured"])
                 + (GRAPH_STATS["replayed"] - g0["replayed"])) // args.steps
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
+    ms_each = [round(step_ev[i].elapsed_time(step_ev[i + 1]), 3) for i in range(args.steps)]
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -407,7 +414,7 @@ def run_mine(args):
             "bytes_formula": "SURVEY 8(d) B_apply_local + coarse block-inverse operator bytes; "
                              "B_op = 8 sum nB^2 + 8 (3 sum nB + n_hat)",
         },
-        "phases_ms": phases,
+        "phases_ms": phases, "ms_each_step": ms_each, "phases_each_step": per_step_phases,
         "iterations": res.iterations, "converged": bool(res.converged),
         "pnumF": res.pnumF, "pnumE": res.pnumE, "n_vertex": res.n_vertex, "n_c": res.n_c,
         "host_preprocessing_s": t_pre,

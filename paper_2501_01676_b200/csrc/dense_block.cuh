@@ -65,9 +65,12 @@ BDDC_DEV void gemm_t(double* C, int ldc, const double* A, int lda, const double*
   __syncthreads();
 }
 
-// Same contract on the DMMA pipe (mma.sync m8n8k4 f64): each warp computes
-// 16 x 8 output tiles (two 8x8 accumulators sharing the B fragment), operands
-// read straight from shared or global memory with zero-fill at the edges.
+// Same contract on the DMMA pipe (mma.sync m8n8k4 f64): each warp computes up
+// to kGT 16 x 8 output tiles at once (two 8x8 accumulators per tile sharing
+// the B fragment), so 2 kGT independent DMMA chains hide the pipe latency;
+// operands read straight from shared or global memory with zero-fill at the
+// edges.
+constexpr int kGT = 4;
 template <bool TA, bool TB>
 BDDC_DEV void gemm_mma_t(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
                          int m, int n, int k, double alpha, double beta) {
@@ -75,35 +78,55 @@ BDDC_DEV void gemm_mma_t(double* C, int ldc, const double* A, int lda, const dou
   const int nw = (int)(blockDim.x >> 5);
   const int g = lane >> 2, t = lane & 3;
   const int mt = (m + 15) >> 4, nt = (n + 7) >> 3;
-  for (int tile = warp; tile < mt * nt; tile += nw) {
-    const int r0 = (tile / nt) * 16, c0 = (tile - (tile / nt) * nt) * 8;
-    const int ra = r0 + g, rb = r0 + 8 + g, cb = c0 + g;
-    double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+  const int ntiles = mt * nt;
+  for (int base = warp; base < ntiles; base += kGT * nw) {
+    int ra[kGT], rb[kGT], cb[kGT];
+    bool on[kGT];
+    double x0[kGT], x1[kGT], y0[kGT], y1[kGT];
+#pragma unroll
+    for (int i = 0; i < kGT; ++i) {
+      const int tile = base + i * nw;
+      on[i] = tile < ntiles;
+      const int tr = on[i] ? tile / nt : 0;
+      const int r0 = tr * 16, c0 = on[i] ? (tile - tr * nt) * 8 : 0;
+      ra[i] = r0 + g;
+      rb[i] = r0 + 8 + g;
+      cb[i] = c0 + g;
+      x0[i] = x1[i] = y0[i] = y1[i] = 0.0;
+    }
     for (int p = 0; p < k; p += 4) {
       const int kk = p + t;
-      double a0 = 0.0, a1 = 0.0, b = 0.0;
-      if (kk < k) {
-        if (ra < m) a0 = TA ? A[kk * lda + ra] : A[ra * lda + kk];
-        if (rb < m) a1 = TA ? A[kk * lda + rb] : A[rb * lda + kk];
-        if (cb < n) b = TB ? B[cb * ldb + kk] : B[kk * ldb + cb];
-      }
-      dmma_8x8x4(x0, x1, a0, b);
-      dmma_8x8x4(y0, y1, a1, b);
-    }
-    const int cc = c0 + 2 * t;
-    const double xs[2] = {x0, x1}, ys[2] = {y0, y1};
+      const bool kin = kk < k;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (cc + h >= n) continue;
-      if (ra < m) {
-        double v = alpha * xs[h];
-        if (beta != 0.0) v += beta * C[ra * ldc + cc + h];
-        C[ra * ldc + cc + h] = v;
+      for (int i = 0; i < kGT; ++i) {
+        double a0 = 0.0, a1 = 0.0, bv = 0.0;
+        if (on[i] && kin) {
+          if (ra[i] < m) a0 = TA ? A[kk * lda + ra[i]] : A[ra[i] * lda + kk];
+          if (rb[i] < m) a1 = TA ? A[kk * lda + rb[i]] : A[rb[i] * lda + kk];
+          if (cb[i] < n) bv = TB ? B[cb[i] * ldb + kk] : B[kk * ldb + cb[i]];
+        }
+        dmma_8x8x4(x0[i], x1[i], a0, bv);
+        dmma_8x8x4(y0[i], y1[i], a1, bv);
       }
-      if (rb < m) {
-        double v = alpha * ys[h];
-        if (beta != 0.0) v += beta * C[rb * ldc + cc + h];
-        C[rb * ldc + cc + h] = v;
+    }
+#pragma unroll
+    for (int i = 0; i < kGT; ++i) {
+      if (!on[i]) continue;
+      const int cc = cb[i] - g + 2 * t;
+      const double xs[2] = {x0[i], x1[i]}, ys[2] = {y0[i], y1[i]};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (cc + h >= n) continue;
+        if (ra[i] < m) {
+          double v = alpha * xs[h];
+          if (beta != 0.0) v += beta * C[ra[i] * ldc + cc + h];
+          C[ra[i] * ldc + cc + h] = v;
+        }
+        if (rb[i] < m) {
+          double v = alpha * ys[h];
+          if (beta != 0.0) v += beta * C[rb[i] * ldc + cc + h];
+          C[rb[i] * ldc + cc + h] = v;
+        }
       }
     }
   }

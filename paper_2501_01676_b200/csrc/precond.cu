@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(256) local_solve_kernel(
 // Primal pieces through the LU, one CTA per subdomain, 8 primal columns at a time:
 //   MP[p] = e_pc - Z Sbar[:, pc],  RP[p] = e_pc - Z^T Sbar[pc, :]^T,  C_i[p][q] = Sbar[pr, :] . MP[q]
 // (Z = Sdd^-1 embedded with zero primal rows / columns)
-constexpr int kPL = 16;
+constexpr int kPL = 8;
 __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
     const int* __restrict__ nB, const long long* __restrict__ soff,
     const long long* __restrict__ voff, const unsigned char* __restrict__ primal_mask,
