@@ -82,6 +82,15 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
                                int require_positive, double* piv_out, long long piv_stride,
                                cudaStream_t stream, double* host_trailing_ms);
 
+/* Converts the result of bddc_schur_eliminate with panel = 128 on square
+ * n x n matrices (npiv = nrows = ncols = n, pinv_step_stride != 0 so every
+ * 64-wide sub-panel keeps its inverse pivot block) into the 64-panel "rows
+ * below only" LU form that bddc_lu_diag_pinv / the local solves use:
+ * A21^(k2) = A[., k2] - A[., k1] W1_Q and W1 = W1_fixed + W1_Q W2 per panel.
+ * Part of replacing lu_factor(Stil) solver.py:99. */
+int bddc_lu128_fixup(double* M, const long long* off, const int* ld, const int* n, int nbatch,
+                     int max_n, cudaStream_t stream);
+
 /* Event log of the bddc_schur_eliminate trailing-update launches (bench
  * roofline measured over the timed region without synchronising inside it):
  * bddc_trailing_log(1) starts logging, bddc_trailing_collect() synchronises on

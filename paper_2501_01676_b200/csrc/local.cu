@@ -573,6 +573,34 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
   return launch_status();
 }
 
+// 128-wide panels -> the 64-wide "rows below only" LU form (lus::lu_solve):
+// for panel k (sub-panels k1 = k, k2 = k + 64)
+//   mode 0: column panel k2, rows >= k + 128:  A21^(k2) = A[., k2] - A[., k1] W1_Q
+//   mode 1: pivot rows k1, cols >= k + 128:    W1 = W1_fixed + W1_Q W2
+// with W1_Q = M[k1, k2 block] (= P1 A[k1, k2]) and W2 = M[k2 rows, >= k+128].
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) lu128_fixup_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ n, int k, int mode) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  const int nb = n[b];
+  const int k2 = k + kTile, s = k + 2 * kTile;
+  if (s >= nb) return;  // no second sub-panel with rows / columns beyond it
+  const int t0 = s + blockIdx.x * kTile;
+  if (t0 >= nb) return;
+  const int L = ld[b];
+  double* M = base + off[b];
+  const int w2 = min(kTile, nb - k2);
+  if (mode == 0) {
+    tile_mma(M + (long long)t0 * L + k2, L, min(kTile, nb - t0), w2, M + (long long)t0 * L + k, L,
+             M + (long long)k * L + k2, L, kTile, -1.0, 1.0, sm);
+  } else {
+    tile_mma(M + (long long)k * L + t0, L, kTile, min(kTile, nb - t0), M + (long long)k * L + k2, L,
+             M + (long long)k2 * L + t0, L, w2, 1.0, 1.0, sm);
+  }
+}
+
 // Optional event log of the trailing-update launches (bench roofline over the
 // timed region without a mid-step synchronisation): bddc_trailing_log(1)
 // starts it, bddc_trailing_collect() sums the logged durations and clears it.
@@ -605,9 +633,11 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
                                                    status, require_positive, piv_out, piv_stride);
   ++launches;
   for (int k = 0; k < max_npiv; k += panel) {
-    double* P = pinv_ws + (long long)(k / panel) * pinv_step_stride;
-    double* Pn = pinv_ws + (long long)(k / panel + 1) * pinv_step_stride;
-    const NextPivot nx_sub{P, pinv_stride, status, require_positive, piv_out, piv_stride};
+    // pivot inverses are kept per 64-wide sub-panel (step stride per 64 pivots)
+    double* P = pinv_ws + (long long)(k / kTile) * pinv_step_stride;
+    double* P2 = pinv_ws + (long long)(k / kTile + 1) * pinv_step_stride;
+    double* Pn = pinv_ws + (long long)((k + panel) / kTile) * pinv_step_stride;
+    const NextPivot nx_sub{P2, pinv_stride, status, require_positive, piv_out, piv_stride};
     const NextPivot nx_next{Pn, pinv_stride, status, require_positive, piv_out, piv_stride};
     bool next_done = false;
     // first (or only) 64-wide sub-panel: W1 = P1 A12 (P1 from the previous launch)
@@ -624,7 +654,7 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
       schur_trailing_kernel<<<dim3(cts, nbatch), kTileThreads, tsm, stream>>>(
           M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1, nx_sub);
       schur_row_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(
-          M, off, ld, npiv, ncols, k + kTile, P, pinv_stride, 0x7fffffff);
+          M, off, ld, npiv, ncols, k + kTile, P2, pinv_stride, 0x7fffffff);
       schur_fix_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k);
       launches += 3;
     }
@@ -735,6 +765,24 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
     gj_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride, symmetric);
     bddc_note_launches(3);
+  }
+  return launch_status();
+}
+
+int bddc_lu128_fixup(double* M, const long long* off, const int* ld, const int* n, int nbatch,
+                     int max_n, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = smem_tile_setup();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lu128_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  for (int k = 0; k + 2 * kTile < max_n; k += 2 * kTile) {
+    const int t = ceil_div(max_n - k - 2 * kTile, kTile);
+    lu128_fixup_kernel<<<dim3(t, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 0);
+    lu128_fixup_kernel<<<dim3(t, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 1);
+    bddc_note_launches(2);
   }
   return launch_status();
 }

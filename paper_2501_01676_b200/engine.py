@@ -246,13 +246,13 @@ def trailing_flops(plan, panel=PANEL, dual_lu=False):
     """Algorithmic flops of the Schur-elimination trailing updates (DMMA kernel,
     mode 0): sum over panels k and subdomains b of 2 * rows * cols * w; the
     subdomain elimination (nI pivots of [I|B] x [I|B|f]) and, with dual_lu,
-    the 64-panel LU of the embedded dual blocks (nB pivots of nB x nB).
+    the LU of the embedded dual blocks (nB pivots of nB x nB, same panels).
     Returns (flops, launches)."""
     nI, nL, nB = (plan.nI.astype(np.int64), plan.nL.astype(np.int64),
                   plan.nB.astype(np.int64))
     f, n = _panel_flops(nI, nL, nL + 1, panel)
     if dual_lu:
-        f2, n2 = _panel_flops(nB, nB, nB, 64)
+        f2, n2 = _panel_flops(nB, nB, nB, panel)
         f, n = f + f2, n + n2
     return f, n
 
@@ -855,7 +855,9 @@ class DevicePreconditioner:
         nsteps = (nbmax + 63) // 64
         pinv_all = torch.empty(nsteps * p.N * 4096, dtype=F64, device="cuda")
         lib.bddc_schur_eliminate(Z, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax, nbmax,
-                                 64, pinv_all, 4096, p.N * 4096, status, 0, None, 0, st)
+                                 PANEL, pinv_all, 4096, p.N * 4096, status, 0, None, 0, st)
+        if PANEL == 128:  # 128-wide elimination -> the 64-panel form of the local solves
+            lib.bddc_lu128_fixup(Z, d.soff, d.nB, d.nB, p.N, nbmax, st)
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError(f"dual block of subdomain {bad + ls.s0} is singular")
