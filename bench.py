@@ -273,10 +273,10 @@ def run_mine(args):
     g0 = dict(GRAPH_STATS)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    lib.bddc_trailing_log(1)  # CUDA events around the trailing launches (pool created here)
     torch.cuda.synchronize()
     e0.record()
     phases = {}
-    lib.bddc_trailing_log(1)  # CUDA events around the trailing launches, read after the loop
     step_ev = [e0]
     per_step_phases = []
     for _ in range(args.steps):
@@ -289,6 +289,8 @@ def run_mine(args):
         step_ev.append(ev)
     e1.record()
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     launches = (int(lib.bddc_launch_count()) - (GRAPH_STATS["captured"] - g0["captured"])
                 + (GRAPH_STATS["replayed"] - g0["replayed"])) // args.steps
     clk = clocks.stop()

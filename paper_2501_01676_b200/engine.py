@@ -182,7 +182,12 @@ class LocalSystem:
             del work
             if before_check is not None:
                 before_check()
+            # norms for the dual-certificate bound (read at the status synchronisation)
+            f = torch.zeros(2 * p.N, dtype=F64, device="cuda")
+            lib.bddc_frob2(self.S, d.soff, d.nB, p.N, f[:p.N], st)
+            lib.bddc_frob2(Binv, d.soff, d.nB, p.N, f[p.N:], st)
             bad = _first_bad(status)
+            self._frob = f.cpu().numpy()
             if bad is not None:
                 B = self.matrix(self.Bsym, bad)
                 raise NumericalError(f"Bsym of subdomain {bad + self.s0} is not positive definite "
@@ -765,16 +770,11 @@ class DevicePreconditioner:
         # global coarse numbering (all subdomains, every rank computes the same)
         gcnt, np_glob = primal_counts(p.g_sub_globs, p.g_sub_glob_start)
         gpgid0 = _ranges(go[:-1][p.g_sub_globs], gcnt)
-        # coarse dofs in reverse Cuthill-McKee order of the primal coupling graph
-        # (each subdomain's primal set is a clique) -> envelope LU / solves
-        self.corder, new_id, self.lim, self.first = coarse_ordering(gpgid0, np_glob, self.n_primal)
-        self.new_id = new_id
         s0, s1 = p.owned
         cnt, self.np_sub = primal_counts(p.sub_globs, p.sub_glob_start)
         pstart = _excl(self.np_sub)
         ppos = _ranges(p.sub_glob_boff, cnt)
         pgid0 = _ranges(go[:-1][p.sub_globs], cnt)
-        pgid = new_id[pgid0]
         mask = np.zeros(int(p.voff[-1]), dtype=np.uint8)
         psub = np.repeat(np.arange(p.N), self.np_sub)
         mask[p.voff[psub] + ppos] = 1
@@ -782,12 +782,9 @@ class DevicePreconditioner:
         gcoff = _excl(np_glob * np_glob)  # coarse blocks C_i of all subdomains, global layout
         c0, c1 = int(gcoff[s0]), int(gcoff[s1])
         coff = gcoff[s0:s1 + 1] - c0
-        self.d_pstart, self.d_ppos, self.d_pgid = dev_i32(pstart), dev_i32(ppos), dev_i32(pgid)
+        self.d_pstart, self.d_ppos = dev_i32(pstart), dev_i32(ppos)
         self.d_poff, d_coff = dev_i64(poff[:-1]), dev_i64(coff[:-1])
         d_mask = torch.from_numpy(mask).cuda()
-        csrc = np.argsort(pgid, kind="stable")
-        self.d_csrc = dev_i64(csrc)
-        self.d_cstart = dev_i64(np.searchsorted(pgid[csrc], np.arange(self.n_primal + 1)))
         self.sum_np = int(pstart[-1])
 
         # change of basis in Householder form (same primal spans; precond.cu)
@@ -858,6 +855,16 @@ class DevicePreconditioner:
                                  PANEL, pinv_all, 4096, p.N * 4096, status, 0, None, 0, st)
         if PANEL == 128:  # 128-wide elimination -> the 64-panel form of the local solves
             lib.bddc_lu128_fixup(Z, d.soff, d.nB, d.nB, p.N, nbmax, st)
+        # host work overlapping the queued factorisation: coarse dofs in reverse
+        # Cuthill-McKee order of the primal coupling graph (each subdomain's primal
+        # set is a clique) -> envelope LU / block-inverse solves
+        self.corder, new_id, self.lim, self.first = coarse_ordering(gpgid0, np_glob, self.n_primal)
+        self.new_id = new_id
+        pgid = new_id[pgid0]
+        self.d_pgid = dev_i32(pgid)
+        csrc = np.argsort(pgid, kind="stable")
+        self.d_csrc = dev_i64(csrc)
+        self.d_cstart = dev_i64(np.searchsorted(pgid[csrc], np.arange(self.n_primal + 1)))
         bad = _first_bad(status)
         if bad is not None:
             raise NumericalError(f"dual block of subdomain {bad + ls.s0} is singular")
