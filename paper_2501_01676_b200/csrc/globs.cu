@@ -673,16 +673,39 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
     }
     const double* Xi = t.BiC + t.sh_doff[k0];
     const double* Xj = t.BiC + t.sh_doff[k0 + 1];
+    const double* SCi = t.SC + t.sh_doff[k0];
+    const double* SCj = t.SC + t.sh_doff[k0 + 1];
+    // X = sym(Xi + Xj) and the five squared Frobenius norms in one pass, one
+    // block reduction
+    __shared__ double fred[(256 / 32) * 5];
+    double q[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
     for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
       const int r = idx / n, c = idx - r * n;
-      S1[idx] = 0.5 * ((Xi[idx] + Xi[c * n + r]) + (Xj[idx] + Xj[c * n + r]));
+      const double xi = Xi[idx], xj = Xj[idx];
+      const double v = 0.5 * ((xi + Xi[c * n + r]) + (xj + Xj[c * n + r]));
+      S1[idx] = v;
+      const double si = SCi[idx], sj = SCj[idx];
+      q[0] = fma(si, si, q[0]);
+      q[1] = fma(sj, sj, q[1]);
+      q[2] = fma(xi, xi, q[2]);
+      q[3] = fma(xj, xj, q[3]);
+      q[4] = fma(v, v, q[4]);
     }
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o);
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int i = 0; i < 5; ++i) fred[(threadIdx.x >> 5) * 5 + i] = q[i];
     __syncthreads();
-    const double nsi = sqrt(blk::frob2(t.SC + t.sh_doff[k0], n, n, n, red));
-    const double nsj = sqrt(blk::frob2(t.SC + t.sh_doff[k0 + 1], n, n, n, red));
-    const double nxi = sqrt(blk::frob2(Xi, n, n, n, red));
-    const double nxj = sqrt(blk::frob2(Xj, n, n, n, red));
-    const double nx = sqrt(blk::frob2(S1, n, n, n, red));
+    double tq[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int wi = 0; wi < (int)(blockDim.x >> 5); ++wi)
+#pragma unroll
+      for (int i = 0; i < 5; ++i) tq[i] += fred[wi * 5 + i];
+    __syncthreads();
+    const double nsi = sqrt(tq[0]), nsj = sqrt(tq[1]), nxi = sqrt(tq[2]), nxj = sqrt(tq[3]);
+    const double nx = sqrt(tq[4]);
     const double cond_m = (nsi + nsj) / (1.0 / nxi + 1.0 / nxj);
     const double cond_x = nx / (1.0 / nsi + 1.0 / nsj);
     if (!(nsi > 0.0) || !(nsj > 0.0) || !(nxi > 0.0) || !(nxj > 0.0) ||

@@ -133,13 +133,15 @@ class LocalSystem:
     def _factor(self):
         p, d, st = self.plan, self.d, stream()
         K = torch.zeros(p.K_total, dtype=F64, device="cuda")
-        Ke, Fe, ebad = self.inputs.get("Ke"), self.inputs.get("Fe"), None
+        Ke, Fe, ebad = self.inputs.get("Ke"), self.inputs.get("Fe"), self.inputs.get("_ebad")
         if Ke is None:  # element blocks built on the device from mesh + coefficients
             Ke, Fe, ebad = device_element_blocks(self.inputs)
         lib.bddc_local_assemble(K, d.off, d.ld, d.nL, d.elem_start, d.elem_ids, d.loc4,
                                 self.inputs["conn"], Ke, Fe, self.inputs["gdir"], p.N,
                                 p.max_elems, st)
         del Ke, Fe
+        # the element blocks are consumed: keep only the index inputs
+        self.inputs = {k: v for k, v in self.inputs.items() if k not in ("Ke", "Fe", "_ebad")}
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
         args = (K, d.off, d.ld, d.nI, d.nL, d.nL1, p.N, int(p.nI.max()), int(p.nL.max()),

@@ -12,8 +12,7 @@ import torch
 
 from .engine import (DeviceInterfaceOperator, DevicePreconditioner, DevicePrimalSpace,
                      DeviceScaling, LocalSystem, PhaseTimer, gmres_device, gmres_right_device,
-                     recover_device,
-                     upload_inputs)
+                     device_element_blocks, recover_device, upload_inputs)
 from .plan import Plan
 
 
@@ -35,12 +34,17 @@ def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8,
         owned = plan.owned if plan is not None else comm.owned(partition.n_subdomains)
     if inputs is None:
         inputs = upload_inputs(system, partition, owned=owned if plan is None or plan.on_device else None)
+    if "Ke" not in inputs and "_supg" in inputs:
+        # device element blocks first: the kernel runs while the host builds the plan
+        Ke, Fe, ebad = device_element_blocks(inputs)
+        inputs = {**inputs, "Ke": Ke, "Fe": Fe, "_ebad": ebad}
     if plan is None:
         tm.mark("symbolic_plan")
         plan = Plan(system, partition, globs, device_inputs=inputs, owned=owned)
     tm.mark("subdomain_ops")
     ls = LocalSystem(system, partition, globs, plan=plan, inputs=inputs,
                      kernel_timing=kernel_timing, dplan=dplan, comm=comm)
+    inputs = None
     tm.mark("bsym_inverse")
     ls.bsym_inverse()
     tm.mark("scaling")

@@ -5,7 +5,11 @@ roofline.traffic (bytes per launch, averaged over the mode-0 trailing
 updates: the subdomain elimination's K = 128 launches and the dual-block
 LU's K = 64 launches).
 
-    python tools/traffic.py gpurun_out/full_trailing_r01c.ncu-rep r01c
+    python tools/traffic.py gpurun_out/full_trailing_r01d.ncu-rep r01d [nI_max nB_max]
+
+The launch order of one step is rebuilt from the 128-wide panel sequence of the
+two eliminations (strip launch when a panel has a second 64-wide sub-panel,
+then the mode-0 trailing update): cfg5 has nI_max = 343, nB_max = 386.
 """
 import csv
 import io
@@ -14,6 +18,14 @@ import subprocess
 import sys
 
 rep, tag = sys.argv[1], sys.argv[2]
+nI_max = int(sys.argv[3]) if len(sys.argv) > 3 else 343
+nB_max = int(sys.argv[4]) if len(sys.argv) > 4 else 386
+seq = []
+for npiv in (nI_max, nB_max):
+    for k in range(0, npiv, 128):
+        if k + 64 < npiv:
+            seq.append("strip")
+        seq.append("update")
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
                       "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
                       "launch__grid_size"], capture_output=True, text=True).stdout
@@ -21,7 +33,9 @@ rows = list(csv.reader(io.StringIO(out)))
 head, units, data = rows[0], rows[1], rows[2:]
 col = {h: i for i, h in enumerate(head)}
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "": 1}
+         "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+         "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9,
+         "": 1}
 def val(r, name):
     v = r[col[name]].replace(",", "")
     return float(v) * scale.get(units[col[name]], 1)
@@ -30,8 +44,7 @@ for r in data:
     launches.append(dict(grid=int(val(r, "launch__grid_size")),
                          ms=val(r, "gpu__time_duration.sum") * 1e3,
                          dram_bytes=val(r, "dram__bytes_read.sum") + val(r, "dram__bytes_write.sum")))
-# elimination order: [strip, big] x 3 (128-wide panels), then the dual LU's 64-wide panels
-mode0 = [l for i, l in enumerate(launches) if (i >= 6 or i % 2 == 1)]
+mode0 = [l for l, kind in zip(launches, seq) if kind == "update"]
 res = {
     "kernel": "schur_trailing_kernel",
     "capture": rep.split("/")[-1],
