@@ -102,7 +102,8 @@ class Plan:
         self.sh_doff = _excl(self.gsize[slot_glob].astype(np.int64) ** 2)
         self.d_total = int(self.sh_doff[-1])
         self.sh_doff = self.sh_doff[:-1]
-        order = np.lexsort((slot_glob, self.sh_sub.astype(np.int64)))
+        # slots by (sharer, glob): one stable argsort of a combined key (unique pairs)
+        order = np.argsort(self.sh_sub.astype(np.int64) * max(G, 1) + slot_glob, kind="stable")
         self.sub_globs = slot_glob[order].astype(np.int32)
         pair_sub = self.sh_sub[order].astype(np.int64)
         self.sub_glob_sh = order.astype(np.int32)
@@ -122,7 +123,13 @@ class Plan:
         gnodes = f["nodes"]
         self._gnodes = gnodes
         gstart = _excl(self.gsize)
-        self.B_nodes = gnodes[_ranges(gstart[self.sub_globs], sizes_k)]
+        # B nodes (glob-major interface nodes of every subdomain) = concatenated
+        # ranges of gnodes; built on the device for the device plan, on the host
+        # only when a host consumer asks (B_nodes property)
+        self._B_starts = gstart[self.sub_globs].astype(np.int64)
+        self._B_counts = sizes_k
+        self._B_range = (0, int(sizes_k.sum()))
+        self._B_nodes = None
         self.pos2k = np.repeat(np.arange(self.sub_globs.size, dtype=np.int32), sizes_k)
         self._iface_nodes = np.asarray(globs.interface_nodes, dtype=np.int64)
 
@@ -147,8 +154,15 @@ class Plan:
         self.nB = self.g_nB[s0:s1]
         v0, v1 = int(self.voff[s0]), int(self.voff[s1])
         self.voff = self.voff[s0:s1 + 1] - v0
-        self.B_nodes = self.B_nodes[v0:v1]
+        self._B_range = (v0, v1)
         self.pos2k = (self.pos2k[v0:v1] - a).astype(np.int32)
+
+    @property
+    def B_nodes(self):
+        if self._B_nodes is None:
+            v0, v1 = self._B_range
+            self._B_nodes = self._gnodes[_ranges(self._B_starts, self._B_counts)][v0:v1]
+        return self._B_nodes
 
     def _interface_maps_numpy(self):
         self.iface_perm = np.searchsorted(self._iface_nodes, self.B_nodes).astype(np.int32)
@@ -160,7 +174,13 @@ class Plan:
         import torch
 
         self._node_maps_device(dv)
-        Bn = _up(self.B_nodes, dv)
+        total = int(self._B_counts.sum())
+        counts = _up(self._B_counts, dv)
+        base = _up(self._B_starts, dv) - (torch.cumsum(counts, 0) - counts)
+        idx = torch.repeat_interleave(base, counts, output_size=total)
+        idx += torch.arange(total, device=dv)
+        v0, v1 = self._B_range
+        Bn = self._gn_d[idx[v0:v1]]
         ifn = self._iface_nodes_d
         perm = torch.searchsorted(ifn, Bn)
         self.iface_perm_d = perm.to(torch.int32)
@@ -258,6 +278,7 @@ class Plan:
         import torch
 
         gn = _up(self._gnodes.astype(np.int64), dv)
+        self._gn_d = gn
         gsz = _up(self.gsize.astype(np.int64), dv)
         gid = torch.repeat_interleave(torch.arange(self.G, device=dv), gsz,
                                       output_size=int(self._gnodes.size))
