@@ -329,7 +329,9 @@ def _input_arrays(system, partition, owned, device_elements):
         device_elements = system.device_fields is not None
     if device_elements and system.device_fields is None:
         raise ValueError("device element blocks need Coefficients.device_fields")
-    arrays = {"conn": (conn if sel is None else conn[sel], np.int64)}
+    # index arrays travel as int32 (half the bytes) and are widened on the device
+    idx_t = np.int32 if system.mesh.n_nodes < 2 ** 31 else np.int64
+    arrays = {"conn": (conn if sel is None else conn[sel], idx_t)}
     meta = None
     if device_elements:
         table, period = system.device_viscosity
@@ -347,8 +349,16 @@ def _input_arrays(system, partition, owned, device_elements):
     arrays["gdir"] = (system.dirichlet_values, np.float64)
     arrays["free"] = (np.asarray(system.node_to_free) >= 0, np.bool_)
     if sub_of is not None:
-        arrays["sub_of"] = (sub_of if sel is None else sub_of[sel], np.int64)
+        arrays["sub_of"] = (sub_of if sel is None else sub_of[sel], idx_t)
     return arrays, meta
+
+
+def _widen(out):
+    """int32 index inputs -> int64 on the device (the kernels take long long)."""
+    for k in ("conn", "sub_of"):
+        if k in out and out[k].dtype != torch.int64:
+            out[k] = out[k].long()
+    return out
 
 
 def stage_inputs(system, partition=None, owned=None, device_elements=None):
@@ -372,8 +382,8 @@ def stage_inputs(system, partition=None, owned=None, device_elements=None):
 
 def upload_staged(staged):
     """Asynchronous H2D of stage_inputs() buffers on the current stream."""
-    return {k: (v.cuda(non_blocking=True) if isinstance(v, torch.Tensor) else v)
-            for k, v in staged.items()}
+    return _widen({k: (v.cuda(non_blocking=True) if isinstance(v, torch.Tensor) else v)
+                   for k, v in staged.items()})
 
 
 def staged_bytes(staged):
@@ -387,8 +397,8 @@ def upload_inputs(system, partition=None, pinned=False, owned=None, device_eleme
     if pinned:
         return upload_staged(stage_inputs(system, partition, owned, device_elements))
     arrays, meta = _input_arrays(system, partition, owned, device_elements)
-    out = {k: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
-           for k, (a, dt) in arrays.items()}
+    out = _widen({k: torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).cuda()
+                  for k, (a, dt) in arrays.items()})
     if meta is not None:
         out["_supg"] = meta
     return out
