@@ -224,6 +224,7 @@ __global__ void __launch_bounds__(128) glob_reflectors_kernel(
     const int i = idx / rr, j = idx - i * rr;
     Wg[idx] = Qg[j * n + i];
   }
+  __syncthreads();  // every read of Q_g before it is reset
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Qg[idx] = (idx / n == idx % n) ? 1.0 : 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -1095,13 +1095,18 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
 
     Orthogonalisation is classical Gram-Schmidt applied twice (same Krylov
     space as the reference's MGS x 2); the least-squares problem is solved
-    with gelsd on the host exactly as the reference does; the true residual
-    uses stored S_hat V_j columns instead of an extra S_hat application."""
+    with gelsd on the host exactly as the reference does (one device->host
+    read of the new Hessenberg column per step); the true residual uses stored
+    S_hat V_j columns instead of an extra S_hat application and its norms are
+    kept on the device and read once at the end."""
     st = stream()
     n = rhs.shape[0]
     nblk = 296
     partial = torch.empty(nblk * (max_iter + 2), dtype=F64, device="cuda")
-    scal = torch.empty(max_iter + 2, dtype=F64, device="cuda")
+    # one buffer for both Gram-Schmidt passes and the norm: [h1 (max_iter+1) | h2 .. hn]
+    hb = torch.empty(2 * (max_iter + 2), dtype=F64, device="cuda")
+    h1, scal = hb[:max_iter + 1], hb[max_iter + 1:]
+    tres = torch.empty(max_iter + 1, dtype=F64, device="cuda")
     z0 = pc.apply_device(rhs)
     lib.bddc_norm2(z0, n, scal, partial, nblk, st)
     ref = float(scal[0].item())
@@ -1113,10 +1118,9 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     H = np.zeros((max_iter + 1, max_iter))
     e1 = np.zeros(max_iter + 1)
     e1[0] = ref
-    h1 = torch.empty(max_iter + 1, dtype=F64, device="cuda")
     w = torch.empty(n, dtype=F64, device="cuda")
     r = torch.empty(n, dtype=F64, device="cuda")
-    true_hist, pre_hist = [], []
+    pre_hist = []
     conv = False
     it = 0
     y = np.zeros(0)
@@ -1130,8 +1134,9 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
         lib.bddc_multi_dot(V.buf, n, m, w, scal, partial, nblk, 0, st)
         lib.bddc_multi_axpy(V.buf, n, m, scal, -1.0, w, st)
         lib.bddc_norm2(w, n, scal[m:], partial, nblk, st)
-        hs = scal[:m + 1].cpu().numpy()
-        hh = h1[:m].cpu().numpy() + hs[:m]
+        hc = hb[:max_iter + 2 + m].cpu().numpy()  # h1[:m] and scal[:m+1] in one read
+        hs = hc[max_iter + 1:max_iter + 2 + m]
+        hh = hc[:m] + hs[:m]
         hn = float(hs[m])
         H[:m, j] = hh
         H[m, j] = hn
@@ -1142,8 +1147,7 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
         yd = dev_f64(y)
         r.copy_(rhs)
         lib.bddc_multi_axpy(U.buf, n, m, yd, -1.0, r, st)
-        lib.bddc_norm2(r, n, scal, partial, nblk, st)
-        true_hist.append(float(scal[0].item()))
+        lib.bddc_norm2(r, n, tres[j:], partial, nblk, st)
         if pre_hist[-1] <= rel_tol:
             conv = True
             break
@@ -1155,6 +1159,7 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     x = torch.zeros(n, dtype=F64, device="cuda")
     if it:
         lib.bddc_multi_axpy(V.buf, n, it, dev_f64(y), 1.0, x, st)
+    true_hist = tres[:it].cpu().numpy().tolist()
     return it, conv, x, true_hist, pre_hist
 
 
