@@ -294,25 +294,8 @@ int bddc_pc_dual_embed(const int* nB, const long long* soff, const long long* vo
                        const unsigned char* primal_mask, const double* Sbar, double* Zin,
                        double* Csym, int nbatch, cudaStream_t stream);
 
-int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* voff,
-                        const unsigned char* primal_mask, double* Z, int nbatch,
-                        cudaStream_t stream);
 
-/* A_i = T_i^T Z T_i (local part of M^-1; DMMA block products).  TTT: caller
- * scratch the size of the TT buffer.  replaces scale/tilde_solve solver.py:163-199. */
-int bddc_pc_local_operator(const int* nB, const long long* soff, const int* sub_glob_start,
-                           int nbatch, const int* sub_globs, const int* sub_glob_boff,
-                           const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
-                           const int* slot_glob, int n_slots, int n_items, int max_nB,
-                           int max_ng, int max_globs, const double* TT, double* TTT,
-                           const double* Z, double* tmp, double* A, cudaStream_t stream);
 
-/* MP = E_P - (Z Sbar)_{:,P}^T rows, RP = E_P - (Sbar Z)_{P,:}, C_i = Sbar_PP - Sbar_P: Z Sbar_:P.
- * replaces solver.py:102-106. */
-int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstart,
-                          const int* ppos, const long long* poff, const double* Sbar,
-                          const double* Z, double* MP, double* RP, double* Cl,
-                          const long long* coff, int nbatch, int max_nB, cudaStream_t stream);
 
 int bddc_pc_primal_rows_T(const int* nB, const long long* voff, const int* pos2k,
                           const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,

@@ -592,59 +592,7 @@ __global__ void dual_embed_kernel(const int* __restrict__ nB, const long long* _
   }
 }
 
-__global__ void zero_primal_kernel(const int* __restrict__ nB, const long long* __restrict__ soff,
-                                   const long long* __restrict__ voff,
-                                   const unsigned char* __restrict__ primal_mask,
-                                   double* __restrict__ Z) {
-  const int b = blockIdx.y;
-  const int n = nB[b];
-  const unsigned char* pm = primal_mask + voff[b];
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
-    if (pm[r] || pm[c]) Z[soff[b] + idx] = 0.0;
-  }
-}
 
-// Per subdomain primal pieces (one CTA per subdomain):
-//   ZS[:, p]  = Z Sbar[:, p]             -> MP[p][:] = e_p - ZS[:, p]   (n_p x nB, "column" form)
-//   SZ[p, :]  = Sbar[p, :] Z             -> RP[p][:] = e_p - SZ[p, :]
-//   C_i[p][q] = Sbar[p][q] - Sbar[p, :] ZS[:, q]
-__global__ void primal_pieces_kernel(const int* __restrict__ nB, const long long* __restrict__ soff,
-                                     const int* __restrict__ pstart, const int* __restrict__ ppos,
-                                     const long long* __restrict__ poff,
-                                     const double* __restrict__ Sbar, const double* __restrict__ Z,
-                                     double* __restrict__ MP, double* __restrict__ RP,
-                                     double* __restrict__ Cl, const long long* __restrict__ coff) {
-  const int b = blockIdx.x;
-  const int n = nB[b];
-  const int p0 = pstart[b], np = pstart[b + 1] - p0;
-  const double* S = Sbar + soff[b];
-  const double* Zb = Z + soff[b];
-  double* M = MP + poff[b];
-  double* R = RP + poff[b];
-  for (int idx = threadIdx.x; idx < np * n; idx += blockDim.x) {
-    const int p = idx / n, r = idx - p * n;
-    const int pc = ppos[p0 + p];
-    double s1 = 0.0, s2 = 0.0;
-    for (int k = 0; k < n; ++k) {
-      s1 += Zb[(long long)r * n + k] * S[(long long)k * n + pc];   // (Z Sbar)[r, pc]
-      s2 += S[(long long)pc * n + k] * Zb[(long long)k * n + r];   // (Sbar Z)[pc, r]
-    }
-    M[(long long)p * n + r] = (r == pc ? 1.0 : 0.0) - s1;
-    R[(long long)p * n + r] = (r == pc ? 1.0 : 0.0) - s2;
-  }
-  __syncthreads();
-  double* C = Cl + coff[b];
-  for (int idx = threadIdx.x; idx < np * np; idx += blockDim.x) {
-    const int p = idx / np, q = idx - p * np;
-    const int pr = ppos[p0 + p], qc = ppos[p0 + q];
-    // Sbar[pr, qc] - Sbar[pr, :] (Z Sbar)[:, qc] = Sbar[pr,:] (e_qc - ZS[:,qc]) = Sbar[pr,:] M[q,:]
-    double s = 0.0;
-    for (int k = 0; k < n; ++k) s += S[(long long)pr * n + k] * M[(long long)q * n + k];
-    C[idx] = s;
-  }
-}
 
 // ---------------------------------------------------------------------------
 // dual solves with the blocked LU of the embedded dual block (lu_solve.cuh)
@@ -1270,44 +1218,8 @@ int bddc_pc_dual_embed(const int* nB, const long long* soff, const long long* vo
   return pc_status();
 }
 
-int bddc_pc_zero_primal(const int* nB, const long long* soff, const long long* voff,
-                        const unsigned char* primal_mask, double* Z, int nbatch,
-                        cudaStream_t stream) {
-  if (nbatch <= 0) return 0;
-  zero_primal_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(nB, soff, voff, primal_mask, Z); bddc_note_launches(1);
-  return pc_status();
-}
 
-// A = TT_blockdiag Z TT_blockdiag^T  (= T^T Z T with T = blockdiag(Q_g D_g^T));
-// TTT: caller scratch of the TT buffer's size
-int bddc_pc_local_operator(const int* nB, const long long* soff, const int* sub_glob_start,
-                           int nbatch, const int* sub_globs, const int* sub_glob_boff,
-                           const int* sub_glob_sh, const int* gsize, const long long* sh_doff,
-                           const int* slot_glob, int n_slots, int n_items, int max_nB,
-                           int max_ng, int max_globs, const double* TT, double* TTT,
-                           const double* Z, double* tmp, double* A, cudaStream_t stream) {
-  if (nbatch <= 0) return 0;
-  transpose_blocks_kernel<<<n_slots, 128, 0, stream>>>(TT, TTT, sh_doff, slot_glob, gsize, n_slots);
-  bddc_note_launches(1);
-  int st = glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
-                    TT, TTT, sh_doff, 1, 1, Z, tmp, n_items, max_nB, max_ng, max_globs, stream);
-  if (st) return st;
-  return glob_mma(nB, soff, sub_glob_start, nbatch, sub_globs, sub_glob_boff, sub_glob_sh, gsize,
-                  TT, TTT, sh_doff, 1, 0, tmp, A, n_items, max_nB, max_ng, max_globs, stream);
-}
 
-int bddc_pc_primal_pieces(const int* nB, const long long* soff, const int* pstart,
-                          const int* ppos, const long long* poff, const double* Sbar,
-                          const double* Z, double* MP, double* RP, double* Cl,
-                          const long long* coff, int nbatch, int max_nB, cudaStream_t stream) {
-  if (nbatch <= 0) return 0;
-  const int smem = 2 * kPC * max_nB * (int)sizeof(double);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(primal_pieces2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  primal_pieces2_kernel<<<nbatch, 256, smem, stream>>>(nB, soff, pstart, ppos, poff, Sbar, Z, MP, RP,
-                                                       Cl, coff, max_nB);
-  bddc_note_launches(1);
-  return pc_status();
-}
 
 int bddc_pc_primal_rows_T(const int* nB, const long long* voff, const int* pos2k,
                           const int* sub_globs, const int* sub_glob_boff, const int* sub_glob_sh,

@@ -164,11 +164,8 @@ class LocalSystem:
         if bad is not None:
             raise NumericalError(f"interior block of subdomain {bad + self.s0} is singular")
 
-    def bsym_inverse(self, before_check=None):
-        """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check.
-        before_check: called after the launches, before the status check (the
-        reference builds the deluxe scaling before it inverts Bsym, so that
-        error is reported first when both fail)."""
+    def bsym_inverse(self):
+        """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check."""
         if self._Binv is None:
             p, d, st = self.plan, self.d, stream()
             Binv = self.Bsym.clone()
@@ -182,8 +179,6 @@ class LocalSystem:
             lib.bddc_gj_inverse128(Binv, d.soff, d.nB, d.nB, p.N, int(p.nB.max()), work, w_off,
                                    w128, w128, pinv, status, 1, st)
             del work
-            if before_check is not None:
-                before_check()
             # norms for the dual-certificate bound (read at the status synchronisation)
             f = torch.zeros(2 * p.N, dtype=F64, device="cuda")
             lib.bddc_frob2(self.S, d.soff, d.nB, p.N, f[:p.N], st)
