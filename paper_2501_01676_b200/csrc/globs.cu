@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(256) deluxe_kernel(GlobTables t, double* __res
                                                      int* __restrict__ status,
                                                      const int* __restrict__ glob_ids) {
   __shared__ double rowbuf[2048];
+  __shared__ MmaGjSmem gsm;
   const int g = glob_ids ? glob_ids[blockIdx.x] : blockIdx.x;
   const int n = t.size[g];
   const int s0 = t.sh_start[g], s1 = t.sh_start[g + 1];
@@ -468,7 +469,10 @@ __global__ void __launch_bounds__(256) deluxe_kernel(GlobTables t, double* __res
     T[idx] = s;
   }
   __syncthreads();
-  const int st = blk::gj_inverse(T, n, n, true, rowbuf);
+  // (sum_k B_k)^-1: register Gauss-Jordan on the DMMA pipe for n <= 64 (same
+  // positive-pivot criterion as the scalar one)
+  const int st = n <= kTile ? (reg_gj64(T, n, n, T, n, 1, nullptr, gsm) ? (int)kNotPositiveDefinite : 0)
+                            : blk::gj_inverse(T, n, n, true, rowbuf);
   if (st) {
     if (threadIdx.x == 0) status[g] = st;
     return;
