@@ -393,10 +393,10 @@ int bddc_coarse_solve_flow(const double* A, long long ld, int n, const double* p
 
 /* Build the block-inverse solve operators from the factors of
  * bddc_coarse_factor (A, ld, pinv as left by it).  Rows are grouped in blocks
- * of 512; for block D (rows [512 D, 512 D + h)):
- *   F_D = Linv_DD [L_(D, cl[D]:512 D) | I_h]       h x ldF, at foff[D]
- *   G_D = Uinv_DD [P_D | W_(D, 512 D + h:cu[D])]    h x ldG, at goff[D]
- * ldF = (512 D - cl[D]) + roundup2(h), ldG = roundup2(cu[D] - 512 D); cl[D]
+ * of B = bddc_coarse_block_rows() (1024); for block D (rows [B D, B D + h)):
+ *   F_D = Linv_DD [L_(D, cl[D]:B D) | I_h]       h x ldF, at foff[D]
+ *   G_D = Uinv_DD [P_D | W_(D, B D + h:cu[D])]    h x ldG, at goff[D]
+ * ldF = (B D - cl[D]) + roundup2(h), ldG = roundup2(cu[D] - B D); cl[D]
  * (64-aligned) is the first column of L coupled to the block, cu[D] the end
  * of its U coupling (device arrays; engine.coarse_blockinv_layout).  max_ldf /
  * max_ldg: largest ldF / ldG.  Part of replacing lu_factor(coarse) solver.py:123. */
@@ -404,6 +404,9 @@ int bddc_coarse_blockinv(const double* A, long long ld, int n, const double* pin
                          long long pinv_step_stride, int nD, const int* cl, const int* cu,
                          const long long* foff, const long long* goff, int max_ldf, int max_ldg,
                          double* F, double* G, cudaStream_t stream);
+
+/* Rows per block of the block-inverse coarse solve (the layout's block size). */
+int bddc_coarse_block_rows(void);
 
 /* x = C^-1 b with the operators of bddc_coarse_blockinv: 2 nD dependent
  * row-parallel GEMV steps in one cooperative launch (128 CTAs).  z: n doubles

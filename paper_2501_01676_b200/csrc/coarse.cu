@@ -4,7 +4,7 @@
 // bddc_coarse_factor leaves C = L diag(P^-1) U in 64-wide panels: L block unit
 // lower (panel columns L' = A21 P_k), U block unit upper (pivot rows
 // W = P_k A12), P_k the inverse pivot blocks.  Rows are grouped into blocks of
-// kCB = 512 rows (8 panels).  For block D (rows [D*kCB, D*kCB + h)):
+// kCB = 1024 rows (16 panels).  For block D (rows [D*kCB, D*kCB + h)):
 //
 //   F_D = Linv_DD [ L_(D, cl_D : D*kCB) | I_h ]        h x (wF + h)
 //   G_D = Uinv_DD [ P_D | W_(D, D*kCB + h : cu_D) ]    h x (cu_D - D*kCB)
@@ -14,7 +14,7 @@
 //   forward   z_D = F_D[:, wF:] b_D - F_D[:, :wF] z[cl_D : D*kCB]
 //   backward  x_D = G_D[:, :h] z_D - G_D[:, h:]  x[D*kCB + h : cu_D]
 // so each block of 512 unknowns is ONE row-parallel GEMV that depends on the
-// previous block only through its 512 newest values: 2 * ceil(n / 512)
+// previous block only through its kCB newest values: 2 * ceil(n / kCB)
 // dependent steps instead of 2 * ceil(n / 64) dependent triangular panels.
 // F and G are built once per preconditioner with the DMMA tile GEMM (the
 // diagonal blocks have identity 64 x 64 diagonal blocks, so the block
@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) coarse_trail_piv
   }
 }
 
-constexpr int kCB = 512;            // rows per block (multiple of 64)
-constexpr int kCRC = 4;             // rows per CTA per block
+constexpr int kCB = 1024;           // rows per block (multiple of 64)
+constexpr int kCRC = 8;             // rows per CTA per block
 constexpr int kCCta = kCB / kCRC;   // CTAs of the solve (128 <= 148 SMs, co-resident)
 constexpr int kCThreads = 256;
 constexpr int kCPer = kCB / kCThreads;  // critical-block columns per thread
@@ -434,6 +434,8 @@ int bddc_coarse_blockinv(const double* A, long long ld, int n, const double* pin
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? 0 : -(int)e;
 }
+
+int bddc_coarse_block_rows(void) { return kCB; }
 
 int bddc_coarse_solve_blockinv(const double* F, const double* G, int n, int nD, const int* cl,
                                const int* cu, const long long* foff, const long long* goff,

@@ -733,11 +733,13 @@ def coarse_ordering(pgid, np_sub, n_c):
     return order, new_id, lim.astype(np.int32), first.astype(np.int32)
 
 
-def coarse_blockinv_layout(lim, n_c, block=512):
+def coarse_blockinv_layout(lim, n_c, block=None):
     """Row blocks of the block-inverse coarse solve (coarse.cu): per block D
     (rows [D*block, D*block + h)) the first coupled column cl (first 64-panel
     whose L' reaches the block), the end of its U coupling cu, and the offsets
     of F_D (h x ldF) and G_D (h x ldG)."""
+    if block is None:
+        block = int(lib.bddc_coarse_block_rows())
     lim = np.asarray(lim, dtype=np.int64)
     nD = (n_c + block - 1) // block
     DB = np.arange(nD, dtype=np.int64) * block
