@@ -371,9 +371,14 @@ __global__ void __launch_bounds__(256) transform_embed_kernel(
     }
   }
   __syncthreads();
-  // right: X <- X Q^T on every glob column block (warp per row)
+  // right: X <- X Q^T on every glob column block (warp per row), then the
+  // finished row goes out: compact primal row / column entries and the
+  // embedded dual block (identity on primal rows / columns)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int k0 = sub_glob_start[b], k1 = sub_glob_start[b + 1];
+  const int* pi = pidx + voff[b];
+  double* Sr = Srows + poff[b];
+  double* Sc = Scols + poff[b];
   for (int row = warp; row < ng; row += nw) {
     double* xr = X + (long long)row * n;
     for (int k = k0; k < k1; ++k) {
@@ -389,20 +394,16 @@ __global__ void __launch_bounds__(256) transform_embed_kernel(
         __syncwarp();
       }
     }
-  }
-  __syncthreads();
-  // compact primal rows / columns and the embedded dual block
-  const int* pi = pidx + voff[b];
-  double* Sr = Srows + poff[b];
-  double* Sc = Scols + poff[b];
-  for (long long idx = threadIdx.x; idx < (long long)ng * n; idx += blockDim.x) {
-    const int i = (int)(idx / n), c = (int)(idx - (long long)i * n);
-    const int rho = bo + i;
-    const double v = X[idx];
-    const int qr = pi[rho], qc = pi[c];
-    if (qr >= 0) Sr[(long long)qr * n + c] = v;
-    if (qc >= 0) Sc[(long long)qc * n + rho] = v;
-    Zb[idx] = (qr >= 0 || qc >= 0) ? (rho == c ? 1.0 : 0.0) : v;
+    const int rho = bo + row;
+    const int qr = pi[rho];
+    double* zr = Zb + (long long)row * n;
+    for (int c = lane; c < n; c += 32) {
+      const double v = xr[c];
+      const int qc = pi[c];
+      if (qr >= 0) Sr[(long long)qr * n + c] = v;
+      if (qc >= 0) Sc[(long long)qc * n + rho] = v;
+      zr[c] = (qr >= 0 || qc >= 0) ? (rho == c ? 1.0 : 0.0) : v;
+    }
   }
 }
 
