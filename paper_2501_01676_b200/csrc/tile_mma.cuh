@@ -6,7 +6,9 @@
 // m <= BM, n <= 64 and K <= 64.  A and B stream through shared memory in
 // K-chunks of 16 with a 3-stage cp.async pipeline (16-byte copies when the
 // source is 16-byte aligned, 8-byte otherwise; out-of-range elements
-// zero-filled); C is read once, at the start (accumulators = (beta/alpha) C).  B may alias C when one CTA
+// zero-filled); C is prefetched into L2 at the start and read once, in the
+// epilogue (out = alpha * acc + beta * C), so the first DMMAs wait only on the
+// first K-chunk.  B may alias C when one CTA
 // owns every row of that C tile and beta == 0 (in-place W = P*W updates):
 // all of B is read before the epilogue writes.
 #pragma once
@@ -22,6 +24,11 @@ namespace bddc {
 #endif
 #ifndef BDDC_TILE_MINB
 #define BDDC_TILE_MINB 4   // <= 64 registers: 4 CTAs x 8 warps per SM (tools/bench_tile.py)
+#endif
+
+#ifndef BDDC_C_LATE
+#define BDDC_C_LATE 1      // zero-start accumulators, C prefetched to L2 and added in the epilogue
+                           // (0: accumulators start from (beta/alpha) C; measured ~2 % slower)
 #endif
 
 #ifndef BDDC_WN
@@ -121,11 +128,27 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
     if (s < nchunks) tile_issue_chunk(sm, s, s, A, lda, B, ldb, m, n, K, a16, b16);
     cp_async_commit();
   }
+  double acc[4][kNJ][2];
+  const bool c16 = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t)(ldc * 8)) & 15) == 0;
+#if BDDC_C_LATE
+  // accumulators start at zero so the first DMMAs wait only on the first
+  // chunk; C is prefetched into L2 now and read in the epilogue
+  if (beta != 0.0) {
+    constexpr int NT = (BM / 32) * (64 / kWN) * 32;
+    for (int idx = threadIdx.x; idx < BM * 4; idx += NT) {
+      const int r = idx >> 2, c = (idx & 3) * 16;
+      if (r < m && c < n)
+        asm volatile("prefetch.global.L2 [%0];\n" ::"l"(C + (long long)r * ldc + c));
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#else
   // accumulators start from (beta/alpha) C: C is read once, early, while the
   // first chunks are in flight
-  double acc[4][kNJ][2];
   const double cscale = (beta != 0.0) ? beta / alpha : 0.0;
-  const bool c16 = ((reinterpret_cast<uintptr_t>(C) | (uintptr_t)(ldc * 8)) & 15) == 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = wm + i * 8 + g;
@@ -143,6 +166,7 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
       }
     }
   }
+#endif
   for (int kc = 0; kc < nchunks; ++kc) {
     cp_async_wait<kStages - 2>();
     __syncthreads();
@@ -165,6 +189,32 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
   }
   cp_async_wait<0>();
   __syncthreads();  // every read of B (which may alias C) is done
+  // final values alpha * acc (+ beta * C when C is read late)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = wm + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < kNJ; ++j) {
+      const int c = wn + j * 8 + 2 * t;
+#if BDDC_C_LATE
+      if (beta != 0.0 && r < m) {
+        if (c + 1 < n && c16) {
+          const double2 v = *reinterpret_cast<const double2*>(C + (long long)r * ldc + c);
+          acc[i][j][0] = fma(alpha, acc[i][j][0], beta * v.x);
+          acc[i][j][1] = fma(alpha, acc[i][j][1], beta * v.y);
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            acc[i][j][h] = (c + h < n) ? fma(alpha, acc[i][j][h], beta * C[(long long)r * ldc + c + h])
+                                       : alpha * acc[i][j][h];
+        }
+        continue;
+      }
+#endif
+      acc[i][j][0] *= alpha;
+      acc[i][j][1] *= alpha;
+    }
+  }
   if (Ct != nullptr) {
     // mirrored copy: Ct[c][r] = tsign * C[r][c], staged through shared memory
     // (the pipeline buffers are free now) so both stores are coalesced
@@ -177,7 +227,7 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t + h;
-          st[c * 65 + r] = tsign * alpha * acc[i][j][h];
+          st[c * 65 + r] = tsign * acc[i][j][h];
         }
     __syncthreads();
     constexpr int NT = (BM / 32) * (64 / kWN) * 32;
@@ -195,11 +245,11 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
     for (int j = 0; j < kNJ; ++j) {
       const int c = wn + j * 8 + 2 * t;
       if (c + 1 < n && c16) {
-        *reinterpret_cast<double2*>(crow + c) = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        *reinterpret_cast<double2*>(crow + c) = make_double2(acc[i][j][0], acc[i][j][1]);
       } else {
 #pragma unroll
         for (int h = 0; h < 2; ++h)
-          if (c + h < n) crow[c + h] = alpha * acc[i][j][h];
+          if (c + h < n) crow[c + h] = acc[i][j][h];
       }
     }
   }
