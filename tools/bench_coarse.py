@@ -2,7 +2,7 @@
 synthetic matrix: n = 12195, envelope half-width BW (default 1500), diagonally
 dominant.  Prints the factor time and the time per 64-wide panel, to separate
 the per-panel latency floor from the trailing-update work.
-Usage: python tools/bench_coarse.py [BW ...]"""
+Usage: [BDDC_LIB=variant.so] python tools/bench_coarse.py [BW ...]"""
 import ctypes
 import sys
 
@@ -10,7 +10,13 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-from paper_2501_01676_b200._lib import lib  # noqa: E402
+import os  # noqa: E402
+
+from paper_2501_01676_b200 import _lib  # noqa: E402
+
+if os.environ.get("BDDC_LIB"):  # a tuning / experiment variant of the library
+    _lib.LIB_PATH = os.environ["BDDC_LIB"]
+lib = _lib.lib
 
 
 def run(bw, n=12195, reps=3):
