@@ -35,6 +35,18 @@ namespace bddc {
 // diagonal block first and inverting it: P_(k+1)] in a second launch, so the
 // pivot inverse and the column scaling leave the critical path.
 // ---------------------------------------------------------------------------
+#ifndef BDDC_COARSE_PDL
+#define BDDC_COARSE_PDL 1  // programmatic dependent launch of the panel kernels
+#endif
+
+// Panel kernels may be launched before their predecessor finishes
+// (programmatic stream serialisation): wait for it before touching memory.
+BDDC_DEV void wait_prev_grid() {
+#if BDDC_COARSE_PDL
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+#endif
+}
+
 union CoarseFactorSmem {
   TileSmem tile;
   MmaGjSmem gj;
@@ -52,6 +64,7 @@ __global__ void __launch_bounds__(kTileThreads) coarse_pivot_kernel(double* M, i
                                                                     double* pinv, double* piv_out,
                                                                     int* status) {
   extern __shared__ __align__(16) unsigned char cf_raw[];
+  wait_prev_grid();
   coarse_pivot(M, n, k, pinv, piv_out, status, *reinterpret_cast<CoarseFactorSmem*>(cf_raw));
 }
 
@@ -61,6 +74,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) coarse_row_scale
     double* M, int n, int k, int lim, int trow, int limp, const double* pinv) {
   extern __shared__ __align__(16) unsigned char cf_raw[];
   TileSmem& sm = reinterpret_cast<CoarseFactorSmem*>(cf_raw)->tile;
+  wait_prev_grid();
   const int w = min(kTile, n - k);
   if ((int)blockIdx.x < trow) {
     const int c0 = k + w + blockIdx.x * kTile;
@@ -84,6 +98,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) coarse_trail_piv
     double* M, int n, int k, int lim, int next, double* pinv, double* piv_out, int* status) {
   extern __shared__ __align__(16) unsigned char cf_raw[];
   CoarseFactorSmem& sm = *reinterpret_cast<CoarseFactorSmem*>(cf_raw);
+  wait_prev_grid();
   const int w = min(kTile, n - k);
   const int s = k + w;
   const int tn_count = (lim - s + kTile - 1) / kTile;
@@ -351,6 +366,28 @@ __global__ void __launch_bounds__(kCThreads, 1) coarse_blk_solve_kernel(
 
 using namespace bddc;
 
+// launch with programmatic stream serialisation (the kernel waits on its
+// predecessor with griddepcontrol.wait), so its launch overlaps the previous
+// panel kernel's tail
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), int grid, int smem, cudaStream_t stream, Args... args) {
+#if BDDC_COARSE_PDL
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTileThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+#else
+  kern<<<grid, kTileThreads, smem, stream>>>(static_cast<KArgs>(args)...);
+#endif
+}
+
 extern "C" {
 
 int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const int* nv, int n,
@@ -382,18 +419,18 @@ int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const in
     const int trow = span > 0 ? ceil_div(span, kTile) : 0;
     const int tsc = (k > 0 && limp > k) ? ceil_div(limp - k, kTile) : 0;
     if (trow + tsc > 0) {
-      coarse_row_scale_kernel<<<trow + tsc, kTileThreads, smem, stream>>>(M, n, k, lim, trow, limp,
-                                                                          pinv);
+      launch_pdl(coarse_row_scale_kernel, trow + tsc, smem, stream, M, n, k, lim, trow, limp,
+                 (const double*)pinv);
       ++launches;
     }
     const int next = k + w < n;
     if (span > 0) {
       const int t = ceil_div(span, kTile);
-      coarse_trail_pivot_kernel<<<t * t, kTileThreads, smem, stream>>>(M, n, k, lim, next, pinv,
-                                                                       piv_out, status);
+      launch_pdl(coarse_trail_pivot_kernel, t * t, smem, stream, M, n, k, lim, next, pinv, piv_out,
+                 status);
       ++launches;
     } else if (next) {
-      coarse_pivot_kernel<<<1, kTileThreads, smem, stream>>>(M, n, k + w, pinv, piv_out, status);
+      launch_pdl(coarse_pivot_kernel, 1, smem, stream, M, n, k + w, pinv, piv_out, status);
       ++launches;
     }
     limp = span > 0 ? lim : 0;
