@@ -52,12 +52,16 @@ int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_e
                    const int* sh_start, const int* sh_sub, const int* sh_boff,
                    const long long* nI, int* loc4, cudaStream_t stream);
 
-/* Dense local matrix [I|B] x [I|B|f] from element blocks with Dirichlet lifting.
+/* Dense local matrix [I|B] x [I|B|f] from element blocks with Dirichlet lifting;
+ * writes every entry of each nloc[b] x ld[b] matrix (no memset needed) in a fixed
+ * summation order (no atomics: bitwise reproducible).  lists: workspace of
+ * 4 * elem_start[nbatch] ints (per-row corner lists); max_nl = max nloc.
  * replaces substructuring.py:98-114 (COO->CSR assembly, load, lifting). */
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
                         const long long* elem_start, const long long* elem_ids, const int* loc4,
                         const long long* conn, const double* Ke, const double* Fe,
-                        const double* gdir, int nbatch, long long max_elems, cudaStream_t stream);
+                        const double* gdir, int nbatch, int max_nl, int* lists,
+                        cudaStream_t stream);
 
 /* Blocked Schur elimination without pivoting (panel 64 or 128 = two 64-wide
  * sub-panels combined so the DMMA trailing update runs with K = 128):
@@ -95,7 +99,8 @@ int bddc_lu128_fixup(double* M, const long long* off, const int* ld, const int* 
  * roofline measured over the timed region without synchronising inside it):
  * bddc_trailing_log(1) starts logging, bddc_trailing_collect() synchronises on
  * the logged events, writes the summed duration (ms, HOST pointer) and the
- * number of logged launches, and clears the log.  Not thread-safe. */
+ * number of logged launches, and clears the log.  The log is per calling host
+ * thread (thread_local), so concurrent threads do not interfere. */
 int bddc_trailing_log(int enable);
 int bddc_trailing_collect(double* total_ms, long long* launches);
 
@@ -138,7 +143,7 @@ int bddc_extract_schur(const double* M, const long long* off, const int* ld, con
 int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
                     cudaStream_t stream);
 
-/* out[b] += ||X_b||_F^2 (square n[b] x n[b] at soff[b]; out zeroed by the caller).
+/* out[b] = ||X_b||_F^2 (square n[b] x n[b] at soff[b]; deterministic reduction).
  * Feeds the certified shortcut of the dual-block Cholesky certificate
  * (engine.DevicePreconditioner, reference solver.py:91-98). */
 int bddc_frob2(const double* X, const long long* soff, const int* n, int nbatch, double* out,
@@ -176,9 +181,14 @@ int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int
                 double* ws, const long long* ws_off, int* status, const int* glob_ids, int n_globs,
                 cudaStream_t stream);
 
-/* Face GEP + selection + change of basis.  fast = 1: certified fast path in a
+/* Face GEP + selection + change of basis.  mode = 1: certified fast path in a
  * compact arena (faces whose certificate fails get status 900 and must be
- * re-run with fast = 0, the general algorithm).
+ * re-run with mode 0); mode = 0: general kernel, certified shortcuts allowed;
+ * mode = -1: the reference algorithm verbatim (eigen-based pseudo-inverse,
+ * general pencil solver).  detail (NULL or per glob at detail_off[g], n = n_g):
+ * [pencil_left n^2 | pencil_right n^2 | eigenvectors n^2 | constraint rows
+ * n_sel x n (n^2 slot) | degenerate flags n], the reference GevpReport fields
+ * (adaptive.py:36-47); implies mode -1.
  * replaces face_gevp adaptive.py:57-72, glob_schur_block substructuring.py:152-171,
  *          parallel_sum / pseudo_inverse / sym_pencil_gevp linalg.py:23-214,
  *          build_change_of_basis adaptive.py:190-206. */
@@ -187,7 +197,8 @@ int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const 
                    const double* BiC, const double* SC, const int* sc_status, const double* D, double theta, double* eig,
                    const long long* eig_off, int* n_sel, int* r, double* Q, const long long* q_off,
                    int* status, double* ws, const long long* ws_off, const int* face_ids,
-                   int n_faces, int max_n, int fast, cudaStream_t stream);
+                   int n_faces, int max_n, int mode, double* detail, const long long* detail_off,
+                   cudaStream_t stream);
 
 /* Prior blocks of the face-transformed Bsym^-1 per subdomain.
  * replaces adaptive.py:310-329 (Minv = Q Bsym^-1 Q^T on face rows/cols, prior_idx). */
@@ -198,6 +209,8 @@ int bddc_priors(const int* kind, const int* size, const int* nB, const long long
                 const long long* xhh_off, int n_sub, cudaStream_t stream);
 
 /* Prior-aware ("new") edge GEP + SVD reduction + change of basis.
+ * general = 1: reference algorithm verbatim (no certified pencil shortcut);
+ * detail as bddc_face_gevp with n = nC = (|n(E)| - 1) n_E (implies general).
  * replaces edge_block_with_priors substructuring.py:174-190, edge_gevp_new
  *          adaptive.py:94-156, reduce_edge_constraints adaptive.py:172-187. */
 int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
@@ -207,9 +220,11 @@ int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, co
                        const long long* ex_off, const int* ex_h, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
-                       const int* edge_ids, int n_edges, int max_dim, cudaStream_t stream);
+                       const int* edge_ids, int n_edges, int max_dim, int general,
+                       double* detail, const long long* detail_off, cudaStream_t stream);
 
-/* Coupled ("old") edge GEP. replaces edge_gevp_old adaptive.py:75-91,
+/* Coupled ("old") edge GEP; general / detail as bddc_edge_gevp_new (n = n_E).
+ * replaces edge_gevp_old adaptive.py:75-91,
  *          parallel_sum_chain linalg.py:70-78. */
 int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                        const int* sh_boff, const long long* sh_doff, const double* BsC,
@@ -217,7 +232,8 @@ int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, co
                        const double* D, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
-                       const int* edge_ids, int n_edges, int max_n, cudaStream_t stream);
+                       const int* edge_ids, int n_edges, int max_n, int general, double* detail,
+                       const long long* detail_off, cudaStream_t stream);
 
 /* Slot-compact glob blocks.  Every (glob, sharer) slot k whose sharer is a
  * subdomain of this rank (slot_sub[k] = its local index, -1 otherwise) gets
@@ -350,10 +366,13 @@ int bddc_pc_primal_pieces_lu(const int* nB, const long long* soff, const long lo
                              const double* LU, double* MP, double* RP, double* Cl,
                              const long long* coff, int nbatch, int max_nB, cudaStream_t stream);
 
-/* coarse[g,g] += contrib.  replaces solver.py:106. */
+/* coarse = sum_i P_i^T C_i P_i (dense n_c x n_c, every entry written, fixed
+ * summation order: no atomics).  cstart (n_c + 1) / csrc: for each coarse dof
+ * the positions in pgid of its (subdomain, local primal) sources, ascending.
+ * replaces solver.py:106. */
 int bddc_coarse_scatter(const int* pstart, const int* pgid, const double* Cl,
-                        const long long* coff, double* C, long long ldc, int nbatch,
-                        cudaStream_t stream);
+                        const long long* coff, const long long* cstart, const long long* csrc,
+                        double* C, long long ldc, int n_c, int nbatch, cudaStream_t stream);
 
 /* y_i = M_i u[perm_i] (+ c_i = G_i u[perm_i]).  replaces interface_operator solver.py:229-233
  * (M = S) and the local half of BddcPreconditioner.apply solver.py:201-209 (M = A). */

@@ -11,7 +11,13 @@ from .engine import DevicePrimalSpace
 
 @dataclass
 class GevpReport:
-    """adaptive.py:36-47 (eigenvalues and counts; vectors are not exported)."""
+    """adaptive.py:36-47.  With the default detail=True of
+    adaptive_primal_space every field is filled from the device run of the
+    reference algorithm: pencil_left / pencil_right are (B, B~) of the pencil
+    (face: B_F and the parallel sum; edge_new: M and the eliminated B~~;
+    edge_old: B_E and the parallel-sum chain), vectors its eigenvectors
+    (columns aligned with eigenvalues), degenerate the common-nullspace mask
+    and constraint_matrix the selected rows (pencil_left v_sel)^T."""
 
     glob_id: str
     variant: str
@@ -55,19 +61,29 @@ class PrimalBasis:
         return self._transforms
 
 
-def adaptive_primal_space(globs, ops_list, scaling, theta_f, theta_e, variant):
-    """Reference signature (adaptive.py:288); returns (PrimalBasis, [GevpReport])."""
+def adaptive_primal_space(globs, ops_list, scaling, theta_f, theta_e, variant, detail=True):
+    """Reference signature (adaptive.py:288); returns (PrimalBasis, [GevpReport]).
+
+    detail=True (the reference's behaviour) runs the reference algorithm
+    verbatim on the device for every glob and fills every GevpReport field;
+    detail=False uses the certified fast paths (same counts and spans, see
+    DESIGN.md) and reports eigenvalues and counts only."""
     ls = ops_list[0].ls
-    dev = DevicePrimalSpace(ls, scaling.device, theta_f, theta_e, variant)
+    dev = DevicePrimalSpace(ls, scaling.device, theta_f, theta_e, variant, detail=detail)
     basis = PrimalBasis(globs, variant=variant, device=dev)
     reports = []
     eig = dev.all_eigenvalues()
+    host = dev.detail.cpu().numpy() if detail else None
     for k, g in enumerate(globs.globs):
         if g.kind == "vertex":
             continue
         v = "face" if g.kind == "face" else ("edge_new" if variant == "new" else "edge_old")
+        if detail:
+            left, right, vecs, degen, rows = dev.glob_detail(k, host)
+        else:
+            left = right = vecs = degen = rows = None
         reports.append(GevpReport(globs.glob_id(g), v, eig.get(k, np.zeros(0)),
-                                  int(dev.n_sel_host[k]), None, g.size))
+                                  int(dev.n_sel_host[k]), rows, g.size, vecs, degen, left, right))
     return basis, reports
 
 

@@ -7,6 +7,7 @@ nvcc compiles every csrc/*.cu for -gencode arch=compute_100a,code=sm_100a with
 are involved (the ABI is plain pointers + cudaStream_t).
 """
 
+import fcntl
 import glob
 import os
 import subprocess
@@ -21,16 +22,29 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-I", INCLUDE]
 
 
+def _fresh(target, deps):
+    return os.path.exists(target) and os.path.getmtime(target) >= max(os.path.getmtime(d) for d in deps)
+
+
 def build(force=False, verbose=False, defines=(), out=None):
     """Compile csrc/*.cu into OUT (or `out`), optionally with -D defines
-    (tuning variants for tools/bench_tile.py)."""
-    global OUT
+    (tuning variants for tools/bench_tile.py).  Concurrent callers (one
+    process per GPU) serialise on a file lock; the header the ctypes
+    binding parses is a dependency too."""
     target = out or OUT
     sources = sorted(glob.glob(os.path.join(SRC, "*.cu")))
-    deps = sources + glob.glob(os.path.join(SRC, "*.cuh")) + glob.glob(os.path.join(SRC, "*.h"))
-    if not force and not defines and os.path.exists(target):
-        if os.path.getmtime(target) >= max(os.path.getmtime(d) for d in deps):
-            return target
+    deps = (sources + glob.glob(os.path.join(SRC, "*.cuh")) + glob.glob(os.path.join(SRC, "*.h"))
+            + [os.path.join(INCLUDE, "bddc_b200.h")])
+    if not force and not defines and _fresh(target, deps):
+        return target
+    with open(os.path.join(HERE, ".build.lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not defines and _fresh(target, deps):
+            return target  # another process built it while we waited
+        return _compile(target, sources, verbose, defines)
+
+
+def _compile(target, sources, verbose, defines):
     objdir = os.path.join(HERE, "build" if not defines else "build_" + "_".join(d.replace("=", "") for d in defines))
     os.makedirs(objdir, exist_ok=True)
     objs = []

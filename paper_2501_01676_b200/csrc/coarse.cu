@@ -397,14 +397,13 @@ int bddc_coarse_factor(double* C, const long long* off, const int* ldv, const in
   (void)nv;
   if (n <= 0) return 0;
   const int smem = (int)sizeof(CoarseFactorSmem);
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce once;
+  once([&] {
     cudaFuncSetAttribute(coarse_pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(coarse_row_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(coarse_trail_pivot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          smem);
-    attr = true;
-  }
+  });
   long long off0 = 0;
   cudaMemcpyAsync(&off0, off, sizeof(long long), cudaMemcpyDeviceToHost, stream);
   cudaStreamSynchronize(stream);
@@ -446,13 +445,12 @@ int bddc_coarse_blockinv(const double* A, long long ld, int n, const double* pin
                          const long long* foff, const long long* goff, int max_ldf, int max_ldg,
                          double* F, double* G, cudaStream_t stream) {
   if (n <= 0 || nD <= 0) return 0;
-  static bool attr = false;
   const int smem = (int)sizeof(TileSmem);
-  if (!attr) {
+  static PerDeviceOnce once;
+  once([&] {
     cudaFuncSetAttribute(coarse_blk_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaFuncSetAttribute(coarse_blk_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  });
   coarse_blk_fill_kernel<<<dim3(kCB / 8, nD), 256, 0, stream>>>(A, ld, n, pinv, pinv_step_stride,
                                                                 cl, cu, foff, goff, F, G);
   int launches = 1;

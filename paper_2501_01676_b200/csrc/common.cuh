@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #define BDDC_DEV __device__ __forceinline__
 
 extern "C" void bddc_note_launches(int n);
@@ -35,5 +37,47 @@ template <typename T>
 BDDC_DEV T ld_nc(const T* p) { return __ldg(p); }
 
 inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+// One-time host-side setup per CUDA device (kernel attributes such as
+// cudaFuncAttributeMaxDynamicSharedMemorySize apply per device).  The setup
+// functions are idempotent, so concurrent first callers may both run them.
+struct PerDeviceOnce {
+  static constexpr int kMaxDev = 64;
+  std::atomic<int> done[kMaxDev] = {};
+  template <class F>
+  void operator()(F&& f) {
+    const int dev = current_device();
+    if (dev < 0 || dev >= kMaxDev) {
+      f();
+      return;
+    }
+    if (done[dev].load(std::memory_order_acquire)) return;
+    f();
+    done[dev].store(1, std::memory_order_release);
+  }
+};
+
+// Per-device cached integer (e.g. an occupancy-derived grid size); 0 = unset.
+struct PerDeviceInt {
+  static constexpr int kMaxDev = 64;
+  std::atomic<int> v[kMaxDev] = {};
+  template <class F>
+  int get(F&& f) {
+    const int dev = current_device();
+    if (dev < 0 || dev >= kMaxDev) return f();
+    int x = v[dev].load(std::memory_order_acquire);
+    if (x == 0) {
+      x = f();
+      v[dev].store(x, std::memory_order_release);
+    }
+    return x;
+  }
+};
 
 }  // namespace bddc

@@ -507,7 +507,47 @@ struct GlobOut {
   double* Q;                // n_g x n_g, q_off[g]
   const long long* q_off;
   int* status;              // per glob
+  // 1: the reference algorithm verbatim (no certified shortcuts: eigen-based
+  // pseudo-inverse in the parallel sums, the general pencil solver)
+  int general;
+  // optional per-glob detail (the reference GevpReport fields), n = n_eig:
+  // detail + detail_off[g] = [pencil_left n^2 | pencil_right n^2 | vectors n^2 |
+  // constraint rows (n_sel x n) n^2 | degenerate flags n]; null = not written
+  double* detail;
+  const long long* detail_off;
 };
+
+BDDC_DEV double* detail_of(const GlobOut& o, int g) {
+  return o.detail ? o.detail + o.detail_off[g] : nullptr;
+}
+
+// copy an m x n block (ld src) to a dense row-major destination
+BDDC_DEV void copy_dense(double* dst, const double* src, int lds, int m, int n) {
+  for (int idx = threadIdx.x; idx < m * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    dst[idx] = src[(long long)r * lds + c];
+  }
+}
+
+// detail: left/right pencils before the eigensolve
+BDDC_DEV void detail_pencil(const GlobOut& o, int g, const double* L, const double* R, int n) {
+  double* d = detail_of(o, g);
+  if (!d) return;
+  copy_dense(d, L, n, n, n);
+  copy_dense(d + n * n, R, n, n, n);
+  __syncthreads();
+}
+
+// detail: all eigenvectors, constraint rows and degenerate flags after selection
+BDDC_DEV void detail_result(const GlobOut& o, int g, const double* vecs, const double* rows,
+                            int nsel, const int* degen, int n) {
+  double* d = detail_of(o, g);
+  if (!d) return;
+  copy_dense(d + 2 * n * n, vecs, n, n, n);
+  copy_dense(d + 3 * n * n, rows, n, nsel, n);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) d[4 * n * n + j] = degen[j] ? 1.0 : 0.0;
+  __syncthreads();
+}
 
 // Arena (doubles) of one face: 10 n^2 + 3 n (+ pad), see face_kernel.
 __host__ __device__ inline long long face_arena(long long n) { return 10 * n * n + 40 * n + 64; }
@@ -561,10 +601,12 @@ __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* _
     if (threadIdx.x == 0) o.status[g] = 101;
     return;
   }
-  if (!psum_fast(Bti, Btj, n, Bt, psw, rowbuf, red)) parallel_sum(Bti, Btj, n, Bt, psw, cs, perm, red);
+  if (o.general || !psum_fast(Bti, Btj, n, Bt, psw, rowbuf, red))
+    parallel_sum(Bti, Btj, n, Bt, psw, cs, perm, red);
+  detail_pencil(o, g, BF, Bt, n);
   double* vals = o.eig + o.eig_off[g];
   st = 0;
-  if (!pencil_fast(BF, Bt, n, theta, vals, VEC, degen, PEN + nn, cs, perm, red))
+  if (o.general || !pencil_fast(BF, Bt, n, theta, vals, VEC, degen, PEN + nn, cs, perm, red))
     st = pencil(BF, Bt, n, vals, VEC, degen, PEN, cs, perm, red);
   if (st) {
     if (threadIdx.x == 0) o.status[g] = 200 + st;
@@ -592,6 +634,7 @@ __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* _
     rows[perm[j] * n + c] = s;
   }
   __syncthreads();
+  detail_result(o, g, VEC, rows, nsel, degen, n);
   const int r = row_space_basis(rows, n, nsel, n, o.Q + o.q_off[g], PEN + nn, cs, perm, red);
   if (threadIdx.x == 0) {
     o.n_sel[g] = nsel;
@@ -1169,7 +1212,8 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
   int* degen = reinterpret_cast<int*>(T2);
   double* rows = T2 + nC;
   int st = 0;
-  if (!pencil_fast(M, Btt, nC, theta, vals, vecs, degen, scratch, cs, perm, red))
+  detail_pencil(o, g, M, Btt, nC);
+  if (o.general || !pencil_fast(M, Btt, nC, theta, vals, vecs, degen, scratch, cs, perm, red))
     st = pencil(M, Btt, nC, vals, vecs, degen, scratch, cs, perm, red);
   if (st) {
     if (threadIdx.x == 0) o.status[g] = 200 + st;
@@ -1196,6 +1240,7 @@ __global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const doubl
     rows[perm[j] * nC + c] = s;
   }
   __syncthreads();
+  detail_result(o, g, vecs, rows, nsel, degen, nC);
   PROF(20);
   // reshape (nsel x nC) row-major -> (nsel*(ns-1)) x ne and reduce
   const int r = row_space_basis(rows, ne, nsel * (ns - 1), ne, o.Q + o.q_off[g], scratch, cs,
@@ -1250,7 +1295,8 @@ __global__ void __launch_bounds__(256) edge_old_kernel(GlobTables t, const doubl
   for (int i = 1; i < ns && !st; ++i) {
     st = glob_schur(t, k0 + i, n, Sb, rowbuf);
     if (st) { bad = i; break; }
-    if (!psum_fast(acc, Sb, n, nxt, scratch, rowbuf, red)) parallel_sum(acc, Sb, n, nxt, scratch, cs, perm, red);
+    if (o.general || !psum_fast(acc, Sb, n, nxt, scratch, rowbuf, red))
+      parallel_sum(acc, Sb, n, nxt, scratch, cs, perm, red);
     blk::copy(acc, n, nxt, n, n, n);
   }
   if (st) {
@@ -1259,7 +1305,8 @@ __global__ void __launch_bounds__(256) edge_old_kernel(GlobTables t, const doubl
   }
   double* vals = o.eig + o.eig_off[g];
   st = 0;
-  if (!pencil_fast(BE, acc, n, theta, vals, vecs, degen, scratch, cs, perm, red))
+  detail_pencil(o, g, BE, acc, n);
+  if (o.general || !pencil_fast(BE, acc, n, theta, vals, vecs, degen, scratch, cs, perm, red))
     st = pencil(BE, acc, n, vals, vecs, degen, scratch, cs, perm, red);
   if (st) {
     if (threadIdx.x == 0) o.status[g] = 200 + st;
@@ -1285,6 +1332,7 @@ __global__ void __launch_bounds__(256) edge_old_kernel(GlobTables t, const doubl
     rows[perm[j] * n + c] = s;
   }
   __syncthreads();
+  detail_result(o, g, vecs, rows, nsel, degen, n);
   const int r = row_space_basis(rows, n, nsel, n, o.Q + o.q_off[g], scratch, cs, perm, red);
   if (threadIdx.x == 0) {
     o.n_sel[g] = nsel;
@@ -1383,12 +1431,16 @@ int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const 
                    const double* BiC, const double* SC, const int* sc_status, const double* D, double theta, double* eig,
                    const long long* eig_off, int* n_sel, int* r, double* Q, const long long* q_off,
                    int* status, double* ws, const long long* ws_off, const int* face_ids,
-                   int n_faces, int max_n, int fast, cudaStream_t stream) {
+                   int n_faces, int max_n, int mode, double* detail, const long long* detail_off,
+                   cudaStream_t stream) {
   if (n_faces <= 0) return 0;
   GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC, SC, sc_status);
-  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
+  // mode 1: certified fast kernel; 0: general kernel with the certified shortcuts;
+  // -1: the reference algorithm verbatim.  A detail request implies mode -1.
+  if (detail) mode = -1;
+  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status, mode < 0 ? 1 : 0, detail, detail_off};
   const int small = face_small_bytes(max_n);
-  if (fast) {
+  if (mode == 1) {
     const long long arena = face_fast_arena(max_n) * 8;
     const int in_smem = (small + arena) <= kFaceFastSmemBudget;
     const int smem = small + (in_smem ? (int)arena : 0);
@@ -1425,11 +1477,12 @@ int bddc_edge_gevp_new(const int* kind, const int* size, const int* sh_start, co
                        const long long* ex_off, const int* ex_h, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
-                       const int* edge_ids, int n_edges, int max_dim, cudaStream_t stream) {
+                       const int* edge_ids, int n_edges, int max_dim, int general, double* detail,
+                       const long long* detail_off, cudaStream_t stream) {
   if (n_edges <= 0) return 0;
   GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC, SC, sc_status);
   PriorTables pr{EX, ex_off, ex_h};
-  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
+  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status, (general || detail) ? 1 : 0, detail, detail_off};
   const int smem = shmem_for(max_dim);
   if (smem > 48 * 1024) cudaFuncSetAttribute(edge_new_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   edge_new_kernel<<<n_edges, 256, smem, stream>>>(t, D, pr, theta, o, ws, ws_off, edge_ids); bddc_note_launches(1);
@@ -1442,10 +1495,11 @@ int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, co
                        const double* D, double theta, double* eig,
                        const long long* eig_off, int* n_sel, int* r, double* Q,
                        const long long* q_off, int* status, double* ws, const long long* ws_off,
-                       const int* edge_ids, int n_edges, int max_n, cudaStream_t stream) {
+                       const int* edge_ids, int n_edges, int max_n, int general, double* detail,
+                       const long long* detail_off, cudaStream_t stream) {
   if (n_edges <= 0) return 0;
   GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC, SC, sc_status);
-  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status};
+  GlobOut o{eig, eig_off, n_sel, r, Q, q_off, status, (general || detail) ? 1 : 0, detail, detail_off};
   const int smem = shmem_for(max_n);
   if (smem > 48 * 1024) cudaFuncSetAttribute(edge_old_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   edge_old_kernel<<<n_edges, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, edge_ids); bddc_note_launches(1);

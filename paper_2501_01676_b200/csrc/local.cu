@@ -20,40 +20,178 @@ namespace bddc {
 
 // ---------------------------------------------------------------------------
 // local assembly: element 4x4 blocks -> dense [I | B] x [I | B | f] matrix
+//
+// Deterministic (no atomics; bitwise reproducible run to run), one CTA per
+// subdomain:
+//  1. the subdomain's element corners are bucketed by local row with a
+//     stable counting sort: warp w histograms a contiguous chunk of corners,
+//     an exclusive scan over (row, warp) gives every warp its cursor in every
+//     row, and each warp places its chunk in order (__match_any_sync ranks
+//     lanes with equal rows), so each row's list is in ascending corner order;
+//  2. one warp per row accumulates the row in shared memory in that order
+//     (lane t adds corner t's four entries, lanes in turn) and writes all ld
+//     entries of the row ([I|B] columns, the load column with the Dirichlet
+//     lifting, padding), so K needs no memset.
 // ---------------------------------------------------------------------------
-__global__ void assemble_kernel(double* __restrict__ base, const long long* __restrict__ off,
-                                const int* __restrict__ ld, const int* __restrict__ nloc,
-                                const long long* __restrict__ elem_start,
-                                const long long* __restrict__ elem_ids,
-                                const int* __restrict__ loc4, const long long* __restrict__ conn,
-                                const double* __restrict__ Ke, const double* __restrict__ Fe,
-                                const double* __restrict__ gdir) {
-  const int b = blockIdx.y;
-  const long long e0 = elem_start[b], e1 = elem_start[b + 1];
-  const long long j = e0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= e1) return;
-  const long long e = elem_ids[j];
-  const int nL = nloc[b];
-  const int L = ld[b];
-  double* M = base + off[b];
-  int li[4];
+constexpr int kAsmWarps = 8;
+
+BDDC_DEV int block_excl_scan_ints(int* a, int n, int* red) {
+  // in-place exclusive scan of a[0..n) by the whole CTA; returns the total.
+  // red: kAsmWarps + 1 ints of shared scratch
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int per = (n + nt - 1) / nt;
+  const int i0 = min(n, t * per), i1 = min(n, i0 + per);
+  int s = 0;
+  for (int i = i0; i < i1; ++i) s += a[i];
+  const int lane = t & 31, w = t >> 5;
+  int x = s;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) li[a] = loc4[e * 4 + a];
-#pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int r = li[a];
-    if (r >= nL) continue;
-    double fr = Fe[e * 4 + a];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double v = Ke[e * 16 + a * 4 + c];
-      if (li[c] < nL)
-        atomicAdd(M + (long long)r * L + li[c], v);
-      else
-        fr -= v * gdir[conn[e * 4 + c]];
-    }
-    atomicAdd(M + (long long)r * L + nL, fr);
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
   }
+  if (lane == 31) red[w] = x;
+  __syncthreads();
+  if (t == 0) {
+    int run = 0;
+    for (int k = 0; k < (nt >> 5); ++k) {
+      const int v = red[k];
+      red[k] = run;
+      run += v;
+    }
+    red[nt >> 5] = run;
+  }
+  __syncthreads();
+  int run = red[w] + x - s;
+  for (int i = i0; i < i1; ++i) {
+    const int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  const int total = red[nt >> 5];
+  __syncthreads();
+  return total;
+}
+
+__global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
+    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
+    const int* __restrict__ nloc, const long long* __restrict__ elem_start,
+    const long long* __restrict__ elem_ids, const int* __restrict__ loc4,
+    const long long* __restrict__ conn, const double* __restrict__ Ke,
+    const double* __restrict__ Fe, const double* __restrict__ gdir, int* __restrict__ lists,
+    int nrowbuf) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int b = blockIdx.x;
+  const int nL = nloc[b], L = ld[b];
+  const long long e0 = elem_start[b], e1 = elem_start[b + 1];
+  const long long nc = 4 * (e1 - e0);
+  const int stride = nL + 1;
+  int* hist = reinterpret_cast<int*>(smem_raw);  // kAsmWarps x (nL + 1): counts, then cursors
+  int* rowptr = hist + kAsmWarps * stride;        // nL + 1
+  int* red = rowptr + stride;                     // kAsmWarps + 1
+  double* rowbuf = reinterpret_cast<double*>(
+      smem_raw + ((((size_t)(kAsmWarps * stride + stride + kAsmWarps + 1)) * 4 + 15) & ~(size_t)15));
+  int* lst = lists + 4 * e0;
+  const long long* eid = elem_ids + e0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i < kAsmWarps * stride; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const long long chunk = (nc + kAsmWarps - 1) / kAsmWarps;
+  const long long c0 = min(nc, (long long)warp * chunk), c1 = min(nc, c0 + chunk);
+  int* h = hist + warp * stride;
+  for (long long j = c0 + lane; j < c1; j += 32) {
+    const int r = loc4[eid[j >> 2] * 4 + (j & 3)];
+    if (r < nL) atomicAdd(h + r, 1);  // integer counts: order-independent
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < nL; r += blockDim.x) {
+    int s = 0;
+#pragma unroll
+    for (int w = 0; w < kAsmWarps; ++w) s += hist[w * stride + r];
+    rowptr[r] = s;
+  }
+  __syncthreads();
+  const int total = block_excl_scan_ints(rowptr, nL, red);
+  if (threadIdx.x == 0) rowptr[nL] = total;
+  for (int r = threadIdx.x; r < nL; r += blockDim.x) {
+    int run = rowptr[r];
+#pragma unroll
+    for (int w = 0; w < kAsmWarps; ++w) {
+      const int v = hist[w * stride + r];
+      hist[w * stride + r] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  // stable placement, 32 corners at a time in order
+  for (long long jb = c0; jb < c1; jb += 32) {
+    const long long j = jb + lane;
+    int r = -1;
+    if (j < c1) {
+      r = loc4[eid[j >> 2] * 4 + (j & 3)];
+      if (r >= nL) r = -1;
+    }
+    const unsigned m = __match_any_sync(0xffffffffu, r);
+    const int rank = __popc(m & ((1u << lane) - 1u));
+    int pos = 0;
+    if (r >= 0) pos = h[r];
+    __syncwarp();
+    if (r >= 0 && rank == 0) h[r] = pos + __popc(m);
+    __syncwarp();
+    if (r >= 0) lst[pos + rank] = (int)j;
+  }
+  __syncthreads();
+  if (warp >= nrowbuf) return;
+  double* rb = rowbuf + (size_t)warp * L;
+  double* M = base + off[b];
+  const int nwr = min(nrowbuf, kAsmWarps);
+  for (int r = warp; r < nL; r += nwr) {
+    for (int c = lane; c < L; c += 32) rb[c] = 0.0;
+    __syncwarp();
+    const int s0 = rowptr[r], s1 = rowptr[r + 1];
+    for (int sb = s0; sb < s1; sb += 32) {
+      const int s = sb + lane;
+      int col[4] = {-1, -1, -1, -1};
+      double val[4] = {0.0, 0.0, 0.0, 0.0};
+      double fr = 0.0;
+      if (s < s1) {
+        const int j = lst[s];
+        const long long e = eid[j >> 2];
+        const int a = j & 3;
+        fr = Fe[e * 4 + a];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double v = Ke[e * 16 + a * 4 + c];
+          const int li = loc4[e * 4 + c];
+          if (li < nL) {
+            col[c] = li;
+            val[c] = v;
+          } else {
+            fr -= v * gdir[conn[e * 4 + c]];
+          }
+        }
+      }
+      const int cnt = min(32, s1 - sb);
+      for (int t = 0; t < cnt; ++t) {
+        if (lane == t) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (col[c] >= 0) rb[col[c]] += val[c];
+          rb[nL] += fr;
+        }
+        __syncwarp();
+      }
+    }
+    double* row = M + (long long)r * L;
+    for (int c = lane; c < L; c += 32) row[c] = rb[c];
+    __syncwarp();
+  }
+}
+
+static size_t assemble_smem_bytes(int max_nl, int nrowbuf) {
+  const size_t ints = (size_t)kAsmWarps * (max_nl + 1) + (max_nl + 1) + kAsmWarps + 1;
+  return ((ints * 4 + 15) & ~(size_t)15) + (size_t)nrowbuf * (max_nl + 2) * 8;
 }
 
 // ---------------------------------------------------------------------------
@@ -443,16 +581,18 @@ __global__ void extract_schur_kernel(const double* __restrict__ base, const long
   }
 }
 
-// out[b] += ||X_b||_F^2 for square batched matrices (ld = n); out zeroed by the caller
-__global__ void frob2_kernel(const double* __restrict__ X, const long long* __restrict__ soff,
-                             const int* __restrict__ nB, double* __restrict__ out) {
-  __shared__ double red[8];
-  const int b = blockIdx.y;
+// out[b] = ||X_b||_F^2 for square batched matrices (ld = n); one CTA per
+// matrix, fixed reduction tree (deterministic)
+__global__ void __launch_bounds__(512) frob2_kernel(const double* __restrict__ X,
+                                                    const long long* __restrict__ soff,
+                                                    const int* __restrict__ nB,
+                                                    double* __restrict__ out) {
+  __shared__ double red[16];
+  const int b = blockIdx.x;
   const long long nn = (long long)nB[b] * nB[b];
   const double* M = X + soff[b];
   double s = 0.0;
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < nn;
-       idx += (long long)gridDim.x * blockDim.x) {
+  for (long long idx = threadIdx.x; idx < nn; idx += blockDim.x) {
     const double v = M[idx];
     s = fma(v, v, s);
   }
@@ -462,7 +602,7 @@ __global__ void frob2_kernel(const double* __restrict__ X, const long long* __re
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-    atomicAdd(out + b, t);
+    out[b] = t;
   }
 }
 
@@ -525,8 +665,8 @@ __global__ void __launch_bounds__(256) recover_kernel(
 using namespace bddc;
 
 static int smem_tile_setup() {
-  static bool done = false;
-  if (!done) {
+  static PerDeviceOnce once;
+  once([&] {
     int bytes = (int)sizeof(TileSmem);
     cudaFuncSetAttribute(schur_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(schur_trailing_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -536,8 +676,7 @@ static int smem_tile_setup() {
     cudaFuncSetAttribute(gj_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(panel_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(schur_fix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    done = true;
-  }
+  });
   return (int)sizeof(TileSmem);
 }
 
@@ -564,11 +703,16 @@ int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_e
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
                         const long long* elem_start, const long long* elem_ids, const int* loc4,
                         const long long* conn, const double* Ke, const double* Fe,
-                        const double* gdir, int nbatch, long long max_elems, cudaStream_t stream) {
-  if (nbatch <= 0 || max_elems <= 0) return 0;
-  dim3 grid(ceil_div(max_elems, 128), nbatch);
-  assemble_kernel<<<grid, 128, 0, stream>>>(K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke,
-                                             Fe, gdir);
+                        const double* gdir, int nbatch, int max_nl, int* lists,
+                        cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  int nrowbuf = kAsmWarps;
+  while (nrowbuf > 1 && assemble_smem_bytes(max_nl, nrowbuf) > 200 * 1024) --nrowbuf;
+  const size_t smem = assemble_smem_bytes(max_nl, nrowbuf);
+  if (smem > 227 * 1024) return -(int)cudaErrorInvalidValue;
+  cudaFuncSetAttribute(assemble_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  assemble_rows_kernel<<<nbatch, kAsmWarps * 32, smem, stream>>>(
+      K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke, Fe, gdir, lists, nrowbuf);
   bddc_note_launches(1);
   return launch_status();
 }
@@ -604,9 +748,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) lu128_fixup_kern
 // Optional event log of the trailing-update launches (bench roofline over the
 // timed region without a mid-step synchronisation): bddc_trailing_log(1)
 // starts it, bddc_trailing_collect() sums the logged durations and clears it.
-static std::vector<cudaEvent_t> g_trail_pool;  // created once, reused
-static size_t g_trail_used = 0;
-static bool g_trail_on = false;
+// per host thread (the C-ABI keeps no process-wide mutable state besides the
+// launch counter): each thread driving a device has its own log
+static thread_local std::vector<cudaEvent_t> g_trail_pool;  // created once, reused
+static thread_local size_t g_trail_used = 0;
+static thread_local bool g_trail_on = false;
 
 static int schur_eliminate_impl(double* M, const long long* off, const int* ld, const int* npiv,
                                 const int* nrows, const int* ncols, int nbatch, int max_npiv,
@@ -773,11 +919,10 @@ int bddc_lu128_fixup(double* M, const long long* off, const int* ld, const int* 
                      int max_n, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   const int smem = smem_tile_setup();
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce once;
+  once([&] {
     cudaFuncSetAttribute(lu128_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  });
   for (int k = 0; k + 2 * kTile < max_n; k += 2 * kTile) {
     const int t = ceil_div(max_n - k - 2 * kTile, kTile);
     lu128_fixup_kernel<<<dim3(t, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 0);
@@ -793,13 +938,12 @@ int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int
                        cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   const int smem = smem_tile_setup();
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce once;
+  once([&] {
     cudaFuncSetAttribute(gj128_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(TileSmemT<128>));
     cudaFuncSetAttribute(gj128_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  });
   const int T = ceil_div(max_n, kTile);
   const NextPivot none{nullptr, 0, nullptr, 0, nullptr, 0};
   for (int k = 0; k < max_n; k += 128) {
@@ -833,7 +977,7 @@ int bddc_extract_schur(const double* M, const long long* off, const int* ld, con
 int bddc_frob2(const double* X, const long long* soff, const int* n, int nbatch, double* out,
                cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  frob2_kernel<<<dim3(16, nbatch), 256, 0, stream>>>(X, soff, n, out);
+  frob2_kernel<<<nbatch, 512, 0, stream>>>(X, soff, n, out);
   bddc_note_launches(1);
   return launch_status();
 }

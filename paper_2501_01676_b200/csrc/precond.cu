@@ -751,17 +751,34 @@ __global__ void primal_rows_times_T_kernel(SubGlobMap m, const double* __restric
   }
 }
 
-// coarse assembly C[gp][gq] += C_i[p][q]
+// coarse assembly C[gp][gq] = sum_i C_i[p][q], deterministic: one warp owns
+// coarse row gp, zeroes it, then adds the rows of its sources (the (subdomain,
+// local primal) pairs mapped to gp, csrc[cstart[gp]..cstart[gp+1]) in ascending
+// subdomain order) one after the other; within one source the columns
+// pgid[p0 + q] are distinct, so the lanes never collide.
 __global__ void coarse_scatter_kernel(const int* __restrict__ pstart, const int* __restrict__ pgid,
                                       const double* __restrict__ Cl,
-                                      const long long* __restrict__ coff, double* __restrict__ C,
-                                      long long ldc) {
-  const int b = blockIdx.x;
-  const int p0 = pstart[b], np = pstart[b + 1] - p0;
-  const double* Cb = Cl + coff[b];
-  for (int idx = threadIdx.x; idx < np * np; idx += blockDim.x) {
-    const int p = idx / np, q = idx - p * np;
-    atomicAdd(C + (long long)pgid[p0 + p] * ldc + pgid[p0 + q], Cb[idx]);
+                                      const long long* __restrict__ coff,
+                                      const long long* __restrict__ cstart,
+                                      const long long* __restrict__ csrc, double* __restrict__ C,
+                                      long long ldc, int n_c, int nbatch) {
+  const int gp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (gp >= n_c) return;
+  double* row = C + (long long)gp * ldc;
+  for (int c = lane; c < n_c; c += 32) row[c] = 0.0;
+  __syncwarp();
+  for (long long s = cstart[gp]; s < cstart[gp + 1]; ++s) {
+    const int f = (int)csrc[s];
+    int lo = 0, hi = nbatch;  // largest b with pstart[b] <= f
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pstart[mid] <= f) lo = mid; else hi = mid;
+    }
+    const int b = lo, p0 = pstart[b], np = pstart[b + 1] - p0, p = f - p0;
+    const double* Cb = Cl + coff[b] + (long long)p * np;
+    for (int q = lane; q < np; q += 32) row[pgid[p0 + q]] += Cb[q];
+    __syncwarp();
   }
 }
 
@@ -1135,12 +1152,11 @@ static int glob_mma(const int* nB, const long long* soff, const int* sub_glob_st
                     const int* gsize, const double* L, const double* LT, const long long* loff,
                     int by_slot, int right, const double* in, double* out, int n_items,
                     int max_nB, int max_ng, int max_globs, cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce once;
+  once([&] {
     cudaFuncSetAttribute(glob_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(TileSmem));
-    attr = true;
-  }
+  });
   if (max_ng >= kMmaMinNg) {
     const int tpi = ceil_div(max_nB, 64);
     dim3 grid((unsigned)(n_items * tpi), ceil_div(max_ng, 64));
@@ -1273,12 +1289,11 @@ int bddc_pc_transform_embed(const int* nB, const long long* soff, const long lon
   const long long bytes = (long long)max_rows_block * max_nB * (long long)sizeof(double);
   dim3 grid((unsigned)max_globs, (unsigned)nbatch);
   if (bytes <= 200 * 1024) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce once;
+    once([&] {
       cudaFuncSetAttribute(transform_embed_kernel<true>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
+    });
     transform_embed_kernel<true><<<grid, 256, (size_t)bytes, stream>>>(
         nB, soff, voff, sub_glob_start, sub_globs, sub_glob_boff, kind, gsize, r, HV, q_off, pidx,
         poff, S, Z, Srows, Scols);
@@ -1317,10 +1332,12 @@ int bddc_pc_primal_pieces_lu(const int* nB, const long long* soff, const long lo
 }
 
 int bddc_coarse_scatter(const int* pstart, const int* pgid, const double* Cl,
-                        const long long* coff, double* C, long long ldc, int nbatch,
-                        cudaStream_t stream) {
-  if (nbatch <= 0) return 0;
-  coarse_scatter_kernel<<<nbatch, 128, 0, stream>>>(pstart, pgid, Cl, coff, C, ldc); bddc_note_launches(1);
+                        const long long* coff, const long long* cstart, const long long* csrc,
+                        double* C, long long ldc, int n_c, int nbatch, cudaStream_t stream) {
+  if (n_c <= 0) return 0;
+  coarse_scatter_kernel<<<ceil_div(n_c, 8), 256, 0, stream>>>(pstart, pgid, Cl, coff, cstart, csrc,
+                                                             C, ldc, n_c, nbatch);
+  bddc_note_launches(1);
   return pc_status();
 }
 
@@ -1363,17 +1380,16 @@ int bddc_coarse_solve(const double* A, long long ld, int n, const double* pinv,
                       long long pinv_step_stride, const int* lim, const int* first, double* b,
                       double* t, cudaStream_t stream) {
   if (n <= 0) return 0;
-  static int grid = 0;
-  if (grid == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+  static PerDeviceInt cached;
+  const int grid = cached.get([] {
+    int dev = current_device(), sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_solve_coop_kernel,
                                                   BDDC_COOP_THREADS, 0);
-    grid = BDDC_COOP_CTAS > 0 ? BDDC_COOP_CTAS : sms;
-    if (grid > sms * per_sm) grid = sms * per_sm;
-    if (grid <= 0) grid = 1;
-  }
+    int g = BDDC_COOP_CTAS > 0 ? BDDC_COOP_CTAS : sms;
+    if (g > sms * per_sm) g = sms * per_sm;
+    return g <= 0 ? 1 : g;
+  });
   void* args[] = {(void*)&A, (void*)&ld, (void*)&n, (void*)&pinv, (void*)&pinv_step_stride,
                   (void*)&lim, (void*)&first, (void*)&b, (void*)&t};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)coarse_solve_coop_kernel, dim3(grid),
@@ -1387,15 +1403,14 @@ int bddc_coarse_solve_flow(const double* A, long long ld, int n, const double* p
                            double* t, int* flags, int epoch, cudaStream_t stream) {
   if (n <= 0) return 0;
   const int smem = (kSP * kSP + 64 * 64 + 2 * kSP) * (int)sizeof(double);
-  static int grid = 0;
-  if (grid == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+  static PerDeviceInt cached;
+  const int grid = cached.get([smem] {
+    int dev = current_device(), sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(coarse_solve_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_solve_flow_kernel, 256, smem);
-    grid = sms * (per_sm > 0 ? per_sm : 1);
-  }
+    return sms * (per_sm > 0 ? per_sm : 1);
+  });
   const int nQ = (n + kSP - 1) / kSP;
   int g = nQ < grid ? nQ : grid;
   void* args[] = {(void*)&A, (void*)&ld, (void*)&n, (void*)&pinv, (void*)&pinv_step_stride,

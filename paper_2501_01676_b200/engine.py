@@ -132,14 +132,15 @@ class LocalSystem:
 
     def _factor(self):
         p, d, st = self.plan, self.d, stream()
-        K = torch.zeros(p.K_total, dtype=F64, device="cuda")
+        K = torch.empty(p.K_total, dtype=F64, device="cuda")  # every entry written by assembly
         Ke, Fe, ebad = self.inputs.get("Ke"), self.inputs.get("Fe"), self.inputs.get("_ebad")
         if Ke is None:  # element blocks built on the device from mesh + coefficients
             Ke, Fe, ebad = device_element_blocks(self.inputs)
+        lists = torch.empty(max(4 * int(p.elem_start[-1]), 1), dtype=torch.int32, device="cuda")
         lib.bddc_local_assemble(K, d.off, d.ld, d.nL, d.elem_start, d.elem_ids, d.loc4,
                                 self.inputs["conn"], Ke, Fe, self.inputs["gdir"], p.N,
-                                p.max_elems, st)
-        del Ke, Fe
+                                int(p.nL.max()), lists, st)
+        del Ke, Fe, lists
         # the element blocks are consumed: keep only the index inputs
         self.inputs = {k: v for k, v in self.inputs.items() if k not in ("Ke", "Fe", "_ebad")}
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
@@ -516,12 +517,17 @@ class DevicePrimalSpace:
     """Per-glob (Q, r) and eigenvalues produced on the device
     (reference adaptive.py:288-342 / PrimalBasis adaptive.py:209-264)."""
 
-    def __init__(self, ls, scaling, theta_f, theta_e, variant):
+    def __init__(self, ls, scaling, theta_f, theta_e, variant, general=False, detail=False):
+        """general: run the reference algorithm verbatim (no certified shortcuts:
+        eigen-based pseudo-inverses, the general pencil solver) for every glob.
+        detail: also keep the reference GevpReport fields per glob (pencils,
+        all eigenvectors, degenerate flags, constraint rows); implies general."""
         if variant not in ("old", "new"):
             raise ValueError(f"unknown variant {variant!r}")
         p, d, st, comm = ls.plan, ls.d, stream(), ls.comm
         multi = _multi(comm)
         self.ls, self.variant = ls, variant
+        self.general = bool(general or detail)
         self.theta_f, self.theta_e = float(theta_f), float(theta_e)
         BsC, BiC = ls.slot_bsym(), ls.slot_binv()
         G = p.G
@@ -537,6 +543,11 @@ class DevicePrimalSpace:
             n_eig = np.where(kind == 1, p.gsize, n_eig)
         self.eig_off = _excl(n_eig)
         self.eig = torch.zeros(max(int(self.eig_off[-1]), 1), dtype=F64, device="cuda")
+        self.detail = self.d_det_off = None
+        if detail:
+            self.det_off = _excl(4 * n_eig * n_eig + n_eig)
+            self.detail = torch.zeros(max(int(self.det_off[-1]), 1), dtype=F64, device="cuda")
+            self.d_det_off = dev_i64(self.det_off[:-1])
         d_eig_off = dev_i64(self.eig_off[:-1])
         self.r = torch.zeros(max(G, 1), dtype=torch.int32, device="cuda")
         self.n_sel = torch.zeros(max(G, 1), dtype=torch.int32, device="cuda")
@@ -554,13 +565,15 @@ class DevicePrimalSpace:
         self.sc_status = torch.zeros(max(int(p.sh_sub.size), 1), dtype=torch.int32, device="cuda")
         lib.bddc_slot_schur(dev_i32(sc_slots), sc_slots.size, d.slot_glob, d.gsize, d.sh_doff, BiC,
                             self.SC, self.sc_status, st)
-        if faces.size:
-            self._run_faces(faces, True, out, scaling, BsC, BiC, d_eig_off)
+        if faces.size and self.general:
+            self._run_faces(faces, -1, out, scaling, BsC, BiC, d_eig_off)
+        elif faces.size:
+            self._run_faces(faces, 1, out, scaling, BsC, BiC, d_eig_off)
             s = status.cpu().numpy()
             redo = faces[s[faces] == 900]
             if redo.size:  # certificates failed: general algorithm (linalg.py:116-214)
                 status[dev_i64(redo)] = 0
-                self._run_faces(redo, False, out, scaling, BsC, BiC, d_eig_off)
+                self._run_faces(redo, 0, out, scaling, BsC, BiC, d_eig_off)
         _allreduce(comm, *out)
         self._raise(status, "face")
         vert = np.flatnonzero(kind == 2)
@@ -613,7 +626,8 @@ class DevicePrimalSpace:
                                        BsC, BiC, self.SC, self.sc_status, scaling.D, EX, d_ex_off, dev_i32(sh_nH),
                                        self.theta_e, e_eig, d_eig_off, e_nsel, e_r, e_Q,
                                        self.d_q_off, e_status, ws, dev_i64(woff[:-1]),
-                                       dev_i32(edges), edges.size, int(wd.max()), st)
+                                       dev_i32(edges), edges.size, int(wd.max()),
+                                       int(self.general), self.detail, self.d_det_off, st)
                 del ws
             del EX
         elif n_edges_all and edges.size:
@@ -625,7 +639,8 @@ class DevicePrimalSpace:
             lib.bddc_edge_gevp_old(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
                                    BsC, BiC, self.SC, self.sc_status, scaling.D, self.theta_e, e_eig, d_eig_off, e_nsel,
                                    e_r, e_Q, self.d_q_off, e_status, ws, dev_i64(woff[:-1]),
-                                   dev_i32(edges), edges.size, int(p.gsize[edges].max()), st)
+                                   dev_i32(edges), edges.size, int(p.gsize[edges].max()),
+                                   int(self.general), self.detail, self.d_det_off, st)
             del ws
         if multi and n_edges_all:
             _allreduce(comm, *eout)
@@ -633,15 +648,19 @@ class DevicePrimalSpace:
                 t += e
         if n_edges_all:
             self._raise(status, "edge")
+        if multi and self.detail is not None:  # each glob's detail was written by one rank
+            comm.allreduce_(self.detail)
         self.r_host = self.r.cpu().numpy().astype(np.int64)
         self.n_sel_host = self.n_sel.cpu().numpy().astype(np.int64)
         del self.SC
 
-    def _run_faces(self, faces, fast, out, scaling, BsC, BiC, d_eig_off):
+    def _run_faces(self, faces, mode, out, scaling, BsC, BiC, d_eig_off):
+        """mode: 1 certified fast kernel, 0 general kernel, -1 reference algorithm verbatim."""
         ls, p, d, st = self.ls, self.ls.plan, self.ls.d, stream()
         eig, n_sel, r, Q, status = out
         G = p.G
         sizes = p.gsize[faces]
+        fast = mode == 1
         budget = FACE_FAST_SMEM_BUDGET if fast else FACE_SMEM_BUDGET
         arena = _face_fast_ws if fast else _face_ws
         small = _face_small_bytes(sizes) + 8 * arena(sizes) <= budget
@@ -658,7 +677,8 @@ class DevicePrimalSpace:
             lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, BsC,
                                BiC, self.SC, self.sc_status, scaling.D, self.theta_f, eig, d_eig_off, n_sel, r, Q,
                                self.d_q_off, status, ws, dev_i64(woff[:-1]), dev_i32(grp),
-                               grp.size, int(p.gsize[grp].max()), 1 if fast else 0, st)
+                               grp.size, int(p.gsize[grp].max()), mode, self.detail,
+                               self.d_det_off, st)
             del ws
 
     def _raise(self, status, what):
@@ -687,6 +707,25 @@ class DevicePrimalSpace:
         e = self.eig.cpu().numpy()
         return {k: e[self.eig_off[k]:self.eig_off[k + 1]] for k in range(self.ls.plan.G)
                 if self.eig_off[k + 1] > self.eig_off[k]}
+
+    def glob_detail(self, k, host=None):
+        """Reference GevpReport fields of glob k (needs detail=True):
+        (pencil_left, pencil_right, vectors, degenerate, constraint_matrix).
+        host: a host copy of self.detail to slice (one bulk D2H for all globs)."""
+        if self.detail is None:
+            raise RuntimeError("primal space built without detail=True")
+        n = int(self.eig_off[k + 1] - self.eig_off[k])
+        o = int(self.det_off[k])
+        src = host if host is not None else self.detail[o:o + 4 * n * n + n].cpu().numpy()
+        blk = src[o:o + 4 * n * n + n] if host is not None else src
+        nn = n * n
+        left = blk[:nn].reshape(n, n)
+        right = blk[nn:2 * nn].reshape(n, n)
+        vecs = blk[2 * nn:3 * nn].reshape(n, n)
+        nsel = int(self.n_sel_host[k])
+        rows = blk[3 * nn:3 * nn + nsel * n].reshape(nsel, n)
+        degen = blk[4 * nn:4 * nn + n] != 0.0
+        return left, right, vecs, degen, rows
 
     def q(self, k):
         n = int(self.ls.plan.gsize[k])
@@ -756,7 +795,7 @@ class DevicePreconditioner:
     """M^-1 = sum_i R_i^T (A_i R_i + N_i P_i C^-1 sum_j P_j^T G_j R_j)
     (reference BddcPreconditioner solver.py:46-209, see precond.cu)."""
 
-    def __init__(self, ls, scaling, r_host, Q, q_off, keep_coarse=8192, householder=True):
+    def __init__(self, ls, scaling, r_host, Q, q_off, householder=True):
         """householder: Q comes from the device primal space (orthogonal, full-rank
         primal rows), so it may be replaced by its Householder form; caller-given
         transforms (possibly degenerate, test_solver.py:62-77) are used as given."""
@@ -897,19 +936,24 @@ class DevicePreconditioner:
                                   self.d_poff, MP, self.Nt, p.N, st)
         del Srows, Scols, MP, RP, pinv
         nc = self.n_primal
-        C = torch.zeros(nc * nc, dtype=F64, device="cuda")
+        C = torch.empty(nc * nc, dtype=F64, device="cuda")  # every entry written by the scatter
         _allreduce(self.comm, Clg)
         if multi:
-            lib.bddc_coarse_scatter(dev_i32(_excl(np_glob)), dev_i32(new_id[gpgid0]), Clg,
-                                    dev_i64(gcoff[:-1]), C, nc, p.N_glob, st)
+            gpg = new_id[gpgid0]
+            gsrc = np.argsort(gpg, kind="stable")
+            gstart = np.searchsorted(gpg[gsrc], np.arange(nc + 1))
+            lib.bddc_coarse_scatter(dev_i32(_excl(np_glob)), dev_i32(gpg), Clg,
+                                    dev_i64(gcoff[:-1]), dev_i64(gstart), dev_i64(gsrc), C, nc, nc,
+                                    p.N_glob, st)
         else:
-            lib.bddc_coarse_scatter(self.d_pstart, self.d_pgid, Clg, d_coff, C, nc, p.N, st)
-        del Clg
-        if nc <= keep_coarse:
-            Cn = C.view(nc, nc).cpu().numpy()
-            self.coarse = Cn[np.ix_(new_id, new_id)].copy()
-        else:
-            self.coarse = None
+            lib.bddc_coarse_scatter(self.d_pstart, self.d_pgid, Clg, d_coff, self.d_cstart,
+                                    self.d_csrc, C, nc, nc, p.N, st)
+        # the (small) subdomain contributions are kept so the dense coarse matrix
+        # can be re-assembled on demand (``coarse``); nothing is copied to the host here
+        self._Clg, self._coarse_scatter_args = Clg, (
+            (dev_i32(_excl(np_glob)), dev_i32(gpg), dev_i64(gcoff[:-1]), dev_i64(gstart),
+             dev_i64(gsrc), p.N_glob) if multi else
+            (self.d_pstart, self.d_pgid, d_coff, self.d_cstart, self.d_csrc, p.N))
         steps = (nc + 63) // 64
         self.coarse_pinv = torch.empty(steps * 4096, dtype=F64, device="cuda")
         piv = torch.zeros(nc, dtype=F64, device="cuda")
@@ -948,6 +992,18 @@ class DevicePreconditioner:
         self.cvals = torch.empty(max(self.sum_np, 1), dtype=F64, device="cuda")
         self.rp = torch.empty(nc, dtype=F64, device="cuda")
         self.up = torch.empty(nc, dtype=F64, device="cuda")
+
+    @property
+    def coarse(self):
+        """Dense coarse matrix sum_i P_i^T C_i P_i in the original primal
+        numbering (reference BddcPreconditioner.coarse, solver.py:106-127),
+        re-assembled on the device on demand and copied to the host."""
+        nc = self.n_primal
+        pst, pg, coff, cst, csrc, nb = self._coarse_scatter_args
+        C = torch.empty(nc * nc, dtype=F64, device="cuda")
+        lib.bddc_coarse_scatter(pst, pg, self._Clg, coff, cst, csrc, C, nc, nc, nb, stream())
+        Cn = C.view(nc, nc).cpu().numpy()
+        return Cn[np.ix_(self.new_id, self.new_id)]
 
     @staticmethod
     def _dual_pd_certified(ls):

@@ -22,12 +22,14 @@ class Result:
 
 def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8, max_iter=300,
         plan=None, inputs=None, timings=True, keep=False, kernel_timing=False,
-        dplan=None, comm=None, side="left", restart=200):
+        dplan=None, comm=None, side="left", restart=200, general=False):
     """Run the whole hot path; returns a Result with counts, solutions
     (device tensors) and phase times in ms (CUDA events).
 
     comm (dist.py): shard the subdomains over its ranks (each rank passes
-    its own comm; results are replicated on every rank)."""
+    its own comm; results are replicated on every rank).
+    general: face / edge eigenproblems by the reference algorithm verbatim
+    (no certified fast paths)."""
     tm = PhaseTimer(timings)
     owned = None
     if comm is not None and comm.size > 1:
@@ -50,7 +52,7 @@ def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8,
     tm.mark("scaling")
     sc = DeviceScaling(ls)
     tm.mark("gevp")
-    ps = DevicePrimalSpace(ls, sc, theta_f, theta_e, variant)
+    ps = DevicePrimalSpace(ls, sc, theta_f, theta_e, variant, general=general)
     tm.mark("pc_setup")
     pc = DevicePreconditioner(ls, sc, ps.r_host, ps.Q, ps.d_q_off)
     op = DeviceInterfaceOperator(ls)

@@ -55,7 +55,7 @@ def inputs(name):
         globs = classify_globs(mesh, part, mesh.boundary_nodes)
         return assemble_system(mesh, const_coefficients()), part, globs
     kw = {"cfg1": (1, {}), "cfg1_lnH": (1, {}), "cfg2": (2, {}), "cfg2_lnH": (2, {}),
-          "cfg3": (3, {}), "cfg4": (4, {}), "cfg4_small": (4, dict(n=16, subs=24)),
+          "cfg3": (3, {}), "cfg4": (4, {}), "cfg5": (5, {}), "cfg4_small": (4, dict(n=16, subs=24)),
           "cfg5_small": (5, dict(n=24, subs=3))}[name]
     p = configs.build_problem(kw[0], **kw[1])
     return p.system, p.partition, p.globs
@@ -63,6 +63,14 @@ def inputs(name):
 
 def golden(name):
     return dict(np.load(os.path.join(GOLDEN, f"{name}.npz")))
+
+
+def probe_vector(g):
+    """The seeded S_hat / M^-1 probe of a fixture (stored in full, or, for the
+    lean cfg5 fixture, regenerated from its seed as make_golden.py drew it)."""
+    if "probe" in g:
+        return g["probe"]
+    return np.random.default_rng(7).standard_normal(int(g["n_hat"]))
 
 
 def variants(g):
@@ -95,5 +103,6 @@ def counts_match(n_primal, ref_n_primal, eig, ref_eig, theta_of):
     return bad
 
 
-FIXTURES = [n for n in ("cfg1", "cfg1_lnH", "cfg2", "cfg2_lnH", "cfg4_small", "cfg5_small", "jump", "cfg3", "cfg4")
+FIXTURES = [n for n in ("cfg1", "cfg1_lnH", "cfg2", "cfg2_lnH", "cfg4_small", "cfg5_small", "jump", "cfg3", "cfg4",
+                        "cfg5")
             if os.path.exists(os.path.join(GOLDEN, f"{n}.npz"))]

@@ -1,0 +1,44 @@
+"""Bitwise reproducibility of the device path: local assembly,
+coarse assembly and every reduction use a fixed summation order (no
+floating-point atomics), so two runs on the same inputs must agree bit for
+bit in S, Bsym^-1, the eigenvalues, the primal counts, the GMRES iteration
+count and the solution."""
+
+import numpy as np
+import pytest
+
+from tests.cases import FIXTURES, inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(name):
+    import torch
+
+    from paper_2501_01676_b200 import pipeline
+
+    system, part, globs = inputs(name)
+    res = pipeline.run(system, part, globs, 10.0, 10.0, "new", keep=True)
+    out = {
+        "S": res.ls.S.cpu().numpy(),
+        "Binv": res.ls.bsym_inverse().cpu().numpy(),
+        "eig": res.space.eig.cpu().numpy(),
+        "n_primal": np.asarray(res.n_primal).copy(),
+        "iterations": res.iterations,
+        "solution": res.solution.cpu().numpy(),
+        "u": res.u.cpu().numpy(),
+        "coarse": res.pc.coarse,
+    }
+    del res
+    torch.cuda.empty_cache()
+    return out
+
+
+@pytest.mark.parametrize("name", [n for n in ("jump", "cfg4_small", "cfg4") if n in FIXTURES])
+def test_two_runs_are_bitwise_identical(name):
+    a = _run(name)
+    b = _run(name)
+    assert a["iterations"] == b["iterations"]
+    assert np.array_equal(a["n_primal"], b["n_primal"])
+    for k in ("S", "Binv", "eig", "solution", "u", "coarse"):
+        assert a[k].tobytes() == b[k].tobytes(), k
