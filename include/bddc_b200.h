@@ -181,6 +181,32 @@ int bddc_deluxe(const int* kind, const int* size, const int* sh_start, const int
                 double* ws, const long long* ws_off, int* status, const int* glob_ids, int n_globs,
                 cudaStream_t stream);
 
+/* Batched linalg.py kernels on arbitrary symmetric n[b] x n[b] inputs at off[b]
+ * (one CTA per member; workspace ws + ws_off[b] of bddc_ws_linalg(n[b]) doubles):
+ *   mode 0: out = pseudo_inverse(A) with cut rel_tol (linalg.py:23-50);
+ *   mode 1: out = parallel_sum(A, B) (linalg.py:53-67);
+ *   mode 2: sym_pencil_gevp(A, B) (linalg.py:116-214): vals / degen at voff[b]
+ *           (n[b] each; +inf first, finite descending, degenerate last), out =
+ *           eigenvectors (columns aligned with vals), status[b] = 3 when B is not
+ *           positive semidefinite (the reference's ValueError).
+ * replaces scipy.linalg.eigh-based pseudo_inverse / parallel_sum / sym_pencil_gevp. */
+long long bddc_ws_linalg(long long n);
+int bddc_linalg_batched(int mode, const double* A, const double* B, const long long* off,
+                        const int* n, int nbatch, double rel_tol, double* out, double* vals,
+                        const long long* voff, int* degen, int* status, double* ws,
+                        const long long* ws_off, int max_n, cudaStream_t stream);
+
+/* Batched change of basis: Q (n[b] x n[b], orthogonal) whose first rank[b]
+ * rows span the rows (m[b] x n[b], row-major) at roff[b]; rank at the
+ * s >= 1e-10 s_max cut (one-sided Jacobi SVD + Householder completion).
+ * Workspace bddc_ws_row_space(m, n) doubles per member.
+ * replaces build_change_of_basis adaptive.py:190-206 and the SVD of
+ * reduce_edge_constraints adaptive.py:172-187. */
+long long bddc_ws_row_space(long long m, long long n);
+int bddc_row_space_batched(const double* rows, const long long* roff, const int* m, const int* n,
+                           int nbatch, double* Q, const long long* qoff, int* rank, double* ws,
+                           const long long* ws_off, int max_dim, cudaStream_t stream);
+
 /* Face GEP + selection + change of basis.  mode = 1: certified fast path in a
  * compact arena (faces whose certificate fails get status 900 and must be
  * re-run with mode 0); mode = 0: general kernel, certified shortcuts allowed;

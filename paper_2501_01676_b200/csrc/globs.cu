@@ -68,7 +68,7 @@ struct GlobTables {
 // ---------------------------------------------------------------------------
 // P <- sym(M)^+ with eigenvalue cut rel_tol*max|w|.  ws: 2 n^2 + n doubles.
 BDDC_DEV void pinv_sym(const double* M, int n, double* P, double* ws, double* cs, int* perm,
-                       double* red) {
+                       double* red, double rel_tol = 1e-12) {
   double* A = ws;
   double* U = ws + n * n;
   double* w = ws + 2 * n * n;
@@ -77,7 +77,7 @@ BDDC_DEV void pinv_sym(const double* M, int n, double* P, double* ws, double* cs
   blk::jacobi_eigh(A, n, n, w, U, n, cs, perm, red);
   double mx = 0.0;
   for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(w[i]));
-  const double cut = 1e-12 * mx;
+  const double cut = rel_tol * mx;
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     int r = idx / n, c = idx - r * n;
     double s = 0.0;
@@ -89,15 +89,15 @@ BDDC_DEV void pinv_sym(const double* M, int n, double* P, double* ws, double* cs
   blk::symmetrize(P, n, n);
 }
 
-// R <- sym(A (A+B)^+ B).  ws: 4 n^2 + n doubles.
+// R <- sym(A (A+B)^+ B).  ws: 5 n^2 + n doubles.
 BDDC_DEV void parallel_sum(const double* A, const double* B, int n, double* R, double* ws,
-                           double* cs, int* perm, double* red) {
+                           double* cs, int* perm, double* red, double rel_tol = 1e-12) {
   double* Sm = ws;
   double* P = ws + n * n;
   double* T = ws + 2 * n * n;
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) Sm[idx] = A[idx] + B[idx];
   __syncthreads();
-  pinv_sym(Sm, n, P, ws + 3 * n * n, cs, perm, red);
+  pinv_sym(Sm, n, P, ws + 3 * n * n, cs, perm, red, rel_tol);
   blk::gemm(T, n, A, n, false, P, n, false, n, n, n, 1.0, 0.0);
   blk::gemm(R, n, T, n, false, B, n, false, n, n, n, 1.0, 0.0);
   blk::symmetrize(R, n, n);
@@ -215,7 +215,8 @@ BDDC_DEV int pencil_fast(const double* B, const double* Bt, int n, double theta,
 // ws: pencil_ws_doubles(n).  Returns a Status.
 // ---------------------------------------------------------------------------
 BDDC_DEV int pencil(const double* B, const double* Bt, int n, double* vals, double* vecs,
-                    int* degen, double* ws, double* cs, int* perm, double* red) {
+                    int* degen, double* ws, double* cs, int* perm, double* red,
+                    double rel_tol = 1e-12) {
   const int nn = n * n;
   // layout: 8 n x n slots [A1 U A2 T1 T2 T3 T4 T5] then mu, bw, lam (n each);
   // Bt may alias A1 (it is only read by the first copy)
@@ -248,7 +249,7 @@ BDDC_DEV int pencil(const double* B, const double* Bt, int n, double* vals, doub
     int n0 = n;
     if (mx > 0.0) {
       n0 = 0;
-      while (n0 < n && !(mu[n0] > 1e-12 * mx)) ++n0;  // mu ascending: range is a suffix
+      while (n0 < n && !(mu[n0] > rel_tol * mx)) ++n0;  // mu ascending: range is a suffix
     }
     s_n0 = n0;
     s_bscale = bs;
@@ -271,22 +272,22 @@ BDDC_DEV int pencil(const double* B, const double* Bt, int n, double* vals, doub
     __shared__ int s_ninf;
     if (threadIdx.x == 0) {
       int c = 0;
-      for (int j = 0; j < n0; ++j) c += fabs(bw[j]) > 1e-12 * tiny;
+      for (int j = 0; j < n0; ++j) c += fabs(bw[j]) > rel_tol * tiny;
       s_ninf = c;
     }
     __syncthreads();
     n_inf = s_ninf;
     for (int j = threadIdx.x; j < n0; j += blockDim.x) {
-      const bool act = fabs(bw[j]) > 1e-12 * tiny;
+      const bool act = fabs(bw[j]) > rel_tol * tiny;
       int rank = 0;
       if (act) {
         for (int i = 0; i < n0; ++i) {
-          if (!(fabs(bw[i]) > 1e-12 * tiny)) continue;
+          if (!(fabs(bw[i]) > rel_tol * tiny)) continue;
           rank += (fabs(bw[i]) > fabs(bw[j])) || (fabs(bw[i]) == fabs(bw[j]) && i < j);
         }
       } else {
         // degenerate: appended after all finite modes, in index order
-        for (int i = 0; i < j; ++i) rank += !(fabs(bw[i]) > 1e-12 * tiny);
+        for (int i = 0; i < j; ++i) rank += !(fabs(bw[i]) > rel_tol * tiny);
         rank += n_inf + n1;
       }
       perm[j] = rank;
@@ -301,7 +302,7 @@ BDDC_DEV int pencil(const double* B, const double* Bt, int n, double* vals, doub
     }
     __syncthreads();
     for (int j = threadIdx.x; j < n0; j += blockDim.x) {
-      const bool act = fabs(bw[j]) > 1e-12 * tiny;
+      const bool act = fabs(bw[j]) > rel_tol * tiny;
       double scale;
       if (act) {
         scale = 1.0 / sqrt(fabs(bw[j]));
@@ -322,7 +323,7 @@ BDDC_DEV int pencil(const double* B, const double* Bt, int n, double* vals, doub
       int r = idx / n0, c = idx - r * n0;
       double s = 0.0;
       for (int k = 0; k < n0; ++k)
-        if (fabs(bw[k]) > 1e-12 * tiny) s += T3[r * n0 + k] * (1.0 / bw[k]) * T3[c * n0 + k];
+        if (fabs(bw[k]) > rel_tol * tiny) s += T3[r * n0 + k] * (1.0 / bw[k]) * T3[c * n0 + k];
       B00p[r * n0 + c] = s;
     }
     __syncthreads();
@@ -1340,6 +1341,64 @@ __global__ void __launch_bounds__(256) edge_old_kernel(GlobTables t, const doubl
   }
 }
 
+// ---------------------------------------------------------------------------
+// Batched linalg.py kernels (one CTA per matrix / pair), the device versions of
+// pseudo_inverse (linalg.py:23-50), parallel_sum (:53-67) and sym_pencil_gevp
+// (:116-214) for arbitrary symmetric inputs; the glob kernels above call the
+// same device functions.  mode 0: P = pinv(sym(A)); 1: R = A : B;
+// 2: pencil (A, B) -> vals, vecs, degen.  Status per member: kNotPSD when the
+// pencil's right-hand side is indefinite.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline long long linalg_ws(long long n) { return 8 * n * n + 3 * n + 16; }
+
+__global__ void __launch_bounds__(256) linalg_batched_kernel(
+    int mode, const double* __restrict__ A, const double* __restrict__ B,
+    const long long* __restrict__ off, const int* __restrict__ nn, double rel_tol,
+    double* __restrict__ out, double* __restrict__ vals, const long long* __restrict__ voff,
+    int* __restrict__ degen, int* __restrict__ status, double* __restrict__ ws,
+    const long long* __restrict__ ws_off, int max_n) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.x;
+  const int n = nn[b];
+  if (n <= 0) return;
+  double* cs = sh;                                               // 2(max_n+2)
+  double* red = cs + 2 * (max_n + 2);                            // 32
+  int* perm = reinterpret_cast<int*>(red + 32);                  // 2(max_n+2)
+  int* dg = perm + 2 * (max_n + 2);                              // max_n + 2
+  double* W = ws + ws_off[b];
+  const double* Ab = A + off[b];
+  double* Ob = out + off[b];
+  if (mode == 0) {
+    pinv_sym(Ab, n, Ob, W, cs, perm, red, rel_tol);
+  } else if (mode == 1) {
+    parallel_sum(Ab, B + off[b], n, Ob, W, cs, perm, red, rel_tol);
+  } else {
+    double* v = vals + voff[b];
+    const int st = pencil(Ab, B + off[b], n, v, Ob, dg, W, cs, perm, red, rel_tol);
+    if (threadIdx.x == 0 && st) status[b] = st;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) degen[voff[b] + j] = dg[j];
+  }
+}
+
+// Batched change of basis (adaptive.py:172-206): Q (n x n orthogonal) whose
+// first r rows span the row space of rows (m x n, row-major, ld n), r at the
+// 1e-10 s_max cut.  One CTA per member.
+__global__ void __launch_bounds__(256) row_space_batched_kernel(
+    const double* __restrict__ rows, const long long* __restrict__ roff,
+    const int* __restrict__ mm, const int* __restrict__ nn, double* __restrict__ Q,
+    const long long* __restrict__ qoff, int* __restrict__ rank, double* __restrict__ ws,
+    const long long* __restrict__ ws_off, int max_dim) {
+  extern __shared__ double sh[];
+  const int b = blockIdx.x;
+  const int m = mm[b], n = nn[b];
+  if (n <= 0) return;
+  double* cs = sh;                                   // 2(max_dim+2)
+  double* red = cs + 2 * (max_dim + 2);              // 32
+  int* perm = reinterpret_cast<int*>(red + 32);      // 2(max_dim+2)
+  const int r = row_space_basis(rows + roff[b], n, m, n, Q + qoff[b], ws + ws_off[b], cs, perm, red);
+  if (threadIdx.x == 0) rank[b] = r;
+}
+
 }  // namespace bddc
 
 // ===========================================================================
@@ -1378,6 +1437,39 @@ static int shmem_for(int dim) {
 extern "C" {
 
 long long bddc_ws_face(long long n) { return face_arena(n); }
+long long bddc_ws_linalg(long long n) { return linalg_ws(n); }
+long long bddc_ws_row_space(long long m, long long n) {
+  const long long mx = m > n ? m : n;
+  return 2 * n * n + n + mx + (m <= n ? n * m : m * n + n * n) + 4 * n + 64;
+}
+
+int bddc_row_space_batched(const double* rows, const long long* roff, const int* m, const int* n,
+                           int nbatch, double* Q, const long long* qoff, int* rank, double* ws,
+                           const long long* ws_off, int max_dim, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = (2 * (max_dim + 2) + 32) * 8 + 2 * (max_dim + 2) * 4 + 16;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(row_space_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  row_space_batched_kernel<<<nbatch, 256, smem, stream>>>(rows, roff, m, n, Q, qoff, rank, ws,
+                                                          ws_off, max_dim);
+  bddc_note_launches(1);
+  return glob_launch_status();
+}
+
+int bddc_linalg_batched(int mode, const double* A, const double* B, const long long* off,
+                        const int* n, int nbatch, double rel_tol, double* out, double* vals,
+                        const long long* voff, int* degen, int* status, double* ws,
+                        const long long* ws_off, int max_n, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  if (mode < 0 || mode > 2) return -(int)cudaErrorInvalidValue;
+  const int smem = (2 * (max_n + 2) + 32) * 8 + (3 * (max_n + 2)) * 4 + 16;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(linalg_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  linalg_batched_kernel<<<nbatch, 256, smem, stream>>>(mode, A, B, off, n, rel_tol, out, vals, voff,
+                                                       degen, status, ws, ws_off, max_n);
+  bddc_note_launches(1);
+  return glob_launch_status();
+}
 long long bddc_ws_face_fast(long long n) { return face_fast_arena(n); }
 long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long nhmax) {
   return bddc_edge_new_ws(ns, ne, wd, nhmax);
