@@ -450,9 +450,15 @@ class DeviceScaling:
         """Raise the reference's error for a singular deluxe block sum."""
         bad = _first_bad(self._status)
         if bad is not None:
-            ls = self.ls
-            raise NumericalError("deluxe block sum is singular "
-                                 f"(glob {ls.globs.glob_id(ls.globs.globs[bad])})")
+            ls, p = self.ls, self.ls.plan
+            n = int(p.gsize[bad])
+            total = np.zeros((n, n))
+            BsC = ls.slot_bsym()
+            for slot in range(int(p.sh_start[bad]), int(p.sh_start[bad + 1])):
+                o = int(p.sh_doff[slot])
+                total += BsC[o:o + n * n].view(n, n).cpu().numpy()
+            raise NumericalError(f"deluxe block sum is singular (cond ~ {np.linalg.cond(total):.2e}; "
+                                 f"glob {ls.globs.glob_id(ls.globs.globs[bad])})")
 
     def family(self, k):
         """{sharer: D (n_g x n_g)} of glob index k, glob-node order."""
@@ -692,9 +698,14 @@ class DevicePrimalSpace:
         gid = globs.glob_id(globs.globs[k])
         p = self.ls.plan
         if 100 <= code < 200:
-            sub = int(p.sh_sub[p.sh_start[k] + code - 100])
-            inner = f"glob Schur block on subdomain {sub} is singular"
-            raise NumericalError(inner)
+            slot = int(p.sh_start[k] + code - 100)
+            sub = int(p.sh_sub[slot])
+            n = int(p.gsize[k])
+            o = int(p.sh_doff[slot])
+            blk = self.ls.slot_binv()[o:o + n * n].view(n, n).cpu().numpy()
+            # (new edges: the edge-with-priors block, substructuring.py:188; same message)
+            raise NumericalError(f"glob Schur block on subdomain {sub} is singular "
+                                 f"(cond ~ {np.linalg.cond(blk):.2e})")
         if code == 200 + 3:
             raise NumericalError(f"eigenproblem on glob {gid} failed: Btil is not positive semidefinite")
         raise NumericalError(f"eigenproblem on glob {gid} failed (status {code})")
