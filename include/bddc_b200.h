@@ -400,6 +400,19 @@ int bddc_coarse_scatter(const int* pstart, const int* pgid, const double* Cl,
                         const long long* coff, const long long* cstart, const long long* csrc,
                         double* C, long long ldc, int n_c, int nbatch, cudaStream_t stream);
 
+/* Dense transformed deluxe weights per subdomain in nodal B order:
+ * Dbar_b[pos, pos] = Q_g TT_(g,b) (= Q_g D_g^(b) Q_g^T) for each slot; nodal maps a
+ * glob-major local position (voff layout) to its nodal one; W: slot-layout scratch;
+ * Dbar zeroed by the caller.  replaces the Dbar loop of solver.py:86-90. */
+int bddc_pc_dbar(const int* slot_glob, const int* slot_sub, const int* gsize, const int* sh_boff,
+                 const long long* sh_doff, const double* Q, const long long* q_off,
+                 const double* TT, const int* nB, const long long* soff, const long long* voff,
+                 const int* nodal, double* W, double* Dbar, int n_slots, cudaStream_t stream);
+
+/* out_b = X_b^T (square n[b] x n[b] at soff[b]). */
+int bddc_transpose_batched(const double* X, const long long* soff, const int* n, int nbatch,
+                           double* out, cudaStream_t stream);
+
 /* y_i = M_i u[perm_i] (+ c_i = G_i u[perm_i]).  replaces interface_operator solver.py:229-233
  * (M = S) and the local half of BddcPreconditioner.apply solver.py:201-209 (M = A). */
 int bddc_local_gemv(const int* nB, const long long* soff, const long long* voff,

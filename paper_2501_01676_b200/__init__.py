@@ -24,7 +24,12 @@ def __getattr__(name):
         "SubdomainOperator": "substructuring",
         "SolveReport": "solver", "BddcPreconditioner": "solver", "build_preconditioner": "solver",
         "gmres_solve": "solver", "interface_operator": "solver", "interface_rhs": "solver",
-        "recover_interior": "solver",
+        "recover_interior": "solver", "averaging_and_jump": "solver",
+        "assemble_dense_schur": "solver", "direct_schur_solve": "solver",
+        "EigenPairList": "linalg", "pseudo_inverse": "linalg", "parallel_sum": "linalg",
+        "parallel_sum_chain": "linalg", "sym_pencil_gevp": "linalg",
+        "build_change_of_basis": "adaptive", "reduce_edge_constraints": "adaptive",
+        "assemble_primal_space": "adaptive",
     }
     if name in table:
         return getattr(importlib.import_module(f".{table[name]}", __name__), name)

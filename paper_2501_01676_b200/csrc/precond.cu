@@ -542,6 +542,48 @@ __global__ void ttblock_kernel(const int* __restrict__ slot_glob, const int* __r
   blk::gemm(TT + sh_doff[s], n, D + sh_doff[s], n, false, Q + q_off[g], n, true, n, n, n, 1.0, 0.0);
 }
 
+// Dense transformed deluxe weights per subdomain in the reference's nodal B
+// order (solver.py:86-90): Dbar_b[pos, pos] = Q_g D_g^(b) Q_g^T for every glob
+// slot (g, b), pos = nodal local positions of g's nodes in b (nodal[] maps a
+// glob-major local position to the nodal one).  W: slot-layout scratch.
+// Dbar must be zeroed by the caller (entries outside glob blocks stay 0).
+__global__ void dbar_kernel(const int* __restrict__ slot_glob, const int* __restrict__ slot_sub,
+                            const int* __restrict__ gsize, const int* __restrict__ sh_boff,
+                            const long long* __restrict__ sh_doff, const double* __restrict__ Q,
+                            const long long* __restrict__ q_off, const double* __restrict__ TT,
+                            const int* __restrict__ nB, const long long* __restrict__ soff,
+                            const long long* __restrict__ voff, const int* __restrict__ nodal,
+                            double* __restrict__ W, double* __restrict__ Dbar) {
+  const int s = blockIdx.x;
+  const int g = slot_glob[s], b = slot_sub[s];
+  const int n = gsize[g];
+  double* Ws = W + sh_doff[s];
+  blk::gemm(Ws, n, Q + q_off[g], n, false, TT + sh_doff[s], n, false, n, n, n, 1.0, 0.0);
+  __syncthreads();
+  const int nb = nB[b];
+  const int* pos = nodal + voff[b] + sh_boff[s];
+  double* Db = Dbar + soff[b];
+  for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    Db[(long long)pos[r] * nb + pos[c]] = Ws[idx];
+  }
+}
+
+// out_b = X_b^T for square batched matrices (ld = n)
+__global__ void transpose_batched_kernel(const double* __restrict__ X,
+                                         const long long* __restrict__ soff,
+                                         const int* __restrict__ nn, double* __restrict__ out) {
+  const int b = blockIdx.y;
+  const int n = nn[b];
+  const double* A = X + soff[b];
+  double* T = out + soff[b];
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
+    T[(long long)c * n + r] = A[idx];
+  }
+}
+
 // out = TT_blockdiag * in  (left) or in * TT_blockdiag^T (right), TT from ttblock_kernel
 __global__ void tt_transform_kernel(SubGlobMap m, const double* __restrict__ TT,
                                     const double* __restrict__ in, double* __restrict__ out,
@@ -1223,6 +1265,25 @@ int bddc_pc_ttblocks(const int* slot_glob, const int* gsize, const double* Q,
                      double* TT, int n_slots, cudaStream_t stream) {
   if (n_slots <= 0) return 0;
   ttblock_kernel<<<n_slots, 128, 0, stream>>>(slot_glob, gsize, Q, q_off, D, sh_doff, TT, n_slots); bddc_note_launches(1);
+  return pc_status();
+}
+
+int bddc_pc_dbar(const int* slot_glob, const int* slot_sub, const int* gsize, const int* sh_boff,
+                 const long long* sh_doff, const double* Q, const long long* q_off,
+                 const double* TT, const int* nB, const long long* soff, const long long* voff,
+                 const int* nodal, double* W, double* Dbar, int n_slots, cudaStream_t stream) {
+  if (n_slots <= 0) return 0;
+  dbar_kernel<<<n_slots, 128, 0, stream>>>(slot_glob, slot_sub, gsize, sh_boff, sh_doff, Q, q_off,
+                                           TT, nB, soff, voff, nodal, W, Dbar);
+  bddc_note_launches(1);
+  return pc_status();
+}
+
+int bddc_transpose_batched(const double* X, const long long* soff, const int* n, int nbatch,
+                           double* out, cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  transpose_batched_kernel<<<dim3(32, nbatch), 256, 0, stream>>>(X, soff, n, out);
+  bddc_note_launches(1);
   return pc_status();
 }
 

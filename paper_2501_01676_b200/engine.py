@@ -813,6 +813,7 @@ class DevicePreconditioner:
         p, d, st = ls.plan, ls.d, stream()
         self.ls, self.plan, self.comm = ls, p, ls.comm
         r = np.asarray(r_host, dtype=np.int64)
+        self.r_host = r
         self.n_hat = p.n_hat
         self.n_primal = int(r.sum())
         if self.n_primal == 0:
@@ -861,6 +862,7 @@ class DevicePreconditioner:
         TT = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
         lib.bddc_pc_ttblocks(d.slot_glob, d.gsize, Q, q_off, scaling.D, d.sh_doff, TT,
                              int(p.sh_sub.size), st)
+        self.Q_used, self.q_off_used = Q, q_off  # the change of basis this preconditioner applies
         npn = max(int(poff[-1]), 1)
         # per local B position: its primal index (or -1), for the compact Sbar rows / columns
         pidx = np.full(int(p.voff[-1]), -1, dtype=np.int32)

@@ -7,8 +7,10 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .engine import (DeviceInterfaceOperator, DevicePreconditioner, NumericalError, dev_f64,
-                     dev_i64, gmres_device, gmres_right_device, recover_device)
+from ._lib import lib, stream
+from .coupled import CoupledMixin, averaging_and_jump
+from .engine import (PANEL, DeviceInterfaceOperator, DevicePreconditioner, NumericalError, dev_f64,
+                     dev_i32, dev_i64, gmres_device, gmres_right_device, recover_device)
 
 F64 = torch.float64
 
@@ -30,8 +32,12 @@ class SolveReport:
     extra: dict = field(default_factory=dict)
 
 
-class BddcPreconditioner(DevicePreconditioner):
-    """Reference class name (solver.py:46); ``apply`` takes numpy or device vectors."""
+class BddcPreconditioner(CoupledMixin, DevicePreconditioner):
+    """Reference class name (solver.py:46); ``apply`` takes numpy or device vectors.
+
+    The reference's internals (dual_loc, primal_loc, gprimal, gdual_pos,
+    primal_pos, Dbar, wt_size, transform, inject, inject_t, scale) are
+    available through coupled.PartiallyCoupledSpace, built on first access."""
 
     def __init__(self, ops, primal, scaling):
         ls = ops[0].ls
@@ -99,6 +105,56 @@ def gmres_solve(operator, rhs, pc, rel_tol=1e-8, max_iter=300, side="left", rest
     return SolveReport(it, conv, x.cpu().numpy(), th, ph, solve_time=time.perf_counter() - t0)
 
 
+def assemble_dense_schur(ops, n):
+    """Dense S_hat = sum_i R_i^T S_i R_i (solver.py:245-249), assembled on the
+    device in a fixed summation order (one warp per row)."""
+    return _dense_schur_device(ops[0].ls, n).view(n, n).cpu().numpy()
+
+
+def _dense_schur_device(ls, n, ld=None):
+    p, d = ls.plan, ls.d
+    if n != p.n_hat:
+        raise ValueError(f"interface size {n} does not match the operators ({p.n_hat})")
+    ld = n if ld is None else ld
+    S = torch.empty(n * ld, dtype=F64, device="cuda")
+    lib.bddc_coarse_scatter(dev_i32(p.voff), d.iface_perm, ls.S, d.soff, d.tstart, d.tsrc, S, ld,
+                            n, p.N, stream())
+    return S
+
+
+def direct_schur_solve(ops, globs, rhs):
+    """Dense assembled interface solve (solver.py:252-259), the oracle of the
+    iterative path: [S_hat | rhs] eliminated on the device by the blocked
+    no-pivot LU of the subdomain kernels (S_hat has a positive-definite
+    symmetric part), then back-substituted."""
+    ls = ops[0].ls
+    n = globs.interface_nodes.shape[0]
+    if (n + 2) * 8 > 220 * 1024:
+        raise ValueError(f"direct_schur_solve: dense interface system of size {n} is beyond the "
+                         "back-substitution kernel (n <= 28,000)")
+    ld = (n + 2) // 2 * 2
+    M = _dense_schur_device(ls, n, ld).view(n, ld)
+    # the kernel wrote columns [0, n); column n carries the right-hand side
+    M[:, n] = torch.as_tensor(np.asarray(rhs, dtype=np.float64)).cuda()
+    if ld > n + 1:
+        M[:, n + 1:] = 0.0
+    M = M.reshape(-1)
+    one = lambda v: dev_i32(np.array([v]))
+    off, ldv, nv = dev_i64(np.array([0])), one(ld), one(n)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pinv = torch.empty(4096, dtype=F64, device="cuda")
+    st = stream()
+    lib.bddc_schur_eliminate(M, off, ldv, nv, nv, one(n + 1), 1, n, n, n + 1, PANEL, pinv, 4096, 0,
+                             status, 0, None, 0, st)
+    if int(status.item()):
+        raise NumericalError("assembled interface operator is singular")
+    x = torch.empty(n, dtype=F64, device="cuda")
+    lib.bddc_recover_interior(M, off, ldv, nv, one(0), dev_i64(np.array([0, 0])), one(0),
+                              dev_i64(np.array([0, n])), torch.arange(n, device="cuda"), x, x, 1,
+                              n, PANEL, st)
+    return x.cpu().numpy()
+
+
 def recover_interior(ops, globs, system, u_hat):
     """solver.py:318-326"""
     ls = ops[0].ls
@@ -107,5 +163,6 @@ def recover_interior(ops, globs, system, u_hat):
 
 
 __all__ = ["BddcPreconditioner", "InterfaceOperator", "NumericalError", "SolveReport",
-           "build_preconditioner", "gmres_solve", "interface_operator", "interface_rhs",
+           "assemble_dense_schur", "averaging_and_jump", "build_preconditioner",
+           "direct_schur_solve", "gmres_solve", "interface_operator", "interface_rhs",
            "recover_interior"]

@@ -100,5 +100,28 @@ def glob_principal_block(op, glob):
     return op.Bsym[np.ix_(idx, idx)]
 
 
+def glob_schur_block(op, glob):
+    """((Bsym^-1)[X,X])^-1, symmetrised (reference substructuring.py:152-171),
+    by the device Gauss-Jordan with the Cholesky criterion (positive pivots)."""
+    import torch
+
+    from ._lib import lib, stream
+    from .engine import dev_i32, dev_i64
+
+    idx = op.glob_index(glob)
+    n = idx.size
+    block = op.bsym_inverse()[np.ix_(idx, idx)]
+    M = torch.from_numpy(np.ascontiguousarray(block)).cuda().reshape(-1)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    pinv = torch.empty(4096, dtype=torch.float64, device="cuda")
+    one = dev_i32(np.array([n]))
+    lib.bddc_gj_inverse(M, dev_i64(np.array([0])), one, one, 1, n, pinv, 4096, status, 1, 0, stream())
+    if int(status.item()):
+        raise NumericalError(f"glob Schur block on subdomain {op.sub_id} is singular "
+                             f"(cond ~ {np.linalg.cond(block):.2e})")
+    out = M.view(n, n)
+    return (0.5 * (out + out.T)).cpu().numpy()
+
+
 __all__ = ["NumericalError", "SubdomainOperator", "build_subdomain_operator",
-           "build_subdomain_operators", "glob_principal_block", "local_system"]
+           "build_subdomain_operators", "glob_principal_block", "glob_schur_block", "local_system"]
