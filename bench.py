@@ -13,10 +13,20 @@ from host (numpy) arrays through the package API and includes the
 host->device copies and the device->host copy of the nodal solution.  Workload (BASELINE.json configs[4]): 128^3 cells (6 Kuhn tets /
 cell, 2,048,383 DOFs), 16^3 subdomains (H/h = 8), nu = 1e-2, b = (1,1,1),
 f = 1, c = 1, Theta = 10.  Working set (~50 GB) >> L2, so no flush is needed.
+The last timed step's counts, iterations and solution are checked against
+the unmodified reference's cfg5 fixture (tests/golden/cfg5.npz): "parity".
 
-``--impl reference``: the CPU oracle (restated reference algorithm, same
-LAPACK/SuperLU calls) on a bounded sample of the same workload (same H/h,
-coefficients and thresholds, 4^3 subdomains), on this host's cores.
+``--gpus N`` without a torchrun environment re-executes itself under
+``torch.distributed.run`` with N ranks (one per GPU; fails if fewer GPUs are
+visible); the subdomains of the one problem are sharded over the ranks.
+
+``--impl reference``: the UNMODIFIED reference package (installed at
+baseline/_ref, driven through its own API in the harness order,
+harness.py:250-292) on a bounded sample of the same workload (same H/h,
+coefficients and thresholds; 48^3 cells, 6^3 subdomains by default) on this
+host's cores; under torchrun only rank 0 runs it.  If baseline/_ref is
+missing, the oracle port (oracle/bddc_oracle.py) stands in and the line says
+so ("kind": "port").
 """
 
 import argparse
@@ -48,8 +58,11 @@ def parse():
     ap.add_argument("--subs", type=int, default=None)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sample-n", type=int, default=32)
-    ap.add_argument("--sample-subs", type=int, default=4)
+    # reference arm sample (timed steps) and my arm's cpu_baseline sample
+    ap.add_argument("--sample-n", type=int, default=48)
+    ap.add_argument("--sample-subs", type=int, default=6)
+    ap.add_argument("--cpu-sample-n", type=int, default=32)
+    ap.add_argument("--cpu-sample-subs", type=int, default=4)
     return ap.parse_args()
 
 
@@ -76,31 +89,98 @@ def workload_desc(cfg, n, subs, prob, world=1):
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle timing (reference arm and cpu_baseline)
+# CPU reference timing (reference arm and cpu_baseline)
 # ---------------------------------------------------------------------------
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
 
 def cpu_sample_problem(cfg, sample_n, sample_subs):
     from paper_2501_01676_b200 import configs
     return configs.build_problem(cfg, n=sample_n, subs=sample_subs)
 
 
-def time_oracle(prob, threads):
-    from threadpoolctl import threadpool_limits
+def reference_available():
+    return os.path.isdir(os.path.join(REF_DIR, "adbddc"))
 
-    from oracle import bddc_oracle as O
+
+class ReferenceCase:
+    """The unmodified reference package (baseline/_ref) on one problem: inputs
+    built once with the reference's own mesh / partition / glob / assembly
+    functions from the config's coefficient callables (not timed), then the
+    hot path through its public API in the harness order (harness.py:250-292)
+    plus recover_interior."""
+
+    def __init__(self, prob):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        import adbddc.decomposition as rd
+        import adbddc.discretization as rdi
+        import adbddc.mesh as rm
+        mesh = rm.box_mesh(prob.mesh.box, prob.mesh.cells)
+        self.part = rd.Partition(prob.partition.subdomain_of.copy(), prob.partition.n_subdomains)
+        self.globs = rd.classify_globs(mesh, self.part, mesh.boundary_nodes)
+        c = prob.coeffs
+        self.system = rdi.assemble_system(mesh, rdi.Coefficients(
+            viscosity=c.viscosity, velocity=c.velocity, reaction=c.reaction, source=c.source,
+            dirichlet=c.dirichlet))
+        self.n_dofs = prob.n_dofs
+
+    def run(self):
+        from adbddc.adaptive import adaptive_primal_space
+        from adbddc.scaling import build_scaling
+        from adbddc.solver import (build_preconditioner, gmres_solve, interface_operator,
+                                   interface_rhs, recover_interior)
+        from adbddc.substructuring import build_subdomain_operator
+        part, globs, system = self.part, self.globs, self.system
+        ops = [build_subdomain_operator(system, part, globs, i) for i in range(part.n_subdomains)]
+        scaling = build_scaling(globs, ops)
+        for op in ops:
+            op.bsym_inverse()
+        n = globs.interface_nodes.shape[0]
+        operator = interface_operator(ops, n)
+        rhs = interface_rhs(ops, n)
+        basis, _ = adaptive_primal_space(globs, ops, scaling, THETA, THETA, "new")
+        pc = build_preconditioner(ops, basis, scaling)
+        rep = gmres_solve(operator, rhs, pc)
+        recover_interior(ops, globs, system, rep.solution)
+        return {"iterations": rep.iterations, "pnumF": basis.pnumF, "pnumE": basis.pnumE}
+
+
+class OracleCase:
+    """Fallback when baseline/_ref is absent: the oracle port (test infrastructure)."""
+
+    def __init__(self, prob):
+        self.prob, self.n_dofs = prob, prob.n_dofs
+
+    def run(self):
+        from oracle import bddc_oracle as O
+        p = self.prob
+        return O.run_pipeline(p.system, p.partition, p.globs, THETA, THETA, "new")
+
+
+def cpu_case(prob):
+    if reference_available():
+        return ReferenceCase(prob), "reference"
+    return OracleCase(prob), "port"
+
+
+def time_case(case, threads):
+    from threadpoolctl import threadpool_limits
     with threadpool_limits(limits=threads):
         t0 = time.perf_counter()
-        res = O.run_pipeline(prob.system, prob.partition, prob.globs, THETA, THETA, "new")
+        res = case.run()
         dt = time.perf_counter() - t0
     return dt, res
 
 
-def best_threads(prob):
+def best_threads(case):
+    """(threads, seconds): the faster of 1 BLAS thread and all host cores."""
     ncpu = os.cpu_count() or 1
-    t1, _ = time_oracle(prob, 1)
+    t1, _ = time_case(case, 1)
     if ncpu == 1:
         return 1, t1
-    tn, _ = time_oracle(prob, ncpu)
+    tn, _ = time_case(case, ncpu)
     return (1, t1) if t1 <= tn else (ncpu, tn)
 
 
@@ -109,26 +189,31 @@ def run_reference(args):
     if rank != 0:  # under torchrun only rank 0 runs the CPU reference arm
         return
     prob = cpu_sample_problem(args.config, args.sample_n, args.sample_subs)
-    threads, _ = best_threads(prob)
-    for _ in range(max(args.warmup - 1, 0)):
-        time_oracle(prob, threads)
+    case, kind = cpu_case(prob)
+    # warm-up on the sample also picks the BLAS thread count (1 vs all cores)
+    threads, _ = best_threads(case)
+    for _ in range(max(args.warmup - 2, 0)):
+        time_case(case, threads)
     times = []
     for _ in range(args.steps):
-        dt, res = time_oracle(prob, threads)
+        dt, res = time_case(case, threads)
         times.append(dt)
     tstep = sum(times) / len(times)
     value = prob.n_dofs / tstep
-    sample = (f"oracle (restated reference hot path, numpy/scipy LAPACK+SuperLU) on a "
-              f"{args.sample_n}^3-cell, {args.sample_subs}^3-subdomain problem with configs[{args.config - 1}]'s "
-              f"H/h, coefficients and thresholds ({prob.n_dofs} DOFs, {res['iterations']} iterations)")
+    what = ("unmodified reference package (baseline/_ref, adbddc API in harness order)" if kind == "reference"
+            else "oracle port of the reference hot path (baseline/_ref missing)")
+    sample = (f"{what} on {args.sample_n}^3 cells, {args.sample_subs}^3 subdomains with "
+              f"configs[{args.config - 1}]'s H/h, coefficients and thresholds ({prob.n_dofs} DOFs, "
+              f"{res['iterations']} iterations); hot path only (inputs built once, untimed)")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": tstep * 1e3,
+        "ms_each_step": [round(t * 1e3, 1) for t in times],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": dict(workload_desc(args.config, args.sample_n, args.sample_subs, prob),
                        parallelism=f"host CPU, {threads} BLAS thread(s) (no GPU)"),
-        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -224,6 +309,50 @@ def hbm_peak():
         return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
     except (OSError, ValueError, KeyError):
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def parity_check(cfg, args, res):
+    """Counts, iterations and solution of the last timed step against the
+    unmodified reference's fixture of this workload (north_star bars: per-glob
+    primal counts exact except eigenvalues within 1e-8 of theta, iterations
+    +-1, solution relative difference <= 1e-8)."""
+    path = os.path.join(ROOT, "tests", "golden", f"cfg{cfg}.npz")
+    if args.n is not None or args.subs is not None or not os.path.exists(path):
+        return {"status": "no fixture for this workload"}
+    g = np.load(path)
+    v = "new"
+    ref_np = g[f"{v}_n_primal"]
+    mine = np.asarray(res.n_primal)[:ref_np.size]
+    ids, lens, vals = g[f"{v}_gevp_ids"], g[f"{v}_gevp_len"], g[f"{v}_gevp_vals"]
+    starts = np.concatenate([[0], np.cumsum(lens)])
+    ev_of = {int(k): vals[starts[j]:starts[j + 1]] for j, k in enumerate(ids)}
+    bad = []
+    for k in np.flatnonzero(mine != ref_np):
+        ev = ev_of.get(int(k), np.zeros(0))
+        ev = ev[np.isfinite(ev)]
+        if not (ev.size and np.min(np.abs(ev / THETA - 1.0)) <= 1e-8):
+            bad.append(int(k))
+    x = res.solution.cpu().numpy()
+    xr = g[f"{v}_solution"]
+    rel = float(np.linalg.norm(x - xr) / np.linalg.norm(xr))
+    it_ok = abs(res.iterations - int(g[f"{v}_iterations"])) <= 1
+    tot_ok = (res.pnumF, res.pnumE, res.n_vertex) == (int(g[f"{v}_pnumF"]), int(g[f"{v}_pnumE"]),
+                                                      int(g[f"{v}_n_vertex"]))
+    ok = it_ok and tot_ok and not bad and rel <= 1e-8
+    return {"status": "ok" if ok else "FAIL", "fixture": f"tests/golden/cfg{cfg}.npz (unmodified reference)",
+            "iterations": [int(res.iterations), int(g[f"{v}_iterations"])],
+            "pnum_FEV": [res.pnumF, res.pnumE, res.n_vertex],
+            "glob_count_mismatches": len(bad), "solution_rel_diff": rel}
+
+
+def reference_cfg5_timing():
+    """One-shot timing of the unmodified reference on the full cfg5 workload
+    on a GPU box's host (tools/ref_cfg5_timing.py -> profiles/), if committed."""
+    path = os.path.join(ROOT, "profiles", "ref_cfg5_timing_r02.json")
+    try:
+        return json.load(open(path))
+    except (OSError, ValueError):
+        return None
 
 
 def run_mine(args):
@@ -431,15 +560,22 @@ def run_mine(args):
                             "built on the device; symbolic plan; full hot path; D2H of nodal u"},
         "gpu_launches": launches,
     }
+    if rank == 0:
+        line["parity"] = parity_check(cfg, args, res)
     if rank == 0 and not args.no_cpu_baseline:
-        sp = cpu_sample_problem(cfg, args.sample_n, args.sample_subs)
-        threads, t_best = best_threads(sp)
+        sp = cpu_sample_problem(cfg, args.cpu_sample_n, args.cpu_sample_subs)
+        case, kind = cpu_case(sp)
+        threads, t_best = best_threads(case)
         line["cpu_baseline"] = {
-            "value": sp.n_dofs / t_best, "unit": "DOF/s", "cores": threads, "kind": "port",
-            "sample": (f"CPU oracle (restated reference hot path) on {args.sample_n}^3 cells, "
-                       f"{args.sample_subs}^3 subdomains, configs[{cfg - 1}] H/h/coefficients/thresholds, "
-                       f"{sp.n_dofs} DOFs; best of 1 and {os.cpu_count()} BLAS threads"),
+            "value": sp.n_dofs / t_best, "unit": "DOF/s", "cores": threads, "kind": kind,
+            "sample": (f"{'unmodified reference (baseline/_ref)' if kind == 'reference' else 'oracle port'} "
+                       f"hot path on {args.cpu_sample_n}^3 cells, {args.cpu_sample_subs}^3 subdomains, "
+                       f"configs[{cfg - 1}] H/h/coefficients/thresholds, {sp.n_dofs} DOFs; best of 1 and "
+                       f"{os.cpu_count()} BLAS threads"),
         }
+        ref5 = reference_cfg5_timing()
+        if ref5 is not None and cfg == 5 and args.n is None and args.subs is None:
+            line["cpu_reference_same_config"] = ref5
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -447,8 +583,32 @@ def run_mine(args):
         torch.distributed.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """--gpus N outside torchrun: re-execute under torch.distributed.run with
+    N ranks (one per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+
+    if args.impl == "mine":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:
