@@ -83,8 +83,10 @@ def workload_desc(cfg, n, subs, prob, world=1):
         "n_hat": int(prob.globs.interface_nodes.size),
         "l2": "working set (~GBs of dense subdomain matrices) > 126 MB L2; no flush",
         "parallelism": ("subdomain batch on one GPU" if world == 1 else
-                        f"subdomains sharded over {world} GPUs (contiguous blocks), glob eigenproblems by "
-                        "first-sharer rank, NCCL sum-allreduce exchanges, coarse LU replicated"),
+                        f"subdomains sharded over {world} GPUs (contiguous blocks); glob eigenproblems by "
+                        "first-sharer rank with point-to-point exchange of cross-rank glob blocks; "
+                        "interface halo exchange (NCCL send/recv), owned-entry dot allreduces, coarse "
+                        "rhs reduced to GPU 0 (single coarse factor) and solution broadcast"),
     }
 
 
@@ -444,7 +446,8 @@ def run_mine(args):
     keep = step(keep=True)
     plan = keep.ls.plan
     pc, op = keep.pc, keep.op
-    r = torch.randn(plan.n_hat, dtype=torch.float64, device="cuda")
+    n_vec = keep.ls.n_loc  # rank-local interface vector length (n_hat on one GPU)
+    r = torch.randn(n_vec, dtype=torch.float64, device="cuda")
     out = torch.empty_like(r)
     for _ in range(3):
         pc.apply_device(r, out)
@@ -465,22 +468,24 @@ def run_mine(args):
     torch.cuda.synchronize()
     pc_ms = a0.elapsed_time(a1) / reps
     nB = plan.nB.astype(np.int64)
-    op_bytes = 8 * int((nB * nB).sum()) + 8 * (3 * int(nB.sum()) + plan.n_hat)
+    op_bytes = 8 * int((nB * nB).sum()) + 8 * (3 * int(nB.sum()) + n_vec)
     npn = pc.np_sub.astype(np.int64)
     nd = nB - npn
     slot_ng2 = int((plan.gsize[plan.sub_globs].astype(np.int64) ** 2).sum())
     # SURVEY 8(d) B_apply_local (dual LU, Phi/primal rows, (Q D) glob blocks at both
     # ends, vectors) + the coarse block-inverse operators read by the coarse solve
     pc_local_bytes = 8 * int((nd * nd).sum() + 2 * (nd * npn).sum() + 2 * slot_ng2) \
-        + 8 * (6 * int(nB.sum()) + 4 * plan.n_hat)
+        + 8 * (6 * int(nB.sum()) + 4 * n_vec)
     coarse_bytes = pc.coarse_factor_bytes
     pc_bytes = pc_local_bytes + coarse_bytes
-    a0.record()
-    for _ in range(reps):
-        pc.coarse_solve(pc.rp, pc.up)
-    a1.record()
-    torch.cuda.synchronize()
-    coarse_ms = a0.elapsed_time(a1) / reps
+    coarse_ms = 0.0
+    if pc.root:  # the coarse factor lives on rank 0 only
+        a0.record()
+        for _ in range(reps):
+            pc.coarse_solve(pc.rp, pc.up)
+        a1.record()
+        torch.cuda.synchronize()
+        coarse_ms = a0.elapsed_time(a1) / reps
     del keep, pc, op
 
     # e2e through the host API: the problem's inputs live in page-locked host

@@ -479,12 +479,29 @@ int bddc_coarse_solve_blockinv(const double* F, const double* G, int n, int nD, 
 
 /* ---- krylov.cu : GMRES vector kernels (solver.py:286-310) ------------------ */
 
+/* As bddc_multi_dot over the first n entries of rows of stride ldv (owned
+ * entries of a rank-local vector on the sharded path). */
+int bddc_multi_dot_ld(const double* V, long long ldv, long long n, int m, const double* w,
+                      double* h, double* partial, int nblocks, int accumulate,
+                      cudaStream_t stream);
 int bddc_multi_dot(const double* V, long long n, int m, const double* w, double* h,
                    double* partial, int nblocks, int accumulate, cudaStream_t stream);
 int bddc_multi_axpy(const double* V, long long n, int m, const double* coef, double alpha,
                     double* w, cudaStream_t stream);
 int bddc_norm2(const double* w, long long n, double* out, double* partial, int nblocks,
                cudaStream_t stream);
+/* x[i] = sqrt(x[i]), i < n (norms after a cross-rank sum of squares). */
+int bddc_sqrt_inplace(double* x, int n, cudaStream_t stream);
+
+/* Halo / slot-exchange packing for the sharded path: dst[i] = src[idx[i]];
+ * unpacking: dst[idx[i]] = src[i] (add = 0) or dst[idx[i]] += src[i] (add = 1),
+ * idx duplicate-free.  replaces the implicit sums over all subdomains in one
+ * process of solver.py:229-242 when subdomains live on several GPUs. */
+int bddc_gather_idx(const double* src, const long long* idx, long long n, double* dst,
+                    cudaStream_t stream);
+int bddc_scatter_idx(double* dst, const long long* idx, long long n, const double* src, int add,
+                     cudaStream_t stream);
+
 int bddc_scale_copy(const double* a, long long n, const double* den, double* out,
                     cudaStream_t stream);
 

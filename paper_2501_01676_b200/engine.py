@@ -128,7 +128,27 @@ class LocalSystem:
         self.d = dplan if dplan is not None else DevicePlan(p)
         self._Binv = None
         self.timer = timer
+        self._distributed_maps()
         self._factor()
+
+    def _distributed_maps(self):
+        """Interface layout (dist.InterfaceLayout) and, on the sharded path,
+        the rank-local gather map / subassembly CSR and the slot exchange."""
+        from .dist import InterfaceLayout, SlotExchange
+
+        p, d = self.plan, self.d
+        self.layout = InterfaceLayout(p, self.comm)
+        if self.layout.multi:
+            perm = self.layout.perm_loc
+            self.iface_perm_l = dev_i32(perm)
+            src = np.argsort(perm, kind="stable")
+            self.tsrc_l = dev_i64(src)
+            self.tstart_l = dev_i64(np.searchsorted(perm[src], np.arange(self.layout.n_loc + 1)))
+            self.slotx = SlotExchange(p, self.comm)
+        else:
+            self.iface_perm_l, self.tstart_l, self.tsrc_l = d.iface_perm, d.tstart, d.tsrc
+            self.slotx = None
+        self.n_loc = self.layout.n_loc
 
     def _factor(self):
         p, d, st = self.plan, self.d, stream()
@@ -193,13 +213,20 @@ class LocalSystem:
             self._Binv = Binv
         return self._Binv
 
+    def slot_sizes(self):
+        return self.plan.gsize[self.plan.slot_glob].astype(np.int64) ** 2
+
     def _slot_blocks(self, src):
+        """Slot blocks [g, g] of `src` for every local slot; on the sharded path
+        the cross-rank slots of locally owned globs arrive from their sharers'
+        ranks (dist.SlotExchange, point to point)."""
         p, d = self.plan, self.d
         out = torch.zeros(max(p.d_total, 1), dtype=F64, device="cuda")
         lib.bddc_extract_slot_blocks(d.slot_local, d.slot_glob, d.gsize, d.sh_boff, d.sh_doff,
                                      d.nB, d.soff, src, None, out, None, int(p.sh_sub.size),
                                      stream())
-        _allreduce(self.comm, out)
+        if self.slotx is not None:
+            self.slotx.run(out, p.sh_doff, self.slot_sizes(), "to_owner")
         return out
 
     def slot_bsym(self):
@@ -441,7 +468,9 @@ class DeviceScaling:
                         ls.slot_bsym(), self.D, ws, dev_i64(ws_off[:-1]), status,
                         None if mine is None else dev_i32(mine),
                         p.G if mine is None else mine.size, stream())
-        _allreduce(comm, self.D, status)
+        if multi:  # the glob owner's deluxe blocks go to the sharers' ranks
+            ls.slotx.run(self.D, p.sh_doff, ls.slot_sizes(), "to_sharers")
+            comm.allreduce_(status)
         self._status = status
         if check:
             self.check()
@@ -580,7 +609,8 @@ class DevicePrimalSpace:
             if redo.size:  # certificates failed: general algorithm (linalg.py:116-214)
                 status[dev_i64(redo)] = 0
                 self._run_faces(redo, 0, out, scaling, BsC, BiC, d_eig_off)
-        _allreduce(comm, *out)
+        if multi:
+            self._share_results(out)
         self._raise(status, "face")
         vert = np.flatnonzero(kind == 2)
         if vert.size:  # vertices are fully primal: 1x1 identity, r = 1
@@ -615,7 +645,8 @@ class DevicePrimalSpace:
             lib.bddc_edge_x_extract(d.slot_local, d.slot_glob, d.gsize, d.kind, d.sh_boff, d.nB,
                                     d.soff, ls.bsym_inverse(), d_pb_off, d_nH, PB, XHH, d_xhh_off,
                                     EX, d_ex_off, int(sh.size), st)
-            _allreduce(comm, EX)
+            if multi:  # prior blocks of remote sharers -> the edge's owner
+                ls.slotx.run(EX, ex_off[:-1], ex_sz, "to_owner")
             del PB, XHH
             if edges.size:
                 ns = nsh[edges]
@@ -649,7 +680,7 @@ class DevicePrimalSpace:
                                    int(self.general), self.detail, self.d_det_off, st)
             del ws
         if multi and n_edges_all:
-            _allreduce(comm, *eout)
+            self._share_results(eout)
             for t, e in zip(out, eout):
                 t += e
         if n_edges_all:
@@ -659,6 +690,19 @@ class DevicePrimalSpace:
         self.r_host = self.r.cpu().numpy().astype(np.int64)
         self.n_sel_host = self.n_sel.cpu().numpy().astype(np.int64)
         del self.SC
+
+    def _share_results(self, out):
+        """Sharded path: per-glob counts, eigenvalues and status are small and
+        allreduced (each glob is written by its owner only, zeros elsewhere);
+        the changes of basis Q go point to point to the ranks of the glob's
+        other sharers."""
+        eig, n_sel, r, Q, status = out
+        ls, p = self.ls, self.ls.plan
+        for t in (eig, n_sel, r, status):
+            ls.comm.allreduce_(t)
+        sg = p.slot_glob.astype(np.int64)
+        ls.slotx.run(Q, self.q_off[sg], p.gsize[sg].astype(np.int64) ** 2, "to_sharers",
+                     per_glob=sg)
 
     def _run_faces(self, faces, mode, out, scaling, BsC, BiC, d_eig_off):
         """mode: 1 certified fast kernel, 0 general kernel, -1 reference algorithm verbatim."""
@@ -949,8 +993,18 @@ class DevicePreconditioner:
                                   self.d_poff, MP, self.Nt, p.N, st)
         del Srows, Scols, MP, RP, pinv
         nc = self.n_primal
+        # sharded: the subdomain contributions are reduced to rank 0, which holds
+        # the only coarse factorisation (north_star: coarse system solved on one GPU)
+        self.root = not multi or self.comm.rank == 0
+        if multi:
+            self.comm.reduce_(Clg, 0)
+        self._cinit_bufs(nc)
+        if not self.root:
+            self.coarse_factor_bytes = 0
+            self._Clg = None
+            self._check_coarse(None, go, ls)
+            return
         C = torch.empty(nc * nc, dtype=F64, device="cuda")  # every entry written by the scatter
-        _allreduce(self.comm, Clg)
         if multi:
             gpg = new_id[gpgid0]
             gsrc = np.argsort(gpg, kind="stable")
@@ -978,14 +1032,7 @@ class DevicePreconditioner:
                                ctypes.cast(self._lim_c, ctypes.c_void_p), self.coarse_pinv, piv,
                                status1, st)
         self.coarse_lu = C
-        dg = np.abs(piv.cpu().numpy())
-        if dg.size and (dg.min() <= 1e-14 * max(dg.max(), 1.0) or not np.all(np.isfinite(dg))):
-            bad_new = int(np.argmin(np.where(np.isfinite(dg), dg, 0.0)))
-            bad = int(self.corder[bad_new])
-            gi = int(np.searchsorted(go[:-1], bad, side="right")) - 1
-            gid = ls.globs.glob_id(ls.globs.globs[gi])
-            raise NumericalError(f"coarse matrix is singular at primal dof {bad} "
-                                 f"(glob {gid}, constraint {bad - go[gi]})")
+        self._check_coarse(piv, go, ls)
         # block-inverse solve operators (coarse.cu); the dense factor is not kept
         lay = coarse_blockinv_layout(self.lim, nc)
         self.cb_nD = lay["nD"]
@@ -1001,10 +1048,31 @@ class DevicePreconditioner:
         self.cb_z = torch.empty(nc, dtype=F64, device="cuda")
         self.coarse_factor_bytes = 8 * (int(lay["foff"][-1]) + int(lay["goff"][-1]))
         del C, self.coarse_lu, self.coarse_pinv
+
+    def _cinit_bufs(self, nc):
+        p = self.plan
         self.y = torch.empty(int(p.voff[-1]), dtype=F64, device="cuda")
         self.cvals = torch.empty(max(self.sum_np, 1), dtype=F64, device="cuda")
         self.rp = torch.empty(nc, dtype=F64, device="cuda")
         self.up = torch.empty(nc, dtype=F64, device="cuda")
+
+    def _check_coarse(self, piv, go, ls):
+        """The reference's pivot check (solver.py:118-127) on the coarse factor;
+        on the sharded path rank 0 decides and every rank raises alike."""
+        bad = -1
+        if piv is not None:
+            dg = np.abs(piv.cpu().numpy())
+            if dg.size and (dg.min() <= 1e-14 * max(dg.max(), 1.0) or not np.all(np.isfinite(dg))):
+                bad = int(self.corder[int(np.argmin(np.where(np.isfinite(dg), dg, 0.0)))])
+        if _multi(self.comm):
+            t = torch.tensor([bad], dtype=torch.int64, device="cuda")
+            self.comm.broadcast_(t, 0)
+            bad = int(t.item())
+        if bad >= 0:
+            gi = int(np.searchsorted(go[:-1], bad, side="right")) - 1
+            gid = ls.globs.glob_id(ls.globs.globs[gi])
+            raise NumericalError(f"coarse matrix is singular at primal dof {bad} "
+                                 f"(glob {gid}, constraint {bad - go[gi]})")
 
     @property
     def coarse(self):
@@ -1066,23 +1134,29 @@ class DevicePreconditioner:
             out.copy_(self._rout)
             return out
         if out is None:
-            out = torch.empty(self.n_hat, dtype=F64, device="cuda")
+            out = torch.empty(self.ls.n_loc, dtype=F64, device="cuda")
         return self._launch(r, out)
 
     def _launch(self, r, out):
-        p, d, st = self.plan, self.ls.d, stream()
+        """r, out: rank-local interface vectors (the global ones on one rank)."""
+        ls, p, d, st = self.ls, self.plan, self.ls.d, stream()
         nbmax = int(p.nB.max())
-        lib.bddc_pc_local_solve(d.nB, d.soff, d.voff, d.iface_perm, self.LU, d.pos2k, d.sub_globs,
-                                d.sub_glob_boff, d.sub_glob_sh, d.gsize, d.sh_doff, self.TT,
-                                self.d_mask, r, self.y, self.d_pstart, self.d_poff, self.G,
-                                self.cvals, p.N, nbmax, st)
+        lib.bddc_pc_local_solve(d.nB, d.soff, d.voff, ls.iface_perm_l, self.LU, d.pos2k,
+                                d.sub_globs, d.sub_glob_boff, d.sub_glob_sh, d.gsize, d.sh_doff,
+                                self.TT, self.d_mask, r, self.y, self.d_pstart, self.d_poff,
+                                self.G, self.cvals, p.N, nbmax, st)
         lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp, self.n_primal, st)
-        _allreduce(self.comm, self.rp)
-        self.coarse_solve(self.rp, self.up)
+        if _multi(self.comm):  # coarse rhs -> rank 0, coarse solve there, solution to all
+            self.comm.reduce_(self.rp, 0)
+            if self.root:
+                self.coarse_solve(self.rp, self.up)
+            self.comm.broadcast_(self.up, 0)
+        else:
+            self.coarse_solve(self.rp, self.up)
         lib.bddc_prolong_primal(d.nB, d.voff, self.d_pstart, self.d_pgid, self.d_poff, self.Nt,
                                 self.up, self.y, p.N, st)
-        lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n_hat, st)
-        _allreduce(self.comm, out)
+        lib.bddc_gather_reduce(ls.tstart_l, ls.tsrc_l, self.y, out, ls.n_loc, st)
+        ls.layout.halo_sum_(out)
         return out
 
     def coarse_solve(self, b, x):
@@ -1098,10 +1172,12 @@ class DevicePreconditioner:
         return x
 
     def apply(self, r):
-        """M^-1 r on nodal interface vectors (numpy or device tensor)."""
-        if isinstance(r, torch.Tensor):
-            return self.apply_device(r.to(device="cuda", dtype=F64).contiguous())
-        return self.apply_device(dev_f64(r)).cpu().numpy()
+        """M^-1 r on global nodal interface vectors (numpy or device tensor); on
+        the sharded path every rank passes the same r and gets the global result."""
+        lay = self.ls.layout
+        x = r.to(device="cuda", dtype=F64).contiguous() if isinstance(r, torch.Tensor) else dev_f64(r)
+        y = lay.to_global(self.apply_device(lay.to_local(x).contiguous()))
+        return y if isinstance(r, torch.Tensor) else y.cpu().numpy()
 
 
 class DeviceInterfaceOperator:
@@ -1109,30 +1185,38 @@ class DeviceInterfaceOperator:
 
     def __init__(self, ls):
         self.ls = ls
-        self.n = ls.plan.n_hat
+        self.n = ls.plan.n_hat       # global interface size (reference n)
+        self.n_loc = ls.n_loc        # rank-local vector length (= n on one rank)
+        self.layout = ls.layout
         self.y = torch.empty(int(ls.plan.voff[-1]), dtype=F64, device="cuda")
 
     def apply_device(self, u, out=None):
-        p, d, st = self.ls.plan, self.ls.d, stream()
+        """S_hat u on rank-local vectors (halo-completed on the sharded path)."""
+        ls, p, d, st = self.ls, self.ls.plan, self.ls.d, stream()
         if out is None:
-            out = torch.empty(self.n, dtype=F64, device="cuda")
-        lib.bddc_local_gemv(d.nB, d.soff, d.voff, d.iface_perm, self.ls.S, u, self.y, None, None,
+            out = torch.empty(self.n_loc, dtype=F64, device="cuda")
+        lib.bddc_local_gemv(d.nB, d.soff, d.voff, ls.iface_perm_l, ls.S, u, self.y, None, None,
                             None, None, p.N, int(p.nB.max()), 2, st)
-        lib.bddc_gather_reduce(d.tstart, d.tsrc, self.y, out, self.n, st)
-        _allreduce(self.ls.comm, out)
-        return out
+        lib.bddc_gather_reduce(ls.tstart_l, ls.tsrc_l, self.y, out, self.n_loc, st)
+        return self.layout.halo_sum_(out)
 
     def __call__(self, u):
-        if isinstance(u, torch.Tensor):
-            return self.apply_device(u.to(device="cuda", dtype=F64).contiguous())
-        return self.apply_device(dev_f64(u)).cpu().numpy()
+        """S_hat u on global vectors (numpy or device tensor)."""
+        lay = self.layout
+        x = u.to(device="cuda", dtype=F64).contiguous() if isinstance(u, torch.Tensor) else dev_f64(u)
+        y = lay.to_global(self.apply_device(lay.to_local(x).contiguous()))
+        return y if isinstance(u, torch.Tensor) else y.cpu().numpy()
+
+    def rhs_local(self):
+        """g_hat = sum R_i^T g_i as a rank-local vector."""
+        ls = self.ls
+        out = torch.empty(self.n_loc, dtype=F64, device="cuda")
+        lib.bddc_gather_reduce(ls.tstart_l, ls.tsrc_l, ls.g, out, self.n_loc, stream())
+        return self.layout.halo_sum_(out)
 
     def rhs_device(self):
-        p, d = self.ls.plan, self.ls.d
-        out = torch.empty(self.n, dtype=F64, device="cuda")
-        lib.bddc_gather_reduce(d.tstart, d.tsrc, self.ls.g, out, self.n, stream())
-        _allreduce(self.ls.comm, out)
-        return out
+        """g_hat as a global vector (replicated on every rank)."""
+        return self.layout.to_global(self.rhs_local())
 
 
 # ---------------------------------------------------------------------------
@@ -1156,6 +1240,29 @@ class _Basis:
         return self.buf[j]
 
 
+class _Dots:
+    """Dot products and norms of rank-local interface vectors: over the owned
+    entries, then one allreduce of the (m) partial results on the sharded
+    path; plain two-pass device reductions on one rank."""
+
+    def __init__(self, layout, n, nblk, partial):
+        self.lay, self.n, self.nblk, self.partial = layout, n, nblk, partial
+        self.n_own = layout.n_own if layout is not None else n
+        self.multi = layout is not None and layout.multi
+
+    def mdot(self, V, m, w, out):
+        lib.bddc_multi_dot_ld(V, self.n, self.n_own, m, w, out, self.partial, self.nblk, 0, stream())
+        if self.multi:
+            self.lay.comm.allreduce_(out[:m])
+
+    def norm(self, w, out):
+        if not self.multi:
+            lib.bddc_norm2(w, self.n, out, self.partial, self.nblk, stream())
+            return
+        self.mdot(w, 1, w, out)
+        lib.bddc_sqrt_inplace(out, 1, stream())
+
+
 def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     """Full left-preconditioned GMRES (reference solver.py:262-315).
 
@@ -1173,8 +1280,9 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     hb = torch.empty(2 * (max_iter + 2), dtype=F64, device="cuda")
     h1, scal = hb[:max_iter + 1], hb[max_iter + 1:]
     tres = torch.empty(max_iter + 1, dtype=F64, device="cuda")
+    dots = _Dots(getattr(operator, "layout", None), n, nblk, partial)
     z0 = pc.apply_device(rhs)
-    lib.bddc_norm2(z0, n, scal, partial, nblk, st)
+    dots.norm(z0, scal)
     ref = float(scal[0].item())
     if ref == 0.0:
         return 0, True, torch.zeros(n, dtype=F64, device="cuda"), [0.0], [0.0]
@@ -1195,11 +1303,11 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
         operator.apply_device(V[j], out=U[j])
         pc.apply_device(U[j], out=w)
         m = j + 1
-        lib.bddc_multi_dot(V.buf, n, m, w, h1, partial, nblk, 0, st)
+        dots.mdot(V.buf, m, w, h1)
         lib.bddc_multi_axpy(V.buf, n, m, h1, -1.0, w, st)
-        lib.bddc_multi_dot(V.buf, n, m, w, scal, partial, nblk, 0, st)
+        dots.mdot(V.buf, m, w, scal)
         lib.bddc_multi_axpy(V.buf, n, m, scal, -1.0, w, st)
-        lib.bddc_norm2(w, n, scal[m:], partial, nblk, st)
+        dots.norm(w, scal[m:])
         hc = hb[:max_iter + 2 + m].cpu().numpy()  # h1[:m] and scal[:m+1] in one read
         hs = hc[max_iter + 1:max_iter + 2 + m]
         hh = hc[:m] + hs[:m]
@@ -1213,7 +1321,7 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
         yd = dev_f64(y)
         r.copy_(rhs)
         lib.bddc_multi_axpy(U.buf, n, m, yd, -1.0, r, st)
-        lib.bddc_norm2(r, n, tres[j:], partial, nblk, st)
+        dots.norm(r, tres[j:])
         if pre_hist[-1] <= rel_tol:
             conv = True
             break
@@ -1244,7 +1352,8 @@ def gmres_right_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300, restart=20
     nblk = 296
     partial = torch.empty(nblk * (restart + 2), dtype=F64, device="cuda")
     scal = torch.empty(restart + 2, dtype=F64, device="cuda")
-    lib.bddc_norm2(rhs, n, scal, partial, nblk, st)
+    dots = _Dots(getattr(operator, "layout", None), n, nblk, partial)
+    dots.norm(rhs, scal)
     bnorm = float(scal[0].item())
     x = torch.zeros(n, dtype=F64, device="cuda")
     if bnorm == 0.0:
@@ -1261,7 +1370,7 @@ def gmres_right_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300, restart=20
     r.copy_(rhs)
     beta = bnorm
     while it < max_iter and not conv:
-        lib.bddc_norm2(r, n, scal, partial, nblk, st)
+        dots.norm(r, scal)
         beta = float(scal[0].item())
         if beta <= rel_tol * bnorm:
             conv = True
@@ -1276,11 +1385,11 @@ def gmres_right_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300, restart=20
             pc.apply_device(V[j], out=Z[j])
             operator.apply_device(Z[j], out=w)
             m = j + 1
-            lib.bddc_multi_dot(V.buf, n, m, w, h1, partial, nblk, 0, st)
+            dots.mdot(V.buf, m, w, h1)
             lib.bddc_multi_axpy(V.buf, n, m, h1, -1.0, w, st)
-            lib.bddc_multi_dot(V.buf, n, m, w, scal, partial, nblk, 0, st)
+            dots.mdot(V.buf, m, w, scal)
             lib.bddc_multi_axpy(V.buf, n, m, scal, -1.0, w, st)
-            lib.bddc_norm2(w, n, scal[m:], partial, nblk, st)
+            dots.norm(w, scal[m:])
             hs = scal[:m + 1].cpu().numpy()
             H[:m, j] = h1[:m].cpu().numpy() + hs[:m]
             hn = float(hs[m])
@@ -1296,7 +1405,7 @@ def gmres_right_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300, restart=20
         lib.bddc_multi_axpy(Z.buf, n, m, dev_f64(y), 1.0, x, st)
         operator.apply_device(x, out=w)
         torch.sub(rhs, w, out=r)
-        lib.bddc_norm2(r, n, scal, partial, nblk, st)
+        dots.norm(r, scal)
         true_rel = float(scal[0].item()) / bnorm
         if hist:
             hist[-1] = true_rel
@@ -1307,7 +1416,10 @@ def gmres_right_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300, restart=20
 
 
 def recover_device(ls, u_hat):
-    """Nodal solution with interiors back-substituted (reference solver.py:318-326)."""
+    """Nodal solution with interiors back-substituted (reference solver.py:318-326).
+    u_hat: the rank-local interface vector (the global one on one rank); on
+    the sharded path the nodal vector is assembled on every rank (interiors
+    and owned interface values of each rank, one allreduce)."""
     p, d, st = ls.plan, ls.d, stream()
     iface = dev_i64(ls.globs.interface_nodes)
     if not _multi(ls.comm):
@@ -1316,13 +1428,15 @@ def recover_device(ls, u_hat):
         lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, d.iface_perm, d.ioff,
                                   d.I_nodes, u_hat, u, p.N, int(p.nL.max()), PANEL, st)
         return u
-    # sharded: each rank writes its interiors into zeros, the sum is the union
+    lay = ls.layout
     ui = torch.zeros_like(ls.inputs["gdir"])
-    lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, d.iface_perm, d.ioff,
+    lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, ls.iface_perm_l, d.ioff,
                               d.I_nodes, u_hat, ui, p.N, int(p.nL.max()), PANEL, st)
+    own_nodes = dev_i64(np.asarray(ls.globs.interface_nodes)[lay.glob_ids[:lay.n_own]])
+    ui[own_nodes] = u_hat[:lay.n_own]
     ls.comm.allreduce_(ui)
     interior = ls.inputs["free"].clone()
     interior[iface] = False
     u = torch.where(interior, ui, ls.inputs["gdir"])
-    u[iface] = u_hat
+    u[iface] = ui[iface]
     return u

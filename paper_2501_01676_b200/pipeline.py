@@ -57,7 +57,7 @@ def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8,
     pc = DevicePreconditioner(ls, sc, ps.r_host, ps.Q, ps.d_q_off)
     op = DeviceInterfaceOperator(ls)
     tm.mark("gmres")
-    rhs = op.rhs_device()
+    rhs = op.rhs_local()
     if side == "left":  # the reference's full left-preconditioned GMRES
         it, conv, x, th, ph = gmres_device(op, rhs, pc, rel_tol, max_iter)
     else:  # right-preconditioned GMRES(restart), BASELINE.json's variant
@@ -69,7 +69,8 @@ def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8,
     kinds = plan.kind
     r = ps.r_host
     res.iterations, res.converged = it, conv
-    res.solution, res.u = x, u
+    res.solution, res.u = ls.layout.to_global(x), u  # solution: global, replicated on every rank
+    res.solution_local = x
     res.true_hist, res.pre_hist = th, ph
     res.pnumF = int(r[kinds == 0].sum())
     res.pnumE = int(r[kinds == 1].sum())

@@ -93,15 +93,16 @@ def gmres_solve(operator, rhs, pc, rel_tol=1e-8, max_iter=300, side="left", rest
                         "build_preconditioner(...) objects from this package")
     t0 = time.perf_counter()
     rhs_d = rhs if isinstance(rhs, torch.Tensor) else dev_f64(rhs)
+    lay = operator.layout
+    b = lay.to_local(rhs_d.to(dtype=F64, device="cuda")).contiguous()
     if side == "left":
-        it, conv, x, th, ph = gmres_device(operator, rhs_d.to(dtype=F64, device="cuda"), pc,
-                                           rel_tol, max_iter)
+        it, conv, x, th, ph = gmres_device(operator, b, pc, rel_tol, max_iter)
     elif side == "right":
-        it, conv, x, th, ph = gmres_right_device(operator, rhs_d.to(dtype=F64, device="cuda"), pc,
-                                                 rel_tol, max_iter,
+        it, conv, x, th, ph = gmres_right_device(operator, b, pc, rel_tol, max_iter,
                                                  200 if restart is None else restart)
     else:
         raise ValueError(f"unknown preconditioning side {side!r}")
+    x = lay.to_global(x)
     return SolveReport(it, conv, x.cpu().numpy(), th, ph, solve_time=time.perf_counter() - t0)
 
 
@@ -159,7 +160,8 @@ def recover_interior(ops, globs, system, u_hat):
     """solver.py:318-326"""
     ls = ops[0].ls
     u_d = u_hat if isinstance(u_hat, torch.Tensor) else dev_f64(u_hat)
-    return recover_device(ls, u_d.to(dtype=F64, device="cuda")).cpu().numpy()
+    u_l = ls.layout.to_local(u_d.to(dtype=F64, device="cuda")).contiguous()
+    return recover_device(ls, u_l).cpu().numpy()
 
 
 __all__ = ["BddcPreconditioner", "InterfaceOperator", "NumericalError", "SolveReport",

@@ -144,3 +144,103 @@ def test_gloo_world2_interface_operator():
     assert dy <= 1e-13 and dg <= 1e-13
     assert counts == ref_counts
     assert all(p.exitcode == 0 for p in ps)
+
+
+@pytest.mark.parametrize("name,size", [("jump", 2), ("jump", 3), ("cfg4_small", 4)])
+def test_interface_layout_and_slot_exchange_plans(name, size):
+    """Owned sets partition the interface; every rank's ghost list towards an
+    owner is exactly that owner's list of dofs it receives from the rank (same
+    global ids, same order); slot-exchange send / receive lists pair up."""
+    from paper_2501_01676_b200.dist import InterfaceLayout, SlotExchange
+
+    class FakeComm:
+        def __init__(self, rank):
+            self.rank, self.size = rank, size
+
+    system, part, globs = inputs(name)
+    plans = [Plan(system, part, globs, owned=block_range(part.n_subdomains, size, r)) for r in range(size)]
+    lays = [InterfaceLayout(plans[r], FakeComm(r)) for r in range(size)]
+    n_hat = globs.interface_nodes.size
+    owned = np.concatenate([l.glob_ids[:l.n_own] for l in lays])
+    assert np.array_equal(np.sort(owned), np.arange(n_hat))
+    for r, lr in enumerate(lays):
+        assert np.array_equal(np.sort(lr.glob_ids), np.unique(plans[r].iface_perm))
+        for s, idx in lr.to_owner.items():
+            back = lays[s].from_touchers[r]
+            assert np.array_equal(lr.glob_ids[idx], lays[s].glob_ids[back])
+        for s, idx in lr.from_touchers.items():
+            assert r in lays[s].to_owner
+    xs = [SlotExchange(plans[r], FakeComm(r)) for r in range(size)]
+    for d in ("to_owner", "to_sharers"):
+        pairs = [x._pairs(d) for x in xs]
+        for r in range(size):
+            send, _ = pairs[r]
+            for s, slots in send.items():
+                assert np.array_equal(slots, pairs[s][1][r])
+
+
+def _halo_worker(rank, size, port, q):
+    """World-size-2 gloo: S_hat v assembled from per-rank partial sums over each
+    rank's touched dofs with the halo exchange (point-to-point send / recv), in
+    the rank-local layout, equals the global subassembly."""
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=size)
+        comm = TorchComm()
+        from oracle import bddc_oracle as O
+        from paper_2501_01676_b200.dist import InterfaceLayout
+
+        system, part, globs = inputs("jump")
+        s0, s1 = comm.owned(part.n_subdomains)
+        plan = Plan(system, part, globs, owned=(s0, s1))
+        lay = InterfaceLayout(plan, comm)
+        n = globs.interface_nodes.size
+        v = np.random.default_rng(7).standard_normal(n)
+        loc = np.full(n, -1)
+        loc[lay.glob_ids] = np.arange(lay.n_loc)
+        y = np.zeros(lay.n_loc)
+        for s in range(s0, s1):
+            op = O.local_operator(system, part, globs, s)
+            y[loc[op.iface_index]] += op.S @ v[op.iface_index]
+        # the two halo rounds of InterfaceLayout.halo_sum_, on host tensors
+        yt = torch.from_numpy(y)
+        sends = {s: yt[torch.from_numpy(i)].clone() for s, i in lay.to_owner.items()}
+        recvs = {s: torch.empty(len(i), dtype=torch.float64) for s, i in lay.from_touchers.items()}
+        comm.exchange(sends, recvs)
+        for s in sorted(recvs):
+            yt[torch.from_numpy(lay.from_touchers[s])] += recvs[s]
+        sends = {s: yt[torch.from_numpy(i)].clone() for s, i in lay.from_touchers.items()}
+        recvs = {s: torch.empty(len(i), dtype=torch.float64) for s, i in lay.to_owner.items()}
+        comm.exchange(sends, recvs)
+        for s in sorted(recvs):
+            yt[torch.from_numpy(lay.to_owner[s])] = recvs[s]
+        full = np.zeros(n)
+        full[lay.glob_ids[:lay.n_own]] = yt.numpy()[:lay.n_own]
+        full = allreduce_np(comm, full)
+        ref = np.zeros(n)
+        for op in O.all_local_operators(system, part, globs):
+            ref[op.iface_index] += op.S @ v[op.iface_index]
+        ghost_ok = np.allclose(yt.numpy(), ref[lay.glob_ids], rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+        if rank == 0:
+            q.put((float(np.abs(full - ref).max() / np.abs(ref).max()), bool(ghost_ok)))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # surfaced to the parent
+        q.put(repr(e))
+        raise
+
+
+def test_gloo_world2_halo_exchange():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_halo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = q.get(timeout=600)
+    for p in ps:
+        p.join(timeout=120)
+    assert not isinstance(res, str), res
+    err, ghost_ok = res
+    assert err <= 1e-13 and ghost_ok
+    assert all(p.exitcode == 0 for p in ps)

@@ -81,3 +81,66 @@ def test_sharded_device_elements_match_single():
         assert it == single.iterations
         assert _rel(x, ref) <= 1e-10
         assert _rel(u, single.u.cpu().numpy()) <= 1e-10
+
+
+def _gloo_gpu_worker(rank, size, port, q, name):
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=size)
+        from paper_2501_01676_b200 import pipeline
+        from paper_2501_01676_b200.dist import TorchComm
+
+        comm = TorchComm()
+        g = golden(name)
+        system, part, globs = inputs(name)
+        res = pipeline.run(system, part, globs, float(g["theta_f"]), float(g["theta_e"]), "new",
+                           comm=comm, keep=True)
+        lay = res.ls.layout
+        out = (res.iterations, _rel(res.solution.cpu().numpy(), g["new_solution"]),
+               _rel(res.u.cpu().numpy(), g["new_u"]), res.pnumF, res.pnumE, res.n_vertex,
+               lay.n_own, lay.n_loc, lay.halo_bytes())
+        q.put((rank, out))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception as e:  # surfaced to the parent
+        q.put((rank, repr(e)))
+        raise
+
+
+@pytest.mark.parametrize("name", ["jump", "cfg4_small"])
+def test_two_processes_torchcomm_end_to_end(name):
+    """pipeline.run(comm=TorchComm()) in two processes on one GPU (gloo,
+    device buffers staged through the host; no kernel waits on the other
+    rank's): halo exchange, owned-entry dots, coarse reduce / solve on rank 0 /
+    broadcast, point-to-point glob-block exchange; against the golden fixture."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_gloo_gpu_worker, args=(r, 2, port, q, name)) for r in range(2)]
+    for p in ps:
+        p.start()
+    outs = dict(q.get(timeout=900) for _ in range(2))
+    for p in ps:
+        p.join(timeout=120)
+    g = golden(name)
+    for r in (0, 1):
+        assert not isinstance(outs[r], str), outs[r]
+        it, dx, du, F, E, V, n_own, n_loc, hb = outs[r]
+        assert abs(it - int(g["new_iterations"])) <= 1
+        assert dx <= 1e-8 and du <= 1e-8
+        assert (F, E, V) == (int(g["new_pnumF"]), int(g["new_pnumE"]), int(g["new_n_vertex"]))
+        assert 0 < n_own <= n_loc and hb > 0
+    assert outs[0][6] + outs[1][6] == int(g["n_hat"])
+    assert all(p.exitcode == 0 for p in ps)
