@@ -490,6 +490,15 @@ int bddc_multi_axpy(const double* V, long long n, int m, const double* coef, dou
                     double* w, cudaStream_t stream);
 int bddc_norm2(const double* w, long long n, double* out, double* partial, int nblocks,
                cudaStream_t stream);
+/* One step of the GMRES least-squares recurrence by Givens rotations on the
+ * device: column m-1 of the Hessenberg matrix is h1[0:m] + h2[0:m] (the two
+ * Gram-Schmidt passes), subdiagonal h2[m]; updates R (column-major, ldr
+ * rows), the rotations cs / sn and the rotated rhs g (g[0] = beta), writes
+ * y = R^-1 g[0:m] and out = {|g[m]|, h2[m]}.  m <= 1023.
+ * replaces scipy.linalg.lstsq(H, beta e1, gelsd) per step, solver.py:297-300. */
+int bddc_gmres_givens(const double* h1, const double* h2, int m, int ldr, double* R, double* cs,
+                      double* sn, double* g, double* y, double* out, cudaStream_t stream);
+
 /* x[i] = sqrt(x[i]), i < n (norms after a cross-rank sum of squares). */
 int bddc_sqrt_inplace(double* x, int n, cudaStream_t stream);
 

@@ -103,6 +103,57 @@ __global__ void scatter_idx_kernel(double* __restrict__ dst, const long long* __
   }
 }
 
+// One GMRES step of the Hessenberg least-squares problem by Givens rotations
+// (replaces the per-step host lstsq/gelsd of solver.py:297 with the
+// mathematically identical QR recurrence; one CTA).  Column m-1 of H is
+// h = h1[0:m] + h2[0:m] (the two classical Gram-Schmidt passes) with
+// subdiagonal hn = h2[m].  R: column-major, ldr rows (upper triangular);
+// cs/sn: rotations; g: rotated beta e1 (g[0] = beta set by the caller);
+// y = R^-1 g[0:m]; out[0] = |g[m]| (the least-squares residual), out[1] = hn.
+__global__ void gmres_givens_kernel(const double* __restrict__ h1, const double* __restrict__ h2,
+                                    int m, int ldr, double* __restrict__ R, double* __restrict__ cs,
+                                    double* __restrict__ sn, double* __restrict__ g,
+                                    double* __restrict__ y, double* __restrict__ out) {
+  __shared__ double col[1024];
+  __shared__ double ys[1024];
+  double* Rc = R + (long long)(m - 1) * ldr;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < m; ++i) col[i] = h1[i] + h2[i];
+    const double hn = h2[m];
+    for (int i = 0; i + 1 < m; ++i) {
+      const double a = col[i], b = col[i + 1];
+      col[i] = cs[i] * a + sn[i] * b;
+      col[i + 1] = -sn[i] * a + cs[i] * b;
+    }
+    const double a = col[m - 1];
+    const double r = hypot(a, hn);
+    const double c = r > 0.0 ? a / r : 1.0, s = r > 0.0 ? hn / r : 0.0;
+    cs[m - 1] = c;
+    sn[m - 1] = s;
+    col[m - 1] = r;
+    const double gm = g[m - 1];
+    g[m - 1] = c * gm;
+    g[m] = -s * gm;
+    for (int i = 0; i < m; ++i) Rc[i] = col[i];
+    out[0] = fabs(g[m]);
+    out[1] = hn;
+  }
+  __syncthreads();
+  // back substitution, one warp: y_i = (g_i - sum_{k>i} R[i,k] y_k) / R[i,i]
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    for (int i = m - 1; i >= 0; --i) {
+      double acc = 0.0;
+      for (int k = i + 1 + lane; k < m; k += 32) acc += R[(long long)k * ldr + i] * ys[k];
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) ys[i] = (g[i] - acc) / R[(long long)i * ldr + i];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) y[i] = ys[i];
+}
+
 }  // namespace bddc
 
 using namespace bddc;
@@ -146,6 +197,14 @@ int bddc_norm2(const double* w, long long n, double* out, double* partial, int n
   int st = bddc_multi_dot(w, n, 1, w, out, partial, nblocks, 0, stream);
   if (st) return st;
   sqrt_kernel<<<1, 1, 0, stream>>>(out); bddc_note_launches(1);
+  return kr_status();
+}
+
+int bddc_gmres_givens(const double* h1, const double* h2, int m, int ldr, double* R, double* cs,
+                      double* sn, double* g, double* y, double* out, cudaStream_t stream) {
+  if (m <= 0 || m > 1023) return -(int)cudaErrorInvalidValue;
+  gmres_givens_kernel<<<1, 128, 0, stream>>>(h1, h2, m, ldr, R, cs, sn, g, y, out);
+  bddc_note_launches(1);
   return kr_status();
 }
 

@@ -1267,16 +1267,19 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     """Full left-preconditioned GMRES (reference solver.py:262-315).
 
     Orthogonalisation is classical Gram-Schmidt applied twice (same Krylov
-    space as the reference's MGS x 2); the least-squares problem is solved
-    with gelsd on the host exactly as the reference does (one device->host
-    read of the new Hessenberg column per step); the true residual uses stored
-    S_hat V_j columns instead of an extra S_hat application and its norms are
-    kept on the device and read once at the end."""
+    space as the reference's MGS x 2).  The least-squares problem of each
+    step (the reference's gelsd, solver.py:297) is the equivalent Givens QR
+    recurrence on the device (bddc_gmres_givens); the true residual uses the
+    stored S_hat V_j columns (no extra operator application).  The host
+    decision whether to stop after step j is taken while step j + 1 already
+    runs (its residual scalars come back through a pinned buffer and an
+    event), so the GPU never idles on the host; the one speculative step
+    after convergence is discarded."""
     st = stream()
     n = rhs.shape[0]
     nblk = 296
     partial = torch.empty(nblk * (max_iter + 2), dtype=F64, device="cuda")
-    # one buffer for both Gram-Schmidt passes and the norm: [h1 (max_iter+1) | h2 .. hn]
+    # [h1 (max_iter+1) | h2 .. hn (max_iter+1)]
     hb = torch.empty(2 * (max_iter + 2), dtype=F64, device="cuda")
     h1, scal = hb[:max_iter + 1], hb[max_iter + 1:]
     tres = torch.empty(max_iter + 1, dtype=F64, device="cuda")
@@ -1289,52 +1292,65 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     V = _Basis(n)
     U = _Basis(n)
     lib.bddc_scale_copy(z0, n, scal, V[0], st)
-    H = np.zeros((max_iter + 1, max_iter))
-    e1 = np.zeros(max_iter + 1)
-    e1[0] = ref
+    ldr = max_iter + 1
+    R = torch.zeros(ldr * max_iter, dtype=F64, device="cuda")
+    cs = torch.zeros(max_iter, dtype=F64, device="cuda")
+    sn = torch.zeros(max_iter, dtype=F64, device="cuda")
+    g = torch.zeros(max_iter + 1, dtype=F64, device="cuda")
+    g[0] = ref
+    ys = torch.zeros((2, max_iter), dtype=F64, device="cuda")   # y of the last two steps
+    out = torch.zeros((max_iter, 2), dtype=F64, device="cuda")
+    host = torch.zeros((max_iter, 2), dtype=F64, pin_memory=True)
+    events = []
     w = torch.empty(n, dtype=F64, device="cuda")
     r = torch.empty(n, dtype=F64, device="cuda")
     pre_hist = []
-    conv = False
+    state = {"conv": False}
+
+    def finished(j):
+        """Stop after step j (m = j + 1)?  Reads that step's residual scalars."""
+        events[j].synchronize()
+        res, hn = float(host[j, 0]), float(host[j, 1])
+        pre_hist.append(res / ref)
+        if res / ref <= rel_tol:
+            state["conv"] = True
+            return True
+        return hn <= 1e-14 * ref
+
     it = 0
-    y = np.zeros(0)
     for j in range(max_iter):
-        U.ensure(j + 1)
+        m = j + 1
+        U.ensure(m)
         operator.apply_device(V[j], out=U[j])
         pc.apply_device(U[j], out=w)
-        m = j + 1
         dots.mdot(V.buf, m, w, h1)
         lib.bddc_multi_axpy(V.buf, n, m, h1, -1.0, w, st)
         dots.mdot(V.buf, m, w, scal)
         lib.bddc_multi_axpy(V.buf, n, m, scal, -1.0, w, st)
         dots.norm(w, scal[m:])
-        hc = hb[:max_iter + 2 + m].cpu().numpy()  # h1[:m] and scal[:m+1] in one read
-        hs = hc[max_iter + 1:max_iter + 2 + m]
-        hh = hc[:m] + hs[:m]
-        hn = float(hs[m])
-        H[:m, j] = hh
-        H[m, j] = hn
-        y = scipy.linalg.lstsq(H[:m + 1, :m], e1[:m + 1], lapack_driver="gelsd")[0]
-        res = float(np.linalg.norm(e1[:m + 1] - H[:m + 1, :m] @ y))
-        it = m
-        pre_hist.append(res / ref)
-        yd = dev_f64(y)
+        y = ys[j % 2]
+        lib.bddc_gmres_givens(h1, scal, m, ldr, R, cs, sn, g, y, out[j], st)
+        host[j].copy_(out[j], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        events.append(ev)
+        # true residual of this step: r = rhs - S_hat V y (from the stored U = S_hat V)
         r.copy_(rhs)
-        lib.bddc_multi_axpy(U.buf, n, m, yd, -1.0, r, st)
+        lib.bddc_multi_axpy(U.buf, n, m, y, -1.0, r, st)
         dots.norm(r, tres[j:])
-        if pre_hist[-1] <= rel_tol:
-            conv = True
-            break
-        if hn <= 1e-14 * ref:
-            conv = pre_hist[-1] <= rel_tol
-            break
         V.ensure(j + 2)
         lib.bddc_scale_copy(w, n, scal[m:], V[j + 1], st)
+        if j >= 1 and finished(j - 1):
+            it = j
+            break
+    else:
+        finished(max_iter - 1)
+        it = max_iter
     x = torch.zeros(n, dtype=F64, device="cuda")
     if it:
-        lib.bddc_multi_axpy(V.buf, n, it, dev_f64(y), 1.0, x, st)
+        lib.bddc_multi_axpy(V.buf, n, it, ys[(it - 1) % 2], 1.0, x, st)
     true_hist = tres[:it].cpu().numpy().tolist()
-    return it, conv, x, true_hist, pre_hist
+    return it, state["conv"], x, true_hist, pre_hist
 
 
 def gmres_right_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300, restart=200):
