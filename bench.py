@@ -82,6 +82,7 @@ def workload_desc(cfg, n, subs, prob, world=1):
         "n_subdomains": int(prob.partition.n_subdomains),
         "n_hat": int(prob.globs.interface_nodes.size),
         "l2": "working set (~GBs of dense subdomain matrices) > 126 MB L2; no flush",
+        "host": "Python cyclic GC paused inside each timed step (collected between steps)",
         "parallelism": ("subdomain batch on one GPU" if world == 1 else
                         f"subdomains sharded over {world} GPUs (contiguous blocks); glob eigenproblems by "
                         "first-sharer rank with point-to-point exchange of cross-rank glob blocks; "
@@ -392,6 +393,8 @@ def run_mine(args):
         return pipeline.run(prob.system, prob.partition, prob.globs, THETA, THETA, "new",
                             inputs=inputs, kernel_timing=kernel_timing, keep=keep, comm=comm)
 
+    import gc
+
     clocks = ClockSampler(local)
     nwarm = max(args.warmup, 3)
     for i in range(nwarm):
@@ -407,6 +410,10 @@ def run_mine(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     lib.bddc_trailing_log(1)  # CUDA events around the trailing launches (pool created here)
+    # the Python cyclic GC stays off inside the timed region (a collection
+    # mid-step stalls the host that feeds the GPU); it runs between regions
+    gc.collect()
+    gc.disable()
     torch.cuda.synchronize()
     e0.record()
     phases = {}
@@ -422,6 +429,7 @@ def run_mine(args):
         step_ev.append(ev)
     e1.record()
     torch.cuda.synchronize()
+    gc.enable()
     if world > 1:
         torch.distributed.barrier()
     launches = (int(lib.bddc_launch_count()) - (GRAPH_STATS["captured"] - g0["captured"])
@@ -498,6 +506,8 @@ def run_mine(args):
     u_pinned = torch.empty(sysm.mesh.n_nodes, dtype=torch.float64, pin_memory=True)
     e2e_ms = []
     for i in range(args.e2e_steps + 1):  # the first (allocator warm-up) is not timed
+        gc.collect()
+        gc.disable()
         torch.cuda.synchronize()
         w0 = time.perf_counter()
         inp = upload_staged(staged)
@@ -508,6 +518,7 @@ def run_mine(args):
         torch.cuda.synchronize()
         if i > 0:
             e2e_ms.append((time.perf_counter() - w0) * 1e3)
+        gc.enable()
         del rr, inp
     e2e_step_ms = float(np.mean(e2e_ms))
     if world > 1:

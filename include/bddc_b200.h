@@ -264,15 +264,17 @@ int bddc_edge_gevp_old(const int* kind, const int* size, const int* sh_start, co
 /* Slot-compact glob blocks.  Every (glob, sharer) slot k whose sharer is a
  * subdomain of this rank (slot_sub[k] = its local index, -1 otherwise) gets
  * the n_g x n_g principal blocks of Bsym / Bsym^-1 at BsC / BiC + sh_doff[k]
- * (BiC may be NULL); the per-glob kernels read only these buffers, so a
- * sum-allreduce of them is the whole exchange the glob phase needs when the
- * subdomains are sharded over ranks.
+ * (BsC or BiC may be NULL); sym = 1: the first source is S and BsC receives
+ * the blocks of Bsym = sym(S).  The per-glob kernels read only these
+ * buffers; on the sharded path the cross-rank slots move point to point
+ * (dist.SlotExchange).
  * replaces the per-glob Bsym[g_idx][:, g_idx] slicing of build_scaling
  *          scaling.py:33-41 and glob_schur_block substructuring.py:152-171. */
 int bddc_extract_slot_blocks(const int* slot_sub, const int* slot_glob, const int* size,
                              const int* sh_boff, const long long* sh_doff, const int* nB,
                              const long long* soff, const double* Bsym, const double* Binv,
-                             double* BsC, double* BiC, int n_slots, cudaStream_t stream);
+                             double* BsC, double* BiC, int n_slots, int sym,
+                             cudaStream_t stream);
 
 /* Glob Schur blocks sym(((Bsym^-1)[g,g])^-1) of the listed slots with
  * n_g <= 64 (register Gauss-Jordan, one CTA per slot) into SC (sh_doff

@@ -881,7 +881,7 @@ __global__ void extract_slot_blocks_kernel(const int* __restrict__ slot_sub,
                                            const double* __restrict__ Bsym,
                                            const double* __restrict__ Binv,
                                            double* __restrict__ BsC, double* __restrict__ BiC,
-                                           int n_slots) {
+                                           int n_slots, int sym) {
   const int k = blockIdx.x;
   if (k >= n_slots) return;
   const int s = slot_sub[k];
@@ -890,7 +890,12 @@ __global__ void extract_slot_blocks_kernel(const int* __restrict__ slot_sub,
   for (int idx = threadIdx.x; idx < n * n; idx += blockDim.x) {
     const int r = idx / n, c = idx - r * n;
     const long long src = soff[s] + (long long)(bo + r) * nb + bo + c;
-    BsC[sh_doff[k] + idx] = Bsym[src];
+    if (BsC) {
+      const double v = Bsym[src];
+      // sym: the source is S; the glob block of Bsym = sym(S) is sym of its block
+      BsC[sh_doff[k] + idx] =
+          sym ? 0.5 * (v + Bsym[soff[s] + (long long)(bo + c) * nb + bo + r]) : v;
+    }
     if (BiC) BiC[sh_doff[k] + idx] = Binv[src];
   }
 }
@@ -1478,10 +1483,12 @@ long long bddc_ws_edge_new(long long ns, long long ne, long long wd, long long n
 int bddc_extract_slot_blocks(const int* slot_sub, const int* slot_glob, const int* size,
                              const int* sh_boff, const long long* sh_doff, const int* nB,
                              const long long* soff, const double* Bsym, const double* Binv,
-                             double* BsC, double* BiC, int n_slots, cudaStream_t stream) {
+                             double* BsC, double* BiC, int n_slots, int sym,
+                             cudaStream_t stream) {
   if (n_slots <= 0) return 0;
   extract_slot_blocks_kernel<<<n_slots, 128, 0, stream>>>(slot_sub, slot_glob, size, sh_boff, sh_doff,
-                                                          nB, soff, Bsym, Binv, BsC, BiC, n_slots);
+                                                          nB, soff, Bsym, Binv, BsC, BiC, n_slots,
+                                                          sym);
   bddc_note_launches(1);
   return glob_launch_status();
 }

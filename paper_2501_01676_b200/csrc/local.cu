@@ -560,25 +560,47 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_col_kernel(
 // ---------------------------------------------------------------------------
 // extraction and small elementwise kernels
 // ---------------------------------------------------------------------------
-// S = M[nI:nL, nI:nL] -> S (ld nB), g = M[nI:nL, nL], Bsym = (S + S^T)/2
-__global__ void extract_schur_kernel(const double* __restrict__ base, const long long* __restrict__ off,
-                                     const int* __restrict__ ld, const int* __restrict__ nI,
-                                     const int* __restrict__ nB, const long long* __restrict__ soff,
-                                     const long long* __restrict__ voff, double* __restrict__ S,
-                                     double* __restrict__ Bsym, double* __restrict__ g) {
+// S = M[nI:nL, nI:nL] -> S (ld nB), g = M[nI:nL, nL], Bsym = (S + S^T)/2.
+// 32x32 tiles staged through shared memory so that both the tile and its
+// transpose are read with coalesced rows (the transposed read of a naive
+// element loop strides by ld).
+__global__ void __launch_bounds__(256) extract_schur_kernel(
+    const double* __restrict__ base, const long long* __restrict__ off,
+    const int* __restrict__ ld, const int* __restrict__ nI, const int* __restrict__ nB,
+    const long long* __restrict__ soff, const long long* __restrict__ voff,
+    double* __restrict__ S, double* __restrict__ Bsym, double* __restrict__ g) {
+  __shared__ double t0[32][33];
+  __shared__ double t1[32][33];
   const int b = blockIdx.y;
   const int n = nB[b], i0 = nI[b], L = ld[b];
   const double* M = base + off[b] + (long long)i0 * L + i0;
   double* Sb = S + soff[b];
   double* Bb = Bsym + soff[b];
-  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < (long long)n * n;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(idx / n), c = (int)(idx - (long long)r * n);
-    const double v = M[(long long)r * L + c];
-    Sb[idx] = v;
-    Bb[idx] = 0.5 * (v + M[(long long)c * L + r]);
-    if (c == 0) g[voff[b] + r] = M[(long long)r * L + n];
+  const int nt = (n + 31) / 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int t = blockIdx.x; t < nt * nt; t += gridDim.x) {
+    const int r0 = (t / nt) * 32, c0 = (t - (t / nt) * nt) * 32;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      const int r = r0 + ty + j, c = c0 + tx;
+      t0[ty + j][tx] = (r < n && c < n) ? M[(long long)r * L + c] : 0.0;
+      const int rr = c0 + ty + j, cc = r0 + tx;  // transposed tile, read by rows
+      t1[ty + j][tx] = (rr < n && cc < n) ? M[(long long)rr * L + cc] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+      const int r = r0 + ty + j, c = c0 + tx;
+      if (r < n && c < n) {
+        const double v = t0[ty + j][tx];
+        Sb[(long long)r * n + c] = v;
+        Bb[(long long)r * n + c] = 0.5 * (v + t1[tx][ty + j]);
+      }
+    }
   }
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    g[voff[b] + r] = M[(long long)r * L + n];
 }
 
 // out[b] = ||X_b||_F^2 for square batched matrices (ld = n); one CTA per
@@ -968,7 +990,7 @@ int bddc_extract_schur(const double* M, const long long* off, const int* ld, con
                        const int* nB, const long long* soff, const long long* voff, double* S,
                        double* Bsym, double* g, int nbatch, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  extract_schur_kernel<<<dim3(64, nbatch), 256, 0, stream>>>(M, off, ld, nI, nB, soff, voff, S,
+  extract_schur_kernel<<<dim3(48, nbatch), 256, 0, stream>>>(M, off, ld, nI, nB, soff, voff, S,
                                                              Bsym, g);
   bddc_note_launches(1);
   return launch_status();

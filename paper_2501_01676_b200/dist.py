@@ -309,13 +309,14 @@ class InterfaceLayout:
         self.multi = size > 1
         n_hat = plan.n_hat
         self.n_hat = n_hat
-        perm = np.asarray(plan.iface_perm_host, dtype=np.int64)  # local B dof -> global interface id
-        if not self.multi:
+        self._dev = None
+        if not self.multi:  # identity layout: nothing to build (no device read of the plan)
             self.n_loc = self.n_own = n_hat
             self.glob_ids = np.arange(n_hat, dtype=np.int64)
-            self.perm_loc = perm
+            self.perm_loc = None
             self.to_owner, self.from_touchers = {}, {}
             return
+        perm = np.asarray(plan.iface_perm_host, dtype=np.int64)  # local B dof -> global interface id
         owner, q_of, glob_of_node, rank_of = interface_owner_rank(plan, size)
         touched = np.unique(perm)
         own = touched[owner[touched] == rank]
@@ -347,7 +348,6 @@ class InterfaceLayout:
                 q = own[has[g]]
                 if q.size:
                     self.from_touchers[s] = loc_of[q]
-        self._dev = None
 
     # -- device index arrays -------------------------------------------------
     def _device(self):

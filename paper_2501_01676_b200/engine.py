@@ -175,9 +175,12 @@ class LocalSystem:
             lib.bddc_schur_eliminate(*args)
         self.K = K
         self.S = torch.empty(p.S_total, dtype=F64, device="cuda")
-        self.Bsym = torch.empty(p.S_total, dtype=F64, device="cuda")
+        # Bsym = sym(S) is written straight into the buffer Bsym^-1 is computed in
+        # (in place); nothing else keeps a dense Bsym (slot_bsym / the API views
+        # symmetrise S blocks on the fly)
+        self._W = torch.empty(p.S_total, dtype=F64, device="cuda")
         self.g = torch.empty(int(p.voff[-1]), dtype=F64, device="cuda")
-        lib.bddc_extract_schur(K, d.off, d.ld, d.nI, d.nB, d.soff, d.voff, self.S, self.Bsym,
+        lib.bddc_extract_schur(K, d.off, d.ld, d.nI, d.nB, d.soff, d.voff, self.S, self._W,
                                self.g, p.N, st)
         if ebad is not None and int(ebad.item()) != -1:
             raise ValueError("mesh contains degenerate or inverted elements")
@@ -189,7 +192,7 @@ class LocalSystem:
         """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check."""
         if self._Binv is None:
             p, d, st = self.plan, self.d, stream()
-            Binv = self.Bsym.clone()
+            Binv, self._W = self._W, None  # holds Bsym; inverted in place
             status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
             pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
             # Bsym is exactly symmetric (extract_schur): symmetric GJ in 128-wide panels,
@@ -207,7 +210,8 @@ class LocalSystem:
             bad = _first_bad(status)
             self._frob = f.cpu().numpy()
             if bad is not None:
-                B = self.matrix(self.Bsym, bad)
+                S = self.matrix(self.S, bad)
+                B = 0.5 * (S + S.T)
                 raise NumericalError(f"Bsym of subdomain {bad + self.s0} is not positive definite "
                                      f"(cond ~ {np.linalg.cond(B):.2e})")
             self._Binv = Binv
@@ -216,14 +220,24 @@ class LocalSystem:
     def slot_sizes(self):
         return self.plan.gsize[self.plan.slot_glob].astype(np.int64) ** 2
 
-    def _slot_blocks(self, src):
-        """Slot blocks [g, g] of `src` for every local slot; on the sharded path
-        the cross-rank slots of locally owned globs arrive from their sharers'
-        ranks (dist.SlotExchange, point to point)."""
+    @property
+    def Bsym(self):
+        """Dense Bsym = sym(S) of every subdomain (formed on demand)."""
+        if self._W is not None:
+            return self._W
+        p, d = self.plan, self.d
+        out = self.S.clone()
+        lib.bddc_symmetrize(out, d.soff, d.nB, p.N, stream())
+        return out
+
+    def _slot_blocks(self, src, sym=0):
+        """Slot blocks [g, g] of `src` (sym = 1: of sym(src)) for every local
+        slot; on the sharded path the cross-rank slots of locally owned globs
+        arrive from their sharers' ranks (dist.SlotExchange, point to point)."""
         p, d = self.plan, self.d
         out = torch.zeros(max(p.d_total, 1), dtype=F64, device="cuda")
         lib.bddc_extract_slot_blocks(d.slot_local, d.slot_glob, d.gsize, d.sh_boff, d.sh_doff,
-                                     d.nB, d.soff, src, None, out, None, int(p.sh_sub.size),
+                                     d.nB, d.soff, src, None, out, None, int(p.sh_sub.size), sym,
                                      stream())
         if self.slotx is not None:
             self.slotx.run(out, p.sh_doff, self.slot_sizes(), "to_owner")
@@ -232,7 +246,7 @@ class LocalSystem:
     def slot_bsym(self):
         """Bsym[g, g] of every (glob, sharer) slot, all ranks' (sh_doff layout)."""
         if self._BsC is None:
-            self._BsC = self._slot_blocks(self.Bsym)
+            self._BsC = self._slot_blocks(self.S, sym=1)
         return self._BsC
 
     def slot_binv(self):
@@ -1271,10 +1285,10 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     step (the reference's gelsd, solver.py:297) is the equivalent Givens QR
     recurrence on the device (bddc_gmres_givens); the true residual uses the
     stored S_hat V_j columns (no extra operator application).  The host
-    decision whether to stop after step j is taken while step j + 1 already
-    runs (its residual scalars come back through a pinned buffer and an
-    event), so the GPU never idles on the host; the one speculative step
-    after convergence is discarded."""
+    decision whether to stop after step j is taken while the S_hat
+    application of step j + 1 already runs (the residual scalars come back
+    through a pinned buffer and an event), so the GPU does not idle on the
+    host; that one S_hat application is discarded after the last step."""
     st = stream()
     n = rhs.shape[0]
     nblk = 296
@@ -1322,6 +1336,11 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
         m = j + 1
         U.ensure(m)
         operator.apply_device(V[j], out=U[j])
+        # decide on step j - 1 while this S_hat application runs (it is the only
+        # work wasted when step j - 1 turns out to be the last)
+        if j >= 1 and finished(j - 1):
+            it = j
+            break
         pc.apply_device(U[j], out=w)
         dots.mdot(V.buf, m, w, h1)
         lib.bddc_multi_axpy(V.buf, n, m, h1, -1.0, w, st)
@@ -1340,9 +1359,6 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
         dots.norm(r, tres[j:])
         V.ensure(j + 2)
         lib.bddc_scale_copy(w, n, scal[m:], V[j + 1], st)
-        if j >= 1 and finished(j - 1):
-            it = j
-            break
     else:
         finished(max_iter - 1)
         it = max_iter

@@ -58,7 +58,8 @@ class SubdomainOperator:
 
     @property
     def Bsym(self):
-        return self._nodal(self.ls.Bsym)
+        S = self.S
+        return 0.5 * (S + S.T)
 
     @property
     def Zskew(self):
