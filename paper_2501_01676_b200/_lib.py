@@ -83,9 +83,39 @@ def _conv(a):
     return a
 
 
+# Optional per-entry-point GPU time profile (tools/kernel_profile.py): CUDA
+# events around every C-ABI call on the current stream, summed by name.
+_PROFILE = {"on": False, "events": []}
+
+
+def profile(enable=True):
+    _PROFILE["on"] = bool(enable)
+    _PROFILE["events"] = []
+
+
+def profile_report():
+    """{name: (calls, ms)} of the calls recorded since profile(True)."""
+    out = {}
+    evs = _PROFILE["events"]
+    if evs:
+        evs[-1][2].synchronize()
+    for name, e0, e1 in evs:
+        c, t = out.get(name, (0, 0.0))
+        out[name] = (c + 1, t + e0.elapsed_time(e1))
+    return out
+
+
 def _checked(name, fn):
     def call(*args):
-        rc = fn(*[_conv(a) for a in args])
+        if _PROFILE["on"] and not name.startswith(("bddc_ws_", "bddc_launch")):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rc = fn(*[_conv(a) for a in args])
+            e1.record()
+            _PROFILE["events"].append((name, e0, e1))
+        else:
+            rc = fn(*[_conv(a) for a in args])
         if isinstance(rc, int) and not name.startswith(("bddc_ws_", "bddc_launch")) and rc < 0:
             raise RuntimeError(f"{name}: CUDA launch failed ({torch.cuda.get_device_name()} "
                                f"error {-rc})")
