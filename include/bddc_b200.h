@@ -55,13 +55,17 @@ int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_e
 /* Dense local matrix [I|B] x [I|B|f] from element blocks with Dirichlet lifting;
  * writes every entry of each nloc[b] x ld[b] matrix (no memset needed) in a fixed
  * summation order (no atomics: bitwise reproducible).  lists: workspace of
- * 4 * elem_start[nbatch] ints (per-row corner lists); max_nl = max nloc.
+ * 4 * elem_start[nbatch] ints (per-row corner lists; 4 x n_elements < 2^31);
+ * max_nl = max nloc.  general = 0: compact row lists (<= 20 distinct columns
+ * per row); a row with more sets *overflow (device int, zeroed by the caller)
+ * and the call must be repeated with general = 1 (dense row buffers, any
+ * mesh).  Both give bitwise identical matrices.
  * replaces substructuring.py:98-114 (COO->CSR assembly, load, lifting). */
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
                         const long long* elem_start, const long long* elem_ids, const int* loc4,
                         const long long* conn, const double* Ke, const double* Fe,
-                        const double* gdir, int nbatch, int max_nl, int* lists,
-                        cudaStream_t stream);
+                        const double* gdir, int nbatch, int max_nl, int* lists, int* overflow,
+                        int general, cudaStream_t stream);
 
 /* Blocked Schur elimination without pivoting (panel 64 or 128 = two 64-wide
  * sub-panels combined so the DMMA trailing update runs with K = 128):

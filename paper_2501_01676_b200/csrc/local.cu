@@ -34,6 +34,7 @@ namespace bddc {
 //     lifting, padding), so K needs no memset.
 // ---------------------------------------------------------------------------
 constexpr int kAsmWarps = 8;
+constexpr int kAsmSlots = 20;  // distinct columns per row in the compact row phase
 
 BDDC_DEV int block_excl_scan_ints(int* a, int n, int* red) {
   // in-place exclusive scan of a[0..n) by the whole CTA; returns the total.
@@ -79,18 +80,20 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
     const long long* __restrict__ elem_ids, const int* __restrict__ loc4,
     const long long* __restrict__ conn, const double* __restrict__ Ke,
     const double* __restrict__ Fe, const double* __restrict__ gdir, int* __restrict__ lists,
-    int nrowbuf) {
+    int nrowbuf, int* __restrict__ overflow, int region0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b = blockIdx.x;
   const int nL = nloc[b], L = ld[b];
   const long long e0 = elem_start[b], e1 = elem_start[b + 1];
   const long long nc = 4 * (e1 - e0);
   const int stride = nL + 1;
-  int* hist = reinterpret_cast<int*>(smem_raw);  // kAsmWarps x (nL + 1): counts, then cursors
-  int* rowptr = hist + kAsmWarps * stride;        // nL + 1
-  int* red = rowptr + stride;                     // kAsmWarps + 1
+  // [region0: warp histograms (counts, then cursors); reused by the compact row
+  //  lists] [rowptr nL + 1] [red kAsmWarps + 1] [row buffers]
+  int* hist = reinterpret_cast<int*>(smem_raw);
+  int* rowptr = reinterpret_cast<int*>(smem_raw + region0);
+  int* red = rowptr + stride;
   double* rowbuf = reinterpret_cast<double*>(
-      smem_raw + ((((size_t)(kAsmWarps * stride + stride + kAsmWarps + 1)) * 4 + 15) & ~(size_t)15));
+      smem_raw + region0 + ((((size_t)(stride + kAsmWarps + 1)) * 4 + 15) & ~(size_t)15));
   int* lst = lists + 4 * e0;
   const long long* eid = elem_ids + e0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -139,12 +142,70 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
     __syncwarp();
     if (r >= 0 && rank == 0) h[r] = pos + __popc(m);
     __syncwarp();
-    if (r >= 0) lst[pos + rank] = (int)j;
+    if (r >= 0) lst[pos + rank] = (int)(eid[j >> 2] * 4 + (j & 3));  // global corner id
   }
   __syncthreads();
+  double* M = base + off[b];
+  if (nrowbuf == 0) {
+    // compact row phase: lane owns a row, keeps its (column, value) pairs in a
+    // short shared-memory list (Kuhn meshes: <= 15 columns per row), then the
+    // warp zero-fills its 32 rows with coalesced stores and every lane writes
+    // its row's nonzeros.  Same summation order as the row-buffer phase below.
+    double* lval = reinterpret_cast<double*>(hist) + (size_t)warp * 32 * kAsmSlots;
+    int* lcol = reinterpret_cast<int*>(reinterpret_cast<double*>(hist) + kAsmWarps * 32 * kAsmSlots) +
+                (size_t)warp * 32 * kAsmSlots;
+    int ovf = 0;
+    for (int rb = warp * 32; rb < nL; rb += kAsmWarps * 32) {
+      const int r = rb + lane;
+      int cnt = 0;
+      double fload = 0.0;
+      if (r < nL) {
+        for (int s = rowptr[r]; s < rowptr[r + 1]; ++s) {
+          const int gc = lst[s];
+          const long long e = gc >> 2;
+          const int a = gc & 3;
+          double fr = Fe[gc];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double v = Ke[e * 16 + a * 4 + c];
+            const int li = loc4[e * 4 + c];
+            if (li < nL) {
+              int t = 0;
+              while (t < cnt && lcol[t * 32 + lane] != li) ++t;
+              if (t < cnt) {
+                lval[t * 32 + lane] += v;
+              } else if (cnt < kAsmSlots) {
+                lcol[cnt * 32 + lane] = li;
+                lval[cnt * 32 + lane] = v;
+                ++cnt;
+              } else {
+                ovf = 1;
+              }
+            } else {
+              fr -= v * gdir[conn[e * 4 + c]];
+            }
+          }
+          fload += fr;
+        }
+      }
+      const int nrows = min(32, nL - rb);
+      for (int q = 0; q < nrows; ++q) {
+        double* row = M + (long long)(rb + q) * L;
+        for (int c = lane; c < L; c += 32) row[c] = 0.0;
+      }
+      __syncwarp();
+      if (r < nL) {
+        double* row = M + (long long)r * L;
+        for (int t = 0; t < cnt; ++t) row[lcol[t * 32 + lane]] = lval[t * 32 + lane];
+        row[nL] = fload;
+      }
+      __syncwarp();
+    }
+    if (ovf && overflow) atomicExch(overflow, 1);
+    return;
+  }
   if (warp >= nrowbuf) return;
   double* rb = rowbuf + (size_t)warp * L;
-  double* M = base + off[b];
   const int nwr = min(nrowbuf, kAsmWarps);
   for (int r = warp; r < nL; r += nwr) {
     for (int c = lane; c < L; c += 32) rb[c] = 0.0;
@@ -156,10 +217,10 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
       double val[4] = {0.0, 0.0, 0.0, 0.0};
       double fr = 0.0;
       if (s < s1) {
-        const int j = lst[s];
-        const long long e = eid[j >> 2];
-        const int a = j & 3;
-        fr = Fe[e * 4 + a];
+        const int gc = lst[s];
+        const long long e = gc >> 2;
+        const int a = gc & 3;
+        fr = Fe[gc];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const double v = Ke[e * 16 + a * 4 + c];
@@ -189,9 +250,19 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
   }
 }
 
+static size_t assemble_region0(int max_nl, int nrowbuf) {
+  size_t hist_bytes = (size_t)kAsmWarps * (max_nl + 1) * 4;
+  if (nrowbuf == 0) {  // compact phase reuses the histogram region for the row lists
+    const size_t lists = (size_t)kAsmWarps * 32 * kAsmSlots * 12;
+    hist_bytes = hist_bytes > lists ? hist_bytes : lists;
+  }
+  return (hist_bytes + 15) & ~(size_t)15;
+}
+
 static size_t assemble_smem_bytes(int max_nl, int nrowbuf) {
-  const size_t ints = (size_t)kAsmWarps * (max_nl + 1) + (max_nl + 1) + kAsmWarps + 1;
-  return ((ints * 4 + 15) & ~(size_t)15) + (size_t)nrowbuf * (max_nl + 2) * 8;
+  const size_t ints = (max_nl + 1) + kAsmWarps + 1;
+  return assemble_region0(max_nl, nrowbuf) + ((ints * 4 + 15) & ~(size_t)15) +
+         (size_t)nrowbuf * (max_nl + 2) * 8;
 }
 
 // ---------------------------------------------------------------------------
@@ -725,16 +796,20 @@ int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_e
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
                         const long long* elem_start, const long long* elem_ids, const int* loc4,
                         const long long* conn, const double* Ke, const double* Fe,
-                        const double* gdir, int nbatch, int max_nl, int* lists,
-                        cudaStream_t stream) {
+                        const double* gdir, int nbatch, int max_nl, int* lists, int* overflow,
+                        int general, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  int nrowbuf = kAsmWarps;
-  while (nrowbuf > 1 && assemble_smem_bytes(max_nl, nrowbuf) > 200 * 1024) --nrowbuf;
+  int nrowbuf = 0;  // compact row phase
+  if (general) {
+    nrowbuf = kAsmWarps;
+    while (nrowbuf > 1 && assemble_smem_bytes(max_nl, nrowbuf) > 200 * 1024) --nrowbuf;
+  }
   const size_t smem = assemble_smem_bytes(max_nl, nrowbuf);
   if (smem > 227 * 1024) return -(int)cudaErrorInvalidValue;
   cudaFuncSetAttribute(assemble_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   assemble_rows_kernel<<<nbatch, kAsmWarps * 32, smem, stream>>>(
-      K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke, Fe, gdir, lists, nrowbuf);
+      K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke, Fe, gdir, lists, nrowbuf, overflow,
+      (int)assemble_region0(max_nl, nrowbuf));
   bddc_note_launches(1);
   return launch_status();
 }

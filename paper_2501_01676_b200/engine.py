@@ -101,6 +101,8 @@ class LocalSystem:
     Replaces build_subdomain_operator x N (reference substructuring.py:78-143)
     and SubdomainOperator.bsym_inverse (substructuring.py:64-75)."""
 
+    general_assembly = False  # True: always the row-buffer assembly (tests)
+
     def __init__(self, system, partition, globs, plan=None, inputs=None, timer=None,
                  kernel_timing=False, dplan=None, comm=None):
         require_cuda()
@@ -156,13 +158,33 @@ class LocalSystem:
         Ke, Fe, ebad = self.inputs.get("Ke"), self.inputs.get("Fe"), self.inputs.get("_ebad")
         if Ke is None:  # element blocks built on the device from mesh + coefficients
             Ke, Fe, ebad = device_element_blocks(self.inputs)
+        n_el = int(self.inputs["conn"].shape[0])
+        if 4 * n_el >= 2 ** 31:
+            raise ValueError(f"{n_el} elements: corner ids exceed the 32-bit assembly lists")
         lists = torch.empty(max(4 * int(p.elem_start[-1]), 1), dtype=torch.int32, device="cuda")
-        lib.bddc_local_assemble(K, d.off, d.ld, d.nL, d.elem_start, d.elem_ids, d.loc4,
-                                self.inputs["conn"], Ke, Fe, self.inputs["gdir"], p.N,
-                                int(p.nL.max()), lists, st)
-        del Ke, Fe, lists
+        ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
+        asm_args = (K, d.off, d.ld, d.nL, d.elem_start, d.elem_ids, d.loc4, self.inputs["conn"],
+                    Ke, Fe, self.inputs["gdir"], p.N, int(p.nL.max()), lists, ovf)
+        lib.bddc_local_assemble(*asm_args, int(self.general_assembly), st)
         # the element blocks are consumed: keep only the index inputs
         self.inputs = {k: v for k, v in self.inputs.items() if k not in ("Ke", "Fe", "_ebad")}
+        status = self._eliminate(K)
+        if int(ovf.item()):
+            # a row with more than 20 distinct columns (not a Kuhn box mesh):
+            # general row-buffer assembly, then the elimination again
+            lib.bddc_local_assemble(*asm_args, 1, st)
+            status = self._eliminate(K)
+        del asm_args, lists
+        if ebad is not None and int(ebad.item()) != -1:
+            raise ValueError("mesh contains degenerate or inverted elements")
+        bad = _first_bad(status)
+        if bad is not None:
+            raise NumericalError(f"interior block of subdomain {bad + self.s0} is singular")
+
+    def _eliminate(self, K):
+        """Blocked Schur elimination of the assembled local matrices and the
+        extraction of S, Bsym and g; returns the per-subdomain status."""
+        p, d, st = self.plan, self.d, stream()
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
         args = (K, d.off, d.ld, d.nI, d.nL, d.nL1, p.N, int(p.nI.max()), int(p.nL.max()),
@@ -182,11 +204,7 @@ class LocalSystem:
         self.g = torch.empty(int(p.voff[-1]), dtype=F64, device="cuda")
         lib.bddc_extract_schur(K, d.off, d.ld, d.nI, d.nB, d.soff, d.voff, self.S, self._W,
                                self.g, p.N, st)
-        if ebad is not None and int(ebad.item()) != -1:
-            raise ValueError("mesh contains degenerate or inverted elements")
-        bad = _first_bad(status)
-        if bad is not None:
-            raise NumericalError(f"interior block of subdomain {bad + self.s0} is singular")
+        return status
 
     def bsym_inverse(self):
         """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check."""
