@@ -55,8 +55,9 @@ int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_e
 /* Dense local matrix [I|B] x [I|B|f] from element blocks with Dirichlet lifting;
  * writes every entry of each nloc[b] x ld[b] matrix (no memset needed) in a fixed
  * summation order (no atomics: bitwise reproducible).  lists: workspace of
- * 4 * elem_start[nbatch] ints (per-row corner lists; 4 x n_elements < 2^31);
- * max_nl = max nloc.  general = 0: compact row lists (<= 20 distinct columns
+ * 4 * elem_start[nbatch] ints (per-row corner lists; 4 x n_elements < 2^31),
+ * keys: 4 * elem_start[nbatch] long longs of scratch; max_nl = max nloc.
+ * general = 0: compact row lists (<= 16 distinct columns
  * per row); a row with more sets *overflow (device int, zeroed by the caller)
  * and the call must be repeated with general = 1 (dense row buffers, any
  * mesh).  Both give bitwise identical matrices.
@@ -64,8 +65,8 @@ int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_e
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
                         const long long* elem_start, const long long* elem_ids, const int* loc4,
                         const long long* conn, const double* Ke, const double* Fe,
-                        const double* gdir, int nbatch, int max_nl, int* lists, int* overflow,
-                        int general, cudaStream_t stream);
+                        const double* gdir, int nbatch, int max_nl, int* lists, long long* keys,
+                        int* overflow, int general, cudaStream_t stream);
 
 /* Blocked Schur elimination without pivoting (panel 64 or 128 = two 64-wide
  * sub-panels combined so the DMMA trailing update runs with K = 128):
@@ -370,19 +371,21 @@ int bddc_pc_local_solve(const int* nB, const long long* soff, const long long* v
                         const int* pstart, const long long* poff, const double* G, double* cvals,
                         int nbatch, int max_nB, cudaStream_t stream);
 
-/* Householder-path fusion of the S-bar transform and the dual embedding, one
- * CTA per (glob slot, subdomain): Sbar = Q S Q^T (reflectors HV, r), then Z =
- * embedded dual block (identity on primal rows / columns), Srows[q] =
- * Sbar[ppos_q, :] and Scols[q] = Sbar[:, ppos_q] (n_p x nB at poff); pidx: per
- * local B position its primal index or -1.  max_rows_block: largest glob size;
- * blocks up to 200 KB are staged in shared memory.  replaces solver.py:85-99. */
+/* Householder-path fusion of the S-bar transform and the dual embedding:
+ * Sbar = Q S Q^T (reflectors HV, r per glob), Z = embedded dual block
+ * (identity on primal rows / columns), Srows[q] = Sbar[ppos_q, :] and
+ * Scols[q] = Sbar[:, ppos_q] (n_p x nB at poff); pidx: per local B position its
+ * primal index or -1.  Left reflectors: one CTA per listed glob block
+ * (left_k[i] into sub_globs, subdomain left_sub[i]); right reflectors and the
+ * outputs: one warp per row, applying only the subdomain's reflected globs
+ * refl_k[refl_start[b] .. refl_start[b + 1]).  replaces solver.py:85-99. */
 int bddc_pc_transform_embed(const int* nB, const long long* soff, const long long* voff,
-                            const int* sub_glob_start, const int* sub_globs,
-                            const int* sub_glob_boff, const int* kind, const int* gsize,
-                            const int* r, const double* HV, const long long* q_off,
-                            const int* pidx, const long long* poff, const double* S, double* Z,
-                            double* Srows, double* Scols, int nbatch, int max_globs,
-                            int max_rows_block, int max_nB, cudaStream_t stream);
+                            const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+                            const int* kind, const int* gsize, const int* r, const double* HV,
+                            const long long* q_off, const int* refl_start, const int* refl_k,
+                            const int* left_k, const int* left_sub, int n_left, const int* pidx,
+                            const long long* poff, const double* S, double* Z, double* Srows,
+                            double* Scols, int nbatch, int max_nB, cudaStream_t stream);
 
 /* Srows / Scols (as above) from a full Sbar (dense-Q path). */
 int bddc_pc_primal_extract(const int* nB, const long long* soff, const long long* voff,

@@ -34,7 +34,7 @@ namespace bddc {
 //     lifting, padding), so K needs no memset.
 // ---------------------------------------------------------------------------
 constexpr int kAsmWarps = 8;
-constexpr int kAsmSlots = 20;  // distinct columns per row in the compact row phase
+constexpr int kAsmSlots = 16;  // distinct columns per row in the compact row phase (Kuhn: 15)
 
 BDDC_DEV int block_excl_scan_ints(int* a, int n, int* red) {
   // in-place exclusive scan of a[0..n) by the whole CTA; returns the total.
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
     const long long* __restrict__ elem_ids, const int* __restrict__ loc4,
     const long long* __restrict__ conn, const double* __restrict__ Ke,
     const double* __restrict__ Fe, const double* __restrict__ gdir, int* __restrict__ lists,
-    int nrowbuf, int* __restrict__ overflow, int region0) {
+    long long* __restrict__ keys, int nrowbuf, int* __restrict__ overflow, int region0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b = blockIdx.x;
   const int nL = nloc[b], L = ld[b];
@@ -103,8 +103,13 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
   const long long chunk = (nc + kAsmWarps - 1) / kAsmWarps;
   const long long c0 = min(nc, (long long)warp * chunk), c1 = min(nc, c0 + chunk);
   int* h = hist + warp * stride;
+  long long* kp = keys + 4 * e0;
+  // pass 1: (row, global corner id) of every corner into keys, per-warp row counts
+#pragma unroll 4
   for (long long j = c0 + lane; j < c1; j += 32) {
-    const int r = loc4[eid[j >> 2] * 4 + (j & 3)];
+    const long long gc = eid[j >> 2] * 4 + (j & 3);
+    const int r = loc4[gc];
+    kp[j] = r < nL ? ((long long)r << 32) | gc : -1;
     if (r < nL) atomicAdd(h + r, 1);  // integer counts: order-independent
   }
   __syncthreads();
@@ -130,11 +135,8 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
   // stable placement, 32 corners at a time in order
   for (long long jb = c0; jb < c1; jb += 32) {
     const long long j = jb + lane;
-    int r = -1;
-    if (j < c1) {
-      r = loc4[eid[j >> 2] * 4 + (j & 3)];
-      if (r >= nL) r = -1;
-    }
+    const long long key = j < c1 ? kp[j] : -1;
+    const int r = key < 0 ? -1 : (int)(key >> 32);
     const unsigned m = __match_any_sync(0xffffffffu, r);
     const int rank = __popc(m & ((1u << lane) - 1u));
     int pos = 0;
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
     __syncwarp();
     if (r >= 0 && rank == 0) h[r] = pos + __popc(m);
     __syncwarp();
-    if (r >= 0) lst[pos + rank] = (int)(eid[j >> 2] * 4 + (j & 3));  // global corner id
+    if (r >= 0) lst[pos + rank] = (int)(key & 0xffffffffll);  // global corner id
   }
   __syncthreads();
   double* M = base + off[b];
@@ -160,15 +162,25 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
       int cnt = 0;
       double fload = 0.0;
       if (r < nL) {
-        for (int s = rowptr[r]; s < rowptr[r + 1]; ++s) {
-          const int gc = lst[s];
+        const int s1 = rowptr[r + 1];
+        int gnext = rowptr[r] < s1 ? lst[rowptr[r]] : 0;
+        for (int s = rowptr[r]; s < s1; ++s) {
+          const int gc = gnext;
+          if (s + 1 < s1) gnext = lst[s + 1];  // next corner's id in flight
           const long long e = gc >> 2;
           const int a = gc & 3;
           double fr = Fe[gc];
+          double kv[4];
+          int kl[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const double v = Ke[e * 16 + a * 4 + c];
-            const int li = loc4[e * 4 + c];
+            kv[c] = Ke[e * 16 + a * 4 + c];
+            kl[c] = loc4[e * 4 + c];
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const double v = kv[c];
+            const int li = kl[c];
             if (li < nL) {
               int t = 0;
               while (t < cnt && lcol[t * 32 + lane] != li) ++t;
@@ -796,8 +808,8 @@ int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_e
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
                         const long long* elem_start, const long long* elem_ids, const int* loc4,
                         const long long* conn, const double* Ke, const double* Fe,
-                        const double* gdir, int nbatch, int max_nl, int* lists, int* overflow,
-                        int general, cudaStream_t stream) {
+                        const double* gdir, int nbatch, int max_nl, int* lists, long long* keys,
+                        int* overflow, int general, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   int nrowbuf = 0;  // compact row phase
   if (general) {
@@ -808,8 +820,8 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
   if (smem > 227 * 1024) return -(int)cudaErrorInvalidValue;
   cudaFuncSetAttribute(assemble_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   assemble_rows_kernel<<<nbatch, kAsmWarps * 32, smem, stream>>>(
-      K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke, Fe, gdir, lists, nrowbuf, overflow,
-      (int)assemble_region0(max_nl, nrowbuf));
+      K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke, Fe, gdir, lists, keys, nrowbuf,
+      overflow, (int)assemble_region0(max_nl, nrowbuf));
   bddc_note_launches(1);
   return launch_status();
 }

@@ -328,39 +328,31 @@ __global__ void __launch_bounds__(256) transform_refl_kernel(
 }
 
 
-// Sbar = Q S Q^T (Householder Q), then in the same pass: the compact primal
-// rows / columns of Sbar (Srows[q] = Sbar[ppos_q, :], Scols[q] = Sbar[:, ppos_q],
-// n_p x n at poff) and the embedded dual block Z (identity on primal rows and
-// columns, Sbar elsewhere) -- the inputs of the dual LU and the primal pieces.
-// CTA (k, b): glob slot k of subdomain b = rows [bo, bo + ng), staged in shared
-// memory (SMEM) or worked on in place in Z's rows.
-template <bool SMEM>
-__global__ void __launch_bounds__(256) transform_embed_kernel(
+// Sbar = Q S Q^T with Q in Householder form (reflectors HV, r per glob), the
+// compact primal rows / columns of Sbar and the embedded dual block Z
+// (identity on primal rows and columns) -- the inputs of the dual LU and the
+// primal pieces:
+//  left pass, one CTA per glob block that has reflectors: X = Q_g S[rows of g]
+//  written into Z's rows (thread per column);
+//  row pass, one warp per row of every subdomain: the row (from Z for rows of
+//  reflected globs, else from S) is staged in shared memory, the right
+//  reflectors of the subdomain's reflected globs only (refl_start / refl_k) are
+//  applied, then the compact primal row / column entries and the embedded dual
+//  block row are written.
+__global__ void __launch_bounds__(256) transform_left_kernel(
     const int* __restrict__ nB, const long long* __restrict__ soff,
-    const long long* __restrict__ voff, const int* __restrict__ sub_glob_start,
+    const int* __restrict__ item_k, const int* __restrict__ item_sub,
     const int* __restrict__ sub_globs, const int* __restrict__ sub_glob_boff,
-    const int* __restrict__ kind, const int* __restrict__ gsize, const int* __restrict__ r,
-    const double* __restrict__ HV, const long long* __restrict__ q_off,
-    const int* __restrict__ pidx, const long long* __restrict__ poff,
-    const double* __restrict__ S, double* __restrict__ Z, double* __restrict__ Srows,
-    double* __restrict__ Scols) {
-  extern __shared__ double xs[];
-  const int b = blockIdx.y;
-  const int kk = sub_glob_start[b] + blockIdx.x;
-  if (kk >= sub_glob_start[b + 1]) return;
+    const int* __restrict__ gsize, const int* __restrict__ r, const double* __restrict__ HV,
+    const long long* __restrict__ q_off, const double* __restrict__ S, double* __restrict__ Z) {
+  const int kk = item_k[blockIdx.x], b = item_sub[blockIdx.x];
   const int n = nB[b];
   const int g = sub_globs[kk], ng = gsize[g], bo = sub_glob_boff[kk];
   const double* Sb = S + soff[b] + (long long)bo * n;
-  double* Zb = Z + soff[b] + (long long)bo * n;
-  double* X = SMEM ? xs : Zb;
-  const int nref = (kind[g] == 2 || ng == 1) ? 0 : min(r[g], ng);
+  double* X = Z + soff[b] + (long long)bo * n;
+  const int nref = min(r[g], ng);
   const double* Hg = HV + q_off[g];
-  // left: X = Q_g S[rows of g]   (thread per column)
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    if (nref == 0) {
-      for (int i = 0; i < ng; ++i) X[(long long)i * n + c] = Sb[(long long)i * n + c];
-      continue;
-    }
     for (int j = 0; j < nref; ++j) {
       const double* src = j == 0 ? Sb : X;
       const double* w = Hg + j * ng;
@@ -370,40 +362,56 @@ __global__ void __launch_bounds__(256) transform_embed_kernel(
         X[(long long)i * n + c] = src[(long long)i * n + c] - (i < j ? 0.0 : d * w[i]);
     }
   }
-  __syncthreads();
-  // right: X <- X Q^T on every glob column block (warp per row), then the
-  // finished row goes out: compact primal row / column entries and the
-  // embedded dual block (identity on primal rows / columns)
+}
+
+__global__ void __launch_bounds__(256) transform_rows_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ soff,
+    const long long* __restrict__ voff, const int* __restrict__ pos2k,
+    const int* __restrict__ sub_globs, const int* __restrict__ sub_glob_boff,
+    const int* __restrict__ kind, const int* __restrict__ gsize, const int* __restrict__ r,
+    const double* __restrict__ HV, const long long* __restrict__ q_off,
+    const int* __restrict__ refl_start, const int* __restrict__ refl_k,
+    const int* __restrict__ pidx, const long long* __restrict__ poff,
+    const double* __restrict__ S, double* __restrict__ Z, double* __restrict__ Srows,
+    double* __restrict__ Scols, int max_nB) {
+  extern __shared__ double rowsm[];
+  const int b = blockIdx.y;
+  const int n = nB[b];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int k0 = sub_glob_start[b], k1 = sub_glob_start[b + 1];
+  const int rho = blockIdx.x * nw + warp;
+  if (rho >= n) return;
+  double* xr = rowsm + (size_t)warp * max_nB;
+  const int k = pos2k[voff[b] + rho];
+  const int g = sub_globs[k];
+  const bool left = !(kind[g] == 2 || gsize[g] == 1) && r[g] > 0;
+  const double* src = (left ? Z : S) + soff[b] + (long long)rho * n;
+  for (int c = lane; c < n; c += 32) xr[c] = src[c];
+  __syncwarp();
+  for (int q = refl_start[b]; q < refl_start[b + 1]; ++q) {
+    const int k2 = refl_k[q];
+    const int h = sub_globs[k2], nh = gsize[h], bh = sub_glob_boff[k2];
+    const int nrh = min(r[h], nh);
+    const double* Hh = HV + q_off[h];
+    for (int j = 0; j < nrh; ++j) {
+      const double* w = Hh + j * nh;
+      double d = 0.0;
+      for (int i = j + lane; i < nh; i += 32) d += xr[bh + i] * w[i];
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+      for (int i = j + lane; i < nh; i += 32) xr[bh + i] -= d * w[i];
+      __syncwarp();
+    }
+  }
   const int* pi = pidx + voff[b];
+  const int qr = pi[rho];
   double* Sr = Srows + poff[b];
   double* Sc = Scols + poff[b];
-  for (int row = warp; row < ng; row += nw) {
-    double* xr = X + (long long)row * n;
-    for (int k = k0; k < k1; ++k) {
-      const int h = sub_globs[k], nh = gsize[h], bh = sub_glob_boff[k];
-      const int nrh = (kind[h] == 2 || nh == 1) ? 0 : min(r[h], nh);
-      const double* Hh = HV + q_off[h];
-      for (int j = 0; j < nrh; ++j) {
-        const double* w = Hh + j * nh;
-        double d = 0.0;
-        for (int i = j + lane; i < nh; i += 32) d += xr[bh + i] * w[i];
-        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        for (int i = j + lane; i < nh; i += 32) xr[bh + i] -= d * w[i];
-        __syncwarp();
-      }
-    }
-    const int rho = bo + row;
-    const int qr = pi[rho];
-    double* zr = Zb + (long long)row * n;
-    for (int c = lane; c < n; c += 32) {
-      const double v = xr[c];
-      const int qc = pi[c];
-      if (qr >= 0) Sr[(long long)qr * n + c] = v;
-      if (qc >= 0) Sc[(long long)qc * n + rho] = v;
-      zr[c] = (qr >= 0 || qc >= 0) ? (rho == c ? 1.0 : 0.0) : v;
-    }
+  double* zr = Z + soff[b] + (long long)rho * n;
+  for (int c = lane; c < n; c += 32) {
+    const double v = xr[c];
+    const int qc = pi[c];
+    if (qr >= 0) Sr[(long long)qr * n + c] = v;
+    if (qc >= 0) Sc[(long long)qc * n + rho] = v;
+    zr[c] = (qr >= 0 || qc >= 0) ? (rho == c ? 1.0 : 0.0) : v;
   }
 }
 
@@ -1340,29 +1348,24 @@ int bddc_pc_local_solve(const int* nB, const long long* soff, const long long* v
 }
 
 int bddc_pc_transform_embed(const int* nB, const long long* soff, const long long* voff,
-                            const int* sub_glob_start, const int* sub_globs,
-                            const int* sub_glob_boff, const int* kind, const int* gsize,
-                            const int* r, const double* HV, const long long* q_off,
-                            const int* pidx, const long long* poff, const double* S, double* Z,
-                            double* Srows, double* Scols, int nbatch, int max_globs,
-                            int max_rows_block, int max_nB, cudaStream_t stream) {
+                            const int* pos2k, const int* sub_globs, const int* sub_glob_boff,
+                            const int* kind, const int* gsize, const int* r, const double* HV,
+                            const long long* q_off, const int* refl_start, const int* refl_k,
+                            const int* left_k, const int* left_sub, int n_left, const int* pidx,
+                            const long long* poff, const double* S, double* Z, double* Srows,
+                            double* Scols, int nbatch, int max_nB, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  const long long bytes = (long long)max_rows_block * max_nB * (long long)sizeof(double);
-  dim3 grid((unsigned)max_globs, (unsigned)nbatch);
-  if (bytes <= 200 * 1024) {
-    static PerDeviceOnce once;
-    once([&] {
-      cudaFuncSetAttribute(transform_embed_kernel<true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    });
-    transform_embed_kernel<true><<<grid, 256, (size_t)bytes, stream>>>(
-        nB, soff, voff, sub_glob_start, sub_globs, sub_glob_boff, kind, gsize, r, HV, q_off, pidx,
-        poff, S, Z, Srows, Scols);
-  } else {
-    transform_embed_kernel<false><<<grid, 256, 0, stream>>>(
-        nB, soff, voff, sub_glob_start, sub_globs, sub_glob_boff, kind, gsize, r, HV, q_off, pidx,
-        poff, S, Z, Srows, Scols);
+  if (n_left > 0) {
+    transform_left_kernel<<<n_left, 256, 0, stream>>>(nB, soff, left_k, left_sub, sub_globs,
+                                                      sub_glob_boff, gsize, r, HV, q_off, S, Z);
+    bddc_note_launches(1);
   }
+  const int smem = 8 * max_nB * (int)sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(transform_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  transform_rows_kernel<<<dim3(ceil_div(max_nB, 8), nbatch), 256, smem, stream>>>(
+      nB, soff, voff, pos2k, sub_globs, sub_glob_boff, kind, gsize, r, HV, q_off, refl_start,
+      refl_k, pidx, poff, S, Z, Srows, Scols, max_nB);
   bddc_note_launches(1);
   return pc_status();
 }

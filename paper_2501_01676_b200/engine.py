@@ -162,19 +162,20 @@ class LocalSystem:
         if 4 * n_el >= 2 ** 31:
             raise ValueError(f"{n_el} elements: corner ids exceed the 32-bit assembly lists")
         lists = torch.empty(max(4 * int(p.elem_start[-1]), 1), dtype=torch.int32, device="cuda")
+        keys = torch.empty(max(4 * int(p.elem_start[-1]), 1), dtype=torch.int64, device="cuda")
         ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
         asm_args = (K, d.off, d.ld, d.nL, d.elem_start, d.elem_ids, d.loc4, self.inputs["conn"],
-                    Ke, Fe, self.inputs["gdir"], p.N, int(p.nL.max()), lists, ovf)
+                    Ke, Fe, self.inputs["gdir"], p.N, int(p.nL.max()), lists, keys, ovf)
         lib.bddc_local_assemble(*asm_args, int(self.general_assembly), st)
         # the element blocks are consumed: keep only the index inputs
         self.inputs = {k: v for k, v in self.inputs.items() if k not in ("Ke", "Fe", "_ebad")}
         status = self._eliminate(K)
         if int(ovf.item()):
-            # a row with more than 20 distinct columns (not a Kuhn box mesh):
+            # a row with more than 16 distinct columns (not a Kuhn box mesh):
             # general row-buffer assembly, then the elimination again
             lib.bddc_local_assemble(*asm_args, 1, st)
             status = self._eliminate(K)
-        del asm_args, lists
+        del asm_args, lists, keys
         if ebad is not None and int(ebad.item()) != -1:
             raise ValueError("mesh contains degenerate or inverted elements")
         bad = _first_bad(status)
@@ -949,11 +950,18 @@ class DevicePreconditioner:
         Scols = torch.empty(npn, dtype=F64, device="cuda")
         Z = torch.empty(p.S_total, dtype=F64, device="cuda")
         if householder:  # Sbar, compact primal rows / columns and Z in one pass
-            lib.bddc_pc_transform_embed(d.nB, d.soff, d.voff, d.sub_glob_start, d.sub_globs,
-                                        d.sub_glob_boff, d.kind, d.gsize, r_d, HV, q_off, d_pidx,
-                                        d_poff_all, ls.S, Z, Srows, Scols, p.N,
-                                        int(np.diff(p.sub_glob_start).max()), 1 << 30,
-                                        int(p.nB.max()), st)
+            # glob blocks with reflectors (left pass) and, per subdomain, the list
+            # of its reflected globs (right pass)
+            gk = p.sub_globs.astype(np.int64)
+            refl = (p.kind[gk] != 2) & (p.gsize[gk] > 1) & (r[gk] > 0)
+            ks = np.flatnonzero(refl)
+            sub_of_k = np.repeat(np.arange(p.N), np.diff(p.sub_glob_start))
+            refl_start = np.searchsorted(ks, p.sub_glob_start.astype(np.int64))
+            lib.bddc_pc_transform_embed(d.nB, d.soff, d.voff, d.pos2k, d.sub_globs,
+                                        d.sub_glob_boff, d.kind, d.gsize, r_d, HV, q_off,
+                                        dev_i32(refl_start), dev_i32(ks), dev_i32(ks),
+                                        dev_i32(sub_of_k[ks]), int(ks.size), d_pidx, d_poff_all,
+                                        ls.S, Z, Srows, Scols, p.N, int(p.nB.max()), st)
             del HV
         else:  # dense block products with the given Q
             Sbar = torch.empty(p.S_total, dtype=F64, device="cuda")
