@@ -70,8 +70,7 @@ def test_reflector_basis_and_transform():
     assert np.abs(a - b).max() <= 1e-12 * np.abs(b).max()
 
 
-@pytest.mark.parametrize("smem", [True, False])
-def test_fused_transform_embed_matches_two_pass(smem):
+def test_fused_transform_embed_matches_two_pass():
     """bddc_pc_transform_embed (Sbar, embedded dual block Z, compact primal
     rows / columns in one pass) equals the two-pass reflector transform +
     dual embedding + extraction."""
@@ -117,14 +116,17 @@ def test_fused_transform_embed_matches_two_pass(smem):
     Sr0, Sc0 = torch.empty(npn, **f64), torch.empty(npn, **f64)
     lib.bddc_pc_primal_extract(d.nB, d.soff, d.voff, dev_i32(pidx), dev_i64(poff[:-1]), Sbar, Sr0,
                                Sc0, p.N, st)
-    # fused (shared-memory staging or in place in Z)
+    # fused: left reflectors per reflected glob block, then the row pass
     Z1 = torch.empty_like(S)
     Sr1, Sc1 = torch.empty(npn, **f64), torch.empty(npn, **f64)
-    rows_block = int(p.gsize.max()) if smem else 10 ** 6  # force the global-memory variant
-    lib.bddc_pc_transform_embed(d.nB, d.soff, d.voff, d.sub_glob_start, d.sub_globs,
-                                d.sub_glob_boff, d.kind, d.gsize, r_d, HV, ps.d_q_off,
+    gk = p.sub_globs.astype(np.int64)
+    ks = np.flatnonzero((p.kind[gk] != 2) & (p.gsize[gk] > 1) & (r[gk] > 0))
+    sub_of_k = np.repeat(np.arange(p.N), np.diff(p.sub_glob_start))
+    refl_start = np.searchsorted(ks, p.sub_glob_start.astype(np.int64))
+    lib.bddc_pc_transform_embed(d.nB, d.soff, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
+                                d.kind, d.gsize, r_d, HV, ps.d_q_off, dev_i32(refl_start),
+                                dev_i32(ks), dev_i32(ks), dev_i32(sub_of_k[ks]), int(ks.size),
                                 dev_i32(pidx), dev_i64(poff[:-1]), S, Z1, Sr1, Sc1, p.N,
-                                int(np.diff(p.sub_glob_start).max()), rows_block,
                                 int(p.nB.max()), st)
     torch.cuda.synchronize()
     for a, b in ((Z1, Z0), (Sr1, Sr0), (Sc1, Sc0)):
