@@ -156,6 +156,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
     double* lval = reinterpret_cast<double*>(hist) + (size_t)warp * 32 * kAsmSlots;
     int* lcol = reinterpret_cast<int*>(reinterpret_cast<double*>(hist) + kAsmWarps * 32 * kAsmSlots) +
                 (size_t)warp * 32 * kAsmSlots;
+    double* rbuf = rowbuf + (size_t)warp * (L + 2);
     int ovf = 0;
     for (int rb = warp * 32; rb < nL; rb += kAsmWarps * 32) {
       const int r = rb + lane;
@@ -200,18 +201,22 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
           fload += fr;
         }
       }
+      // dense rows through the warp's shared-memory row buffer: every row of K
+      // is written once, with full-line (16-byte vector) stores
       const int nrows = min(32, nL - rb);
+      double2* rb2 = reinterpret_cast<double2*>(rbuf);
       for (int q = 0; q < nrows; ++q) {
-        double* row = M + (long long)(rb + q) * L;
-        for (int c = lane; c < L; c += 32) row[c] = 0.0;
+        for (int c = lane; c < (L >> 1); c += 32) rb2[c] = make_double2(0.0, 0.0);
+        __syncwarp();
+        const int cq = __shfl_sync(0xffffffffu, cnt, q);
+        const double fq = __shfl_sync(0xffffffffu, fload, q);
+        if (lane < cq) rbuf[lcol[lane * 32 + q]] = lval[lane * 32 + q];
+        if (lane == 0) rbuf[nL] = fq;
+        __syncwarp();
+        double2* row2 = reinterpret_cast<double2*>(M + (long long)(rb + q) * L);
+        for (int c = lane; c < (L >> 1); c += 32) row2[c] = rb2[c];
+        __syncwarp();
       }
-      __syncwarp();
-      if (r < nL) {
-        double* row = M + (long long)r * L;
-        for (int t = 0; t < cnt; ++t) row[lcol[t * 32 + lane]] = lval[t * 32 + lane];
-        row[nL] = fload;
-      }
-      __syncwarp();
     }
     if (ovf && overflow) atomicExch(overflow, 1);
     return;
@@ -273,8 +278,9 @@ static size_t assemble_region0(int max_nl, int nrowbuf) {
 
 static size_t assemble_smem_bytes(int max_nl, int nrowbuf) {
   const size_t ints = (max_nl + 1) + kAsmWarps + 1;
+  const int nbuf = nrowbuf == 0 ? kAsmWarps : nrowbuf;  // the compact phase has one per warp
   return assemble_region0(max_nl, nrowbuf) + ((ints * 4 + 15) & ~(size_t)15) +
-         (size_t)nrowbuf * (max_nl + 2) * 8;
+         (size_t)nbuf * (max_nl + 4) * 8;
 }
 
 // ---------------------------------------------------------------------------
@@ -811,7 +817,7 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
                         const double* gdir, int nbatch, int max_nl, int* lists, long long* keys,
                         int* overflow, int general, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  int nrowbuf = 0;  // compact row phase
+  int nrowbuf = 0;  // compact row phase (row lists + one row buffer per warp)
   if (general) {
     nrowbuf = kAsmWarps;
     while (nrowbuf > 1 && assemble_smem_bytes(max_nl, nrowbuf) > 200 * 1024) --nrowbuf;
