@@ -376,7 +376,7 @@ def run_mine(args):
 
     cfg = args.config
     t0 = time.perf_counter()
-    prob = configs.build_problem(cfg, n=args.n, subs=args.subs)
+    prob = configs.build_problem(cfg, n=args.n, subs=args.subs, device="cuda")
     t_pre = time.perf_counter() - t0
     n_cells = prob.mesh.cells[0]
     comm, owned = None, None

@@ -166,11 +166,12 @@ class Problem:
         return self.system.n_free
 
 
-def build_problem(config, n=None, subs=None, theta_f=THETA, theta_e=THETA, seed=0):
+def build_problem(config, n=None, subs=None, theta_f=THETA, theta_e=THETA, seed=0, device=None):
     """Mesh, partition, globs and element data of one BASELINE config.
 
     ``n`` / ``subs`` override the mesh and subdomain grid (same coefficients),
-    which is how bounded CPU samples of a config are made."""
+    which is how bounded CPU samples of a config are made.  ``device``
+    ("cuda"): glob classification on the GPU (same globs)."""
     defaults = {1: (16, 4), 2: (32, 4), 3: (64, 8), 4: (64, None), 5: (128, 16)}
     n0, s0 = defaults[config]
     n = n or n0
@@ -204,7 +205,7 @@ def build_problem(config, n=None, subs=None, theta_f=THETA, theta_e=THETA, seed=
         cell_nu, vel, aff = np.full(n ** 3, 1e-2), _const_velocity(b), (Z, b)
     else:
         raise ValueError(f"unknown config {config}")
-    globs = classify_globs(mesh, part, mesh.boundary_nodes)
+    globs = classify_globs(mesh, part, mesh.boundary_nodes, device=device)
     coeffs = _coeffs(cell_nu, n, vel, aff)
     system = assemble_system(mesh, coeffs)
     if theta_f is None:

@@ -168,8 +168,9 @@ def _components(members, adj):
     return comps
 
 
-def classify_globs(mesh, part, dirichlet_nodes):
-    """Faces / edges / vertices of the interface (reference decomposition.py:253-325)."""
+def _faces_and_multi_host(mesh, part, dirichlet_nodes):
+    """Face node groups (nodes sorted by (s0, s1, node) with their sharer pair)
+    and the nodes with >= 3 sharers with their sharer tuples, on the host."""
     node, sub = node_sharer_pairs(mesh, part)
     n_nodes = mesh.n_nodes
     is_dir = np.zeros(n_nodes, dtype=bool)
@@ -177,13 +178,75 @@ def classify_globs(mesh, part, dirichlet_nodes):
     count = np.bincount(node, minlength=n_nodes)
     start = np.zeros(n_nodes + 1, dtype=np.int64)
     np.cumsum(count, out=start[1:])
-
-    # faces: nodes with exactly two sharers, grouped by (s0, s1)
     two = np.flatnonzero((count == 2) & ~is_dir)
     s0 = sub[start[two]]
     s1 = sub[start[two] + 1]
     order = np.lexsort((two, s1, s0))
+    multi = np.flatnonzero((count >= 3) & ~is_dir)
+    mcount = count[multi]
+    msub = sub[np.repeat(start[multi], mcount) + np.arange(int(mcount.sum())) -
+               np.repeat(np.cumsum(mcount) - mcount, mcount)] if multi.size else np.zeros(0, np.int64)
+    member = np.zeros(n_nodes, dtype=bool)
+    member[multi] = True
+    return two[order], s0[order], s1[order], multi, mcount, msub, _adjacency_among(mesh, member)
+
+
+def _faces_and_multi_device(mesh, part, dirichlet_nodes, device):
+    """Same outputs as _faces_and_multi_host; the sharer pairs of all element
+    corners (a sort-unique of 4 x n_elements keys), the sharer counts, the face
+    grouping sort and the member-edge filter run on the GPU (torch); only the
+    small sets (face nodes, nodes with >= 3 sharers, their edges) come back."""
+    import torch
+
+    N = int(part.n_subdomains)
+    n_nodes = mesh.n_nodes
+    el = torch.from_numpy(np.ascontiguousarray(mesh.elements, dtype=np.int64)).to(device)
+    so = torch.from_numpy(np.ascontiguousarray(part.subdomain_of, dtype=np.int64)).to(device)
+    key = torch.unique((el * N + so[:, None]).reshape(-1))        # sorted (node, sub) pairs
+    node, sub = key // N, key % N
+    count = torch.bincount(node, minlength=n_nodes)
+    start = torch.zeros(n_nodes + 1, dtype=torch.int64, device=device)
+    torch.cumsum(count, 0, out=start[1:])
+    is_dir = torch.zeros(n_nodes, dtype=torch.bool, device=device)
+    is_dir[torch.from_numpy(np.asarray(dirichlet_nodes, dtype=np.int64)).to(device)] = True
+    two = torch.nonzero((count == 2) & ~is_dir).squeeze(1)
+    s0, s1 = sub[start[two]], sub[start[two] + 1]
+    fkey = (s0 * N + s1) * n_nodes + two
+    order = torch.sort(fkey).indices
     two, s0, s1 = two[order], s0[order], s1[order]
+    multi = torch.nonzero((count >= 3) & ~is_dir).squeeze(1)
+    mcount = count[multi]
+    idx = torch.repeat_interleave(start[multi], mcount) + torch.arange(int(mcount.sum()), device=device) \
+        - torch.repeat_interleave(torch.cumsum(mcount, 0) - mcount, mcount)
+    msub = sub[idx]
+    member = torch.zeros(n_nodes, dtype=torch.bool, device=device)
+    member[multi] = True
+    pairs = []
+    for a, b in _TET_EDGES:
+        u, v = el[:, a], el[:, b]
+        keep = member[u] & member[v]
+        pairs.append(torch.stack([torch.minimum(u[keep], v[keep]), torch.maximum(u[keep], v[keep])], 1))
+    pairs = torch.unique(torch.cat(pairs), dim=0).cpu().numpy()
+    nbrs = defaultdict(set)
+    for x, y in pairs.tolist():
+        nbrs[x].add(y)
+        nbrs[y].add(x)
+    host = lambda t: t.cpu().numpy()
+    return host(two), host(s0), host(s1), host(multi), host(mcount), host(msub), nbrs
+
+
+def classify_globs(mesh, part, dirichlet_nodes, device=None):
+    """Faces / edges / vertices of the interface (reference decomposition.py:253-325).
+
+    device (e.g. "cuda"): the sharer pairs, counts and face grouping are
+    computed on the GPU (identical result, tests/test_gpu_elements.py)."""
+    if device is not None:
+        two, s0, s1, multi, mcount, msub, nbrs = _faces_and_multi_device(mesh, part,
+                                                                         dirichlet_nodes, device)
+    else:
+        two, s0, s1, multi, mcount, msub, nbrs = _faces_and_multi_host(mesh, part, dirichlet_nodes)
+
+    # faces: nodes with exactly two sharers, grouped by (s0, s1)
     globs = []
     if two.size:
         cut = np.flatnonzero((np.diff(s0) != 0) | (np.diff(s1) != 0)) + 1
@@ -191,13 +254,10 @@ def classify_globs(mesh, part, dirichlet_nodes):
             globs.append(Glob("face", two[a:b].astype(np.int64), (int(s0[a]), int(s1[a]))))
 
     # three or more sharers: components, then vertex promotion
-    multi = np.flatnonzero((count >= 3) & ~is_dir)
     classes = defaultdict(list)
-    for n in multi.tolist():
-        classes[tuple(sub[start[n]:start[n + 1]].tolist())].append(n)
-    member = np.zeros(n_nodes, dtype=bool)
-    member[multi] = True
-    nbrs = _adjacency_among(mesh, member)
+    mstart = np.concatenate([[0], np.cumsum(mcount)]).astype(np.int64)
+    for i, n in enumerate(multi.tolist()):
+        classes[tuple(msub[mstart[i]:mstart[i + 1]].tolist())].append(n)
 
     edge_comps, vertices = [], []
     for s in sorted(classes):

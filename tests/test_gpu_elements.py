@@ -53,3 +53,21 @@ def test_device_elements_owned_subset_and_errors():
     with pytest.raises(ValueError, match="shifted reaction"):
         device_element_blocks({**inp, "_supg": (f, inp["_supg"][1])})
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("name", ["jump", "cfg1", "cfg4_small", "cfg3"])
+def test_device_glob_classification_matches_host(name):
+    """Glob classification with the sharer pairs, counts and face grouping on
+    the GPU (reference decomposition.py:242-325) gives the host's globs:
+    same kinds, sizes, sharers, node lists and order."""
+    import numpy as np
+
+    from paper_2501_01676_b200.decomposition import classify_globs
+    from tests.cases import inputs
+
+    system, part, globs = inputs(name)
+    dev = classify_globs(system.mesh, part, system.mesh.boundary_nodes, device="cuda")
+    a, b = globs.flat(), dev.flat()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(globs.interface_nodes, dev.interface_nodes)
