@@ -175,16 +175,33 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
     cp_async_commit();
     const int st = kc % kStages;
     const int kmax = min(kKC, K - kc * kKC);
-    for (int k0 = 0; k0 < kmax; k0 += 4) {
-      double a[4], b[kNJ];
+    if (kmax == kKC) {
+      // full chunk: unrolled, so the fragment loads of step k0 + 4 are issued
+      // while the DMMAs of step k0 run
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = sm.A[st][wm + i * 8 + g][k0 + t];
+      for (int k0 = 0; k0 < kKC; k0 += 4) {
+        double a[4], b[kNJ];
 #pragma unroll
-      for (int j = 0; j < kNJ; ++j) b[j] = sm.B[st][k0 + t][wn + j * 8 + g];
+        for (int i = 0; i < 4; ++i) a[i] = sm.A[st][wm + i * 8 + g][k0 + t];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < kNJ; ++j) b[j] = sm.B[st][k0 + t][wn + j * 8 + g];
 #pragma unroll
-        for (int j = 0; j < kNJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < kNJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    } else {
+      for (int k0 = 0; k0 < kmax; k0 += 4) {
+        double a[4], b[kNJ];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = sm.A[st][wm + i * 8 + g][k0 + t];
+#pragma unroll
+        for (int j = 0; j < kNJ; ++j) b[j] = sm.B[st][k0 + t][wn + j * 8 + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < kNJ; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
     }
   }
   cp_async_wait<0>();
