@@ -1057,7 +1057,10 @@ struct PriorTables {
   const int* ex_h;         // nH of the sharer
 };
 
-__global__ void __launch_bounds__(256) edge_new_kernel(GlobTables t, const double* __restrict__ D,
+#ifndef BDDC_EDGE_MINB
+#define BDDC_EDGE_MINB 1
+#endif
+__global__ void __launch_bounds__(256, BDDC_EDGE_MINB) edge_new_kernel(GlobTables t, const double* __restrict__ D,
                                                        PriorTables pr, double theta, GlobOut o,
                                                        double* __restrict__ ws,
                                                        const long long* __restrict__ ws_off,
