@@ -667,10 +667,7 @@ __global__ void lu_diag_pinv_kernel(double* __restrict__ LU, const long long* __
 // local part of M^-1 and the coarse restriction, one CTA per subdomain:
 //   x = r[perm];  cvals = G x;  t = TT^T x (primal entries zeroed);  t = Sdd^-1 t (LU);
 //   y = TT t        (= A_i x with A_i = TT Z TT^T, without forming A_i)
-#ifndef BDDC_LS_MINB
-#define BDDC_LS_MINB 1
-#endif
-__global__ void __launch_bounds__(256, BDDC_LS_MINB) local_solve_kernel(
+__global__ void __launch_bounds__(256) local_solve_kernel(
     const int* __restrict__ nB, const long long* __restrict__ soff,
     const long long* __restrict__ voff, const int* __restrict__ iface_perm,
     const double* __restrict__ LU, const int* __restrict__ pos2k,
@@ -718,10 +715,7 @@ __global__ void __launch_bounds__(256, BDDC_LS_MINB) local_solve_kernel(
 //   MP[p] = e_pc - Z Sbar[:, pc],  RP[p] = e_pc - Z^T Sbar[pc, :]^T,  C_i[p][q] = Sbar[pr, :] . MP[q]
 // (Z = Sdd^-1 embedded with zero primal rows / columns)
 constexpr int kPL = 8;
-#ifndef BDDC_PP_MINB
-#define BDDC_PP_MINB 1
-#endif
-__global__ void __launch_bounds__(256, BDDC_PP_MINB) primal_pieces_lu_kernel(
+__global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
     const int* __restrict__ nB, const long long* __restrict__ soff,
     const long long* __restrict__ voff, const unsigned char* __restrict__ primal_mask,
     const int* __restrict__ pstart, const int* __restrict__ ppos,
