@@ -72,6 +72,10 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
  * sub-panels combined so the DMMA trailing update runs with K = 128):
  * eliminates npiv[b] leading pivots; trailing block becomes the Schur complement,
  * pivot rows keep W = A11^-1 A12 for back-substitution.
+ * col_hole0 / col_hole1 (per matrix, both null: none): the pivot rows have no
+ * entries in columns [col_hole0[b], col_hole1[b]), so the panel steps skip
+ * them (first phase of the two-phase subdomain elimination: the deep interior
+ * pivots touch only the interior block and the load column; nrows = nI there).
  * replaces splu(A_II) + lu.solve + A_BI @ (...)  substructuring.py:120-127,
  *          lu_factor(coarse) solver.py:123 (with piv_out for the pivot check :124-132),
  *          cho_factor(sym(Sdd)) certificate solver.py:94 (require_positive = 1). */
@@ -80,7 +84,7 @@ int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const i
                          int max_rows, int max_cols, int panel, double* pinv_ws,
                          long long pinv_stride, long long pinv_step_stride, int* status,
                          int require_positive, double* piv_out, long long piv_stride,
-                         cudaStream_t stream);
+                         const int* col_hole0, const int* col_hole1, cudaStream_t stream);
 
 /* Same, recording CUDA events around every trailing-update launch; the summed
  * device time (ms) is written to the HOST pointer host_trailing_ms (bench roofline). */
@@ -89,7 +93,8 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
                                int max_rows, int max_cols, int panel, double* pinv_ws,
                                long long pinv_stride, long long pinv_step_stride, int* status,
                                int require_positive, double* piv_out, long long piv_stride,
-                               cudaStream_t stream, double* host_trailing_ms);
+                               const int* col_hole0, const int* col_hole1, cudaStream_t stream,
+                               double* host_trailing_ms);
 
 /* Converts the result of bddc_schur_eliminate with panel = 128 on square
  * n x n matrices (npiv = nrows = ncols = n, pinv_step_stride != 0 so every
@@ -154,13 +159,16 @@ int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
 int bddc_frob2(const double* X, const long long* soff, const int* n, int nbatch, double* out,
                cudaStream_t stream);
 
-/* u_I = A_II^-1 (f_I - A_IB u_B) by block back-substitution.
+/* u_I = A_II^-1 (f_I - A_IB u_B) by block back-substitution over the stored
+ * W rows.  ndeep (per matrix, null: 0): the leading pivots eliminated in a
+ * separate first phase (bddc_schur_eliminate with a column hole); the panels
+ * of the second phase start at ndeep[b].
  * replaces recover_interior solver.py:318-326. */
 int bddc_recover_interior(const double* M, const long long* off, const int* ld, const int* nI,
                           const int* nB, const long long* voff, const int* iface_perm,
                           const long long* ioff, const long long* interior_nodes,
                           const double* u_hat, double* u, int nbatch, int max_nloc, int panel,
-                          cudaStream_t stream);
+                          const int* ndeep, cudaStream_t stream);
 
 /* ---- elements.cu : SUPG element blocks ------------------------------------ */
 

@@ -340,22 +340,49 @@ __global__ void __launch_bounds__(256, 4) pivot_inverse_kernel(
 // Schur elimination (LU-style, rows below only):
 //   W = A11^-1 A12 stored over A12;   A22 -= A21 W
 // ---------------------------------------------------------------------------
+// Column hole (two-phase elimination, deep interior pivots): the pivot rows of
+// the first phase have no entries in columns [h0, h1) (the interface block), so
+// the column tiles of a panel step cover [s, h0) and [h1, nc) only.
+struct ColHole {
+  const int* h0;  // per matrix, null: no hole
+  const int* h1;
+};
+
+BDDC_DEV int tile_col_count(int s, int nc, int h0, int h1) {
+  if (h0 >= h1) return (nc - s + kTile - 1) / kTile;
+  return (max(h0 - s, 0) + kTile - 1) / kTile + (max(nc - h1, 0) + kTile - 1) / kTile;
+}
+
+// column tile tn of [s, nc) minus [h0, h1): first column and width; false past the end
+BDDC_DEV bool tile_cols(int s, int tn, int nc, int h0, int h1, int& c0, int& n) {
+  int c = s + tn * kTile, end = nc;
+  if (h0 < h1) {
+    const int t0 = (max(h0 - s, 0) + kTile - 1) / kTile;  // tiles before the hole
+    if (tn < t0) end = h0;
+    else c = h1 + (tn - t0) * kTile;
+  }
+  if (c >= end) return false;
+  c0 = c;
+  n = min(kTile, end - c);
+  return true;
+}
+
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_row_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ ncols, int k,
-    const double* __restrict__ pinv, long long pinv_stride, int lim) {
+    const double* __restrict__ pinv, long long pinv_stride, int lim, ColHole hole) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
   const int w = min(kTile, npiv[b] - k);
   if (w <= 0) return;
   const int nc = min(ncols[b], lim);
-  const int c0 = k + w + blockIdx.x * kTile;
-  if (c0 >= nc) return;
+  const int h0 = hole.h0 ? hole.h0[b] : 0, h1 = hole.h0 ? hole.h1[b] : 0;
+  int c0, n;
+  if (!tile_cols(k + w, blockIdx.x, nc, h0, h1, c0, n)) return;
   const int L = ld[b];
   double* C = base + off[b] + (long long)k * L + c0;
-  tile_mma(C, L, w, min(kTile, nc - c0), pinv + (long long)b * pinv_stride, kTile, C, L, w,
-           1.0, 0.0, sm);
+  tile_mma(C, L, w, n, pinv + (long long)b * pinv_stride, kTile, C, L, w, 1.0, 0.0, sm);
 }
 
 constexpr int kTrailBM = 64;
@@ -378,7 +405,7 @@ struct NextPivot {
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ nrows, const int* __restrict__ ncols,
-    int k, int lim, int nbw, int mode, NextPivot nx) {
+    int k, int lim, int nbw, int mode, NextPivot nx, ColHole hole) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmemT<kTrailBM>& sm = *reinterpret_cast<TileSmemT<kTrailBM>*>(smem_raw);
   const int b = blockIdx.y;
@@ -399,14 +426,16 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_k
     r_begin = k + w1;
     r_end = k + wt;
   }
-  const int tn_count = (nc - s + kTile - 1) / kTile;
+  const int h0 = hole.h0 ? hole.h0[b] : 0, h1 = hole.h0 ? hole.h1[b] : 0;
+  const int tn_count = tile_col_count(s, nc, h0, h1);
   if (tn_count <= 0) return;
   const int tm = blockIdx.x / tn_count, tn = blockIdx.x - tm * tn_count;
-  const int r0 = r_begin + tm * kTrailBM, c0 = s + tn * kTile;
-  if (r0 >= r_end) return;
+  const int r0 = r_begin + tm * kTrailBM;
+  int c0, cn;
+  if (r0 >= r_end || !tile_cols(s, tn, nc, h0, h1, c0, cn)) return;
   const int L = ld[b];
   double* M = base + off[b];
-  tile_mma_t<kTrailBM>(M + (long long)r0 * L + c0, L, min(kTrailBM, r_end - r0), min(kTile, nc - c0),
+  tile_mma_t<kTrailBM>(M + (long long)r0 * L + c0, L, min(kTrailBM, r_end - r0), cn,
                        M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0,
                        sm);
   if (nx.pinv != nullptr && blockIdx.x == 0) {
@@ -430,7 +459,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_k
 // where W1_Q = M[k:k+64, k+64:k+w] and W2 = M[k+64:k+w, k+w:]
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_fix_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ npiv, const int* __restrict__ ncols, int k) {
+    const int* __restrict__ npiv, const int* __restrict__ ncols, int k, ColHole hole) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
@@ -438,11 +467,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_fix_kernel
   const int wt = min(2 * kTile, np);
   if (wt <= kTile) return;
   const int w2 = wt - kTile;
-  const int c0 = k + wt + blockIdx.x * kTile;
-  if (c0 >= ncols[b]) return;
+  const int h0 = hole.h0 ? hole.h0[b] : 0, h1 = hole.h0 ? hole.h1[b] : 0;
+  int c0, cn;
+  if (!tile_cols(k + wt, blockIdx.x, ncols[b], h0, h1, c0, cn)) return;
   const int L = ld[b];
   double* M = base + off[b];
-  tile_mma(M + (long long)k * L + c0, L, kTile, min(kTile, ncols[b] - c0),
+  tile_mma(M + (long long)k * L + c0, L, kTile, cn,
            M + (long long)k * L + k + kTile, L, M + (long long)(k + kTile) * L + c0, L, w2, -1.0,
            1.0, sm);
 }
@@ -743,27 +773,35 @@ __global__ void __launch_bounds__(256) recover_kernel(
     const int* __restrict__ nI, const int* __restrict__ nB, const long long* __restrict__ voff,
     const int* __restrict__ iface_perm, const long long* __restrict__ ioff,
     const long long* __restrict__ interior_nodes, const double* __restrict__ u_hat,
-    double* __restrict__ u, int panel) {
+    double* __restrict__ u, int panel, const int* __restrict__ ndeep) {
   extern __shared__ double us[];  // nI + nB
   const int b = blockIdx.x;
   const int ni = nI[b], nb = nB[b], L = ld[b], nl = ni + nb;
+  const int nd = ndeep ? ndeep[b] : 0;
   const double* M = base + off[b];
   for (int j = threadIdx.x; j < nb; j += blockDim.x) us[ni + j] = u_hat[iface_perm[voff[b] + j]];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  // panels of the elimination (W = A11^-1 A12 per panel, identity diagonal)
-  const int last = ((ni - 1) / panel) * panel;
-  for (int k = last; k >= 0; k -= panel) {
-    const int w = min(panel, ni - k);
-    for (int r = k + warp; r < k + w; r += nw) {
-      const double* row = M + (long long)r * L;
-      double s = 0.0;
-      for (int c = k + w + lane; c < nl; c += 32) s += row[c] * us[c];
+  // panels of the elimination (W = A11^-1 A12 per panel, identity diagonal):
+  // second phase (pivots [nd, ni), panels from nd) first, then the deep pivots
+  // [0, nd), whose rows have no entries in the interface columns
+  for (int phase = 1; phase >= 0; --phase) {
+    const int p0 = phase ? nd : 0, p1 = phase ? ni : nd;
+    if (p1 <= p0) continue;
+    const int cend = phase ? nl : ni;
+    const int last = p0 + ((p1 - p0 - 1) / panel) * panel;
+    for (int k = last; k >= p0; k -= panel) {
+      const int w = min(panel, p1 - k);
+      for (int r = k + warp; r < k + w; r += nw) {
+        const double* row = M + (long long)r * L;
+        double s = 0.0;
+        for (int c = k + w + lane; c < cend; c += 32) s += row[c] * us[c];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) us[r] = row[nl] - s;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) us[r] = row[nl] - s;
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
   for (int j = threadIdx.x; j < ni; j += blockDim.x) u[interior_nodes[ioff[b] + j]] = us[j];
 }
@@ -874,9 +912,11 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
                                 int max_rows, int max_cols, int panel, double* pinv_ws,
                                 long long pinv_stride, long long pinv_step_stride, int* status,
                                 int require_positive, double* piv_out, long long piv_stride,
-                                cudaStream_t stream, double* host_trailing_ms) {
+                                const int* hole0, const int* hole1, cudaStream_t stream,
+                                double* host_trailing_ms) {
   if (nbatch <= 0) return 0;
   if (panel != 2 * kTile) panel = kTile;
+  const ColHole hole{hole0, hole0 ? hole1 : nullptr};
   const int smem = smem_tile_setup();
   const int nsteps = (max_npiv + panel - 1) / panel;
   cudaEvent_t* ev = nullptr;
@@ -904,8 +944,8 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
     // first (or only) 64-wide sub-panel: W1 = P1 A12 (P1 from the previous launch)
     const int ct1 = ceil_div(max_cols - k, kTile);
     if (ct1 > 0) {
-      schur_row_kernel<<<dim3(ct1, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
-                                                                         P, pinv_stride, 0x7fffffff);
+      schur_row_kernel<<<dim3(ct1, nbatch), kTileThreads, smem, stream>>>(
+          M, off, ld, npiv, ncols, k, P, pinv_stride, 0x7fffffff, hole);
       ++launches;
     }
     if (panel == 2 * kTile && k + kTile < max_npiv) {
@@ -913,10 +953,11 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
       // W2, then W_top -= W1_Q W2 so the pivot rows hold A11^-1 A12 for all 128
       const int cts = ceil_div(max_cols - k - kTile, kTile);
       schur_trailing_kernel<<<dim3(cts, nbatch), kTileThreads, tsm, stream>>>(
-          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1, nx_sub);
+          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1, nx_sub, hole);
       schur_row_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(
-          M, off, ld, npiv, ncols, k + kTile, P2, pinv_stride, 0x7fffffff);
-      schur_fix_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k);
+          M, off, ld, npiv, ncols, k + kTile, P2, pinv_stride, 0x7fffffff, hole);
+      schur_fix_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
+                                                                         hole);
       launches += 3;
     }
     const int ct = ceil_div(max_cols - k, kTile);
@@ -927,7 +968,7 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
       if (lg) cudaEventRecord(g_trail_pool[g_trail_used], stream);
       if (ev) cudaEventRecord(ev[2 * timed], stream);
       schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, tsm, stream>>>(
-          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, panel, 0, more ? nx_next : none);
+          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, panel, 0, more ? nx_next : none, hole);
       ++launches;
       next_done = true;
       if (ev) cudaEventRecord(ev[2 * timed + 1], stream);
@@ -963,10 +1004,11 @@ int bddc_schur_eliminate(double* M, const long long* off, const int* ld, const i
                          int max_rows, int max_cols, int panel, double* pinv_ws,
                          long long pinv_stride, long long pinv_step_stride, int* status,
                          int require_positive, double* piv_out, long long piv_stride,
-                         cudaStream_t stream) {
+                         const int* col_hole0, const int* col_hole1, cudaStream_t stream) {
   return schur_eliminate_impl(M, off, ld, npiv, nrows, ncols, nbatch, max_npiv, max_rows,
                               max_cols, panel, pinv_ws, pinv_stride, pinv_step_stride, status,
-                              require_positive, piv_out, piv_stride, stream, nullptr);
+                              require_positive, piv_out, piv_stride, col_hole0, col_hole1, stream,
+                              nullptr);
 }
 
 int bddc_trailing_log(int enable) {
@@ -997,10 +1039,12 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
                                int max_rows, int max_cols, int panel, double* pinv_ws,
                                long long pinv_stride, long long pinv_step_stride, int* status,
                                int require_positive, double* piv_out, long long piv_stride,
-                               cudaStream_t stream, double* host_trailing_ms) {
+                               const int* col_hole0, const int* col_hole1, cudaStream_t stream,
+                               double* host_trailing_ms) {
   return schur_eliminate_impl(M, off, ld, npiv, nrows, ncols, nbatch, max_npiv, max_rows,
                               max_cols, panel, pinv_ws, pinv_stride, pinv_step_stride, status,
-                              require_positive, piv_out, piv_stride, stream, host_trailing_ms);
+                              require_positive, piv_out, piv_stride, col_hole0, col_hole1, stream,
+                              host_trailing_ms);
 }
 
 int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n, int nbatch,
@@ -1109,13 +1153,13 @@ int bddc_recover_interior(const double* M, const long long* off, const int* ld, 
                           const int* nB, const long long* voff, const int* iface_perm,
                           const long long* ioff, const long long* interior_nodes,
                           const double* u_hat, double* u, int nbatch, int max_nloc, int panel,
-                          cudaStream_t stream) {
+                          const int* ndeep, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   const int smem = max_nloc * (int)sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(recover_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   recover_kernel<<<nbatch, 256, smem, stream>>>(M, off, ld, nI, nB, voff, iface_perm, ioff,
-                                                interior_nodes, u_hat, u, panel);
+                                                interior_nodes, u_hat, u, panel, ndeep);
   bddc_note_launches(1);
   return launch_status();
 }

@@ -24,6 +24,7 @@ from .plan import Plan, _excl, _ranges
 
 F64 = torch.float64
 PANEL = 128  # elimination panel width (two 64-wide sub-panels; DMMA trailing update with K = 128)
+TWO_PHASE = True  # deep interior pivots eliminated first, restricted to the interior block (plan.nDeep)
 
 
 # kernels launched through CUDA-graph replays (the C-ABI launch counter sees
@@ -188,14 +189,30 @@ class LocalSystem:
         p, d, st = self.plan, self.d, stream()
         status = torch.zeros(p.N, dtype=torch.int32, device="cuda")
         pinv = torch.empty(p.N * 4096, dtype=F64, device="cuda")
-        args = (K, d.off, d.ld, d.nI, d.nL, d.nL1, p.N, int(p.nI.max()), int(p.nL.max()),
-                int(p.nL.max()) + 1, PANEL, pinv, 4096, 0, status, 0, None, 0, st)
-        if self.kernel_timing:
-            ms = ctypes.c_double(0.0)
-            lib.bddc_schur_eliminate_timed(*args, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
-            self.trailing_ms = ms.value
+        # two phases (plan.py): the deep interior pivots [0, nDeep) touch only the
+        # interior block and the load column (column hole [nI, nL), rows < nI);
+        # the shell pivots [nDeep, nI) are the leading pivots of the sub-matrix
+        # starting at (nDeep, nDeep), eliminated over its full width
+        phases = []
+        if TWO_PHASE and int(p.nDeep.max()) > 0:
+            phases.append((d.off, d.nDeep, d.nI, d.nL1, int(p.nDeep.max()), int(p.nI.max()),
+                           int(p.nI.max()) + 65, d.nI, d.nL))
+            phases.append((d.off_shell, d.n_shell, d.nL_shell, d.nL1_shell,
+                           int((p.nI - p.nDeep).max()), int((p.nL - p.nDeep).max()),
+                           int((p.nL - p.nDeep).max()) + 1, None, None))
         else:
-            lib.bddc_schur_eliminate(*args)
+            phases.append((d.off, d.nI, d.nL, d.nL1, int(p.nI.max()), int(p.nL.max()),
+                           int(p.nL.max()) + 1, None, None))
+        self.trailing_ms = 0.0 if self.kernel_timing else None
+        for off, npiv, nrows, ncols, max_npiv, max_rows, max_cols, h0, h1 in phases:
+            args = (K, off, d.ld, npiv, nrows, ncols, p.N, max_npiv, max_rows, max_cols, PANEL,
+                    pinv, 4096, 0, status, 0, None, 0, h0, h1, st)
+            if self.kernel_timing:
+                ms = ctypes.c_double(0.0)
+                lib.bddc_schur_eliminate_timed(*args, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
+                self.trailing_ms += ms.value
+            else:
+                lib.bddc_schur_eliminate(*args)
         self.K = K
         self.S = torch.empty(p.S_total, dtype=F64, device="cuda")
         # Bsym = sym(S) is written straight into the buffer Bsym^-1 is computed in
@@ -313,7 +330,15 @@ def trailing_flops(plan, panel=PANEL, dual_lu=False):
     Returns (flops, launches)."""
     nI, nL, nB = (plan.nI.astype(np.int64), plan.nL.astype(np.int64),
                   plan.nB.astype(np.int64))
-    f, n = _panel_flops(nI, nL, nL + 1, panel)
+    nd = plan.nDeep.astype(np.int64)
+    if TWO_PHASE and int(nd.max()) > 0:
+        # deep phase: rows [., nI), columns [., nI) + the load column; shell phase:
+        # the sub-matrix from (nDeep, nDeep)
+        f, n = _panel_flops(nd, nI, nI + 1, panel)
+        f2, n2 = _panel_flops(nI - nd, nL - nd, nL + 1 - nd, panel)
+        f, n = f + f2, n + n2
+    else:
+        f, n = _panel_flops(nI, nL, nL + 1, panel)
     if dual_lu:
         f2, n2 = _panel_flops(nB, nB, nB, panel)
         f, n = f + f2, n + n2
@@ -336,6 +361,12 @@ class DevicePlan:
         self.nB = dev_i32(p.nB)
         self.nL = dev_i32(p.nL)
         self.nL1 = dev_i32(p.nL + 1)
+        nd = p.nDeep
+        self.nDeep = dev_i32(nd)
+        self.off_shell = dev_i64(p.off + nd * (p.ld + 1))
+        self.n_shell = dev_i32(p.nI - nd)
+        self.nL_shell = dev_i32(p.nL - nd)
+        self.nL1_shell = dev_i32(p.nL + 1 - nd)
         self.soff = dev_i64(p.soff)
         self.voff = dev_i64(p.voff)
         self.ioff = dev_i64(p.ioff)
@@ -986,7 +1017,7 @@ class DevicePreconditioner:
             Csym = Z.clone()  # sym(Z): sym(Sbar_dd) embedded with the identity
             lib.bddc_symmetrize(Csym, d.soff, d.nB, p.N, st)
             lib.bddc_schur_eliminate(Csym, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax,
-                                     nbmax, PANEL, pinv, 4096, 0, status, 1, None, 0, st)
+                                     nbmax, PANEL, pinv, 4096, 0, status, 1, None, 0, None, None, st)
             del Csym
             bad = _first_bad(status)
             if bad is not None:
@@ -997,7 +1028,7 @@ class DevicePreconditioner:
         nsteps = (nbmax + 63) // 64
         pinv_all = torch.empty(nsteps * p.N * 4096, dtype=F64, device="cuda")
         lib.bddc_schur_eliminate(Z, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax, nbmax,
-                                 PANEL, pinv_all, 4096, p.N * 4096, status, 0, None, 0, st)
+                                 PANEL, pinv_all, 4096, p.N * 4096, status, 0, None, 0, None, None, st)
         if PANEL == 128:  # 128-wide elimination -> the 64-panel form of the local solves
             lib.bddc_lu128_fixup(Z, d.soff, d.nB, d.nB, p.N, nbmax, st)
         # host work overlapping the queued factorisation: coarse dofs in reverse
@@ -1484,12 +1515,14 @@ def recover_device(ls, u_hat):
         u = ls.inputs["gdir"].clone()
         u[iface] = u_hat
         lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, d.iface_perm, d.ioff,
-                                  d.I_nodes, u_hat, u, p.N, int(p.nL.max()), PANEL, st)
+                                  d.I_nodes, u_hat, u, p.N, int(p.nL.max()), PANEL,
+                                  d.nDeep if TWO_PHASE else None, st)
         return u
     lay = ls.layout
     ui = torch.zeros_like(ls.inputs["gdir"])
     lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, ls.iface_perm_l, d.ioff,
-                              d.I_nodes, u_hat, ui, p.N, int(p.nL.max()), PANEL, st)
+                              d.I_nodes, u_hat, ui, p.N, int(p.nL.max()), PANEL,
+                              d.nDeep if TWO_PHASE else None, st)
     own_nodes = dev_i64(np.asarray(ls.globs.interface_nodes)[lay.glob_ids[:lay.n_own]])
     ui[own_nodes] = u_hat[:lay.n_own]
     ls.comm.allreduce_(ui)

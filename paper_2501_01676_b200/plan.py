@@ -5,8 +5,13 @@ Local numbering per subdomain (reference substructuring.py:85-96 sorts B and
 I dofs by global node id; here B dofs are *glob-major*: the subdomain's globs
 in glob order, each glob's nodes in glob order, so every glob is a
 contiguous block and the per-glob change of basis, deluxe blocks and prior
-rows are contiguous block operations).  Interior dofs stay sorted by node
-id.  Nothing downstream depends on the ordering beyond rounding.
+rows are contiguous block operations).  Interior dofs: the *deep* ones first (no
+element shared with an interface node, so their rows and columns have no
+entries in the interface block and their elimination only touches the
+interior block and the load column), then the shell; each group sorted by
+node id.  ``nDeep`` (even: 16-byte aligned sub-blocks) is the number of
+leading interior dofs eliminated in that restricted first phase.  Nothing
+downstream depends on the ordering beyond rounding.
 
 Two builders produce identical plans:
 * ``Plan(system, partition, globs)`` — numpy on the host (reference for tests);
@@ -208,10 +213,14 @@ class Plan:
         on_iface[self._iface_nodes] = True
         interior = free[node] & ~on_iface[node]
         I_sub, I_node = sub[interior], node[interior]
-        o = np.lexsort((I_node, I_sub))
+        # deep interior nodes (no element shared with an interface node) first
+        shell = np.zeros(n_nodes, dtype=bool)
+        shell[el[on_iface[el].any(axis=1)].ravel()] = True
+        o = np.lexsort((I_node, shell[I_node], I_sub))
         self.I_nodes = I_node[o]
         self.nI = np.bincount(I_sub, minlength=N).astype(np.int64)
         self.ioff = _excl(self.nI)
+        self.nDeep = np.bincount(I_sub[~shell[I_node]], minlength=N).astype(np.int64) & ~np.int64(1)
         eorder = np.argsort(sub_of, kind="stable")
         self.elem_ids = mine[eorder].astype(np.int64)
         self.elem_start = _excl(np.bincount(sub_of, minlength=N))
@@ -256,10 +265,19 @@ class Plan:
         on_iface[self._iface_nodes_d] = True
         I_all = torch.nonzero(free & ~on_iface & (owner >= 0)).squeeze(1)   # ascending node ids
         I_sub_all = owner[I_all]
-        o = torch.sort(I_sub_all, stable=True).indices
+        # deep interior nodes (no element shared with an interface node) first
+        # (integer scatter-add of the per-element flag: no host sync, order-independent)
+        touch = on_iface[conn].any(dim=1).to(torch.int32)
+        shell = torch.zeros(n_nodes, dtype=torch.int32, device=dv)
+        shell.index_add_(0, conn.reshape(-1), touch[:, None].expand(-1, 4).reshape(-1))
+        sh_all = (shell[I_all] > 0).to(torch.int64)
+        o = torch.sort(I_sub_all * 2 + sh_all, stable=True).indices
         I_node, I_sub = I_all[o], I_sub_all[o]
-        nI = torch.bincount(I_sub, minlength=N)
-        self.nI = nI.cpu().numpy().astype(np.int64)
+        cnt = torch.bincount(I_sub * 2 + sh_all[o], minlength=2 * N).view(N, 2)
+        nI = cnt.sum(dim=1)
+        cnt_h = cnt.cpu().numpy().astype(np.int64)
+        self.nI = cnt_h.sum(axis=1)
+        self.nDeep = cnt_h[:, 0] & ~np.int64(1)
         self.ioff = _excl(self.nI)
         self.I_nodes_d = I_node
         iloc = torch.full((n_nodes,), -1, dtype=torch.int32, device=dv)

@@ -146,13 +146,13 @@ def direct_schur_solve(ops, globs, rhs):
     pinv = torch.empty(4096, dtype=F64, device="cuda")
     st = stream()
     lib.bddc_schur_eliminate(M, off, ldv, nv, nv, one(n + 1), 1, n, n, n + 1, PANEL, pinv, 4096, 0,
-                             status, 0, None, 0, st)
+                             status, 0, None, 0, None, None, st)
     if int(status.item()):
         raise NumericalError("assembled interface operator is singular")
     x = torch.empty(n, dtype=F64, device="cuda")
     lib.bddc_recover_interior(M, off, ldv, nv, one(0), dev_i64(np.array([0, 0])), one(0),
                               dev_i64(np.array([0, n])), torch.arange(n, device="cuda"), x, x, 1,
-                              n, PANEL, st)
+                              n, PANEL, None, st)
     return x.cpu().numpy()
 
 

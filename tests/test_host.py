@@ -61,7 +61,18 @@ def test_plan_local_numbering(name):
         ref_I = nodes[free & ~iface]
         B = p.B_nodes[p.voff[i]:p.voff[i + 1]]
         assert np.array_equal(np.sort(B), ref_B)
-        assert np.array_equal(p.I_nodes[p.ioff[i]:p.ioff[i + 1]], ref_I)
+        # interior: deep nodes (no element shared with an interface node) first,
+        # each group in ascending node order; nDeep = even number of leading deep dofs
+        I = p.I_nodes[p.ioff[i]:p.ioff[i + 1]]
+        assert np.array_equal(np.sort(I), ref_I)
+        touch = np.isin(el[elems], globs.interface_nodes).any(axis=1)
+        shell = np.isin(I, np.unique(el[elems][touch]))
+        n_deep = int((~shell).sum())
+        assert not shell[:n_deep].any() and shell[n_deep:].all()
+        assert np.array_equal(I[:n_deep], np.sort(I[:n_deep]))
+        assert np.array_equal(I[n_deep:], np.sort(I[n_deep:]))
+        assert p.nDeep[i] == n_deep - (n_deep & 1)
+        ref_I = I
         # glob-major: every glob of the subdomain is one contiguous block
         for k in range(p.sub_glob_start[i], p.sub_glob_start[i + 1]):
             g = globs.globs[p.sub_globs[k]]

@@ -41,7 +41,7 @@ def run(path, N=4096, nI=343, nB=386, reps=3):
         ms = ctypes.c_double(0)
         torch.cuda.synchronize()
         f(P(M), P(off), P(i32(ld)), P(i32(nI)), P(i32(nL)), P(i32(nL + 1)), N, nI, nL, nL + 1, PANEL,
-          P(pinv), 4096, 0, P(st), 0, None, 0, stream, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
+          P(pinv), 4096, 0, P(st), 0, None, 0, None, None, stream, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
         torch.cuda.synchronize()
         best = min(best, ms.value)
     # GJ inverse of N x nB^2: general, and symmetric (SPD input)
