@@ -121,10 +121,6 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp / WNW) * 32, wn = (warp % WNW) * kWN;  // (BM/32) x WNW warps
   const int nchunks = (K + kKC - 1) / kKC;
-  // active DMMA slices of this warp (all of them for an interior tile)
-  const int mi = max(0, min(4, (m - wm + 7) >> 3));
-  const int nj = max(0, min(kNJ, (n - wn + 7) >> 3));
-  const bool full_mn = mi == 4 && nj == kNJ;
   const bool a16 = ((reinterpret_cast<uintptr_t>(A) | (uintptr_t)(lda * 8)) & 15) == 0;
   const bool b16 = ((reinterpret_cast<uintptr_t>(B) | (uintptr_t)(ldb * 8)) & 15) == 0;
 #pragma unroll
@@ -179,23 +175,7 @@ BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A
     cp_async_commit();
     const int st = kc % kStages;
     const int kmax = min(kKC, K - kc * kKC);
-    if (!full_mn) {
-      // edge tile: only the 8-row / 8-column DMMA slices that hold rows < m and
-      // columns < n of this warp's 32 x kWN sub-tile are issued (warp-uniform
-      // bounds), so a tile with a few valid rows costs a fraction of a full one
-      for (int k0 = 0; k0 < kmax; k0 += 4) {
-        double a[4], b[kNJ];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = i < mi ? sm.A[st][wm + i * 8 + g][k0 + t] : 0.0;
-#pragma unroll
-        for (int j = 0; j < kNJ; ++j) b[j] = j < nj ? sm.B[st][k0 + t][wn + j * 8 + g] : 0.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < kNJ; ++j)
-            if (i < mi && j < nj) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-      }
-    } else if (kmax == kKC) {
+    if (kmax == kKC) {
       // full chunk: unrolled, so the fragment loads of step k0 + 4 are issued
       // while the DMMAs of step k0 run
 #pragma unroll
