@@ -155,6 +155,55 @@ BDDC_DEV void cols_gemv(const double* __restrict__ A, long long lda, int m, int 
   __syncthreads();
 }
 
+// Eight right-hand sides on the DMMA pipe (mma.sync m8n8k4.f64):
+//   Y[r][q] = beta * Y[r][q] + alpha * sum_c op(A)[r][c] X[c][q]   (r < m, c < k, q < 8)
+// op(A) = A (m x k, TA = false) or A^T (A stored k x m, TA = true).  A warp
+// owns 8-row units (one 8 x 8 accumulator each), up to four at a time sharing
+// the X fragment, fragments straight from global memory (32-byte row
+// segments, every sector fully used) and X from shared memory: no shuffle
+// reductions, unlike the warp-per-row products above.  Ends with a barrier.
+template <bool TA>
+BDDC_DEV void panel_mma8(const double* __restrict__ A, long long lda, int m, int k,
+                         const double* X, int xs, double* Y, int ys, double alpha, double beta) {
+  const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
+  const int nw = (int)(blockDim.x >> 5);
+  const int g = lane >> 2, t = lane & 3;
+  const int mt = (m + 7) >> 3;  // 8-row units; a warp takes units warp, warp + nw, ... four at a time
+  for (int u0 = warp; u0 < mt; u0 += 4 * nw) {
+    int rr[4];
+    bool on[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      on[i] = u0 + i * nw < mt;  // warp-uniform
+      rr[i] = (u0 + i * nw) * 8 + g;
+    }
+    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll 4
+    for (int p = 0; p < k; p += 4) {
+      const int kk = p + t;
+      const bool kin = kk < k;
+      const double bv = kin ? X[kk * xs + g] : 0.0;
+      double a[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        a[i] = (kin && rr[i] < m) ? (TA ? A[(long long)kk * lda + rr[i]] : A[(long long)rr[i] * lda + kk])
+                                  : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (on[i]) dmma_8x8x4(acc[i][0], acc[i][1], a[i], bv);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (rr[i] >= m) continue;
+      double* y = Y + rr[i] * ys + 2 * t;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        y[h] = (beta == 0.0 ? 0.0 : beta * y[h]) + alpha * acc[i][h];
+    }
+  }
+  __syncthreads();
+}
+
 // x <- A^-1 x (TRANS: A^-T x); M: n x n LU (ld n) with P^-1 diagonal blocks;
 // X: n rows of stride xstride(NR); tmp: 64 * xstride(NR) doubles; red: blockDim * NR
 // doubles (transposed solve only)
@@ -162,6 +211,42 @@ template <int NR, bool TRANS>
 BDDC_DEV void lu_solve(const double* __restrict__ M, int n, double* X, double* tmp, double* red) {
   constexpr int XS = xstride<NR>();
   const int np = (n + kP - 1) / kP;
+  if (NR == 8) {
+    // eight right-hand sides: every panel product on the DMMA pipe
+    if (!TRANS) {
+      for (int j = 0; j < np; ++j) {
+        const int j0 = j * kP, w = min(kP, n - j0), j1 = j0 + w;
+        panel_mma8<false>(M + (long long)j0 * n + j0, n, w, w, X + j0 * XS, XS, tmp, XS, 1.0, 0.0);
+        for (int i = threadIdx.x; i < w * XS; i += blockDim.x) X[j0 * XS + i] = tmp[i];
+        __syncthreads();
+        if (j1 < n)
+          panel_mma8<false>(M + (long long)j1 * n + j0, n, n - j1, w, X + j0 * XS, XS, X + j1 * XS, XS,
+                            -1.0, 1.0);
+      }
+      for (int k = np - 2; k >= 0; --k) {
+        const int k0 = k * kP, k1 = k0 + kP;
+        panel_mma8<false>(M + (long long)k0 * n + k1, n, kP, n - k1, X + k1 * XS, XS, X + k0 * XS, XS,
+                          -1.0, 1.0);
+      }
+    } else {
+      for (int j = 0; j < np; ++j) {
+        const int j0 = j * kP, w = min(kP, n - j0), j1 = j0 + w;
+        if (j1 < n)
+          panel_mma8<true>(M + (long long)j0 * n + j1, n, n - j1, w, X + j0 * XS, XS, X + j1 * XS, XS,
+                           -1.0, 1.0);
+      }
+      for (int k = np - 1; k >= 0; --k) {
+        const int k0 = k * kP, w = min(kP, n - k0), k1 = k0 + w;
+        if (k1 < n)
+          panel_mma8<true>(M + (long long)k1 * n + k0, n, w, n - k1, X + k1 * XS, XS, X + k0 * XS, XS,
+                           -1.0, 1.0);
+        panel_mma8<true>(M + (long long)k0 * n + k0, n, w, w, X + k0 * XS, XS, tmp, XS, 1.0, 0.0);
+        for (int i = threadIdx.x; i < w * XS; i += blockDim.x) X[k0 * XS + i] = tmp[i];
+        __syncthreads();
+      }
+    }
+    return;
+  }
   if (!TRANS) {
     for (int j = 0; j < np; ++j) {
       const int j0 = j * kP, w = min(kP, n - j0), j1 = j0 + w;
