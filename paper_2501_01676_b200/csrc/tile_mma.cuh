@@ -111,12 +111,61 @@ BDDC_DEV void tile_issue_chunk(TileSmemT<BM>& sm, int st, int kc, const double* 
   }
 }
 
+// Thin edge tile (n <= 8 columns or m <= 8 rows, e.g. the two extra dofs of
+// nB = 386 = 6 * 64 + 2): every warp owns one 8 x 8 DMMA accumulator (row
+// block `warp` for thin columns, column block `warp` for thin rows) and reads
+// its fragments straight from global memory, so the tile costs 1/8 of a full
+// one.  Same contract as tile_mma_t (B may alias C: all reads precede the
+// writes).  Not inlined: the hot path's register allocation stays untouched.
+template <int BM>
+__device__ __noinline__ void tile_mma_thin(double* C, long long ldc, int m, int n, const double* A,
+                                           long long lda, const double* B, long long ldb, int K,
+                                           double alpha, double beta, double* Ct, long long ldct,
+                                           double tsign) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const bool thin_cols = n <= 8;
+  const int r0 = thin_cols ? 8 * warp : 0, c0 = thin_cols ? 0 : 8 * warp;
+  const int ra = r0 + g, cb = c0 + g;
+  const bool on = r0 < m && c0 < n;  // warp-uniform
+  double x0 = 0.0, x1 = 0.0;
+  if (on) {
+#pragma unroll 4
+    for (int p = 0; p < K; p += 4) {
+      const int kk = p + t;
+      const double a = (kk < K && ra < m) ? A[(long long)ra * lda + kk] : 0.0;
+      const double b = (kk < K && cb < n) ? B[(long long)kk * ldb + cb] : 0.0;
+      dmma_8x8x4(x0, x1, a, b);
+    }
+  }
+  const int cc = c0 + 2 * t;
+  double v[2] = {alpha * x0, alpha * x1};
+  if (on && ra < m && beta != 0.0) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (cc + h < n) v[h] = fma(beta, C[(long long)ra * ldc + cc + h], v[h]);
+  }
+  __syncthreads();  // every read of B (which may alias C) is done
+  if (on && ra < m) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (cc + h < n) {
+        C[(long long)ra * ldc + cc + h] = v[h];
+        if (Ct != nullptr) Ct[(long long)(cc + h) * ldct + ra] = tsign * v[h];
+      }
+  }
+}
+
 template <int BM>
 BDDC_DEV void tile_mma_t(double* C, long long ldc, int m, int n, const double* A, long long lda,
                          const double* B, long long ldb, int K, double alpha, double beta,
                          TileSmemT<BM>& sm, double* Ct = nullptr, long long ldct = 0,
                          double tsign = 1.0) {
   constexpr int WNW = 64 / kWN;  // warps along n
+  if (n <= 8 || m <= 8) {  // CTA-uniform
+    tile_mma_thin<BM>(C, ldc, m, n, A, lda, B, ldb, K, alpha, beta, Ct, ldct, tsign);
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp / WNW) * 32, wn = (warp % WNW) * kWN;  // (BM/32) x WNW warps
