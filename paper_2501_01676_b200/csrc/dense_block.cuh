@@ -36,6 +36,32 @@ BDDC_DEV void fill(double* A, int ld, int m, int n, double v) {
   __syncthreads();
 }
 
+// L2 prefetch of `count` contiguous doubles (every 128-byte line once, whole
+// block): the cold operand blocks of a glob kernel are requested up front so
+// that the later dependent loads hit L2 instead of waiting on DRAM in turn.
+BDDC_DEV void prefetch_l2(const double* p, int count) {
+  const char* b = reinterpret_cast<const char*>(p);
+  const long long bytes = (long long)count * 8;
+  for (long long o = (long long)threadIdx.x * 128; o < bytes; o += (long long)blockDim.x * 128)
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(b + o));
+}
+
+// dst[i] = src[i], i < count (contiguous), four independent loads in flight per
+// thread before the first store (generic-pointer stores would otherwise
+// serialise the loads); no trailing barrier.
+BDDC_DEV void copy_flat4(double* dst, const double* __restrict__ src, int count) {
+  const int nt = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + 3 * nt < count; i += 4 * nt) {
+    const double a = src[i], b = src[i + nt], c = src[i + 2 * nt], d = src[i + 3 * nt];
+    dst[i] = a;
+    dst[i + nt] = b;
+    dst[i + 2 * nt] = c;
+    dst[i + 3 * nt] = d;
+  }
+  for (; i < count; i += nt) dst[i] = src[i];
+}
+
 // A <- (A + A^T)/2
 BDDC_DEV void symmetrize(double* A, int ld, int n) {
   BLK_FOR_RC(n, n) {
@@ -190,31 +216,38 @@ BDDC_DEV int gj_inverse(double* A, int ld, int n, bool require_positive, double*
 // Cholesky A = L L^T in place (lower triangle).  Returns false when a pivot
 // is <= 0 or not finite (LAPACK potrf failure).
 BDDC_DEV bool cholesky(double* A, int ld, int n) {
-  __shared__ int bad;
-  if (tid() == 0) bad = 0;
-  __syncthreads();
+  // Right-looking with ONE barrier per column: step j updates the trailing
+  // lower triangle with the unscaled column, A[r][c] -= A[r][j] A[c][j] / d_j
+  // (column j is outside the trailing block, so nothing written in a step is
+  // read in the same step); the columns are scaled by 1 / sqrt(d_j) at the end.
+  // Every thread reads the same pivot after the barrier: uniform early exit.
+  bool ok = true;
   for (int j = 0; j < n; ++j) {
     const double d = A[j * ld + j];
     if (!(d > 0.0) || isinf(d)) {
-      if (tid() == 0) bad = 1;
-      __syncthreads();
+      ok = false;
       break;
     }
-    const double s = sqrt(d);
-    __syncthreads();
-    for (int i = j + 1 + tid(); i < n; i += nth()) A[i * ld + j] /= s;
-    if (tid() == 0) A[j * ld + j] = s;
-    __syncthreads();
+    const double id = 1.0 / d;
     const int m = n - j - 1;
     BLK_FOR_RC(m, m) {
       if (c <= r) {
-        int ri = j + 1 + r, ci = j + 1 + c;
-        A[ri * ld + ci] -= A[ri * ld + j] * A[ci * ld + j];
+        const int ri = j + 1 + r, ci = j + 1 + c;
+        A[ri * ld + ci] -= A[ri * ld + j] * A[ci * ld + j] * id;
       }
     }
     __syncthreads();
   }
-  bool ok = bad == 0;
+  if (ok) {
+    BLK_FOR_RC(n, n) {
+      if (c <= r) {
+        const double s = sqrt(A[c * ld + c]);
+        if (c < r) A[r * ld + c] /= s;
+      }
+    }
+    __syncthreads();
+    for (int j = tid(); j < n; j += nth()) A[j * ld + j] = sqrt(A[j * ld + j]);
+  }
   __syncthreads();
   return ok;
 }
@@ -613,7 +646,8 @@ BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, dou
       tau[k] = t;
       e[k] = beta;
     }
-    __syncthreads();
+    // (no barrier here: the product below reads v straight from column k of A,
+    // which this step only overwrites after the next barrier)
     if (t != 0.0) {
       // p = t * A22 v   (A22 = A[k+1:, k+1:], symmetric: use full stored block);
       // 4 lanes per row, each a strided quarter of the columns (short
@@ -623,7 +657,8 @@ BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, dou
         double s = 0.0;
         if (q < 4 * m) {
           const double* ar = A + (k + 1 + r) * ld + k + 1;
-          for (int c = part; c < m; c += 4) s += ar[c] * v[c];
+          const double* vc = A + (k + 1) * ld + k;
+          for (int c = part; c < m; c += 4) s += ar[c] * (c == 0 ? 1.0 : vc[c * ld] * scal);
         }
         s += __shfl_xor_sync(0xffffffffu, s, 1);
         s += __shfl_xor_sync(0xffffffffu, s, 2);
@@ -641,8 +676,9 @@ BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, dou
       }
     }
     // keep v_k below the subdiagonal for the back-transformation (column k is
-    // outside A22: no conflict with the update)
-    for (int i = 1 + tid(); i < m; i += nth()) A[(k + 1 + i) * ld + k] = v[i];
+    // outside A22: no conflict with the update); each thread stores the entries
+    // it computed itself
+    for (int i = 1 + tid(); i < m; i += nth()) A[(k + 1 + i) * ld + k] *= scal;
     __syncthreads();
   }
   for (int i = tid(); i < n; i += nth()) d[i] = A[i * ld + i];
@@ -730,12 +766,12 @@ BDDC_DEV void tridiag_eigvals(const double* d, const double* e, int n, double* w
   __syncthreads();
 }
 
-// Solve (T - lam I) x = b in place by Gaussian elimination with partial
-// pivoting on the tridiagonal (single thread; scratch u0,u1,u2,ml: n each,
-// pv: n ints).  Zero pivots are replaced by +-tiny.
-BDDC_DEV void tridiag_shift_solve(const double* d, const double* e, int n, double lam, double tiny,
-                                  double* x, double* u0, double* u1, double* u2, double* ml,
-                                  int* pv) {
+// (T - lam I) = P L U by Gaussian elimination with partial pivoting on the
+// tridiagonal (single thread; u0,u1,u2,ml: n doubles each, pv: n ints).  Zero
+// pivots are replaced by +-tiny; u0 returns the RECIPROCAL pivots, so that the
+// repeated solves of an inverse iteration need no division.
+BDDC_DEV void tridiag_shift_factor(const double* d, const double* e, int n, double lam, double tiny,
+                                   double* u0, double* u1, double* u2, double* ml, int* pv) {
   for (int i = 0; i < n; ++i) {
     u0[i] = d[i] - lam;
     u1[i] = (i < n - 1) ? e[i] : 0.0;
@@ -746,8 +782,9 @@ BDDC_DEV void tridiag_shift_solve(const double* d, const double* e, int n, doubl
     if (fabs(sub) > fabs(u0[k])) {
       const double a = u0[k], b = u1[k], c = u2[k];
       const double dn = u0[k + 1], s1 = u1[k + 1];
-      const double l = a / sub;
-      u0[k] = sub;
+      const double isub = 1.0 / sub;
+      const double l = a * isub;
+      u0[k] = isub;
       u1[k] = dn;
       u2[k] = s1;
       u0[k + 1] = b - l * dn;
@@ -756,7 +793,9 @@ BDDC_DEV void tridiag_shift_solve(const double* d, const double* e, int n, doubl
       pv[k] = 1;
     } else {
       if (u0[k] == 0.0) u0[k] = tiny;
-      const double l = sub / u0[k];
+      const double ip = 1.0 / u0[k];
+      const double l = sub * ip;
+      u0[k] = ip;
       u0[k + 1] -= l * u1[k];
       u1[k + 1] -= l * u2[k];
       ml[k] = l;
@@ -764,6 +803,12 @@ BDDC_DEV void tridiag_shift_solve(const double* d, const double* e, int n, doubl
     }
   }
   if (u0[n - 1] == 0.0) u0[n - 1] = tiny;
+  u0[n - 1] = 1.0 / u0[n - 1];
+}
+
+// x <- (T - lam I)^-1 x with the factors of tridiag_shift_factor
+BDDC_DEV void tridiag_shift_solve(int n, double* x, const double* u0, const double* u1,
+                                  const double* u2, const double* ml, const int* pv) {
   for (int k = 0; k < n - 1; ++k) {
     if (pv[k]) {
       const double t = x[k];
@@ -777,7 +822,7 @@ BDDC_DEV void tridiag_shift_solve(const double* d, const double* e, int n, doubl
     double s = x[i];
     if (i + 1 < n) s -= u1[i] * x[i + 1];
     if (i + 2 < n) s -= u2[i] * x[i + 2];
-    x[i] = s / u0[i];
+    x[i] = s * u0[i];
   }
 }
 
@@ -817,8 +862,9 @@ BDDC_DEV void tridiag_eigvecs(const double* d, const double* e, int n, const dou
       const bool isolated = (j == j0) && (wi == 0 || w[wi] - w[wi - 1] > 1e-3 * tn) &&
                             (wi == n - 1 || w[wi + 1] - w[wi] > 1e-3 * tn);
       const int iters = isolated ? 3 : 5;
+      tridiag_shift_factor(d, e, n, lam, tiny, u0, u1, u2, ml, pv);  // once per shift
       for (int it = 0; it < iters; ++it) {
-        tridiag_shift_solve(d, e, n, lam, tiny, x, u0, u1, u2, ml, pv);
+        tridiag_shift_solve(n, x, u0, u1, u2, ml, pv);
         // orthogonalise against the earlier members of the cluster
         for (int q = j0; q < j; ++q) {
           double dot = 0.0;

@@ -691,11 +691,34 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   const double* Bj = t.BsC + t.sh_doff[k0 + 1];
   const int ldi = n, ldj = n;
   PROF_INIT
-  // 1. B_F = sym(Dj^T Bi Dj + Di^T Bj Di)
-  blk::gemm(S1, n, Bi, ldi, false, Dj, n, false, n, n, n, 1.0, 0.0);
-  blk::gemm(S0, n, Dj, n, true, S1, n, false, n, n, n, 1.0, 0.0);
-  blk::gemm(S1, n, Bj, ldj, false, Di, n, false, n, n, n, 1.0, 0.0);
-  blk::gemm(S0, n, Di, n, true, S1, n, false, n, n, n, 1.0, 1.0);
+  // 1. B_F = sym(Dj^T Bi Dj + Di^T Bj Di); with the arena in shared memory the
+  // four operand blocks are staged there first (coalesced, one latency) so the
+  // DMMA fragments of the products come from shared memory
+  if (arena_in_smem) {
+    // every cold input block of this face is requested from DRAM now
+    blk::prefetch_l2(Di, nn);
+    if (t.SC != nullptr && n <= kTile) {
+      blk::prefetch_l2(t.BiC + t.sh_doff[k0], nn);
+      blk::prefetch_l2(t.BiC + t.sh_doff[k0 + 1], nn);
+      blk::prefetch_l2(t.SC + t.sh_doff[k0], nn);
+      blk::prefetch_l2(t.SC + t.sh_doff[k0 + 1], nn);
+    }
+    blk::copy_flat4(S2, Bi, nn);
+    blk::copy_flat4(S3, Dj, nn);
+    blk::copy_flat4(S4, Bj, nn);
+    __syncthreads();
+    blk::gemm(S1, n, S2, n, false, S3, n, false, n, n, n, 1.0, 0.0);
+    blk::gemm(S0, n, S3, n, true, S1, n, false, n, n, n, 1.0, 0.0);
+    blk::copy_flat4(S3, Di, nn);
+    __syncthreads();
+    blk::gemm(S1, n, S4, n, false, S3, n, false, n, n, n, 1.0, 0.0);
+    blk::gemm(S0, n, S3, n, true, S1, n, false, n, n, n, 1.0, 1.0);
+  } else {
+    blk::gemm(S1, n, Bi, ldi, false, Dj, n, false, n, n, n, 1.0, 0.0);
+    blk::gemm(S0, n, Dj, n, true, S1, n, false, n, n, n, 1.0, 0.0);
+    blk::gemm(S1, n, Bj, ldj, false, Di, n, false, n, n, n, 1.0, 0.0);
+    blk::gemm(S0, n, Di, n, true, S1, n, false, n, n, n, 1.0, 1.0);
+  }
   blk::symmetrize(S0, n, n);
   PROF(0);
   const double nb = sqrt(blk::frob2(S0, n, n, n, red));
@@ -727,17 +750,31 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
     // block reduction
     __shared__ double fred[(256 / 32) * 5];
     double q[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-    for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
-      const int r = idx / n, c = idx - r * n;
-      const double xi = Xi[idx], xj = Xj[idx];
-      const double v = 0.5 * ((xi + Xi[c * n + r]) + (xj + Xj[c * n + r]));
-      S1[idx] = v;
-      const double si = SCi[idx], sj = SCj[idx];
-      q[0] = fma(si, si, q[0]);
-      q[1] = fma(sj, sj, q[1]);
-      q[2] = fma(xi, xi, q[2]);
-      q[3] = fma(xj, xj, q[3]);
-      q[4] = fma(v, v, q[4]);
+    for (int i0 = threadIdx.x; i0 < nn; i0 += 2 * blockDim.x) {
+      // two entries per trip: twelve independent loads before the first store
+      const int i1 = i0 + blockDim.x;
+      const bool two = i1 < nn;
+      const int r0 = i0 / n, c0 = i0 - r0 * n;
+      const int r1 = two ? i1 / n : 0, c1 = two ? i1 - r1 * n : 0;
+      const double xi0 = Xi[i0], xj0 = Xj[i0], ti0 = Xi[c0 * n + r0], tj0 = Xj[c0 * n + r0];
+      const double si0 = SCi[i0], sj0 = SCj[i0];
+      const double xi1 = two ? Xi[i1] : 0.0, xj1 = two ? Xj[i1] : 0.0;
+      const double ti1 = two ? Xi[c1 * n + r1] : 0.0, tj1 = two ? Xj[c1 * n + r1] : 0.0;
+      const double si1 = two ? SCi[i1] : 0.0, sj1 = two ? SCj[i1] : 0.0;
+      const double v0 = 0.5 * ((xi0 + ti0) + (xj0 + tj0));
+      const double v1 = 0.5 * ((xi1 + ti1) + (xj1 + tj1));
+      S1[i0] = v0;
+      if (two) S1[i1] = v1;
+      q[0] = fma(si0, si0, q[0]);
+      q[1] = fma(sj0, sj0, q[1]);
+      q[2] = fma(xi0, xi0, q[2]);
+      q[3] = fma(xj0, xj0, q[3]);
+      q[4] = fma(v0, v0, q[4]);
+      q[0] = fma(si1, si1, q[0]);
+      q[1] = fma(sj1, sj1, q[1]);
+      q[2] = fma(xi1, xi1, q[2]);
+      q[3] = fma(xj1, xj1, q[3]);
+      q[4] = fma(v1, v1, q[4]);
     }
 #pragma unroll
     for (int i = 0; i < 5; ++i)

@@ -612,6 +612,19 @@ def _edge_new_ws(ns, ne, wd, nhmax):
     return base + sc + 32 * nC + 64
 
 
+def _edge_new_ws_t(ns, ne, wd, nhmax):
+    """_edge_new_ws on int64 device tensors."""
+    mx = torch.maximum
+    nC = (ns - 1) * ne
+    nr = wd - nC
+    xd = ne + nhmax
+    base = ns * ne * nC + nC * nC + wd * wd + xd * xd + 2 * wd * wd
+    m, n = nC * (ns - 1), ne
+    rs = 2 * n * n + n + mx(m, n) + torch.where(m <= n, n * m, m * n + n * n)
+    sc = mx(mx(8 * nC * nC + 3 * nC, 3 * nr * nr + nr), rs)
+    return base + sc + 32 * nC + 64
+
+
 class DevicePrimalSpace:
     """Per-glob (Q, r) and eigenvalues produced on the device
     (reference adaptive.py:288-342 / PrimalBasis adaptive.py:209-264)."""
@@ -664,27 +677,64 @@ class DevicePrimalSpace:
         self.sc_status = torch.zeros(max(int(p.sh_sub.size), 1), dtype=torch.int32, device="cuda")
         lib.bddc_slot_schur(dev_i32(sc_slots), sc_slots.size, d.slot_glob, d.gsize, d.sh_doff, BiC,
                             self.SC, self.sc_status, st)
+        vert = np.flatnonzero(kind == 2)
+
+        def set_vertices():  # vertices are fully primal: 1x1 identity, r = 1
+            if vert.size:
+                self.Q[dev_i64(self.q_off[vert])] = 1.0
+                self.r[dev_i64(vert)] = dev_i32(p.gsize[vert])
+
+        if not multi:  # (sharded: after the face results are summed over the ranks)
+            set_vertices()
+        n_edges_all = int((kind == 1).sum())
+        # one rank, new edges: the sizes that depend on the face results (prior
+        # counts -> PB / XHH / EX offsets, edge workspaces) are computed on the
+        # device behind the face kernel, so only their totals cross to the host
+        dev_sizes = n_edges_all and variant == "new" and not multi and edges.size
+        sz = None
         if faces.size and self.general:
             self._run_faces(faces, -1, out, scaling, BsC, BiC, d_eig_off)
         elif faces.size:
             self._run_faces(faces, 1, out, scaling, BsC, BiC, d_eig_off)
+            if dev_sizes:
+                sz = self._new_edge_sizes(edges, nsh)
             s = status.cpu().numpy()
             redo = faces[s[faces] == 900]
             if redo.size:  # certificates failed: general algorithm (linalg.py:116-214)
                 status[dev_i64(redo)] = 0
                 self._run_faces(redo, 0, out, scaling, BsC, BiC, d_eig_off)
+                sz = None
         if multi:
             self._share_results(out)
+            set_vertices()
         self._raise(status, "face")
-        vert = np.flatnonzero(kind == 2)
-        if vert.size:  # vertices are fully primal: 1x1 identity, r = 1
-            self.Q[dev_i64(self.q_off[vert])] = 1.0
-            self.r[dev_i64(vert)] = dev_i32(p.gsize[vert])
-        r_host = self.r.cpu().numpy()
-        n_edges_all = int((kind == 1).sum())
         # edge results of all ranks are summed into zeroed buffers, then added
         eout = tuple(torch.zeros_like(t) for t in out) if multi else out
-        if n_edges_all and variant == "new":
+        if dev_sizes:
+            if sz is None:
+                sz = self._new_edge_sizes(edges, nsh)
+            tot = sz["totals"].cpu().numpy()
+            PB = torch.empty(max(int(tot[0]), 1), dtype=F64, device="cuda")
+            XHH = torch.empty(max(int(tot[1]), 1), dtype=F64, device="cuda")
+            lib.bddc_priors(d.kind, d.gsize, d.nB, d.soff, ls.bsym_inverse(), d.sub_glob_start,
+                            d.sub_globs, d.sub_glob_boff, self.r, self.Q, self.d_q_off, sz["pb_off"],
+                            sz["nH"], PB, XHH, sz["xhh_off"], p.N, st)
+            EX = torch.empty(max(int(tot[2]), 1), dtype=F64, device="cuda")
+            lib.bddc_edge_x_extract(d.slot_local, d.slot_glob, d.gsize, d.kind, d.sh_boff, d.nB,
+                                    d.soff, ls.bsym_inverse(), sz["pb_off"], sz["nH"], PB, XHH,
+                                    sz["xhh_off"], EX, sz["ex_off"], int(p.sh_sub.size), st)
+            del PB, XHH
+            ws = torch.empty(max(int(tot[3]), 1), dtype=F64, device="cuda")
+            e_eig, e_nsel, e_r, e_Q, e_status = eout
+            lib.bddc_edge_gevp_new(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff,
+                                   BsC, BiC, self.SC, self.sc_status, scaling.D, EX, sz["ex_off"],
+                                   sz["sh_nH"], self.theta_e, e_eig, d_eig_off, e_nsel, e_r, e_Q,
+                                   self.d_q_off, e_status, ws, sz["woff"], dev_i32(edges),
+                                   edges.size, int(tot[4]), int(self.general), self.detail,
+                                   self.d_det_off, st)
+            del ws, EX
+        elif n_edges_all and variant == "new":
+            r_host = self.r.cpu().numpy()
             # prior sizes per subdomain: vertices + leading r_F of each face
             sh = p.sh_sub.astype(np.int64)
             contrib = np.where(kind == 2, p.gsize, np.where(kind == 0, r_host[:G], 0))[p.slot_glob]
@@ -754,6 +804,37 @@ class DevicePrimalSpace:
         self.r_host = self.r.cpu().numpy().astype(np.int64)
         self.n_sel_host = self.n_sel.cpu().numpy().astype(np.int64)
         del self.SC
+
+    def _new_edge_sizes(self, edges, nsh):
+        """Device-side sizing of the new-edge phase from the face results
+        (self.r): prior counts nH per subdomain, offsets of PB (nH x nB), XHH
+        (nH x nH) and of the per-slot X blocks ((n_e + nH)^2), the edge
+        workspaces (_edge_new_ws) and their totals [PB, XHH, EX, ws, max wd]."""
+        p, d = self.ls.plan, self.ls.d
+        i64 = torch.int64
+
+        def excl(t):
+            return torch.cumsum(t, 0) - t
+
+        kind, gs, sg, sh = d.kind.to(i64), d.gsize.to(i64), d.slot_glob.to(i64), d.sh_sub.to(i64)
+        r = self.r[:p.G].to(i64)
+        zero = torch.zeros((), dtype=i64, device="cuda")
+        contrib = torch.where(kind == 2, gs, torch.where(kind == 0, r, zero))[sg]
+        nH = torch.zeros(p.N_glob, dtype=i64, device="cuda").index_add_(0, sh, contrib)
+        pb_sz, xhh_sz = nH * d.nB.to(i64), nH * nH
+        sh_nH = nH[sh]
+        ex_sz = torch.where(kind[sg] == 1, (gs[sg] + sh_nH) ** 2, zero)
+        sumH = torch.zeros(p.G, dtype=i64, device="cuda").index_add_(0, sg, sh_nH)
+        maxH = torch.zeros(p.G, dtype=i64, device="cuda").scatter_reduce_(0, sg, sh_nH, "amax")
+        e = dev_i64(edges)
+        ns, ne = dev_i64(nsh[edges]), gs[e]
+        wd = (ns - 1) * ne + ne + sumH[e]
+        wsz = _edge_new_ws_t(ns, ne, wd, maxH[e])
+        woff = torch.zeros(p.G, dtype=i64, device="cuda")
+        woff[e] = excl(wsz)
+        totals = torch.stack([pb_sz.sum(), xhh_sz.sum(), ex_sz.sum(), wsz.sum(), wd.max()])
+        return dict(nH=nH.to(torch.int32), pb_off=excl(pb_sz), xhh_off=excl(xhh_sz),
+                    ex_off=excl(ex_sz), sh_nH=sh_nH.to(torch.int32), woff=woff, totals=totals)
 
     def _share_results(self, out):
         """Sharded path: per-glob counts, eigenvalues and status are small and

@@ -77,11 +77,16 @@ class Plan:
         self.n_nodes = system.mesh.n_nodes
         self.n_hat = int(np.asarray(globs.interface_nodes).size)
         self.on_device = device_inputs is not None
+        self._iface_nodes = np.asarray(globs.interface_nodes, dtype=np.int64)
+        if self.on_device:
+            # the sorts of the element part are queued first and run while the
+            # host builds the glob part
+            self._element_pre_torch(system, device_inputs, s1 - s0)
         self._glob_part(globs)
         self._restrict(s0, s1)
         if self.on_device:
             self._interface_maps_torch(device_inputs["conn"].device)
-            self._element_part_torch(system, partition, device_inputs)
+            self._element_post_torch(device_inputs)
         else:
             self._interface_maps_numpy()
             self._element_part_numpy(system, partition)
@@ -136,7 +141,6 @@ class Plan:
         self._B_range = (0, int(sizes_k.sum()))
         self._B_nodes = None
         self.pos2k = np.repeat(np.arange(self.sub_globs.size, dtype=np.int32), sizes_k)
-        self._iface_nodes = np.asarray(globs.interface_nodes, dtype=np.int64)
 
     def _restrict(self, s0, s1):
         """Keep subdomains s0..s1-1 (local ids 0..s1-s0-1)."""
@@ -243,12 +247,12 @@ class Plan:
         found = keys[pos] == q
         return np.where(found, vals[pos], np.int64(2 ** 30)).astype(np.int32)
 
-    def _element_part_torch(self, system, partition, dev):
+    def _element_pre_torch(self, system, dev, N):
+        """Device work of the element part that needs no glob table: interior
+        dofs (deep first), their counts, the element order.  No host sync."""
         import torch
 
-        from ._lib import lib, stream
-
-        N, n_nodes = self.N, self.n_nodes
+        n_nodes = self.n_nodes
         s0 = self.owned[0]
         conn = dev["conn"]                 # (E_local, 4) int64 on the GPU, input order
         sub_g = dev["sub_of"]              # (E_local,) global subdomain ids
@@ -257,6 +261,7 @@ class Plan:
         free = dev.get("free")
         if free is None:
             free = _up(np.asarray(system.node_to_free) >= 0, dv)
+        self._iface_nodes_d = _up(self._iface_nodes, dv)
         # interior nodes: free, not on the interface, touched by a (single) local
         # subdomain -- its owner, read off any element containing it
         owner = torch.full((n_nodes,), -1, dtype=torch.int64, device=dv)
@@ -273,22 +278,32 @@ class Plan:
         sh_all = (shell[I_all] > 0).to(torch.int64)
         o = torch.sort(I_sub_all * 2 + sh_all, stable=True).indices
         I_node, I_sub = I_all[o], I_sub_all[o]
-        cnt = torch.bincount(I_sub * 2 + sh_all[o], minlength=2 * N).view(N, 2)
-        nI = cnt.sum(dim=1)
-        cnt_h = cnt.cpu().numpy().astype(np.int64)
+        self._cnt_d = torch.bincount(I_sub * 2 + sh_all[o], minlength=2 * N).view(N, 2)
+        self.I_nodes_d, self._I_sub_d = I_node, I_sub
+        self.elem_ids_d = torch.sort(sub_of, stable=True).indices
+        self._ecnt_d = torch.bincount(sub_of, minlength=N)
+
+    def _element_post_torch(self, dev):
+        import torch
+
+        from ._lib import lib, stream
+
+        N, n_nodes = self.N, self.n_nodes
+        conn, dv = dev["conn"], dev["conn"].device
+        cnt_h = self._cnt_d.cpu().numpy().astype(np.int64)
         self.nI = cnt_h.sum(axis=1)
         self.nDeep = cnt_h[:, 0] & ~np.int64(1)
         self.ioff = _excl(self.nI)
-        self.I_nodes_d = I_node
+        self.elem_start = _excl(self._ecnt_d.cpu().numpy())
+        I_node, I_sub = self.I_nodes_d, self._I_sub_d
         iloc = torch.full((n_nodes,), -1, dtype=torch.int32, device=dv)
         iloc[I_node] = (torch.arange(I_node.numel(), device=dv) - _up(self.ioff, dv)[I_sub]).to(torch.int32)
-        eorder = torch.sort(sub_of, stable=True).indices
-        self.elem_ids_d = eorder
-        self.elem_start = _excl(torch.bincount(sub_of, minlength=N).cpu().numpy())
         self.loc4_d = torch.empty((conn.shape[0], 4), dtype=torch.int32, device=dv)
-        lib.bddc_plan_loc4(conn, sub_g, conn.shape[0], s0, iloc, self._glob_of_node_d,
-                           self._pos_in_glob_d, _up(self.sh_start, dv), _up(self.sh_sub, dv),
-                           _up(self.sh_boff, dv), nI.to(torch.int64), self.loc4_d, stream())
+        lib.bddc_plan_loc4(conn, dev["sub_of"], conn.shape[0], self.owned[0], iloc,
+                           self._glob_of_node_d, self._pos_in_glob_d, _up(self.sh_start, dv),
+                           _up(self.sh_sub, dv), _up(self.sh_boff, dv),
+                           _up(self.nI, dv), self.loc4_d, stream())
+        del self._cnt_d, self._ecnt_d, self._I_sub_d
 
     def _node_maps_device(self, dv):
         """node -> glob index and position in the glob (-1 off the interface),
@@ -307,7 +322,6 @@ class Plan:
         pos[gn] = (torch.arange(gn.numel(), device=dv) - gst[gid]).to(torch.int32)
         self._glob_of_node_d = gof
         self._pos_in_glob_d = pos
-        self._iface_nodes_d = _up(self._iface_nodes, dv)
 
     def _layout(self):
         self.nL = self.nI + self.nB
