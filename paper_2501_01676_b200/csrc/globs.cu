@@ -644,23 +644,235 @@ __global__ void __launch_bounds__(256) face_kernel(GlobTables t, const double* _
 }
 
 // ---------------------------------------------------------------------------
-// Face eigenproblem, certified fast path only, in a compact shared-memory
-// arena (5 n^2 + vector region) so that two faces of 49 dofs run per SM.
-// Faces whose certificates fail get status kNeedFallback and are re-run by
-// face_kernel (general algorithm) in a second launch.
+// Face eigenproblem, certified fast path only.  Faces whose certificates fail
+// get status kNeedFallback and are re-run by face_kernel (general algorithm)
+// in a second launch.
+//  * n <= 64 (the per-slot glob Schur blocks SC exist): THREE n x n regions
+//    (A, B, C) plus vectors, so that three faces of 49 dofs run per SM:
+//      C = B_F;  A = chol(Bt_i^-1 + Bt_j^-1) = Lw;  B = B_F Lw;  C = Lw^T B = Bh
+//      C -> tridiagonal (reflectors stay in C), eigenvalues by bisection,
+//      A = selected eigenvectors X (n x k), back-transformed with C,
+//      C = (B X) Lambda^-1/2 = (constraint rows)^T,  basis from C with A, B
+//    (the constraint rows (B_F V)^T with V = Lw X Lambda^-1/2 need no V).
+//  * n > 64: glob Schur blocks formed here, five regions (global workspace).
 // ---------------------------------------------------------------------------
 constexpr int kNeedFallback = 900;
 
 __host__ __device__ inline long long face_fast_arena(long long n) {
-  return 5 * n * n + 4 * n + (long long)blk::kIILanes * 6 * n + 4 * n + 32;
+  return (n <= kTile ? 3 : 5) * n * n + 4 * n + (long long)blk::kIILanes * 6 * n + 4 * n + 32;
 }
 
-__global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const double* __restrict__ D,
-                                                        double theta, GlobOut o,
-                                                        double* __restrict__ ws,
-                                                        const long long* __restrict__ ws_off,
-                                                        const int* __restrict__ face_ids,
-                                                        int arena_in_smem, int max_n) {
+// Right singular basis from the TRANSPOSED rows X (n x m, m <= n; destroyed):
+// row_space_basis with caller-placed workspaces U, H (n x n each), vb, sg (n each)
+BDDC_DEV int row_space_basis_t(double* X, int m, int n, double* Q, double* U, double* H,
+                               double* vb, double* sg, double* cs, int* perm, double* red) {
+  __shared__ int s_rt;
+  if (m == 0) {
+    blk::set_identity(Q, n, n, n);
+    return 0;
+  }
+  blk::onesided_jacobi(X, m, n, m, nullptr, 0, cs, perm, red);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n; ++r) s += X[r * m + j] * X[r * m + j];
+    sg[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    int rank = 0;
+    for (int i = 0; i < m; ++i) rank += (sg[i] > sg[j]) || (sg[i] == sg[j] && i < j);
+    perm[j] = rank;
+  }
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < m; ++i) mx = fmax(mx, sg[i]);
+    int r = 0;
+    for (int i = 0; i < m; ++i) r += sg[i] >= 1e-10 * mx;
+    s_rt = (mx > 0.0) ? r : 0;
+  }
+  __syncthreads();
+  const int r = s_rt;
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    const int o = perm[j];
+    if (o >= r) continue;
+    const double inv = 1.0 / sg[j];
+    for (int c = 0; c < n; ++c) U[o * n + c] = X[c * m + j] * inv;
+  }
+  __syncthreads();
+  blk::complete_basis(U, n, r, n, Q, n, H, n, vb, red);
+  return r;
+}
+
+// n <= 64 path in three regions (see above); W: 3 n^2 + vectors
+BDDC_DEV void face_fast_small(const GlobTables& t, const double* __restrict__ D, double theta,
+                              const GlobOut& o, int g, int n, double* W, double* cs, double* red,
+                              int* perm, bool prefetch) {
+  const int nn = n * n;
+  double* A = W;
+  double* B = A + nn;
+  double* C = B + nn;
+  double* dd = C + nn;
+  double* ee = dd + n;
+  double* tau = ee + n;
+  double* w = tau + n;
+  double* scr = w + n;                                              // kIILanes * 5 n
+  int* iscr = reinterpret_cast<int*>(scr + blk::kIILanes * 5 * n);  // kIILanes * n ints
+  double* vb = scr + blk::kIILanes * 6 * n;
+  double* sg = vb + n;
+  const int k0 = t.sh_start[g];
+  const double* Di = D + t.sh_doff[k0];
+  const double* Dj = D + t.sh_doff[k0 + 1];
+  const double* Bi = t.BsC + t.sh_doff[k0];
+  const double* Bj = t.BsC + t.sh_doff[k0 + 1];
+  const double* Xi = t.BiC + t.sh_doff[k0];
+  const double* Xj = t.BiC + t.sh_doff[k0 + 1];
+  const double* SCi = t.SC + t.sh_doff[k0];
+  const double* SCj = t.SC + t.sh_doff[k0 + 1];
+  PROF_INIT
+  if (t.sc_status[k0]) {
+    if (threadIdx.x == 0) o.status[g] = 100;
+    return;
+  }
+  if (t.sc_status[k0 + 1]) {
+    if (threadIdx.x == 0) o.status[g] = 101;
+    return;
+  }
+  if (prefetch) {  // every cold input block of this face is requested from DRAM now
+    blk::prefetch_l2(Di, nn);
+    blk::prefetch_l2(Bj, nn);
+    blk::prefetch_l2(Xi, nn);
+    blk::prefetch_l2(Xj, nn);
+    blk::prefetch_l2(SCi, nn);
+    blk::prefetch_l2(SCj, nn);
+  }
+  // 1. B_F = sym(Dj^T Bi Dj + Di^T Bj Di) -> C
+  blk::copy_flat4(B, Dj, nn);
+  blk::copy_flat4(C, Bi, nn);
+  __syncthreads();
+  blk::gemm(A, n, C, n, false, B, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(C, n, B, n, true, A, n, false, n, n, n, 1.0, 0.0);
+  blk::copy_flat4(B, Di, nn);
+  __syncthreads();
+  blk::gemm(A, n, Bj, n, false, B, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(C, n, B, n, true, A, n, false, n, n, n, 1.0, 1.0);
+  blk::symmetrize(C, n, n);
+  PROF(0);
+  const double nb = sqrt(blk::frob2(C, n, n, n, red));
+  // 2. The parallel sum's inverse is the sum of the inverses:
+  //   Bt^-1 = Bt_i^-1 + Bt_j^-1 = (Bsym_i^-1)[F,F] + (Bsym_j^-1)[F,F],
+  // so Bt needs no inverse: Bt^-1 = Lw Lw^T (Cholesky) whitens the pencil,
+  // Bh = Lw^T B_F Lw.  Certificates (Frobenius bounds on the extreme
+  // eigenvalues): cond(Bt_i + Bt_j) < 1e11 (the reference's pinv is the
+  // inverse, linalg.py:44-48) and cond(Bt) < 1e11 (no null / degenerate
+  // modes, linalg.py:153); otherwise the general kernel re-runs the face.
+  __shared__ double fred[(256 / 32) * 5];
+  double q[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int i0 = threadIdx.x; i0 < nn; i0 += 2 * blockDim.x) {
+    // two entries per trip: twelve independent loads before the first store
+    const int i1 = i0 + blockDim.x;
+    const bool two = i1 < nn;
+    const int r0 = i0 / n, c0 = i0 - r0 * n;
+    const int r1 = two ? i1 / n : 0, c1 = two ? i1 - r1 * n : 0;
+    const double xi0 = Xi[i0], xj0 = Xj[i0], ti0 = Xi[c0 * n + r0], tj0 = Xj[c0 * n + r0];
+    const double si0 = SCi[i0], sj0 = SCj[i0];
+    const double xi1 = two ? Xi[i1] : 0.0, xj1 = two ? Xj[i1] : 0.0;
+    const double ti1 = two ? Xi[c1 * n + r1] : 0.0, tj1 = two ? Xj[c1 * n + r1] : 0.0;
+    const double si1 = two ? SCi[i1] : 0.0, sj1 = two ? SCj[i1] : 0.0;
+    const double v0 = 0.5 * ((xi0 + ti0) + (xj0 + tj0));
+    const double v1 = 0.5 * ((xi1 + ti1) + (xj1 + tj1));
+    A[i0] = v0;
+    if (two) A[i1] = v1;
+    q[0] = fma(si0, si0, q[0]);
+    q[1] = fma(sj0, sj0, q[1]);
+    q[2] = fma(xi0, xi0, q[2]);
+    q[3] = fma(xj0, xj0, q[3]);
+    q[4] = fma(v0, v0, q[4]);
+    q[0] = fma(si1, si1, q[0]);
+    q[1] = fma(sj1, sj1, q[1]);
+    q[2] = fma(xi1, xi1, q[2]);
+    q[3] = fma(xj1, xj1, q[3]);
+    q[4] = fma(v1, v1, q[4]);
+  }
+#pragma unroll
+  for (int i = 0; i < 5; ++i)
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) q[i] += __shfl_xor_sync(0xffffffffu, q[i], o2);
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) fred[(threadIdx.x >> 5) * 5 + i] = q[i];
+  __syncthreads();
+  double tq[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int wi = 0; wi < (int)(blockDim.x >> 5); ++wi)
+#pragma unroll
+    for (int i = 0; i < 5; ++i) tq[i] += fred[wi * 5 + i];
+  __syncthreads();
+  const double nsi = sqrt(tq[0]), nsj = sqrt(tq[1]), nxi = sqrt(tq[2]), nxj = sqrt(tq[3]);
+  const double nx = sqrt(tq[4]);
+  const double cond_m = (nsi + nsj) / (1.0 / nxi + 1.0 / nxj);
+  const double cond_x = nx / (1.0 / nsi + 1.0 / nsj);
+  if (!(nsi > 0.0) || !(nsj > 0.0) || !(nxi > 0.0) || !(nxj > 0.0) ||
+      !(cond_m < 1e11) || !(cond_x < 1e11) || !(theta > 1e-14 * nb) ||
+      !blk::cholesky(A, n, n)) {
+    if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+    return;
+  }
+  PROF(2);
+  for (int idx = threadIdx.x; idx < nn; idx += blockDim.x) {
+    const int r = idx / n, c = idx - r * n;
+    if (c > r) A[idx] = 0.0;
+  }
+  __syncthreads();
+  PROF(3);
+  // 3. B = B_F Lw, Bh = Lw^T B -> C (B_F is not needed again: the constraint rows
+  // come from B)
+  blk::gemm(B, n, C, n, false, A, n, false, n, n, n, 1.0, 0.0);
+  blk::gemm(C, n, A, n, true, B, n, false, n, n, n, 1.0, 0.0);
+  PROF(4);
+  blk::symmetrize(C, n, n);
+  PROF(5);
+  blk::tridiagonalize(C, n, n, dd, ee, tau, scr, red);
+  PROF(6);
+  blk::tridiag_eigvals(dd, ee, n, w, red);
+  PROF(7);
+  double* vals = o.eig + o.eig_off[g];
+  __shared__ int s_k;
+  if (threadIdx.x == 0) {
+    int k = 0;
+    for (int j = n - 1; j >= 0 && w[j] >= theta; --j) perm[k++] = j;
+    s_k = k;
+  }
+  for (int j = threadIdx.x; j < n; j += blockDim.x) vals[n - 1 - j] = w[j];
+  __syncthreads();
+  const int k = s_k;
+  if (k > 0) {
+    blk::tridiag_eigvecs(dd, ee, n, w, perm, k, A, scr, iscr);
+    blk::apply_householder(C, n, n, tau, A, k, k);
+    // (rows)^T (n x k) = B_F V = (B_F Lw) X Lambda^-1/2 -> C (the reflectors are done)
+    for (int idx = threadIdx.x; idx < n * k; idx += blockDim.x) {
+      const int r = idx / k, qq = idx - r * k;
+      double s = 0.0;
+      for (int tt = 0; tt < n; ++tt) s += B[r * n + tt] * A[tt * k + qq];
+      C[idx] = s / sqrt(fabs(w[perm[qq]]));
+    }
+    __syncthreads();
+  }
+  PROF(8);
+  // 4. change of basis from the constraint rows
+  const int r = row_space_basis_t(C, k, n, o.Q + o.q_off[g], A, B, vb, sg, cs, perm, red);
+  PROF(9);
+  if (threadIdx.x == 0) {
+    o.n_sel[g] = k;
+    o.r[g] = r;
+  }
+}
+
+// SMALL: every face of the launch has n <= 64 and its arena in shared memory
+// (three CTAs per SM: <= 80 registers); otherwise both paths, global workspace
+template <bool SMALL>
+__global__ void __launch_bounds__(256, SMALL ? 3 : 1) face_fast_kernel(
+    GlobTables t, const double* __restrict__ D, double theta, GlobOut o, double* __restrict__ ws,
+    const long long* __restrict__ ws_off, const int* __restrict__ face_ids, int arena_in_smem,
+    int max_n) {
   extern __shared__ double sh[];
   const int g = face_ids[blockIdx.x];
   const int n = t.size[g];
@@ -672,6 +884,15 @@ __global__ void __launch_bounds__(256) face_fast_kernel(GlobTables t, const doub
   int* degen = perm + 2 * (max_n + 2);                   // max_n + 2
   double* W = arena_in_smem ? reinterpret_cast<double*>(degen + ((max_n + 2 + 1) & ~1))
                             : ws + ws_off[g];
+  if (n <= kTile) {
+    if (t.SC == nullptr) {  // the three-region path needs the slot Schur blocks
+      if (threadIdx.x == 0) o.status[g] = kNeedFallback;
+      return;
+    }
+    face_fast_small(t, D, theta, o, g, n, W, cs, red, perm, arena_in_smem != 0);
+    return;
+  }
+  if (SMALL) return;  // (not reached: the launcher sends n > 64 to the other instantiation)
   double* S0 = W;            // B_F
   double* S1 = S0 + nn;      // scratch / Bt_i / L^-1 / rows
   double* S2 = S1 + nn;      // Bt_j / L^-1 B_F / eigenvectors
@@ -1583,8 +1804,17 @@ int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const 
     const long long arena = face_fast_arena(max_n) * 8;
     const int in_smem = (small + arena) <= kFaceFastSmemBudget;
     const int smem = small + (in_smem ? (int)arena : 0);
-    if (smem > 48 * 1024) cudaFuncSetAttribute(face_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    face_fast_kernel<<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids, in_smem, max_n);
+    if (in_smem && max_n <= kTile) {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(face_fast_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      face_fast_kernel<true><<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids,
+                                                            in_smem, max_n);
+    } else {
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(face_fast_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      face_fast_kernel<false><<<n_faces, 256, smem, stream>>>(t, D, theta, o, ws, ws_off, face_ids,
+                                                             in_smem, max_n);
+    }
   } else {
     const long long arena = face_arena(max_n) * 8;
     const int in_smem = (small + arena) <= kFaceSmemBudget;

@@ -155,16 +155,17 @@ BDDC_DEV void cols_gemv(const double* __restrict__ A, long long lda, int m, int 
   __syncthreads();
 }
 
-// Eight right-hand sides on the DMMA pipe (mma.sync m8n8k4.f64):
-//   Y[r][q] = beta * Y[r][q] + alpha * sum_c op(A)[r][c] X[c][q]   (r < m, c < k, q < 8)
+// NR = 8 or 16 right-hand sides on the DMMA pipe (mma.sync m8n8k4.f64):
+//   Y[r][q] = beta * Y[r][q] + alpha * sum_c op(A)[r][c] X[c][q]   (r < m, c < k, q < NR)
 // op(A) = A (m x k, TA = false) or A^T (A stored k x m, TA = true).  A warp
-// owns 8-row units (one 8 x 8 accumulator each), up to four at a time sharing
-// the X fragment, fragments straight from global memory (32-byte row
+// owns 8-row units (NR / 8 accumulators each, sharing the A fragment), up to
+// four at a time, A fragments straight from global memory (32-byte row
 // segments, every sector fully used) and X from shared memory: no shuffle
 // reductions, unlike the warp-per-row products above.  Ends with a barrier.
-template <bool TA>
-BDDC_DEV void panel_mma8(const double* __restrict__ A, long long lda, int m, int k,
-                         const double* X, int xs, double* Y, int ys, double alpha, double beta) {
+template <int NR, bool TA>
+BDDC_DEV void panel_mma(const double* __restrict__ A, long long lda, int m, int k,
+                        const double* X, int xs, double* Y, int ys, double alpha, double beta) {
+  constexpr int NB = NR / 8;
   const int warp = (int)(threadIdx.x >> 5), lane = (int)(threadIdx.x & 31);
   const int nw = (int)(blockDim.x >> 5);
   const int g = lane >> 2, t = lane & 3;
@@ -177,12 +178,18 @@ BDDC_DEV void panel_mma8(const double* __restrict__ A, long long lda, int m, int
       on[i] = u0 + i * nw < mt;  // warp-uniform
       rr[i] = (u0 + i * nw) * 8 + g;
     }
-    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    double acc[4][NB][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll 4
     for (int p = 0; p < k; p += 4) {
       const int kk = p + t;
       const bool kin = kk < k;
-      const double bv = kin ? X[kk * xs + g] : 0.0;
+      double bv[NB];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) bv[j] = kin ? X[kk * xs + 8 * j + g] : 0.0;
       double a[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -190,15 +197,21 @@ BDDC_DEV void panel_mma8(const double* __restrict__ A, long long lda, int m, int
                                   : 0.0;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (on[i]) dmma_8x8x4(acc[i][0], acc[i][1], a[i], bv);
+        if (on[i]) {
+#pragma unroll
+          for (int j = 0; j < NB; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], bv[j]);
+        }
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       if (rr[i] >= m) continue;
-      double* y = Y + rr[i] * ys + 2 * t;
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        y[h] = (beta == 0.0 ? 0.0 : beta * y[h]) + alpha * acc[i][h];
+      for (int j = 0; j < NB; ++j) {
+        double* y = Y + rr[i] * ys + 8 * j + 2 * t;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          y[h] = (beta == 0.0 ? 0.0 : beta * y[h]) + alpha * acc[i][j][h];
+      }
     }
   }
   __syncthreads();
@@ -211,36 +224,36 @@ template <int NR, bool TRANS>
 BDDC_DEV void lu_solve(const double* __restrict__ M, int n, double* X, double* tmp, double* red) {
   constexpr int XS = xstride<NR>();
   const int np = (n + kP - 1) / kP;
-  if (NR == 8) {
-    // eight right-hand sides: every panel product on the DMMA pipe
+  if constexpr (NR % 8 == 0) {
+    // 8 or 16 right-hand sides: every panel product on the DMMA pipe
     if (!TRANS) {
       for (int j = 0; j < np; ++j) {
         const int j0 = j * kP, w = min(kP, n - j0), j1 = j0 + w;
-        panel_mma8<false>(M + (long long)j0 * n + j0, n, w, w, X + j0 * XS, XS, tmp, XS, 1.0, 0.0);
+        panel_mma<NR, false>(M + (long long)j0 * n + j0, n, w, w, X + j0 * XS, XS, tmp, XS, 1.0, 0.0);
         for (int i = threadIdx.x; i < w * XS; i += blockDim.x) X[j0 * XS + i] = tmp[i];
         __syncthreads();
         if (j1 < n)
-          panel_mma8<false>(M + (long long)j1 * n + j0, n, n - j1, w, X + j0 * XS, XS, X + j1 * XS, XS,
+          panel_mma<NR, false>(M + (long long)j1 * n + j0, n, n - j1, w, X + j0 * XS, XS, X + j1 * XS, XS,
                             -1.0, 1.0);
       }
       for (int k = np - 2; k >= 0; --k) {
         const int k0 = k * kP, k1 = k0 + kP;
-        panel_mma8<false>(M + (long long)k0 * n + k1, n, kP, n - k1, X + k1 * XS, XS, X + k0 * XS, XS,
+        panel_mma<NR, false>(M + (long long)k0 * n + k1, n, kP, n - k1, X + k1 * XS, XS, X + k0 * XS, XS,
                           -1.0, 1.0);
       }
     } else {
       for (int j = 0; j < np; ++j) {
         const int j0 = j * kP, w = min(kP, n - j0), j1 = j0 + w;
         if (j1 < n)
-          panel_mma8<true>(M + (long long)j0 * n + j1, n, n - j1, w, X + j0 * XS, XS, X + j1 * XS, XS,
+          panel_mma<NR, true>(M + (long long)j0 * n + j1, n, n - j1, w, X + j0 * XS, XS, X + j1 * XS, XS,
                            -1.0, 1.0);
       }
       for (int k = np - 1; k >= 0; --k) {
         const int k0 = k * kP, w = min(kP, n - k0), k1 = k0 + w;
         if (k1 < n)
-          panel_mma8<true>(M + (long long)k1 * n + k0, n, w, n - k1, X + k1 * XS, XS, X + k0 * XS, XS,
+          panel_mma<NR, true>(M + (long long)k1 * n + k0, n, w, n - k1, X + k1 * XS, XS, X + k0 * XS, XS,
                            -1.0, 1.0);
-        panel_mma8<true>(M + (long long)k0 * n + k0, n, w, w, X + k0 * XS, XS, tmp, XS, 1.0, 0.0);
+        panel_mma<NR, true>(M + (long long)k0 * n + k0, n, w, w, X + k0 * XS, XS, tmp, XS, 1.0, 0.0);
         for (int i = threadIdx.x; i < w * XS; i += blockDim.x) X[k0 * XS + i] = tmp[i];
         __syncthreads();
       }

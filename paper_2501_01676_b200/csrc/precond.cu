@@ -711,11 +711,45 @@ __global__ void __launch_bounds__(256) local_solve_kernel(
   }
 }
 
-// Primal pieces through the LU, one CTA per subdomain, 8 primal columns at a time:
+// Primal pieces through the LU, one CTA per subdomain, 8 (n_p <= 8) or 16
+// primal columns at a time (every sweep reads the whole LU once: the kernel is
+// bound by that traffic, so as many right-hand sides as fit share a sweep):
 //   MP[p] = e_pc - Z Sbar[:, pc],  RP[p] = e_pc - Z^T Sbar[pc, :]^T,  C_i[p][q] = Sbar[pr, :] . MP[q]
 // (Z = Sdd^-1 embedded with zero primal rows / columns)
-constexpr int kPL = 8;
-__global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
+constexpr int kPL = 16;
+
+template <int NR>
+BDDC_DEV void primal_pieces_chunk(int n, int c0, int pc_n, const unsigned char* pm,
+                                  const int* __restrict__ ppos_b, const double* __restrict__ Sr,
+                                  const double* __restrict__ Sc, const double* __restrict__ L,
+                                  double* __restrict__ Mb, double* __restrict__ Rb, double* X,
+                                  double* tmp) {
+  constexpr int XS = lus::xstride<NR>();
+  for (int idx = threadIdx.x; idx < n * NR; idx += blockDim.x) {
+    const int q = idx / n, r = idx - q * n;  // coalesced along the Sbar column (stored as a row)
+    X[r * XS + q] = (q < pc_n && !pm[r]) ? Sc[(long long)(c0 + q) * n + r] : 0.0;
+  }
+  __syncthreads();
+  lus::lu_solve<NR, false>(L, n, X, tmp, nullptr);
+  for (int idx = threadIdx.x; idx < n * pc_n; idx += blockDim.x) {
+    const int q = idx / n, r = idx - q * n;
+    Mb[(long long)(c0 + q) * n + r] = (r == ppos_b[c0 + q] ? 1.0 : 0.0) - X[r * XS + q];
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n * NR; idx += blockDim.x) {
+    const int q = idx / n, r = idx - q * n;  // coalesced along the Sbar row
+    X[r * XS + q] = (q < pc_n && !pm[r]) ? Sr[(long long)(c0 + q) * n + r] : 0.0;
+  }
+  __syncthreads();
+  lus::lu_solve<NR, true>(L, n, X, tmp, nullptr);
+  for (int idx = threadIdx.x; idx < n * pc_n; idx += blockDim.x) {
+    const int q = idx / n, r = idx - q * n;
+    Rb[(long long)(c0 + q) * n + r] = (r == ppos_b[c0 + q] ? 1.0 : 0.0) - X[r * XS + q];
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256, 3) primal_pieces_lu_kernel(
     const int* __restrict__ nB, const long long* __restrict__ soff,
     const long long* __restrict__ voff, const unsigned char* __restrict__ primal_mask,
     const int* __restrict__ pstart, const int* __restrict__ ppos,
@@ -727,40 +761,22 @@ __global__ void __launch_bounds__(256) primal_pieces_lu_kernel(
   const int n = nB[b];
   const int p0 = pstart[b], np = pstart[b + 1] - p0;
   if (np == 0) return;
-  constexpr int XS = lus::xstride<kPL>();
-  double* X = psm;                      // n x XS
-  double* tmp = psm + n * XS;           // 64 x XS
-  double* red = tmp + 64 * XS;          // blockDim x kPL
+  double* X = psm;                                  // n x xstride
+  double* tmp = psm + n * lus::xstride<kPL>();      // 64 x xstride
   const double* Sr = Srows + poff[b];  // Sbar[ppos_q, :] as row q (n_p x n)
   const double* Sc = Scols + poff[b];  // Sbar[:, ppos_q] as row q
   const double* L = LU + soff[b];
   const unsigned char* pm = primal_mask + voff[b];
   double* Mb = MP + poff[b];
   double* Rb = RP + poff[b];
-  for (int c0 = 0; c0 < np; c0 += kPL) {
-    const int pc_n = min(kPL, np - c0);
-    for (int idx = threadIdx.x; idx < n * kPL; idx += blockDim.x) {
-      const int r = idx / kPL, q = idx - r * kPL;
-      X[r * XS + q] = (q < pc_n && !pm[r]) ? Sc[(long long)(c0 + q) * n + r] : 0.0;
+  if (np <= 8) {
+    primal_pieces_chunk<8>(n, 0, np, pm, ppos + p0, Sr, Sc, L, Mb, Rb, X, tmp);
+  } else {
+    for (int c0 = 0; c0 < np; c0 += kPL) {
+      const int left = np - c0;
+      if (left <= 8) primal_pieces_chunk<8>(n, c0, left, pm, ppos + p0, Sr, Sc, L, Mb, Rb, X, tmp);
+      else primal_pieces_chunk<kPL>(n, c0, min(kPL, left), pm, ppos + p0, Sr, Sc, L, Mb, Rb, X, tmp);
     }
-    __syncthreads();
-    lus::lu_solve<kPL, false>(L, n, X, tmp, red);
-    for (int idx = threadIdx.x; idx < n * pc_n; idx += blockDim.x) {
-      const int q = idx / n, r = idx - q * n;
-      Mb[(long long)(c0 + q) * n + r] = (r == ppos[p0 + c0 + q] ? 1.0 : 0.0) - X[r * XS + q];
-    }
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < n * kPL; idx += blockDim.x) {
-      const int q = idx / n, r = idx - q * n;  // coalesced along the Sbar row
-      X[r * XS + q] = (q < pc_n && !pm[r]) ? Sr[(long long)(c0 + q) * n + r] : 0.0;
-    }
-    __syncthreads();
-    lus::lu_solve<kPL, true>(L, n, X, tmp, red);
-    for (int idx = threadIdx.x; idx < n * pc_n; idx += blockDim.x) {
-      const int q = idx / n, r = idx - q * n;
-      Rb[(long long)(c0 + q) * n + r] = (r == ppos[p0 + c0 + q] ? 1.0 : 0.0) - X[r * XS + q];
-    }
-    __syncthreads();
   }
   double* C = Cl + coff[b];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -1386,7 +1402,7 @@ int bddc_pc_primal_pieces_lu(const int* nB, const long long* soff, const long lo
                              const double* LU, double* MP, double* RP, double* Cl,
                              const long long* coff, int nbatch, int max_nB, cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  const int smem = (max_nB * lus::xstride<kPL>() + 64 * lus::xstride<kPL>() + 256 * kPL) * (int)sizeof(double);
+  const int smem = (max_nB * lus::xstride<kPL>() + 64 * lus::xstride<kPL>()) * (int)sizeof(double);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(primal_pieces_lu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   primal_pieces_lu_kernel<<<nbatch, 256, smem, stream>>>(nB, soff, voff, primal_mask, pstart, ppos,

@@ -382,7 +382,7 @@ class DevicePlan:
         else:
             self.iface_perm = dev_i32(p.iface_perm)
             self.tsrc, self.tstart = dev_i64(p.tsrc), dev_i64(p.tstart)
-        self.pos2k = dev_i32(p.pos2k)
+        self.pos2k = p.pos2k_device("cuda")  # expanded on the device (no 4 B / dof upload)
         self.sub_globs = dev_i32(p.sub_globs)
         self.sub_glob_boff = dev_i32(p.sub_glob_boff)
         self.sub_glob_sh = dev_i32(p.sub_glob_sh)
@@ -577,7 +577,7 @@ def _face_ws(n):
 def _face_fast_ws(n):
     """face_fast_arena() in csrc/globs.cu"""
     n = np.asarray(n, dtype=np.int64)
-    return 5 * n * n + 4 * n + 4 * 6 * n + 4 * n + 32
+    return np.where(n <= 64, 3, 5) * n * n + 4 * n + 4 * 6 * n + 4 * n + 32
 
 
 def _face_small_bytes(n):
@@ -1009,6 +1009,23 @@ class DevicePreconditioner:
             raise NumericalError("empty primal space: no coarse problem to anchor the solver")
         go = _excl(r)
         self.glob_primal_offset = go[:-1]
+        # queued first, so that the index work below overlaps them: change of basis
+        # in Householder form (same primal spans; precond.cu) and T^T = D Q^T blocks
+        r_d = dev_i32(r)
+        HV = None
+        if householder:
+            Q = Q.clone()
+            HV = torch.zeros_like(Q)
+            w_sz = np.where(p.kind == 2, 0, p.gsize.astype(np.int64) * np.minimum(r, p.gsize))
+            w_off = _excl(w_sz)
+            Wsc = torch.empty(max(int(w_off[-1]), 1), dtype=F64, device="cuda")
+            lib.bddc_pc_glob_reflectors(d.kind, d.gsize, r_d, Q, q_off, HV, Wsc,
+                                        dev_i64(w_off[:-1]), p.G, int(p.gsize.max()), st)
+            del Wsc
+        TT = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
+        lib.bddc_pc_ttblocks(d.slot_glob, d.gsize, Q, q_off, scaling.D, d.sh_doff, TT,
+                             int(p.sh_sub.size), st)
+        self.Q_used, self.q_off_used = Q, q_off  # the change of basis this preconditioner applies
 
         def primal_counts(sub_globs, sub_glob_start):
             cnt = r[sub_globs]
@@ -1036,22 +1053,6 @@ class DevicePreconditioner:
         d_mask = torch.from_numpy(mask).cuda()
         self.sum_np = int(pstart[-1])
 
-        # change of basis in Householder form (same primal spans; precond.cu)
-        r_d = dev_i32(r)
-        HV = None
-        if householder:
-            Q = Q.clone()
-            HV = torch.zeros_like(Q)
-            w_sz = np.where(p.kind == 2, 0, p.gsize.astype(np.int64) * np.minimum(r, p.gsize))
-            w_off = _excl(w_sz)
-            Wsc = torch.empty(max(int(w_off[-1]), 1), dtype=F64, device="cuda")
-            lib.bddc_pc_glob_reflectors(d.kind, d.gsize, r_d, Q, q_off, HV, Wsc,
-                                        dev_i64(w_off[:-1]), p.G, int(p.gsize.max()), st)
-            del Wsc
-        TT = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
-        lib.bddc_pc_ttblocks(d.slot_glob, d.gsize, Q, q_off, scaling.D, d.sh_doff, TT,
-                             int(p.sh_sub.size), st)
-        self.Q_used, self.q_off_used = Q, q_off  # the change of basis this preconditioner applies
         npn = max(int(poff[-1]), 1)
         # per local B position: its primal index (or -1), for the compact Sbar rows / columns
         pidx = np.full(int(p.voff[-1]), -1, dtype=np.int32)

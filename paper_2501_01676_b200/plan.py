@@ -113,7 +113,12 @@ class Plan:
         self.d_total = int(self.sh_doff[-1])
         self.sh_doff = self.sh_doff[:-1]
         # slots by (sharer, glob): one stable argsort of a combined key (unique pairs)
-        order = np.argsort(self.sh_sub.astype(np.int64) * max(G, 1) + slot_glob, kind="stable")
+        # (the slots are glob-major already, so a stable sort by sharer orders them by
+        # (sharer, glob); 16-bit keys take numpy's radix sort)
+        if N <= 0xffff:
+            order = np.argsort(self.sh_sub.astype(np.uint16), kind="stable")
+        else:
+            order = np.argsort(self.sh_sub.astype(np.int64) * max(G, 1) + slot_glob, kind="stable")
         self.sub_globs = slot_glob[order].astype(np.int32)
         pair_sub = self.sh_sub[order].astype(np.int64)
         self.sub_glob_sh = order.astype(np.int32)
@@ -140,7 +145,7 @@ class Plan:
         self._B_counts = sizes_k
         self._B_range = (0, int(sizes_k.sum()))
         self._B_nodes = None
-        self.pos2k = np.repeat(np.arange(self.sub_globs.size, dtype=np.int32), sizes_k)
+        self._pos2k = None  # per local interface position: its (subdomain, glob) pair; lazy
 
     def _restrict(self, s0, s1):
         """Keep subdomains s0..s1-1 (local ids 0..s1-s0-1)."""
@@ -164,7 +169,21 @@ class Plan:
         v0, v1 = int(self.voff[s0]), int(self.voff[s1])
         self.voff = self.voff[s0:s1 + 1] - v0
         self._B_range = (v0, v1)
-        self.pos2k = (self.pos2k[v0:v1] - a).astype(np.int32)
+
+    @property
+    def pos2k(self):
+        """Index into sub_globs of every local interface position (host copy)."""
+        if self._pos2k is None:
+            sizes = self.gsize[self.sub_globs].astype(np.int64)
+            self._pos2k = np.repeat(np.arange(self.sub_globs.size, dtype=np.int32), sizes)
+        return self._pos2k
+
+    def pos2k_device(self, dv):
+        import torch
+
+        sizes = _up(self.gsize[self.sub_globs].astype(np.int64), dv)
+        return torch.repeat_interleave(torch.arange(self.sub_globs.size, dtype=torch.int32, device=dv),
+                                       sizes, output_size=int(self.voff[-1]))
 
     @property
     def B_nodes(self):
