@@ -516,6 +516,21 @@ int bddc_norm2(const double* w, long long n, double* out, double* partial, int n
 int bddc_gmres_givens(const double* h1, const double* h2, int m, int ldr, double* R, double* cs,
                       double* sn, double* g, double* y, double* out, cudaStream_t stream);
 
+/* One whole GMRES step after w = M^-1 S_hat v_(m-1) in a single cooperative
+ * launch (one rank): CGS2 against V[0:m] (h1, h2[0:m], h2[m] = ||w||), the
+ * Givens recurrence of bddc_gmres_givens (R, cs, sn, g, y, out), the next
+ * basis vector vnext = w / ||w|| and the true residual norm
+ * tres[0] = ||rhs - U[0:m]^T y||.  V, U: m rows of stride ldv; partial:
+ * (2 m + 2) * bddc_gmres_step_blocks() doubles of workspace.  Returns 1 (nothing
+ * launched) when the vectors do not fit the resident chunks: the caller then
+ * uses the separate kernels above.  Fixed-order reductions (reproducible).
+ * replaces the inner loop of gmres_solve, solver.py:283-306. */
+int bddc_gmres_step(const double* V, const double* U, long long ldv, long long n, int m,
+                    const double* w, const double* rhs, double* h1, double* h2, int ldr, double* R,
+                    double* cs, double* sn, double* g, double* y, double* out, double* tres,
+                    double* vnext, double* partial, cudaStream_t stream);
+int bddc_gmres_step_blocks(void);
+
 /* x[i] = sqrt(x[i]), i < n (norms after a cross-rank sum of squares). */
 int bddc_sqrt_inplace(double* x, int n, cudaStream_t stream);
 

@@ -323,14 +323,14 @@ __global__ void __launch_bounds__(256, 4) pivot_inverse_kernel(
     const double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, int k, double* __restrict__ pinv, long long pinv_stride,
     int* __restrict__ status, int require_positive, double* __restrict__ piv_out,
-    long long piv_stride) {
+    long long piv_stride, int ldo = kTile) {
   __shared__ MmaGjSmem sm;
   const int b = blockIdx.x;
   const int w = min(kTile, npiv[b] - k);
   if (w <= 0) return;
   const int L = ld[b];
   const double* M = base + off[b] + (long long)k * L + k;
-  const bool bad = reg_gj64(M, L, w, pinv + (long long)b * pinv_stride, kTile, require_positive,
+  const bool bad = reg_gj64(M, L, w, pinv + (long long)b * pinv_stride, ldo, require_positive,
                             piv_out ? piv_out + (long long)b * piv_stride + k : nullptr, sm);
   if (threadIdx.x == 0 && bad && status)
     atomicCAS(status + b, 0, require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
@@ -1106,13 +1106,21 @@ int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int
   const int T = ceil_div(max_n, kTile);
   const NextPivot none{nullptr, 0, nullptr, 0, nullptr, 0};
   for (int k = 0; k < max_n; k += 128) {
-    gj128_extract_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work);
-    bddc_note_launches(1);
-    // P = (pivot block)^-1: symmetric 64-panel Gauss-Jordan on the 128 x 128 copies
-    // (positive LDL^T pivots <=> positive definite: the cho_factor criterion)
-    int rc = bddc_gj_inverse(work, work_off, work_ld, work_n, nbatch, 128, pinv_ws, 4096, status,
-                             require_positive, 1, stream);
-    if (rc) return rc;
+    if (max_n - k <= kTile) {
+      // last panel of at most 64 pivots in every matrix: its inverse straight into
+      // the work block (leading dimension 128), one register Gauss-Jordan
+      pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work, 128 * 128, status,
+                                                       require_positive, nullptr, 0, 128);
+      bddc_note_launches(1);
+    } else {
+      gj128_extract_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work);
+      bddc_note_launches(1);
+      // P = (pivot block)^-1: symmetric 64-panel Gauss-Jordan on the 128 x 128 copies
+      // (positive LDL^T pivots <=> positive definite: the cho_factor criterion)
+      int rc = bddc_gj_inverse(work, work_off, work_ld, work_n, nbatch, 128, pinv_ws, 4096, status,
+                               require_positive, 1, stream);
+      if (rc) return rc;
+    }
     gj128_row_kernel<<<dim3(T, nbatch), 512, sizeof(TileSmemT<128>), stream>>>(M, off, ld, n, k,
                                                                                work);
     gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 1,

@@ -24,6 +24,7 @@ from .plan import Plan, _excl, _ranges
 
 F64 = torch.float64
 PANEL = 128  # elimination panel width (two 64-wide sub-panels; DMMA trailing update with K = 128)
+FUSED_GMRES = True  # one cooperative launch per GMRES step for the vector work (one rank)
 TWO_PHASE = True  # deep interior pivots eliminated first, restricted to the interior block (plan.nDeep)
 
 
@@ -1431,7 +1432,10 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
     st = stream()
     n = rhs.shape[0]
     nblk = 296
-    partial = torch.empty(nblk * (max_iter + 2), dtype=F64, device="cuda")
+    fused = not (getattr(operator, "layout", None) is not None and operator.layout.multi) and FUSED_GMRES
+    nstep = int(lib.bddc_gmres_step_blocks()) if fused else 0
+    partial = torch.empty(max(nblk * (max_iter + 2), nstep * (2 * max_iter + 4)), dtype=F64,
+                          device="cuda")
     # [h1 (max_iter+1) | h2 .. hn (max_iter+1)]
     hb = torch.empty(2 * (max_iter + 2), dtype=F64, device="cuda")
     h1, scal = hb[:max_iter + 1], hb[max_iter + 1:]
@@ -1481,23 +1485,34 @@ def gmres_device(operator, rhs, pc, rel_tol=1e-8, max_iter=300):
             it = j
             break
         pc.apply_device(U[j], out=w)
-        dots.mdot(V.buf, m, w, h1)
-        lib.bddc_multi_axpy(V.buf, n, m, h1, -1.0, w, st)
-        dots.mdot(V.buf, m, w, scal)
-        lib.bddc_multi_axpy(V.buf, n, m, scal, -1.0, w, st)
-        dots.norm(w, scal[m:])
         y = ys[j % 2]
-        lib.bddc_gmres_givens(h1, scal, m, ldr, R, cs, sn, g, y, out[j], st)
+        V.ensure(j + 2)
+        if fused:
+            # Gram-Schmidt, Givens recurrence, next basis vector and the true residual
+            # norm of this step in one cooperative launch (csrc/krylov.cu)
+            rc = lib.bddc_gmres_step(V.buf, U.buf, n, n, m, w, rhs, h1, scal, ldr, R, cs, sn, g, y,
+                                     out[j], tres[j:], V[j + 1], partial, st)
+            if rc == 1:  # vectors too long for the resident chunks
+                fused = False
+            elif rc:
+                raise RuntimeError(f"bddc_gmres_step failed ({rc})")
+        if not fused:
+            dots.mdot(V.buf, m, w, h1)
+            lib.bddc_multi_axpy(V.buf, n, m, h1, -1.0, w, st)
+            dots.mdot(V.buf, m, w, scal)
+            lib.bddc_multi_axpy(V.buf, n, m, scal, -1.0, w, st)
+            dots.norm(w, scal[m:])
+            lib.bddc_gmres_givens(h1, scal, m, ldr, R, cs, sn, g, y, out[j], st)
         host[j].copy_(out[j], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
         events.append(ev)
-        # true residual of this step: r = rhs - S_hat V y (from the stored U = S_hat V)
-        r.copy_(rhs)
-        lib.bddc_multi_axpy(U.buf, n, m, y, -1.0, r, st)
-        dots.norm(r, tres[j:])
-        V.ensure(j + 2)
-        lib.bddc_scale_copy(w, n, scal[m:], V[j + 1], st)
+        if not fused:
+            # true residual of this step: r = rhs - S_hat V y (from the stored U = S_hat V)
+            r.copy_(rhs)
+            lib.bddc_multi_axpy(U.buf, n, m, y, -1.0, r, st)
+            dots.norm(r, tres[j:])
+            lib.bddc_scale_copy(w, n, scal[m:], V[j + 1], st)
     else:
         finished(max_iter - 1)
         it = max_iter
