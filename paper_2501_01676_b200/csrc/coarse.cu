@@ -455,15 +455,36 @@ int bddc_coarse_blockinv(const double* A, long long ld, int n, const double* pin
                                                                 cl, cu, foff, goff, F, G);
   int launches = 1;
   const int panels = kCB / 64;
+  // the forward (F) and backward (G) chains are independent sequences of small
+  // dependent launches: they run side by side, the backward one on a helper
+  // stream (per device and host thread) forked / joined with events
+  static thread_local cudaStream_t side[PerDeviceOnce::kMaxDev] = {};
+  static thread_local cudaEvent_t ev[PerDeviceOnce::kMaxDev][2] = {};
+  const int dev = current_device();
+  cudaStream_t s2 = stream;
+  if (dev >= 0 && dev < PerDeviceOnce::kMaxDev) {
+    if (!side[dev]) {
+      cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&ev[dev][0], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ev[dev][1], cudaEventDisableTiming);
+    }
+    s2 = side[dev];
+    cudaEventRecord(ev[dev][0], stream);
+    cudaStreamWaitEvent(s2, ev[dev][0], 0);
+  }
+  for (int p = panels - 2; p >= 0; --p) {
+    coarse_blk_bwd_kernel<<<dim3(ceil_div(max_ldg, 64), nD), kTileThreads, smem, s2>>>(
+        A, ld, n, cl, cu, goff, G, p);
+    ++launches;
+  }
   for (int p = 1; p < panels; ++p) {
     coarse_blk_fwd_kernel<<<dim3(ceil_div(max_ldf, 64), nD), kTileThreads, smem, stream>>>(
         A, ld, n, cl, cu, foff, F, p);
     ++launches;
   }
-  for (int p = panels - 2; p >= 0; --p) {
-    coarse_blk_bwd_kernel<<<dim3(ceil_div(max_ldg, 64), nD), kTileThreads, smem, stream>>>(
-        A, ld, n, cl, cu, goff, G, p);
-    ++launches;
+  if (s2 != stream) {
+    cudaEventRecord(ev[dev][1], s2);
+    cudaStreamWaitEvent(stream, ev[dev][1], 0);
   }
   bddc_note_launches(launches);
   cudaError_t e = cudaGetLastError();

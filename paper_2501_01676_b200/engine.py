@@ -346,6 +346,19 @@ def trailing_flops(plan, panel=PANEL, dual_lu=False):
     return f, n
 
 
+_SIDE = {}
+
+
+def _side_stream():
+    """Helper stream of the current device and host thread."""
+    import threading
+
+    key = (torch.cuda.current_device(), threading.get_ident())
+    if key not in _SIDE:
+        _SIDE[key] = torch.cuda.Stream()
+    return _SIDE[key]
+
+
 def _first_bad(status):
     s = status.cpu().numpy()
     nz = np.flatnonzero(s)
@@ -1139,12 +1152,23 @@ class DevicePreconditioner:
                                      nbmax, st)
         self.G = torch.empty(npn, dtype=F64, device="cuda")
         self.Nt = torch.empty(npn, dtype=F64, device="cuda")
-        lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
-                                  d.sub_glob_sh, d.gsize, d.sh_doff, TT, self.d_pstart,
-                                  self.d_poff, RP, self.G, p.N, st)
-        lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
-                                  d.sub_glob_sh, d.gsize, d.sh_doff, TT, self.d_pstart,
-                                  self.d_poff, MP, self.Nt, p.N, st)
+        # G = RP T and N^T = MP T do not feed the coarse matrix: they run on a side
+        # stream next to the coarse factorisation (a chain of small dependent
+        # launches that leaves most of the GPU idle) and are joined at the end
+        main = torch.cuda.current_stream()
+        side = _side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            s2 = stream()
+            lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
+                                      d.sub_glob_sh, d.gsize, d.sh_doff, TT, self.d_pstart,
+                                      self.d_poff, RP, self.G, p.N, s2)
+            lib.bddc_pc_primal_rows_T(d.nB, d.voff, d.pos2k, d.sub_globs, d.sub_glob_boff,
+                                      d.sub_glob_sh, d.gsize, d.sh_doff, TT, self.d_pstart,
+                                      self.d_poff, MP, self.Nt, p.N, s2)
+        for t in (MP, RP):
+            t.record_stream(side)
+        self._side = side
         del Srows, Scols, MP, RP, pinv
         nc = self.n_primal
         # sharded: the subdomain contributions are reduced to rank 0, which holds
@@ -1156,6 +1180,7 @@ class DevicePreconditioner:
         if not self.root:
             self.coarse_factor_bytes = 0
             self._Clg = None
+            main.wait_stream(side)
             self._check_coarse(None, go, ls)
             return
         C = torch.empty(nc * nc, dtype=F64, device="cuda")  # every entry written by the scatter
@@ -1201,6 +1226,7 @@ class DevicePreconditioner:
         self.cb_epoch = 0
         self.cb_z = torch.empty(nc, dtype=F64, device="cuda")
         self.coarse_factor_bytes = 8 * (int(lay["foff"][-1]) + int(lay["goff"][-1]))
+        main.wait_stream(side)
         del C, self.coarse_lu, self.coarse_pinv
 
     def _cinit_bufs(self, nc):
