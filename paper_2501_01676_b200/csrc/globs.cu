@@ -9,7 +9,6 @@
 #include "common.cuh"
 #include "bddc_b200.h"
 #include "dense_block.cuh"
-#include "reg_gj.cuh"
 #include "glob_layout.h"
 
 // Optional phase profile (tools/prof_globs.py builds a -DBDDC_PROF variant):
@@ -34,10 +33,21 @@ extern "C" int bddc_prof_read(unsigned long long* host, int reset) {
   }
   return 0;
 }
+#define GJ_PROF 1
+#define GJ_PROF_INIT long long _tg = clock64();
+#define GJ_PROF(i)                                                             \
+  do {                                                                         \
+    if (threadIdx.x == 0) {                                                    \
+      long long _t = clock64();                                                \
+      atomicAdd(&g_prof[i], (unsigned long long)(_t - _tg));                   \
+      _tg = _t;                                                                \
+    }                                                                          \
+  } while (0)
 #else
 #define PROF_INIT
 #define PROF(i)
 #endif
+#include "reg_gj.cuh"
 
 namespace bddc {
 

@@ -5,6 +5,11 @@
 #include "common.cuh"
 #include "tile_mma.cuh"
 
+#ifndef GJ_PROF
+#define GJ_PROF_INIT
+#define GJ_PROF(i)
+#endif
+
 namespace bddc {
 
 struct RegGjSmem {
@@ -157,6 +162,7 @@ BDDC_DEV bool reg_gj64_fma(const double* __restrict__ M, long long L, int w,
 BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double* __restrict__ out,
                        long long ldo, int require_positive, double* __restrict__ piv,
                        MmaGjSmem& sm, int max_steps = 1 << 30) {
+  GJ_PROF_INIT
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int row = 8 * warp + g;
@@ -170,6 +176,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
     }
   if (threadIdx.x == 0) sm.bad = 0;
   const int nsteps = min((w + 3) >> 2, max_steps);
+  GJ_PROF(36);
   for (int s = 0; s < nsteps; ++s) {
     const int par = s & 1, p = 4 * s, pw = s >> 1, g0 = 4 * (s & 1);
     // publish pivot rows (owner warp) and pivot columns (tile jp = pw, lanes holding them)
@@ -189,6 +196,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
       }
     }
     __syncthreads();
+    GJ_PROF(32);
     // 4x4 Gauss-Jordan of the pivot block in every warp (lane 4i+j holds Mi[i][j],
     // lanes 16..31 mirror lanes 0..15): no shared-memory round trip for Mi
     double m;
@@ -209,6 +217,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
         else m = (jj == q) ? -cq * ip : m - cq * rq * ip;
       }
     }
+    GJ_PROF(33);
     {  // U = Mi R, pivot columns I + Mi: one value per thread (i is warp-uniform)
       const int i = threadIdx.x >> 6, col = threadIdx.x & 63;
       const double m0 = __shfl_sync(0xffffffffu, m, 4 * i), m1 = __shfl_sync(0xffffffffu, m, 4 * i + 1);
@@ -231,6 +240,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
       mp[h] = __shfl_sync(0xffffffffu, m, 4 * gi + k);
     }
     __syncthreads();
+    GJ_PROF(34);
     // M -= F U on the tensor pipe
     const double a = -sm.F[par][row][t];
 #pragma unroll
@@ -245,6 +255,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
           c[j][h] = (col >= p && col < p + 4) ? mp[h] : sm.U[g - g0][col];
         }
     }
+    GJ_PROF(35);
   }
   __syncthreads();
 #pragma unroll
@@ -256,6 +267,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
     }
   const bool failed = sm.bad != 0;
   __syncthreads();
+  GJ_PROF(37);
   return failed;
 }
 

@@ -1055,23 +1055,24 @@ class DevicePreconditioner:
         pstart = _excl(self.np_sub)
         ppos = _ranges(p.sub_glob_boff, cnt)
         pgid0 = _ranges(go[:-1][p.sub_globs], cnt)
-        mask = np.zeros(int(p.voff[-1]), dtype=np.uint8)
         psub = np.repeat(np.arange(p.N), self.np_sub)
-        mask[p.voff[psub] + ppos] = 1
+        # primal mask / primal index per local interface position: scattered on the
+        # device from the (few) primal positions instead of uploading dense arrays
+        d_primal_at = dev_i64(p.voff[psub] + ppos)
+        d_mask = torch.zeros(int(p.voff[-1]), dtype=torch.uint8, device="cuda")
+        d_mask[d_primal_at] = 1
         poff = _excl(self.np_sub * p.nB)
         gcoff = _excl(np_glob * np_glob)  # coarse blocks C_i of all subdomains, global layout
         c0, c1 = int(gcoff[s0]), int(gcoff[s1])
         coff = gcoff[s0:s1 + 1] - c0
         self.d_pstart, self.d_ppos = dev_i32(pstart), dev_i32(ppos)
         self.d_poff, d_coff = dev_i64(poff[:-1]), dev_i64(coff[:-1])
-        d_mask = torch.from_numpy(mask).cuda()
         self.sum_np = int(pstart[-1])
 
         npn = max(int(poff[-1]), 1)
         # per local B position: its primal index (or -1), for the compact Sbar rows / columns
-        pidx = np.full(int(p.voff[-1]), -1, dtype=np.int32)
-        pidx[p.voff[psub] + ppos] = (np.arange(ppos.size) - pstart[psub]).astype(np.int32)
-        d_pidx = dev_i32(pidx)
+        d_pidx = torch.full((int(p.voff[-1]),), -1, dtype=torch.int32, device="cuda")
+        d_pidx[d_primal_at] = dev_i32(np.arange(ppos.size) - pstart[psub])
         d_poff_all = dev_i64(poff[:-1])
         Srows = torch.empty(npn, dtype=F64, device="cuda")
         Scols = torch.empty(npn, dtype=F64, device="cuda")

@@ -46,7 +46,9 @@ for it in range(2):
 read(buf, 0)
 v = np.array(buf[:], dtype=np.float64)
 print(f"phases (ms) {res.times_ms}")
-for name, lo, labels in (("face_fast_kernel", 0, FACE), ("edge_new_kernel", 16, EDGE)):
+GJ = ["publish + barrier", "4x4 pivot chain", "U + barrier", "DMMA + pivot rows", "load", "store"]
+for name, lo, labels in (("face_fast_kernel", 0, FACE), ("edge_new_kernel", 16, EDGE),
+                         ("reg_gj64 (slot_schur / edge kernels)", 32, GJ)):
     tot = v[lo:lo + len(labels)].sum()
     print(f"\n{name}: total {tot:.3e} CTA-cycles")
     for i, lab in enumerate(labels):
