@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_row_kernel
   tile_mma(C, L, w, n, pinv + (long long)b * pinv_stride, kTile, C, L, w, 1.0, 0.0, sm);
 }
 
-constexpr int kTrailBM = 64;
+constexpr int kTrailBM = 64;  // row-tile height of the big (mode 0) trailing updates (128 x 64 tiles, 512 threads: measured slower, 34.8 -> 38.2 ms)
 
 // Trailing update of a panel step.  mode 0: rows/cols from k + w, K = w with
 // w = min(nbw, npiv - k) (nbw = 64 or 128).  mode 1 (strip inside a 128-wide
@@ -402,12 +402,13 @@ struct NextPivot {
   long long piv_stride;
 };
 
-__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_kernel(
+template <int BM>
+__global__ void __launch_bounds__(BM * 4, BM == 64 ? kTileMinBlocks : 2) schur_trailing_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, const int* __restrict__ nrows, const int* __restrict__ ncols,
     int k, int lim, int nbw, int mode, NextPivot nx, ColHole hole) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmemT<kTrailBM>& sm = *reinterpret_cast<TileSmemT<kTrailBM>*>(smem_raw);
+  TileSmemT<BM>& sm = *reinterpret_cast<TileSmemT<BM>*>(smem_raw);
   const int b = blockIdx.y;
   const int np = npiv[b] - k;
   if (np <= 0) return;
@@ -430,27 +431,28 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_trailing_k
   const int tn_count = tile_col_count(s, nc, h0, h1);
   if (tn_count <= 0) return;
   const int tm = blockIdx.x / tn_count, tn = blockIdx.x - tm * tn_count;
-  const int r0 = r_begin + tm * kTrailBM;
+  const int r0 = r_begin + tm * BM;
   int c0, cn;
   if (r0 >= r_end || !tile_cols(s, tn, nc, h0, h1, c0, cn)) return;
   const int L = ld[b];
   double* M = base + off[b];
-  tile_mma_t<kTrailBM>(M + (long long)r0 * L + c0, L, min(kTrailBM, r_end - r0), cn,
-                       M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0,
-                       sm);
+  tile_mma_t<BM>(M + (long long)r0 * L + c0, L, min(BM, r_end - r0), cn,
+                 M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm);
   if (nx.pinv != nullptr && blockIdx.x == 0) {
     const int wn = min(kTile, npiv[b] - s);
     if (wn > 0) {
       __syncthreads();  // tile written; the pipeline smem is free
-      static_assert(sizeof(MmaGjSmem) <= sizeof(TileSmemT<kTrailBM>), "smem reuse");
+      static_assert(sizeof(MmaGjSmem) <= sizeof(TileSmemT<BM>), "smem reuse");
       MmaGjSmem& gsm = *reinterpret_cast<MmaGjSmem*>(smem_raw);
-      const bool bad = reg_gj64(M + (long long)s * L + s, L, wn, nx.pinv + (long long)b * nx.stride,
-                                kTile, nx.require_positive,
-                                nx.piv_out ? nx.piv_out + (long long)b * nx.piv_stride + s : nullptr,
-                                gsm);
-      if (threadIdx.x == 0 && bad && nx.status)
-        atomicCAS(nx.status + b, 0,
-                  nx.require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
+      if (threadIdx.x < 256) {  // the register Gauss-Jordan runs on 256 threads (named barrier)
+        const bool bad = reg_gj64(M + (long long)s * L + s, L, wn,
+                                  nx.pinv + (long long)b * nx.stride, kTile, nx.require_positive,
+                                  nx.piv_out ? nx.piv_out + (long long)b * nx.piv_stride + s : nullptr,
+                                  gsm);
+        if (threadIdx.x == 0 && bad && nx.status)
+          atomicCAS(nx.status + b, 0,
+                    nx.require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
+      }
     }
   }
 }
@@ -818,8 +820,10 @@ static int smem_tile_setup() {
   once([&] {
     int bytes = (int)sizeof(TileSmem);
     cudaFuncSetAttribute(schur_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(schur_trailing_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(schur_trailing_kernel<kTrailBM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(TileSmemT<kTrailBM>));
+    cudaFuncSetAttribute(schur_trailing_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(TileSmemT<64>));
     cudaFuncSetAttribute(gj_row_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(gj_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -952,7 +956,7 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
       // second sub-panel: strip update of its 64 rows (+ its pivot inverse),
       // W2, then W_top -= W1_Q W2 so the pivot rows hold A11^-1 A12 for all 128
       const int cts = ceil_div(max_cols - k - kTile, kTile);
-      schur_trailing_kernel<<<dim3(cts, nbatch), kTileThreads, tsm, stream>>>(
+      schur_trailing_kernel<64><<<dim3(cts, nbatch), kTileThreads, sizeof(TileSmemT<64>), stream>>>(
           M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1, nx_sub, hole);
       schur_row_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(
           M, off, ld, npiv, ncols, k + kTile, P2, pinv_stride, 0x7fffffff, hole);
@@ -967,7 +971,7 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
       const bool lg = g_trail_on && !ev && g_trail_used + 2 <= g_trail_pool.size();
       if (lg) cudaEventRecord(g_trail_pool[g_trail_used], stream);
       if (ev) cudaEventRecord(ev[2 * timed], stream);
-      schur_trailing_kernel<<<dim3(ct * rt, nbatch), kTileThreads, tsm, stream>>>(
+      schur_trailing_kernel<kTrailBM><<<dim3(ct * rt, nbatch), kTrailBM * 4, tsm, stream>>>(
           M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, panel, 0, more ? nx_next : none, hole);
       ++launches;
       next_done = true;

@@ -12,6 +12,10 @@
 
 namespace bddc {
 
+// barrier of the 256 threads running reg_gj64: a named barrier, so that the
+// first 256 threads of a larger CTA can run the inverse on their own
+BDDC_DEV void gj_sync256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
 struct RegGjSmem {
   double rowb[2][4][kTile];
   double colb[2][4][kTile];
@@ -152,7 +156,9 @@ BDDC_DEV bool reg_gj64_fma(const double* __restrict__ M, long long L, int w,
 
 // Same inverse with the rank-4 updates on the DMMA pipe.  The matrix lives in
 // DMMA accumulator fragments: warp w owns rows 8w..8w+7, thread (g, t) holds
-// (8w + g, 8j + 2t + h) for j < 8, h < 2.  Step s (pivots p = 4s..4s+3):
+// (8w + g, 8j + 2t + h) for j < 8, h < 2.  Called by exactly 256 threads
+// (threadIdx.x < 256; all barriers are the named barrier gj_sync256).
+// Step s (pivots p = 4s..4s+3):
 //   publish pivot rows R (owner warp) and pivot columns F (all warps);
 //   Mi = R[:, p:p+4]^-1 (one thread: the 4x4 Gauss-Jordan, scalar pivots);
 //   U = Mi R with U[:, p:p+4] = I + Mi, so that the single update
@@ -195,7 +201,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
         if (cc >= 0 && cc < 4) sm.F[par][row][cc] = c[j][h];
       }
     }
-    __syncthreads();
+    gj_sync256();
     GJ_PROF(32);
     // 4x4 Gauss-Jordan of the pivot block in every warp (lane 4i+j holds Mi[i][j],
     // lanes 16..31 mirror lanes 0..15): no shared-memory round trip for Mi
@@ -239,7 +245,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
       const int gi = (g - g0) & 3, k = (2 * t + h - g0) & 3;
       mp[h] = __shfl_sync(0xffffffffu, m, 4 * gi + k);
     }
-    __syncthreads();
+    gj_sync256();
     GJ_PROF(34);
     // M -= F U on the tensor pipe
     const double a = -sm.F[par][row][t];
@@ -257,7 +263,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
     }
     GJ_PROF(35);
   }
-  __syncthreads();
+  gj_sync256();
 #pragma unroll
   for (int j = 0; j < 8; ++j)
 #pragma unroll
@@ -266,7 +272,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
       if (row < w && col < w) out[(long long)row * ldo + col] = c[j][h];
     }
   const bool failed = sm.bad != 0;
-  __syncthreads();
+  gj_sync256();
   GJ_PROF(37);
   return failed;
 }
