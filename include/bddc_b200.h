@@ -61,17 +61,25 @@ int bddc_plan_loc4(const long long* conn, const long long* sub_of, long long n_e
  * per row); a row with more sets *overflow (device int, zeroed by the caller)
  * and the call must be repeated with general = 1 (dense row buffers, any
  * mesh).  Both give bitwise identical matrices.
+ * nint / ndeep (both null: none): interior and deep-interior counts of the
+ * two-phase elimination; the compact path then leaves the two blocks nobody
+ * reads unwritten (deep rows x interface columns, interface rows x deep
+ * columns: structurally zero and skipped by the panel kernels, the
+ * extraction and the recovery).
  * replaces substructuring.py:98-114 (COO->CSR assembly, load, lifting). */
 int bddc_local_assemble(double* K, const long long* off, const int* ld, const int* nloc,
                         const long long* elem_start, const long long* elem_ids, const int* loc4,
                         const long long* conn, const double* Ke, const double* Fe,
                         const double* gdir, int nbatch, int max_nl, int* lists, long long* keys,
-                        int* overflow, int general, cudaStream_t stream);
+                        int* overflow, int general, const int* nint, const int* ndeep,
+                        cudaStream_t stream);
 
 /* Blocked Schur elimination without pivoting (panel 64 or 128 = two 64-wide
  * sub-panels combined so the DMMA trailing update runs with K = 128):
- * eliminates npiv[b] leading pivots; trailing block becomes the Schur complement,
- * pivot rows keep W = A11^-1 A12 for back-substitution.
+ * eliminates npiv[b] leading pivots; trailing block becomes the Schur complement.
+ * The factors are those of 64-wide panels in either case ("rows below only"
+ * LU form): pivot rows keep W_k = P_k A12^(k) (P_k the inverse 64 x 64 pivot
+ * block) for back-substitution, the column panels below keep A21^(k).
  * col_hole0 / col_hole1 (per matrix, both null: none): the pivot rows have no
  * entries in columns [col_hole0[b], col_hole1[b]), so the panel steps skip
  * them (first phase of the two-phase subdomain elimination: the deep interior
@@ -95,15 +103,6 @@ int bddc_schur_eliminate_timed(double* M, const long long* off, const int* ld, c
                                int require_positive, double* piv_out, long long piv_stride,
                                const int* col_hole0, const int* col_hole1, cudaStream_t stream,
                                double* host_trailing_ms);
-
-/* Converts the result of bddc_schur_eliminate with panel = 128 on square
- * n x n matrices (npiv = nrows = ncols = n, pinv_step_stride != 0 so every
- * 64-wide sub-panel keeps its inverse pivot block) into the 64-panel "rows
- * below only" LU form that bddc_lu_diag_pinv / the local solves use:
- * A21^(k2) = A[., k2] - A[., k1] W1_Q and W1 = W1_fixed + W1_Q W2 per panel.
- * Part of replacing lu_factor(Stil) solver.py:99. */
-int bddc_lu128_fixup(double* M, const long long* off, const int* ld, const int* n, int nbatch,
-                     int max_n, cudaStream_t stream);
 
 /* Event log of the bddc_schur_eliminate trailing-update launches (bench
  * roofline measured over the timed region without synchronising inside it):
@@ -367,9 +366,19 @@ int bddc_lu_diag_pinv(double* LU, const long long* soff, const int* nB, int nbat
                       const double* pinv, long long pinv_stride, long long step_stride,
                       cudaStream_t stream);
 
+/* The coarse restriction alone: cvals = G x, x = u[perm] (G = null in
+ * bddc_pc_local_solve then skips it there), so that the coarse solve can run
+ * on another stream next to the local solves.
+ * replaces the primal part of Rtil^T Dtil^T ... solver.py:180-186. */
+int bddc_pc_primal_restrict(const int* nB, const long long* voff, const int* iface_perm,
+                            const double* u, const int* pstart, const long long* poff,
+                            const double* G, double* cvals, int nbatch, int max_nB,
+                            cudaStream_t stream);
+
 /* Local part of the preconditioner and the coarse restriction per subdomain:
- * x = u[perm]; cvals = G x; y = TT (Sdd^-1 (TT^T x with primal entries zeroed))
- * through the dual-block LU (the reference's lu_solve of Stil, solver.py:187-195).
+ * x = u[perm]; cvals = G x (skipped when G is null); y = TT (Sdd^-1 (TT^T x
+ * with primal entries zeroed)) through the dual-block LU (the reference's
+ * lu_solve of Stil, solver.py:187-195).
  * replaces BddcPreconditioner.apply local solves solver.py:138-209. */
 int bddc_pc_local_solve(const int* nB, const long long* soff, const long long* voff,
                         const int* iface_perm, const double* LU, const int* pos2k,

@@ -1360,6 +1360,13 @@ __global__ void __launch_bounds__(256, BDDC_EDGE_MINB) edge_new_kernel(GlobTable
   double* scratch = T2 + (long long)Wd * Wd;
 
   PROF_INIT
+  // the cold input blocks of this edge (prior Schur inputs X, B_E) are requested
+  // from DRAM now; they are first read several dependent steps later
+  for (int i = 0; i < ns; ++i) {
+    const int d = ne + pr.ex_h[k0 + i];
+    blk::prefetch_l2(pr.EX + pr.ex_off[k0 + i], d * d);
+    blk::prefetch_l2(t.BsC + t.sh_doff[k0 + i], ne * ne);
+  }
   // J_i = [delta_ik I - D_k]_{k=1..ns-1}
   for (int idx = threadIdx.x; idx < ns * ne * nC; idx += blockDim.x) {
     int i = idx / (ne * nC), rem = idx - i * ne * nC;

@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
     const long long* __restrict__ elem_ids, const int* __restrict__ loc4,
     const long long* __restrict__ conn, const double* __restrict__ Ke,
     const double* __restrict__ Fe, const double* __restrict__ gdir, int* __restrict__ lists,
-    long long* __restrict__ keys, int nrowbuf, int* __restrict__ overflow, int region0) {
+    long long* __restrict__ keys, int nrowbuf, int* __restrict__ overflow, int region0,
+    const int* __restrict__ nint, const int* __restrict__ ndeep) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int b = blockIdx.x;
   const int nL = nloc[b], L = ld[b];
@@ -156,6 +157,7 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
     double* lval = reinterpret_cast<double*>(hist) + (size_t)warp * 32 * kAsmSlots;
     int* lcol = reinterpret_cast<int*>(reinterpret_cast<double*>(hist) + kAsmWarps * 32 * kAsmSlots) +
                 (size_t)warp * 32 * kAsmSlots;
+    const int nd = ndeep ? ndeep[b] : 0, nIb = nint ? nint[b] : nL;
     double* rbuf = rowbuf + (size_t)warp * (L + 2);
     int ovf = 0;
     for (int rb = warp * 32; rb < nL; rb += kAsmWarps * 32) {
@@ -202,10 +204,24 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
         }
       }
       // dense rows through the warp's shared-memory row buffer: every row of K
-      // is written once, with full-line (16-byte vector) stores
+      // is written once, with full-line (16-byte vector) stores.  With the
+      // two-phase elimination the blocks nobody reads are not written at all:
+      // deep rows x interface columns and interface rows x deep columns (both
+      // structurally zero; the panel kernels, the extraction and the recovery
+      // skip them).
       const int nrows = min(32, nL - rb);
       double2* rb2 = reinterpret_cast<double2*>(rbuf);
       for (int q = 0; q < nrows; ++q) {
+        const int rr = rb + q;
+        int z0 = 0, z1 = 0;
+        if (nd > 0) {
+          if (rr < nd) {
+            z0 = nIb;
+            z1 = nL;
+          } else if (rr >= nIb) {
+            z1 = nd;
+          }
+        }
         for (int c = lane; c < (L >> 1); c += 32) rb2[c] = make_double2(0.0, 0.0);
         __syncwarp();
         const int cq = __shfl_sync(0xffffffffu, cnt, q);
@@ -213,8 +229,9 @@ __global__ void __launch_bounds__(kAsmWarps * 32) assemble_rows_kernel(
         if (lane < cq) rbuf[lcol[lane * 32 + q]] = lval[lane * 32 + q];
         if (lane == 0) rbuf[nL] = fq;
         __syncwarp();
-        double2* row2 = reinterpret_cast<double2*>(M + (long long)(rb + q) * L);
-        for (int c = lane; c < (L >> 1); c += 32) row2[c] = rb2[c];
+        double2* row2 = reinterpret_cast<double2*>(M + (long long)rr * L);
+        for (int c = lane; c < (L >> 1); c += 32)
+          if (!(2 * c >= z0 && 2 * c + 1 < z1)) row2[c] = rb2[c];
         __syncwarp();
       }
     }
@@ -388,8 +405,11 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_row_kernel
 constexpr int kTrailBM = 64;  // row-tile height of the big (mode 0) trailing updates (128 x 64 tiles, 512 threads: measured slower, 34.8 -> 38.2 ms)
 
 // Trailing update of a panel step.  mode 0: rows/cols from k + w, K = w with
-// w = min(nbw, npiv - k) (nbw = 64 or 128).  mode 1 (strip inside a 128-wide
-// panel): rows [k + w1, k + w), cols from k + w1, K = w1, w1 = min(64, npiv - k).
+// w = min(nbw, npiv - k) (nbw = 64 or 128).  mode 1 (inside a 128-wide panel,
+// K = w1 = min(64, npiv - k)): the strip rows [k + w1, k + w), cols from k + w1,
+// and (extra CTAs) the column panel rows >= k + w, cols [k + w1, k + w), so that
+// the factors of a 128-wide panel are those of two 64-wide panels ("rows below
+// only" form: pivot rows W_k = P_k A12^(k), column panels A21^(k)).
 // Lookahead (pnext != null): CTA 0 of each matrix owns the next pivot block
 // (rows / cols from s) and inverts it right after its tile update, so the
 // next panel needs no separate pivot launch.
@@ -430,12 +450,25 @@ __global__ void __launch_bounds__(BM * 4, BM == 64 ? kTileMinBlocks : 2) schur_t
   const int h0 = hole.h0 ? hole.h0[b] : 0, h1 = hole.h0 ? hole.h1[b] : 0;
   const int tn_count = tile_col_count(s, nc, h0, h1);
   if (tn_count <= 0) return;
+  const int L = ld[b];
+  double* M = base + off[b];
+  if (mode == 1 && (int)blockIdx.x >= tn_count) {
+    // the same K = w1 update on the column panel of the second sub-panel below the
+    // 128-wide panel: A21^(k2) = A[., k2] - A[., k1] W1[:, k2 block], so that the
+    // K = 128 trailing update below multiplies [A[., k1] | A21^(k2)] by [W1; W2]
+    // and the factors stay in the 64-panel "rows below only" form
+    const int wt = min(2 * kTile, np);
+    const int r0 = k + wt + ((int)blockIdx.x - tn_count) * BM;
+    const int rend = min(nrows[b], lim);
+    if (r0 >= rend) return;
+    tile_mma_t<BM>(M + (long long)r0 * L + s, L, min(BM, rend - r0), wt - w,
+                   M + (long long)r0 * L + k, L, M + (long long)k * L + s, L, w, -1.0, 1.0, sm);
+    return;
+  }
   const int tm = blockIdx.x / tn_count, tn = blockIdx.x - tm * tn_count;
   const int r0 = r_begin + tm * BM;
   int c0, cn;
   if (r0 >= r_end || !tile_cols(s, tn, nc, h0, h1, c0, cn)) return;
-  const int L = ld[b];
-  double* M = base + off[b];
   tile_mma_t<BM>(M + (long long)r0 * L + c0, L, min(BM, r_end - r0), cn,
                  M + (long long)r0 * L + k, L, M + (long long)k * L + c0, L, w, -1.0, 1.0, sm);
   if (nx.pinv != nullptr && blockIdx.x == 0) {
@@ -455,28 +488,6 @@ __global__ void __launch_bounds__(BM * 4, BM == 64 ? kTileMinBlocks : 2) schur_t
       }
     }
   }
-}
-
-// 128-wide panels: W_top -= W1_Q W2 on rows [k, k+64), cols [k + w, ncols),
-// where W1_Q = M[k:k+64, k+64:k+w] and W2 = M[k+64:k+w, k+w:]
-__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) schur_fix_kernel(
-    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ npiv, const int* __restrict__ ncols, int k, ColHole hole) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-  const int b = blockIdx.y;
-  const int np = npiv[b] - k;
-  const int wt = min(2 * kTile, np);
-  if (wt <= kTile) return;
-  const int w2 = wt - kTile;
-  const int h0 = hole.h0 ? hole.h0[b] : 0, h1 = hole.h0 ? hole.h1[b] : 0;
-  int c0, cn;
-  if (!tile_cols(k + wt, blockIdx.x, ncols[b], h0, h1, c0, cn)) return;
-  const int L = ld[b];
-  double* M = base + off[b];
-  tile_mma(M + (long long)k * L + c0, L, kTile, cn,
-           M + (long long)k * L + k + kTile, L, M + (long long)(k + kTile) * L + c0, L, w2, -1.0,
-           1.0, sm);
 }
 
 // L' = A21 P_k in place on the panel column rows [k+w, lim) (coarse envelope
@@ -828,7 +839,6 @@ static int smem_tile_setup() {
     cudaFuncSetAttribute(gj_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(gj_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     cudaFuncSetAttribute(panel_scale_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    cudaFuncSetAttribute(schur_fix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   });
   return (int)sizeof(TileSmem);
 }
@@ -857,7 +867,8 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
                         const long long* elem_start, const long long* elem_ids, const int* loc4,
                         const long long* conn, const double* Ke, const double* Fe,
                         const double* gdir, int nbatch, int max_nl, int* lists, long long* keys,
-                        int* overflow, int general, cudaStream_t stream) {
+                        int* overflow, int general, const int* nint, const int* ndeep,
+                        cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   int nrowbuf = 0;  // compact row phase (row lists + one row buffer per warp)
   if (general) {
@@ -869,37 +880,9 @@ int bddc_local_assemble(double* K, const long long* off, const int* ld, const in
   cudaFuncSetAttribute(assemble_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   assemble_rows_kernel<<<nbatch, kAsmWarps * 32, smem, stream>>>(
       K, off, ld, nloc, elem_start, elem_ids, loc4, conn, Ke, Fe, gdir, lists, keys, nrowbuf,
-      overflow, (int)assemble_region0(max_nl, nrowbuf));
+      overflow, (int)assemble_region0(max_nl, nrowbuf), nint, ndeep);
   bddc_note_launches(1);
   return launch_status();
-}
-
-// 128-wide panels -> the 64-wide "rows below only" LU form (lus::lu_solve):
-// for panel k (sub-panels k1 = k, k2 = k + 64)
-//   mode 0: column panel k2, rows >= k + 128:  A21^(k2) = A[., k2] - A[., k1] W1_Q
-//   mode 1: pivot rows k1, cols >= k + 128:    W1 = W1_fixed + W1_Q W2
-// with W1_Q = M[k1, k2 block] (= P1 A[k1, k2]) and W2 = M[k2 rows, >= k+128].
-__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) lu128_fixup_kernel(
-    double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ n, int k, int mode) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
-  const int b = blockIdx.y;
-  const int nb = n[b];
-  const int k2 = k + kTile, s = k + 2 * kTile;
-  if (s >= nb) return;  // no second sub-panel with rows / columns beyond it
-  const int t0 = s + blockIdx.x * kTile;
-  if (t0 >= nb) return;
-  const int L = ld[b];
-  double* M = base + off[b];
-  const int w2 = min(kTile, nb - k2);
-  if (mode == 0) {
-    tile_mma(M + (long long)t0 * L + k2, L, min(kTile, nb - t0), w2, M + (long long)t0 * L + k, L,
-             M + (long long)k * L + k2, L, kTile, -1.0, 1.0, sm);
-  } else {
-    tile_mma(M + (long long)k * L + t0, L, kTile, min(kTile, nb - t0), M + (long long)k * L + k2, L,
-             M + (long long)k2 * L + t0, L, w2, 1.0, 1.0, sm);
-  }
 }
 
 // Optional event log of the trailing-update launches (bench roofline over the
@@ -953,16 +936,17 @@ static int schur_eliminate_impl(double* M, const long long* off, const int* ld, 
       ++launches;
     }
     if (panel == 2 * kTile && k + kTile < max_npiv) {
-      // second sub-panel: strip update of its 64 rows (+ its pivot inverse),
-      // W2, then W_top -= W1_Q W2 so the pivot rows hold A11^-1 A12 for all 128
+      // second sub-panel: the K = 64 update by the first one on its 64 rows (+ its
+      // pivot inverse) and on its column panel below the 128-wide panel, then W2
       const int cts = ceil_div(max_cols - k - kTile, kTile);
-      schur_trailing_kernel<64><<<dim3(cts, nbatch), kTileThreads, sizeof(TileSmemT<64>), stream>>>(
-          M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1, nx_sub, hole);
+      // (column-panel tiles start at row k + w_b >= k + 65 of each matrix: bound for all)
+      const int rts = max(0, ceil_div(max_rows - k - kTile, kTile));
+      schur_trailing_kernel<64><<<dim3(cts + rts, nbatch), kTileThreads, sizeof(TileSmemT<64>),
+                                  stream>>>(M, off, ld, npiv, nrows, ncols, k, 0x7fffffff, kTile, 1,
+                                            nx_sub, hole);
       schur_row_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(
           M, off, ld, npiv, ncols, k + kTile, P2, pinv_stride, 0x7fffffff, hole);
-      schur_fix_kernel<<<dim3(cts, nbatch), kTileThreads, smem, stream>>>(M, off, ld, npiv, ncols, k,
-                                                                         hole);
-      launches += 3;
+      launches += 2;
     }
     const int ct = ceil_div(max_cols - k, kTile);
     const int rt = ceil_div(max_rows - k, kTrailBM);
@@ -1074,23 +1058,6 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
     gj_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride, symmetric);
     bddc_note_launches(3);
-  }
-  return launch_status();
-}
-
-int bddc_lu128_fixup(double* M, const long long* off, const int* ld, const int* n, int nbatch,
-                     int max_n, cudaStream_t stream) {
-  if (nbatch <= 0) return 0;
-  const int smem = smem_tile_setup();
-  static PerDeviceOnce once;
-  once([&] {
-    cudaFuncSetAttribute(lu128_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  });
-  for (int k = 0; k + 2 * kTile < max_n; k += 2 * kTile) {
-    const int t = ceil_div(max_n - k - 2 * kTile, kTile);
-    lu128_fixup_kernel<<<dim3(t, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 0);
-    lu128_fixup_kernel<<<dim3(t, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 1);
-    bddc_note_launches(2);
   }
   return launch_status();
 }

@@ -664,6 +664,24 @@ __global__ void lu_diag_pinv_kernel(double* __restrict__ LU, const long long* __
   }
 }
 
+// coarse restriction alone, cvals = G x with x = u[perm] (one CTA per subdomain, warp
+// per primal row): lets the coarse solve start while the local solves still run
+__global__ void __launch_bounds__(256) primal_restrict_kernel(
+    const int* __restrict__ nB, const long long* __restrict__ voff,
+    const int* __restrict__ iface_perm, const double* __restrict__ u,
+    const int* __restrict__ pstart, const long long* __restrict__ poff,
+    const double* __restrict__ G, double* __restrict__ cvals) {
+  extern __shared__ double rsm[];
+  const int b = blockIdx.x;
+  const int n = nB[b];
+  const int np = pstart[b + 1] - pstart[b];
+  if (np == 0) return;
+  const long long v0 = voff[b];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) rsm[j] = u[iface_perm[v0 + j]];
+  __syncthreads();
+  lus::rows_gemv<1>(G + poff[b], n, np, n, rsm, cvals + pstart[b], 1.0, 0.0);
+}
+
 // local part of M^-1 and the coarse restriction, one CTA per subdomain:
 //   x = r[perm];  cvals = G x;  t = TT^T x (primal entries zeroed);  t = Sdd^-1 t (LU);
 //   y = TT t        (= A_i x with A_i = TT Z TT^T, without forming A_i)
@@ -687,7 +705,7 @@ __global__ void __launch_bounds__(256) local_solve_kernel(
   for (int j = threadIdx.x; j < n; j += blockDim.x) xs[j] = u[iface_perm[v0 + j]];
   __syncthreads();
   const int np = pstart[b + 1] - pstart[b];
-  if (np) lus::rows_gemv<1>(G + poff[b], n, np, n, xs, cvals + pstart[b], 1.0, 0.0);
+  if (np && G) lus::rows_gemv<1>(G + poff[b], n, np, n, xs, cvals + pstart[b], 1.0, 0.0);
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     double s = 0.0;
     if (!primal_mask[v0 + i]) {
@@ -1359,6 +1377,20 @@ int bddc_pc_local_solve(const int* nB, const long long* soff, const long long* v
   local_solve_kernel<<<nbatch, 256, smem, stream>>>(nB, soff, voff, iface_perm, LU, pos2k, sub_globs,
                                                     sub_glob_boff, sub_glob_sh, gsize, sh_doff, TT,
                                                     primal_mask, u, y, pstart, poff, G, cvals);
+  bddc_note_launches(1);
+  return pc_status();
+}
+
+int bddc_pc_primal_restrict(const int* nB, const long long* voff, const int* iface_perm,
+                            const double* u, const int* pstart, const long long* poff,
+                            const double* G, double* cvals, int nbatch, int max_nB,
+                            cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  const int smem = max_nB * (int)sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(primal_restrict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  primal_restrict_kernel<<<nbatch, 256, smem, stream>>>(nB, voff, iface_perm, u, pstart, poff, G,
+                                                        cvals);
   bddc_note_launches(1);
   return pc_status();
 }

@@ -24,6 +24,7 @@ from .plan import Plan, _excl, _ranges
 
 F64 = torch.float64
 PANEL = 128  # elimination panel width (two 64-wide sub-panels; DMMA trailing update with K = 128)
+OVERLAP_COARSE = True  # M^-1: coarse branch on a side stream next to the local solves (one rank)
 FUSED_GMRES = True  # one cooperative launch per GMRES step for the vector work (one rank)
 TWO_PHASE = True  # deep interior pivots eliminated first, restricted to the interior block (plan.nDeep)
 
@@ -168,14 +169,15 @@ class LocalSystem:
         ovf = torch.zeros(1, dtype=torch.int32, device="cuda")
         asm_args = (K, d.off, d.ld, d.nL, d.elem_start, d.elem_ids, d.loc4, self.inputs["conn"],
                     Ke, Fe, self.inputs["gdir"], p.N, int(p.nL.max()), lists, keys, ovf)
-        lib.bddc_local_assemble(*asm_args, int(self.general_assembly), st)
+        skip = (d.nI, d.nDeep) if TWO_PHASE else (None, None)  # blocks the elimination never reads
+        lib.bddc_local_assemble(*asm_args, int(self.general_assembly), *skip, st)
         # the element blocks are consumed: keep only the index inputs
         self.inputs = {k: v for k, v in self.inputs.items() if k not in ("Ke", "Fe", "_ebad")}
         status = self._eliminate(K)
         if int(ovf.item()):
             # a row with more than 16 distinct columns (not a Kuhn box mesh):
             # general row-buffer assembly, then the elimination again
-            lib.bddc_local_assemble(*asm_args, 1, st)
+            lib.bddc_local_assemble(*asm_args, 1, None, None, st)
             status = self._eliminate(K)
         del asm_args, lists, keys
         if ebad is not None and int(ebad.item()) != -1:
@@ -349,13 +351,13 @@ def trailing_flops(plan, panel=PANEL, dual_lu=False):
 _SIDE = {}
 
 
-def _side_stream():
+def _side_stream(high_priority=False):
     """Helper stream of the current device and host thread."""
     import threading
 
-    key = (torch.cuda.current_device(), threading.get_ident())
+    key = (torch.cuda.current_device(), threading.get_ident(), bool(high_priority))
     if key not in _SIDE:
-        _SIDE[key] = torch.cuda.Stream()
+        _SIDE[key] = torch.cuda.Stream(priority=-1 if high_priority else 0)
     return _SIDE[key]
 
 
@@ -1126,8 +1128,6 @@ class DevicePreconditioner:
         pinv_all = torch.empty(nsteps * p.N * 4096, dtype=F64, device="cuda")
         lib.bddc_schur_eliminate(Z, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax, nbmax,
                                  PANEL, pinv_all, 4096, p.N * 4096, status, 0, None, 0, None, None, st)
-        if PANEL == 128:  # 128-wide elimination -> the 64-panel form of the local solves
-            lib.bddc_lu128_fixup(Z, d.soff, d.nB, d.nB, p.N, nbmax, st)
         # host work overlapping the queued factorisation: coarse dofs in reverse
         # Cuthill-McKee order of the primal coupling graph (each subdomain's primal
         # set is a clique) -> envelope LU / block-inverse solves
@@ -1322,6 +1322,30 @@ class DevicePreconditioner:
         """r, out: rank-local interface vectors (the global ones on one rank)."""
         ls, p, d, st = self.ls, self.plan, self.ls.d, stream()
         nbmax = int(p.nB.max())
+        if OVERLAP_COARSE and not _multi(self.comm):
+            # the coarse branch (restriction, coarse rhs, block-inverse solve: a latency
+            # chain on a few SMs) runs on a high-priority side stream next to the local
+            # solves (HBM bound) and is joined before the prolongation
+            main = torch.cuda.current_stream()
+            side = _side_stream(high_priority=True)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                s2 = stream()
+                lib.bddc_pc_primal_restrict(d.nB, d.voff, ls.iface_perm_l, r, self.d_pstart,
+                                            self.d_poff, self.G, self.cvals, p.N, nbmax, s2)
+                lib.bddc_gather_reduce(self.d_cstart, self.d_csrc, self.cvals, self.rp,
+                                       self.n_primal, s2)
+                self.coarse_solve(self.rp, self.up)
+            lib.bddc_pc_local_solve(d.nB, d.soff, d.voff, ls.iface_perm_l, self.LU, d.pos2k,
+                                    d.sub_globs, d.sub_glob_boff, d.sub_glob_sh, d.gsize,
+                                    d.sh_doff, self.TT, self.d_mask, r, self.y, self.d_pstart,
+                                    self.d_poff, None, self.cvals, p.N, nbmax, st)
+            main.wait_stream(side)
+            lib.bddc_prolong_primal(d.nB, d.voff, self.d_pstart, self.d_pgid, self.d_poff, self.Nt,
+                                    self.up, self.y, p.N, st)
+            lib.bddc_gather_reduce(ls.tstart_l, ls.tsrc_l, self.y, out, ls.n_loc, st)
+            ls.layout.halo_sum_(out)
+            return out
         lib.bddc_pc_local_solve(d.nB, d.soff, d.voff, ls.iface_perm_l, self.LU, d.pos2k,
                                 d.sub_globs, d.sub_glob_boff, d.sub_glob_sh, d.gsize, d.sh_doff,
                                 self.TT, self.d_mask, r, self.y, self.d_pstart, self.d_poff,
@@ -1639,13 +1663,13 @@ def recover_device(ls, u_hat):
         u = ls.inputs["gdir"].clone()
         u[iface] = u_hat
         lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, d.iface_perm, d.ioff,
-                                  d.I_nodes, u_hat, u, p.N, int(p.nL.max()), PANEL,
+                                  d.I_nodes, u_hat, u, p.N, int(p.nL.max()), 64,
                                   d.nDeep if TWO_PHASE else None, st)
         return u
     lay = ls.layout
     ui = torch.zeros_like(ls.inputs["gdir"])
     lib.bddc_recover_interior(ls.K, d.off, d.ld, d.nI, d.nB, d.voff, ls.iface_perm_l, d.ioff,
-                              d.I_nodes, u_hat, ui, p.N, int(p.nL.max()), PANEL,
+                              d.I_nodes, u_hat, ui, p.N, int(p.nL.max()), 64,
                               d.nDeep if TWO_PHASE else None, st)
     own_nodes = dev_i64(np.asarray(ls.globs.interface_nodes)[lay.glob_ids[:lay.n_own]])
     ui[own_nodes] = u_hat[:lay.n_own]

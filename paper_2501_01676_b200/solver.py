@@ -152,7 +152,7 @@ def direct_schur_solve(ops, globs, rhs):
     x = torch.empty(n, dtype=F64, device="cuda")
     lib.bddc_recover_interior(M, off, ldv, nv, one(0), dev_i64(np.array([0, 0])), one(0),
                               dev_i64(np.array([0, n])), torch.arange(n, device="cuda"), x, x, 1,
-                              n, PANEL, None, st)
+                              n, 64, None, st)
     return x.cpu().numpy()
 
 
