@@ -134,13 +134,16 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
 /* Symmetric in-place Gauss-Jordan inverse in 128-wide panels (K = 128 DMMA
  * trailing updates, half the passes of the 64-panel variant).  Per panel the
  * 128 x 128 pivot block is copied to work (nbatch x 128 x 128; work_off[b] =
- * b * 16384, work_ld[b] = work_n[b] = 128) and inverted there by
- * bddc_gj_inverse (pinv_ws: nbatch x 4096); positive pivots <=> positive
- * definite (the cho_factor criterion).  replaces cho_factor/cho_solve(Bsym, I)
- * substructuring.py:64-75. */
+ * b * 16384, work_ld[b] = 128; work_n: nbatch ints of scratch, distinct from
+ * work_ld) and inverted there by bddc_gj_inverse (pinv_ws: nbatch x 4096);
+ * a pivot block of at most 64 pivots (the last panel of a matrix) is
+ * inverted by one register Gauss-Jordan instead, whatever the other matrices
+ * of the batch need (results do not depend on the batch).  Positive pivots
+ * <=> positive definite (the cho_factor criterion).
+ * replaces cho_factor/cho_solve(Bsym, I) substructuring.py:64-75. */
 int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int* n, int nbatch,
                        int max_n, double* work, const long long* work_off, const int* work_ld,
-                       const int* work_n, double* pinv_ws, int* status, int require_positive,
+                       int* work_n, double* pinv_ws, int* status, int require_positive,
                        cudaStream_t stream);
 
 /* S, g, Bsym = (S + S^T)/2 from the eliminated local matrices.

@@ -340,11 +340,12 @@ __global__ void __launch_bounds__(256, 4) pivot_inverse_kernel(
     const double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
     const int* __restrict__ npiv, int k, double* __restrict__ pinv, long long pinv_stride,
     int* __restrict__ status, int require_positive, double* __restrict__ piv_out,
-    long long piv_stride, int ldo = kTile) {
+    long long piv_stride, int ldo = kTile, int only_small = 0) {
   __shared__ MmaGjSmem sm;
   const int b = blockIdx.x;
   const int w = min(kTile, npiv[b] - k);
   if (w <= 0) return;
+  if (only_small && npiv[b] - k > kTile) return;  // wider pivot blocks: the 128-panel route
   const int L = ld[b];
   const double* M = base + off[b] + (long long)k * L + k;
   const bool bad = reg_gj64(M, L, w, pinv + (long long)b * pinv_stride, ldo, require_positive,
@@ -600,9 +601,14 @@ BDDC_DEV void gj_mirror_tile(double* M, long long L, int k, int w, int r0, int h
 __global__ void gj128_extract_kernel(const double* __restrict__ base,
                                      const long long* __restrict__ off,
                                      const int* __restrict__ ld, const int* __restrict__ n, int k,
-                                     double* __restrict__ work) {
+                                     double* __restrict__ work, int* __restrict__ work_n) {
   const int b = blockIdx.x;
   const int w = max(0, min(128, n[b] - k));
+  // pivot blocks of at most 64 pivots are inverted by one register Gauss-Jordan
+  // (pivot_inverse_kernel), whatever the rest of the batch needs: the work copy
+  // is skipped (size 0), so every matrix takes the same route in any batch
+  if (threadIdx.x == 0) work_n[b] = w > kTile ? 128 : 0;
+  if (w <= kTile) return;
   const double* M = base + off[b] + (long long)k * ld[b] + k;
   double* W = work + (long long)b * 128 * 128;
   for (int idx = threadIdx.x; idx < 128 * 128; idx += blockDim.x) {
@@ -1064,7 +1070,7 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
 
 int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int* n, int nbatch,
                        int max_n, double* work, const long long* work_off, const int* work_ld,
-                       const int* work_n, double* pinv_ws, int* status, int require_positive,
+                       int* work_n, double* pinv_ws, int* status, int require_positive,
                        cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   const int smem = smem_tile_setup();
@@ -1077,14 +1083,13 @@ int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int
   const int T = ceil_div(max_n, kTile);
   const NextPivot none{nullptr, 0, nullptr, 0, nullptr, 0};
   for (int k = 0; k < max_n; k += 128) {
-    if (max_n - k <= kTile) {
-      // last panel of at most 64 pivots in every matrix: its inverse straight into
-      // the work block (leading dimension 128), one register Gauss-Jordan
-      pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work, 128 * 128, status,
-                                                       require_positive, nullptr, 0, 128);
-      bddc_note_launches(1);
-    } else {
-      gj128_extract_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work);
+    // panels of at most 64 pivots (the last one of a matrix): the inverse straight
+    // into the work block (leading dimension 128) by one register Gauss-Jordan
+    pivot_inverse_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work, 128 * 128, status,
+                                                     require_positive, nullptr, 0, 128, 1);
+    bddc_note_launches(1);
+    if (max_n - k > kTile) {
+      gj128_extract_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work, work_n);
       bddc_note_launches(1);
       // P = (pivot block)^-1: symmetric 64-panel Gauss-Jordan on the 128 x 128 copies
       // (positive LDL^T pivots <=> positive definite: the cho_factor criterion)

@@ -239,8 +239,9 @@ class LocalSystem:
             work = torch.empty(p.N * 128 * 128, dtype=F64, device="cuda")
             w_off = torch.arange(p.N, dtype=torch.int64, device="cuda") * (128 * 128)
             w128 = torch.full((p.N,), 128, dtype=torch.int32, device="cuda")
+            wn = torch.empty(p.N, dtype=torch.int32, device="cuda")  # per-panel sizes (scratch)
             lib.bddc_gj_inverse128(Binv, d.soff, d.nB, d.nB, p.N, int(p.nB.max()), work, w_off,
-                                   w128, w128, pinv, status, 1, st)
+                                   w128, wn, pinv, status, 1, st)
             del work
             # norms for the dual-certificate bound (read at the status synchronisation)
             f = torch.zeros(2 * p.N, dtype=F64, device="cuda")
