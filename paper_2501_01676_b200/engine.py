@@ -227,8 +227,11 @@ class LocalSystem:
                                self.g, p.N, st)
         return status
 
-    def bsym_inverse(self):
-        """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check."""
+    def bsym_inverse(self, check=True):
+        """Bsym^-1 for all subdomains (cached); Cholesky-equivalent PD check.
+        check=False queues the work only; check_bsym() then reads the status
+        (the pipeline calls it at its next synchronisation, so the host keeps
+        queueing the following phases meanwhile)."""
         if self._Binv is None:
             p, d, st = self.plan, self.d, stream()
             Binv, self._W = self._W, None  # holds Bsym; inverted in place
@@ -247,15 +250,28 @@ class LocalSystem:
             f = torch.zeros(2 * p.N, dtype=F64, device="cuda")
             lib.bddc_frob2(self.S, d.soff, d.nB, p.N, f[:p.N], st)
             lib.bddc_frob2(Binv, d.soff, d.nB, p.N, f[p.N:], st)
-            bad = _first_bad(status)
-            self._frob = f.cpu().numpy()
-            if bad is not None:
-                S = self.matrix(self.S, bad)
-                B = 0.5 * (S + S.T)
-                raise NumericalError(f"Bsym of subdomain {bad + self.s0} is not positive definite "
-                                     f"(cond ~ {np.linalg.cond(B):.2e})")
             self._Binv = Binv
+            self._bsym_pending = (status, f)
+        if check:
+            self.check_bsym()
         return self._Binv
+
+    def check_bsym(self):
+        """Reads the status of the queued Bsym^-1 (and the norms of the dual
+        certificate); raises the reference's error for a Bsym that is not PD."""
+        pend = getattr(self, "_bsym_pending", None)
+        if pend is None:
+            return
+        status, f = pend
+        self._bsym_pending = None
+        bad = _first_bad(status)
+        self._frob = f.cpu().numpy()
+        if bad is not None:
+            self._Binv = None
+            S = self.matrix(self.S, bad)
+            B = 0.5 * (S + S.T)
+            raise NumericalError(f"Bsym of subdomain {bad + self.s0} is not positive definite "
+                                 f"(cond ~ {np.linalg.cond(B):.2e})")
 
     def slot_sizes(self):
         return self.plan.gsize[self.plan.slot_glob].astype(np.int64) ** 2
@@ -292,7 +308,7 @@ class LocalSystem:
     def slot_binv(self):
         """(Bsym^-1)[g, g] of every (glob, sharer) slot, all ranks'."""
         if self._BiC is None:
-            self._BiC = self._slot_blocks(self.bsym_inverse())
+            self._BiC = self._slot_blocks(self.bsym_inverse(check=False))
         return self._BiC
 
     @property
@@ -647,7 +663,10 @@ class DevicePrimalSpace:
     (reference adaptive.py:288-342 / PrimalBasis adaptive.py:209-264)."""
 
     def __init__(self, ls, scaling, theta_f, theta_e, variant, general=False, detail=False):
-        """general: run the reference algorithm verbatim (no certified shortcuts:
+        """The status checks of Bsym^-1 and of the scaling may have been deferred
+        (bsym_inverse(check=False), DeviceScaling(check=False)): they are read at
+        this phase's first synchronisation, before its own status.
+        general: run the reference algorithm verbatim (no certified shortcuts:
         eigen-based pseudo-inverses, the general pencil solver) for every glob.
         detail: also keep the reference GevpReport fields per glob (pencils,
         all eigenvectors, degenerate flags, constraint rows); implies general."""
@@ -656,6 +675,7 @@ class DevicePrimalSpace:
         p, d, st, comm = ls.plan, ls.d, stream(), ls.comm
         multi = _multi(comm)
         self.ls, self.variant = ls, variant
+        pre_checks = (ls.check_bsym, scaling.check)
         self.general = bool(general or detail)
         self.theta_f, self.theta_e = float(theta_f), float(theta_e)
         BsC, BiC = ls.slot_bsym(), ls.slot_binv()
@@ -716,6 +736,9 @@ class DevicePrimalSpace:
             if dev_sizes:
                 sz = self._new_edge_sizes(edges, nsh)
             s = status.cpu().numpy()
+            for chk in pre_checks:  # (an earlier failure explains any status here)
+                chk()
+            pre_checks = ()
             redo = faces[s[faces] == 900]
             if redo.size:  # certificates failed: general algorithm (linalg.py:116-214)
                 status[dev_i64(redo)] = 0
@@ -724,6 +747,8 @@ class DevicePrimalSpace:
         if multi:
             self._share_results(out)
             set_vertices()
+        for chk in pre_checks:
+            chk()
         self._raise(status, "face")
         # edge results of all ranks are summed into zeroed buffers, then added
         eout = tuple(torch.zeros_like(t) for t in out) if multi else out
@@ -733,12 +758,12 @@ class DevicePrimalSpace:
             tot = sz["totals"].cpu().numpy()
             PB = torch.empty(max(int(tot[0]), 1), dtype=F64, device="cuda")
             XHH = torch.empty(max(int(tot[1]), 1), dtype=F64, device="cuda")
-            lib.bddc_priors(d.kind, d.gsize, d.nB, d.soff, ls.bsym_inverse(), d.sub_glob_start,
+            lib.bddc_priors(d.kind, d.gsize, d.nB, d.soff, ls.bsym_inverse(check=False), d.sub_glob_start,
                             d.sub_globs, d.sub_glob_boff, self.r, self.Q, self.d_q_off, sz["pb_off"],
                             sz["nH"], PB, XHH, sz["xhh_off"], p.N, st)
             EX = torch.empty(max(int(tot[2]), 1), dtype=F64, device="cuda")
             lib.bddc_edge_x_extract(d.slot_local, d.slot_glob, d.gsize, d.kind, d.sh_boff, d.nB,
-                                    d.soff, ls.bsym_inverse(), sz["pb_off"], sz["nH"], PB, XHH,
+                                    d.soff, ls.bsym_inverse(check=False), sz["pb_off"], sz["nH"], PB, XHH,
                                     sz["xhh_off"], EX, sz["ex_off"], int(p.sh_sub.size), st)
             del PB, XHH
             ws = torch.empty(max(int(tot[3]), 1), dtype=F64, device="cuda")
@@ -763,7 +788,7 @@ class DevicePrimalSpace:
             PB = torch.empty(max(int(pb_off[-1]), 1), dtype=F64, device="cuda")
             XHH = torch.empty(max(int(xhh_off[-1]), 1), dtype=F64, device="cuda")
             d_pb_off, d_nH, d_xhh_off = dev_i64(pb_off[:-1]), dev_i32(nH), dev_i64(xhh_off[:-1])
-            lib.bddc_priors(d.kind, d.gsize, d.nB, d.soff, ls.bsym_inverse(), d.sub_glob_start,
+            lib.bddc_priors(d.kind, d.gsize, d.nB, d.soff, ls.bsym_inverse(check=False), d.sub_glob_start,
                             d.sub_globs, d.sub_glob_boff, self.r, self.Q, self.d_q_off, d_pb_off,
                             d_nH, PB, XHH, d_xhh_off, p.N, st)
             # X blocks [[Binv_EE, PB_E^T], [PB_E, XHH]] per (edge, sharer) slot
@@ -774,7 +799,7 @@ class DevicePrimalSpace:
             EX = (torch.zeros if multi else torch.empty)(max(int(ex_off[-1]), 1), dtype=F64, device="cuda")
             d_ex_off = dev_i64(ex_off[:-1])
             lib.bddc_edge_x_extract(d.slot_local, d.slot_glob, d.gsize, d.kind, d.sh_boff, d.nB,
-                                    d.soff, ls.bsym_inverse(), d_pb_off, d_nH, PB, XHH, d_xhh_off,
+                                    d.soff, ls.bsym_inverse(check=False), d_pb_off, d_nH, PB, XHH, d_xhh_off,
                                     EX, d_ex_off, int(sh.size), st)
             if multi:  # prior blocks of remote sharers -> the edge's owner
                 ls.slotx.run(EX, ex_off[:-1], ex_sz, "to_owner")
@@ -1209,26 +1234,29 @@ class DevicePreconditioner:
         self._lim_c = (ctypes.c_int * steps)(*self.lim.tolist())
         self._first_c = (ctypes.c_int * steps)(*self.first.tolist())
         self.d_lim, self.d_first = dev_i32(self.lim), dev_i32(self.first)
-        lib.bddc_coarse_factor(C, dev_i64([0]), dev_i32([nc]), dev_i32([nc]), nc,
-                               ctypes.cast(self._lim_c, ctypes.c_void_p), self.coarse_pinv, piv,
-                               status1, st)
-        self.coarse_lu = C
-        self._check_coarse(piv, go, ls)
-        # block-inverse solve operators (coarse.cu); the dense factor is not kept
+        # layout and buffers of the block-inverse solve operators (coarse.cu) before the
+        # factorisation is queued: nothing but the pivot check sits between the two
         lay = coarse_blockinv_layout(self.lim, nc)
         self.cb_nD = lay["nD"]
         self.cb_cl, self.cb_cu = dev_i32(lay["cl"]), dev_i32(lay["cu"])
         self.cb_foff, self.cb_goff = dev_i64(lay["foff"][:-1]), dev_i64(lay["goff"][:-1])
         self.cb_F = torch.empty(max(int(lay["foff"][-1]), 1), dtype=F64, device="cuda")
         self.cb_G = torch.empty(max(int(lay["goff"][-1]), 1), dtype=F64, device="cuda")
+        self.cb_cnt = torch.zeros(2 * self.cb_nD, dtype=torch.int32, device="cuda")
+        self.cb_z = torch.empty(nc, dtype=F64, device="cuda")
+        lib.bddc_coarse_factor(C, dev_i64([0]), dev_i32([nc]), dev_i32([nc]), nc,
+                               ctypes.cast(self._lim_c, ctypes.c_void_p), self.coarse_pinv, piv,
+                               status1, st)
+        self.coarse_lu = C
+        # the block inverses are queued behind the factor before its pivots are read
+        # back (a singular factor raises below, before anything uses them)
         lib.bddc_coarse_blockinv(C, nc, nc, self.coarse_pinv, 4096, self.cb_nD, self.cb_cl,
                                  self.cb_cu, self.cb_foff, self.cb_goff, lay["max_ldf"],
                                  lay["max_ldg"], self.cb_F, self.cb_G, st)
-        self.cb_cnt = torch.zeros(2 * self.cb_nD, dtype=torch.int32, device="cuda")
         self.cb_epoch = 0
-        self.cb_z = torch.empty(nc, dtype=F64, device="cuda")
         self.coarse_factor_bytes = 8 * (int(lay["foff"][-1]) + int(lay["goff"][-1]))
         main.wait_stream(side)
+        self._check_coarse(piv, go, ls)
         del C, self.coarse_lu, self.coarse_pinv
 
     def _cinit_bufs(self, nc):

@@ -47,10 +47,12 @@ def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8,
     ls = LocalSystem(system, partition, globs, plan=plan, inputs=inputs,
                      kernel_timing=kernel_timing, dplan=dplan, comm=comm)
     inputs = None
+    # the status checks of Bsym^-1 and of the scaling are read at the first
+    # synchronisation of the GEP phase: the host keeps queueing meanwhile
     tm.mark("bsym_inverse")
-    ls.bsym_inverse()
+    ls.bsym_inverse(check=False)
     tm.mark("scaling")
-    sc = DeviceScaling(ls)
+    sc = DeviceScaling(ls, check=False)
     tm.mark("gevp")
     ps = DevicePrimalSpace(ls, sc, theta_f, theta_e, variant, general=general)
     tm.mark("pc_setup")
