@@ -287,20 +287,26 @@ class Plan:
         owner[conn.reshape(-1)] = sub_of[:, None].expand(-1, 4).reshape(-1)
         on_iface = torch.zeros(n_nodes, dtype=torch.bool, device=dv)
         on_iface[self._iface_nodes_d] = True
-        I_all = torch.nonzero(free & ~on_iface & (owner >= 0)).squeeze(1)   # ascending node ids
-        I_sub_all = owner[I_all]
+        interior = free & ~on_iface & (owner >= 0)
         # deep interior nodes (no element shared with an interface node) first
-        # (integer scatter-add of the per-element flag: no host sync, order-independent)
+        # (integer scatter-add of the per-element flag: order-independent)
         touch = on_iface[conn].any(dim=1).to(torch.int32)
         shell = torch.zeros(n_nodes, dtype=torch.int32, device=dv)
         shell.index_add_(0, conn.reshape(-1), touch[:, None].expand(-1, 4).reshape(-1))
-        sh_all = (shell[I_all] > 0).to(torch.int64)
-        o = torch.sort(I_sub_all * 2 + sh_all, stable=True).indices
-        I_node, I_sub = I_all[o], I_sub_all[o]
-        self._cnt_d = torch.bincount(I_sub * 2 + sh_all[o], minlength=2 * N).view(N, 2)
-        self.I_nodes_d, self._I_sub_d = I_node, I_sub
+        # Nothing here synchronises with the host (no nonzero / bincount / mask
+        # indexing): every node gets the key 2 * owner + shell, non-interior nodes a
+        # sentinel that sorts last; one stable sort orders the interior nodes by
+        # (subdomain, shell, node id) and the counts come from an integer scatter-add.
+        # The interior prefix is cut off once the counts are on the host.
+        key = torch.where(interior, owner * 2 + (shell > 0), torch.full_like(owner, 2 * N))
+        self._node_order_d = torch.sort(key, stable=True).indices
+        self._owner_d = owner
+        one = torch.ones((), dtype=torch.int64, device=dv)
+        self._cnt_d = torch.zeros(2 * N + 1, dtype=torch.int64, device=dv).index_add_(
+            0, key, one.expand(n_nodes))
         self.elem_ids_d = torch.sort(sub_of, stable=True).indices
-        self._ecnt_d = torch.bincount(sub_of, minlength=N)
+        self._ecnt_d = torch.zeros(N, dtype=torch.int64, device=dv).index_add_(
+            0, sub_of, one.expand(sub_of.numel()))
 
     def _element_post_torch(self, dev):
         import torch
@@ -309,12 +315,14 @@ class Plan:
 
         N, n_nodes = self.N, self.n_nodes
         conn, dv = dev["conn"], dev["conn"].device
-        cnt_h = self._cnt_d.cpu().numpy().astype(np.int64)
+        cnt_h = self._cnt_d[:2 * N].view(N, 2).cpu().numpy().astype(np.int64)  # the one sync
         self.nI = cnt_h.sum(axis=1)
         self.nDeep = cnt_h[:, 0] & ~np.int64(1)
         self.ioff = _excl(self.nI)
         self.elem_start = _excl(self._ecnt_d.cpu().numpy())
-        I_node, I_sub = self.I_nodes_d, self._I_sub_d
+        I_node = self._node_order_d[:int(self.nI.sum())]
+        I_sub = self._owner_d[I_node]
+        self.I_nodes_d = I_node
         iloc = torch.full((n_nodes,), -1, dtype=torch.int32, device=dv)
         iloc[I_node] = (torch.arange(I_node.numel(), device=dv) - _up(self.ioff, dv)[I_sub]).to(torch.int32)
         self.loc4_d = torch.empty((conn.shape[0], 4), dtype=torch.int32, device=dv)
@@ -322,7 +330,7 @@ class Plan:
                            self._glob_of_node_d, self._pos_in_glob_d, _up(self.sh_start, dv),
                            _up(self.sh_sub, dv), _up(self.sh_boff, dv),
                            _up(self.nI, dv), self.loc4_d, stream())
-        del self._cnt_d, self._ecnt_d, self._I_sub_d
+        del self._cnt_d, self._ecnt_d, self._node_order_d, self._owner_d
 
     def _node_maps_device(self, dv):
         """node -> glob index and position in the glob (-1 off the interface),
