@@ -26,6 +26,7 @@ struct MmaGjSmem {
   double R[2][4][kTile];     // pivot rows (double-buffered by step parity)
   double F[2][kTile][4];     // pivot columns
   double U[4][68];           // Mi * R (pivot columns: I + Mi); stride 68: conflict-free B fragments
+  double pv[kTile];          // scalar pivots (written to piv at the end)
   int bad;
 };
 
@@ -180,7 +181,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
       const int col = 8 * j + 2 * t + h;
       c[j][h] = (row < w && col < w) ? M[(long long)row * L + col] : (row == col ? 1.0 : 0.0);
     }
-  if (threadIdx.x == 0) sm.bad = 0;
+  bool bad_any = false;
   const int nsteps = min((w + 3) >> 2, max_steps);
   GJ_PROF(36);
   for (int s = 0; s < nsteps; ++s) {
@@ -207,20 +208,30 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
     // lanes 16..31 mirror lanes 0..15): no shared-memory round trip for Mi
     double m;
     {
+      // (the pivot bookkeeping stays out of this dependent chain: every lane
+      // holds the same pivot, so the validity test is uniform and branch-free;
+      // the pivots go to shared memory once per step and to piv at the end)
       const int i = (lane >> 2) & 3, jj = lane & 3;
       m = sm.R[par][i][p + jj];
+      double pvq[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const double pv = __shfl_sync(0xffffffffu, m, 5 * q);
         const double rq = __shfl_sync(0xffffffffu, m, 4 * q + jj);
         const double cq = __shfl_sync(0xffffffffu, m, 4 * i + q);
-        if (threadIdx.x == 0 && p + q < w) {
-          if (piv) piv[p + q] = pv;
-          if (!(pv == pv) || pv == 0.0 || isinf(pv) || (require_positive && !(pv > 0.0))) sm.bad = 1;
-        }
+        pvq[q] = pv;
+        bad_any |= (p + q < w) &&
+                   (!(pv == pv) || pv == 0.0 || isinf(pv) || (require_positive && !(pv > 0.0)));
         const double ip = 1.0 / pv;
         if (i == q) m = (jj == q) ? ip : rq * ip;
         else m = (jj == q) ? -cq * ip : m - cq * rq * ip;
+      }
+      if (threadIdx.x < 4) {
+        double v = pvq[0];
+#pragma unroll
+        for (int q = 1; q < 4; ++q)
+          if ((int)threadIdx.x == q) v = pvq[q];
+        sm.pv[p + threadIdx.x] = v;
       }
     }
     GJ_PROF(33);
@@ -271,10 +282,11 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
       const int col = 8 * j + 2 * t + h;
       if (row < w && col < w) out[(long long)row * ldo + col] = c[j][h];
     }
-  const bool failed = sm.bad != 0;
-  gj_sync256();
+  if (piv)
+    for (int i = threadIdx.x; i < min(w, 4 * nsteps); i += 256) piv[i] = sm.pv[i];
+  gj_sync256();  // sm reusable after return
   GJ_PROF(37);
-  return failed;
+  return bad_any;  // the same value in every thread
 }
 
 }  // namespace bddc
