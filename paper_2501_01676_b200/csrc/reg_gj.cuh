@@ -16,6 +16,16 @@ namespace bddc {
 // first 256 threads of a larger CTA can run the inverse on their own
 BDDC_DEV void gj_sync256() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
+// reciprocal on the dependent pivot chain: hardware approximation plus two
+// Newton steps (a few ulps; zero / non-finite pivots are flagged separately)
+BDDC_DEV double gj_rcp(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  r = fma(r, fma(-q, r, 1.0), r);
+  r = fma(r, fma(-q, r, 1.0), r);
+  return r;
+}
+
 struct RegGjSmem {
   double rowb[2][4][kTile];
   double colb[2][4][kTile];
@@ -222,7 +232,7 @@ BDDC_DEV bool reg_gj64(const double* __restrict__ M, long long L, int w, double*
         pvq[q] = pv;
         bad_any |= (p + q < w) &&
                    (!(pv == pv) || pv == 0.0 || isinf(pv) || (require_positive && !(pv > 0.0)));
-        const double ip = 1.0 / pv;
+        const double ip = gj_rcp(pv);
         if (i == q) m = (jj == q) ? ip : rq * ip;
         else m = (jj == q) ? -cq * ip : m - cq * rq * ip;
       }
