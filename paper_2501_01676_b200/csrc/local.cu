@@ -13,7 +13,6 @@
 #include "bddc_b200.h"
 #include "tile_mma.cuh"
 #include "reg_gj.cuh"
-#include "dense_block.cuh"
 
 #include <vector>
 
@@ -618,55 +617,6 @@ __global__ void gj128_extract_kernel(const double* __restrict__ base,
   }
 }
 
-// Inverse of the 128-wide pivot block of step k (64 < w <= 128 pivots) in ONE
-// launch, one CTA per matrix, by the 2 x 2 block formula on 64-blocks:
-//   P1 = A11^-1,  X = P1 A12,  S = A22 - A21 X,  P2 = S^-1,
-//   inv = [[P1 + X P2 X^T, -X P2], [-P2 X^T, P2]]
-// (two register Gauss-Jordans + four 64^3 products on DMMA; the positive
-// pivots of A11 and S are the LDL^T pivots of the block: cho_factor criterion).
-// Result in work (ld 128); matrices with w <= 64 are left to pivot_inverse_kernel.
-__device__ __noinline__ void gemm_ni(double* C, int ldc, const double* A, int lda, bool ta,
-                                     const double* B, int ldb, bool tb, int m, int n, int k,
-                                     double alpha, double beta) {
-  blk::gemm(C, ldc, A, lda, ta, B, ldb, tb, m, n, k, alpha, beta);
-}
-
-__global__ void __launch_bounds__(256, 3) gj128_pivot_kernel(
-    const double* __restrict__ base, const long long* __restrict__ off,
-    const int* __restrict__ ld, const int* __restrict__ n, int k, double* __restrict__ work,
-    int* __restrict__ status, int require_positive) {
-  __shared__ MmaGjSmem gsm;
-  const int b = blockIdx.x;
-  const int wfull = n[b] - k;
-  if (wfull <= kTile) return;
-  const int w2 = min(128, wfull) - kTile;  // second block: 1..64 pivots
-  const int L = ld[b];
-  const double* M = base + off[b] + (long long)k * L + k;
-  double* W = work + (long long)b * 128 * 128;
-  double* W11 = W;
-  double* W12 = W + kTile;
-  double* W21 = W + (long long)kTile * 128;
-  double* W22 = W21 + kTile;
-  bool bad = reg_gj64(M, L, kTile, W11, 128, require_positive, nullptr, gsm);
-  __syncthreads();
-  // X = P1 A12 -> W12
-  gemm_ni(W12, 128, W11, 128, false, M + kTile, L, false, kTile, w2, kTile, 1.0, 0.0);
-  // S = A22 - A21 X -> W22 (A21 read from the matrix)
-  blk::copy(W22, 128, M + (long long)kTile * L + kTile, L, w2, w2);
-  gemm_ni(W22, 128, M + (long long)kTile * L, L, false, W12, 128, false, w2, w2, kTile, -1.0, 1.0);
-  bad |= reg_gj64(W22, 128, w2, W22, 128, require_positive, nullptr, gsm);
-  __syncthreads();
-  // -P2 X^T -> W21;  P1 + X P2 X^T = P1 - X W21 -> W11;  W12 = W21^T
-  gemm_ni(W21, 128, W22, 128, false, W12, 128, true, w2, kTile, w2, -1.0, 0.0);
-  gemm_ni(W11, 128, W12, 128, false, W21, 128, false, kTile, kTile, w2, -1.0, 1.0);
-  for (int idx = threadIdx.x; idx < kTile * w2; idx += blockDim.x) {
-    const int r = idx / w2, c = idx - r * w2;
-    W12[r * 128 + c] = W21[c * 128 + r];
-  }
-  if (threadIdx.x == 0 && bad && status)
-    atomicCAS(status + b, 0, require_positive ? (int)kNotPositiveDefinite : (int)kSingularPivot);
-}
-
 // W = P A_(k, c0) in place (one 128 x 64 tile per CTA; BM = 128 so a single CTA
 // owns every row it overwrites); the pivot column tiles receive sym(P)
 __global__ void __launch_bounds__(512) gj128_row_kernel(double* __restrict__ base,
@@ -1139,10 +1089,13 @@ int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int
                                                      require_positive, nullptr, 0, 128, 1);
     bddc_note_launches(1);
     if (max_n - k > kTile) {
-      // wider pivot blocks: 2 x 2 block inverse on 64-blocks, one launch
-      gj128_pivot_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work, status,
-                                                     require_positive);
+      gj128_extract_kernel<<<nbatch, 256, 0, stream>>>(M, off, ld, n, k, work, work_n);
       bddc_note_launches(1);
+      // P = (pivot block)^-1: symmetric 64-panel Gauss-Jordan on the 128 x 128 copies
+      // (positive LDL^T pivots <=> positive definite: the cho_factor criterion)
+      int rc = bddc_gj_inverse(work, work_off, work_ld, work_n, nbatch, 128, pinv_ws, 4096, status,
+                               require_positive, 1, stream);
+      if (rc) return rc;
     }
     gj128_row_kernel<<<dim3(T, nbatch), 512, sizeof(TileSmemT<128>), stream>>>(M, off, ld, n, k,
                                                                                work);
