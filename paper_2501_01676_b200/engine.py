@@ -708,7 +708,10 @@ class DevicePrimalSpace:
         edges = np.flatnonzero((kind == 1) & p.glob_mine)
         # glob Schur blocks sym(((Bsym^-1)[g,g])^-1) of every slot of those globs
         # (n_g <= 64), batched: one register Gauss-Jordan per CTA
-        sel = (kind[p.slot_glob] != 2) & p.glob_mine[p.slot_glob] & (p.gsize[p.slot_glob] <= 64)
+        # (faces always; edges only for the old edge eigenproblem -- the new one forms
+        # its Schur blocks from the prior-augmented X blocks instead)
+        want = (kind[p.slot_glob] == 0) if variant == "new" else (kind[p.slot_glob] != 2)
+        sel = want & p.glob_mine[p.slot_glob] & (p.gsize[p.slot_glob] <= 64)
         sc_slots = np.flatnonzero(sel)
         self.SC = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
         self.sc_status = torch.zeros(max(int(p.sh_sub.size), 1), dtype=torch.int32, device="cuda")
