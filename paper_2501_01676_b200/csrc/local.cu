@@ -544,7 +544,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_row_kernel(
 // computed and each off-diagonal result is mirrored with that sign.
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel(
     double* __restrict__ base, const long long* __restrict__ off, const int* __restrict__ ld,
-    const int* __restrict__ n, int k, int symmetric, NextPivot nx, int pw) {
+    const int* __restrict__ n, int k, int symmetric, NextPivot nx, int pw, int compact) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   TileSmem& sm = *reinterpret_cast<TileSmem*>(smem_raw);
   const int b = blockIdx.y;
@@ -552,8 +552,23 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks) gj_update_kernel
   const int w = min(pw, nb - k);  // pivots of this step (panel width pw = 64 or 128)
   if (w <= 0) return;
   const int T = (nb + kTile - 1) / kTile;
-  const int tm = blockIdx.x / T, tn = blockIdx.x - tm * T;
-  if (tm >= T) return;
+  int tm, tn;
+  if (compact) {
+    // symmetric variant, compact grid: blockIdx.x enumerates only the lower-triangular
+    // pairs (i >= j) of the tiles outside the pivot range (no CTAs that exit at once)
+    const int x = blockIdx.x;
+    int i = (int)((sqrtf(8.0f * (float)x + 1.0f) - 1.0f) * 0.5f);
+    while ((i + 1) * (i + 2) / 2 <= x) ++i;
+    while (i * (i + 1) / 2 > x) --i;
+    const int j = x - i * (i + 1) / 2;
+    const int ip = k / kTile, npv = pw / kTile;
+    tm = i < ip ? i : i + npv;
+    tn = j < ip ? j : j + npv;
+  } else {
+    tm = blockIdx.x / T;
+    tn = blockIdx.x - tm * T;
+  }
+  if (tm >= T || tn >= T) return;
   const int r0 = tm * kTile, c0 = tn * kTile;
   if ((r0 >= k && r0 < k + pw) || (c0 >= k && c0 < k + pw)) return;
   if (symmetric && tn > tm) return;
@@ -1059,8 +1074,15 @@ int bddc_gj_inverse(double* M, const long long* off, const int* ld, const int* n
     }
     gj_row_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride, symmetric);
-    gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(
-        M, off, ld, n, k, symmetric, look && k + kTile < max_n ? nx : none, kTile);
+    if (symmetric) {  // lower-triangular pairs of the T - 1 tiles outside the pivot tile
+      const int na = T - 1;
+      if (na > 0)
+        gj_update_kernel<<<dim3(na * (na + 1) / 2, nbatch), kTileThreads, smem, stream>>>(
+            M, off, ld, n, k, 1, look && k + kTile < max_n ? nx : none, kTile, 1);
+    } else {
+      gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 0, none,
+                                                                           kTile, 0);
+    }
     gj_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, pinv_ws,
                                                                   pinv_stride, symmetric);
     bddc_note_launches(3);
@@ -1099,8 +1121,12 @@ int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int
     }
     gj128_row_kernel<<<dim3(T, nbatch), 512, sizeof(TileSmemT<128>), stream>>>(M, off, ld, n, k,
                                                                                work);
-    gj_update_kernel<<<dim3(T * T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k, 1,
-                                                                         none, 128);
+    {  // lower-triangular pairs of the tiles outside the (up to two) pivot tiles
+      const int na = T - min(2, T - k / kTile);
+      if (na > 0)
+        gj_update_kernel<<<dim3(na * (na + 1) / 2, nbatch), kTileThreads, smem, stream>>>(
+            M, off, ld, n, k, 1, none, 128, 1);
+    }
     gj128_col_kernel<<<dim3(T, nbatch), kTileThreads, smem, stream>>>(M, off, ld, n, k);
     bddc_note_launches(3);
   }
