@@ -649,6 +649,65 @@ BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, dou
     // (no barrier here: the product below reads v straight from column k of A,
     // which this step only overwrites after the next barrier)
     if (t != 0.0) {
+      if (nth() == 256 && m <= 48) {
+        // Register-tiled form for the common size (shared-memory bandwidth is what
+        // bounds this loop): thread (ty, tx) of a 16 x 16 grid owns the 3 x 3
+        // elements (ty + 16 a, tx + 16 b); v and p are read once per row / column
+        // of the tile instead of once per element (the update does the same
+        // operations per element as the general form below).
+        const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+        const double* vcol = A + (k + 1) * ld + k;
+        double vc[3], s3[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int bq = 0; bq < 3; ++bq) {
+          const int c = tx + 16 * bq;
+          vc[bq] = c < m ? (c == 0 ? 1.0 : vcol[c * ld] * scal) : 0.0;
+        }
+#pragma unroll
+        for (int a3 = 0; a3 < 3; ++a3) {
+          const int r = ty + 16 * a3;
+          if (r < m) {
+            const double* ar = A + (k + 1 + r) * ld + k + 1;
+#pragma unroll
+            for (int bq = 0; bq < 3; ++bq) {
+              const int c = tx + 16 * bq;
+              if (c < m) s3[a3] += ar[c] * vc[bq];
+            }
+          }
+        }
+        // sum over the 16 threads of a row group (same ty: one half-warp)
+#pragma unroll
+        for (int a3 = 0; a3 < 3; ++a3) {
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) s3[a3] += __shfl_xor_sync(0xffffffffu, s3[a3], o);
+          const int r = ty + 16 * a3;
+          if (tx == 0 && r < m) p[r] = t * s3[a3];
+        }
+        __syncthreads();
+        double pv = 0.0;
+        for (int i = lane; i < m; i += 32) pv += p[i] * v[i];
+        for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+        const double hc = 0.5 * t * pv;
+        double vr[3], wr[3], wc[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int r = ty + 16 * q, c = tx + 16 * q;
+          vr[q] = r < m ? v[r] : 0.0;
+          wr[q] = r < m ? p[r] - hc * vr[q] : 0.0;
+          wc[q] = c < m ? p[c] - hc * vc[q] : 0.0;
+        }
+#pragma unroll
+        for (int a3 = 0; a3 < 3; ++a3) {
+          const int r = ty + 16 * a3;
+          if (r >= m) continue;
+          double* ar = A + (k + 1 + r) * ld + k + 1;
+#pragma unroll
+          for (int bq = 0; bq < 3; ++bq) {
+            const int c = tx + 16 * bq;
+            if (c < m) ar[c] -= vr[a3] * wc[bq] + wr[a3] * vc[bq];
+          }
+        }
+      } else {
       // p = t * A22 v   (A22 = A[k+1:, k+1:], symmetric: use full stored block);
       // 4 lanes per row, each a strided quarter of the columns (short
       // dependency chains instead of one warp-wide reduction per row)
@@ -673,6 +732,7 @@ BDDC_DEV void tridiagonalize(double* A, int ld, int n, double* d, double* e, dou
       BLK_FOR_RC(m, m) {
         const double wr = p[r] - hc * v[r], wc = p[c] - hc * v[c];
         A[(k + 1 + r) * ld + k + 1 + c] -= v[r] * wc + wr * v[c];
+      }
       }
     }
     // keep v_k below the subdiagonal for the back-transformation (column k is
