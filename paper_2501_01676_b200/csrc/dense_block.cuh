@@ -230,10 +230,33 @@ BDDC_DEV bool cholesky(double* A, int ld, int n) {
     }
     const double id = 1.0 / d;
     const int m = n - j - 1;
-    BLK_FOR_RC(m, m) {
-      if (c <= r) {
-        const int ri = j + 1 + r, ci = j + 1 + c;
-        A[ri * ld + ci] -= A[ri * ld + j] * A[ci * ld + j] * id;
+    if (nth() == 256 && m <= 48) {
+      // register-tiled (3 x 3 elements per thread of a 16 x 16 grid): the column
+      // entries are read once per tile row / column instead of once per element
+      const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+      double ar[3], ac[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const int r = ty + 16 * q, c = tx + 16 * q;
+        ar[q] = r < m ? A[(j + 1 + r) * ld + j] : 0.0;
+        ac[q] = c < m ? A[(j + 1 + c) * ld + j] : 0.0;
+      }
+#pragma unroll
+      for (int a3 = 0; a3 < 3; ++a3) {
+        const int r = ty + 16 * a3;
+        if (r >= m) continue;
+#pragma unroll
+        for (int bq = 0; bq < 3; ++bq) {
+          const int c = tx + 16 * bq;
+          if (c <= r) A[(j + 1 + r) * ld + j + 1 + c] -= ar[a3] * ac[bq] * id;
+        }
+      }
+    } else {
+      BLK_FOR_RC(m, m) {
+        if (c <= r) {
+          const int ri = j + 1 + r, ci = j + 1 + c;
+          A[ri * ld + ci] -= A[ri * ld + j] * A[ci * ld + j] * id;
+        }
       }
     }
     __syncthreads();
