@@ -230,12 +230,18 @@ int bddc_row_space_batched(const double* rows, const long long* roff, const int*
  * [pencil_left n^2 | pencil_right n^2 | eigenvectors n^2 | constraint rows
  * n_sel x n (n^2 slot) | degenerate flags n], the reference GevpReport fields
  * (adaptive.py:36-47); implies mode -1.
+ * SC / sc_status: the per-slot glob Schur blocks of bddc_slot_schur, or NULL; with
+ * SC = NULL the fast path (mode 1, n <= 64) bounds their norms by the Bsym
+ * principal blocks and needs sub_ok (per subdomain: 1 when cond(Bsym) is
+ * certified, ||S||_F ||Bsym^-1||_F < 1e11) in place of the per-block PD checks;
+ * faces of uncertified subdomains get status 900.
  * replaces face_gevp adaptive.py:57-72, glob_schur_block substructuring.py:152-171,
  *          parallel_sum / pseudo_inverse / sym_pencil_gevp linalg.py:23-214,
  *          build_change_of_basis adaptive.py:190-206. */
 int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                    const int* sh_boff, const long long* sh_doff, const double* BsC,
-                   const double* BiC, const double* SC, const int* sc_status, const double* D, double theta, double* eig,
+                   const double* BiC, const double* SC, const int* sc_status, const int* sub_ok,
+                   const double* D, double theta, double* eig,
                    const long long* eig_off, int* n_sel, int* r, double* Q, const long long* q_off,
                    int* status, double* ws, const long long* ws_off, const int* face_ids,
                    int n_faces, int max_n, int mode, double* detail, const long long* detail_off,

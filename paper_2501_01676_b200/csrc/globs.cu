@@ -71,6 +71,9 @@ struct GlobTables {
   // per slot: sym((Bsym^-1)[g,g]^-1) for n_g <= 64 (slot_schur_kernel), or null
   const double* SC;
   const int* sc_status;
+  // per subdomain (face fast path without SC): 1 when ||S||_F ||Bsym^-1||_F < 1e11,
+  // i.e. cond(Bsym) certified, so every principal block of Bsym^-1 is numerically PD
+  const int* sub_ok;
 };
 
 // ---------------------------------------------------------------------------
@@ -736,15 +739,27 @@ BDDC_DEV void face_fast_small(const GlobTables& t, const double* __restrict__ D,
   const double* Bj = t.BsC + t.sh_doff[k0 + 1];
   const double* Xi = t.BiC + t.sh_doff[k0];
   const double* Xj = t.BiC + t.sh_doff[k0 + 1];
-  const double* SCi = t.SC + t.sh_doff[k0];
-  const double* SCj = t.SC + t.sh_doff[k0 + 1];
+  // Norm bounds of the glob Schur blocks Bt_s = ((Bsym_s^-1)[F,F])^-1 for the
+  // certificates: ||SC_s||_F when the slot Schur blocks were formed
+  // (slot_schur_kernel), else ||Bsym_s[F,F]||_F >= ||Bt_s||_2 (a Schur complement
+  // of an SPD matrix is below its principal block) -- then no block is inverted
+  // at all, and the subdomain certificate sub_ok stands in for the PD check of
+  // (Bsym_s^-1)[F,F] (_invert_principal, substructuring.py:161-171).
+  const bool have_sc = t.SC != nullptr;
+  const double* SCi = have_sc ? t.SC + t.sh_doff[k0] : Bi;
+  const double* SCj = have_sc ? t.SC + t.sh_doff[k0 + 1] : Bj;
   PROF_INIT
-  if (t.sc_status[k0]) {
-    if (threadIdx.x == 0) o.status[g] = 100;
-    return;
-  }
-  if (t.sc_status[k0 + 1]) {
-    if (threadIdx.x == 0) o.status[g] = 101;
+  if (have_sc) {
+    if (t.sc_status[k0]) {
+      if (threadIdx.x == 0) o.status[g] = 100;
+      return;
+    }
+    if (t.sc_status[k0 + 1]) {
+      if (threadIdx.x == 0) o.status[g] = 101;
+      return;
+    }
+  } else if (!t.sub_ok[t.sh_sub[k0]] || !t.sub_ok[t.sh_sub[k0 + 1]]) {
+    if (threadIdx.x == 0) o.status[g] = kNeedFallback;
     return;
   }
   if (prefetch) {  // every cold input block of this face is requested from DRAM now
@@ -752,8 +767,10 @@ BDDC_DEV void face_fast_small(const GlobTables& t, const double* __restrict__ D,
     blk::prefetch_l2(Bj, nn);
     blk::prefetch_l2(Xi, nn);
     blk::prefetch_l2(Xj, nn);
-    blk::prefetch_l2(SCi, nn);
-    blk::prefetch_l2(SCj, nn);
+    if (have_sc) {
+      blk::prefetch_l2(SCi, nn);
+      blk::prefetch_l2(SCj, nn);
+    }
   }
   // 1. B_F = sym(Dj^T Bi Dj + Di^T Bj Di) -> C
   blk::copy_flat4(B, Dj, nn);
@@ -895,7 +912,7 @@ __global__ void __launch_bounds__(256, SMALL ? 3 : 1) face_fast_kernel(
   double* W = arena_in_smem ? reinterpret_cast<double*>(degen + ((max_n + 2 + 1) & ~1))
                             : ws + ws_off[g];
   if (n <= kTile) {
-    if (t.SC == nullptr) {  // the three-region path needs the slot Schur blocks
+    if (t.SC == nullptr && t.sub_ok == nullptr) {  // needs one of the two norm sources
       if (threadIdx.x == 0) o.status[g] = kNeedFallback;
       return;
     }
@@ -1805,13 +1822,15 @@ int bddc_slot_schur(const int* slots, int n_slots, const int* slot_glob, const i
 
 int bddc_face_gevp(const int* kind, const int* size, const int* sh_start, const int* sh_sub,
                    const int* sh_boff, const long long* sh_doff, const double* BsC,
-                   const double* BiC, const double* SC, const int* sc_status, const double* D, double theta, double* eig,
+                   const double* BiC, const double* SC, const int* sc_status, const int* sub_ok,
+                   const double* D, double theta, double* eig,
                    const long long* eig_off, int* n_sel, int* r, double* Q, const long long* q_off,
                    int* status, double* ws, const long long* ws_off, const int* face_ids,
                    int n_faces, int max_n, int mode, double* detail, const long long* detail_off,
                    cudaStream_t stream) {
   if (n_faces <= 0) return 0;
   GlobTables t = make_tables(kind, size, sh_start, sh_sub, sh_boff, sh_doff, BsC, BiC, SC, sc_status);
+  t.sub_ok = sub_ok;
   // mode 1: certified fast kernel; 0: general kernel with the certified shortcuts;
   // -1: the reference algorithm verbatim.  A detail request implies mode -1.
   if (detail) mode = -1;

@@ -713,10 +713,22 @@ class DevicePrimalSpace:
         want = (kind[p.slot_glob] == 0) if variant == "new" else (kind[p.slot_glob] != 2)
         sel = want & p.glob_mine[p.slot_glob] & (p.gsize[p.slot_glob] <= 64)
         sc_slots = np.flatnonzero(sel)
-        self.SC = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
         self.sc_status = torch.zeros(max(int(p.sh_sub.size), 1), dtype=torch.int32, device="cuda")
-        lib.bddc_slot_schur(dev_i32(sc_slots), sc_slots.size, d.slot_glob, d.gsize, d.sh_doff, BiC,
-                            self.SC, self.sc_status, st)
+        self.sub_ok = None
+        pend = getattr(ls, "_bsym_pending", None)
+        if variant == "new" and not self.general and not multi and pend is not None:
+            # one rank, certified fast faces, new edges: no slot Schur block is needed
+            # at all -- the face kernel bounds their norms by the Bsym principal blocks
+            # and uses the subdomain certificate cond(Bsym) <= ||S||_F ||Bsym^-1||_F <
+            # 1e11 (the squared norms are on the device already) instead of the
+            # per-block Cholesky checks; uncertified faces fall back to the general kernel
+            f = pend[1]
+            self.sub_ok = (f[:p.N] * f[p.N:] < 1e22).to(torch.int32)
+            self.SC = None
+        else:
+            self.SC = torch.empty(max(p.d_total, 1), dtype=F64, device="cuda")
+            lib.bddc_slot_schur(dev_i32(sc_slots), sc_slots.size, d.slot_glob, d.gsize, d.sh_doff,
+                                BiC, self.SC, self.sc_status, st)
         vert = np.flatnonzero(kind == 2)
 
         def set_vertices():  # vertices are fully primal: 1x1 identity, r = 1
@@ -915,7 +927,8 @@ class DevicePrimalSpace:
                 woff[grp] = _excl(wsz)[:-1]
                 ws = torch.empty(int(wsz.sum()), dtype=F64, device="cuda")
             lib.bddc_face_gevp(d.kind, d.gsize, d.sh_start, d.sh_sub, d.sh_boff, d.sh_doff, BsC,
-                               BiC, self.SC, self.sc_status, scaling.D, self.theta_f, eig, d_eig_off, n_sel, r, Q,
+                               BiC, self.SC, self.sc_status, self.sub_ok, scaling.D, self.theta_f, eig,
+                               d_eig_off, n_sel, r, Q,
                                self.d_q_off, status, ws, dev_i64(woff[:-1]), dev_i32(grp),
                                grp.size, int(p.gsize[grp].max()), mode, self.detail,
                                self.d_det_off, st)
