@@ -172,6 +172,24 @@ int bddc_recover_interior(const double* M, const long long* off, const int* ld, 
                           const double* u_hat, double* u, int nbatch, int max_nloc, int panel,
                           const int* ndeep, cudaStream_t stream);
 
+/* ---- plan_host.cu : host side of the symbolic plan ------------------------ */
+
+/* Glob tables of the symbolic plan, all HOST arrays (no device work): from the
+ * glob sizes gsize[G], sharer counts nsh[G] and the flat sharer list
+ * (glob-major, ascending per glob) to the slot tables sh_start[G+1],
+ * slot_glob[ns], sh_doff[ns+1] (n_g^2 per slot), the per-subdomain glob lists
+ * sub_globs / sub_glob_sh[ns] with sub_glob_start[N+1], the block offset of
+ * every glob in its sharer's glob-major interface order (sub_glob_boff[ns] by
+ * (subdomain, glob), sh_boff[ns] by slot), nB[N] and the start of each glob's
+ * nodes in the flat glob-node list b_starts[ns].  Returns -2 for a sharer id
+ * outside [0, N).  replaces the per-subdomain glob bookkeeping of
+ * build_subdomain_operator substructuring.py:85-96. */
+int bddc_plan_glob_tables(int G, int N, const int* gsize, const long long* nsh,
+                          const long long* sharers, int* sh_start, int* slot_glob,
+                          long long* sh_doff, int* sub_globs, int* sub_glob_sh,
+                          int* sub_glob_start, int* sub_glob_boff, int* sh_boff, long long* nB,
+                          long long* b_starts);
+
 /* ---- elements.cu : SUPG element blocks ------------------------------------ */
 
 /* Ke (m x 16) and Fe (m x 4) of the SUPG-stabilised P1 tetrahedra for

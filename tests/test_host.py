@@ -167,3 +167,22 @@ def test_device_fields_reproduce_coefficient_callables(config):
     m = prob.mesh.n_elements
     nu_dev = np.asarray(df.viscosity_table)[np.arange(m) % df.viscosity_period]
     np.testing.assert_array_equal(nu_dev, prob.system.viscosity)
+
+
+@pytest.mark.parametrize("name", ["jump", "cfg1", "cfg4_small"])
+def test_native_glob_tables_match_numpy(name, monkeypatch):
+    """csrc/plan_host.cu (bddc_plan_glob_tables) builds the same glob tables as
+    the numpy reference path of plan.py."""
+    from paper_2501_01676_b200 import build
+    from paper_2501_01676_b200 import plan as P
+
+    build.build()
+    system, part, globs = inputs(name)
+    a = P.Plan(system, part, globs)
+    monkeypatch.setattr(P, "NATIVE_GLOB_TABLES", False)
+    b = P.Plan(system, part, globs)
+    for k in ("sh_start", "sh_sub", "slot_glob", "sh_doff", "sub_globs", "sub_glob_sh",
+              "sub_glob_start", "sub_glob_boff", "sh_boff", "nB", "voff", "_B_starts", "_B_counts",
+              "B_nodes", "pos2k", "iface_perm", "loc4", "I_nodes"):
+        assert np.array_equal(np.asarray(getattr(a, k)), np.asarray(getattr(b, k))), k
+    assert a.d_total == b.d_total and a._B_range == b._B_range
