@@ -14,7 +14,6 @@ exchanged and the code path is the single-GPU one.
 """
 
 import ctypes
-import os
 
 import numpy as np
 import scipy.linalg
@@ -216,17 +215,7 @@ class LocalSystem:
                 lib.bddc_schur_eliminate_timed(*args, ctypes.cast(ctypes.pointer(ms), ctypes.c_void_p))
                 self.trailing_ms += ms.value
             else:
-                G = int(os.environ.get("BDDC_ELIM_GROUP_B" if h0 is None else "BDDC_ELIM_GROUP_A", "0")) or p.N
-                if G >= p.N:
-                    lib.bddc_schur_eliminate(*args)
-                else:
-                    for g0 in range(0, p.N, G):
-                        g1 = min(p.N, g0 + G)
-                        sl = slice(g0, g1)
-                        lib.bddc_schur_eliminate(
-                            K, off[sl], d.ld[sl], npiv[sl], nrows[sl], ncols[sl], g1 - g0, max_npiv,
-                            max_rows, max_cols, PANEL, pinv[g0 * 4096:], 4096, 0, status[sl], 0, None,
-                            0, None if h0 is None else h0[sl], None if h1 is None else h1[sl], st)
+                lib.bddc_schur_eliminate(*args)
         self.K = K
         self.S = torch.empty(p.S_total, dtype=F64, device="cuda")
         # Bsym = sym(S) is written straight into the buffer Bsym^-1 is computed in
@@ -254,12 +243,8 @@ class LocalSystem:
             w_off = torch.arange(p.N, dtype=torch.int64, device="cuda") * (128 * 128)
             w128 = torch.full((p.N,), 128, dtype=torch.int32, device="cuda")
             wn = torch.empty(p.N, dtype=torch.int32, device="cuda")  # per-panel sizes (scratch)
-            G = int(os.environ.get("BDDC_GJ_GROUP", "0")) or p.N
-            for g0 in range(0, p.N, G):
-                g1 = min(p.N, g0 + G)
-                lib.bddc_gj_inverse128(Binv, d.soff[g0:g1], d.nB[g0:g1], d.nB[g0:g1], g1 - g0,
-                                       int(p.nB.max()), work, w_off[g0:g1], w128[g0:g1],
-                                       wn[g0:g1], pinv[g0 * 4096:], status[g0:g1], 1, st)
+            lib.bddc_gj_inverse128(Binv, d.soff, d.nB, d.nB, p.N, int(p.nB.max()), work, w_off,
+                                   w128, wn, pinv, status, 1, st)
             del work
             # norms for the dual-certificate bound (read at the status synchronisation)
             f = torch.zeros(2 * p.N, dtype=F64, device="cuda")
@@ -1183,13 +1168,8 @@ class DevicePreconditioner:
         # moved into the diagonal blocks): the reference's lu_factor(Stil)
         nsteps = (nbmax + 63) // 64
         pinv_all = torch.empty(nsteps * p.N * 4096, dtype=F64, device="cuda")
-        G = int(os.environ.get("BDDC_DUAL_GROUP", "0")) or p.N
-        for g0 in range(0, p.N, G):
-            g1 = min(p.N, g0 + G)
-            lib.bddc_schur_eliminate(Z, d.soff[g0:g1], d.nB[g0:g1], d.nB[g0:g1], d.nB[g0:g1],
-                                     d.nB[g0:g1], g1 - g0, nbmax, nbmax, nbmax, PANEL,
-                                     pinv_all[g0 * 4096:], 4096, p.N * 4096, status[g0:g1], 0,
-                                     None, 0, None, None, st)
+        lib.bddc_schur_eliminate(Z, d.soff, d.nB, d.nB, d.nB, d.nB, p.N, nbmax, nbmax, nbmax,
+                                 PANEL, pinv_all, 4096, p.N * 4096, status, 0, None, 0, None, None, st)
         # host work overlapping the queued factorisation: coarse dofs in reverse
         # Cuthill-McKee order of the primal coupling graph (each subdomain's primal
         # set is a clique) -> envelope LU / block-inverse solves
