@@ -157,6 +157,7 @@ class LocalSystem:
 
     def _factor(self):
         p, d, st = self.plan, self.d, stream()
+        wait_late_inputs(self.inputs)
         K = torch.empty(p.K_total, dtype=F64, device="cuda")  # every entry written by assembly
         Ke, Fe, ebad = self.inputs.get("Ke"), self.inputs.get("Fe"), self.inputs.get("_ebad")
         if Ke is None:  # element blocks built on the device from mesh + coefficients
@@ -500,10 +501,39 @@ def stage_inputs(system, partition=None, owned=None, device_elements=None):
     return out
 
 
-def upload_staged(staged):
-    """Asynchronous H2D of stage_inputs() buffers on the current stream."""
-    return _widen({k: (v.cuda(non_blocking=True) if isinstance(v, torch.Tensor) else v)
-                   for k, v in staged.items()})
+_LATE_INPUTS = ("nodes", "nu_tab", "gdir", "Ke", "Fe")
+
+
+def wait_late_inputs(inputs):
+    """Orders the current stream behind the late part of upload_staged()."""
+    ev = inputs.get("_late")
+    if ev is not None:
+        torch.cuda.current_stream().wait_event(ev)
+
+
+def upload_staged(staged, overlap=True):
+    """Asynchronous H2D of stage_inputs() buffers.  What the symbolic plan reads
+    (connectivity, element -> subdomain map, free mask) goes first on the
+    current stream; the mesh nodes, the viscosity table and the Dirichlet
+    values (or the element blocks) follow on a copy stream, so that their
+    transfer runs behind the plan.  out["_late"] is the event their consumers
+    wait for (wait_late_inputs: device_element_blocks, LocalSystem)."""
+    cur = torch.cuda.current_stream()
+    late = [k for k, v in staged.items() if isinstance(v, torch.Tensor) and k in _LATE_INPUTS]
+    if not overlap:
+        late = []
+    out = _widen({k: (v.cuda(non_blocking=True) if isinstance(v, torch.Tensor) else v)
+                  for k, v in staged.items() if k not in late})
+    if late:
+        side = _side_stream()
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            for k in late:
+                out[k] = staged[k].cuda(non_blocking=True)
+                out[k].record_stream(cur)
+            out["_late"] = torch.cuda.Event()
+            out["_late"].record(side)
+    return out
 
 
 def staged_bytes(staged):
@@ -529,6 +559,7 @@ def device_element_blocks(inputs):
     ["nu_tab"] and the packed fields (reference element_contributions,
     discretization.py:101-158); bad: device flag of the first element with a
     non-positive volume (~0 if none)."""
+    wait_late_inputs(inputs)
     fields, period = inputs["_supg"]
     if not fields[14] > 0.0:  # c - div(a)/2 is constant: the reference reports element 0
         raise ValueError("shifted reaction c - div(a)/2 is not positive on element 0; "

@@ -12,7 +12,7 @@ import torch
 
 from .engine import (DeviceInterfaceOperator, DevicePreconditioner, DevicePrimalSpace,
                      DeviceScaling, LocalSystem, PhaseTimer, gmres_device, gmres_right_device,
-                     device_element_blocks, recover_device, upload_inputs)
+                     _side_stream, device_element_blocks, recover_device, upload_inputs)
 from .plan import Plan
 
 
@@ -38,8 +38,22 @@ def run(system, partition, globs, theta_f, theta_e, variant="new", rel_tol=1e-8,
         inputs = upload_inputs(system, partition, owned=owned if plan is None or plan.on_device else None)
     if "Ke" not in inputs and "_supg" in inputs:
         # device element blocks first: the kernel runs while the host builds the plan
-        Ke, Fe, ebad = device_element_blocks(inputs)
-        inputs = {**inputs, "Ke": Ke, "Fe": Fe, "_ebad": ebad}
+        if inputs.get("_late") is not None:
+            # staged upload (engine.upload_staged): the nodes / viscosity table are
+            # still in flight on the copy stream; the element kernel follows them
+            # there, next to the plan's device work, and LocalSystem waits for it
+            cur, aux = torch.cuda.current_stream(), _side_stream()
+            inputs["conn"].record_stream(aux)
+            with torch.cuda.stream(aux):
+                Ke, Fe, ebad = device_element_blocks(inputs)
+                for t in (Ke, Fe, ebad):
+                    t.record_stream(cur)
+                done = torch.cuda.Event()
+                done.record(aux)
+            inputs = {**inputs, "Ke": Ke, "Fe": Fe, "_ebad": ebad, "_late": done}
+        else:
+            Ke, Fe, ebad = device_element_blocks(inputs)
+            inputs = {**inputs, "Ke": Ke, "Fe": Fe, "_ebad": ebad}
     if plan is None:
         tm.mark("symbolic_plan")
         plan = Plan(system, partition, globs, device_inputs=inputs, owned=owned)
