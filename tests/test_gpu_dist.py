@@ -83,6 +83,40 @@ def test_sharded_device_elements_match_single():
         assert _rel(u, single.u.cpu().numpy()) <= 1e-10
 
 
+def test_sharded_ranks_with_staged_uploads_match_single():
+    """What bench.py does per rank: page-locked per-rank element subsets
+    (stage_inputs(owned=...)), the staged upload with its late inputs on the
+    copy stream, then the sharded pipeline."""
+    import torch
+
+    from paper_2501_01676_b200 import configs, pipeline
+    from paper_2501_01676_b200.dist import run_threads
+    from paper_2501_01676_b200.engine import stage_inputs, upload_staged
+
+    prob = configs.build_problem(2, n=16, subs=2)
+    args = (prob.system, prob.partition, prob.globs, 1.0 + np.log(8.0), 10.0, "new")
+    single = pipeline.run(*args)
+
+    def rank(comm):
+        owned = comm.owned(prob.partition.n_subdomains)
+        staged = stage_inputs(prob.system, prob.partition, owned=owned)
+        out = []
+        for _ in range(2):
+            inp = upload_staged(staged)
+            assert inp.get("_late") is not None
+            res = pipeline.run(*args, inputs=inp, comm=comm)
+            torch.cuda.synchronize()
+            out.append((res.iterations, res.solution.cpu().numpy(), res.u.cpu().numpy()))
+        return out
+
+    for runs in run_threads(2, rank):
+        for it, x, u in runs:
+            assert it == single.iterations
+            assert _rel(x, single.solution.cpu().numpy()) <= 1e-10
+            assert _rel(u, single.u.cpu().numpy()) <= 1e-10
+        assert np.array_equal(runs[0][1], runs[1][1]) and np.array_equal(runs[0][2], runs[1][2])
+
+
 def _gloo_gpu_worker(rank, size, port, q, name):
     import os
 
