@@ -146,11 +146,14 @@ int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int
                        int* work_n, double* pinv_ws, int* status, int require_positive,
                        cudaStream_t stream);
 
-/* S, g, Bsym = (S + S^T)/2 from the eliminated local matrices.
+/* S, g, Bsym = (S + S^T)/2 from the eliminated local matrices.  s_norm2 (or
+ * null): ||S_b||_F^2 per matrix, accumulated while S is written (fixed
+ * reduction order) through norm_ws (48 * nbatch doubles of scratch).
  * replaces SubdomainOperator.__init__ substructuring.py:35-40. */
 int bddc_extract_schur(const double* M, const long long* off, const int* ld, const int* nI,
                        const int* nB, const long long* soff, const long long* voff, double* S,
-                       double* Bsym, double* g, int nbatch, cudaStream_t stream);
+                       double* Bsym, double* g, int nbatch, double* s_norm2, double* norm_ws,
+                       cudaStream_t stream);
 
 int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
                     cudaStream_t stream);

@@ -721,9 +721,12 @@ __global__ void __launch_bounds__(256) extract_schur_kernel(
     const double* __restrict__ base, const long long* __restrict__ off,
     const int* __restrict__ ld, const int* __restrict__ nI, const int* __restrict__ nB,
     const long long* __restrict__ soff, const long long* __restrict__ voff,
-    double* __restrict__ S, double* __restrict__ Bsym, double* __restrict__ g) {
+    double* __restrict__ S, double* __restrict__ Bsym, double* __restrict__ g,
+    double* __restrict__ s_norm2) {
   __shared__ double t0[32][33];
   __shared__ double t1[32][33];
+  __shared__ double red[8];
+  double sq = 0.0;
   const int b = blockIdx.y;
   const int n = nB[b], i0 = nI[b], L = ld[b];
   const double* M = base + off[b] + (long long)i0 * L + i0;
@@ -747,6 +750,7 @@ __global__ void __launch_bounds__(256) extract_schur_kernel(
       const int r = r0 + ty + j, c = c0 + tx;
       if (r < n && c < n) {
         const double v = t0[ty + j][tx];
+        sq = fma(v, v, sq);
         Sb[(long long)r * n + c] = v;
         Bb[(long long)r * n + c] = 0.5 * (v + t1[tx][ty + j]);
       }
@@ -754,6 +758,28 @@ __global__ void __launch_bounds__(256) extract_schur_kernel(
   }
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
     g[voff[b] + r] = M[(long long)r * L + n];
+  if (s_norm2 != nullptr) {  // this CTA's share of ||S_b||_F^2, fixed reduction tree
+    for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+    __syncthreads();
+    if (tx == 0) red[ty] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += red[w];
+      s_norm2[(long long)b * gridDim.x + blockIdx.x] = t;
+    }
+  }
+}
+
+// out[b] = sum of the kExtractParts partial sums of matrix b, in order
+constexpr int kExtractParts = 48;
+__global__ void sum_parts_kernel(const double* __restrict__ part, double* __restrict__ out,
+                                 int nbatch) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nbatch) return;
+  double t = 0.0;
+  for (int x = 0; x < kExtractParts; ++x) t += part[(long long)b * kExtractParts + x];
+  out[b] = t;
 }
 
 // out[b] = ||X_b||_F^2 for square batched matrices (ld = n); one CTA per
@@ -1135,11 +1161,17 @@ int bddc_gj_inverse128(double* M, const long long* off, const int* ld, const int
 
 int bddc_extract_schur(const double* M, const long long* off, const int* ld, const int* nI,
                        const int* nB, const long long* soff, const long long* voff, double* S,
-                       double* Bsym, double* g, int nbatch, cudaStream_t stream) {
+                       double* Bsym, double* g, int nbatch, double* s_norm2, double* norm_ws,
+                       cudaStream_t stream) {
   if (nbatch <= 0) return 0;
-  extract_schur_kernel<<<dim3(48, nbatch), 256, 0, stream>>>(M, off, ld, nI, nB, soff, voff, S,
-                                                             Bsym, g);
+  const bool norms = s_norm2 != nullptr && norm_ws != nullptr;
+  extract_schur_kernel<<<dim3(kExtractParts, nbatch), 256, 0, stream>>>(
+      M, off, ld, nI, nB, soff, voff, S, Bsym, g, norms ? norm_ws : nullptr);
   bddc_note_launches(1);
+  if (norms) {
+    sum_parts_kernel<<<ceil_div(nbatch, 256), 256, 0, stream>>>(norm_ws, s_norm2, nbatch);
+    bddc_note_launches(1);
+  }
   return launch_status();
 }
 

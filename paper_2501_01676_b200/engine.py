@@ -224,8 +224,11 @@ class LocalSystem:
         # symmetrise S blocks on the fly)
         self._W = torch.empty(p.S_total, dtype=F64, device="cuda")
         self.g = torch.empty(int(p.voff[-1]), dtype=F64, device="cuda")
+        # ||S_b||_F^2 for the dual certificate / the face fast path rides along
+        self._frob_dev = torch.empty(2 * p.N, dtype=F64, device="cuda")
+        norm_ws = torch.empty(48 * p.N, dtype=F64, device="cuda")
         lib.bddc_extract_schur(K, d.off, d.ld, d.nI, d.nB, d.soff, d.voff, self.S, self._W,
-                               self.g, p.N, st)
+                               self.g, p.N, self._frob_dev[:p.N], norm_ws, st)
         return status
 
     def bsym_inverse(self, check=True):
@@ -248,8 +251,7 @@ class LocalSystem:
                                    w128, wn, pinv, status, 1, st)
             del work
             # norms for the dual-certificate bound (read at the status synchronisation)
-            f = torch.zeros(2 * p.N, dtype=F64, device="cuda")
-            lib.bddc_frob2(self.S, d.soff, d.nB, p.N, f[:p.N], st)
+            f = self._frob_dev  # ||S||_F^2 from extract_schur
             lib.bddc_frob2(Binv, d.soff, d.nB, p.N, f[p.N:], st)
             self._Binv = Binv
             self._bsym_pending = (status, f)
