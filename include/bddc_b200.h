@@ -164,6 +164,13 @@ int bddc_symmetrize(double* X, const long long* soff, const int* n, int nbatch,
 int bddc_frob2(const double* X, const long long* soff, const int* n, int nbatch, double* out,
                cudaStream_t stream);
 
+/* out[b] = trace(X_b)^2: for symmetric positive definite X_b an upper bound of
+ * ||X_b||_F^2 from the diagonal alone (used for ||Bsym^-1|| in the certificates
+ * that replace cho_factor(sym(Sdd)) solver.py:94 and the per-block checks of
+ * substructuring.py:166-170). */
+int bddc_trace2(const double* X, const long long* soff, const int* n, int nbatch, double* out,
+                cudaStream_t stream);
+
 /* u_I = A_II^-1 (f_I - A_IB u_B) by block back-substitution over the stored
  * W rows.  ndeep (per matrix, null: 0): the leading pivots eliminated in a
  * separate first phase (bddc_schur_eliminate with a column hole); the panels

@@ -807,6 +807,21 @@ __global__ void __launch_bounds__(512) frob2_kernel(const double* __restrict__ X
   }
 }
 
+// out[b] = trace(X_b)^2 (ld = n): for a symmetric positive definite X_b an upper
+// bound of ||X_b||_F^2 (sum of squared eigenvalues <= squared sum) that reads
+// only the diagonal; one warp per matrix, fixed reduction tree
+__global__ void trace2_kernel(const double* __restrict__ X, const long long* __restrict__ soff,
+                              const int* __restrict__ nB, double* __restrict__ out, int nbatch) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= nbatch) return;
+  const int n = nB[b], lane = threadIdx.x & 31;
+  const double* M = X + soff[b];
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s += M[(long long)i * (n + 1)];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[b] = s * s;
+}
+
 // X <- (X + X^T)/2 for square batched matrices (ld = n)
 __global__ void symmetrize_kernel(double* __restrict__ X, const long long* __restrict__ soff,
                                   const int* __restrict__ nB) {
@@ -1179,6 +1194,14 @@ int bddc_frob2(const double* X, const long long* soff, const int* n, int nbatch,
                cudaStream_t stream) {
   if (nbatch <= 0) return 0;
   frob2_kernel<<<nbatch, 512, 0, stream>>>(X, soff, n, out);
+  bddc_note_launches(1);
+  return launch_status();
+}
+
+int bddc_trace2(const double* X, const long long* soff, const int* n, int nbatch, double* out,
+                cudaStream_t stream) {
+  if (nbatch <= 0) return 0;
+  trace2_kernel<<<ceil_div(nbatch, 8), 256, 0, stream>>>(X, soff, n, out, nbatch);
   bddc_note_launches(1);
   return launch_status();
 }

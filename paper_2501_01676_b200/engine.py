@@ -251,8 +251,9 @@ class LocalSystem:
                                    w128, wn, pinv, status, 1, st)
             del work
             # norms for the dual-certificate bound (read at the status synchronisation)
-            f = self._frob_dev  # ||S||_F^2 from extract_schur
-            lib.bddc_frob2(Binv, d.soff, d.nB, p.N, f[p.N:], st)
+            # ||S||_F^2 from extract_schur; ||Bsym^-1||_F^2 <= trace^2 (SPD), diagonal only
+            f = self._frob_dev
+            lib.bddc_trace2(Binv, d.soff, d.nB, p.N, f[p.N:], st)
             self._Binv = Binv
             self._bsym_pending = (status, f)
         if check:
@@ -1354,7 +1355,9 @@ class DevicePreconditioner:
         [1/||Bsym^-1||, ||S||] up to the rounding of forming Sbar (<= 8 nB eps ||S||);
         Cholesky of an SPD matrix of order n runs to completion when
         20 n^1.5 eps cond < 1.  Certified when
-        ||S||_F ||Bsym^-1||_F (20 nB^1.5 + 8 nB) eps < 1/4 for every subdomain."""
+        ||S||_F ||Bsym^-1||_F (20 nB^1.5 + 8 nB) eps < 1/4 for every subdomain
+        (||Bsym^-1||_F itself bounded by trace(Bsym^-1) when it comes from
+        bsym_inverse: no second pass over the inverses)."""
         p, d, st = ls.plan, ls.d, stream()
         if getattr(ls, "_frob", None) is None:
             f = torch.zeros(2 * p.N, dtype=F64, device="cuda")
