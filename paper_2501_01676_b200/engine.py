@@ -1739,7 +1739,9 @@ def recover_device(ls, u_hat):
     the sharded path the nodal vector is assembled on every rank (interiors
     and owned interface values of each rank, one allreduce)."""
     p, d, st = ls.plan, ls.d, stream()
-    iface = dev_i64(ls.globs.interface_nodes)
+    iface = getattr(p, "_iface_nodes_d", None)  # uploaded by the device plan
+    if iface is None:
+        iface = dev_i64(ls.globs.interface_nodes)
     if not _multi(ls.comm):
         u = ls.inputs["gdir"].clone()
         u[iface] = u_hat
